@@ -1,0 +1,167 @@
+/*
+ * asot.h -- C ABI of the B200-native ASOT pairwise-distance library (libasot.so).
+ *
+ * The hot path of Anchor Space Optimal Transport (arXiv 2310.16123, PAPER.md):
+ *   a1  Gibbs kernel      K := exp(-C_s / eps)
+ *   a2  mapping P_o       j*(p) = argmin_j ||x_p - w_j||^2, lowest j
+ *   a3  mapped marginals  a' = Z^T a (one-hot => histogram; 1/n dropped) P:100
+ *   a4  pair set          all i < j (Def. 1, i != j), upper-triangular tiles
+ *   a5  batched Sinkhorn  U = A / (K V), V = B / (K^T U), v0 = 1, exactly L iterations
+ *   a6  cost              d_ij = <diag(u) K diag(v), C_s> = u^T ((K (.) C_s) v), mirrored,
+ *                         zero diagonal
+ * Readings of the paper where it is silent or garbled are listed in DESIGN.md ("Readings").
+ *
+ * Conventions (all entry points):
+ *   - Every buffer is caller-owned.  Pointers documented "device" must be device memory of the
+ *     current CUDA device; "host" pointers are ordinary host memory (pinned recommended).
+ *   - The library keeps no global device state and never allocates device memory: scratch
+ *     space is the caller's `workspace` (device, 256-byte aligned), sized by the matching
+ *     *_workspace_bytes query.
+ *   - Calls only ENQUEUE work on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream) and return without synchronising, except the *_host variant, which
+ *     synchronises `stream` before returning.
+ *   - Host-checkable argument errors return synchronously (status codes below) and enqueue
+ *     nothing.  Data-dependent conditions are OR-ed by the kernels into the caller's device
+ *     word `status` (ASOT_FLAG_* bits); the caller reads it after synchronising.
+ *   - asot_last_error() returns a thread-local message for the last non-OK return.
+ *   - Floating point: inputs are fp32.  Mapping decisions are taken in fp64 wherever fp32
+ *     cannot decide them (bit-exact against the fp64 definition); histograms are accumulated in
+ *     fp64 in point order and rounded to fp32; Sinkhorn runs in fp32 (ASOT_PREC_FP32, CUDA
+ *     cores, IEEE division) or on tcgen05 tensor cores with TF32 operands and fp32
+ *     accumulation (ASOT_PREC_TF32).
+ */
+#ifndef ASOT_H_
+#define ASOT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASOT_ABI_VERSION 1
+
+typedef enum {
+  ASOT_OK = 0,
+  ASOT_ERR_INVALID_ARGUMENT = 1, /* null pointer, size < 1, eps <= 0 / non-finite, iters < 1,
+                                    max(C_s)/eps > 80 (fp32 Gibbs underflow guard), bad range */
+  ASOT_ERR_INFEASIBLE_MASS = 2,  /* reserved for callers mapping ASOT_FLAG_EMPTY_DIST/BAD_MASS */
+  ASOT_ERR_NUMERIC = 3,          /* reserved for callers mapping ASOT_FLAG_NONFINITE_* */
+  ASOT_ERR_CUDA = 4,             /* a CUDA runtime call or launch failed (message in last_error) */
+  ASOT_ERR_UNSUPPORTED = 5,      /* size outside what this build implements (e.g. K > 1024) */
+  ASOT_ERR_WORKSPACE = 6         /* workspace NULL or smaller than the query returned */
+} asot_status;
+
+typedef enum {
+  ASOT_PREC_FP32 = 0, /* fp32 CUDA-core Sinkhorn, IEEE divide: target rel. err <= 1e-4      */
+  ASOT_PREC_TF32 = 1  /* tcgen05 kind::tf32 MMA (RNA-rounded G and U/V, fp32 accumulate):
+                         target rel. err <= 2e-3; needs K <= 128 in this build, else falls
+                         back to ASOT_PREC_FP32 (reported by asot_effective_precision)     */
+} asot_precision;
+
+/* Bits OR-ed into the caller's device status word. */
+#define ASOT_FLAG_EMPTY_DIST       1u  /* a distribution with n_i = 0 (S:24 requires n >= 1)      */
+#define ASOT_FLAG_BAD_MASS         2u  /* negative weight or |sum w - 1| > 1e-5 (fp32)     */
+#define ASOT_FLAG_NONFINITE_INPUT  4u  /* NaN/Inf in points, weights or anchors                  */
+#define ASOT_FLAG_DENOM_CLAMPED    8u  /* a Sinkhorn denominator < FLT_MIN was clamped     */
+#define ASOT_FLAG_NONFINITE_OUTPUT 16u /* a distance came out NaN/Inf                            */
+
+/* Distance-matrix tiling (step a4).  Distributions are grouped in blocks of 16; block pairs
+ * (bi <= bj) are enumerated row-major over the upper triangle of the block grid; each block
+ * pair is two tiles of 8 x 16 = 128 pair slots (tile 2b+h holds rows 16bi+8h .. +7 against
+ * columns 16bj .. +15).  Slot `lane` of a tile is the pair (i, j) = (16bi+8h+lane/16,
+ * 16bj+lane%16), valid iff i < j < N.  Multi-GPU callers split [0, asot_num_tiles(N)). */
+#define ASOT_TILE_SLOTS 128
+int64_t asot_num_tiles(int64_t n_dist);
+
+/* Step a2 + a3: one-hot nearest-anchor mapping and the N x K mapped-marginal histograms.
+ *   points   [T, dim] f32 row-major, device;  T = offsets[n_dist] (read from host copy below)
+ *   offsets  [n_dist+1] i64, device, offsets[0] = 0, non-decreasing
+ *   offsets_host  the same array in host memory (sizes are needed for launch shapes)
+ *   weights  [T] f32, device; per distribution >= 0 and summing to 1 +- 1e-5 (not renormalised)
+ *   anchors  [n_anchors, dim] f32 row-major, device; 1 <= n_anchors <= 1024, 1 <= dim <= 128
+ *   assign_out [T] i32, device: j*(p) (bit-exact vs the fp64 definition, lowest index on ties)
+ *   hist_out [n_dist, n_anchors] f32 row-major, device: H[i, j] = sum of w_p over points p of
+ *            distribution i with j*(p) = j, accumulated in fp64 in point order, rounded to f32
+ *   status   device u32, OR-ed with ASOT_FLAG_EMPTY_DIST / BAD_MASS / NONFINITE_INPUT */
+asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
+                                const int64_t* offsets_host, const float* weights,
+                                int64_t n_dist, int32_t dim, const float* anchors,
+                                int32_t n_anchors, int32_t* assign_out, float* hist_out,
+                                uint32_t* status, void* stream);
+
+/* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed):
+ *   hist     [n_dist, n_anchors] f32 device (rows are a' / b')
+ *   cost     [n_anchors, n_anchors] f32 device: C_s symmetric, >= 0, zero diagonal
+ *   eps > 0 (max(C_s)/eps <= 80 is checked against cost_max, a host value the caller supplies:
+ *            the library does not read device memory synchronously), iters >= 1
+ *   pair_i, pair_j [n_pairs] i32 device, 0 <= i, j < n_dist (i != j expected, not required)
+ *   dist_out [n_pairs] f32 device: d(pair_i[p], pair_j[p]) with a = H[pair_i] on the u side */
+asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_anchors,
+                                   const float* cost, float cost_max, float eps, int32_t iters,
+                                   asot_precision prec, const int32_t* pair_i,
+                                   const int32_t* pair_j, int64_t n_pairs, float* dist_out,
+                                   uint32_t* status, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec);
+
+/* Full pipeline a1-a6 on the tile range [tile_begin, tile_end) (device buffers):
+ *   hist_in  NULL: map + histogram all distributions into the workspace first (needs points,
+ *            offsets, offsets_host, weights, anchors, dim); non-NULL: use this [n_dist,
+ *            n_anchors] histogram (multi-GPU passes the all-gathered H) and skip mapping
+ *   dist_out [n_dist, n_dist] f32 or NULL: D[i,j] = D[j,i] = d_ij for the range's pairs; when
+ *            the range is the whole triangle the diagonal is set to 0 as well
+ *   packed_out [(tile_end - tile_begin) * 128] f32 or NULL: slot-ordered results (0 for
+ *            invalid slots) -- the unit multi-GPU ranks gather
+ *   assign_out [T] i32 or NULL, hist_out [n_dist, n_anchors] f32 or NULL: optional copies of
+ *            the mapping results (only when hist_in == NULL) */
+asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
+                                 const int64_t* offsets_host, const float* weights,
+                                 int64_t n_dist, int32_t dim, const float* anchors,
+                                 int32_t n_anchors, const float* cost, float cost_max, float eps,
+                                 int32_t iters, asot_precision prec, const float* hist_in,
+                                 int64_t tile_begin, int64_t tile_end, float* dist_out,
+                                 float* packed_out, int32_t* assign_out, float* hist_out,
+                                 uint32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream);
+size_t asot_distance_matrix_workspace_bytes(int64_t n_dist, int64_t n_points, int32_t n_anchors,
+                                            asot_precision prec);
+
+/* Same pipeline end to end from HOST buffers (the e2e entry point): copies points, offsets,
+ * weights, anchors and cost host->device on `stream`, runs the whole triangle, copies the
+ * N x N matrix (and status) back to `dist_host` / `status_host`, and synchronises `stream`.
+ * All scratch (inputs, H, G images, D) lives in the caller's device `workspace`. */
+asot_status asot_distance_matrix_host(const float* points_host, const int64_t* offsets_host,
+                                      const float* weights_host, int64_t n_dist, int32_t dim,
+                                      const float* anchors_host, int32_t n_anchors,
+                                      const float* cost_host, float eps, int32_t iters,
+                                      asot_precision prec, float* dist_host,
+                                      uint32_t* status_host, void* workspace,
+                                      size_t workspace_bytes, void* stream);
+size_t asot_distance_matrix_host_workspace_bytes(int64_t n_dist, int64_t n_points, int32_t dim,
+                                                 int32_t n_anchors, asot_precision prec);
+
+/* KN6: scatter packed tile results [(tile_end - tile_begin) * 128] into the N x N matrix
+ * (both triangles).  Zeroes the diagonal when zero_diag != 0. */
+asot_status asot_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
+                              int64_t tile_end, float* dist_out, int32_t zero_diag, void* stream);
+
+/* Host-side enumeration of tile slots (no device work): for s in [0, (tile_end-tile_begin)*128)
+ * writes pair (i_out[s], j_out[s]) and valid_out[s] (1 iff i < j < n_dist).  Host pointers. */
+asot_status asot_tile_pairs_host(int64_t n_dist, int64_t tile_begin, int64_t tile_end,
+                                 int32_t* i_out, int32_t* j_out, uint8_t* valid_out);
+
+/* Precision actually used for a given K and request (TF32 needs K <= 128 in this build). */
+asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
+
+/* Number of kernel launches the last distance_matrix / pairwise call on this thread issued. */
+int32_t asot_last_launch_count(void);
+
+const char* asot_last_error(void);
+int32_t asot_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASOT_H_ */

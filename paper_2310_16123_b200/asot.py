@@ -1,0 +1,257 @@
+"""Thin Python binding over libasot.so (C ABI: include/asot.h).
+
+Argument marshalling only: torch tensors provide device memory and streams, every step of
+the path (mapping, histograms, Gibbs kernel, Sinkhorn, cost, mirroring) runs in the library's
+CUDA kernels.  Names follow the ABI / the paper: H is the N x K matrix of mapped marginals
+(a' rows), cost is C_s, eps and iters are the Sinkhorn settings.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+FP32 = 0  # ASOT_PREC_FP32: CUDA-core fp32, IEEE divide (rel. err <= 1e-4 target)
+TF32 = 1  # ASOT_PREC_TF32: tcgen05 kind::tf32 MMA, fp32 accumulate (rel. err <= 2e-3 target)
+TILE_SLOTS = 128
+
+FLAG_EMPTY_DIST = 1
+FLAG_BAD_MASS = 2
+FLAG_NONFINITE_INPUT = 4
+FLAG_DENOM_CLAMPED = 8
+FLAG_NONFINITE_OUTPUT = 16
+
+_STATUS_EXC = {1: ValueError, 2: ValueError, 3: FloatingPointError, 4: RuntimeError,
+               5: NotImplementedError, 6: MemoryError}
+
+
+class AsotStatusError(RuntimeError):
+    pass
+
+
+def _lib_handle():
+    return _lib.load()
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib_handle().asot_last_error().decode()
+        raise _STATUS_EXC.get(rc, RuntimeError)(f"asot status {rc}: {msg}")
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _stream(stream) -> Optional[int]:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and (not isinstance(t, torch.Tensor) or not t.is_cuda):
+            raise ValueError("device tensors (cuda) are required; there is no CPU path")
+
+
+def num_tiles(n_dist: int) -> int:
+    return int(_lib_handle().asot_num_tiles(int(n_dist)))
+
+
+def effective_precision(n_anchors: int, precision: int) -> int:
+    return int(_lib_handle().asot_effective_precision(int(n_anchors), int(precision)))
+
+
+def last_launch_count() -> int:
+    return int(_lib_handle().asot_last_launch_count())
+
+
+def new_status(device=None) -> torch.Tensor:
+    return torch.zeros(1, dtype=torch.int32, device=device or "cuda")
+
+
+def check_status(status, allow: int = FLAG_DENOM_CLAMPED) -> int:
+    """Raise on data-dependent failures the kernels flagged (call after synchronising)."""
+    v = int(status.item()) if isinstance(status, torch.Tensor) else int(status)
+    bad = v & ~allow
+    if bad & (FLAG_EMPTY_DIST | FLAG_BAD_MASS):
+        raise ValueError(f"infeasible mass (status flags {v:#x})")
+    if bad & (FLAG_NONFINITE_INPUT | FLAG_NONFINITE_OUTPUT):
+        raise FloatingPointError(f"non-finite values (status flags {v:#x})")
+    return v
+
+
+class Workspace:
+    """Caller-owned device scratch (grown on demand, reused across calls)."""
+
+    def __init__(self, device=None):
+        self.device = device or "cuda"
+        self.buf = torch.empty(0, dtype=torch.uint8, device=self.device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def _ws(workspace: Optional[Workspace], device) -> Workspace:
+    if workspace is not None:
+        return workspace
+    key = str(device)
+    if key not in _default_ws:
+        _default_ws[key] = Workspace(device)
+    return _default_ws[key]
+
+
+def _host_offsets(offsets, offsets_host):
+    if offsets_host is not None:
+        return np.ascontiguousarray(offsets_host, dtype=np.int64)
+    return np.ascontiguousarray(offsets.detach().cpu().numpy(), dtype=np.int64)
+
+
+def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
+                   anchors: torch.Tensor, offsets_host: Optional[np.ndarray] = None,
+                   status: Optional[torch.Tensor] = None, stream=None):
+    """Steps a2 + a3: returns (assign [T] int32, H [N, K] f32, status)."""
+    _need_cuda(points, offsets, weights, anchors)
+    oh = _host_offsets(offsets, offsets_host)
+    N = oh.shape[0] - 1
+    T = int(oh[-1])
+    K, d = anchors.shape
+    assign = torch.empty(max(T, 1), dtype=torch.int32, device=points.device)
+    H = torch.empty((N, K), dtype=torch.float32, device=points.device)
+    st = new_status(points.device) if status is None else status
+    _check(_lib_handle().asot_map_to_anchors(
+        _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(anchors), int(K),
+        _ptr(assign), _ptr(H), _ptr(st), _stream(stream)))
+    return assign[:T], H, st
+
+
+def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: int,
+                      pair_i: torch.Tensor, pair_j: torch.Tensor, precision: int = TF32,
+                      cost_max: Optional[float] = None, status: Optional[torch.Tensor] = None,
+                      workspace: Optional[Workspace] = None, stream=None) -> torch.Tensor:
+    """Steps a1 + a5 + a6 on explicit pairs (a = H[pair_i] on the u side)."""
+    _need_cuda(H, cost, pair_i, pair_j)
+    N, K = H.shape
+    n = int(pair_i.numel())
+    out = torch.empty(n, dtype=torch.float32, device=H.device)
+    cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
+    st = new_status(H.device) if status is None else status
+    L = _lib_handle()
+    ws = _ws(workspace, H.device).get(L.asot_pairwise_workspace_bytes(int(K), int(precision)))
+    _check(L.asot_pairwise_sinkhorn(
+        _ptr(H), N, int(K), _ptr(cost), cmax, float(eps), int(iters), int(precision),
+        _ptr(pair_i), _ptr(pair_j), n, _ptr(out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def distance_matrix(points: Optional[torch.Tensor], offsets: Optional[torch.Tensor],
+                    weights: Optional[torch.Tensor], anchors: Optional[torch.Tensor],
+                    cost: torch.Tensor, eps: float, iters: int, precision: int = TF32,
+                    hist: Optional[torch.Tensor] = None, n_dist: Optional[int] = None,
+                    tile_range: Optional[Sequence[int]] = None, out: Optional[torch.Tensor] = None,
+                    packed: Optional[torch.Tensor] = None, want_matrix: bool = True,
+                    assign_out: Optional[torch.Tensor] = None, hist_out: Optional[torch.Tensor] = None,
+                    offsets_host: Optional[np.ndarray] = None, cost_max: Optional[float] = None,
+                    status: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
+                    stream=None):
+    """Full pipeline a1-a6.  Returns the N x N matrix (when want_matrix) and/or fills `packed`
+    ([(tile_end - tile_begin) * 128] slot-ordered results) for the tile range."""
+    _need_cuda(cost, hist, points, offsets, weights, anchors)
+    L = _lib_handle()
+    K = int(cost.shape[0])
+    if hist is None:
+        oh = _host_offsets(offsets, offsets_host)
+        N = oh.shape[0] - 1
+        T = int(oh[-1])
+        d = int(points.shape[1])
+        dev = points.device
+    else:
+        oh = None
+        N = int(hist.shape[0]) if n_dist is None else int(n_dist)
+        T, d = 0, 1
+        dev = hist.device
+    nt = num_tiles(N)
+    t0, t1 = (0, nt) if tile_range is None else (int(tile_range[0]), int(tile_range[1]))
+    if want_matrix and out is None:
+        out = torch.empty((N, N), dtype=torch.float32, device=dev)
+    if not want_matrix:
+        out = None
+    cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
+    st = new_status(dev) if status is None else status
+    ws = _ws(workspace, dev).get(L.asot_distance_matrix_workspace_bytes(N, T, K, int(precision)))
+    _check(L.asot_distance_matrix(
+        _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, d, _ptr(anchors), K, _ptr(cost),
+        cmax, float(eps), int(iters), int(precision), _ptr(hist), t0, t1, _ptr(out), _ptr(packed),
+        _ptr(assign_out), _ptr(hist_out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def host_workspace_bytes(n_dist: int, n_points: int, dim: int, n_anchors: int,
+                         precision: int = TF32) -> int:
+    return int(_lib_handle().asot_distance_matrix_host_workspace_bytes(
+        int(n_dist), int(n_points), int(dim), int(n_anchors), int(precision)))
+
+
+def distance_matrix_host(points: np.ndarray, offsets: np.ndarray, weights: np.ndarray,
+                         anchors: np.ndarray, cost: np.ndarray, eps: float, iters: int,
+                         precision: int = TF32, out: Optional[np.ndarray] = None,
+                         workspace: Optional[Workspace] = None, device=None, stream=None):
+    """End to end from host buffers (H2D copies, the whole pipeline, D2H of the matrix) through
+    the single C-ABI call asot_distance_matrix_host.  Returns (D [N, N] host f32, status)."""
+    pts = np.ascontiguousarray(points, dtype=np.float32)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    w = np.ascontiguousarray(weights, dtype=np.float32)
+    anc = np.ascontiguousarray(anchors, dtype=np.float32)
+    cst = np.ascontiguousarray(cost, dtype=np.float32)
+    N = offs.shape[0] - 1
+    K, d = anc.shape
+    if out is None:
+        out = np.empty((N, N), dtype=np.float32)
+    status = np.zeros(1, dtype=np.uint32)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    L = _lib_handle()
+    ws = _ws(workspace, dev).get(host_workspace_bytes(N, pts.shape[0], d, K, precision))
+    _check(L.asot_distance_matrix_host(
+        _ptr(pts), _ptr(offs), _ptr(w), N, int(d), _ptr(anc), int(K), _ptr(cst), float(eps),
+        int(iters), int(precision), _ptr(out), _ptr(status), _ptr(ws), ws.numel(), _stream(stream)))
+    return out, int(status[0])
+
+
+def tile_pairs(n_dist: int, tile_begin: int = 0, tile_end: Optional[int] = None):
+    """Host enumeration of the tile slots: returns (i, j, valid) numpy arrays."""
+    t1 = num_tiles(n_dist) if tile_end is None else int(tile_end)
+    n = (t1 - int(tile_begin)) * TILE_SLOTS
+    i = np.empty(n, np.int32)
+    j = np.empty(n, np.int32)
+    v = np.empty(n, np.uint8)
+    _check(_lib_handle().asot_tile_pairs_host(int(n_dist), int(tile_begin), t1, _ptr(i), _ptr(j), _ptr(v)))
+    return i, j, v.astype(bool)
+
+
+def unpack_tiles(packed: torch.Tensor, n_dist: int, tile_begin: int, tile_end: int,
+                 out: torch.Tensor, zero_diag: bool = True, stream=None) -> torch.Tensor:
+    """KN6: scatter slot-ordered tile results into the N x N matrix (both triangles)."""
+    _need_cuda(packed, out)
+    _check(_lib_handle().asot_unpack_tiles(_ptr(packed), int(n_dist), int(tile_begin),
+                                           int(tile_end), _ptr(out), int(bool(zero_diag)),
+                                           _stream(stream)))
+    return out

@@ -1,0 +1,321 @@
+// asot_api.cu -- the C ABI (include/asot.h): argument checks, workspace carving, dispatch.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "asot_internal.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int32_t g_launches = 0;
+
+asot_status fail(asot_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+#define ASOT_CHECK_ARG(cond, msg) \
+  do {                            \
+    if (!(cond)) return fail(ASOT_ERR_INVALID_ARGUMENT, msg); \
+  } while (0)
+
+#define ASOT_CUDA(call)                                                                        \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(ASOT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+#define ASOT_LAUNCH(call)   \
+  do {                      \
+    ++g_launches;           \
+    ASOT_CUDA(call);        \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// Bump allocator over the caller's workspace.
+struct Carver {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  bool overflow = false;
+  void* take(size_t bytes) {
+    void* p = base ? base + used : nullptr;
+    used += align_up(bytes);
+    if (used > cap) overflow = true;
+    return p;
+  }
+};
+
+asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t iters, float cost_max) {
+  ASOT_CHECK_ARG(n_dist >= 1, "n_dist must be >= 1");
+  ASOT_CHECK_ARG(n_anchors >= 1, "n_anchors must be >= 1");
+  if (n_anchors > asot::kMaxAnchors)
+    return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024 is not supported by this build");
+  ASOT_CHECK_ARG(std::isfinite(eps) && eps > 0.0f, "eps must be finite and > 0");
+  ASOT_CHECK_ARG(iters >= 1, "iters must be >= 1");
+  ASOT_CHECK_ARG(std::isfinite(cost_max) && cost_max >= 0.0f, "cost_max must be finite and >= 0");
+  ASOT_CHECK_ARG((double)cost_max / (double)eps <= 80.0,
+                 "max(C_s)/eps > 80: the fp32 Gibbs kernel would underflow (R#12)");
+  return ASOT_OK;
+}
+
+bool use_tc(int32_t K, asot_precision prec) {
+  return prec == ASOT_PREC_TF32 && asot::sinkhorn_tc_supported(K);
+}
+
+// Gibbs buffers: plain G / GC (SIMT) or swizzled TF32 images (tensor-core path).
+struct GibbsBufs {
+  float* G = nullptr;
+  float* GC = nullptr;
+  uint32_t* g_img = nullptr;
+  uint32_t* gc_img = nullptr;
+};
+
+GibbsBufs carve_gibbs(Carver& cv, int32_t K, bool tc) {
+  GibbsBufs b;
+  if (tc) {
+    const size_t kp = (size_t)asot::kpad32(K);
+    b.g_img = (uint32_t*)cv.take(kp * kp * 4);
+    b.gc_img = (uint32_t*)cv.take(kp * kp * 4);
+  } else {
+    b.G = (float*)cv.take((size_t)K * K * 4);
+    b.GC = (float*)cv.take((size_t)K * K * 4);
+  }
+  return b;
+}
+
+asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink, const float* H,
+                         const float* cost, float eps, int32_t K, int32_t iters, bool tc,
+                         const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
+                         cudaStream_t s) {
+  ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
+                                      tc ? asot::kpad32(K) : K, s));
+  if (tc) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
+                                         gb.gc_img, iters, s));
+  } else {
+    ASOT_LAUNCH(asot::launch_sinkhorn_simt(ps, sink, H, K, gb.G, gb.GC, iters, s));
+  }
+  return ASOT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t asot_abi_version(void) { return ASOT_ABI_VERSION; }
+const char* asot_last_error(void) { return g_last_error.c_str(); }
+int32_t asot_last_launch_count(void) { return g_launches; }
+int64_t asot_num_tiles(int64_t n_dist) { return n_dist < 1 ? 0 : asot::num_tiles(n_dist); }
+
+asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
+  return use_tc(n_anchors, requested) ? ASOT_PREC_TF32 : ASOT_PREC_FP32;
+}
+
+asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
+                                const int64_t* offsets_host, const float* weights,
+                                int64_t n_dist, int32_t dim, const float* anchors,
+                                int32_t n_anchors, int32_t* assign_out, float* hist_out,
+                                uint32_t* status, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(points && offsets && offsets_host && weights && anchors && assign_out &&
+                     hist_out && status,
+                 "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1, "n_dist must be >= 1");
+  ASOT_CHECK_ARG(dim >= 1, "dim must be >= 1");
+  if (dim > asot::kMaxDim) return fail(ASOT_ERR_UNSUPPORTED, "dim > 128 is not supported");
+  ASOT_CHECK_ARG(n_anchors >= 1, "n_anchors must be >= 1");
+  if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
+  ASOT_CHECK_ARG(offsets_host[0] == 0, "offsets[0] must be 0");
+  for (int64_t i = 0; i < n_dist; ++i)
+    ASOT_CHECK_ARG(offsets_host[i + 1] >= offsets_host[i], "offsets must be non-decreasing");
+  const int64_t T = offsets_host[n_dist];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (T > 0) ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
+  ASOT_LAUNCH(asot::launch_histograms(assign_out, weights, offsets, n_dist, n_anchors, hist_out, status, s));
+  return ASOT_OK;
+}
+
+size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
+  Carver cv{nullptr, 0};
+  (void)prec;
+  carve_gibbs(cv, n_anchors, false);  // explicit pair lists run on the fp32 SIMT kernel
+  return cv.used;
+}
+
+asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_anchors,
+                                   const float* cost, float cost_max, float eps, int32_t iters,
+                                   asot_precision prec, const int32_t* pair_i,
+                                   const int32_t* pair_j, int64_t n_pairs, float* dist_out,
+                                   uint32_t* status, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(hist && cost && pair_i && pair_j && dist_out && status, "null pointer argument");
+  asot_status st = check_common(n_dist, n_anchors, eps, iters, cost_max);
+  if (st != ASOT_OK) return st;
+  ASOT_CHECK_ARG(n_pairs >= 0, "n_pairs must be >= 0");
+  if (n_pairs == 0) return ASOT_OK;
+  (void)prec;
+  Carver cv{(char*)workspace, workspace_bytes};
+  GibbsBufs gb = carve_gibbs(cv, n_anchors, false);
+  if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  asot::PairSource ps{pair_i, pair_j, n_pairs, 0, n_dist};
+  asot::PairSink sink{dist_out, nullptr, n_dist, status};
+  return run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, false, gb, 0, 0,
+                      (cudaStream_t)stream);
+}
+
+size_t asot_distance_matrix_workspace_bytes(int64_t n_dist, int64_t n_points, int32_t n_anchors,
+                                            asot_precision prec) {
+  Carver cv{nullptr, 0};
+  cv.take((size_t)n_dist * n_anchors * 4);   // H
+  cv.take((size_t)n_points * 4);             // assign scratch
+  carve_gibbs(cv, n_anchors, use_tc(n_anchors, prec));
+  return cv.used;
+}
+
+asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
+                                 const int64_t* offsets_host, const float* weights,
+                                 int64_t n_dist, int32_t dim, const float* anchors,
+                                 int32_t n_anchors, const float* cost, float cost_max, float eps,
+                                 int32_t iters, asot_precision prec, const float* hist_in,
+                                 int64_t tile_begin, int64_t tile_end, float* dist_out,
+                                 float* packed_out, int32_t* assign_out, float* hist_out,
+                                 uint32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(cost && status, "null pointer argument");
+  asot_status st = check_common(n_dist, n_anchors, eps, iters, cost_max);
+  if (st != ASOT_OK) return st;
+  const int64_t n_tiles = asot::num_tiles(n_dist);
+  ASOT_CHECK_ARG(0 <= tile_begin && tile_begin <= tile_end && tile_end <= n_tiles,
+                 "tile range outside [0, asot_num_tiles(n_dist)]");
+  ASOT_CHECK_ARG(dist_out || packed_out, "need dist_out and/or packed_out");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tc = use_tc(n_anchors, prec);
+
+  int64_t T = 0;
+  if (!hist_in) {
+    ASOT_CHECK_ARG(points && offsets && offsets_host && weights && anchors,
+                   "mapping inputs required when hist_in is NULL");
+    T = offsets_host[n_dist];
+  }
+  Carver cv{(char*)workspace, workspace_bytes};
+  float* H = (float*)cv.take((size_t)n_dist * n_anchors * 4);
+  int32_t* assign = (int32_t*)cv.take((size_t)T * 4);
+  GibbsBufs gb = carve_gibbs(cv, n_anchors, tc);
+  if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+
+  const float* Huse = hist_in;
+  if (!hist_in) {
+    int32_t* asg = assign_out ? assign_out : assign;
+    float* Hw = hist_out ? hist_out : H;
+    const int32_t launches_before = g_launches;
+    st = asot_map_to_anchors(points, offsets, offsets_host, weights, n_dist, dim, anchors,
+                             n_anchors, asg, Hw, status, stream);
+    g_launches += launches_before;
+    if (st != ASOT_OK) return st;
+    Huse = Hw;
+  }
+  asot::PairSource ps{nullptr, nullptr, (tile_end - tile_begin) * asot::kTileSlots, tile_begin, n_dist};
+  asot::PairSink sink{packed_out, dist_out, n_dist, status};
+  st = run_sinkhorn(ps, sink, Huse, cost, eps, n_anchors, iters, tc, gb, tile_begin, tile_end, s);
+  if (st != ASOT_OK) return st;
+  if (dist_out && tile_begin == 0 && tile_end == n_tiles) ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, s));
+  return ASOT_OK;
+}
+
+size_t asot_distance_matrix_host_workspace_bytes(int64_t n_dist, int64_t n_points, int32_t dim,
+                                                 int32_t n_anchors, asot_precision prec) {
+  Carver cv{nullptr, 0};
+  cv.take((size_t)n_points * dim * 4);          // points
+  cv.take((size_t)(n_dist + 1) * 8);            // offsets
+  cv.take((size_t)n_points * 4);                // weights
+  cv.take((size_t)n_anchors * dim * 4);         // anchors
+  cv.take((size_t)n_anchors * n_anchors * 4);   // cost
+  cv.take((size_t)n_dist * n_dist * 4);         // D
+  cv.take(4);                                   // status
+  return cv.used + asot_distance_matrix_workspace_bytes(n_dist, n_points, n_anchors, prec);
+}
+
+asot_status asot_distance_matrix_host(const float* points_host, const int64_t* offsets_host,
+                                      const float* weights_host, int64_t n_dist, int32_t dim,
+                                      const float* anchors_host, int32_t n_anchors,
+                                      const float* cost_host, float eps, int32_t iters,
+                                      asot_precision prec, float* dist_host,
+                                      uint32_t* status_host, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  ASOT_CHECK_ARG(points_host && offsets_host && weights_host && anchors_host && cost_host &&
+                     dist_host && status_host,
+                 "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1 && dim >= 1 && n_anchors >= 1, "sizes must be >= 1");
+  const int64_t T = offsets_host[n_dist];
+  float cmax = 0.0f;
+  for (int64_t e = 0; e < (int64_t)n_anchors * n_anchors; ++e) cmax = fmaxf(cmax, cost_host[e]);
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver cv{(char*)workspace, workspace_bytes};
+  float* d_points = (float*)cv.take((size_t)T * dim * 4);
+  int64_t* d_offsets = (int64_t*)cv.take((size_t)(n_dist + 1) * 8);
+  float* d_weights = (float*)cv.take((size_t)T * 4);
+  float* d_anchors = (float*)cv.take((size_t)n_anchors * dim * 4);
+  float* d_cost = (float*)cv.take((size_t)n_anchors * n_anchors * 4);
+  float* d_D = (float*)cv.take((size_t)n_dist * n_dist * 4);
+  uint32_t* d_status = (uint32_t*)cv.take(4);
+  if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  char* rest = (char*)workspace + cv.used;
+  const size_t rest_bytes = workspace_bytes - cv.used;
+
+  // one cudaMemcpyAsync per buffer (no batched-copy APIs)
+  ASOT_CUDA(cudaMemcpyAsync(d_points, points_host, (size_t)T * dim * 4, cudaMemcpyHostToDevice, s));
+  ASOT_CUDA(cudaMemcpyAsync(d_offsets, offsets_host, (size_t)(n_dist + 1) * 8, cudaMemcpyHostToDevice, s));
+  ASOT_CUDA(cudaMemcpyAsync(d_weights, weights_host, (size_t)T * 4, cudaMemcpyHostToDevice, s));
+  ASOT_CUDA(cudaMemcpyAsync(d_anchors, anchors_host, (size_t)n_anchors * dim * 4, cudaMemcpyHostToDevice, s));
+  ASOT_CUDA(cudaMemcpyAsync(d_cost, cost_host, (size_t)n_anchors * n_anchors * 4, cudaMemcpyHostToDevice, s));
+  ASOT_CUDA(cudaMemsetAsync(d_status, 0, 4, s));
+  asot_status st = asot_distance_matrix(d_points, d_offsets, offsets_host, d_weights, n_dist, dim,
+                                        d_anchors, n_anchors, d_cost, cmax, eps, iters, prec,
+                                        nullptr, 0, asot::num_tiles(n_dist), d_D, nullptr,
+                                        nullptr, nullptr, d_status, rest, rest_bytes, stream);
+  if (st != ASOT_OK) return st;
+  ASOT_CUDA(cudaMemcpyAsync(dist_host, d_D, (size_t)n_dist * n_dist * 4, cudaMemcpyDeviceToHost, s));
+  ASOT_CUDA(cudaMemcpyAsync(status_host, d_status, 4, cudaMemcpyDeviceToHost, s));
+  ASOT_CUDA(cudaStreamSynchronize(s));
+  return ASOT_OK;
+}
+
+asot_status asot_tile_pairs_host(int64_t n_dist, int64_t tile_begin, int64_t tile_end,
+                                 int32_t* i_out, int32_t* j_out, uint8_t* valid_out) {
+  ASOT_CHECK_ARG(i_out && j_out && valid_out, "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1, "n_dist must be >= 1");
+  ASOT_CHECK_ARG(0 <= tile_begin && tile_begin <= tile_end && tile_end <= asot::num_tiles(n_dist),
+                 "bad tile range");
+  int64_t s = 0;
+  for (int64_t t = tile_begin; t < tile_end; ++t)
+    for (int lane = 0; lane < asot::kTileSlots; ++lane, ++s) {
+      int i, j;
+      valid_out[s] = asot::tile_slot_pair(t, lane, n_dist, i, j) ? 1 : 0;
+      i_out[s] = i;
+      j_out[s] = j;
+    }
+  return ASOT_OK;
+}
+
+asot_status asot_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
+                              int64_t tile_end, float* dist_out, int32_t zero_diag, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(packed && dist_out, "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1, "n_dist must be >= 1");
+  ASOT_CHECK_ARG(0 <= tile_begin && tile_begin <= tile_end && tile_end <= asot::num_tiles(n_dist),
+                 "bad tile range");
+  cudaStream_t s = (cudaStream_t)stream;
+  ASOT_LAUNCH(asot::launch_unpack_tiles(packed, n_dist, tile_begin, tile_end, dist_out, s));
+  if (zero_diag) ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, s));
+  return ASOT_OK;
+}
+
+}  // extern "C"

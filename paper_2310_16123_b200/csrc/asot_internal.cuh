@@ -1,0 +1,131 @@
+// asot_internal.cuh -- device helpers and launcher declarations shared by the libasot kernels.
+// Product code only (never includes or mirrors anything under oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "asot.h"
+
+namespace asot {
+
+constexpr int kTileSlots = ASOT_TILE_SLOTS;  // 128 pair slots per tile (8 rows x 16 cols)
+constexpr int kBlockDist = 16;               // distributions per block of the tile grid
+constexpr int kMaxAnchors = 1024;
+constexpr int kMaxDim = 128;
+
+// ------------------------------------------------------------------------------------------
+// Step a4: the pair set.  Tile t -> block pair b = t/2 (row-major over bi <= bj of the
+// nb x nb block grid), half h = t%2; slot lane -> (i, j) = (16bi + 8h + lane/16, 16bj + lane%16).
+// ------------------------------------------------------------------------------------------
+__host__ __device__ inline int64_t num_blocks(int64_t n) { return (n + kBlockDist - 1) / kBlockDist; }
+__host__ __device__ inline int64_t num_tiles(int64_t n) {
+  const int64_t nb = num_blocks(n);
+  return nb * (nb + 1);  // 2 tiles per block pair, nb(nb+1)/2 block pairs
+}
+
+__host__ __device__ inline void block_pair_decode(int64_t b, int64_t nb, int64_t& bi, int64_t& bj) {
+  // rows before r: S(r) = r*nb - r(r-1)/2; find the largest r with S(r) <= b.
+  const double B = 2.0 * (double)nb + 1.0;
+  double disc = B * B - 8.0 * (double)b;
+  if (disc < 0) disc = 0;
+  int64_t r = (int64_t)((B - sqrt(disc)) * 0.5);
+  if (r < 0) r = 0;
+  if (r > nb - 1) r = nb - 1;
+  while (r > 0 && r * nb - r * (r - 1) / 2 > b) --r;
+  while (r + 1 < nb && (r + 1) * nb - (r + 1) * r / 2 <= b) ++r;
+  bi = r;
+  bj = r + (b - (r * nb - r * (r - 1) / 2));
+}
+
+// (i, j) of slot `lane` in tile t; returns validity (i < j < n).
+__host__ __device__ inline bool tile_slot_pair(int64_t t, int lane, int64_t n, int& i, int& j) {
+  const int64_t nb = num_blocks(n);
+  int64_t bi, bj;
+  block_pair_decode(t >> 1, nb, bi, bj);
+  const int64_t ii = bi * kBlockDist + (t & 1) * 8 + (lane >> 4);
+  const int64_t jj = bj * kBlockDist + (lane & 15);
+  i = (int)ii;
+  j = (int)jj;
+  return ii < jj && jj < n;
+}
+
+// Where pairs come from: an explicit (pair_i, pair_j) list, or consecutive tile slots.
+struct PairSource {
+  const int32_t* pi;   // explicit mode when non-null
+  const int32_t* pj;
+  int64_t n_slots;     // explicit: n_pairs; tile mode: (tile_end - tile_begin) * 128
+  int64_t tile_begin;  // tile mode
+  int64_t n_dist;
+};
+
+__device__ inline bool decode_slot(const PairSource& ps, int64_t s, int& i, int& j) {
+  if (s >= ps.n_slots) return false;
+  if (ps.pi != nullptr) {
+    i = ps.pi[s];
+    j = ps.pj[s];
+    return i >= 0 && j >= 0 && i < ps.n_dist && j < ps.n_dist;
+  }
+  return tile_slot_pair(ps.tile_begin + s / kTileSlots, (int)(s % kTileSlots), ps.n_dist, i, j);
+}
+
+// Where results go.
+struct PairSink {
+  float* vec;     // [n_slots] or null
+  float* mat;     // [n_dist, n_dist] or null (both triangles written)
+  int64_t n_dist;
+  uint32_t* status;
+};
+
+__device__ inline void write_result(const PairSink& out, int64_t s, bool valid, int i, int j, float d) {
+  if (valid) {
+    if (!isfinite(d)) atomicOr(out.status, ASOT_FLAG_NONFINITE_OUTPUT);
+    if (out.vec) out.vec[s] = d;
+    if (out.mat) {
+      out.mat[(int64_t)i * out.n_dist + j] = d;
+      out.mat[(int64_t)j * out.n_dist + i] = d;
+    }
+  } else if (out.vec) {
+    out.vec[s] = 0.0f;
+  }
+}
+
+// Round-to-nearest (ties away) fp32 -> TF32, returned in an fp32 container (low 13 bits zero).
+__device__ __forceinline__ uint32_t tf32_rna_bits(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// Byte offset of element (row n, k) in the K-major SWIZZLE_128B UMMA operand image of an
+// [rows x kpad] fp32 matrix: k-blocks of 32 elements (128 B) stored one after another, each
+// [rows][128 B] with 8-row / 1024 B swizzle atoms (16-byte chunk index XOR row%8).
+__host__ __device__ inline uint32_t sw128_kmajor_offset(uint32_t n, uint32_t k, uint32_t rows) {
+  const uint32_t kb = k >> 5, kin = k & 31;
+  const uint32_t lin = kb * rows * 128u + n * 128u + kin * 4u;
+  return lin ^ (((lin >> 7) & 7u) << 4);
+}
+
+// ------------------------------------------------------------------------------------------
+// Launchers (return cudaGetLastError() after the launch).
+// ------------------------------------------------------------------------------------------
+cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, float* GC,
+                              uint32_t* g_img, uint32_t* gc_img, int kpad, cudaStream_t s);
+cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
+                              int32_t* assign, uint32_t* status, cudaStream_t s);
+cudaError_t launch_histograms(const int32_t* assign, const float* weights, const int64_t* offsets,
+                              int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s);
+cudaError_t launch_sinkhorn_simt(const PairSource& ps, const PairSink& out, const float* H, int K,
+                                 const float* G, const float* GC, int iters, cudaStream_t s);
+// tcgen05 TF32 kernel, tile mode only, K <= 128 (images padded to kpad = roundup(K, 32)).
+bool sinkhorn_tc_supported(int K);
+cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_dist,
+                               const PairSink& out, const float* H, int K, const uint32_t* g_img,
+                               const uint32_t* gc_img, int iters, cudaStream_t s);
+cudaError_t launch_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
+                                int64_t tile_end, float* mat, cudaStream_t s);
+cudaError_t launch_zero_diag(float* mat, int64_t n_dist, cudaStream_t s);
+
+inline int kpad32(int K) { return (K + 31) & ~31; }
+
+}  // namespace asot

@@ -1,0 +1,302 @@
+// asot_map.cu -- steps a1 (Gibbs kernel), a2 (one-hot nearest-anchor mapping) and a3 (mapped
+// marginal histograms) for sm_100a.
+//
+// a2 (P:214 one-hot P_o; "P_o is the clustering operator"; S:378 argmin, lowest index on
+// ties).  The decision must be bit-exact against the fp64 definition (reading R#8):
+// D_pj = sum_k (x_pk - w_jk)^2 accumulated sequentially in k in fp64 with every op rounded.
+// Kernel: a point x anchor distance tile.  Each point is held in registers by 4 lanes; each lane
+// scans every 4th anchor of the SMEM-staged anchor chunk in fp32 (direct differences, FMA), the
+// 4 lanes merge (best, index, second-best) with warp shuffles.  fp32 with a rigorous bound:
+// for d non-negative rounded terms, |D32 - D| <= gamma_{d+2} D (gamma_n = n u / (1 - n u),
+// u = 2^-24).  If the runner-up D32 exceeds best * (1 + 5 gamma) (+ an absolute underflow
+// slack) the fp32 winner provably is the fp64 winner; otherwise the 4 lanes recompute all K
+// distances with the fp64 op sequence above and take the (value, index) minimum.
+//
+// a3 (Eq. (5) P:100 with the 1/n factor dropped, R#1; Lemma 1 proof a' = Z^T a P:145, P:417;
+// S:196).  One warp per distribution builds H[i, :] in shared memory in fp64: points are
+// visited in order and the lane owning bin (j mod 32) adds w_p, so every bin is a sequential
+// point-order fp64 sum, rounded once to fp32.
+#include <cfloat>
+#include <cmath>
+
+#include "asot_internal.cuh"
+
+namespace asot {
+
+// ------------------------------------------------------------------------------ a1: Gibbs prep
+__global__ void gibbs_prep_kernel(const float* __restrict__ cost, int K, float eps,
+                                  float* __restrict__ G, float* __restrict__ GC,
+                                  uint32_t* __restrict__ g_img, uint32_t* __restrict__ gc_img,
+                                  int kpad) {
+  const int64_t total = (int64_t)kpad * kpad;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(idx / kpad), k = (int)(idx % kpad);
+    const bool in = n < K && k < K;
+    const double c = in ? (double)cost[(int64_t)n * K + k] : 0.0;
+    const double g = in ? exp(-c / (double)eps) : 0.0;  // P:183  K := exp(-C_s / eps)
+    const float g32 = (float)g, gc32 = (float)(g * c);
+    if (in && G != nullptr) {
+      G[(int64_t)n * K + k] = g32;
+      GC[(int64_t)n * K + k] = gc32;
+    }
+    if (g_img != nullptr) {
+      const uint32_t off = sw128_kmajor_offset((uint32_t)n, (uint32_t)k, (uint32_t)kpad) >> 2;
+      g_img[off] = tf32_rna_bits(g32);
+      gc_img[off] = tf32_rna_bits(gc32);
+    }
+  }
+}
+
+cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, float* GC,
+                              uint32_t* g_img, uint32_t* gc_img, int kpad, cudaStream_t s) {
+  const int64_t total = (int64_t)kpad * kpad;
+  const int threads = 256;
+  const int blocks = (int)((total + threads - 1) / threads);
+  gibbs_prep_kernel<<<blocks, threads, 0, s>>>(cost, K, eps, G, GC, g_img, gc_img, kpad);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ a2: mapping
+constexpr int kMapThreads = 256;
+constexpr int kLanesPerPoint = 4;
+constexpr int kPointsPerBlock = kMapThreads / kLanesPerPoint;  // 64
+
+struct BestTriple {
+  float best;
+  float second;
+  int idx;
+};
+
+__device__ __forceinline__ void merge_triple(BestTriple& a, float ob, float os, int oi) {
+  // (value, index) order for the best; second = smallest value among the rest
+  if (ob < a.best || (ob == a.best && oi < a.idx)) {
+    a.second = fminf(a.best, os);
+    a.best = ob;
+    a.idx = oi;
+  } else {
+    a.second = fminf(a.second, ob);
+  }
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kMapThreads)
+map_assign_kernel(const float* __restrict__ points, int64_t T, int dim,
+                  const float* __restrict__ anchors, int K, int chunk,
+                  int32_t* __restrict__ assign, uint32_t* __restrict__ status) {
+  extern __shared__ float4 map_smem4[];
+  float* Ws = reinterpret_cast<float*>(map_smem4);  // [chunk][DP + 4]
+  constexpr int RS = DP + 4;                        // row stride: 16-byte shift per row
+  const int lane = threadIdx.x & 31;
+  const int q = threadIdx.x & (kLanesPerPoint - 1);
+  const int64_t p = (int64_t)blockIdx.x * kPointsPerBlock + (threadIdx.x >> 2);
+  const bool valid = p < T;
+
+  float x[DP];
+  bool finite = true;
+#pragma unroll
+  for (int k = 0; k < DP; ++k) {
+    const float v = (valid && k < dim) ? points[p * dim + k] : 0.0f;
+    finite &= isfinite(v);
+    x[k] = v;
+  }
+  if (!finite) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
+
+  BestTriple bt{INFINITY, INFINITY, 0x7fffffff};
+  for (int j0 = 0; j0 < K; j0 += chunk) {
+    const int nc = min(chunk, K - j0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * DP; e += kMapThreads) {
+      const int jj = e / DP, k = e % DP;
+      const float v = k < dim ? anchors[(int64_t)(j0 + jj) * dim + k] : 0.0f;
+      if (!isfinite(v)) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
+      Ws[jj * RS + k] = v;
+    }
+    __syncthreads();
+    for (int jj = q; jj < nc; jj += kLanesPerPoint) {
+      const float4* w4 = reinterpret_cast<const float4*>(Ws + jj * RS);
+      float acc = 0.0f;
+#pragma unroll
+      for (int k4 = 0; k4 < DP / 4; ++k4) {
+        const float4 w = w4[k4];
+        float t = x[4 * k4 + 0] - w.x; acc = fmaf(t, t, acc);
+        t = x[4 * k4 + 1] - w.y; acc = fmaf(t, t, acc);
+        t = x[4 * k4 + 2] - w.z; acc = fmaf(t, t, acc);
+        t = x[4 * k4 + 3] - w.w; acc = fmaf(t, t, acc);
+      }
+      const int j = j0 + jj;  // increasing per lane: strict < keeps the lowest index
+      if (acc < bt.best) {
+        bt.second = bt.best;
+        bt.best = acc;
+        bt.idx = j;
+      } else if (acc < bt.second) {
+        bt.second = acc;
+      }
+    }
+  }
+  // warp-shuffle argmin across the 4 lanes that share this point
+#pragma unroll
+  for (int off = 1; off < kLanesPerPoint; off <<= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, bt.best, off);
+    const float os = __shfl_xor_sync(0xffffffffu, bt.second, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bt.idx, off);
+    merge_triple(bt, ob, os, oi);
+  }
+
+  // near-tie test with the rigorous fp32 bound (gamma_{d+2}, 5x slack incl. rounding of thr)
+  const float u = 5.9604645e-8f;  // 2^-24
+  const float nd = (float)(dim + 2);
+  const float gamma = nd * u / (1.0f - nd * u);
+  const float thr = bt.best * (1.0f + 5.0f * gamma) + 1e-35f;
+  const bool refine = valid && K > 1 && (bt.second <= thr);
+  if (__any_sync(0xffffffffu, refine)) {
+    // fp64 recomputation in the pinned op order: t = x - w; sq = t*t; acc = acc + sq (no FMA)
+    double bd = INFINITY;
+    int bi = 0x7fffffff;
+    if (refine) {
+      for (int j = q; j < K; j += kLanesPerPoint) {
+        const float* wr = anchors + (int64_t)j * dim;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+          const double w = k < dim ? (double)wr[k] : 0.0;
+          const double t = __dsub_rn((double)x[k], w);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+        if (acc < bd) {
+          bd = acc;
+          bi = j;
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < kLanesPerPoint; off <<= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, bd, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ob < bd || (ob == bd && oi < bi)) {
+        bd = ob;
+        bi = oi;
+      }
+    }
+    if (refine) bt.idx = bi;
+  }
+  (void)lane;
+  if (valid && q == 0) assign[p] = bt.idx;
+}
+
+template <int DP>
+static cudaError_t launch_map_dp(const float* points, int64_t T, int dim, const float* anchors,
+                                 int K, int32_t* assign, uint32_t* status, cudaStream_t s) {
+  const int rs_bytes = (DP + 4) * 4;
+  int chunk = (96 * 1024) / rs_bytes;
+  if (chunk > K) chunk = K;
+  const size_t smem = (size_t)chunk * rs_bytes;
+  cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t blocks = (T + kPointsPerBlock - 1) / kPointsPerBlock;
+  if (blocks == 0) return cudaSuccess;
+  map_assign_kernel<DP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, T, dim, anchors, K,
+                                                                   chunk, assign, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
+                              int32_t* assign, uint32_t* status, cudaStream_t s) {
+  if (dim <= 8) return launch_map_dp<8>(points, T, dim, anchors, K, assign, status, s);
+  if (dim <= 16) return launch_map_dp<16>(points, T, dim, anchors, K, assign, status, s);
+  if (dim <= 32) return launch_map_dp<32>(points, T, dim, anchors, K, assign, status, s);
+  if (dim <= 64) return launch_map_dp<64>(points, T, dim, anchors, K, assign, status, s);
+  return launch_map_dp<128>(points, T, dim, anchors, K, assign, status, s);
+}
+
+// ------------------------------------------------------------------------------ a3: histograms
+constexpr int kHistWarps = 4;
+
+__global__ void __launch_bounds__(kHistWarps * 32)
+histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ weights,
+                 const int64_t* __restrict__ offsets, int64_t n_dist, int K,
+                 float* __restrict__ H, uint32_t* __restrict__ status) {
+  extern __shared__ double hist_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kHistWarps + warp;
+  if (i >= n_dist) return;
+  double* h = hist_smem + (size_t)warp * K;
+  for (int r = lane; r < K; r += 32) h[r] = 0.0;
+  __syncwarp();
+  const int64_t s = offsets[i], e = offsets[i + 1];
+  if (lane == 0 && e <= s) atomicOr(status, ASOT_FLAG_EMPTY_DIST);
+  double msum = 0.0;
+  bool bad = false;
+  for (int64_t p0 = s; p0 < e; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const int a = p < e ? assign[p] : 0;
+    const float w = p < e ? weights[p] : 0.0f;
+    if (p < e) {
+      bad |= !(w >= 0.0f) || !isfinite(w) || a < 0 || a >= K;
+      msum += (double)w;
+    }
+    const int cnt = (e - p0) < 32 ? (int)(e - p0) : 32;
+    for (int t = 0; t < cnt; ++t) {  // point order
+      const int at = __shfl_sync(0xffffffffu, a, t);
+      const float wt = __shfl_sync(0xffffffffu, w, t);
+      if (lane == (at & 31) && at >= 0 && at < K) h[at] = h[at] + (double)wt;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) msum += __shfl_xor_sync(0xffffffffu, msum, off);
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) atomicOr(status, ASOT_FLAG_BAD_MASS | ASOT_FLAG_NONFINITE_INPUT);
+  } else if (lane == 0 && e > s && fabs(msum - 1.0) > 1e-5) {
+    atomicOr(status, ASOT_FLAG_BAD_MASS);
+  }
+  __syncwarp();
+  for (int r = lane; r < K; r += 32) H[i * K + r] = (float)h[r];
+}
+
+cudaError_t launch_histograms(const int32_t* assign, const float* weights, const int64_t* offsets,
+                              int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s) {
+  if (n_dist == 0) return cudaSuccess;
+  const size_t smem = (size_t)kHistWarps * K * sizeof(double);
+  cudaFuncSetAttribute(histogram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t blocks = (n_dist + kHistWarps - 1) / kHistWarps;
+  histogram_kernel<<<(unsigned)blocks, kHistWarps * 32, smem, s>>>(assign, weights, offsets, n_dist,
+                                                                  K, H, status);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ KN6 helpers
+__global__ void unpack_tiles_kernel(const float* __restrict__ packed, int64_t n_dist,
+                                    int64_t tile_begin, int64_t n_slots, float* __restrict__ mat) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_slots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int i, j;
+    if (tile_slot_pair(tile_begin + s / kTileSlots, (int)(s % kTileSlots), n_dist, i, j)) {
+      const float d = packed[s];
+      mat[(int64_t)i * n_dist + j] = d;
+      mat[(int64_t)j * n_dist + i] = d;
+    }
+  }
+}
+
+cudaError_t launch_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
+                                int64_t tile_end, float* mat, cudaStream_t s) {
+  const int64_t n_slots = (tile_end - tile_begin) * kTileSlots;
+  if (n_slots <= 0) return cudaSuccess;
+  int64_t blocks = (n_slots + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  unpack_tiles_kernel<<<(unsigned)blocks, 256, 0, s>>>(packed, n_dist, tile_begin, n_slots, mat);
+  return cudaGetLastError();
+}
+
+__global__ void zero_diag_kernel(float* mat, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mat[i * n + i] = 0.0f;  // R#9: D[i, i] := 0, never computed
+}
+
+cudaError_t launch_zero_diag(float* mat, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  zero_diag_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mat, n);
+  return cudaGetLastError();
+}
+
+}  // namespace asot

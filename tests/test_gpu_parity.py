@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): anchor assignments bit-exact; histograms equal to the oracle's
+fp64 point-order sums rounded to f32; distances within relative error 1e-4 (ASOT_PREC_FP32) or
+2e-3 (ASOT_PREC_TF32) with rel = |D_gpu - D_orc| / max(D_orc, 1e-3 max C_s) (R#20).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from asot_inputs import make_inputs, random_pairs  # noqa: E402
+from oracle import asot_oracle as O  # noqa: E402
+
+TOL = {0: 1e-4, 1: 2e-3}
+
+
+@pytest.fixture(scope="module")
+def asot():
+    import paper_2310_16123_b200 as m
+    return m
+
+
+def dev_inputs(inp):
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t(inp.points), t(inp.offsets), t(inp.weights), t(inp.anchors), t(inp.cost)
+
+
+def rel_err(Dg, Do, cmax):
+    return np.abs(np.asarray(Dg, np.float64) - Do) / np.maximum(Do, 1e-3 * cmax)
+
+
+_oracle_cache = {}
+
+
+def oracle_full(cfg, n):
+    key = (cfg, n)
+    if key not in _oracle_cache:
+        inp = make_inputs(cfg, n_dist=n)
+        D, assign, H = O.distance_matrix(inp.points, inp.offsets, inp.weights, inp.anchors,
+                                         inp.cost, inp.eps, inp.iters)
+        _oracle_cache[key] = (inp, D, assign, H)
+    return _oracle_cache[key]
+
+
+# ------------------------------------------------------------------ mapping + histograms
+@pytest.mark.parametrize("cfg,n", [("c1", 64), ("c2", 1000), ("c3", 200), ("c4", 8000), ("c5", 40)])
+def test_mapping_bit_exact(asot, cfg, n):
+    inp = make_inputs(cfg, n_dist=n)
+    pts, offs, w, anc, _ = dev_inputs(inp)
+    assign, H, st = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    a_o = O.map_assign(inp.points, inp.anchors)
+    a_g = assign.cpu().numpy()
+    assert np.array_equal(a_g, a_o), f"{(a_g != a_o).sum()} of {a_o.size} assignments differ"
+    H_o = O.histograms(a_o, inp.weights, inp.offsets, inp.n_anchors).astype(np.float32)
+    np.testing.assert_array_equal(H.cpu().numpy(), H_o)
+
+
+def test_mapping_adversarial_ties(asot):
+    rng = np.random.default_rng(5)
+    d, K = 32, 64
+    W = rng.integers(-3, 4, size=(K, d)).astype(np.float32)
+    W[10] = W[3]                                     # duplicate anchor -> lower index
+    pts = []
+    for _ in range(600):                             # exact midpoints of integer anchors: exact ties
+        a, b = rng.choice(K, 2, replace=False)
+        pts.append((W[a] + W[b]) / 2)
+    for gap in (1e-9, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4):  # near ties at relative gaps
+        for _ in range(300):
+            a, b = rng.choice(K, 2, replace=False)
+            m = (W[a].astype(np.float64) + W[b]) / 2 + gap * (W[b].astype(np.float64) - W[a])
+            pts.append(m)
+    pts.append(W[3]); pts.append(W[10]); pts.append(W[0])
+    X = np.asarray(pts, dtype=np.float32)
+    off = np.array([0, X.shape[0]], np.int64)
+    w = np.full(X.shape[0], np.float32(1.0 / X.shape[0]))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    assign, H, st = asot.map_to_anchors(t(X), t(off), t(w), t(W), offsets_host=off)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(assign.cpu().numpy(), O.map_assign(X, W))
+    assert assign.cpu().numpy()[-2] == 3
+
+
+# ------------------------------------------------------------------ distances (whole pipeline)
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("cfg,n", [("c1", 64), ("c2", 90), ("c3", 36), ("c4", 50), ("c5", 18)])
+def test_distance_matrix_parity(asot, cfg, n, prec):
+    inp, Do, _, _ = oracle_full(cfg, n)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                             offsets_host=inp.offsets, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    Dg = D.cpu().numpy()
+    eff = asot.effective_precision(inp.n_anchors, prec)
+    assert np.all(np.diag(Dg) == 0)
+    np.testing.assert_array_equal(Dg, Dg.T)
+    assert np.all(Dg >= 0)
+    r = rel_err(Dg, Do, float(inp.cost.max()))
+    assert r.max() <= TOL[eff], f"{cfg} prec={eff}: max rel {r.max():.3e} p99 {np.quantile(r, .99):.3e}"
+
+
+def test_pairwise_explicit_pairs(asot):
+    inp, Do, _, H_o = oracle_full("c2", 90)
+    pi, pj = random_pairs(inp.n_dist, 700, seed=9)
+    pi = np.concatenate([pi, pj[:50]]).astype(np.int32)  # include reversed orientation (R#10)
+    pj2 = np.concatenate([pj, pi[:50]]).astype(np.int32)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    _, H, _ = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+    d = asot.pairwise_sinkhorn(H, cst, float(inp.eps), inp.iters, torch.from_numpy(pi).cuda(),
+                               torch.from_numpy(pj2).cuda(), precision=asot.FP32)
+    c_o, _ = O.pair_costs(H_o, inp.cost, inp.eps, inp.iters, pi.astype(np.int64), pj2.astype(np.int64))
+    r = rel_err(d.cpu().numpy(), c_o, float(inp.cost.max()))
+    assert r.max() <= 1e-4
+
+
+def test_tile_ranges_and_determinism(asot):
+    inp, _, _, _ = oracle_full("c2", 90)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    for prec in (0, 1):
+        D1 = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                                  offsets_host=inp.offsets)
+        D2 = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                                  offsets_host=inp.offsets)
+        assert torch.equal(D1, D2)                        # bitwise re-run determinism
+        nt = asot.num_tiles(inp.n_dist)
+        D3 = torch.full_like(D1, -1.0)
+        cuts = [0, 3, nt // 2, nt - 1, nt]
+        for a, b in zip(cuts[:-1], cuts[1:]):             # rank-style partition + unpack (KN6)
+            packed = torch.empty((b - a) * 128, device="cuda")
+            asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                                 offsets_host=inp.offsets, tile_range=(a, b), packed=packed,
+                                 want_matrix=False)
+            asot.unpack_tiles(packed, inp.n_dist, a, b, D3, zero_diag=(b == nt))
+        assert torch.equal(D1, D3)
+
+
+def test_host_entry_point_matches_device(asot):
+    inp, _, _, _ = oracle_full("c1", 64)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    for prec in (0, 1):
+        Dd = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                                  offsets_host=inp.offsets).cpu().numpy()
+        Dh, status = asot.distance_matrix_host(inp.points, inp.offsets, inp.weights, inp.anchors,
+                                               inp.cost, float(inp.eps), inp.iters, precision=prec)
+        assert status == 0
+        np.testing.assert_array_equal(Dh, Dd)
+
+
+def test_one_hot_histograms_exact_cost(asot):
+    """Special case: one-hot a', b' => d = C_s(u, v) exactly for any eps, L (oracle pin); on the
+    GPU only the fp32 / TF32 rounding of K and K (.) C_s remains."""
+    K, N = 128, 40
+    rng = np.random.default_rng(2)
+    W = rng.normal(size=(K, 8)).astype(np.float32)
+    from asot_inputs import normalized_sqeuclid_cost
+    C = normalized_sqeuclid_cost(W)
+    u = rng.integers(0, K, N)
+    H = np.zeros((N, K), np.float32)
+    H[np.arange(N), u] = 1.0
+    Ht = torch.from_numpy(H).cuda()
+    Ct = torch.from_numpy(C).cuda()
+    for prec in (0, 1):
+        D = asot.distance_matrix(None, None, None, None, Ct, 0.05, 30, precision=prec, hist=Ht).cpu().numpy()
+        want = C[u][:, u].astype(np.float64)
+        np.fill_diagonal(want, 0)
+        r = rel_err(D, want, 1.0)
+        assert r.max() <= TOL[asot.effective_precision(K, prec)]
+
+
+def test_full_size_sampled_parity_c2(asot):
+    """BASELINE configs[1] at full size (N = 1000) in the launch configuration bench.py times:
+    sampled pairs against the oracle evaluated pair by pair."""
+    inp = make_inputs("c2")
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=asot.TF32,
+                             offsets_host=inp.offsets, cost_max=1.0, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    assign_o, H_o = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
+    pi, pj = random_pairs(inp.n_dist, 400, seed=17)
+    edge_i = np.array([0, 0, 15, 16, 991, 998, 7, 8], np.int32)   # block / tile boundaries, tail
+    edge_j = np.array([1, 999, 16, 17, 999, 999, 8, 15], np.int32)
+    pi = np.concatenate([pi, edge_i]); pj = np.concatenate([pj, edge_j])
+    c_o, _ = O.pair_costs(H_o, inp.cost, inp.eps, inp.iters, pi.astype(np.int64), pj.astype(np.int64))
+    Dg = D.cpu().numpy()
+    r = rel_err(Dg[pi, pj], c_o, 1.0)
+    eff = asot.effective_precision(inp.n_anchors, asot.TF32)
+    assert r.max() <= TOL[eff]
+    np.testing.assert_array_equal(Dg, Dg.T)
+    assert np.all(np.diag(Dg) == 0)
