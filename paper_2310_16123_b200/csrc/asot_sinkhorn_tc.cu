@@ -1,9 +1,376 @@
-// asot_sinkhorn_tc.cu -- placeholder until the tcgen05 kernel lands.
+// asot_sinkhorn_tc.cu -- steps a5 + a6 on the 5th-gen tensor cores (tcgen05, kind::tf32), K <= 128.
+//
+// Batched Sinkhorn on the shared Gibbs kernel ("GPU parallelization version"):
+//   U = A / (K V),  V = B / (K^T U)  with  V^(0) = 1, exactly L iterations (R#4, R#5),
+// then d = <diag(u) K diag(v), C_s> = sum_c v_c ((K (.) C_s)^T u)_c  (R#3, R#6).
+//
+// Layout: pairs are the MMA M dimension.  A pair tile (128 slots, step a4) is one M = 128 MMA:
+//   D[p, r] = sum_c X[p, c] * K[c, r]       (X = V^T or U^T, K symmetric)
+// with X held in TENSOR MEMORY as the A operand (lane p = pair, column c = anchor, TF32 bits),
+// the Gibbs kernel K (and K (.) C_s for the cost) resident in SHARED MEMORY as the B operand
+// (K-major SWIZZLE_128B image staged once per CTA by a TMA bulk copy), and the fp32 accumulator
+// D in TMEM.  The scalings of a tile never leave the SM for all 2L+1 MMA phases.
+//
+// Warp roles (256 threads): warps 0-3 (slot 0) and 4-7 (slot 1) are two warpgroups, each owning
+// one pair tile; after a warpgroup barrier one elected thread issues that slot's tcgen05.mma
+// chain and commits it to the slot's mbarrier.  While the tensor core computes one slot's
+// product, the other warpgroup turns its own accumulator into the next scaling (tcgen05.ld -> u = a * rcp(max(D, FLT_MIN)) -> cvt.rna.tf32
+// -> tcgen05.st), so MMA and the elementwise divide overlap (ping-pong).  Each thread owns one
+// pair (its TMEM lane) and all K anchors, so the final cost reduction needs no cross-thread sum:
+// the last v-update keeps v (fp32) in registers, the cost phase multiplies by K (.) C_s applied
+// to u (TMEM) and reduces in-thread.
+//
+// TMEM map (columns): slot s: A at 2s*KP, D at 2s*KP + KP.  SMEM: [K image | KC image |
+// marginal rows (8 a-rows, 16 b-rows, 1 zero row) per slot | mbarriers].
+#include <cfloat>
+
 #include "asot_internal.cuh"
+
 namespace asot {
-bool sinkhorn_tc_supported(int K) { (void)K; return false; }
-cudaError_t launch_sinkhorn_tc(int64_t, int64_t, int64_t, const PairSink&, const float*, int,
-                               const uint32_t*, const uint32_t*, int, cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace tc {
+
+constexpr int kThreads = 256;
+constexpr int kEpiWarps = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (Blackwell version 1), SBO = 1024 B.
+__device__ __forceinline__ uint64_t make_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;          // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;  // SBO: 8-row group stride
+  d |= (uint64_t)1u << 46;          // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;          // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+#define ASOT_R32(a)                                                                          \
+  "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),        \
+      "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]), \
+      "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]),          \
+      "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]), "=r"(a[25]),          \
+      "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31])
+#define ASOT_W32(a)                                                                        \
+  "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),  \
+      "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]),    \
+      "r"(a[15]), "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]),  \
+      "r"(a[22]), "r"(a[23]), "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]),  \
+      "r"(a[29]), "r"(a[30]), "r"(a[31])
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : ASOT_R32(r)
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31, %32};" ::"r"(taddr),
+      ASOT_W32(r)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int KP>
+struct Smem {
+  static constexpr int kRS = KP + 4;                      // marginal row stride (floats)
+  static constexpr int kRows = 8 + 16 + 1;                // a-rows, b-rows, zero row
+  static constexpr size_t kImg = (size_t)KP * KP * 4;     // one operand image
+  static constexpr size_t kMarg = (size_t)kRows * kRS * 4;
+  static constexpr size_t kOffG = 0;
+  static constexpr size_t kOffGC = kImg;
+  static constexpr size_t kOffMarg = 2 * kImg;
+  static constexpr size_t kOffBar = kOffMarg + 2 * kMarg;
+  static constexpr size_t kBytes = kOffBar + 64 + 1024;  // + alignment slack
+};
+
+template <int KP>
+__global__ void __launch_bounds__(kThreads, 1)
+sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
+                   const float* __restrict__ H, int K, const uint32_t* __restrict__ g_img,
+                   const uint32_t* __restrict__ gc_img, int iters) {
+  using S = Smem<KP>;
+  constexpr uint32_t kTmemCols = (4 * KP <= 32) ? 32 : (4 * KP <= 64) ? 64 : (4 * KP <= 128) ? 128
+                               : (4 * KP <= 256) ? 256 : 512;
+  constexpr uint32_t kIdesc = make_idesc_tf32(128, KP);
+  constexpr int kWG = kEpiWarps * 32;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* marg = (float*)(smem + S::kOffMarg);
+  uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
+  uint32_t* tmem_holder = (uint32_t*)(bars + 6);
+  const uint32_t bar_g = smem_u32(&bars[0]);
+  const uint32_t bar_mma0 = smem_u32(&bars[1]);  // +8*s
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = warp / kEpiWarps;         // slot (pair tile) owned by this warpgroup
+  const int sub = warp & 3;               // TMEM lane quarter this warp may access
+  const int p = sub * 32 + lane;          // pair slot within the tile == TMEM lane
+  const int wg_tid = threadIdx.x - s * kWG;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_g, 1);
+    mbar_init(bar_mma0, 1);
+    mbar_init(bar_mma0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) {  // stage K and K (.) C_s once per CTA (TMA bulk copies)
+    mbar_expect_tx(bar_g, (uint32_t)(2 * S::kImg));
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t off = 0; off < S::kImg; off += kChunk) {
+      const uint32_t n = (uint32_t)((S::kImg - off) < kChunk ? (S::kImg - off) : kChunk);
+      bulk_g2s(smem_u32(smem + S::kOffG + off), (const uint8_t*)g_img + off, n, bar_g);
+      bulk_g2s(smem_u32(smem + S::kOffGC + off), (const uint8_t*)gc_img + off, n, bar_g);
+    }
+  }
+
+  float* mrows = marg + (size_t)s * S::kRows * S::kRS;
+  const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+  const uint32_t a_col = (uint32_t)(2 * s * KP);
+  const uint32_t a_tmem = tmem_base + lane_off + a_col;   // this thread's lane of A
+  const uint32_t d_tmem = a_tmem + KP;                    // this thread's lane of D
+  const uint32_t bar_mma = bar_mma0 + 8 * s;
+  const uint32_t g_base = smem_u32(smem + S::kOffG), gc_base = smem_u32(smem + S::kOffGC);
+  uint32_t mma_par = 0;
+  bool g_ready = false;
+  float stash[KP];
+
+  // Warpgroup barrier, then one elected thread issues D = A (.) B for this slot and commits.
+  auto issue_phase = [&](bool cost_phase) {
+    tc_fence_before();
+    named_bar_sync(1 + s, kWG);
+    if (wg_tid == 0) {
+      if (!g_ready) {
+        mbar_wait(bar_g, 0);
+        g_ready = true;
+      }
+      tc_fence_after();
+      const uint32_t a0 = tmem_base + a_col, d0 = tmem_base + a_col + KP;
+      const uint32_t b_base = cost_phase ? gc_base : g_base;
+#pragma unroll
+      for (int ks = 0; ks < KP / 8; ++ks) {
+        const uint32_t b_addr = b_base + (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32);
+        mma_tf32_ts(d0, a0 + 8 * ks, make_sw128_desc(b_addr), kIdesc, ks > 0 ? 1u : 0u);
+      }
+      mma_commit(bar_mma);
+    }
+  };
+
+  for (int64_t tk = s;; tk += 2) {
+    const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
+    if (tr >= n_tiles) break;
+    const int64_t t = tile_begin + tr;
+    // ---- tile init: marginal rows -> SMEM, V^T = 1 -> TMEM (A operand)
+    int64_t bi, bj;
+    block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
+    const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
+    named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows
+    for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
+      const int r = e / KP, c = e % KP;
+      const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
+      mrows[r * S::kRS + c] = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+    }
+    int ii, jj;
+    const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
+    const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS;
+    const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS;
+    {
+      uint32_t ones[32];
+#pragma unroll
+      for (int c = 0; c < KP / 32; ++c) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) ones[e] = (valid && c * 32 + e < K) ? 0x3f800000u : 0u;
+        tmem_st32(a_tmem + c * 32, ones);
+      }
+    }
+    tmem_wait_st();
+    issue_phase(false);  // (also publishes mrows to the warpgroup)
+
+    for (int f = 0; f < 2 * iters; ++f) {
+      mbar_wait(bar_mma, mma_par);
+      mma_par ^= 1u;
+      tc_fence_after();
+      const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
+      const bool last = f == 2 * iters - 1;
+#pragma unroll
+      for (int c = 0; c < KP / 32; ++c) {
+        uint32_t d[32];
+        tmem_ld32(d_tmem + c * 32, d);
+        tmem_wait_ld();
+        uint32_t o[32];
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 m4 = *reinterpret_cast<const float4*>(mrow + c * 32 + e);
+          const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float den = fmaxf(__uint_as_float(d[e + q]), FLT_MIN);
+            const float x = mv[q] * rcp_approx(den);  // 0 / x = 0 (R#11)
+            stash[c * 32 + e + q] = x;
+            o[e + q] = tf32_rna_bits(x);
+          }
+        }
+        if (!last) tmem_st32(a_tmem + c * 32, o);
+      }
+      if (!last) tmem_wait_st();
+      issue_phase(last);  // after the last v-update: D = U_L^T (K (.) C_s)
+    }
+    // ---- cost phase: d = sum_c v_c ((K (.) C_s)^T u)_c, in-thread (one pair per thread)
+    mbar_wait(bar_mma, mma_par);
+    mma_par ^= 1u;
+    tc_fence_after();
+    float acc = 0.0f;
+#pragma unroll
+    for (int c = 0; c < KP / 32; ++c) {
+      uint32_t d[32];
+      tmem_ld32(d_tmem + c * 32, d);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) acc = fmaf(stash[c * 32 + e], __uint_as_float(d[e]), acc);
+    }
+    write_result(out, tr * kTileSlots + p, valid, ii, jj, acc);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+template <int KP>
+static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, const PairSink& out,
+                             const float* H, int K, const uint32_t* g_img, const uint32_t* gc_img,
+                             int iters, cudaStream_t s) {
+  const size_t smem = Smem<KP>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(sinkhorn_tc_kernel<KP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (n_tiles + 1) / 2;
+  if (grid > sms) grid = sms;
+  if (grid < 1) return cudaSuccess;
+  sinkhorn_tc_kernel<KP><<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+                                                               g_img, gc_img, iters);
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+
+bool sinkhorn_tc_supported(int K) { return K >= 1 && K <= 128; }
+
+cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_dist,
+                               const PairSink& out, const float* H, int K, const uint32_t* g_img,
+                               const uint32_t* gc_img, int iters, cudaStream_t s) {
+  const int64_t n_tiles = tile_end - tile_begin;
+  if (n_tiles <= 0) return cudaSuccess;
+  switch (kpad32(K)) {
+    case 32: return tc::launch_kp<32>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
+    case 64: return tc::launch_kp<64>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
+    case 96: return tc::launch_kp<96>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
+    case 128: return tc::launch_kp<128>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 }  // namespace asot
