@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""ASOT pairwise-distance benchmark (BASELINE.json metric) on 1..N B200s.
+
+A step = the whole hot path over one batch: device-resident points,
+offsets, weights, anchors and C_s  ->  mapping + histograms, Gibbs kernel, batched Sinkhorn on
+every pair i < j, cost reduction  ->  the complete N x N matrix on rank 0.  Multi-GPU shards the
+upper-triangular pair tiles (strong scaling of one fixed matrix) with the two NCCL exchanges of
+distributed.py.  Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier +
+synchronize; each step is timed with CUDA events on the launch stream and the L2 is flushed
+(256 MiB write) between steps outside the events; max over ranks.
+
+Extra JSON keys: roofline (dominant kernel, live CUDA-event
+timing via the library's profiling hook), cpu_baseline (the fp64 oracle on host cores, bounded
+sample), e2e (host buffers through asot_distance_matrix_host), clocks, gpu_launches.
+`--impl reference` times the oracle itself (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+TF32_OVER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense tf32 / bf16
+FP32_ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max SM clock
+
+
+def baseline_metric() -> str:
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        return json.load(f)["metric"]
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["_source"] = "measured"
+        return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "_source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def pairs_of(n: int) -> int:
+    return n * (n - 1) // 2
+
+
+# ------------------------------------------------------------------------------ oracle legs
+def oracle_sample_rate(inp, budget_s: float, seed: int = 0):
+    """The oracle (as it stands) on a bounded sample of the same workload: full mapping of every
+    point, then Sinkhorn on seeded random pairs until the time budget.  Returns whole-job pairs/s
+    extrapolated as P / (t_map + P / pair_rate), and a description."""
+    from asot_inputs import random_pairs
+    from oracle import asot_oracle as O
+
+    t0 = time.perf_counter()
+    _, H = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
+    t_map = time.perf_counter() - t0
+    pi, pj = random_pairs(inp.n_dist, 200000, seed=seed)
+    done, t_pairs, batch = 0, 0.0, 256
+    while t_pairs < budget_s and done < len(pi):
+        s = time.perf_counter()
+        O.pair_costs(H, inp.cost, inp.eps, inp.iters, pi[done:done + batch].astype(np.int64),
+                     pj[done:done + batch].astype(np.int64), batch=batch)
+        t_pairs += time.perf_counter() - s
+        done += batch
+    rate = done / t_pairs
+    P = inp.n_pairs
+    value = P / (t_map + P / rate)
+    sample = (f"fp64 oracle: mapping of all {inp.n_points} points ({t_map:.2f} s) + Sinkhorn on "
+              f"{done} seeded random pairs ({t_pairs:.2f} s, {rate:.0f} pairs/s); whole-job "
+              f"throughput extrapolated to all {P} pairs")
+    return value, sample
+
+
+def run_reference(args, inp, rank, world):
+    """--impl reference: the oracle as it stands, each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    from asot_inputs import random_pairs
+    from oracle import asot_oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    n_sample = args.ref_pairs
+
+    def ref_step(k):
+        pi, pj = random_pairs(inp.n_dist, n_sample, seed=1000 + k)
+        dists = np.unique(np.concatenate([pi, pj]))
+        # map + histogram the distributions the sample touches, then Sinkhorn on the sample
+        H = np.zeros((inp.n_dist, inp.n_anchors))
+        for d in dists:
+            s, e = inp.offsets[d], inp.offsets[d + 1]
+            _, h = O.map_and_histogram(inp.points[s:e], np.array([0, e - s]), inp.weights[s:e],
+                                       inp.anchors)
+            H[d] = h[0]
+        O.pair_costs(H, inp.cost, inp.eps, inp.iters, pi.astype(np.int64), pj.astype(np.int64))
+
+    for k in range(args.warmup):
+        ref_step(-1 - k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        ref_step(k)
+    dt = time.perf_counter() - t0
+    value = n_sample * args.steps / dt
+    sample = (f"per step: {n_sample} seeded random pairs of {inp.name} (mapping of the touched "
+              f"distributions + fp64 Sinkhorn, L={inp.iters})")
+    line = {
+        "impl": "reference", "metric": baseline_metric(), "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(inp, args, world),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(inp, args, world):
+    return {
+        "workload": f"{inp.name} (BASELINE.json configs[{int(inp.name[1]) - 1}]): N={inp.n_dist} "
+                    f"distributions, K={inp.n_anchors} anchors, d={inp.dim}, L={inp.iters}, "
+                    f"eps={float(inp.eps)}",
+        "n_dist": inp.n_dist, "n_points": inp.n_points, "dim": inp.dim,
+        "n_anchors": inp.n_anchors, "iters": inp.iters, "pairs": inp.n_pairs,
+        "precision": args.precision, "l2_flush": "256 MiB write between timed steps",
+        "parallelism": f"pair-tiles x{world}",
+    }
+
+
+# ------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-pairs", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from asot_inputs import make_inputs
+
+    inp = make_inputs(args.config)
+    if args.impl == "reference":
+        run_reference(args, inp, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_16123_b200 as asot
+    from paper_2310_16123_b200 import distributed as D_
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    prec = asot.TF32 if args.precision == "tf32" else asot.FP32
+    eff = asot.effective_precision(inp.n_anchors, prec)
+
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    pts, offs, w, anc, cst = t(inp.points), t(inp.offsets), t(inp.weights), t(inp.anchors), t(inp.cost)
+    cmax = float(inp.cost.max())
+    status = asot.asot.new_status(dev)
+    ws = asot.Workspace(dev)
+    Dbuf = torch.empty((inp.n_dist, inp.n_dist), dtype=torch.float32, device=dev)
+    n_tiles = asot.num_tiles(inp.n_dist)
+    launches = [0]
+
+    if world == 1:
+        def step():
+            asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                                 out=Dbuf, offsets_host=inp.offsets, cost_max=cmax, status=status,
+                                 workspace=ws)
+            launches[0] += asot.last_launch_count()
+            return Dbuf
+    else:
+        steps_impl = D_.cuda_steps(pts, offs, inp.offsets, w, anc, cst, float(inp.eps), inp.iters,
+                                   prec, cmax, status, workspace=ws)
+
+        def counted(fn):
+            def inner(*a):
+                r = fn(*a)
+                launches[0] += asot.last_launch_count()
+                return r
+            return inner
+
+        steps_impl = D_.DistSteps(counted(steps_impl.map_range), counted(steps_impl.tiles),
+                                  counted(steps_impl.unpack), counted(steps_impl.zero_diag))
+
+        def step():
+            return D_.distance_matrix_distributed(inp.n_dist, inp.n_anchors, inp.offsets, n_tiles,
+                                                  steps_impl, device=dev)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    asot.check_status(status)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    asot.asot.profile_enable(True)
+    asot.asot.profile_read(reset=True)
+    launches[0] = 0
+    clocks = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.2)
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        Dres = step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    asot.asot.profile_enable(False)
+    kern_ms, kern_n = asot.asot.profile_read(reset=True)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = sum(step_ms)
+    gpu_launches = launches[0]
+    if world > 1:
+        tt = torch.tensor([tot_ms, kern_ms / max(kern_n, 1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot_ms, kern_avg_ms = float(tt[0]), float(tt[1])
+        gl = torch.tensor([gpu_launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(gl)
+        gpu_launches = int(gl.item())
+    else:
+        kern_avg_ms = kern_ms / max(kern_n, 1)
+    asot.check_status(status)
+    if rank == 0:
+        Dh = Dres
+        assert torch.isfinite(Dh).all() and torch.equal(Dh, Dh.T) and torch.all(torch.diagonal(Dh) == 0)
+
+    P = inp.n_pairs
+    value = P * args.steps / (tot_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (Sinkhorn, a5+a6), live CUDA-event timing
+    K, L = inp.n_anchors, inp.iters
+    flops_per_pair = 4 * K * K * L + 2 * K * K           # SURVEY §8(d) algorithmic work per pair
+    pairs_per_launch = P if world == 1 else -(-P // world)
+    peaks = measured_peaks()
+    if eff == asot.TF32:
+        peak = peaks["bf16_tflops"] * TF32_OVER_BF16
+        bound, peak_note = "tensor", (f"dense TF32 = {peaks['_source']} bf16 {peaks['bf16_tflops']} "
+                                      f"TFLOP/s (burst) x nominal tf32/bf16 1.1/2.25")
+    else:
+        peak = FP32_ALU_PEAK_TFLOPS
+        bound, peak_note = "alu", "FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz"
+    achieved = flops_per_pair * pairs_per_launch / (kern_avg_ms / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{inp.name}:{args.precision}")
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "sinkhorn_tc_kernel" if eff == asot.TF32
+                else "sinkhorn_simt_kernel", "kernel_ms_per_launch": kern_avg_ms,
+                "kernel_share_of_step": kern_avg_ms * kern_n / max(tot_ms, 1e-9) if world == 1 else None,
+                "flops_per_pair": flops_per_pair, "pairs_per_launch": pairs_per_launch,
+                "peak_note": peak_note,
+                "peak_sustained_based": peaks.get("bf16_tflops_sustained", 0) * (TF32_OVER_BF16 if eff == asot.TF32 else 0) or None}
+
+    # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
+    # distributed public API with H2D / D2H inside the timed region (N > 1)
+    e2e = None
+    if world == 1:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        hp, ho, hw, ha, hc = pin(inp.points), pin(inp.offsets), pin(inp.weights), pin(inp.anchors), pin(inp.cost)
+        hD = torch.empty((inp.n_dist, inp.n_dist), dtype=torch.float32).pin_memory().numpy()
+        wsh = asot.Workspace(dev)
+        asot.distance_matrix_host(hp, ho, hw, ha, hc, float(inp.eps), inp.iters, precision=prec,
+                                  out=hD, workspace=wsh)
+        torch.cuda.synchronize()
+        e_ms = []
+        for _ in range(args.e2e_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, st = asot.distance_matrix_host(hp, ho, hw, ha, hc, float(inp.eps), inp.iters,
+                                              precision=prec, out=hD, workspace=wsh)
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+            assert st == 0
+        h2d = hp.nbytes + ho.nbytes + hw.nbytes + ha.nbytes + hc.nbytes
+        d2h = hD.nbytes + 4
+        e2e = {"value": P * len(e_ms) / (sum(e_ms) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "asot_distance_matrix_host (pinned host buffers, wall clock)"}
+    else:
+        hp = torch.from_numpy(inp.points).pin_memory()
+        hw_ = torch.from_numpy(inp.weights).pin_memory()
+        ha = torch.from_numpy(inp.anchors).pin_memory()
+        hc = torch.from_numpy(inp.cost).pin_memory()
+        ho = torch.from_numpy(inp.offsets).pin_memory()
+        e_ms = []
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pts.copy_(hp, non_blocking=True); w.copy_(hw_, non_blocking=True)
+            anc.copy_(ha, non_blocking=True); cst.copy_(hc, non_blocking=True)
+            offs.copy_(ho, non_blocking=True)
+            Dr = step()
+            if rank == 0:
+                Dr.cpu()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+        tt = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        h2d = (hp.numel() * 4 + hw_.numel() * 4 + ha.numel() * 4 + hc.numel() * 4 + ho.numel() * 8) * world
+        e2e = {"value": P * len(e_ms) / (float(tt[0]) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(inp.n_dist ** 2 * 4),
+               "api": "paper_2310_16123_b200.distributed (pinned host copies + D to host on rank 0)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample = oracle_sample_rate(inp, args.cpu_budget)
+        cpu = {"value": v, "unit": "pairs/s", "cores": len(os.sched_getaffinity(0)),
+               "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": baseline_metric(), "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "tf32" if eff == asot.TF32 else "f32", "data": "synthetic",
+            "config": workload_config(inp, args, world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": gpu_launches, "clocks": clk,
+            "wall_s_timed_region": wall,
+            "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -155,6 +155,13 @@ asot_status asot_tile_pairs_host(int64_t n_dist, int64_t tile_begin, int64_t til
 /* Precision actually used for a given K and request (TF32 needs K <= 128 in this build). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
 
+/* Optional timing of the dominant kernel (bench.py's roofline): while enabled on this thread,
+ * the library records a CUDA event pair on the launch stream immediately around every Sinkhorn
+ * kernel launch.  asot_profile_read synchronises on the recorded events and returns the summed
+ * kernel milliseconds and launch count since the last reset.  Host-side only; never on by default. */
+asot_status asot_profile_enable(int32_t on);
+asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset);
+
 /* Number of kernel launches the last distance_matrix / pairwise call on this thread issued. */
 int32_t asot_last_launch_count(void);
 

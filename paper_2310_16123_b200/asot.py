@@ -80,6 +80,19 @@ def last_launch_count() -> int:
     return int(_lib_handle().asot_last_launch_count())
 
 
+def profile_enable(on: bool = True) -> None:
+    """Time every Sinkhorn kernel launch with CUDA events on its launch stream (this thread)."""
+    _check(_lib_handle().asot_profile_enable(int(bool(on))))
+
+
+def profile_read(reset: bool = True) -> tuple[float, int]:
+    """(summed Sinkhorn-kernel milliseconds, launches) since the last reset."""
+    ms = ctypes.c_double(0.0)
+    n = ctypes.c_int64(0)
+    _check(_lib_handle().asot_profile_read(ctypes.byref(ms), ctypes.byref(n), int(bool(reset))))
+    return float(ms.value), int(n.value)
+
+
 def new_status(device=None) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device or "cuda")
 

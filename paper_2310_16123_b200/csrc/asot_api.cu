@@ -3,6 +3,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "asot_internal.cuh"
 
@@ -89,12 +91,39 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, bool tc) {
   return b;
 }
 
+// Profiling of the dominant kernel (asot_profile_*): event pairs recorded around each launch.
+thread_local bool g_prof_on = false;
+thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+thread_local size_t g_prof_used = 0;
+
+std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
+  if (g_prof_used == g_prof_events.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    g_prof_events.emplace_back(a, b);
+  }
+  return g_prof_events[g_prof_used++];
+}
+
 asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink, const float* H,
                          const float* cost, float eps, int32_t K, int32_t iters, bool tc,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
                          cudaStream_t s) {
   ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
                                       tc ? asot::kpad32(K) : K, s));
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (g_prof_on) {
+    ev = prof_pair();
+    ASOT_CUDA(cudaEventRecord(ev.first, s));
+  }
+  struct Rec {
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    cudaStream_t s;
+    ~Rec() {
+      if (ev.second) cudaEventRecord(ev.second, s);
+    }
+  } rec{ev, s};
   if (tc) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                          gb.gc_img, iters, s));
@@ -111,6 +140,26 @@ extern "C" {
 int32_t asot_abi_version(void) { return ASOT_ABI_VERSION; }
 const char* asot_last_error(void) { return g_last_error.c_str(); }
 int32_t asot_last_launch_count(void) { return g_launches; }
+
+asot_status asot_profile_enable(int32_t on) {
+  g_prof_on = on != 0;
+  return ASOT_OK;
+}
+
+asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset) {
+  ASOT_CHECK_ARG(sinkhorn_ms && launches, "null pointer argument");
+  double total = 0.0;
+  for (size_t k = 0; k < g_prof_used; ++k) {
+    ASOT_CUDA(cudaEventSynchronize(g_prof_events[k].second));
+    float ms = 0.0f;
+    ASOT_CUDA(cudaEventElapsedTime(&ms, g_prof_events[k].first, g_prof_events[k].second));
+    total += ms;
+  }
+  *sinkhorn_ms = total;
+  *launches = (int64_t)g_prof_used;
+  if (reset) g_prof_used = 0;
+  return ASOT_OK;
+}
 int64_t asot_num_tiles(int64_t n_dist) { return n_dist < 1 ? 0 : asot::num_tiles(n_dist); }
 
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
