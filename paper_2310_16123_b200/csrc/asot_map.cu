@@ -41,9 +41,12 @@ __global__ void gibbs_prep_kernel(const float* __restrict__ cost, int K, float e
       GC[(int64_t)n * K + k] = gc32;
     }
     if (g_img != nullptr) {
+      // Padding (K < kpad) for the tensor-core path: K entries outside the real K x K block are
+      // 1 so every denominator (K v)_r stays > 0 (padded scalings are exactly 0, so the real
+      // block is untouched); K (.) C_s padding is 0 so the cost is untouched.
       const uint32_t off = sw128_kmajor_offset((uint32_t)n, (uint32_t)k, (uint32_t)kpad) >> 2;
-      g_img[off] = tf32_rna_bits(g32);
-      gc_img[off] = tf32_rna_bits(gc32);
+      g_img[off] = in ? tf32_rna_bits(g32) : 0x3f800000u;
+      gc_img[off] = in ? tf32_rna_bits(gc32) : 0u;
     }
   }
 }

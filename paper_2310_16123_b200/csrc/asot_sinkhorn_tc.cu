@@ -14,11 +14,11 @@
 // Warp roles (256 threads): warps 0-3 (slot 0) and 4-7 (slot 1) are two warpgroups, each owning
 // one pair tile; after a warpgroup barrier one elected thread issues that slot's tcgen05.mma
 // chain and commits it to the slot's mbarrier.  While the tensor core computes one slot's
-// product, the other warpgroup turns its own accumulator into the next scaling (tcgen05.ld -> u = a * rcp(max(D, FLT_MIN)) -> cvt.rna.tf32
-// -> tcgen05.st), so MMA and the elementwise divide overlap (ping-pong).  Each thread owns one
+// product, the other warpgroup turns its own accumulator into the next scaling (tcgen05.ld -> u = a / D with one MUFU.RCP per
+// two anchors -> RNA rounding to TF32 -> tcgen05.st), so MMA and the elementwise divide overlap (ping-pong).  Each thread owns one
 // pair (its TMEM lane) and all K anchors, so the final cost reduction needs no cross-thread sum:
-// the last v-update keeps v (fp32) in registers, the cost phase multiplies by K (.) C_s applied
-// to u (TMEM) and reduces in-thread.
+// the last v-update writes v_L in place into D, two N = K/2 MMAs apply K (.) C_s to it (output
+// into the consumed half of A), and each thread reduces sum_r u_r ((K (.) C_s) v)_r in-thread.
 //
 // TMEM map (columns): slot s: A at 2s*KP, D at 2s*KP + KP.  SMEM: [K image | KC image |
 // marginal rows (8 a-rows, 16 b-rows, 1 zero row) per slot | mbarriers].
@@ -146,8 +146,33 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Round-to-nearest, ties away (RNA) to TF32 for finite inputs, as two integer ops
+// (same result as cvt.rna.tf32.f32, which ptxas expands into a longer guarded sequence).
+__device__ __forceinline__ uint32_t tf32_rna_fast(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+}
+
+__device__ __forceinline__ void lds128(uint32_t saddr, float* v) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+               : "r"(saddr));
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
@@ -177,9 +202,12 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   constexpr uint32_t kTmemCols = (4 * KP <= 32) ? 32 : (4 * KP <= 64) ? 64 : (4 * KP <= 128) ? 128
                                : (4 * KP <= 256) ? 256 : 512;
   constexpr uint32_t kIdesc = make_idesc_tf32(128, KP);
+  constexpr uint32_t kIdescHalf = make_idesc_tf32(128, KP / 2);
   constexpr int kWG = kEpiWarps * 32;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned base derived from smem_raw by pointer arithmetic, so the compiler keeps
+  // the shared address space (LDS, not generic loads) for everything carved from it
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* marg = (float*)(smem + S::kOffMarg);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
   uint32_t* tmem_holder = (uint32_t*)(bars + 6);
@@ -229,10 +257,12 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   const uint32_t g_base = smem_u32(smem + S::kOffG), gc_base = smem_u32(smem + S::kOffGC);
   uint32_t mma_par = 0;
   bool g_ready = false;
-  float stash[KP];
 
-  // Warpgroup barrier, then one elected thread issues D = A (.) B for this slot and commits.
-  auto issue_phase = [&](bool cost_phase) {
+  // Warpgroup barrier, then one elected thread issues this slot's MMA chain and commits it.
+  //   mode 0:    D = A K                  (N = KP; A = V^T or U^T in TMEM, K in SMEM)
+  //   mode 1, 2: A[:, 0:KP/2] = D (K (.) C_s)[:, half]   (N = KP/2; D holds v_L^T as the
+  //              A operand, the output overwrites the half of u_L already consumed)
+  auto issue_mma = [&](int mode) {
     tc_fence_before();
     named_bar_sync(1 + s, kWG);
     if (wg_tid == 0) {
@@ -242,14 +272,27 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
       }
       tc_fence_after();
       const uint32_t a0 = tmem_base + a_col, d0 = tmem_base + a_col + KP;
-      const uint32_t b_base = cost_phase ? gc_base : g_base;
+      if (mode == 0) {
 #pragma unroll
-      for (int ks = 0; ks < KP / 8; ++ks) {
-        const uint32_t b_addr = b_base + (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32);
-        mma_tf32_ts(d0, a0 + 8 * ks, make_sw128_desc(b_addr), kIdesc, ks > 0 ? 1u : 0u);
+        for (int ks = 0; ks < KP / 8; ++ks) {
+          const uint32_t b_addr = g_base + (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32);
+          mma_tf32_ts(d0, a0 + 8 * ks, make_sw128_desc(b_addr), kIdesc, ks > 0 ? 1u : 0u);
+        }
+      } else {
+        const uint32_t row0 = (uint32_t)((mode - 1) * (KP / 2) * 128);
+#pragma unroll
+        for (int ks = 0; ks < KP / 8; ++ks) {
+          const uint32_t b_addr = gc_base + (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32) + row0;
+          mma_tf32_ts(a0, d0 + 8 * ks, make_sw128_desc(b_addr), kIdescHalf, ks > 0 ? 1u : 0u);
+        }
       }
       mma_commit(bar_mma);
     }
+  };
+  auto wait_mma = [&]() {
+    mbar_wait(bar_mma, mma_par);
+    mma_par ^= 1u;
+    tc_fence_after();
   };
 
   for (int64_t tk = s;; tk += 2) {
@@ -264,7 +307,9 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
       const int r = e / KP, c = e % KP;
       const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
-      mrows[r * S::kRS + c] = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+      float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+      if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
+      mrows[r * S::kRS + c] = v;
     }
     int ii, jj;
     const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
@@ -275,54 +320,68 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
 #pragma unroll
       for (int c = 0; c < KP / 32; ++c) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) ones[e] = (valid && c * 32 + e < K) ? 0x3f800000u : 0u;
+        for (int e = 0; e < 32; ++e) ones[e] = (c * 32 + e < K) ? 0x3f800000u : 0u;
         tmem_st32(a_tmem + c * 32, ones);
       }
     }
     tmem_wait_st();
-    issue_phase(false);  // (also publishes mrows to the warpgroup)
+    issue_mma(0);  // (its barrier also publishes mrows to the warpgroup)
 
     for (int f = 0; f < 2 * iters; ++f) {
-      mbar_wait(bar_mma, mma_par);
-      mma_par ^= 1u;
-      tc_fence_after();
+      wait_mma();
       const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
-      const bool last = f == 2 * iters - 1;
+      // u / v scalings go back to A (next MMA operand); the last v_L goes into D in place
+      const uint32_t dst = (f == 2 * iters - 1) ? d_tmem : a_tmem;
 #pragma unroll
       for (int c = 0; c < KP / 32; ++c) {
         uint32_t d[32];
         tmem_ld32(d_tmem + c * 32, d);
         tmem_wait_ld();
         uint32_t o[32];
+        const float4* m4 = reinterpret_cast<const float4*>(mrow + c * 32);
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 m4 = *reinterpret_cast<const float4*>(mrow + c * 32 + e);
-          const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float den = fmaxf(__uint_as_float(d[e + q]), FLT_MIN);
-            const float x = mv[q] * rcp_approx(den);  // 0 / x = 0 (R#11)
-            stash[c * 32 + e + q] = x;
-            o[e + q] = tf32_rna_bits(x);
-          }
+        for (int e = 0; e < 32; e += 2) {
+          const float4 mq = m4[e >> 2];
+          const float m0 = (e & 2) ? mq.z : mq.x, m1 = (e & 2) ? mq.w : mq.y;
+          // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r, m1/D1 = m1 D0 r.
+          // D > 0 by construction (padded K = 1, dummy marginals); m = 0 gives exactly 0 (R#11).
+          const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
+          const float r = rcp_approx(d0 * d1);
+          o[e] = tf32_rna_fast((m0 * d1) * r);
+          o[e + 1] = tf32_rna_fast((m1 * d0) * r);
         }
-        if (!last) tmem_st32(a_tmem + c * 32, o);
+        tmem_st32(dst + c * 32, o);
       }
-      if (!last) tmem_wait_st();
-      issue_phase(last);  // after the last v-update: D = U_L^T (K (.) C_s)
+      tmem_wait_st();
+      if (f != 2 * iters - 1) issue_mma(0);
     }
-    // ---- cost phase: d = sum_c v_c ((K (.) C_s)^T u)_c, in-thread (one pair per thread)
-    mbar_wait(bar_mma, mma_par);
-    mma_par ^= 1u;
-    tc_fence_after();
+    // ---- cost (a6): d = sum_r u_r ((K (.) C_s) v)_r with u_L in A and v_L in D, in two halves
+    // of N = KP/2 so the product can land in the already-consumed half of A.
+    float ust[KP / 2];
+#pragma unroll
+    for (int c = 0; c < KP / 32; ++c) tmem_ld16(a_tmem + 16 * c, &ust[16 * c]);
+    tmem_wait_ld();
+    issue_mma(1);
+    wait_mma();
     float acc = 0.0f;
 #pragma unroll
     for (int c = 0; c < KP / 32; ++c) {
-      uint32_t d[32];
-      tmem_ld32(d_tmem + c * 32, d);
+      float g[16];
+      tmem_ld16(a_tmem + 16 * c, g);
       tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 32; ++e) acc = fmaf(stash[c * 32 + e], __uint_as_float(d[e]), acc);
+      for (int e = 0; e < 16; ++e) acc = fmaf(ust[16 * c + e], g[e], acc);
+    }
+    issue_mma(2);
+    wait_mma();
+#pragma unroll
+    for (int c = 0; c < KP / 32; ++c) {
+      float g[16], u[16];
+      tmem_ld16(a_tmem + 16 * c, g);
+      tmem_ld16(a_tmem + KP / 2 + 16 * c, u);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc = fmaf(u[e], g[e], acc);
     }
     write_result(out, tr * kTileSlots + p, valid, ii, jj, acc);
   }
