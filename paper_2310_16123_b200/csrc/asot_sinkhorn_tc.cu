@@ -11,17 +11,20 @@
 // (K-major SWIZZLE_128B image staged once per CTA by a TMA bulk copy), and the fp32 accumulator
 // D in TMEM.  The scalings of a tile never leave the SM for all 2L+1 MMA phases.
 //
-// Warp roles (256 threads): warps 0-3 (slot 0) and 4-7 (slot 1) are two warpgroups, each owning
-// one pair tile; after a warpgroup barrier one elected thread issues that slot's tcgen05.mma
-// chain and commits it to the slot's mbarrier.  While the tensor core computes one slot's
-// product, the other warpgroup turns its own accumulator into the next scaling (tcgen05.ld -> u = a / D with one MUFU.RCP per
-// two anchors -> RNA rounding to TF32 -> tcgen05.st), so MMA and the elementwise divide overlap (ping-pong).  Each thread owns one
-// pair (its TMEM lane) and all K anchors, so the final cost reduction needs no cross-thread sum:
-// the last v-update writes v_L in place into D, two N = K/2 MMAs apply K (.) C_s to it (output
-// into the consumed half of A), and each thread reduces sum_r u_r ((K (.) C_s) v)_r in-thread.
+// Warp roles (512 threads): warps 0-7 own slot 0 and warps 8-15 slot 1 (one pair tile each);
+// warp w reads TMEM lane quarter w%4 and the column half (w%8)/4, so each SMSP runs two
+// independent instruction streams per slot.  After a slot barrier one elected thread issues
+// that slot's tcgen05.mma chain and commits it to the slot's mbarrier.  While the tensor core
+// computes one slot's product, the other slot's warps turn their accumulator into the next
+// scaling (tcgen05.ld x16, double-buffered -> u = a / D with one MUFU.RCP per two anchors ->
+// RNA rounding to TF32 -> tcgen05.st), so MMA and the elementwise divide overlap (ping-pong).
+// Each pair lives in one TMEM lane; its two column halves are reduced in-thread and summed
+// through SMEM once per tile.  The cost (a6): the last v-update writes v_L in place into D, two
+// N = K/2 MMAs apply K (.) C_s to it (output into the consumed half of A), and the threads
+// reduce sum_r u_r ((K (.) C_s) v)_r.
 //
 // TMEM map (columns): slot s: A at 2s*KP, D at 2s*KP + KP.  SMEM: [K image | KC image |
-// marginal rows (8 a-rows, 16 b-rows, 1 zero row) per slot | mbarriers].
+// marginal rows (8 a-rows, 16 b-rows, 1 dummy row) per slot | partial costs | mbarriers].
 #include <cfloat>
 
 #include "asot_internal.cuh"
@@ -29,8 +32,8 @@
 namespace asot {
 namespace tc {
 
-constexpr int kThreads = 256;
-constexpr int kEpiWarps = 4;
+constexpr int kWarpsPerSlot = 8;
+constexpr int kThreads = 2 * kWarpsPerSlot * 32;  // 512
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -159,6 +162,46 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
 }
 
+__device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[e]);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+// Ties the registers written by an asynchronous tcgen05.ld to the preceding wait::ld so the
+// compiler cannot schedule their first use above it.
+__device__ __forceinline__ void reg_fence16(uint32_t (&r)[16]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -183,16 +226,19 @@ __device__ __forceinline__ float rcp_approx(float x) {
 template <int KP>
 struct Smem {
   static constexpr int kRS = KP + 4;                      // marginal row stride (floats)
-  static constexpr int kRows = 8 + 16 + 1;                // a-rows, b-rows, zero row
+  static constexpr int kRows = 8 + 16 + 1;                // a-rows, b-rows, dummy row
   static constexpr size_t kImg = (size_t)KP * KP * 4;     // one operand image
   static constexpr size_t kMarg = (size_t)kRows * kRS * 4;
   static constexpr size_t kOffG = 0;
   static constexpr size_t kOffGC = kImg;
   static constexpr size_t kOffMarg = 2 * kImg;
-  static constexpr size_t kOffBar = kOffMarg + 2 * kMarg;
-  static constexpr size_t kBytes = kOffBar + 64 + 1024;  // + alignment slack
+  static constexpr size_t kOffRed = kOffMarg + 2 * kMarg;     // [2 slots][128] partial costs
+  static constexpr size_t kOffBar = kOffRed + 2 * 128 * 4;
+  static constexpr size_t kBytes = kOffBar + 64 + 1024;      // + alignment slack
 };
 
+// Per-thread view: thread = (slot s, TMEM lane quarter, column half h).  Columns are processed
+// in chunks of 16 with the next chunk's tcgen05.ld in flight while the current one is computed.
 template <int KP>
 __global__ void __launch_bounds__(kThreads, 1)
 sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
@@ -203,21 +249,26 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
                                : (4 * KP <= 256) ? 256 : 512;
   constexpr uint32_t kIdesc = make_idesc_tf32(128, KP);
   constexpr uint32_t kIdescHalf = make_idesc_tf32(128, KP / 2);
-  constexpr int kWG = kEpiWarps * 32;
+  constexpr int kWG = kWarpsPerSlot * 32;
+  constexpr int CW = KP / 2;    // columns per thread in the Sinkhorn phases
+  constexpr int NC = CW / 16;   // x16 chunks per phase
+  constexpr int CQ = KP / 4;    // columns per thread in each cost half
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base derived from smem_raw by pointer arithmetic, so the compiler keeps
   // the shared address space (LDS, not generic loads) for everything carved from it
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* marg = (float*)(smem + S::kOffMarg);
+  float* red = (float*)(smem + S::kOffRed);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
   uint32_t* tmem_holder = (uint32_t*)(bars + 6);
   const uint32_t bar_g = smem_u32(&bars[0]);
   const uint32_t bar_mma0 = smem_u32(&bars[1]);  // +8*s
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = warp / kEpiWarps;         // slot (pair tile) owned by this warpgroup
-  const int sub = warp & 3;               // TMEM lane quarter this warp may access
-  const int p = sub * 32 + lane;          // pair slot within the tile == TMEM lane
+  const int s = warp / kWarpsPerSlot;          // slot (pair tile) owned by this warpgroup pair
+  const int sub = warp & 3;                    // TMEM lane quarter this warp may access
+  const int h = (warp % kWarpsPerSlot) >> 2;   // column half
+  const int p = sub * 32 + lane;               // pair slot within the tile == TMEM lane
   const int wg_tid = threadIdx.x - s * kWG;
 
   if (threadIdx.x == 0) {
@@ -258,7 +309,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   uint32_t mma_par = 0;
   bool g_ready = false;
 
-  // Warpgroup barrier, then one elected thread issues this slot's MMA chain and commits it.
+  // Slot barrier, then one elected thread issues this slot's MMA chain and commits it.
   //   mode 0:    D = A K                  (N = KP; A = V^T or U^T in TMEM, K in SMEM)
   //   mode 1, 2: A[:, 0:KP/2] = D (K (.) C_s)[:, half]   (N = KP/2; D holds v_L^T as the
   //              A operand, the output overwrites the half of u_L already consumed)
@@ -303,7 +354,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     int64_t bi, bj;
     block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
     const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
-    named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows
+    named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows / red
     for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
       const int r = e / KP, c = e % KP;
       const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
@@ -313,77 +364,87 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     }
     int ii, jj;
     const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
-    const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS;
-    const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS;
-    {
-      uint32_t ones[32];
+    const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS + h * CW;
+    const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS + h * CW;
 #pragma unroll
-      for (int c = 0; c < KP / 32; ++c) {
+    for (int c = 0; c < NC; ++c) {
+      uint32_t ones[16];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) ones[e] = (c * 32 + e < K) ? 0x3f800000u : 0u;
-        tmem_st32(a_tmem + c * 32, ones);
-      }
+      for (int e = 0; e < 16; ++e) ones[e] = (h * CW + c * 16 + e < K) ? 0x3f800000u : 0u;
+      tmem_st16(a_tmem + h * CW + c * 16, ones);
     }
     tmem_wait_st();
-    issue_mma(0);  // (its barrier also publishes mrows to the warpgroup)
+    issue_mma(0);  // (its barrier also publishes mrows to the slot's warps)
 
     for (int f = 0; f < 2 * iters; ++f) {
       wait_mma();
       const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
       // u / v scalings go back to A (next MMA operand); the last v_L goes into D in place
-      const uint32_t dst = (f == 2 * iters - 1) ? d_tmem : a_tmem;
+      const uint32_t dst = ((f == 2 * iters - 1) ? d_tmem : a_tmem) + h * CW;
+      const uint32_t src = d_tmem + h * CW;
+      uint32_t d[2][16];
+      tmem_ld16u(src, d[0]);
+      tmem_wait_ld();
+      reg_fence16(d[0]);
 #pragma unroll
-      for (int c = 0; c < KP / 32; ++c) {
-        uint32_t d[32];
-        tmem_ld32(d_tmem + c * 32, d);
-        tmem_wait_ld();
-        uint32_t o[32];
-        const float4* m4 = reinterpret_cast<const float4*>(mrow + c * 32);
+      for (int c = 0; c < NC; ++c) {
+        if (c + 1 < NC) tmem_ld16u(src + (c + 1) * 16, d[(c + 1) & 1]);
+        const uint32_t* dc = d[c & 1];
+        uint32_t o[16];
+        const float4* m4 = reinterpret_cast<const float4*>(mrow + c * 16);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
+        for (int e = 0; e < 16; e += 2) {
           const float4 mq = m4[e >> 2];
           const float m0 = (e & 2) ? mq.z : mq.x, m1 = (e & 2) ? mq.w : mq.y;
           // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r, m1/D1 = m1 D0 r.
           // D > 0 by construction (padded K = 1, dummy marginals); m = 0 gives exactly 0 (R#11).
-          const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
+          const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
           const float r = rcp_approx(d0 * d1);
           o[e] = tf32_rna_fast((m0 * d1) * r);
           o[e + 1] = tf32_rna_fast((m1 * d0) * r);
         }
-        tmem_st32(dst + c * 32, o);
+        tmem_st16(dst + c * 16, o);
+        if (c + 1 < NC) {
+          tmem_wait_ld();
+          reg_fence16(d[(c + 1) & 1]);
+        }
       }
       tmem_wait_st();
       if (f != 2 * iters - 1) issue_mma(0);
     }
     // ---- cost (a6): d = sum_r u_r ((K (.) C_s) v)_r with u_L in A and v_L in D, in two halves
-    // of N = KP/2 so the product can land in the already-consumed half of A.
-    float ust[KP / 2];
+    // of N = KP/2 so the product can land in the already-consumed half of A.  Thread half h
+    // covers columns [h KP/4, (h+1) KP/4) of each half; the two partials meet in SMEM.
+    float ust[CQ];
 #pragma unroll
-    for (int c = 0; c < KP / 32; ++c) tmem_ld16(a_tmem + 16 * c, &ust[16 * c]);
+    for (int c = 0; c < CQ / 8; ++c) tmem_ld8(a_tmem + h * CQ + 8 * c, &ust[8 * c]);
     tmem_wait_ld();
     issue_mma(1);
     wait_mma();
     float acc = 0.0f;
 #pragma unroll
-    for (int c = 0; c < KP / 32; ++c) {
-      float g[16];
-      tmem_ld16(a_tmem + 16 * c, g);
+    for (int c = 0; c < CQ / 8; ++c) {
+      float g[8];
+      tmem_ld8(a_tmem + h * CQ + 8 * c, g);
       tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc = fmaf(ust[16 * c + e], g[e], acc);
+      for (int e = 0; e < 8; ++e) acc = fmaf(ust[8 * c + e], g[e], acc);
     }
     issue_mma(2);
     wait_mma();
 #pragma unroll
-    for (int c = 0; c < KP / 32; ++c) {
-      float g[16], u[16];
-      tmem_ld16(a_tmem + 16 * c, g);
-      tmem_ld16(a_tmem + KP / 2 + 16 * c, u);
+    for (int c = 0; c < CQ / 8; ++c) {
+      float g[8], u[8];
+      tmem_ld8(a_tmem + h * CQ + 8 * c, g);
+      tmem_ld8(a_tmem + KP / 2 + h * CQ + 8 * c, u);
       tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc = fmaf(u[e], g[e], acc);
+      for (int e = 0; e < 8; ++e) acc = fmaf(u[e], g[e], acc);
     }
-    write_result(out, tr * kTileSlots + p, valid, ii, jj, acc);
+    float* rs = red + s * 128;
+    if (h == 1) rs[p] = acc;
+    named_bar_sync(1 + s, kWG);
+    if (h == 0) write_result(out, tr * kTileSlots + p, valid, ii, jj, acc + rs[p]);
   }
   tc_fence_before();
   __syncthreads();
