@@ -26,11 +26,15 @@
 // TMEM map (columns): slot s: A at 2s*KP, D at 2s*KP + KP.  SMEM: [K image | KC image |
 // marginal rows (8 a-rows, 16 b-rows, 1 dummy row) per slot | partial costs | mbarriers].
 #include <cfloat>
+#include <cstdlib>
 
 #include "asot_internal.cuh"
 
 namespace asot {
 namespace tc {
+
+// Debug timeline (ASOT_TC_DEBUG_MODE=3): slot, event, phase -> clock64 for CTA 0's first tile.
+__device__ long long g_tc_trace[2][4][512];
 
 constexpr int kWarpsPerSlot = 8;
 constexpr int kThreads = 2 * kWarpsPerSlot * 32;  // 512
@@ -74,6 +78,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
+}
+
+// One lane of a converged warp (elect.sync); the rest of the warp skips the guarded block.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, %1;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -223,6 +239,26 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
+// One slot's MMA chain with compile-time TMEM addresses (TMEM base is 0) and descriptors formed
+// from the uniform SMEM base plus constant offsets.
+//   MODE 0:    D_S = A_S (x) B          (N = KP, B = K image)
+//   MODE 1, 2: A_S[:, 0:KP/2] = D_S (x) B[rows (MODE-1)*KP/2 ...]   (N = KP/2, B = K (.) C_s)
+template <int KP, int S, int MODE>
+__device__ __forceinline__ void issue_chain(uint32_t b_base) {
+  constexpr uint32_t a0 = 2u * S * KP, d0 = a0 + KP;
+  constexpr uint32_t idesc = make_idesc_tf32(128, MODE == 0 ? KP : KP / 2);
+  constexpr uint32_t row0 = MODE == 0 ? 0u : (uint32_t)((MODE - 1) * (KP / 2) * 128);
+  const uint64_t desc0 = make_sw128_desc(b_base + row0);
+#pragma unroll
+  for (int ks = 0; ks < KP / 8; ++ks) {
+    const uint64_t desc = desc0 + (uint64_t)(((ks >> 2) * KP * 128 + (ks & 3) * 32) >> 4);
+    if (MODE == 0)
+      mma_tf32_ts(d0, a0 + 8 * ks, desc, idesc, ks > 0 ? 1u : 0u);
+    else
+      mma_tf32_ts(a0, d0 + 8 * ks, desc, idesc, ks > 0 ? 1u : 0u);
+  }
+}
+
 template <int KP>
 struct Smem {
   static constexpr int kRS = KP + 4;                      // marginal row stride (floats)
@@ -239,14 +275,16 @@ struct Smem {
 
 // Per-thread view: thread = (slot s, TMEM lane quarter, column half h).  Columns are processed
 // in chunks of 16 with the next chunk's tcgen05.ld in flight while the current one is computed.
-template <int KP>
+template <int KP, int DBG>
 __global__ void __launch_bounds__(kThreads, 1)
 sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                    const float* __restrict__ H, int K, const uint32_t* __restrict__ g_img,
                    const uint32_t* __restrict__ gc_img, int iters) {
   using S = Smem<KP>;
-  constexpr uint32_t kTmemCols = (4 * KP <= 32) ? 32 : (4 * KP <= 64) ? 64 : (4 * KP <= 128) ? 128
-                               : (4 * KP <= 256) ? 256 : 512;
+  // All 512 columns: the allocation then necessarily starts at column 0 (one CTA per SM), so
+  // every TMEM address below is a compile-time constant per slot and the MMA operands live in
+  // uniform registers (no per-instruction R2UR / ELECT loops in the issue path).
+  constexpr uint32_t kTmemCols = 512;
   constexpr uint32_t kIdesc = make_idesc_tf32(128, KP);
   constexpr uint32_t kIdescHalf = make_idesc_tf32(128, KP / 2);
   constexpr int kWG = kWarpsPerSlot * 32;
@@ -261,6 +299,11 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   float* red = (float*)(smem + S::kOffRed);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
   uint32_t* tmem_holder = (uint32_t*)(bars + 6);
+  // Tensor-pipe turn token: the two slots issue their MMA chains strictly alternately, so one
+  // slot's chain finishes while the other's is still queued and the epilogues interleave with
+  // MMAs instead of both slots running in lockstep (issue blocks for about the chain's duration).
+  volatile int* turn = (volatile int*)(bars + 7);
+  volatile int* slot_done = turn + 1;  // [2]
   const uint32_t bar_g = smem_u32(&bars[0]);
   const uint32_t bar_mma0 = smem_u32(&bars[1]);  // +8*s
 
@@ -272,6 +315,9 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   const int wg_tid = threadIdx.x - s * kWG;
 
   if (threadIdx.x == 0) {
+    turn[0] = 0;
+    slot_done[0] = 0;
+    slot_done[1] = 0;
     mbar_init(bar_g, 1);
     mbar_init(bar_mma0, 1);
     mbar_init(bar_mma0 + 8, 1);
@@ -289,6 +335,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (tmem_base != 0) __trap();  // cannot happen with a full 512-column allocation
   if (threadIdx.x == 0) {  // stage K and K (.) C_s once per CTA (TMA bulk copies)
     mbar_expect_tx(bar_g, (uint32_t)(2 * S::kImg));
     constexpr uint32_t kChunk = 32768;
@@ -313,31 +360,35 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   //   mode 0:    D = A K                  (N = KP; A = V^T or U^T in TMEM, K in SMEM)
   //   mode 1, 2: A[:, 0:KP/2] = D (K (.) C_s)[:, half]   (N = KP/2; D holds v_L^T as the
   //              A operand, the output overwrites the half of u_L already consumed)
-  auto issue_mma = [&](int mode) {
+  auto issue_mma = [&](int mode, int fdbg) {
     tc_fence_before();
     named_bar_sync(1 + s, kWG);
-    if (wg_tid == 0) {
+    if (wg_tid < 32) {  // the slot's first warp, converged: one elected lane issues
+      if (DBG == 3 && blockIdx.x == 0 && fdbg >= 0 && fdbg < 512 && lane == 0) g_tc_trace[s][3][fdbg] = clock64();
       if (!g_ready) {
         mbar_wait(bar_g, 0);
         g_ready = true;
       }
+      while (*turn != s && !slot_done[s ^ 1]) __nanosleep(32);
+      __syncwarp();
+      if (DBG == 3 && blockIdx.x == 0 && fdbg >= 0 && fdbg < 512 && lane == 0) g_tc_trace[s][1][fdbg] = clock64();
       tc_fence_after();
-      const uint32_t a0 = tmem_base + a_col, d0 = tmem_base + a_col + KP;
-      if (mode == 0) {
-#pragma unroll
-        for (int ks = 0; ks < KP / 8; ++ks) {
-          const uint32_t b_addr = g_base + (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32);
-          mma_tf32_ts(d0, a0 + 8 * ks, make_sw128_desc(b_addr), kIdesc, ks > 0 ? 1u : 0u);
+      if (elect_one()) {
+        if (DBG != 2) {
+          if (s == 0) {
+            if (mode == 0) issue_chain<KP, 0, 0>(g_base);
+            else if (mode == 1) issue_chain<KP, 0, 1>(gc_base);
+            else issue_chain<KP, 0, 2>(gc_base);
+          } else {
+            if (mode == 0) issue_chain<KP, 1, 0>(g_base);
+            else if (mode == 1) issue_chain<KP, 1, 1>(gc_base);
+            else issue_chain<KP, 1, 2>(gc_base);
+          }
         }
-      } else {
-        const uint32_t row0 = (uint32_t)((mode - 1) * (KP / 2) * 128);
-#pragma unroll
-        for (int ks = 0; ks < KP / 8; ++ks) {
-          const uint32_t b_addr = gc_base + (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32) + row0;
-          mma_tf32_ts(a0, d0 + 8 * ks, make_sw128_desc(b_addr), kIdescHalf, ks > 0 ? 1u : 0u);
-        }
+        mma_commit(bar_mma);
+        *turn = s ^ 1;
       }
-      mma_commit(bar_mma);
+      __syncwarp();
     }
   };
   auto wait_mma = [&]() {
@@ -348,7 +399,13 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
 
   for (int64_t tk = s;; tk += 2) {
     const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
-    if (tr >= n_tiles) break;
+    if (tr >= n_tiles) {
+      if (wg_tid == 0) {
+        slot_done[s] = 1;
+        *turn = s ^ 1;
+      }
+      break;
+    }
     const int64_t t = tile_begin + tr;
     // ---- tile init: marginal rows -> SMEM, V^T = 1 -> TMEM (A operand)
     int64_t bi, bj;
@@ -374,14 +431,19 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
       tmem_st16(a_tmem + h * CW + c * 16, ones);
     }
     tmem_wait_st();
-    issue_mma(0);  // (its barrier also publishes mrows to the slot's warps)
+    issue_mma(0, -1);  // (its barrier also publishes mrows to the slot's warps)
 
     for (int f = 0; f < 2 * iters; ++f) {
       wait_mma();
+      if (DBG == 3 && blockIdx.x == 0 && tk < 2 && wg_tid == 0 && f < 512) g_tc_trace[s][0][f] = clock64();
       const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
       // u / v scalings go back to A (next MMA operand); the last v_L goes into D in place
       const uint32_t dst = ((f == 2 * iters - 1) ? d_tmem : a_tmem) + h * CW;
       const uint32_t src = d_tmem + h * CW;
+      if (DBG == 1) {
+        if (f != 2 * iters - 1) issue_mma(0, -1);
+        continue;
+      }
       uint32_t d[2][16];
       tmem_ld16u(src, d[0]);
       tmem_wait_ld();
@@ -410,7 +472,8 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
         }
       }
       tmem_wait_st();
-      if (f != 2 * iters - 1) issue_mma(0);
+      if (f != 2 * iters - 1) issue_mma(0, (DBG == 3 && tk < 2) ? f : -1);
+      if (DBG == 3 && blockIdx.x == 0 && tk < 2 && wg_tid == 0 && f < 512) g_tc_trace[s][2][f] = clock64();
     }
     // ---- cost (a6): d = sum_r u_r ((K (.) C_s) v)_r with u_L in A and v_L in D, in two halves
     // of N = KP/2 so the product can land in the already-consumed half of A.  Thread half h
@@ -419,7 +482,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
 #pragma unroll
     for (int c = 0; c < CQ / 8; ++c) tmem_ld8(a_tmem + h * CQ + 8 * c, &ust[8 * c]);
     tmem_wait_ld();
-    issue_mma(1);
+    issue_mma(1, -1);
     wait_mma();
     float acc = 0.0f;
 #pragma unroll
@@ -430,7 +493,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc = fmaf(ust[8 * c + e], g[e], acc);
     }
-    issue_mma(2);
+    issue_mma(2, -1);
     wait_mma();
 #pragma unroll
     for (int c = 0; c < CQ / 8; ++c) {
@@ -461,7 +524,10 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
                              const float* H, int K, const uint32_t* g_img, const uint32_t* gc_img,
                              int iters, cudaStream_t s) {
   const size_t smem = Smem<KP>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(sinkhorn_tc_kernel<KP>,
+  static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
+  auto kern = dbg == 1 ? sinkhorn_tc_kernel<KP, 1> : dbg == 2 ? sinkhorn_tc_kernel<KP, 2>
+            : dbg == 3 ? sinkhorn_tc_kernel<KP, 3> : sinkhorn_tc_kernel<KP, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -470,7 +536,7 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   int64_t grid = (n_tiles + 1) / 2;
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
-  sinkhorn_tc_kernel<KP><<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+  kern<<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
                                                                g_img, gc_img, iters);
   return cudaGetLastError();
 }
@@ -494,3 +560,7 @@ cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_d
 }
 
 }  // namespace asot
+
+extern "C" int asot_debug_tc_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, asot::tc::g_tc_trace, sizeof(asot::tc::g_tc_trace));
+}
