@@ -1,0 +1,95 @@
+"""Summarise ncu artefacts into profiles/ (run here, on the CPU box, after a gpurun call).
+
+  python tools/summarize_ncu.py launches <launches.csv> <out.md>
+  python tools/summarize_ncu.py full <prof.ncu-rep> <out.json> [traffic-key]
+"""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__issue_active.avg.pct_of_peak_sustained_elapsed',
+        'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
+        'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active',
+        'smsp__inst_executed.sum', 'sm__cycles_elapsed.avg.per_second',
+        'launch__registers_per_thread', 'launch__shared_mem_per_block_dynamic', 'launch__grid_size',
+        'launch__block_size', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'dram__throughput.avg.pct_of_peak_sustained_elapsed',
+        'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active']
+
+
+def ours(name):
+    return 'asot' in name or 'sinkhorn' in name or 'map_assign' in name or 'histogram' in name
+
+
+def launches(csv_path, out_md):
+    rows = list(csv.reader(open(csv_path)))
+    hdr = next(i for i, r in enumerate(rows) if 'Kernel Name' in r)
+    h = rows[hdr]
+    ki, vi = h.index('Kernel Name'), h.index('Metric Value')
+    agg = collections.OrderedDict()
+    for r in rows[hdr + 1:]:
+        if len(r) > vi:
+            agg.setdefault(r[ki].split('(')[0][:80], []).append(float(r[vi].replace(',', '')))
+    tot = sum(sum(x) for x in agg.values())
+    our = sum(sum(x) for k, x in agg.items() if ours(k))
+    lines = ["kernel | launches | mean ns | share of all launches | share of libasot launches",
+             "---|---|---|---|---"]
+    for k, x in agg.items():
+        lines.append(f"{k} | {len(x)} | {sum(x) / len(x):.0f} | {sum(x) / tot:.4f} | "
+                     f"{(sum(x) / our if ours(k) else 0):.4f}")
+    with open(out_md, 'w') as f:
+        f.write(f"# ncu launch list ({os.path.basename(csv_path)}): gpu__time_duration.sum, "
+                "--clock-control none\n\nCold-cache, serialised launches: compare SHARES, not "
+                "absolute times.  Non-libasot rows are torch plumbing (L2 flush, checks).\n\n")
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def full(rep, out_json, traffic_key=None):
+    raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, u, v = rows[0], rows[1], rows[2]
+    out = {'kernel': v[h.index('Kernel Name')] if 'Kernel Name' in h else None}
+    for k in KEYS:
+        if k in h:
+            i = h.index(k)
+            out[k] = f"{v[i]} {u[i]}".strip()
+    stalls = {}
+    for i, name in enumerate(h):
+        if 'average_warps_issue_stalled' in name and name.endswith('per_issue_active.ratio'):
+            try:
+                if float(v[i]) > 0.05:
+                    stalls[name.replace('smsp__average_warps_issue_stalled_', '').replace(
+                        '_per_issue_active.ratio', '')] = float(v[i])
+            except ValueError:
+                pass
+    out['stall_reasons_per_issue'] = stalls
+
+    def num(k):
+        i = h.index(k)
+        scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}.get(u[i], 1)
+        return float(v[i].replace(',', '')) * scale
+    traffic = num('dram__bytes_read.sum') + num('dram__bytes_write.sum')
+    out['dram_bytes_per_launch'] = traffic
+    with open(out_json, 'w') as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+    if traffic_key:
+        tpath = os.path.join(ROOT, 'profiles', 'ncu_traffic.json')
+        t = json.load(open(tpath)) if os.path.exists(tpath) else {}
+        t[traffic_key] = traffic
+        json.dump(t, open(tpath, 'w'), indent=1)
+
+
+if __name__ == '__main__':
+    if sys.argv[1] == 'launches':
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
