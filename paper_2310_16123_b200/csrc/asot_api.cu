@@ -66,9 +66,15 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
   return ASOT_OK;
 }
 
-bool use_tc(int32_t K, asot_precision prec) {
-  return prec == ASOT_PREC_TF32 && asot::sinkhorn_tc_supported(K);
+// Tensor-core kernel selection for TF32 requests: 0 = none (fp32 SIMT), 1 = single-CTA
+// (K <= 128), 2 = CTA pair (128 < K <= 256).
+int tc_kind(int32_t K, asot_precision prec) {
+  if (prec != ASOT_PREC_TF32) return 0;
+  if (asot::sinkhorn_tc_supported(K)) return 1;
+  if (asot::sinkhorn_tc2_supported(K)) return 2;
+  return 0;
 }
+bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
 
 // Gibbs buffers: plain G / GC (SIMT) or swizzled TF32 images (tensor-core path).
 struct GibbsBufs {
@@ -80,7 +86,10 @@ struct GibbsBufs {
 
 GibbsBufs carve_gibbs(Carver& cv, int32_t K, bool tc) {
   GibbsBufs b;
-  if (tc) {
+  if (tc && asot::sinkhorn_tc2_supported(K)) {
+    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
+    b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
+  } else if (tc) {
     const size_t kp = (size_t)asot::kpad32(K);
     b.g_img = (uint32_t*)cv.take(kp * kp * 4);
     b.gc_img = (uint32_t*)cv.take(kp * kp * 4);
@@ -110,8 +119,13 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                          const float* cost, float eps, int32_t K, int32_t iters, bool tc,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
                          cudaStream_t s) {
-  ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
-                                      tc ? asot::kpad32(K) : K, s));
+  const bool pair_kernel = tc && asot::sinkhorn_tc2_supported(K);
+  if (pair_kernel) {
+    ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
+  } else {
+    ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
+                                        tc ? asot::kpad32(K) : K, s));
+  }
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (g_prof_on) {
     ev = prof_pair();
@@ -124,7 +138,10 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
       if (ev.second) cudaEventRecord(ev.second, s);
     }
   } rec{ev, s};
-  if (tc) {
+  if (pair_kernel) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink, H, K,
+                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
+  } else if (tc) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                          gb.gc_img, iters, s));
   } else {

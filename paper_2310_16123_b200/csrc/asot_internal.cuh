@@ -122,6 +122,14 @@ bool sinkhorn_tc_supported(int K);
 cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_dist,
                                const PairSink& out, const float* H, int K, const uint32_t* g_img,
                                const uint32_t* gc_img, int iters, cudaStream_t s);
+// tcgen05 cta_group::2 kernel for 128 < K <= 256 (tile mode; images: 2 ranks x 128 KB each).
+bool sinkhorn_tc2_supported(int K);
+size_t sinkhorn_tc2_image_bytes();
+cudaError_t launch_gibbs_prep_tc2(const float* cost, int K, float eps, uint8_t* g_img, uint8_t* gc_img,
+                                  cudaStream_t s);
+cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
+                                cudaStream_t s);
 cudaError_t launch_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
                                 int64_t tile_end, float* mat, cudaStream_t s);
 cudaError_t launch_zero_diag(float* mat, int64_t n_dist, cudaStream_t s);
