@@ -340,8 +340,10 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f).get(f"{inp.name}:{args.precision}")
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "sinkhorn_tc_kernel" if eff == asot.TF32
-                else "sinkhorn_simt_kernel", "kernel_ms_per_launch": kern_avg_ms,
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": ("sinkhorn_simt_kernel" if eff != asot.TF32 else
+                           "sinkhorn_tc_kernel (1 SM, M=128)" if inp.n_anchors <= 128 else
+                           "sinkhorn_tc2_kernel (CTA pair, cta_group::2, M=256)"), "kernel_ms_per_launch": kern_avg_ms,
                 "kernel_share_of_step": kern_avg_ms * kern_n / max(tot_ms, 1e-9) if world == 1 else None,
                 "flops_per_pair": flops_per_pair, "pairs_per_launch": pairs_per_launch,
                 "peak_note": peak_note,

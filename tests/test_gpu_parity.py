@@ -195,3 +195,44 @@ def test_full_size_sampled_parity_c2(asot):
     assert r.max() <= TOL[eff]
     np.testing.assert_array_equal(Dg, Dg.T)
     assert np.all(np.diag(Dg) == 0)
+
+
+def test_pair_kernel_odd_tile_ranges(asot):
+    """K = 256 runs on the CTA-pair kernel, whose unit is a block pair (two tiles); ranges that
+    start or end on an odd tile must mask the half outside the range."""
+    inp, Do, _, _ = oracle_full("c3", 36)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    D1 = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=asot.TF32,
+                              offsets_host=inp.offsets)
+    nt = asot.num_tiles(inp.n_dist)
+    D3 = torch.full_like(D1, -1.0)
+    cuts = [0, 1, 4, 7, nt - 3, nt]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        packed = torch.full(((b - a) * 128,), -7.0, device="cuda")
+        asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=asot.TF32,
+                             offsets_host=inp.offsets, tile_range=(a, b), packed=packed, want_matrix=False)
+        assert not torch.any(packed == -7.0)          # every slot of the range written (0 if invalid)
+        asot.unpack_tiles(packed, inp.n_dist, a, b, D3, zero_diag=(b == nt))
+    assert torch.equal(D1, D3)
+    r = rel_err(D1.cpu().numpy(), Do, 1.0)
+    assert r.max() <= 2e-3
+
+
+def test_full_size_sampled_parity_c3(asot):
+    """c3 at full size (N = 2000, the multi-GPU configuration) on the CTA-pair kernel: sampled
+    pairs against the oracle evaluated pair by pair."""
+    inp = make_inputs("c3")
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=asot.TF32,
+                             offsets_host=inp.offsets, cost_max=1.0, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    _, H_o = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
+    pi, pj = random_pairs(inp.n_dist, 300, seed=23)
+    pi = np.concatenate([pi, np.array([0, 15, 1984, 1998], np.int32)])
+    pj = np.concatenate([pj, np.array([1, 16, 1999, 1999], np.int32)])
+    c_o, _ = O.pair_costs(H_o, inp.cost, inp.eps, inp.iters, pi.astype(np.int64), pj.astype(np.int64))
+    Dg = D.cpu().numpy()
+    assert rel_err(Dg[pi, pj], c_o, 1.0).max() <= 2e-3
+    np.testing.assert_array_equal(Dg, Dg.T)
