@@ -56,7 +56,8 @@ typedef enum {
 typedef enum {
   ASOT_PREC_FP32 = 0, /* fp32 CUDA-core Sinkhorn, IEEE divide: target rel. err <= 1e-4      */
   ASOT_PREC_TF32 = 1  /* tcgen05 kind::tf32 MMA (RNA-rounded G and U/V, fp32 accumulate):
-                         target rel. err <= 2e-3; needs K <= 256 in this build, else falls
+                         target rel. err <= 2e-3; K <= 1024 (all supported K) runs on
+                         tcgen05 (resident kernels for K <= 256, streamed above); else falls
                          back to ASOT_PREC_FP32 (reported by asot_effective_precision)     */
 } asot_precision;
 
@@ -152,7 +153,7 @@ asot_status asot_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_
 asot_status asot_tile_pairs_host(int64_t n_dist, int64_t tile_begin, int64_t tile_end,
                                  int32_t* i_out, int32_t* j_out, uint8_t* valid_out);
 
-/* Precision actually used for a given K and request (TF32 needs K <= 256 in this build). */
+/* Precision actually used for a given K and request (TF32 covers K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
 
 /* Optional timing of the dominant kernel (bench.py's roofline): while enabled on this thread,

@@ -67,29 +67,45 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 }
 
 // Tensor-core kernel selection for TF32 requests: 0 = none (fp32 SIMT), 1 = single-CTA
-// (K <= 128), 2 = CTA pair (128 < K <= 256).
+// resident (K <= 128), 2 = CTA-pair resident (128 < K <= 256), 4 = CTA-pair streamed (K <= 1024).
 int tc_kind(int32_t K, asot_precision prec) {
   if (prec != ASOT_PREC_TF32) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
+  if (asot::sinkhorn_tc4_supported(K)) return 4;
   return 0;
 }
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
 
-// Gibbs buffers: plain G / GC (SIMT) or swizzled TF32 images (tensor-core path).
+int device_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// Gibbs buffers: plain G / GC (SIMT) or swizzled TF32 operand images (tensor-core kernels), plus
+// the streamed kernel's scratch (padded marginals, per-CTA scaling buffers).
 struct GibbsBufs {
+  int kind = 0;
   float* G = nullptr;
   float* GC = nullptr;
   uint32_t* g_img = nullptr;
   uint32_t* gc_img = nullptr;
+  uint8_t* scratch = nullptr;
 };
 
-GibbsBufs carve_gibbs(Carver& cv, int32_t K, bool tc) {
+GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   GibbsBufs b;
-  if (tc && asot::sinkhorn_tc2_supported(K)) {
+  b.kind = kind;
+  if (kind == 4) {
+    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes());
+    b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes());
+    b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc4_scratch_bytes(n_dist, device_sms()) + 1024);
+  } else if (kind == 2) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
-  } else if (tc) {
+  } else if (kind == 1) {
     const size_t kp = (size_t)asot::kpad32(K);
     b.g_img = (uint32_t*)cv.take(kp * kp * 4);
     b.gc_img = (uint32_t*)cv.take(kp * kp * 4);
@@ -116,15 +132,17 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
 }
 
 asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink, const float* H,
-                         const float* cost, float eps, int32_t K, int32_t iters, bool tc,
+                         const float* cost, float eps, int32_t K, int32_t iters,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
                          cudaStream_t s) {
-  const bool pair_kernel = tc && asot::sinkhorn_tc2_supported(K);
-  if (pair_kernel) {
+  const int kind = gb.kind;
+  if (kind == 4) {
+    ASOT_LAUNCH(asot::launch_gibbs_prep_tc4(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
+  } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else {
     ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
-                                        tc ? asot::kpad32(K) : K, s));
+                                        kind == 1 ? asot::kpad32(K) : K, s));
   }
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (g_prof_on) {
@@ -138,10 +156,14 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
       if (ev.second) cudaEventRecord(ev.second, s);
     }
   } rec{ev, s};
-  if (pair_kernel) {
+  if (kind == 4) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink, H, K,
+                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img,
+                                          (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
+  } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
-  } else if (tc) {
+  } else if (kind == 1) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                          gb.gc_img, iters, s));
   } else {
@@ -210,7 +232,7 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
 size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
   Carver cv{nullptr, 0};
   (void)prec;
-  carve_gibbs(cv, n_anchors, false);  // explicit pair lists run on the fp32 SIMT kernel
+  carve_gibbs(cv, n_anchors, 0, 0);  // explicit pair lists run on the fp32 SIMT kernel
   return cv.used;
 }
 
@@ -228,11 +250,11 @@ asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_
   if (n_pairs == 0) return ASOT_OK;
   (void)prec;
   Carver cv{(char*)workspace, workspace_bytes};
-  GibbsBufs gb = carve_gibbs(cv, n_anchors, false);
+  GibbsBufs gb = carve_gibbs(cv, n_anchors, 0, 0);
   if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
   asot::PairSource ps{pair_i, pair_j, n_pairs, 0, n_dist};
   asot::PairSink sink{dist_out, nullptr, n_dist, status};
-  return run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, false, gb, 0, 0,
+  return run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, gb, 0, 0,
                       (cudaStream_t)stream);
 }
 
@@ -241,7 +263,7 @@ size_t asot_distance_matrix_workspace_bytes(int64_t n_dist, int64_t n_points, in
   Carver cv{nullptr, 0};
   cv.take((size_t)n_dist * n_anchors * 4);   // H
   cv.take((size_t)n_points * 4);             // assign scratch
-  carve_gibbs(cv, n_anchors, use_tc(n_anchors, prec));
+  carve_gibbs(cv, n_anchors, tc_kind(n_anchors, prec), n_dist);
   return cv.used;
 }
 
@@ -274,7 +296,7 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
   Carver cv{(char*)workspace, workspace_bytes};
   float* H = (float*)cv.take((size_t)n_dist * n_anchors * 4);
   int32_t* assign = (int32_t*)cv.take((size_t)T * 4);
-  GibbsBufs gb = carve_gibbs(cv, n_anchors, tc);
+  GibbsBufs gb = carve_gibbs(cv, n_anchors, tc_kind(n_anchors, prec), n_dist);
   if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
 
   const float* Huse = hist_in;
@@ -290,7 +312,7 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
   }
   asot::PairSource ps{nullptr, nullptr, (tile_end - tile_begin) * asot::kTileSlots, tile_begin, n_dist};
   asot::PairSink sink{packed_out, dist_out, n_dist, status};
-  st = run_sinkhorn(ps, sink, Huse, cost, eps, n_anchors, iters, tc, gb, tile_begin, tile_end, s);
+  st = run_sinkhorn(ps, sink, Huse, cost, eps, n_anchors, iters, gb, tile_begin, tile_end, s);
   if (st != ASOT_OK) return st;
   if (dist_out && tile_begin == 0 && tile_end == n_tiles) ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, s));
   return ASOT_OK;

@@ -1,0 +1,350 @@
+// asot_sinkhorn_tc4.cu -- steps a5 + a6 for 256 < K <= 1024: the HBM/L2-streamed GEMM form.
+//
+// Same recurrence as the resident kernels (R#3-R#6, R#11).  At K = 1024 neither the
+// Gibbs kernel (4 MB TF32) nor one tile's scalings (128 pairs x 4 KB) fit on chip, so every
+// phase is a GEMM  D[256 pairs x 1024] = X[256 x 1024] . K[1024 x 1024]  per CTA pair
+// (tcgen05.mma.cta_group::2.kind::tf32, M = 256, N = 256 per instruction, both operands from
+// SMEM) with the divide fused into the epilogue:
+//   - X (the current scaling, TF32 bits in the K-major SW128 operand layout) lives in a
+//     per-CTA ping-pong buffer in global memory (L2 / HBM); K and K (.) C_s live in global
+//     images pre-arranged so each (K-chunk, N-half) operand slice is one contiguous block;
+//   - a producer warp streams 48 KB stages (A: 128 pairs x 32 anchors of X; B: this CTA's 256
+//     output anchors x 32) with TMA bulk copies into a 3-stage mbarrier pipeline; the leader's
+//     MMA warp waits for both CTAs' stages (the peer relays its "full" to the leader) and frees
+//     them with multicast commits;
+//   - each phase is two passes over N (512 anchors each, D = 512 TMEM columns); after a pass the
+//     16 epilogue warps compute x = m / D (one MUFU per two anchors), RNA-round to TF32 and
+//     write the next X to global; the last phase multiplies by K (.) C_s and reduces
+//     sum_r u_r ((K (.) C_s) v)_r against u_L read back from global.
+#include <cfloat>
+#include <cstdlib>
+
+#include "asot_internal.cuh"
+#include "asot_tcgen05.cuh"
+
+namespace asot {
+namespace tc4 {
+
+using namespace ::asot::ptx;
+
+constexpr int kKP = 1024;
+constexpr int kEpiWarps = 16;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = kEpiThreads + 64;  // + producer warp + MMA (leader) / relay (peer) warp
+constexpr int kStages = 3;
+constexpr uint32_t kAChunk = 16384;          // 128 pair rows x 128 B (32 anchors)
+constexpr uint32_t kBChunk = 32768;          // 2 N-subs x 128 anchor rows x 128 B
+constexpr uint32_t kStageBytes = kAChunk + kBChunk;
+constexpr int kKC = kKP / 32;                // 32 K-chunks per pass
+constexpr uint32_t kXBytes = 512 * 1024;     // one X buffer: 128 rows x 1024 x 4 B
+constexpr size_t kImgRankBytes = (size_t)2 * 1024 * 1024;  // one rank's half of a K image
+
+struct Smem {
+  static constexpr size_t kOffStage = 0;
+  static constexpr size_t kOffRed = (size_t)kStages * kStageBytes;  // [4][128] floats
+  static constexpr size_t kOffBar = kOffRed + 4 * 128 * 4;
+  static constexpr size_t kBytes = kOffBar + 256 + 1024;
+};
+
+__host__ __device__ inline uint32_t sw_rows(uint32_t r, uint32_t kin) {  // [rows][128 B] block
+  const uint32_t lin = r * 128u + kin * 4u;
+  return lin ^ (((lin >> 7) & 7u) << 4);
+}
+// X buffer (A operand image): [kc 32][128 rows][128 B]
+__host__ __device__ inline uint32_t x_offset(uint32_t p, uint32_t k) { return (k >> 5) * kAChunk + sw_rows(p, k & 31); }
+// K image of one rank: [nh 2][kc 32][ns 2][128 rows][128 B]; output anchor n = nh*512 + ns*256 + rank*128 + r
+__host__ __device__ inline uint32_t b_offset(uint32_t nh, uint32_t ns, uint32_t r, uint32_t k) {
+  return ((nh * 32u + (k >> 5)) * 2u + ns) * 16384u + sw_rows(r, k & 31);
+}
+
+// 16 consecutive anchors [k0, k0+16) of pair row p in an X image: four 16-byte chunks
+__device__ __forceinline__ void x_load16(const uint8_t* xb, uint32_t p, uint32_t k0, float* v) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float4 q = *reinterpret_cast<const float4*>(xb + x_offset(p, k0 + 4 * c));
+    v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+  }
+}
+
+template <int DBG>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
+                    const float* __restrict__ Hp, int K, const uint8_t* __restrict__ g_img,
+                    const uint8_t* __restrict__ gc_img, uint8_t* __restrict__ xbuf, int iters) {
+  using S = Smem;
+  constexpr uint32_t kIdesc = make_idesc_tf32(256, 256);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* red = (float*)(smem + S::kOffRed);
+  uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
+  // bars: [0,3) full, [3,6) empty, [6,9) peer_full (leader), 9 mma_done, 10 tmem_free (leader), 11 x_ready
+  uint32_t* tmem_holder = (uint32_t*)(bars + 12);
+  const uint32_t bar_full = smem_u32(&bars[0]), bar_empty = smem_u32(&bars[3]);
+  const uint32_t bar_peer = smem_u32(&bars[6]), bar_done = smem_u32(&bars[9]);
+  const uint32_t bar_free = smem_u32(&bars[10]), bar_xr = smem_u32(&bars[11]);
+  const uint32_t stage0 = smem_u32(smem + S::kOffStage);
+
+  const uint32_t rank = cluster_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+      mbar_init(bar_peer + 8 * s, 1);
+    }
+    mbar_init(bar_done, 1);
+    mbar_init(bar_free, 2);
+    mbar_init(bar_xr, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (*tmem_holder != 0) __trap();
+
+  uint8_t* xb = xbuf + (size_t)blockIdx.x * (2 * kXBytes);
+  const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
+  const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int phases = 2 * iters + 1;
+
+  if (warp == kEpiWarps) {
+    // ------------------------------------------------------------------ producer (TMA)
+    if (lane == 0) {
+      int64_t it = 0;
+      uint32_t xr_par = 0;
+      for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+        for (int f = 0; f < phases; ++f) {
+          const uint8_t* xin = xb + (f & 1) * kXBytes;
+          const uint8_t* img = (f < phases - 1 ? g_img : gc_img) + rank * kImgRankBytes;
+          mbar_wait(bar_xr, xr_par);  // X_in fully written (previous phase / tile init)
+          xr_par ^= 1u;
+          fence_proxy_async_global();
+          for (int nh = 0; nh < 2; ++nh) {
+            for (int kc = 0; kc < kKC; ++kc, ++it) {
+              const int s = (int)(it % kStages);
+              if (it >= kStages) mbar_wait(bar_empty + 8 * s, (uint32_t)((it / kStages - 1) & 1));
+              mbar_expect_tx(bar_full + 8 * s, kStageBytes);
+              bulk_g2s(stage0 + s * kStageBytes, xin + kc * kAChunk, kAChunk, bar_full + 8 * s);
+              bulk_g2s(stage0 + s * kStageBytes + kAChunk, img + (size_t)(nh * kKC + kc) * kBChunk, kBChunk,
+                       bar_full + 8 * s);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kEpiWarps + 1) {
+    // ------------------------------------------------------------------ MMA (leader) / relay (peer)
+    int64_t it = 0;
+    uint32_t free_par = 0;
+    bool first = true;
+    for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+      for (int f = 0; f < phases; ++f) {
+        for (int nh = 0; nh < 2; ++nh) {
+          if (rank == 0 && !first) {
+            mbar_wait(bar_free, free_par);  // both CTAs drained D of the previous pass
+            free_par ^= 1u;
+          }
+          first = false;
+          for (int kc = 0; kc < kKC; ++kc, ++it) {
+            const int s = (int)(it % kStages);
+            const uint32_t par = (uint32_t)((it / kStages) & 1);
+            mbar_wait(bar_full + 8 * s, par);
+            if (rank != 0) {
+              if (lane == 0) mbar_arrive_cluster(mapa(bar_peer + 8 * s, 0));
+              continue;
+            }
+            mbar_wait(bar_peer + 8 * s, par);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t a_base = stage0 + s * kStageBytes, b_base = a_base + kAChunk;
+              const uint64_t a0 = make_sw128_desc(a_base), b0 = make_sw128_desc(b_base);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+                for (int ns = 0; ns < 2; ++ns) {
+                  if (DBG != 2)
+                    mma2_tf32_ss((uint32_t)(ns * 256), a0 + (uint64_t)((ks * 32) >> 4),
+                                 b0 + (uint64_t)((ns * 16384 + ks * 32) >> 4), kIdesc, (kc | ks) ? 1u : 0u);
+                }
+              }
+              mma2_commit_mc(bar_empty + 8 * s);
+              if (kc == kKC - 1) mma2_commit_mc(bar_done);
+            }
+            __syncwarp();
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (16 warps)
+    const int q = warp & 3, g = warp >> 2;  // TMEM lane quarter, column group (128 of a pass)
+    const int p = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t free_remote = mapa(bar_free, 0);
+    uint32_t done_par = 0;
+    for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+      const int64_t t = 2 * b + rank;
+      const bool t_in = t >= tile_begin && t < tile_end;
+      int ii, jj;
+      const bool valid = tile_slot_pair(t, p, n_dist, ii, jj) && t_in;
+      const float* arow = Hp + (size_t)(valid ? ii : n_dist) * kKP;
+      const float* brow = Hp + (size_t)(valid ? jj : n_dist) * kKP;
+      // tile init: X_in of phase 0 = V^T = 1 on real anchors (padding stays 0), my row, anchors
+      // [g*256, g*256+256)
+      for (int k = g * 256; k < g * 256 + 256; k += 4) {
+        uint32_t v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (k + e < K) ? 0x3f800000u : 0u;
+        stg128(xb + x_offset(p, k), v[0], v[1], v[2], v[3]);
+      }
+      fence_proxy_async_global();
+      named_bar_sync(1, kEpiThreads);
+      if (threadIdx.x == 0) mbar_arrive_local(bar_xr);
+      float acc = 0.0f;
+      for (int f = 0; f < phases; ++f) {
+        const bool cost_phase = f == phases - 1;
+        uint8_t* xout = xb + ((f + 1) & 1) * kXBytes;
+        const uint8_t* ubuf = xb + kXBytes;  // u_L (read in the cost phase only)
+        const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
+        for (int nh = 0; nh < 2; ++nh) {
+          mbar_wait(bar_done, done_par);
+          done_par ^= 1u;
+          tc_fence_after();
+          const uint32_t col0 = (uint32_t)(nh * 512 + g * 128);   // global anchor index of my first column
+          const uint32_t tcol = lane_off + (uint32_t)(g * 128);   // my TMEM columns (N-subs = g>>1)
+          if (DBG != 1) {
+            uint32_t d[2][16];
+            tmem_ld16u(tcol, d[0]);
+            tmem_wait_ld();
+            reg_fence16(d[0]);
+#pragma unroll 2
+            for (int c = 0; c < 8; ++c) {
+              if (c + 1 < 8) tmem_ld16u(tcol + (c + 1) * 16, d[(c + 1) & 1]);
+              const uint32_t* dc = d[c & 1];
+              const uint32_t k0 = col0 + c * 16;
+              if (!cost_phase) {
+                float m[16];
+#pragma unroll
+                for (int e = 0; e < 16; e += 4) {
+                  const float4 mq = *reinterpret_cast<const float4*>(mrow + k0 + e);
+                  m[e] = mq.x; m[e + 1] = mq.y; m[e + 2] = mq.z; m[e + 3] = mq.w;
+                }
+                uint32_t o[16];
+#pragma unroll
+                for (int e = 0; e < 16; e += 2) {
+                  const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
+                  const float r = rcp_approx(d0 * d1);
+                  o[e] = tf32_rna_pre((m[e] * d1) * r);
+                  o[e + 1] = tf32_rna_pre((m[e + 1] * d0) * r);
+                }
+#pragma unroll
+                for (int e = 0; e < 16; e += 4) stg128(xout + x_offset(p, k0 + e), o[e], o[e + 1], o[e + 2], o[e + 3]);
+              } else {
+                float u[16];
+                x_load16(ubuf, p, k0, u);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) acc = fmaf(tf32_mask(u[e]), __uint_as_float(dc[e]), acc);
+              }
+              if (c + 1 < 8) {
+                tmem_wait_ld();
+                reg_fence16(d[(c + 1) & 1]);
+              }
+            }
+          }
+          if (!cost_phase && nh == 1) fence_proxy_async_global();
+          tc_fence_before();
+          named_bar_sync(1, kEpiThreads);
+          if (threadIdx.x == 0) {
+            mbar_arrive_cluster(free_remote);
+            if (!cost_phase && nh == 1) mbar_arrive_local(bar_xr);
+          }
+        }
+      }
+      red[g * 128 + p] = acc;
+      named_bar_sync(1, kEpiThreads);
+      if (g == 0 && t_in)
+        write_result(out, (t - tile_begin) * kTileSlots + p, valid, ii, jj,
+                     red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
+      named_bar_sync(1, kEpiThreads);  // red reused by the next tile
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(0u) : "memory");
+}
+
+// ----------------------------------------------------------------------------- prep kernels
+__global__ void gibbs_prep_tc4_kernel(const float* __restrict__ cost, int K, float eps, uint8_t* __restrict__ g_img,
+                                      uint8_t* __restrict__ gc_img) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < kKP * kKP; idx += gridDim.x * blockDim.x) {
+    const int n = idx / kKP, k = idx % kKP;
+    const bool in = n < K && k < K;
+    const double c = in ? (double)cost[(int64_t)n * K + k] : 0.0;
+    const double gv = in ? exp(-c / (double)eps) : 0.0;               // P:183  K := exp(-C_s / eps)
+    const uint32_t gb = in ? tf32_rna_bits((float)gv) : 0x3f800000u;  // padding = 1 (R#12)
+    const uint32_t gcb = in ? tf32_rna_bits((float)(gv * c)) : 0u;
+    const uint32_t nh = n >> 9, ns = (n >> 8) & 1, rk = (n >> 7) & 1, r = n & 127;
+    const size_t off = (size_t)rk * kImgRankBytes + b_offset(nh, ns, r, k);
+    *(uint32_t*)(g_img + off) = gb;
+    *(uint32_t*)(gc_img + off) = gcb;
+  }
+}
+
+// Marginal rows padded to 1024 anchors, plus a dummy row (index N) for invalid pair slots.
+__global__ void pad_marginals_kernel(const float* __restrict__ H, int64_t n_dist, int K, float* __restrict__ Hp) {
+  const int64_t total = (n_dist + 1) * kKP;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / kKP;
+    const int c = (int)(idx % kKP);
+    float v = 0.0f;
+    if (c < K) v = row < n_dist ? H[row * K + c] : 1.0f / (float)K;
+    Hp[idx] = v;
+  }
+}
+
+}  // namespace tc4
+
+bool sinkhorn_tc4_supported(int K) { return K > 256 && K <= 1024; }
+size_t sinkhorn_tc4_image_bytes() { return 2 * tc4::kImgRankBytes; }
+size_t sinkhorn_tc4_scratch_bytes(int64_t n_dist, int sms) {
+  return (size_t)(n_dist + 1) * tc4::kKP * 4 + (size_t)sms * 2 * tc4::kXBytes;
+}
+
+cudaError_t launch_gibbs_prep_tc4(const float* cost, int K, float eps, uint8_t* g_img, uint8_t* gc_img,
+                                  cudaStream_t s) {
+  tc4::gibbs_prep_tc4_kernel<<<1024, 256, 0, s>>>(cost, K, eps, g_img, gc_img);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
+                                int iters, cudaStream_t s) {
+  if (tile_end <= tile_begin) return cudaSuccess;
+  float* Hp = (float*)scratch;
+  uint8_t* xbuf = scratch + (((size_t)(n_dist + 1) * tc4::kKP * 4 + 1023) & ~(size_t)1023);
+  tc4::pad_marginals_kernel<<<512, 256, 0, s>>>(H, n_dist, K, Hp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
+  auto kern = dbg == 1 ? tc4::sinkhorn_tc4_kernel<1> : dbg == 2 ? tc4::sinkhorn_tc4_kernel<2> : tc4::sinkhorn_tc4_kernel<0>;
+  const size_t smem = tc4::Smem::kBytes;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_bp = ((tile_end + 1) >> 1) - (tile_begin >> 1);
+  int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
+  if (clusters < 1) clusters = 1;
+  kern<<<(unsigned)(2 * clusters), tc4::kThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, Hp, K, g_img,
+                                                             gc_img, xbuf, iters);
+  return cudaGetLastError();
+}
+
+}  // namespace asot
