@@ -209,6 +209,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-pairs", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n-dist", type=int, default=None,
+                    help="shrink N (profiling runs only; bench lines use the full config)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -217,7 +219,7 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     from asot_inputs import make_inputs
 
-    inp = make_inputs(args.config)
+    inp = make_inputs(args.config, n_dist=args.n_dist)
     if args.impl == "reference":
         run_reference(args, inp, rank, world)
         return

@@ -9,7 +9,7 @@
 //     per-CTA ping-pong buffer in global memory (L2 / HBM); K and K (.) C_s live in global
 //     images pre-arranged so each (K-chunk, N-half) operand slice is one contiguous block;
 //   - a producer warp streams 48 KB stages (A: 128 pairs x 32 anchors of X; B: this CTA's 256
-//     output anchors x 32) with TMA bulk copies into a 3-stage mbarrier pipeline; the leader's
+//     output anchors x 32) with TMA bulk copies into a 4-stage mbarrier pipeline; the leader's
 //     MMA warp waits for both CTAs' stages (the peer relays its "full" to the leader) and frees
 //     them with multicast commits;
 //   - each phase is two passes over N (512 anchors each, D = 512 TMEM columns); after a pass the
@@ -31,7 +31,7 @@ constexpr int kKP = 1024;
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = kEpiThreads + 64;  // + producer warp + MMA (leader) / relay (peer) warp
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr uint32_t kAChunk = 16384;          // 128 pair rows x 128 B (32 anchors)
 constexpr uint32_t kBChunk = 32768;          // 2 N-subs x 128 anchor rows x 128 B
 constexpr uint32_t kStageBytes = kAChunk + kBChunk;
@@ -40,24 +40,38 @@ constexpr uint32_t kXBytes = 512 * 1024;     // one X buffer: 128 rows x 1024 x 
 constexpr size_t kImgRankBytes = (size_t)2 * 1024 * 1024;  // one rank's half of a K image
 
 struct Smem {
+  static constexpr int kMRS = 512 + 4;  // marginal half-row stride (floats), 16-byte shift per row
   static constexpr size_t kOffStage = 0;
-  static constexpr size_t kOffRed = (size_t)kStages * kStageBytes;  // [4][128] floats
-  static constexpr size_t kOffBar = kOffRed + 4 * 128 * 4;
+  static constexpr size_t kOffMarg = (size_t)kStages * kStageBytes;     // [16 rows][516] floats
+  static constexpr size_t kOffRed = kOffMarg;                           // [4][128] floats (aliases marg)
+  static constexpr size_t kOffBar = kOffMarg + (size_t)16 * kMRS * 4;
   static constexpr size_t kBytes = kOffBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "shared memory budget");
 };
 
 __host__ __device__ inline uint32_t sw_rows(uint32_t r, uint32_t kin) {  // [rows][128 B] block
   const uint32_t lin = r * 128u + kin * 4u;
   return lin ^ (((lin >> 7) & 7u) << 4);
 }
-// X buffer (A operand image): [kc 32][128 rows][128 B]
-__host__ __device__ inline uint32_t x_offset(uint32_t p, uint32_t k) { return (k >> 5) * kAChunk + sw_rows(p, k & 31); }
+// X buffer (A operand image) in the no-swizzle K-major core-matrix layout [k/4][128 rows][16 B]:
+// a warp (32 consecutive pair rows) writes 512 contiguous bytes per 16-byte store, and each
+// 32-anchor K-chunk is one contiguous 16 KB block for the TMA bulk load.  Descriptor: LBO (next
+// core matrix along K) = 2048 B, SBO (next 8-row group) = 128 B.
+__host__ __device__ inline uint32_t x_offset(uint32_t p, uint32_t k) { return (k >> 2) * 2048u + p * 16u + (k & 3) * 4u; }
+__device__ __forceinline__ uint64_t make_noswz_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(2048u >> 4) << 16;  // LBO
+  d |= (uint64_t)(128u >> 4) << 32;   // SBO
+  d |= (uint64_t)1u << 46;            // version (sm_100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
 // K image of one rank: [nh 2][kc 32][ns 2][128 rows][128 B]; output anchor n = nh*512 + ns*256 + rank*128 + r
 __host__ __device__ inline uint32_t b_offset(uint32_t nh, uint32_t ns, uint32_t r, uint32_t k) {
   return ((nh * 32u + (k >> 5)) * 2u + ns) * 16384u + sw_rows(r, k & 31);
 }
 
-// 16 consecutive anchors [k0, k0+16) of pair row p in an X image: four 16-byte chunks
+// 16 consecutive anchors [k0, k0+16) (k0 % 4 == 0) of pair row p in an X image: four 16-byte chunks
 __device__ __forceinline__ void x_load16(const uint8_t* xb, uint32_t p, uint32_t k0, float* v) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -65,6 +79,11 @@ __device__ __forceinline__ void x_load16(const uint8_t* xb, uint32_t p, uint32_t
     v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
   }
 }
+
+// Debug timeline (ASOT_TC_DEBUG_MODE=3): [event][pass] for CTA 0's first tile:
+//   0 issuer: first MMA of the pass issued, 1 issuer: last MMA issued,
+//   2 epilogue woke (D ready), 3 epilogue done (after the barrier), 4 producer: first load issued
+__device__ long long g_tc4_trace[5][256];
 
 template <int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -75,13 +94,14 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   constexpr uint32_t kIdesc = make_idesc_tf32(256, 256);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* red = (float*)(smem + S::kOffRed);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
-  // bars: [0,3) full, [3,6) empty, [6,9) peer_full (leader), 9 mma_done, 10 tmem_free (leader), 11 x_ready
-  uint32_t* tmem_holder = (uint32_t*)(bars + 12);
-  const uint32_t bar_full = smem_u32(&bars[0]), bar_empty = smem_u32(&bars[3]);
-  const uint32_t bar_peer = smem_u32(&bars[6]), bar_done = smem_u32(&bars[9]);
-  const uint32_t bar_free = smem_u32(&bars[10]), bar_xr = smem_u32(&bars[11]);
+  // bars: full[S], empty[S], peer_full[S] (leader), mma_done, tmem_free (leader), x_ready
+  constexpr int S3 = 3 * kStages;
+  static_assert((S3 + 4) * 8 <= 256, "barrier area");
+  uint32_t* tmem_holder = (uint32_t*)(bars + S3 + 3);
+  const uint32_t bar_full = smem_u32(&bars[0]), bar_empty = smem_u32(&bars[kStages]);
+  const uint32_t bar_peer = smem_u32(&bars[2 * kStages]), bar_done = smem_u32(&bars[S3]);
+  const uint32_t bar_free = smem_u32(&bars[S3 + 1]), bar_xr = smem_u32(&bars[S3 + 2]);
   const uint32_t stage0 = smem_u32(smem + S::kOffStage);
 
   const uint32_t rank = cluster_rank();
@@ -129,6 +149,8 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             for (int kc = 0; kc < kKC; ++kc, ++it) {
               const int s = (int)(it % kStages);
               if (it >= kStages) mbar_wait(bar_empty + 8 * s, (uint32_t)((it / kStages - 1) & 1));
+              if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && kc == 0 && 2 * f + nh < 256)
+                g_tc4_trace[4][2 * f + nh] = clock64();
               mbar_expect_tx(bar_full + 8 * s, kStageBytes);
               bulk_g2s(stage0 + s * kStageBytes, xin + kc * kAChunk, kAChunk, bar_full + 8 * s);
               bulk_g2s(stage0 + s * kStageBytes + kAChunk, img + (size_t)(nh * kKC + kc) * kBChunk, kBChunk,
@@ -161,15 +183,18 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             }
             mbar_wait(bar_peer + 8 * s, par);
             tc_fence_after();
+            if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && lane == 0 && (kc == 0 || kc == kKC - 1) &&
+                2 * f + nh < 256)
+              g_tc4_trace[kc == 0 ? 0 : 1][2 * f + nh] = clock64();
             if (elect_one()) {
               const uint32_t a_base = stage0 + s * kStageBytes, b_base = a_base + kAChunk;
-              const uint64_t a0 = make_sw128_desc(a_base), b0 = make_sw128_desc(b_base);
+              const uint64_t a0 = make_noswz_desc(a_base), b0 = make_sw128_desc(b_base);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
                 for (int ns = 0; ns < 2; ++ns) {
                   if (DBG != 2)
-                    mma2_tf32_ss((uint32_t)(ns * 256), a0 + (uint64_t)((ks * 32) >> 4),
+                    mma2_tf32_ss((uint32_t)(ns * 256), a0 + (uint64_t)((ks * 4096) >> 4),
                                  b0 + (uint64_t)((ns * 16384 + ks * 32) >> 4), kIdesc, (kc | ks) ? 1u : 0u);
                 }
               }
@@ -193,8 +218,13 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       const bool t_in = t >= tile_begin && t < tile_end;
       int ii, jj;
       const bool valid = tile_slot_pair(t, p, n_dist, ii, jj) && t_in;
-      const float* arow = Hp + (size_t)(valid ? ii : n_dist) * kKP;
-      const float* brow = Hp + (size_t)(valid ? jj : n_dist) * kKP;
+      // marginal rows of this tile: u side = distributions i0 + [0, 8), v side = j0 + [0, 16)
+      int64_t bi, bj;
+      block_pair_decode(b, num_blocks(n_dist), bi, bj);
+      const int64_t i0 = bi * kBlockDist + rank * 8, j0 = bj * kBlockDist;
+      // invalid slots read row 0 of the staged side (finite, discarded: MMA rows are independent)
+      const int arow_s = valid ? (p >> 4) : 0, brow_s = valid ? (p & 15) : 0;
+      float* marg = (float*)(smem + S::kOffMarg);
       // tile init: X_in of phase 0 = V^T = 1 on real anchors (padding stays 0), my row, anchors
       // [g*256, g*256+256)
       for (int k = g * 256; k < g * 256 + 256; k += 4) {
@@ -211,29 +241,57 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         const bool cost_phase = f == phases - 1;
         uint8_t* xout = xb + ((f + 1) & 1) * kXBytes;
         const uint8_t* ubuf = xb + kXBytes;  // u_L (read in the cost phase only)
-        const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
+        // u-update: a = H[i] (8 rows); v-update: b = H[j] (16 rows)
+        const int nrows = (f & 1) ? 16 : 8;
+        const int64_t row0 = (f & 1) ? j0 : i0;
+        const float* mrow = marg + ((f & 1) ? brow_s : arow_s) * S::kMRS;
         for (int nh = 0; nh < 2; ++nh) {
+          if (!cost_phase) {
+            // stage this pass's marginal half-rows (<= 32 KB) while the pass's MMAs run; the
+            // previous epilogue's barrier guarantees nobody still reads the buffer
+            for (int e = threadIdx.x; e < nrows * 128; e += kEpiThreads) {
+              const int r = e >> 7, c4 = (e & 127) * 4;
+              const int64_t row = row0 + r < n_dist ? row0 + r : n_dist;
+              *reinterpret_cast<float4*>(marg + r * S::kMRS + c4) =
+                  *reinterpret_cast<const float4*>(Hp + (size_t)row * kKP + nh * 512 + c4);
+            }
+            named_bar_sync(1, kEpiThreads);
+          }
           mbar_wait(bar_done, done_par);
           done_par ^= 1u;
           tc_fence_after();
+          if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && threadIdx.x == 0 && 2 * f + nh < 256)
+            g_tc4_trace[2][2 * f + nh] = clock64();
           const uint32_t col0 = (uint32_t)(nh * 512 + g * 128);   // global anchor index of my first column
           const uint32_t tcol = lane_off + (uint32_t)(g * 128);   // my TMEM columns (N-subs = g>>1)
           if (DBG != 1) {
             uint32_t d[2][16];
+            float4 mq[2][4];  // marginals of the next chunk are prefetched with its TMEM load
             tmem_ld16u(tcol, d[0]);
+            if (!cost_phase) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) mq[0][e] = *reinterpret_cast<const float4*>(mrow + g * 128 + 4 * e);
+            }
             tmem_wait_ld();
             reg_fence16(d[0]);
 #pragma unroll 2
             for (int c = 0; c < 8; ++c) {
-              if (c + 1 < 8) tmem_ld16u(tcol + (c + 1) * 16, d[(c + 1) & 1]);
+              if (c + 1 < 8) {
+                tmem_ld16u(tcol + (c + 1) * 16, d[(c + 1) & 1]);
+                if (!cost_phase) {
+#pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    mq[(c + 1) & 1][e] = *reinterpret_cast<const float4*>(mrow + g * 128 + (c + 1) * 16 + 4 * e);
+                }
+              }
               const uint32_t* dc = d[c & 1];
               const uint32_t k0 = col0 + c * 16;
               if (!cost_phase) {
                 float m[16];
 #pragma unroll
-                for (int e = 0; e < 16; e += 4) {
-                  const float4 mq = *reinterpret_cast<const float4*>(mrow + k0 + e);
-                  m[e] = mq.x; m[e + 1] = mq.y; m[e + 2] = mq.z; m[e + 3] = mq.w;
+                for (int e = 0; e < 4; ++e) {
+                  const float4 q4 = mq[c & 1][e];
+                  m[4 * e] = q4.x; m[4 * e + 1] = q4.y; m[4 * e + 2] = q4.z; m[4 * e + 3] = q4.w;
                 }
                 uint32_t o[16];
 #pragma unroll
@@ -260,12 +318,15 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
           if (!cost_phase && nh == 1) fence_proxy_async_global();
           tc_fence_before();
           named_bar_sync(1, kEpiThreads);
+          if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && threadIdx.x == 0 && 2 * f + nh < 256)
+            g_tc4_trace[3][2 * f + nh] = clock64();
           if (threadIdx.x == 0) {
             mbar_arrive_cluster(free_remote);
             if (!cost_phase && nh == 1) mbar_arrive_local(bar_xr);
           }
         }
       }
+      float* red = (float*)(smem + S::kOffRed);
       red[g * 128 + p] = acc;
       named_bar_sync(1, kEpiThreads);
       if (g == 0 && t_in)
@@ -332,7 +393,8 @@ cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
-  auto kern = dbg == 1 ? tc4::sinkhorn_tc4_kernel<1> : dbg == 2 ? tc4::sinkhorn_tc4_kernel<2> : tc4::sinkhorn_tc4_kernel<0>;
+  auto kern = dbg == 1 ? tc4::sinkhorn_tc4_kernel<1> : dbg == 2 ? tc4::sinkhorn_tc4_kernel<2>
+            : dbg == 3 ? tc4::sinkhorn_tc4_kernel<3> : tc4::sinkhorn_tc4_kernel<0>;
   const size_t smem = tc4::Smem::kBytes;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -348,3 +410,7 @@ cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_
 }
 
 }  // namespace asot
+
+extern "C" int asot_debug_tc4_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, asot::tc4::g_tc4_trace, sizeof(asot::tc4::g_tc4_trace));
+}
