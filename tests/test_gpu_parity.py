@@ -236,3 +236,36 @@ def test_full_size_sampled_parity_c3(asot):
     Dg = D.cpu().numpy()
     assert rel_err(Dg[pi, pj], c_o, 1.0).max() <= 2e-3
     np.testing.assert_array_equal(Dg, Dg.T)
+
+
+@pytest.mark.parametrize("cfg,n", [("c2", 70), ("c3", 40)])
+def test_distributed_path_single_rank_nccl(asot, cfg, n):
+    """The multi-GPU orchestration with the CUDA steps (partitioned mapping + NCCL all-gather of H,
+    tile-range sharding, NCCL gather of packed tiles, KN6 unpack) on a 1-rank NCCL group: must be
+    bitwise identical to the single-call matrix."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2310_16123_b200 import distributed as D_
+
+    inp = make_inputs(cfg, n_dist=n)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    D1 = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=asot.TF32,
+                              offsets_host=inp.offsets)
+    created = False
+    if not dist.is_initialized():
+        s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        created = True
+    try:
+        st = asot.asot.new_status()
+        steps = D_.cuda_steps(pts, offs, inp.offsets, w, anc, cst, float(inp.eps), inp.iters, asot.TF32,
+                              1.0, st)
+        D2 = D_.distance_matrix_distributed(inp.n_dist, inp.n_anchors, inp.offsets,
+                                            asot.num_tiles(inp.n_dist), steps, device=torch.device("cuda", 0))
+        torch.cuda.synchronize()
+        assert torch.equal(D1, D2)
+    finally:
+        if created:
+            dist.destroy_process_group()
