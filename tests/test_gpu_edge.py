@@ -1,0 +1,137 @@
+"""GPU edge cases through the C ABI: padding paths of every Sinkhorn kernel (K not a multiple of
+the tile), tiny and degenerate problems, and the data-dependent status flags."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from asot_inputs import make_inputs, normalized_sqeuclid_cost  # noqa: E402
+from asot_inputs.synth import AsotInputs  # noqa: E402
+from oracle import asot_oracle as O  # noqa: E402
+
+TOL = {0: 1e-4, 1: 2e-3}
+
+
+@pytest.fixture(scope="module")
+def asot():
+    import paper_2310_16123_b200 as m
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def with_anchors(inp, K, dim=None):
+    """Same point sets, first K anchors (and optionally the first `dim` coordinates)."""
+    d = inp.dim if dim is None else dim
+    anchors = np.ascontiguousarray(inp.anchors[:K, :d])
+    return AsotInputs(inp.name, np.ascontiguousarray(inp.points[:, :d]), inp.offsets, inp.weights,
+                      anchors, normalized_sqeuclid_cost(anchors), inp.eps, inp.iters)
+
+
+def run_both(asot, inp, prec):
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors),
+                             dev(inp.cost), float(inp.eps), inp.iters, precision=prec,
+                             offsets_host=inp.offsets, status=st)
+    torch.cuda.synchronize()
+    Do, _, _ = O.distance_matrix(inp.points, inp.offsets, inp.weights, inp.anchors, inp.cost,
+                                 inp.eps, inp.iters)
+    return D.cpu().numpy(), Do, int(st.item())
+
+
+@pytest.mark.parametrize("K", [1, 7, 33, 100, 129, 200, 257, 300, 700])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_padded_anchor_counts(asot, K, prec):
+    """K off the 32 / 256 / 1024 tile grids exercises the padding of every kernel
+    (1-SM K<=128, CTA pair K<=256, streamed K<=1024)."""
+    base = make_inputs("c5", n_dist=21, iters=12)
+    inp = with_anchors(base, K, dim=37)          # also a dimension that is not a multiple of 4
+    Dg, Do, st = run_both(asot, inp, prec)
+    assert st == 0
+    eff = asot.effective_precision(K, prec)
+    r = np.abs(Dg.astype(np.float64) - Do) / np.maximum(Do, 1e-3)
+    assert r.max() <= TOL[eff], f"K={K} prec={eff} max rel {r.max():.3e}"
+    np.testing.assert_array_equal(Dg, Dg.T)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17])
+def test_tiny_n(asot, n):
+    inp = make_inputs("c2", n_dist=n, iters=5)
+    for prec in (0, 1):
+        Dg, Do, st = run_both(asot, inp, prec)
+        assert st == 0 and Dg.shape == (n, n)
+        assert np.all(np.diag(Dg) == 0)
+        r = np.abs(Dg.astype(np.float64) - Do) / np.maximum(Do, 1e-3)
+        assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)]
+
+
+def test_single_point_distributions_and_duplicates(asot):
+    """n_i = 1 everywhere (one-hot marginals: d = C_s(u, v) exactly up to K's rounding) and
+    duplicated distributions (same histogram on both sides)."""
+    base = make_inputs("c2", n_dist=30, iters=20)
+    pts = base.points[base.offsets[:-1]]           # first point of each distribution
+    pts = np.concatenate([pts, pts[:5]])           # + 5 duplicates
+    N = pts.shape[0]
+    offs = np.arange(N + 1, dtype=np.int64)
+    w = np.ones(N, np.float32)
+    inp = AsotInputs("c2", np.ascontiguousarray(pts), offs, w, base.anchors, base.cost, base.eps, base.iters)
+    for prec in (0, 1):
+        Dg, Do, st = run_both(asot, inp, prec)
+        assert st == 0
+        a = O.map_assign(pts, base.anchors)
+        exact = base.cost.astype(np.float64)[a][:, a]
+        np.fill_diagonal(exact, 0)
+        np.testing.assert_allclose(Do, exact, rtol=1e-12, atol=1e-15)   # oracle: closed form
+        r = np.abs(Dg.astype(np.float64) - exact) / np.maximum(exact, 1e-3)
+        assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)]
+
+
+def test_single_anchor(asot):
+    inp = with_anchors(make_inputs("c1", n_dist=9, iters=4), 1)
+    for prec in (0, 1):
+        Dg, Do, st = run_both(asot, inp, prec)
+        assert np.all(Dg == 0) and np.all(Do == 0)
+
+
+def test_status_flags(asot):
+    inp = make_inputs("c1", n_dist=6, iters=3)
+    import paper_2310_16123_b200.asot as A
+    # empty distribution
+    offs = inp.offsets.copy(); offs[3] = offs[2]
+    pts = inp.points; w = inp.weights.copy()
+    st = A.new_status()
+    A.distance_matrix(dev(pts), dev(offs), dev(w), dev(inp.anchors), dev(inp.cost), float(inp.eps),
+                      inp.iters, offsets_host=offs, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & A.FLAG_EMPTY_DIST
+    with pytest.raises(ValueError):
+        A.check_status(st)
+    # mass not summing to one
+    w2 = inp.weights.copy(); w2[0] *= 3
+    st = A.new_status()
+    A.map_to_anchors(dev(pts), dev(inp.offsets), dev(w2), dev(inp.anchors), offsets_host=inp.offsets, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & A.FLAG_BAD_MASS
+    # non-finite coordinate
+    p2 = inp.points.copy(); p2[4, 1] = np.nan
+    st = A.new_status()
+    A.map_to_anchors(dev(p2), dev(inp.offsets), dev(inp.weights), dev(inp.anchors), offsets_host=inp.offsets,
+                     status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & A.FLAG_NONFINITE_INPUT
+    with pytest.raises(FloatingPointError):
+        A.check_status(st)
+
+
+def test_rejects_cpu_tensors_and_bad_args(asot):
+    inp = make_inputs("c1", n_dist=4, iters=2)
+    with pytest.raises(ValueError):
+        asot.distance_matrix(torch.from_numpy(inp.points), None, None, None, torch.from_numpy(inp.cost),
+                             0.05, 2)
+    with pytest.raises(ValueError):   # eps such that max(C)/eps > 80 (R#12)
+        asot.distance_matrix(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors),
+                             dev(inp.cost), 0.001, 2, offsets_host=inp.offsets)
