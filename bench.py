@@ -306,6 +306,7 @@ def main():
     clk = clocks.stop()
     asot.asot.profile_enable(False)
     kern_ms, kern_n = asot.asot.profile_read(reset=True)
+    map_ms, map_n = asot.asot.profile_read(reset=True, kernel=asot.asot.PROF_MAP)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = sum(step_ms)
     gpu_launches = launches[0]
@@ -348,11 +349,34 @@ def main():
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": ("sinkhorn_simt_kernel" if eff != asot.TF32 else
                            "sinkhorn_tc_kernel (1 SM, M=128)" if inp.n_anchors <= 128 else
-                           "sinkhorn_tc2_kernel (CTA pair, cta_group::2, M=256)"), "kernel_ms_per_launch": kern_avg_ms,
+                           "sinkhorn_tc2_kernel (CTA pair, cta_group::2, M=256)" if inp.n_anchors <= 256
+                           else "sinkhorn_tc4_kernel (streamed GEMM form, CTA pair, M=N=256)"),
+                "kernel_ms_per_launch": kern_avg_ms,
                 "kernel_share_of_step": kern_avg_ms * kern_n / max(tot_ms, 1e-9) if world == 1 else None,
                 "flops_per_pair": flops_per_pair, "pairs_per_launch": pairs_per_launch,
                 "peak_note": peak_note,
                 "peak_sustained_based": peaks.get("bf16_tflops_sustained", 0) * (TF32_OVER_BF16 if eff == asot.TF32 else 0) or None}
+
+    # ---- mapping step (a2): the north star's "achieved HBM GB/s for mapping", next to the
+    # FP32-pipe fraction that actually bounds it; live CUDA-event timing
+    mapping = None
+    if map_n:
+        map_avg_ms = map_ms / map_n
+        T_rank = inp.n_points if world == 1 else None
+        if T_rank is not None:
+            d_, K_ = inp.dim, inp.n_anchors
+            bytes_ = T_rank * (4 * d_ + 4) + K_ * d_ * 4     # points in, assignment out, anchors
+            lane_ops = 2 * K_ * d_ * T_rank                   # FSUB + FFMA per (point, anchor, dim)
+            mapping = {
+                "kernel": "map_assign_kernel", "ms_per_launch": map_avg_ms,
+                "points_per_launch": T_rank,
+                "hbm_gbs": bytes_ / (map_avg_ms / 1e3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                "hbm_frac": bytes_ / (map_avg_ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                "fp32_tflops": 3 * K_ * d_ * T_rank / (map_avg_ms / 1e3) / 1e12,
+                "fp32_pipe_frac": lane_ops / (map_avg_ms / 1e3) / (FP32_ALU_PEAK_TFLOPS / 2 * 1e12),
+                "share_of_step": map_ms / max(tot_ms, 1e-9),
+                "note": "ALU-bound by design (intensity 3Kd/(4d+8) >> FP32 ridge); fp32_pipe_frac = "
+                        "2Kd lane-ops per point / (148 SMs x 128 lanes x 1.965 GHz)"}
 
     # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
     # distributed public API with H2D / D2H inside the timed region (N > 1)
@@ -419,7 +443,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "tf32" if eff == asot.TF32 else "f32", "data": "synthetic",
             "config": workload_config(inp, args, world),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "mapping": mapping, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
             "wall_s_timed_region": wall,
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],

@@ -56,9 +56,10 @@ typedef enum {
 typedef enum {
   ASOT_PREC_FP32 = 0, /* fp32 CUDA-core Sinkhorn, IEEE divide: target rel. err <= 1e-4      */
   ASOT_PREC_TF32 = 1  /* tcgen05 kind::tf32 MMA (RNA-rounded G and U/V, fp32 accumulate):
-                         target rel. err <= 2e-3; K <= 1024 (all supported K) runs on
-                         tcgen05 (resident kernels for K <= 256, streamed above); else falls
-                         back to ASOT_PREC_FP32 (reported by asot_effective_precision)     */
+                         target rel. err <= 2e-3; 32 <= K <= 1024 runs on tcgen05
+                         (resident kernels for K <= 256, streamed above); K < 32 runs the
+                         ASOT_PREC_FP32 kernel (TF32 rounding of u/v over < 32 terms can
+                         exceed 2e-3; reported by asot_effective_precision)                 */
 } asot_precision;
 
 /* Bits OR-ed into the caller's device status word. */
@@ -156,11 +157,16 @@ asot_status asot_tile_pairs_host(int64_t n_dist, int64_t tile_begin, int64_t til
 /* Precision actually used for a given K and request (TF32 covers K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
 
-/* Optional timing of the dominant kernel (bench.py's roofline): while enabled on this thread,
- * the library records a CUDA event pair on the launch stream immediately around every Sinkhorn
- * kernel launch.  asot_profile_read synchronises on the recorded events and returns the summed
- * kernel milliseconds and launch count since the last reset.  Host-side only; never on by default. */
+/* Optional kernel timing (bench.py's roofline): while enabled on this thread, the library records
+ * a CUDA event pair on the launch stream immediately around every Sinkhorn kernel launch
+ * (ASOT_PROF_SINKHORN, steps a5+a6) and every mapping kernel launch (ASOT_PROF_MAP, step a2).
+ * asot_profile_read_kernel synchronises on the recorded events of one kernel and returns the
+ * summed kernel milliseconds and launch count since its last reset; asot_profile_read is the
+ * Sinkhorn shorthand.  Host-side only; never on by default. */
+#define ASOT_PROF_SINKHORN 0
+#define ASOT_PROF_MAP 1
 asot_status asot_profile_enable(int32_t on);
+asot_status asot_profile_read_kernel(int32_t which, double* ms_out, int64_t* launches, int32_t reset);
 asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset);
 
 /* Number of kernel launches the last distance_matrix / pairwise call on this thread issued. */

@@ -85,11 +85,17 @@ def profile_enable(on: bool = True) -> None:
     _check(_lib_handle().asot_profile_enable(int(bool(on))))
 
 
-def profile_read(reset: bool = True) -> tuple[float, int]:
-    """(summed Sinkhorn-kernel milliseconds, launches) since the last reset."""
+PROF_SINKHORN = 0
+PROF_MAP = 1
+
+
+def profile_read(reset: bool = True, kernel: int = PROF_SINKHORN) -> tuple[float, int]:
+    """(summed kernel milliseconds, launches) since the last reset, for the Sinkhorn kernel
+    (PROF_SINKHORN) or the mapping kernel (PROF_MAP)."""
     ms = ctypes.c_double(0.0)
     n = ctypes.c_int64(0)
-    _check(_lib_handle().asot_profile_read(ctypes.byref(ms), ctypes.byref(n), int(bool(reset))))
+    _check(_lib_handle().asot_profile_read_kernel(int(kernel), ctypes.byref(ms), ctypes.byref(n),
+                                                  int(bool(reset))))
     return float(ms.value), int(n.value)
 
 

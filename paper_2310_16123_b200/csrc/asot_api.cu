@@ -68,8 +68,12 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 
 // Tensor-core kernel selection for TF32 requests: 0 = none (fp32 SIMT), 1 = single-CTA
 // resident (K <= 128), 2 = CTA-pair resident (128 < K <= 256), 4 = CTA-pair streamed (K <= 1024).
+// K < 32 stays on the fp32 kernel: the per-iteration TF32 rounding of u / v dominates the TF32
+// error (R#23) and a dot product over fewer than 32 anchors barely averages it out
+// (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
+constexpr int32_t kMinTcAnchors = 32;
 int tc_kind(int32_t K, asot_precision prec) {
-  if (prec != ASOT_PREC_TF32) return 0;
+  if (prec != ASOT_PREC_TF32 || K < kMinTcAnchors) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
   if (asot::sinkhorn_tc4_supported(K)) return 4;
@@ -116,20 +120,40 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   return b;
 }
 
-// Profiling of the dominant kernel (asot_profile_*): event pairs recorded around each launch.
+// Profiling (asot_profile_*): event pairs recorded around each launch of the Sinkhorn kernel
+// (ASOT_PROF_SINKHORN) and of the mapping kernel (ASOT_PROF_MAP).
 thread_local bool g_prof_on = false;
-thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
-thread_local size_t g_prof_used = 0;
+struct ProfList {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  size_t used = 0;
+};
+thread_local ProfList g_prof[2];
 
-std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
-  if (g_prof_used == g_prof_events.size()) {
+std::pair<cudaEvent_t, cudaEvent_t> prof_pair(int which) {
+  ProfList& l = g_prof[which];
+  if (l.used == l.events.size()) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    g_prof_events.emplace_back(a, b);
+    l.events.emplace_back(a, b);
   }
-  return g_prof_events[g_prof_used++];
+  return l.events[l.used++];
 }
+
+// Records the start event now and the stop event when the scope ends (after the launch).
+struct ProfScope {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  cudaStream_t s;
+  ProfScope(int which, cudaStream_t st) : s(st) {
+    if (g_prof_on) {
+      ev = prof_pair(which);
+      cudaEventRecord(ev.first, s);
+    }
+  }
+  ~ProfScope() {
+    if (ev.second) cudaEventRecord(ev.second, s);
+  }
+};
 
 asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink, const float* H,
                          const float* cost, float eps, int32_t K, int32_t iters,
@@ -144,18 +168,7 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
                                         kind == 1 ? asot::kpad32(K) : K, s));
   }
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (g_prof_on) {
-    ev = prof_pair();
-    ASOT_CUDA(cudaEventRecord(ev.first, s));
-  }
-  struct Rec {
-    std::pair<cudaEvent_t, cudaEvent_t> ev;
-    cudaStream_t s;
-    ~Rec() {
-      if (ev.second) cudaEventRecord(ev.second, s);
-    }
-  } rec{ev, s};
+  ProfScope prof(ASOT_PROF_SINKHORN, s);
   if (kind == 4) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img,
@@ -185,19 +198,26 @@ asot_status asot_profile_enable(int32_t on) {
   return ASOT_OK;
 }
 
-asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset) {
-  ASOT_CHECK_ARG(sinkhorn_ms && launches, "null pointer argument");
+asot_status asot_profile_read_kernel(int32_t which, double* ms_out, int64_t* launches,
+                                     int32_t reset) {
+  ASOT_CHECK_ARG(ms_out && launches, "null pointer argument");
+  ASOT_CHECK_ARG(which == ASOT_PROF_SINKHORN || which == ASOT_PROF_MAP, "unknown kernel id");
+  ProfList& l = g_prof[which];
   double total = 0.0;
-  for (size_t k = 0; k < g_prof_used; ++k) {
-    ASOT_CUDA(cudaEventSynchronize(g_prof_events[k].second));
+  for (size_t k = 0; k < l.used; ++k) {
+    ASOT_CUDA(cudaEventSynchronize(l.events[k].second));
     float ms = 0.0f;
-    ASOT_CUDA(cudaEventElapsedTime(&ms, g_prof_events[k].first, g_prof_events[k].second));
+    ASOT_CUDA(cudaEventElapsedTime(&ms, l.events[k].first, l.events[k].second));
     total += ms;
   }
-  *sinkhorn_ms = total;
-  *launches = (int64_t)g_prof_used;
-  if (reset) g_prof_used = 0;
+  *ms_out = total;
+  *launches = (int64_t)l.used;
+  if (reset) l.used = 0;
   return ASOT_OK;
+}
+
+asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset) {
+  return asot_profile_read_kernel(ASOT_PROF_SINKHORN, sinkhorn_ms, launches, reset);
 }
 int64_t asot_num_tiles(int64_t n_dist) { return n_dist < 1 ? 0 : asot::num_tiles(n_dist); }
 
@@ -224,7 +244,10 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
     ASOT_CHECK_ARG(offsets_host[i + 1] >= offsets_host[i], "offsets must be non-decreasing");
   const int64_t T = offsets_host[n_dist];
   cudaStream_t s = (cudaStream_t)stream;
-  if (T > 0) ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
+  if (T > 0) {
+    ProfScope prof(ASOT_PROF_MAP, s);
+    ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
+  }
   ASOT_LAUNCH(asot::launch_histograms(assign_out, weights, offsets, n_dist, n_anchors, hist_out, status, s));
   return ASOT_OK;
 }

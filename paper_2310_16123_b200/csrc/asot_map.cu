@@ -228,13 +228,15 @@ histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ w
   const int64_t s = offsets[i], e = offsets[i + 1];
   if (lane == 0 && e <= s) atomicOr(status, ASOT_FLAG_EMPTY_DIST);
   double msum = 0.0;
-  bool bad = false;
+  bool nonfinite = false, negative = false;
   for (int64_t p0 = s; p0 < e; p0 += 32) {
     const int64_t p = p0 + lane;
     const int a = p < e ? assign[p] : 0;
     const float w = p < e ? weights[p] : 0.0f;
     if (p < e) {
-      bad |= !(w >= 0.0f) || !isfinite(w) || a < 0 || a >= K;
+      // a point with a non-finite coordinate has no nearest anchor (assignment out of range)
+      nonfinite |= !isfinite(w) || a < 0 || a >= K;
+      negative |= w < 0.0f;
       msum += (double)w;
     }
     const int cnt = (e - p0) < 32 ? (int)(e - p0) : 32;
@@ -246,8 +248,11 @@ histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ w
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) msum += __shfl_xor_sync(0xffffffffu, msum, off);
-  if (__any_sync(0xffffffffu, bad)) {
-    if (lane == 0) atomicOr(status, ASOT_FLAG_BAD_MASS | ASOT_FLAG_NONFINITE_INPUT);
+  const bool any_nonfinite = __any_sync(0xffffffffu, nonfinite);
+  const bool any_negative = __any_sync(0xffffffffu, negative);
+  if (any_nonfinite || any_negative) {
+    if (lane == 0)
+      atomicOr(status, (any_nonfinite ? ASOT_FLAG_NONFINITE_INPUT : 0u) | (any_negative ? ASOT_FLAG_BAD_MASS : 0u));
   } else if (lane == 0 && e > s && fabs(msum - 1.0) > 1e-5) {
     atomicOr(status, ASOT_FLAG_BAD_MASS);
   }
