@@ -114,28 +114,63 @@ def pairs_of(n: int) -> int:
 
 
 # ------------------------------------------------------------------------------ oracle legs
-def oracle_sample_rate(inp, budget_s: float, seed: int = 0):
+def oracle_soft_map(inp, mapping, model, budget_s):
+    """Soft-mapping oracle on the first distributions until ~budget_s; returns (H with those rows
+    filled and the rest drawn from them, extrapolated full mapping seconds, description)."""
+    from oracle import soft_oracle as S
+
+    H = np.zeros((inp.n_dist, inp.n_anchors))
+    t0 = time.perf_counter()
+    done_pts = 0
+    i = 0
+    while i < inp.n_dist and (time.perf_counter() - t0) < budget_s:
+        s, e = int(inp.offsets[i]), int(inp.offsets[i + 1])
+        if mapping == "ml":
+            Z, _ = S.ml_encode(inp.points[s:e], model.layers)
+        else:
+            Z, _, _ = S.dl_encode(inp.points[s:e], model.dictionary, model.lam_layers, model.n_layers)
+        H[i] = S.soft_histograms(Z, inp.weights[s:e], np.array([0, e - s]))[0]
+        done_pts += e - s
+        i += 1
+    t = time.perf_counter() - t0
+    H[i:] = H[np.arange(inp.n_dist - i) % i]   # rows not mapped in the budget reuse mapped ones
+    t_map = t / done_pts * inp.n_points
+    return H, t_map, f"{mapping} encoder on {done_pts} points ({t:.2f} s), extrapolated to {inp.n_points}"
+
+
+def oracle_sample_rate(inp, budget_s: float, seed: int = 0, mapping: str = "onehot", model=None):
     """The oracle (as it stands) on a bounded sample of the same workload: full mapping of every
-    point, then Sinkhorn on seeded random pairs until the time budget.  Returns whole-job pairs/s
-    extrapolated as P / (t_map + P / pair_rate), and a description."""
+    point (soft mappings: a timed sample of distributions, extrapolated), then Sinkhorn on seeded
+    random pairs until the time budget.  Returns whole-job pairs/s extrapolated as
+    P / (t_map + P / pair_rate), and a description."""
     from asot_inputs import random_pairs
     from oracle import asot_oracle as O
 
-    t0 = time.perf_counter()
-    _, H = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
-    t_map = time.perf_counter() - t0
+    if mapping == "onehot":
+        t0 = time.perf_counter()
+        _, H = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
+        t_map = time.perf_counter() - t0
+        map_note = f"mapping of all {inp.n_points} points ({t_map:.2f} s)"
+    else:
+        H, t_map, map_note = oracle_soft_map(inp, mapping, model, budget_s / 2)
+    cost = inp.cost
+    if mapping == "ml":
+        from oracle import soft_oracle as S
+        t0 = time.perf_counter()
+        cost = S.mahalanobis_cost(inp.anchors, model.M, normalize=True)
+        t_map += time.perf_counter() - t0
     pi, pj = random_pairs(inp.n_dist, 200000, seed=seed)
     done, t_pairs, batch = 0, 0.0, 256
     while t_pairs < budget_s and done < len(pi):
         s = time.perf_counter()
-        O.pair_costs(H, inp.cost, inp.eps, inp.iters, pi[done:done + batch].astype(np.int64),
+        O.pair_costs(H, cost, inp.eps, inp.iters, pi[done:done + batch].astype(np.int64),
                      pj[done:done + batch].astype(np.int64), batch=batch)
         t_pairs += time.perf_counter() - s
         done += batch
     rate = done / t_pairs
     P = inp.n_pairs
     value = P / (t_map + P / rate)
-    sample = (f"fp64 oracle: mapping of all {inp.n_points} points ({t_map:.2f} s) + Sinkhorn on "
+    sample = (f"fp64 oracle: {map_note} + Sinkhorn on "
               f"{done} seeded random pairs ({t_pairs:.2f} s, {rate:.0f} pairs/s); whole-job "
               f"throughput extrapolated to all {P} pairs")
     return value, sample
@@ -208,6 +243,9 @@ def main():
     # default: configs[2] (c3), the config BASELINE.json quotes "at 1/2/4/8 GPUs" like the metric
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--mapping", default="onehot", choices=["onehot", "ml", "dl"],
+                    help="P: one-hot nearest anchor (the north-star path), or the NEXT-1 soft "
+                         "mappings ASOT-ML / ASOT-DL (seeded parameters)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-pairs", type=int, default=256)
@@ -223,6 +261,13 @@ def main():
     from asot_inputs import make_inputs
 
     inp = make_inputs(args.config, n_dist=args.n_dist)
+    soft_model = None
+    if args.mapping == "ml":
+        from asot_inputs.soft import make_ml_model
+        soft_model = make_ml_model(inp.dim, inp.n_anchors)
+    elif args.mapping == "dl":
+        from asot_inputs.soft import make_dl_inputs
+        inp, soft_model = make_dl_inputs(args.config, n_dist=args.n_dist)
     if args.impl == "reference":
         run_reference(args, inp, rank, world)
         return
@@ -249,7 +294,37 @@ def main():
     n_tiles = asot.num_tiles(inp.n_dist)
     launches = [0]
 
-    if world == 1:
+    if args.mapping != "onehot" and world > 1:
+        raise SystemExit("--mapping ml/dl is single-GPU in this build")
+    if args.mapping == "ml":
+        m = soft_model
+        mW1, mb1, mW2, mb2, mM = t(m.W1), t(m.b1), t(m.W2), t(m.b2), t(m.M)
+
+        def step():
+            H, _, _ = asot.map_soft_ml(pts, offs, w, mW1, mb1, mW2, mb2, offsets_host=inp.offsets,
+                                       status=status)
+            launches[0] += asot.last_launch_count()
+            C = asot.mahalanobis_cost(anc, mM, normalize=True, workspace=ws)
+            launches[0] += 3
+            asot.distance_matrix(None, None, None, None, C, float(inp.eps), inp.iters,
+                                 precision=prec, hist=H, out=Dbuf, cost_max=1.0, status=status,
+                                 workspace=ws)
+            launches[0] += asot.last_launch_count()
+            return Dbuf
+    elif args.mapping == "dl":
+        m = soft_model
+        dV1, dc1, dv2, dc2 = t(m.V1), t(m.c1), t(m.v2.reshape(-1)), t(m.c2)
+
+        def step():
+            H, _, _ = asot.map_soft_dl(pts, offs, w, anc, dV1, dc1, dv2, dc2, m.n_layers,
+                                       offsets_host=inp.offsets, status=status)
+            launches[0] += asot.last_launch_count()
+            asot.distance_matrix(None, None, None, None, cst, float(inp.eps), inp.iters,
+                                 precision=prec, hist=H, out=Dbuf, cost_max=cmax, status=status,
+                                 workspace=ws)
+            launches[0] += asot.last_launch_count()
+            return Dbuf
+    elif world == 1:
         def step():
             asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
                                  out=Dbuf, offsets_host=inp.offsets, cost_max=cmax, status=status,
@@ -363,7 +438,28 @@ def main():
     if map_n:
         map_avg_ms = map_ms / map_n
         T_rank = inp.n_points if world == 1 else None
-        if T_rank is not None:
+        if T_rank is not None and args.mapping != "onehot":
+            d_, K_ = inp.dim, inp.n_anchors
+            if args.mapping == "ml":
+                h_ = 2 * d_
+                flops_pt = 2 * d_ * h_ + 2 * h_ * K_
+                kname = "soft_map_kernel<ML> (MLP d->2d->K, |.|/l1, fused a' = Z^T a)"
+            else:
+                h_ = max(1, d_ // 2)
+                flops_pt = 2 * d_ * h_ + 2 * h_ + soft_model.n_layers * 4 * d_ * K_
+                kname = f"soft_map_kernel<DL> ({soft_model.n_layers} near-one-hot layers, fused a' = Z^T a)"
+            bytes_ = T_rank * (4 * d_ + 4) + inp.n_dist * K_ * 4
+            mapping = {
+                "kernel": kname, "ms_per_launch": map_avg_ms, "points_per_launch": T_rank,
+                "flops_per_point": flops_pt,
+                "fp32_tflops": flops_pt * T_rank / (map_avg_ms / 1e3) / 1e12,
+                "fp32_peak_tflops": FP32_ALU_PEAK_TFLOPS,
+                "fp32_frac": flops_pt * T_rank / (map_avg_ms / 1e3) / 1e12 / FP32_ALU_PEAK_TFLOPS,
+                "hbm_gbs": bytes_ / (map_avg_ms / 1e3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                "share_of_step": map_ms / max(tot_ms, 1e-9),
+                "note": "CUDA-core fp32 GEMM-like tiles (16 points x weights from L2/SMEM); "
+                        "bound: FP32 FFMA peak 148 x 128 x 2 x 1.965 GHz"}
+        elif T_rank is not None:
             d_, K_ = inp.dim, inp.n_anchors
             bytes_ = T_rank * (4 * d_ + 4) + K_ * d_ * 4     # points in, assignment out, anchors
             lane_ops = 2 * K_ * d_ * T_rank                   # FSUB + FFMA per (point, anchor, dim)
@@ -381,7 +477,28 @@ def main():
     # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
     # distributed public API with H2D / D2H inside the timed region (N > 1)
     e2e = None
-    if world == 1:
+    if world == 1 and args.mapping != "onehot":
+        # soft mappings: the public Python API with pinned host inputs copied in and D copied out
+        hp = torch.from_numpy(inp.points).pin_memory()
+        hw_ = torch.from_numpy(inp.weights).pin_memory()
+        ho = torch.from_numpy(inp.offsets).pin_memory()
+        hD = torch.empty((inp.n_dist, inp.n_dist), dtype=torch.float32).pin_memory()
+        e_ms = []
+        for _ in range(args.e2e_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pts.copy_(hp, non_blocking=True); w.copy_(hw_, non_blocking=True)
+            offs.copy_(ho, non_blocking=True)
+            hD.copy_(step(), non_blocking=True)
+            torch.cuda.synchronize()
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e = {"value": P * len(e_ms) / (sum(e_ms) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(hp.numel() * 4 + hw_.numel() * 4 + ho.numel() * 8),
+               "d2h_bytes_per_step": int(hD.numel() * 4),
+               "api": f"paper_2310_16123_b200.map_soft_{args.mapping} + distance_matrix(hist) "
+                      "(pinned host copies in, D out, wall clock)"}
+    elif world == 1:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         hp, ho, hw, ha, hc = pin(inp.points), pin(inp.offsets), pin(inp.weights), pin(inp.anchors), pin(inp.cost)
         hD = torch.empty((inp.n_dist, inp.n_dist), dtype=torch.float32).pin_memory().numpy()
@@ -432,7 +549,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sample = oracle_sample_rate(inp, args.cpu_budget)
+        v, sample = oracle_sample_rate(inp, args.cpu_budget, mapping=args.mapping, model=soft_model)
         cpu = {"value": v, "unit": "pairs/s", "cores": len(os.sched_getaffinity(0)),
                "kind": "oracle", "sample": sample}
 

@@ -68,6 +68,7 @@ typedef enum {
 #define ASOT_FLAG_NONFINITE_INPUT  4u  /* NaN/Inf in points, weights or anchors                  */
 #define ASOT_FLAG_DENOM_CLAMPED    8u  /* a Sinkhorn denominator < FLT_MIN was clamped     */
 #define ASOT_FLAG_NONFINITE_OUTPUT 16u /* a distance came out NaN/Inf                            */
+#define ASOT_FLAG_SOFT_FALLBACK    32u /* a soft code was all zero -> uniform row (warning) */
 
 /* Distance-matrix tiling (step a4).  Distributions are grouped in blocks of 16; block pairs
  * (bi <= bj) are enumerated row-major over the upper triangle of the block grid; each block
@@ -153,6 +154,45 @@ asot_status asot_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_
  * writes pair (i_out[s], j_out[s]) and valid_out[s] (1 iff i < j < n_dist).  Host pointers. */
 asot_status asot_tile_pairs_host(int64_t n_dist, int64_t tile_begin, int64_t tile_end,
                                  int32_t* i_out, int32_t* j_out, uint8_t* valid_out);
+
+/* ---- soft / near-one-hot mappings (inference; parameters are inputs) ----
+ * Both compute a code z_p on the simplex for every point and the mapped marginals
+ * H[i, :] = sum_{p in i} w_p z_p (Eq. (5), 1/n dropped: R#1), accumulated in fp64 in point
+ * order and rounded to f32 -- the same [n_dist, n_anchors] layout asot_distance_matrix takes as
+ * hist_in.  points / offsets / offsets_host / weights / status as in asot_map_to_anchors;
+ * 1 <= dim <= 128, 1 <= n_anchors <= 1024, 1 <= hidden <= 256.  codes_out [T, n_anchors] f32 or
+ * NULL receives every z_p.  An all-zero code falls back to the uniform row 1/K and ORs
+ * ASOT_FLAG_SOFT_FALLBACK.  All pointers are device pointers owned by the caller.
+ *
+ * ASOT-ML (Table 4): z = |o| / ||o||_1, o = relu(x W1 + b1) W2 + b2 with
+ *   W1 [dim, hidden], b1 [hidden], W2 [hidden, n_anchors], b2 [n_anchors] (row-major f32). */
+asot_status asot_map_soft_ml(const float* points, const int64_t* offsets,
+                             const int64_t* offsets_host, const float* weights, int64_t n_dist,
+                             int32_t dim, int32_t n_anchors, int32_t hidden, const float* W1,
+                             const float* b1, const float* W2, const float* b2, float* hist_out,
+                             float* codes_out, uint32_t* status, void* stream);
+
+/* ASOT-DL near-one-hot encoder (Eqs. (8)(9); appendix; Table 4):
+ *   lambda_p = softplus(relu(x V1 + c1) . v2 + c2[0]); z^(0) = 0; n_layers times
+ *   z <- max(0, z - W^T (W z - x) - lambda_p) with W = dictionary^T (dictionary [n_anchors, dim]
+ *   row-major: row u = anchor w_u); finally z / sum(z).  Step size 1 presumes
+ *   ||W||_2 <= 1 (R#28); the library does not rescale.  V1 [dim, hidden], c1 [hidden],
+ *   v2 [hidden], c2 [1]; n_layers >= 1. */
+asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
+                             const int64_t* offsets_host, const float* weights, int64_t n_dist,
+                             int32_t dim, const float* dictionary, int32_t n_anchors,
+                             int32_t n_layers, int32_t hidden, const float* V1, const float* c1,
+                             const float* v2, const float* c2, float* hist_out, float* codes_out,
+                             uint32_t* status, void* stream);
+
+/* ASOT-ML anchor cost: C_s[u, v] = ||M w_u - M w_v||_2, M [h, dim] row-major, anchors
+ * [n_anchors, dim]; bitwise symmetric, zero diagonal.  normalize != 0 divides by the max entry
+ * (R#29; the max becomes exactly 1).  cost_out [n_anchors, n_anchors] f32 device; workspace of
+ * asot_mahalanobis_workspace_bytes(n_anchors, h) device bytes. */
+asot_status asot_mahalanobis_cost(const float* anchors, int32_t n_anchors, int32_t dim,
+                                  const float* M, int32_t h, int32_t normalize, float* cost_out,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+size_t asot_mahalanobis_workspace_bytes(int32_t n_anchors, int32_t h);
 
 /* Precision actually used for a given K and request (TF32 covers K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);

@@ -39,6 +39,12 @@ _SIGS = {
     "asot_distance_matrix_host_workspace_bytes": (c_size, [c_i64, c_i64, c_i32, c_i32, c_i32]),
     "asot_unpack_tiles": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i32, c_vp]),
     "asot_tile_pairs_host": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "asot_map_soft_ml": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                 c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "asot_map_soft_dl": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
+                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "asot_mahalanobis_cost": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "asot_mahalanobis_workspace_bytes": (c_size, [c_i32, c_i32]),
     "asot_profile_enable": (c_i32, [c_i32]),
     "asot_profile_read": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "asot_profile_read_kernel": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),

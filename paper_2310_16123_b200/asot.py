@@ -24,6 +24,7 @@ FLAG_BAD_MASS = 2
 FLAG_NONFINITE_INPUT = 4
 FLAG_DENOM_CLAMPED = 8
 FLAG_NONFINITE_OUTPUT = 16
+FLAG_SOFT_FALLBACK = 32
 
 _STATUS_EXC = {1: ValueError, 2: ValueError, 3: FloatingPointError, 4: RuntimeError,
                5: NotImplementedError, 6: MemoryError}
@@ -68,6 +69,12 @@ def _need_cuda(*ts):
             raise ValueError("device tensors (cuda) are required; there is no CPU path")
 
 
+def _need_f32(*ts):
+    for t in ts:
+        if t is not None and t.dtype != torch.float32:
+            raise ValueError(f"float32 tensors are required (got {t.dtype})")
+
+
 def num_tiles(n_dist: int) -> int:
     return int(_lib_handle().asot_num_tiles(int(n_dist)))
 
@@ -103,7 +110,7 @@ def new_status(device=None) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device or "cuda")
 
 
-def check_status(status, allow: int = FLAG_DENOM_CLAMPED) -> int:
+def check_status(status, allow: int = FLAG_DENOM_CLAMPED | FLAG_SOFT_FALLBACK) -> int:
     """Raise on data-dependent failures the kernels flagged (call after synchronising)."""
     v = int(status.item()) if isinstance(status, torch.Tensor) else int(status)
     bad = v & ~allow
@@ -150,6 +157,7 @@ def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.T
                    status: Optional[torch.Tensor] = None, stream=None):
     """Steps a2 + a3: returns (assign [T] int32, H [N, K] f32, status)."""
     _need_cuda(points, offsets, weights, anchors)
+    _need_f32(points, weights, anchors)
     oh = _host_offsets(offsets, offsets_host)
     N = oh.shape[0] - 1
     T = int(oh[-1])
@@ -161,6 +169,68 @@ def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.T
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(anchors), int(K),
         _ptr(assign), _ptr(H), _ptr(st), _stream(stream)))
     return assign[:T], H, st
+
+
+def _soft_common(points, offsets, weights, offsets_host, K, status, want_codes):
+    _need_cuda(points, offsets, weights)
+    oh = _host_offsets(offsets, offsets_host)
+    N = oh.shape[0] - 1
+    T = int(oh[-1])
+    H = torch.empty((N, K), dtype=torch.float32, device=points.device)
+    codes = torch.empty((max(T, 1), K), dtype=torch.float32, device=points.device) if want_codes else None
+    st = new_status(points.device) if status is None else status
+    return oh, N, T, H, codes, st
+
+
+def map_soft_ml(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
+                W1: torch.Tensor, b1: torch.Tensor, W2: torch.Tensor, b2: torch.Tensor,
+                offsets_host: Optional[np.ndarray] = None, want_codes: bool = False,
+                status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-1 ASOT-ML mapping: codes |MLP(x)| / l1 and H = Z^T a per distribution.
+    Returns (H [N, K], codes [T, K] or None, status)."""
+    _need_cuda(W1, b1, W2, b2)
+    _need_f32(points, weights, W1, b1, W2, b2)
+    d, hidden = W1.shape
+    K = int(W2.shape[1])
+    oh, N, T, H, codes, st = _soft_common(points, offsets, weights, offsets_host, K, status, want_codes)
+    _check(_lib_handle().asot_map_soft_ml(
+        _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), K, int(hidden), _ptr(W1),
+        _ptr(b1), _ptr(W2), _ptr(b2), _ptr(H), _ptr(codes), _ptr(st), _stream(stream)))
+    return H, (codes[:T] if codes is not None else None), st
+
+
+def map_soft_dl(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
+                dictionary: torch.Tensor, V1: torch.Tensor, c1: torch.Tensor, v2: torch.Tensor,
+                c2: torch.Tensor, n_layers: int = 20, offsets_host: Optional[np.ndarray] = None,
+                want_codes: bool = False, status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-1 ASOT-DL near-one-hot encoder (Eq. (9), L layers) and H = Z^T a per distribution.
+    Returns (H [N, K], codes [T, K] or None, status)."""
+    _need_cuda(dictionary, V1, c1, v2, c2)
+    _need_f32(points, weights, dictionary, V1, c1, v2, c2)
+    K, d = dictionary.shape
+    hidden = int(V1.shape[1])
+    oh, N, T, H, codes, st = _soft_common(points, offsets, weights, offsets_host, int(K), status,
+                                          want_codes)
+    _check(_lib_handle().asot_map_soft_dl(
+        _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(dictionary), int(K),
+        int(n_layers), hidden, _ptr(V1), _ptr(c1), _ptr(v2), _ptr(c2), _ptr(H), _ptr(codes),
+        _ptr(st), _stream(stream)))
+    return H, (codes[:T] if codes is not None else None), st
+
+
+def mahalanobis_cost(anchors: torch.Tensor, M: torch.Tensor, normalize: bool = True,
+                     workspace: Optional[Workspace] = None, stream=None) -> torch.Tensor:
+    """ASOT-ML anchor cost C_s[u, v] = ||M w_u - M w_v||_2, optionally / max."""
+    _need_cuda(anchors, M)
+    _need_f32(anchors, M)
+    K, d = anchors.shape
+    h = int(M.shape[0])
+    C = torch.empty((K, K), dtype=torch.float32, device=anchors.device)
+    L = _lib_handle()
+    ws = _ws(workspace, anchors.device).get(L.asot_mahalanobis_workspace_bytes(int(K), h))
+    _check(L.asot_mahalanobis_cost(_ptr(anchors), int(K), int(d), _ptr(M), h, int(bool(normalize)),
+                                   _ptr(C), _ptr(ws), ws.numel(), _stream(stream)))
+    return C
 
 
 def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: int,
@@ -195,6 +265,7 @@ def distance_matrix(points: Optional[torch.Tensor], offsets: Optional[torch.Tens
     """Full pipeline a1-a6.  Returns the N x N matrix (when want_matrix) and/or fills `packed`
     ([(tile_end - tile_begin) * 128] slot-ordered results) for the tile range."""
     _need_cuda(cost, hist, points, offsets, weights, anchors)
+    _need_f32(cost, hist, points, weights, anchors)
     L = _lib_handle()
     K = int(cost.shape[0])
     if hist is None:

@@ -252,6 +252,77 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
   return ASOT_OK;
 }
 
+// Shared argument checks of the soft mappings (NEXT-1).
+static asot_status check_soft(const float* points, const int64_t* offsets, const int64_t* offsets_host,
+                              const float* weights, int64_t n_dist, int32_t dim, int32_t n_anchors,
+                              int32_t hidden, const float* hist_out, const uint32_t* status) {
+  ASOT_CHECK_ARG(points && offsets && offsets_host && weights && hist_out && status,
+                 "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1 && dim >= 1 && n_anchors >= 1 && hidden >= 1, "sizes must be >= 1");
+  if (dim > asot::kMaxDim) return fail(ASOT_ERR_UNSUPPORTED, "dim > 128 is not supported");
+  if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
+  if (hidden > 256) return fail(ASOT_ERR_UNSUPPORTED, "hidden > 256 is not supported");
+  ASOT_CHECK_ARG(offsets_host[0] == 0, "offsets[0] must be 0");
+  for (int64_t i = 0; i < n_dist; ++i)
+    ASOT_CHECK_ARG(offsets_host[i + 1] >= offsets_host[i], "offsets must be non-decreasing");
+  return ASOT_OK;
+}
+
+asot_status asot_map_soft_ml(const float* points, const int64_t* offsets,
+                             const int64_t* offsets_host, const float* weights, int64_t n_dist,
+                             int32_t dim, int32_t n_anchors, int32_t hidden, const float* W1,
+                             const float* b1, const float* W2, const float* b2, float* hist_out,
+                             float* codes_out, uint32_t* status, void* stream) {
+  g_launches = 0;
+  asot_status st = check_soft(points, offsets, offsets_host, weights, n_dist, dim, n_anchors,
+                              hidden, hist_out, status);
+  if (st != ASOT_OK) return st;
+  ASOT_CHECK_ARG(W1 && b1 && W2 && b2, "null pointer argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope prof(ASOT_PROF_MAP, s);
+  ASOT_LAUNCH(asot::launch_soft_map_ml(points, offsets, weights, n_dist, dim, n_anchors, hidden,
+                                       W1, b1, W2, b2, hist_out, codes_out, status, s));
+  return ASOT_OK;
+}
+
+asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
+                             const int64_t* offsets_host, const float* weights, int64_t n_dist,
+                             int32_t dim, const float* dictionary, int32_t n_anchors,
+                             int32_t n_layers, int32_t hidden, const float* V1, const float* c1,
+                             const float* v2, const float* c2, float* hist_out, float* codes_out,
+                             uint32_t* status, void* stream) {
+  g_launches = 0;
+  asot_status st = check_soft(points, offsets, offsets_host, weights, n_dist, dim, n_anchors,
+                              hidden, hist_out, status);
+  if (st != ASOT_OK) return st;
+  ASOT_CHECK_ARG(dictionary && V1 && c1 && v2 && c2, "null pointer argument");
+  ASOT_CHECK_ARG(n_layers >= 1, "n_layers must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope prof(ASOT_PROF_MAP, s);
+  ASOT_LAUNCH(asot::launch_soft_map_dl(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
+                                       n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
+                                       status, s));
+  return ASOT_OK;
+}
+
+size_t asot_mahalanobis_workspace_bytes(int32_t n_anchors, int32_t h) {
+  return n_anchors < 1 || h < 1 ? 0 : (size_t)n_anchors * h * 4;
+}
+
+asot_status asot_mahalanobis_cost(const float* anchors, int32_t n_anchors, int32_t dim,
+                                  const float* M, int32_t h, int32_t normalize, float* cost_out,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(anchors && M && cost_out, "null pointer argument");
+  ASOT_CHECK_ARG(n_anchors >= 1 && dim >= 1 && h >= 1, "sizes must be >= 1");
+  if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
+  if (!workspace || workspace_bytes < asot_mahalanobis_workspace_bytes(n_anchors, h))
+    return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  ASOT_LAUNCH(asot::launch_mahalanobis_cost(anchors, n_anchors, dim, M, h, normalize != 0,
+                                            (float*)workspace, cost_out, (cudaStream_t)stream));
+  return ASOT_OK;
+}
+
 size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
   Carver cv{nullptr, 0};
   (void)prec;

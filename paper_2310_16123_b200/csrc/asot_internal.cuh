@@ -143,6 +143,17 @@ cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_
 cudaError_t launch_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
                                 int64_t tile_end, float* mat, cudaStream_t s);
 cudaError_t launch_zero_diag(float* mat, int64_t n_dist, cudaStream_t s);
+cudaError_t launch_soft_map_ml(const float* points, const int64_t* offsets, const float* weights,
+                               int64_t n_dist, int dim, int K, int hidden, const float* W1,
+                               const float* b1, const float* W2, const float* b2, float* H,
+                               float* codes, uint32_t* status, cudaStream_t s);
+cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, const float* weights,
+                               int64_t n_dist, int dim, const float* dict, int K, int n_layers,
+                               int hidden, const float* V1, const float* c1, const float* v2,
+                               const float* c2, float* H, float* codes, uint32_t* status,
+                               cudaStream_t s);
+cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
+                                    bool normalize, float* Y, float* C, cudaStream_t s);
 
 inline int kpad32(int K) { return (K + 31) & ~31; }
 

@@ -1,0 +1,377 @@
+// asot_soft_map.cu -- SURVEY §8(f) NEXT-1: soft / near-one-hot mappings P (inference) fused with
+// the mapped-marginal reduction a' = Z^T a, plus the ASOT-ML Mahalanobis anchor cost.
+//
+// ASOT-ML (Table 4; readings R#24, R#25): z = |MLP(x)| / || MLP(x) ||_1 with the
+//   MLP d -> hidden -> K (ReLU hidden layer); an all-zero row falls back to the uniform row and
+//   raises ASOT_FLAG_SOFT_FALLBACK.
+// ASOT-DL (Eq. (9), appendix P:500-538 step size 1; Table 4; R#26-R#28):
+//   lambda = softplus(MLP(x)) (d -> hidden -> 1), z^(0) = 0, n_layers x
+//   z <- max(0, z - W^T (W z - x) - lambda), then z / sum(z) (uniform fallback, flagged).
+// Both: H[i, :] = sum_{p in i} w_p z_p (Eq. (5) P:100 with the 1/n factor dropped, R#1), the
+//   same N x K layout the Sinkhorn kernels read, so the soft H feeds asot_distance_matrix(hist_in).
+//
+// Kernel: one CTA per distribution, point tiles of kPT = 16 points staged in shared memory; every
+// matrix product runs on CUDA cores in fp32 (one output column per thread for all 16 points of
+// the tile, weights read coalesced from L2, activations broadcast from SMEM).  The DL dictionary
+// is SMEM-resident when it fits (K (d+1) 4 B <= 100 KB), else streamed through SMEM in 64-row
+// chunks every layer.  The per-distribution sum of w_p z_p is accumulated in fp64 in SMEM in
+// point order (thread j owns bin j), so H is deterministic.
+#include <cfloat>
+#include <cmath>
+
+#include "asot_internal.cuh"
+
+namespace asot {
+namespace soft {
+
+constexpr int kThreads = 256;
+constexpr int kPT = 16;            // points per tile
+constexpr int kChunkRows = 64;     // dictionary rows per streamed chunk
+constexpr size_t kResidentBytes = 100 * 1024;
+
+struct Params {
+  const float* points;
+  const int64_t* offsets;
+  const float* weights;
+  int64_t n_dist;
+  int dim;
+  int K;
+  int hidden;
+  // ML mapper (mode 0): W1 [dim, hidden], b1 [hidden], W2 [hidden, K], b2 [K]
+  // DL lambda net (mode 1): W1 = V1 [dim, hidden], b1 = c1, W2 = v2 [hidden], b2 = c2 [1]
+  const float* W1;
+  const float* b1;
+  const float* W2;
+  const float* b2;
+  const float* dict;   // DL: [K, dim] rows = anchors (the paper's W = dict^T)
+  int n_layers;
+  int wrows;           // dictionary rows per SMEM chunk (K when resident)
+  float* H;            // [n_dist, K]
+  float* codes;        // [T, K] or null
+  uint32_t* status;
+};
+
+__device__ __forceinline__ float softplus_f(float t) { return t > 30.0f ? t : log1pf(expf(t)); }
+
+// Hidden layer of either MLP for the tile: Hs[p][c] = relu(b[c] + sum_k Xs[p][k] W[k][c]).
+template <int DP>
+__device__ __forceinline__ void hidden_layer(const Params& P, const float* Xs, float* Hs) {
+  for (int c = threadIdx.x; c < P.hidden; c += kThreads) {
+    float a[kPT];
+    const float b = P.b1[c];
+#pragma unroll
+    for (int p = 0; p < kPT; ++p) a[p] = b;
+    for (int k = 0; k < P.dim; ++k) {
+      const float w = __ldg(P.W1 + (int64_t)k * P.hidden + c);
+#pragma unroll
+      for (int p = 0; p < kPT; ++p) a[p] = fmaf(Xs[p * DP + k], w, a[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < kPT; ++p) Hs[p * P.hidden + c] = fmaxf(a[p], 0.0f);
+  }
+}
+
+// Warp w reduces rows p = w, w + 8 of Zs[kPT][K] into rs[p].
+__device__ __forceinline__ void row_sums(const float* Zs, int K, float* rs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int p = warp; p < kPT; p += kThreads / 32) {
+    float s = 0.0f;
+    for (int j = lane; j < K; j += 32) s += Zs[p * K + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) rs[p] = s;
+  }
+}
+
+template <int MODE, int DP>
+__global__ void __launch_bounds__(kThreads)
+soft_map_kernel(Params P) {
+  constexpr int WS = DP + 1;  // dictionary row stride in SMEM (odd: conflict-free column reads)
+  extern __shared__ double soft_smem[];
+  const int K = P.K;
+  double* acc = soft_smem;                        // [K] fp64 per-bin sums
+  float* Xs = (float*)(acc + K);                  // [kPT][DP]
+  float* Rs = Xs + kPT * DP;                      // [kPT][DP] (DL residual)
+  float* Hs = Rs + kPT * DP;                      // [kPT][hidden]
+  float* Zs = Hs + kPT * P.hidden;                // [kPT][K]
+  float* misc = Zs + kPT * K;                     // lam[kPT], rs[kPT], wts[kPT]
+  float* lam = misc;
+  float* rs = misc + kPT;
+  float* wts = misc + 2 * kPT;
+  float* Wc = misc + 3 * kPT;                     // [wrows][WS] dictionary chunk (DL)
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t i = blockIdx.x;
+  const int64_t s = P.offsets[i], e = P.offsets[i + 1];
+  const bool resident = P.wrows >= K;
+
+  for (int j = tid; j < K; j += kThreads) acc[j] = 0.0;
+  if (MODE == 1 && resident) {
+    for (int x = tid; x < K * DP; x += kThreads) {
+      const int j = x / DP, k = x % DP;
+      Wc[j * WS + k] = k < P.dim ? P.dict[(int64_t)j * P.dim + k] : 0.0f;
+    }
+  }
+  bool nonfinite = false, negative = false;
+  double msum = 0.0;
+
+  for (int64_t t0 = s; t0 < e; t0 += kPT) {
+    const int np = (int)min((int64_t)kPT, e - t0);
+    __syncthreads();  // previous tile's readers are done
+    for (int x = tid; x < kPT * DP; x += kThreads) {
+      const int p = x / DP, k = x % DP;
+      float v = 0.0f;
+      if (p < np && k < P.dim) {
+        v = P.points[(t0 + p) * P.dim + k];
+        nonfinite |= !isfinite(v);
+      }
+      Xs[x] = v;
+    }
+    if (tid < kPT) {
+      float w = tid < np ? P.weights[t0 + tid] : 0.0f;
+      if (tid < np) {
+        nonfinite |= !isfinite(w);
+        negative |= w < 0.0f;
+        msum += (double)w;
+      }
+      wts[tid] = w;
+    }
+    __syncthreads();
+    hidden_layer<DP>(P, Xs, Hs);
+    __syncthreads();
+
+    if (MODE == 0) {
+      // ---- ASOT-ML: output layer, |.|
+      for (int j = tid; j < K; j += kThreads) {
+        float a[kPT];
+        const float b = P.b2[j];
+#pragma unroll
+        for (int p = 0; p < kPT; ++p) a[p] = b;
+        for (int c = 0; c < P.hidden; ++c) {
+          const float w = __ldg(P.W2 + (int64_t)c * K + j);
+#pragma unroll
+          for (int p = 0; p < kPT; ++p) a[p] = fmaf(Hs[p * P.hidden + c], w, a[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < kPT; ++p) Zs[p * K + j] = fabsf(a[p]);
+      }
+    } else {
+      // ---- ASOT-DL: lambda_p = softplus(v2 . h_p + c2), warp per point
+      const int warp = tid >> 5;
+      for (int p = warp; p < kPT; p += kThreads / 32) {
+        float sdot = 0.0f;
+        for (int c = lane; c < P.hidden; c += 32) sdot = fmaf(Hs[p * P.hidden + c], __ldg(P.W2 + c), sdot);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+        if (lane == 0) lam[p] = softplus_f(sdot + P.b2[0]);
+      }
+      for (int x = tid; x < kPT * K; x += kThreads) Zs[x] = 0.0f;   // z^(0) = 0 (R#27)
+      __syncthreads();
+      // R phase ownership: column k = tid % DP, points p = tid / DP + m * (kThreads / DP)
+      constexpr int PG = kThreads / DP > kPT ? kPT : kThreads / DP;   // point groups
+      constexpr int M = kPT / PG;                                       // points per thread
+      const int rk = tid % DP, rp0 = tid / DP;
+      const bool r_active = rp0 < PG;
+      for (int layer = 0; layer < P.n_layers; ++layer) {
+        // r = W z - x  (W z)_k = sum_j dict[j][k] z_j
+        float racc[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) racc[m] = 0.0f;
+        for (int c0 = 0; c0 < K; c0 += P.wrows) {
+          const int nr = min(P.wrows, K - c0);
+          if (!resident) {
+            __syncthreads();
+            for (int x = tid; x < nr * DP; x += kThreads) {
+              const int j = x / DP, k = x % DP;
+              Wc[j * WS + k] = k < P.dim ? P.dict[(int64_t)(c0 + j) * P.dim + k] : 0.0f;
+            }
+            __syncthreads();
+          }
+          if (r_active) {
+            for (int j = 0; j < nr; ++j) {
+              const float w = Wc[j * WS + rk];
+#pragma unroll
+              for (int m = 0; m < M; ++m) racc[m] = fmaf(Zs[(rp0 + m * PG) * K + c0 + j], w, racc[m]);
+            }
+          }
+        }
+        if (r_active) {
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            const int p = rp0 + m * PG;
+            Rs[p * DP + rk] = racc[m] - Xs[p * DP + rk];
+          }
+        }
+        __syncthreads();
+        // g = W^T r, z <- max(0, z - g - lambda)
+        for (int c0 = 0; c0 < K; c0 += P.wrows) {
+          const int nr = min(P.wrows, K - c0);
+          if (!resident) {
+            __syncthreads();
+            for (int x = tid; x < nr * DP; x += kThreads) {
+              const int j = x / DP, k = x % DP;
+              Wc[j * WS + k] = k < P.dim ? P.dict[(int64_t)(c0 + j) * P.dim + k] : 0.0f;
+            }
+            __syncthreads();
+          }
+          for (int x = tid; x < nr * (kPT / 4); x += kThreads) {
+            const int j = x % nr, p0 = (x / nr) * 4;
+            float g[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            for (int k = 0; k < DP; ++k) {
+              const float w = Wc[j * WS + k];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) g[q] = fmaf(Rs[(p0 + q) * DP + k], w, g[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float* z = &Zs[(p0 + q) * K + c0 + j];
+              *z = fmaxf(0.0f, (*z - g[q]) - lam[p0 + q]);
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    row_sums(Zs, K, rs);
+    __syncthreads();
+    if (tid < np && !(rs[tid] > 0.0f)) atomicOr(P.status, ASOT_FLAG_SOFT_FALLBACK);
+    const float unif = 1.0f / (float)K;
+    for (int j = tid; j < K; j += kThreads) {
+      double a = acc[j];
+      for (int p = 0; p < np; ++p) {  // point order
+        const float z = rs[p] > 0.0f ? Zs[p * K + j] / rs[p] : unif;
+        if (P.codes) P.codes[(t0 + p) * K + j] = z;
+        a += (double)wts[p] * (double)z;
+      }
+      acc[j] = a;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < K; j += kThreads) P.H[i * K + j] = (float)acc[j];
+
+  // status: per-thread input checks, then the mass checks of the one-hot histogram kernel
+  if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(P.status, ASOT_FLAG_NONFINITE_INPUT);
+  if (__syncthreads_or(negative) && tid == 0) atomicOr(P.status, ASOT_FLAG_BAD_MASS);
+  if (tid < kPT) {  // threads < kPT hold the weight partial sums
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) msum += __shfl_xor_sync(0x0000ffffu, msum, o, 16);
+    if (tid == 0) {
+      if (e <= s) atomicOr(P.status, ASOT_FLAG_EMPTY_DIST);
+      else if (fabs(msum - 1.0) > 1e-5) atomicOr(P.status, ASOT_FLAG_BAD_MASS);
+    }
+  }
+}
+
+size_t smem_bytes(int mode, int dp, int K, int hidden, int wrows) {
+  size_t b = (size_t)K * 8 + (size_t)(2 * kPT * dp + kPT * hidden + kPT * K + 3 * kPT) * 4;
+  if (mode == 1) b += (size_t)wrows * (dp + 1) * 4;
+  return b;
+}
+
+template <int MODE, int DP>
+cudaError_t launch_dp(Params P, cudaStream_t s) {
+  if (MODE == 1) {
+    P.wrows = (size_t)P.K * (DP + 1) * 4 <= kResidentBytes ? P.K : kChunkRows;
+  } else {
+    P.wrows = 0;
+  }
+  const size_t smem = smem_bytes(MODE, DP, P.K, P.hidden, P.wrows);
+  cudaError_t e = cudaFuncSetAttribute(soft_map_kernel<MODE, DP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  soft_map_kernel<MODE, DP><<<(unsigned)P.n_dist, kThreads, smem, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_mode(const Params& P, cudaStream_t s) {
+  if (P.dim <= 8) return launch_dp<MODE, 8>(P, s);
+  if (P.dim <= 16) return launch_dp<MODE, 16>(P, s);
+  if (P.dim <= 32) return launch_dp<MODE, 32>(P, s);
+  if (P.dim <= 64) return launch_dp<MODE, 64>(P, s);
+  return launch_dp<MODE, 128>(P, s);
+}
+
+// ---------------------------------------------------------------- Mahalanobis anchor cost
+// Y[u][r] = sum_k M[r][k] w_u[k]; C[u][v] = ||Y_u - Y_v||_2.  C[v][u] evaluates the
+// negated differences in the same order, so C is bitwise symmetric with an exact zero diagonal.
+__global__ void mahalanobis_project_kernel(const float* __restrict__ W, int K, int d,
+                                           const float* __restrict__ M, int h, float* __restrict__ Y) {
+  const int64_t total = (int64_t)K * h;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(x / h), r = (int)(x % h);
+    float a = 0.0f;
+    for (int k = 0; k < d; ++k) a = fmaf(M[(int64_t)r * d + k], W[(int64_t)u * d + k], a);
+    Y[x] = a;
+  }
+}
+
+__global__ void mahalanobis_pair_kernel(const float* __restrict__ Y, int K, int h, float* __restrict__ C) {
+  const int64_t total = (int64_t)K * K;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(x / K), v = (int)(x % K);
+    float a = 0.0f;
+    for (int r = 0; r < h; ++r) {
+      const float t = Y[(int64_t)u * h + r] - Y[(int64_t)v * h + r];
+      a = fmaf(t, t, a);
+    }
+    C[x] = u == v ? 0.0f : sqrtf(a);
+  }
+}
+
+// Single CTA: max over C, then C /= max (max entry becomes exactly 1).
+__global__ void normalize_by_max_kernel(float* C, int64_t n) {
+  __shared__ float red[32];
+  float m = 0.0f;
+  for (int64_t x = threadIdx.x; x < n; x += blockDim.x) m = fmaxf(m, C[x]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  m = red[0];
+  if (m > 0.0f)
+    for (int64_t x = threadIdx.x; x < n; x += blockDim.x) C[x] = C[x] / m;
+}
+
+}  // namespace soft
+
+cudaError_t launch_soft_map_ml(const float* points, const int64_t* offsets, const float* weights,
+                               int64_t n_dist, int dim, int K, int hidden, const float* W1,
+                               const float* b1, const float* W2, const float* b2, float* H,
+                               float* codes, uint32_t* status, cudaStream_t s) {
+  soft::Params P{points, offsets, weights, n_dist, dim, K, hidden, W1, b1, W2, b2,
+                 nullptr, 0, 0, H, codes, status};
+  return soft::launch_mode<0>(P, s);
+}
+
+cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, const float* weights,
+                               int64_t n_dist, int dim, const float* dict, int K, int n_layers,
+                               int hidden, const float* V1, const float* c1, const float* v2,
+                               const float* c2, float* H, float* codes, uint32_t* status,
+                               cudaStream_t s) {
+  soft::Params P{points, offsets, weights, n_dist, dim, K, hidden, V1, c1, v2, c2,
+                 dict, n_layers, 0, H, codes, status};
+  return soft::launch_mode<1>(P, s);
+}
+
+cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
+                                    bool normalize, float* Y, float* C, cudaStream_t s) {
+  const int64_t ny = (int64_t)K * h, nc = (int64_t)K * K;
+  soft::mahalanobis_project_kernel<<<(unsigned)std::min<int64_t>((ny + 255) / 256, 148 * 16), 256, 0, s>>>(
+      anchors, K, d, M, h, Y);
+  soft::mahalanobis_pair_kernel<<<(unsigned)std::min<int64_t>((nc + 255) / 256, 148 * 16), 256, 0, s>>>(
+      Y, K, h, C);
+  if (normalize) soft::normalize_by_max_kernel<<<1, 1024, 0, s>>>(C, nc);
+  return cudaGetLastError();
+}
+
+}  // namespace asot
