@@ -84,3 +84,15 @@ def make_dl_inputs(cfg: str = "c2", n_dist: Optional[int] = None, iters: Optiona
     inp = AsotInputs(base.name + "-dl", points, base.offsets, base.weights, dictionary,
                      normalized_sqeuclid_cost(dictionary), base.eps, base.iters)
     return inp, model
+
+
+def make_kmeans_draws(points: np.ndarray, K: int, iters: int, batch: int,
+                      seed: int = 303) -> tuple[np.ndarray, np.ndarray]:
+    """NEXT-2 random draws of mini-batch k-means (passed to both sides, R#30): Forgy
+    initialisation (K distinct point indices -> their coordinates) and iters x batch point
+    indices drawn with replacement."""
+    rng = np.random.default_rng(seed)
+    T = points.shape[0]
+    init_idx = rng.choice(T, size=K, replace=False)
+    batch_idx = rng.integers(0, T, size=(iters, batch), dtype=np.int64)
+    return np.ascontiguousarray(points[init_idx]), np.ascontiguousarray(batch_idx)
