@@ -230,6 +230,9 @@ def workload_config(inp, args, world):
         "n_anchors": inp.n_anchors, "iters": inp.iters, "pairs": inp.n_pairs,
         "precision": args.precision, "l2_flush": "256 MiB write between timed steps",
         "parallelism": f"pair-tiles x{world}",
+        "mapping": getattr(args, "mapping", "onehot"),
+        "anchors": (getattr(args, "anchors", "seeded") if getattr(args, "anchors", "seeded") == "seeded"
+                    else f"kmeans (iters={args.kmeans_iters}, batch={args.kmeans_batch}, in every step)"),
     }
 
 
@@ -243,6 +246,11 @@ def main():
     # default: configs[2] (c3), the config BASELINE.json quotes "at 1/2/4/8 GPUs" like the metric
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--anchors", default="seeded", choices=["seeded", "kmeans"],
+                    help="seeded anchors (the north-star path) or NEXT-2 ASOT-k: anchors learned "
+                         "inside every step by mini-batch k-means (Forgy init + batch draws seeded)")
+    ap.add_argument("--kmeans-iters", type=int, default=50)
+    ap.add_argument("--kmeans-batch", type=int, default=4096)
     ap.add_argument("--mapping", default="onehot", choices=["onehot", "ml", "dl"],
                     help="P: one-hot nearest anchor (the north-star path), or the NEXT-1 soft "
                          "mappings ASOT-ML / ASOT-DL (seeded parameters)")
@@ -294,8 +302,16 @@ def main():
     n_tiles = asot.num_tiles(inp.n_dist)
     launches = [0]
 
-    if args.mapping != "onehot" and world > 1:
-        raise SystemExit("--mapping ml/dl is single-GPU in this build")
+    if (args.mapping != "onehot" or args.anchors != "seeded") and world > 1:
+        raise SystemExit("--mapping ml/dl and --anchors kmeans are single-GPU in this build")
+    km_events = []
+    if args.anchors == "kmeans":
+        if args.mapping != "onehot":
+            raise SystemExit("--anchors kmeans runs with the one-hot mapping (ASOT-k)")
+        from asot_inputs.soft import make_kmeans_draws
+        km_init, km_idx = make_kmeans_draws(inp.points, inp.n_anchors, args.kmeans_iters,
+                                            args.kmeans_batch)
+        km_init_d, km_idx_d = t(km_init), t(km_idx)
     if args.mapping == "ml":
         m = soft_model
         mW1, mb1, mW2, mb2, mM = t(m.W1), t(m.b1), t(m.W2), t(m.b2), t(m.M)
@@ -321,6 +337,21 @@ def main():
             launches[0] += asot.last_launch_count()
             asot.distance_matrix(None, None, None, None, cst, float(inp.eps), inp.iters,
                                  precision=prec, hist=H, out=Dbuf, cost_max=cmax, status=status,
+                                 workspace=ws)
+            launches[0] += asot.last_launch_count()
+            return Dbuf
+    elif args.anchors == "kmeans":
+        def step():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, A, _, _ = asot.kmeans_minibatch(pts, km_init_d, km_idx_d, status=status)
+            e1.record()
+            km_events.append((e0, e1))
+            launches[0] += asot.last_launch_count()
+            C = asot.sqeuclid_cost(A)
+            launches[0] += 2
+            asot.distance_matrix(pts, offs, w, A, C, float(inp.eps), inp.iters, precision=prec,
+                                 out=Dbuf, offsets_host=inp.offsets, cost_max=1.0, status=status,
                                  workspace=ws)
             launches[0] += asot.last_launch_count()
             return Dbuf
@@ -474,10 +505,22 @@ def main():
                 "note": "ALU-bound by design (intensity 3Kd/(4d+8) >> FP32 ridge); fp32_pipe_frac = "
                         "2Kd lane-ops per point / (148 SMs x 128 lanes x 1.965 GHz)"}
 
+    kmeans = None
+    if km_events:
+        timed = km_events[-args.steps:]
+        km_ms = sum(a.elapsed_time(b) for a, b in timed) / len(timed)
+        pts_assigned = args.kmeans_iters * args.kmeans_batch
+        kmeans = {"iters": args.kmeans_iters, "batch": args.kmeans_batch, "ms_per_step": km_ms,
+                  "points_assigned_per_s": pts_assigned / (km_ms / 1e3),
+                  "launches_per_step": 1 + 2 * args.kmeans_iters,
+                  "share_of_step": km_ms * len(timed) / max(tot_ms, 1e-9),
+                  "note": "per iteration: map_assign_kernel on the gathered batch + one update "
+                          "launch (K CTAs); launch-latency bound at these batch sizes"}
+
     # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
     # distributed public API with H2D / D2H inside the timed region (N > 1)
     e2e = None
-    if world == 1 and args.mapping != "onehot":
+    if world == 1 and (args.mapping != "onehot" or args.anchors != "seeded"):
         # soft mappings: the public Python API with pinned host inputs copied in and D copied out
         hp = torch.from_numpy(inp.points).pin_memory()
         hw_ = torch.from_numpy(inp.weights).pin_memory()
@@ -496,8 +539,10 @@ def main():
         e2e = {"value": P * len(e_ms) / (sum(e_ms) / 1e3), "unit": "pairs/s",
                "h2d_bytes_per_step": int(hp.numel() * 4 + hw_.numel() * 4 + ho.numel() * 8),
                "d2h_bytes_per_step": int(hD.numel() * 4),
-               "api": f"paper_2310_16123_b200.map_soft_{args.mapping} + distance_matrix(hist) "
-                      "(pinned host copies in, D out, wall clock)"}
+               "api": ("paper_2310_16123_b200.kmeans_minibatch + sqeuclid_cost + distance_matrix"
+                       if args.anchors == "kmeans" else
+                       f"paper_2310_16123_b200.map_soft_{args.mapping} + distance_matrix(hist)")
+                      + " (pinned host copies in, D out, wall clock)"}
     elif world == 1:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         hp, ho, hw, ha, hc = pin(inp.points), pin(inp.offsets), pin(inp.weights), pin(inp.anchors), pin(inp.cost)
@@ -548,7 +593,7 @@ def main():
                "api": "paper_2310_16123_b200.distributed (pinned host copies + D to host on rank 0)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.anchors == "seeded":
         v, sample = oracle_sample_rate(inp, args.cpu_budget, mapping=args.mapping, model=soft_model)
         cpu = {"value": v, "unit": "pairs/s", "cores": len(os.sched_getaffinity(0)),
                "kind": "oracle", "sample": sample}
@@ -560,7 +605,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "tf32" if eff == asot.TF32 else "f32", "data": "synthetic",
             "config": workload_config(inp, args, world),
-            "roofline": roofline, "mapping": mapping, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
             "wall_s_timed_region": wall,
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],

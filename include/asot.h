@@ -194,6 +194,29 @@ asot_status asot_mahalanobis_cost(const float* anchors, int32_t n_anchors, int32
                                   void* workspace, size_t workspace_bytes, void* stream);
 size_t asot_mahalanobis_workspace_bytes(int32_t n_anchors, int32_t h);
 
+/* ---- ASOT-k anchor learning (mini-batch k-means; Table 4) ----
+ * Runs `iters` iterations; iteration t uses the `batch` point indices batch_idx[t * batch ...]
+ * (device i64, 0 <= idx < n_points; the random draws are inputs):
+ *   assignment j*(x) against the f32 anchors (bit-exact vs the fp64 definition, lowest index on
+ *   ties, R#8); per-center batch sums in batch order in fp64; c_j <- (v_j c_j + S_j) / (v_j + m_j),
+ *   v_j <- v_j + m_j (Sculley's 1/v learning rate, R#31) in explicitly rounded fp64.
+ *   points     [n_points, dim] f32 device
+ *   centers    [n_anchors, dim] f64 device, in/out (initial centers in, learned centers out)
+ *   counts     [n_anchors] i64 device, in/out (0 for a fresh run)
+ *   anchors_out [n_anchors, dim] f32 device: the f32 copy of the centers (what P_o then uses)
+ *   assign_ws  [batch] i32 device scratch; status as in asot_map_to_anchors.
+ * Centers and counts are bit-identical to the oracle's for the same inputs. */
+asot_status asot_kmeans_minibatch(const float* points, int64_t n_points, int32_t dim,
+                                  int32_t n_anchors, const int64_t* batch_idx, int32_t batch,
+                                  int32_t iters, double* centers, int64_t* counts,
+                                  float* anchors_out, int32_t* assign_ws, uint32_t* status,
+                                  void* stream);
+
+/* Squared-Euclidean anchor cost of (learned) anchors: C_s[u, v] = ||w_u - w_v||^2 in fp32
+ * (bitwise symmetric, zero diagonal), divided by its max when normalize != 0 (R#7). */
+asot_status asot_sqeuclid_cost(const float* anchors, int32_t n_anchors, int32_t dim,
+                               int32_t normalize, float* cost_out, void* stream);
+
 /* Precision actually used for a given K and request (TF32 covers K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
 

@@ -233,6 +233,40 @@ def mahalanobis_cost(anchors: torch.Tensor, M: torch.Tensor, normalize: bool = T
     return C
 
 
+def kmeans_minibatch(points: torch.Tensor, init_centers: torch.Tensor, batch_idx: torch.Tensor,
+                     status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-2 ASOT-k anchor learning: mini-batch k-means.  batch_idx [iters, b]
+    int64 point indices (the random draws).  Returns (centers f64 [K, d], anchors f32 [K, d],
+    counts i64 [K], status)."""
+    _need_cuda(points, init_centers, batch_idx)
+    _need_f32(points)
+    if batch_idx.dtype != torch.int64:
+        raise ValueError("batch_idx must be int64")
+    T, d = points.shape
+    K = int(init_centers.shape[0])
+    iters, b = batch_idx.shape
+    centers = init_centers.to(torch.float64).contiguous().clone()
+    counts = torch.zeros(K, dtype=torch.int64, device=points.device)
+    anchors = torch.empty((K, d), dtype=torch.float32, device=points.device)
+    assign = torch.empty(max(int(b), 1), dtype=torch.int32, device=points.device)
+    st = new_status(points.device) if status is None else status
+    _check(_lib_handle().asot_kmeans_minibatch(
+        _ptr(points), int(T), int(d), K, _ptr(batch_idx), int(b), int(iters),
+        _ptr(centers), _ptr(counts), _ptr(anchors), _ptr(assign), _ptr(st), _stream(stream)))
+    return centers, anchors, counts, st
+
+
+def sqeuclid_cost(anchors: torch.Tensor, normalize: bool = True, stream=None) -> torch.Tensor:
+    """C_s[u, v] = ||w_u - w_v||^2 (/ max) of device anchors (R#7)."""
+    _need_cuda(anchors)
+    _need_f32(anchors)
+    K, d = anchors.shape
+    C = torch.empty((K, K), dtype=torch.float32, device=anchors.device)
+    _check(_lib_handle().asot_sqeuclid_cost(_ptr(anchors), int(K), int(d), int(bool(normalize)),
+                                            _ptr(C), _stream(stream)))
+    return C
+
+
 def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: int,
                       pair_i: torch.Tensor, pair_j: torch.Tensor, precision: int = TF32,
                       cost_max: Optional[float] = None, status: Optional[torch.Tensor] = None,

@@ -323,6 +323,42 @@ asot_status asot_mahalanobis_cost(const float* anchors, int32_t n_anchors, int32
   return ASOT_OK;
 }
 
+asot_status asot_kmeans_minibatch(const float* points, int64_t n_points, int32_t dim,
+                                  int32_t n_anchors, const int64_t* batch_idx, int32_t batch,
+                                  int32_t iters, double* centers, int64_t* counts,
+                                  float* anchors_out, int32_t* assign_ws, uint32_t* status,
+                                  void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(points && (batch_idx || iters == 0) && centers && counts && anchors_out &&
+                     (assign_ws || iters == 0) && status,
+                 "null pointer argument");
+  ASOT_CHECK_ARG(n_points >= 1 && dim >= 1 && n_anchors >= 1 && batch >= 1 && iters >= 0,
+                 "sizes must be >= 1 (iters >= 0)");
+  if (dim > asot::kMaxDim) return fail(ASOT_ERR_UNSUPPORTED, "dim > 128 is not supported");
+  if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
+  cudaStream_t s = (cudaStream_t)stream;
+  ASOT_LAUNCH(asot::launch_kmeans_prepare(centers, n_anchors, dim, anchors_out, s));
+  for (int32_t t = 0; t < iters; ++t) {
+    const int64_t* bt = batch_idx + (int64_t)t * batch;
+    ASOT_LAUNCH(asot::launch_map_assign(points, batch, dim, anchors_out, n_anchors, assign_ws,
+                                        status, s, bt));
+    ASOT_LAUNCH(asot::launch_kmeans_update(points, dim, bt, batch, assign_ws, n_anchors, centers,
+                                           anchors_out, counts, s));
+  }
+  return ASOT_OK;
+}
+
+asot_status asot_sqeuclid_cost(const float* anchors, int32_t n_anchors, int32_t dim,
+                               int32_t normalize, float* cost_out, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(anchors && cost_out, "null pointer argument");
+  ASOT_CHECK_ARG(n_anchors >= 1 && dim >= 1, "sizes must be >= 1");
+  if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
+  ASOT_LAUNCH(asot::launch_sqeuclid_cost(anchors, n_anchors, dim, normalize != 0, cost_out,
+                                         (cudaStream_t)stream));
+  return ASOT_OK;
+}
+
 size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
   Carver cv{nullptr, 0};
   (void)prec;

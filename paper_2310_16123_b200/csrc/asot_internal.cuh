@@ -112,7 +112,8 @@ __host__ __device__ inline uint32_t sw128_kmajor_offset(uint32_t n, uint32_t k, 
 cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, float* GC,
                               uint32_t* g_img, uint32_t* gc_img, int kpad, cudaStream_t s);
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
-                              int32_t* assign, uint32_t* status, cudaStream_t s);
+                              int32_t* assign, uint32_t* status, cudaStream_t s,
+                              const int64_t* gather = nullptr);
 cudaError_t launch_histograms(const int32_t* assign, const float* weights, const int64_t* offsets,
                               int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s);
 cudaError_t launch_sinkhorn_simt(const PairSource& ps, const PairSink& out, const float* H, int K,
@@ -154,6 +155,13 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
                                cudaStream_t s);
 cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
                                     bool normalize, float* Y, float* C, cudaStream_t s);
+cudaError_t launch_normalize_by_max(float* C, int64_t n, cudaStream_t s);
+cudaError_t launch_sqeuclid_cost(const float* anchors, int K, int d, bool normalize, float* C,
+                                 cudaStream_t s);
+cudaError_t launch_kmeans_prepare(const double* centers, int K, int d, float* anchors, cudaStream_t s);
+cudaError_t launch_kmeans_update(const float* points, int dim, const int64_t* batch_idx, int batch,
+                                 const int32_t* assign, int K, double* centers, float* anchors,
+                                 int64_t* counts, cudaStream_t s);
 
 inline int kpad32(int K) { return (K + 31) & ~31; }
 

@@ -84,8 +84,8 @@ __device__ __forceinline__ void merge_triple(BestTriple& a, float ob, float os, 
 
 template <int DP>
 __global__ void __launch_bounds__(kMapThreads)
-map_assign_kernel(const float* __restrict__ points, int64_t T, int dim,
-                  const float* __restrict__ anchors, int K, int chunk,
+map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ gather, int64_t T,
+                  int dim, const float* __restrict__ anchors, int K, int chunk,
                   int32_t* __restrict__ assign, uint32_t* __restrict__ status) {
   extern __shared__ float4 map_smem4[];
   float* Ws = reinterpret_cast<float*>(map_smem4);  // [chunk][DP + 4]
@@ -95,11 +95,13 @@ map_assign_kernel(const float* __restrict__ points, int64_t T, int dim,
   const int64_t p = (int64_t)blockIdx.x * kPointsPerBlock + (threadIdx.x >> 2);
   const bool valid = p < T;
 
+  // point p of this launch is row gather[p] of `points` (k-means batches) or row p
+  const int64_t row = valid ? (gather ? gather[p] : p) : 0;
   float x[DP];
   bool finite = true;
 #pragma unroll
   for (int k = 0; k < DP; ++k) {
-    const float v = (valid && k < dim) ? points[p * dim + k] : 0.0f;
+    const float v = (valid && k < dim) ? points[row * dim + k] : 0.0f;
     finite &= isfinite(v);
     x[k] = v;
   }
@@ -188,8 +190,9 @@ map_assign_kernel(const float* __restrict__ points, int64_t T, int dim,
 }
 
 template <int DP>
-static cudaError_t launch_map_dp(const float* points, int64_t T, int dim, const float* anchors,
-                                 int K, int32_t* assign, uint32_t* status, cudaStream_t s) {
+static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int64_t T, int dim,
+                                 const float* anchors, int K, int32_t* assign, uint32_t* status,
+                                 cudaStream_t s) {
   const int rs_bytes = (DP + 4) * 4;
   int chunk = (96 * 1024) / rs_bytes;
   if (chunk > K) chunk = K;
@@ -197,18 +200,19 @@ static cudaError_t launch_map_dp(const float* points, int64_t T, int dim, const 
   cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = (T + kPointsPerBlock - 1) / kPointsPerBlock;
   if (blocks == 0) return cudaSuccess;
-  map_assign_kernel<DP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, T, dim, anchors, K,
-                                                                   chunk, assign, status);
+  map_assign_kernel<DP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, gather, T, dim, anchors,
+                                                                   K, chunk, assign, status);
   return cudaGetLastError();
 }
 
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
-                              int32_t* assign, uint32_t* status, cudaStream_t s) {
-  if (dim <= 8) return launch_map_dp<8>(points, T, dim, anchors, K, assign, status, s);
-  if (dim <= 16) return launch_map_dp<16>(points, T, dim, anchors, K, assign, status, s);
-  if (dim <= 32) return launch_map_dp<32>(points, T, dim, anchors, K, assign, status, s);
-  if (dim <= 64) return launch_map_dp<64>(points, T, dim, anchors, K, assign, status, s);
-  return launch_map_dp<128>(points, T, dim, anchors, K, assign, status, s);
+                              int32_t* assign, uint32_t* status, cudaStream_t s,
+                              const int64_t* gather) {
+  if (dim <= 8) return launch_map_dp<8>(points, gather, T, dim, anchors, K, assign, status, s);
+  if (dim <= 16) return launch_map_dp<16>(points, gather, T, dim, anchors, K, assign, status, s);
+  if (dim <= 32) return launch_map_dp<32>(points, gather, T, dim, anchors, K, assign, status, s);
+  if (dim <= 64) return launch_map_dp<64>(points, gather, T, dim, anchors, K, assign, status, s);
+  return launch_map_dp<128>(points, gather, T, dim, anchors, K, assign, status, s);
 }
 
 // ------------------------------------------------------------------------------ a3: histograms

@@ -363,6 +363,11 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
   return soft::launch_mode<1>(P, s);
 }
 
+cudaError_t launch_normalize_by_max(float* C, int64_t n, cudaStream_t s) {
+  soft::normalize_by_max_kernel<<<1, 1024, 0, s>>>(C, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
                                     bool normalize, float* Y, float* C, cudaStream_t s) {
   const int64_t ny = (int64_t)K * h, nc = (int64_t)K * K;
