@@ -91,6 +91,15 @@ def normalized_sqeuclid_cost(anchors: np.ndarray) -> np.ndarray:
     return c.astype(np.float32)
 
 
+def anchor_sqdist_scale(anchors: np.ndarray) -> np.float32:
+    """1 / max_{u,v} ||w_u - w_v||^2 as f32: the normalisation of normalized_sqeuclid_cost, for
+    ground costs on the original points that must be on the anchors' scale (NEXT-4, R#32)."""
+    w = anchors.astype(np.float64)
+    diff = w[:, None, :] - w[None, :, :]
+    m = np.einsum("uvk,uvk->uv", diff, diff).max()
+    return np.float32(1.0 / m if m > 0 else 1.0)
+
+
 def make_inputs(cfg: str, seed: Optional[int] = None, n_dist: Optional[int] = None,
                 iters: Optional[int] = None) -> AsotInputs:
     """Build config ``cfg`` (c1..c5). ``n_dist`` shrinks N for oracle-sized parity runs

@@ -251,6 +251,10 @@ def main():
                          "inside every step by mini-batch k-means (Forgy init + batch draws seeded)")
     ap.add_argument("--kmeans-iters", type=int, default=50)
     ap.add_argument("--kmeans-batch", type=int, default=4096)
+    ap.add_argument("--baseline", default="none", choices=["none", "eot"],
+                    help="NEXT-4: also time entropic OT on the original point sets (the paper's "
+                         "eOT / BDS-eOT comparison) on a seeded pair sample, on the same GPU")
+    ap.add_argument("--eot-pairs", type=int, default=20000)
     ap.add_argument("--mapping", default="onehot", choices=["onehot", "ml", "dl"],
                     help="P: one-hot nearest anchor (the north-star path), or the NEXT-1 soft "
                          "mappings ASOT-ML / ASOT-DL (seeded parameters)")
@@ -517,6 +521,42 @@ def main():
                   "note": "per iteration: map_assign_kernel on the gathered batch + one update "
                           "launch (K CTAs); launch-latency bound at these batch sizes"}
 
+    # ---- NEXT-4: the paper's comparison system on the same box (eOT on the original points)
+    eot_base = None
+    if args.baseline == "eot" and rank == 0:
+        from asot_inputs import anchor_sqdist_scale, random_pairs
+        scale = float(anchor_sqdist_scale(inp.anchors))
+        ei, ej = random_pairs(inp.n_dist, min(args.eot_pairs, inp.n_pairs), seed=77)
+        ei_d, ej_d = t(ei.astype(np.int32)), t(ej.astype(np.int32))
+        est = asot.asot.new_status(dev)
+        asot.eot_pairs(pts, offs, w, ei_d, ej_d, float(inp.eps), inp.iters, scale,
+                       offsets_host=inp.offsets, status=est)          # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d_eot = asot.eot_pairs(pts, offs, w, ei_d, ej_d, float(inp.eps), inp.iters, scale,
+                               offsets_host=inp.offsets, status=est)
+        e1.record()
+        torch.cuda.synchronize()
+        asot.check_status(est)
+        ms = e0.elapsed_time(e1)
+        de = d_eot.cpu().numpy().astype(np.float64)
+        da = Dres.cpu().numpy()[ei, ej].astype(np.float64) if world == 1 else None
+        rate = len(ei) / (ms / 1e3)
+        eot_base = {
+            "kernel": "eot_pairs_kernel (per-pair n_i x n_j Gibbs kernel, SMEM or L2 slot)",
+            "sample_pairs": int(len(ei)), "ms": ms, "pairs_per_s": rate,
+            "whole_job_s_extrapolated": inp.n_pairs / rate,
+            "asot_speedup": value / rate,
+            "ground_cost": "normalised squared Euclidean on the original points (R#32)",
+        }
+        if da is not None:
+            rel = np.abs(da - de) / np.maximum(de, 1e-3)
+            eot_base.update({"asot_vs_eot_rmse": float(np.sqrt(np.mean((da - de) ** 2))),
+                             "asot_vs_eot_rel_p50": float(np.median(rel)),
+                             "asot_vs_eot_rel_p90": float(np.quantile(rel, 0.9)),
+                             "eot_mean_distance": float(de.mean())})
+
     # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
     # distributed public API with H2D / D2H inside the timed region (N > 1)
     e2e = None
@@ -605,7 +645,8 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "tf32" if eff == asot.TF32 else "f32", "data": "synthetic",
             "config": workload_config(inp, args, world),
-            "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "eot_baseline": eot_base,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
             "wall_s_timed_region": wall,
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],

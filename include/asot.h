@@ -217,6 +217,22 @@ asot_status asot_kmeans_minibatch(const float* points, int64_t n_points, int32_t
 asot_status asot_sqeuclid_cost(const float* anchors, int32_t n_anchors, int32_t dim,
                                int32_t normalize, float* cost_out, void* stream);
 
+/* ---- comparison baseline -- entropic OT on the ORIGINAL point sets ----
+ * For each pair p: C[r][c] = cost_scale * ||x_r - y_c||^2 over the n_i x n_j points of
+ * distributions i = pair_i[p], j = pair_j[p] (device i32), K = exp(-C / eps), v0 = 1, exactly
+ * `iters` Sinkhorn iterations with a = w_i, b = w_j, dist_out[p] = <diag(u) K diag(v), C>
+ * (fp32 arithmetic, fp64 final reduction).  This is the per-pair cost instantiation ASOT avoids
+ * (Table 2 eOT / BDS-eOT rows P:333-334).  Every distribution must have
+ * n_i <= 16384 points.  Denominators below FLT_MIN are clamped and flagged (DENOM_CLAMPED).
+ * workspace: asot_eot_workspace_bytes(n_dist, offsets_host, n_pairs) device bytes (per-CTA slots
+ * for kernels larger than the 160 KB kept in shared memory). */
+asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const int64_t* offsets_host,
+                           const float* weights, int64_t n_dist, int32_t dim, float cost_scale,
+                           float eps, int32_t iters, const int32_t* pair_i, const int32_t* pair_j,
+                           int64_t n_pairs, float* dist_out, uint32_t* status, void* workspace,
+                           size_t workspace_bytes, void* stream);
+size_t asot_eot_workspace_bytes(int64_t n_dist, const int64_t* offsets_host, int64_t n_pairs);
+
 /* Precision actually used for a given K and request (TF32 covers K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
 

@@ -48,6 +48,9 @@ _SIGS = {
     "asot_kmeans_minibatch": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp,
                                       c_vp, c_vp, c_vp]),
     "asot_sqeuclid_cost": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "asot_eot_pairs": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_f32, c_f32, c_i32, c_vp, c_vp,
+                               c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "asot_eot_workspace_bytes": (c_size, [c_i64, c_vp, c_i64]),
     "asot_profile_enable": (c_i32, [c_i32]),
     "asot_profile_read": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "asot_profile_read_kernel": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),

@@ -267,6 +267,29 @@ def sqeuclid_cost(anchors: torch.Tensor, normalize: bool = True, stream=None) ->
     return C
 
 
+def eot_pairs(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
+              pair_i: torch.Tensor, pair_j: torch.Tensor, eps: float, iters: int,
+              cost_scale: float, offsets_host: Optional[np.ndarray] = None,
+              status: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
+              stream=None) -> torch.Tensor:
+    """NEXT-4 baseline: entropic OT on the original point sets for explicit pairs (ground cost
+    cost_scale * ||x - y||^2).  Returns dist [n_pairs] f32."""
+    _need_cuda(points, offsets, weights, pair_i, pair_j)
+    _need_f32(points, weights)
+    oh = _host_offsets(offsets, offsets_host)
+    N = oh.shape[0] - 1
+    n = int(pair_i.numel())
+    out = torch.empty(max(n, 1), dtype=torch.float32, device=points.device)
+    st = new_status(points.device) if status is None else status
+    L = _lib_handle()
+    ws = _ws(workspace, points.device).get(L.asot_eot_workspace_bytes(N, _ptr(oh), n))
+    _check(L.asot_eot_pairs(_ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N,
+                            int(points.shape[1]), float(cost_scale), float(eps), int(iters),
+                            _ptr(pair_i), _ptr(pair_j), n, _ptr(out), _ptr(st), _ptr(ws),
+                            ws.numel(), _stream(stream)))
+    return out[:n]
+
+
 def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: int,
                       pair_i: torch.Tensor, pair_j: torch.Tensor, precision: int = TF32,
                       cost_max: Optional[float] = None, status: Optional[torch.Tensor] = None,

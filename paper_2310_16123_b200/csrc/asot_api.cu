@@ -359,6 +359,42 @@ asot_status asot_sqeuclid_cost(const float* anchors, int32_t n_anchors, int32_t 
   return ASOT_OK;
 }
 
+static int64_t max_dist_size(int64_t n_dist, const int64_t* offsets_host) {
+  int64_t m = 0;
+  for (int64_t i = 0; i < n_dist; ++i) m = std::max<int64_t>(m, offsets_host[i + 1] - offsets_host[i]);
+  return m;
+}
+
+size_t asot_eot_workspace_bytes(int64_t n_dist, const int64_t* offsets_host, int64_t n_pairs) {
+  if (!offsets_host || n_dist < 1 || n_pairs < 1) return 0;
+  return asot::eot_slot_floats(max_dist_size(n_dist, offsets_host)) * 4 *
+         (size_t)asot::eot_grid(n_pairs, device_sms());
+}
+
+asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const int64_t* offsets_host,
+                           const float* weights, int64_t n_dist, int32_t dim, float cost_scale,
+                           float eps, int32_t iters, const int32_t* pair_i, const int32_t* pair_j,
+                           int64_t n_pairs, float* dist_out, uint32_t* status, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(points && offsets && offsets_host && weights && pair_i && pair_j && dist_out && status,
+                 "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1 && dim >= 1 && iters >= 1 && n_pairs >= 0, "bad sizes");
+  ASOT_CHECK_ARG(std::isfinite(eps) && eps > 0.0f && std::isfinite(cost_scale) && cost_scale >= 0.0f,
+                 "eps must be > 0 and cost_scale >= 0, finite");
+  const int64_t mx = max_dist_size(n_dist, offsets_host);
+  if (!asot::eot_supported(mx)) return fail(ASOT_ERR_UNSUPPORTED, "a distribution has > 16384 points");
+  if (n_pairs == 0) return ASOT_OK;
+  const size_t need = asot_eot_workspace_bytes(n_dist, offsets_host, n_pairs);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  const int grid = asot::eot_grid(n_pairs, device_sms());
+  ASOT_LAUNCH(asot::launch_eot_pairs(points, offsets, weights, dim, cost_scale, eps, iters, pair_i,
+                                     pair_j, n_pairs, dist_out, (float*)workspace,
+                                     (int64_t)asot::eot_slot_floats(mx), grid, (int)mx, status,
+                                     (cudaStream_t)stream));
+  return ASOT_OK;
+}
+
 size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
   Carver cv{nullptr, 0};
   (void)prec;

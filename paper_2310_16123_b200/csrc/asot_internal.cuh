@@ -156,6 +156,14 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
 cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
                                     bool normalize, float* Y, float* C, cudaStream_t s);
 cudaError_t launch_normalize_by_max(float* C, int64_t n, cudaStream_t s);
+size_t eot_slot_floats(int64_t max_n);
+int eot_grid(int64_t n_pairs, int sms);
+bool eot_supported(int64_t max_n);
+cudaError_t launch_eot_pairs(const float* points, const int64_t* offsets, const float* weights,
+                             int dim, float scale, float eps, int iters, const int32_t* pair_i,
+                             const int32_t* pair_j, int64_t n_pairs, float* dist_out,
+                             float* kslots, int64_t slot_floats, int grid, int max_n,
+                             uint32_t* status, cudaStream_t s);
 cudaError_t launch_sqeuclid_cost(const float* anchors, int K, int d, bool normalize, float* C,
                                  cudaStream_t s);
 cudaError_t launch_kmeans_prepare(const double* centers, int K, int d, float* anchors, cudaStream_t s);

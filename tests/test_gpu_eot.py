@@ -1,0 +1,50 @@
+"""GPU parity of the NEXT-4 baseline (entropic OT on the original point sets, per pair) against
+the fp64 oracle (oracle/eot_oracle.py) through the C ABI: SMEM-resident kernels (c1/c2) and the
+workspace-slot path for n_i n_j > 40960 (c3/c5), single-point closed forms."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from asot_inputs import anchor_sqdist_scale, make_inputs  # noqa: E402
+from oracle import asot_oracle as O  # noqa: E402
+from oracle import eot_oracle as E  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def asot():
+    import paper_2310_16123_b200 as m
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("cfg,n,iters", [("c1", 20, 100), ("c2", 24, 60), ("c3", 7, 20), ("c5", 3, 8)])
+def test_eot_pairs_vs_oracle(asot, cfg, n, iters):
+    inp = make_inputs(cfg, n_dist=n)
+    s = anchor_sqdist_scale(inp.anchors)
+    pi, pj = O.upper_pairs(n)
+    pi = np.concatenate([pi, pj[:5]]).astype(np.int32)      # + a few reversed pairs
+    pj = np.concatenate([pj, pi[:5]]).astype(np.int32)
+    st = asot.asot.new_status()
+    d = asot.eot_pairs(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(pi), dev(pj),
+                       float(inp.eps), iters, float(s), offsets_host=inp.offsets, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    do = E.eot_pair_costs(inp.points, inp.offsets, inp.weights, inp.eps, iters, pi, pj, s)
+    rel = np.abs(d.cpu().numpy().astype(np.float64) - do) / np.maximum(do, 1e-3)
+    assert rel.max() <= 1e-4, rel.max()
+
+
+def test_eot_single_points(asot):
+    X = np.array([[0, 0], [3, 4], [1, 1]], np.float32)
+    offs = np.array([0, 1, 2, 3], np.int64)
+    w = np.ones(3, np.float32)
+    pi = np.array([0, 0, 2], np.int32)
+    pj = np.array([1, 2, 2], np.int32)
+    d = asot.eot_pairs(dev(X), dev(offs), dev(w), dev(pi), dev(pj), 0.05, 5, 0.04, offsets_host=offs)
+    np.testing.assert_allclose(d.cpu().numpy(), [1.0, 0.08, 0.0], rtol=1e-6)
