@@ -233,8 +233,13 @@ asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const in
                            size_t workspace_bytes, void* stream);
 size_t asot_eot_workspace_bytes(int64_t n_dist, const int64_t* offsets_host, int64_t n_pairs);
 
-/* Precision actually used for a given K and request (TF32 covers K <= 1024). */
+/* Precision actually used for a given K and request (TF32 covers 32 <= K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);
+
+/* Which Sinkhorn kernel asot_distance_matrix runs for (K, request): 0 = fp32 CUDA-core kernel,
+ * 1 = TF32 1-SM resident (K <= 128), 2 = TF32 CTA pair (K <= 256), 3 = 3xTF32 fp32-accurate
+ * 1-SM resident (ASOT_PREC_FP32, 32 <= K <= 128), 4 = TF32 CTA-pair streamed (K <= 1024). */
+int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 
 /* Optional kernel timing (bench.py's roofline): while enabled on this thread, the library records
  * a CUDA event pair on the launch stream immediately around every Sinkhorn kernel launch

@@ -66,14 +66,17 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
   return ASOT_OK;
 }
 
-// Tensor-core kernel selection for TF32 requests: 0 = none (fp32 SIMT), 1 = single-CTA
-// resident (K <= 128), 2 = CTA-pair resident (128 < K <= 256), 4 = CTA-pair streamed (K <= 1024).
+// Tensor-core kernel selection: 0 = none (fp32 SIMT), 1 = single-CTA resident TF32 (K <= 128),
+// 2 = CTA-pair resident TF32 (128 < K <= 256), 4 = CTA-pair streamed TF32 (K <= 1024),
+// 3 = single-CTA resident 3xTF32 for fp32-accurate requests (K <= 128).
 // K < 32 stays on the fp32 kernel: the per-iteration TF32 rounding of u / v dominates the TF32
 // error (R#23) and a dot product over fewer than 32 anchors barely averages it out
 // (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
 constexpr int32_t kMinTcAnchors = 32;
 int tc_kind(int32_t K, asot_precision prec) {
-  if (prec != ASOT_PREC_TF32 || K < kMinTcAnchors) return 0;
+  if (K < kMinTcAnchors) return 0;
+  if (prec == ASOT_PREC_FP32) return asot::sinkhorn_tc3_supported(K) ? 3 : 0;
+  if (prec != ASOT_PREC_TF32) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
   if (asot::sinkhorn_tc4_supported(K)) return 4;
@@ -113,6 +116,10 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
     const size_t kp = (size_t)asot::kpad32(K);
     b.g_img = (uint32_t*)cv.take(kp * kp * 4);
     b.gc_img = (uint32_t*)cv.take(kp * kp * 4);
+  } else if (kind == 3) {  // K_hi image, K_lo image, plain K (.) C_s
+    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
+    b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
+    b.GC = (float*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
   } else {
     b.G = (float*)cv.take((size_t)K * K * 4);
     b.GC = (float*)cv.take((size_t)K * K * 4);
@@ -164,6 +171,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc4(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
+  } else if (kind == 3) {
+    ASOT_LAUNCH(asot::launch_gibbs_prep_tc3(cost, K, eps, gb.g_img, gb.gc_img, gb.GC, s));
   } else {
     ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
                                         kind == 1 ? asot::kpad32(K) : K, s));
@@ -179,6 +188,9 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   } else if (kind == 1) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                          gb.gc_img, iters, s));
+  } else if (kind == 3) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
+                                          gb.gc_img, gb.GC, iters, s));
   } else {
     ASOT_LAUNCH(asot::launch_sinkhorn_simt(ps, sink, H, K, gb.G, gb.GC, iters, s));
   }
@@ -221,8 +233,13 @@ asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t re
 }
 int64_t asot_num_tiles(int64_t n_dist) { return n_dist < 1 ? 0 : asot::num_tiles(n_dist); }
 
+int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {
+  return tc_kind(n_anchors, requested);
+}
+
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
-  return use_tc(n_anchors, requested) ? ASOT_PREC_TF32 : ASOT_PREC_FP32;
+  return tc_kind(n_anchors, requested) == 0 || tc_kind(n_anchors, requested) == 3 ? ASOT_PREC_FP32
+                                                                                 : ASOT_PREC_TF32;
 }
 
 asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,

@@ -156,6 +156,13 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
 cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
                                     bool normalize, float* Y, float* C, cudaStream_t s);
 cudaError_t launch_normalize_by_max(float* C, int64_t n, cudaStream_t s);
+bool sinkhorn_tc3_supported(int K);
+size_t sinkhorn_tc3_image_bytes(int K);
+cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t* ghi, uint32_t* glo,
+                                  float* gc, cudaStream_t s);
+cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
+                                const float* gc, int iters, cudaStream_t s);
 size_t eot_slot_floats(int64_t max_n);
 int eot_grid(int64_t n_pairs, int sms);
 bool eot_supported(int64_t max_n);

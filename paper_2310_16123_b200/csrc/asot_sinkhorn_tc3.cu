@@ -1,0 +1,391 @@
+// asot_sinkhorn_tc3.cu -- steps a5 + a6 with fp32 accuracy on the 5th-gen tensor cores
+// (3xTF32, K <= 128): the ASOT_PREC_FP32 path (north star: 1e-4 of the fp64 oracle).
+//
+// Same recurrence as the TF32 kernels (R#4, R#5, R#11): U = A / (K V), V = B / (K^T U),
+// V^(0) = 1, exactly L iterations; d = <diag(u) K diag(v), C_s> (R#3, R#6).
+// Every product K x is evaluated as x_hi K_hi + x_lo K_hi + x_hi K_lo (3 tcgen05.mma kind::tf32
+// chains, fp32 accumulate), with x_hi = RNA_tf32(x), x_lo = x - x_hi (exact in fp32) and the same
+// split of the Gibbs kernel: the dropped x_lo K_lo term and the TF32 truncation of the lo parts
+// are O(2^-21) relative, i.e. fp32-level (SURVEY §8(d) precision table: 3xTF32 <= 1e-6 vs 2e-3 for
+// one pass; R#22 emulation: a 2-term split without K_lo fails 1e-4 at c2).
+//
+// Layout: pairs are the MMA M dimension (128 pair slots of a tile = 128 TMEM lanes).  TMEM is two
+// regions R0 = [0, 2KP), R1 = [2KP, 4KP) of [x_hi | x_lo] columns; phase f reads A from R(f%2)
+// and accumulates D into the hi columns of R((f+1)%2); the epilogue turns D in place into the
+// next x_hi and writes x_lo next to it.  K_hi and K_lo are SW128 K-major images in SMEM (TMA bulk
+// copies, once per CTA); K (.) C_s is a plain fp32 [KP][KP] SMEM copy for the cost, which runs on
+// the CUDA cores (1% of the MMA work) so all of SMEM goes to the two Gibbs images.
+//
+// One slot per CTA (TMEM holds one tile's hi/lo scalings twice), so the epilogue is overlapped
+// with the MMAs of the same tile: each phase is issued in four parts (K-half, N-half) =
+// (0,0) (0,1) (1,0) | commit D-half-0 | (1,1) | commit D-half-1.  The epilogue of N-half 0 runs
+// during part (1,1); the next phase's parts (0,0) (0,1) need only K-half 0 of the new x and run
+// during the N-half-1 epilogue.  Warps 0-15 are epilogue warps (lane quarter w%4, column group
+// w/4); warp 16 issues the MMAs.
+#include <cfloat>
+#include <cstdlib>
+
+#include "asot_internal.cuh"
+#include "asot_tcgen05.cuh"
+
+namespace asot {
+namespace tc3 {
+
+using namespace ptx;
+
+constexpr int kEpiWarps = 16;
+constexpr int kEpiThreads = kEpiWarps * 32;   // 512
+constexpr int kThreads = kEpiThreads + 32;    // + the MMA issuer warp
+constexpr uint32_t kTmemCols = 512;
+
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+
+template <int KP>
+struct Smem {
+  static constexpr int kRS = KP + 4;                       // marginal row stride (floats)
+  static constexpr int kRows = 8 + 16 + 1;                 // a-rows, b-rows, dummy row
+  static constexpr size_t kImg = (size_t)KP * KP * 4;      // one operand image / the GC copy
+  static constexpr size_t kOffGhi = 0;
+  static constexpr size_t kOffGlo = kImg;
+  static constexpr size_t kOffGC = 2 * kImg;
+  static constexpr size_t kOffMarg = 3 * kImg;
+  static constexpr size_t kOffRed = kOffMarg + (size_t)kRows * kRS * 4;   // [4][128] partial costs
+  static constexpr size_t kOffBar = kOffRed + 4 * 128 * 4;
+  static constexpr size_t kBytes = kOffBar + 64 + 1024;
+};
+
+// One part of a phase: D[:, nh*KP/2 ...] (+)= sum over K-half kh of
+// (A_hi K_hi + A_lo K_hi + A_hi K_lo), N = KP/2.
+template <int KP>
+__device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint32_t ghi, uint32_t glo,
+                                           int kh, int nh) {
+  constexpr int NH = KP / 2;
+  constexpr uint32_t idesc = make_idesc_tf32(128, NH);
+  const uint32_t d = d_reg + (uint32_t)(nh * NH);
+  const uint32_t row0 = (uint32_t)(nh * NH * 128);  // byte offset of row nh*NH inside a k-block
+#pragma unroll
+  for (int s = 0; s < KP / 16; ++s) {
+    const int ks = kh * (KP / 16) + s;  // 8-wide k step
+    const uint32_t boff = (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32) + row0;
+    const uint64_t dhi = make_sw128_desc(ghi + boff), dlo = make_sw128_desc(glo + boff);
+    const uint32_t acc0 = (kh > 0 || s > 0) ? 1u : 0u;
+    mma_ts(d, a_reg + 8 * ks, dhi, idesc, acc0);         // x_hi K_hi
+    mma_ts(d, a_reg + KP + 8 * ks, dhi, idesc, 1u);      // x_lo K_hi
+    mma_ts(d, a_reg + 8 * ks, dlo, idesc, 1u);           // x_hi K_lo
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kThreads, 1)
+sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
+                    const float* __restrict__ H, int K, const uint32_t* __restrict__ ghi_img,
+                    const uint32_t* __restrict__ glo_img, const float* __restrict__ gc_plain, int iters) {
+  using S = Smem<KP>;
+  constexpr int NH = KP / 2;          // columns per N-half
+  constexpr int CPT = NH / 4;         // columns per epilogue thread per half (4 column groups)
+  constexpr int CQ = KP / 4;          // columns per thread in the cost
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* marg = (float*)(smem + S::kOffMarg);
+  float* red = (float*)(smem + S::kOffRed);
+  const float* gcs = (const float*)(smem + S::kOffGC);
+  uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
+  uint32_t* tmem_holder = (uint32_t*)(bars + 7);
+  const uint32_t bar_g = smem_u32(&bars[0]);
+  const uint32_t bar_d0 = smem_u32(&bars[1]), bar_d1 = smem_u32(&bars[2]);   // D halves done
+  const uint32_t bar_x0 = smem_u32(&bars[3]), bar_x1 = smem_u32(&bars[4]);   // x halves ready
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(bar_g, 1);
+    mbar_init(bar_d0, 1);
+    mbar_init(bar_d1, 1);
+    mbar_init(bar_x0, kEpiWarps);
+    mbar_init(bar_x1, kEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_holder != 0) __trap();  // full allocation starts at column 0 (one CTA per SM)
+  if (threadIdx.x == 0) {           // K_hi, K_lo images and the GC copy, once per CTA (TMA bulk)
+    mbar_expect_tx(bar_g, (uint32_t)(3 * S::kImg));
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t off = 0; off < S::kImg; off += kChunk) {
+      const uint32_t n = (uint32_t)((S::kImg - off) < kChunk ? (S::kImg - off) : kChunk);
+      bulk_g2s(smem_u32(smem + S::kOffGhi + off), (const uint8_t*)ghi_img + off, n, bar_g);
+      bulk_g2s(smem_u32(smem + S::kOffGlo + off), (const uint8_t*)glo_img + off, n, bar_g);
+      bulk_g2s(smem_u32(smem + S::kOffGC + off), (const uint8_t*)gc_plain + off, n, bar_g);
+    }
+  }
+
+  if (warp == kEpiWarps) {
+    // ------------------------------------------------------------------ MMA issuer warp
+    const uint32_t ghi = smem_u32(smem + S::kOffGhi), glo = smem_u32(smem + S::kOffGlo);
+    mbar_wait(bar_g, 0);
+    uint32_t xpar = 0;
+    for (int64_t tr = blockIdx.x; tr < n_tiles; tr += gridDim.x) {
+      for (int f = 0; f < 2 * iters; ++f) {
+        const uint32_t a_reg = (uint32_t)((f & 1) * 2 * KP), d_reg = (uint32_t)(((f + 1) & 1) * 2 * KP);
+        mbar_wait(bar_x0, xpar);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_part<KP>(a_reg, d_reg, ghi, glo, 0, 0);
+          issue_part<KP>(a_reg, d_reg, ghi, glo, 0, 1);
+        }
+        __syncwarp();
+        mbar_wait(bar_x1, xpar);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_part<KP>(a_reg, d_reg, ghi, glo, 1, 0);
+          mma_commit(bar_d0);
+          issue_part<KP>(a_reg, d_reg, ghi, glo, 1, 1);
+          mma_commit(bar_d1);
+        }
+        __syncwarp();
+        xpar ^= 1u;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue warps
+    const int q = warp & 3, cg = warp >> 2;   // TMEM lane quarter, column group
+    const int p = q * 32 + lane;              // pair slot == TMEM lane
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    uint32_t dpar = 0;
+    bool clamped = false;
+    for (int64_t tr = blockIdx.x; tr < n_tiles; tr += gridDim.x) {
+      const int64_t t = tile_begin + tr;
+      int64_t bi, bj;
+      block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
+      const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
+      named_bar_sync(1, kEpiThreads);  // previous tile's cost readers are done (marg, red, R0)
+      for (int e = threadIdx.x; e < S::kRows * KP; e += kEpiThreads) {
+        const int r = e / KP, c = e % KP;
+        const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
+        float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+        if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
+        marg[r * S::kRS + c] = v;
+      }
+      int ii, jj;
+      const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
+      const float* arow = marg + (valid ? (p >> 4) : 24) * S::kRS;
+      const float* brow = marg + (valid ? 8 + (p & 15) : 24) * S::kRS;
+      // x^(0) = v0 = 1 on the real anchors, hi = 1, lo = 0, into R0 (both halves)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int c4 = 0; c4 < CPT; c4 += 4) {
+          const int c = h * NH + cg * CPT + c4;
+          uint32_t hi[4], lo[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hi[e] = (c + e < K) ? 0x3f800000u : 0u;
+          tmem_st4(lane_off + (uint32_t)c, hi);
+          tmem_st4(lane_off + (uint32_t)(KP + c), lo);
+        }
+      }
+      tmem_wait_st();
+      named_bar_sync(1, kEpiThreads);  // marginals visible to every epilogue thread
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_local(bar_x0);
+        mbar_arrive_local(bar_x1);
+      }
+      for (int f = 0; f < 2 * iters; ++f) {
+        const uint32_t d_reg = (uint32_t)(((f + 1) & 1) * 2 * KP);
+        const float* mrow = (f & 1) ? brow : arow;   // u-update: a = H[i]; v-update: b = H[j]
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(h == 0 ? bar_d0 : bar_d1, dpar);
+          tc_fence_after();
+#pragma unroll
+          for (int c4 = 0; c4 < CPT; c4 += 4) {
+            const int c = h * NH + cg * CPT + c4;
+            uint32_t dv[4], hi[4], lo[4];
+            tmem_ld4(lane_off + d_reg + (uint32_t)c, dv);
+            tmem_wait_ld();
+            const float4 m4 = *reinterpret_cast<const float4*>(mrow + c);
+            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float den = __uint_as_float(dv[e]);
+              if (den < FLT_MIN) {          // S:62 clamp + flag (cannot happen for real rows)
+                clamped |= mm[e] > 0.0f;
+                den = FLT_MIN;
+              }
+              const float x = mm[e] * rcp_approx(den);     // m = 0 -> exactly 0 (R#11)
+              const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;  // RNA to TF32
+              hi[e] = xh;
+              lo[e] = __float_as_uint(x - __uint_as_float(xh));
+            }
+            tmem_st4(lane_off + d_reg + (uint32_t)c, hi);
+            tmem_st4(lane_off + d_reg + (uint32_t)(KP + c), lo);
+          }
+          tmem_wait_st();
+          if (f + 1 < 2 * iters) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(h == 0 ? bar_x0 : bar_x1);
+          }
+        }
+        dpar ^= 1u;
+      }
+      // ---- cost (a6): u_L in R1, v_L in R0 (hi + lo = the fp32 values).  Thread (p, cg):
+      // t_c = sum_r (K (.) C_s)[r][c] u_r for its CQ columns, partial = sum_c v_c t_c.
+      // Every thread reads all columns of its lane, written by the other column groups' warps.
+      tc_fence_before();
+      named_bar_sync(1, kEpiThreads);
+      tc_fence_after();
+      float tacc[CQ];
+#pragma unroll
+      for (int c = 0; c < CQ; ++c) tacc[c] = 0.0f;
+      const uint32_t r1 = lane_off + (uint32_t)(2 * KP);
+      for (int r0 = 0; r0 < KP; r0 += 4) {
+        uint32_t uh[4], ul[4];
+        tmem_ld4(r1 + (uint32_t)r0, uh);
+        tmem_ld4(r1 + (uint32_t)(KP + r0), ul);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float ur = __uint_as_float(uh[e]) + __uint_as_float(ul[e]);
+          const float4* g4 = reinterpret_cast<const float4*>(gcs + (size_t)(r0 + e) * KP + cg * CQ);
+#pragma unroll
+          for (int c4 = 0; c4 < CQ / 4; ++c4) {
+            const float4 g = g4[c4];
+            tacc[4 * c4 + 0] = fmaf(g.x, ur, tacc[4 * c4 + 0]);
+            tacc[4 * c4 + 1] = fmaf(g.y, ur, tacc[4 * c4 + 1]);
+            tacc[4 * c4 + 2] = fmaf(g.z, ur, tacc[4 * c4 + 2]);
+            tacc[4 * c4 + 3] = fmaf(g.w, ur, tacc[4 * c4 + 3]);
+          }
+        }
+      }
+      float part = 0.0f;
+#pragma unroll
+      for (int c4 = 0; c4 < CQ; c4 += 4) {
+        uint32_t vh[4], vl[4];
+        tmem_ld4(lane_off + (uint32_t)(cg * CQ + c4), vh);
+        tmem_ld4(lane_off + (uint32_t)(KP + cg * CQ + c4), vl);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          part = fmaf(__uint_as_float(vh[e]) + __uint_as_float(vl[e]), tacc[c4 + e], part);
+      }
+      red[cg * 128 + p] = part;
+      named_bar_sync(1, kEpiThreads);
+      if (cg == 0) {
+        const float dsum = (red[p] + red[128 + p]) + (red[256 + p] + red[384 + p]);
+        write_result(out, tr * kTileSlots + p, valid, ii, jj, dsum);
+      }
+      tc_fence_before();
+    }
+    if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(0u), "r"(kTmemCols) : "memory");
+  }
+}
+
+// K_hi / K_lo SW128 images and the plain padded K (.) C_s copy.  Padding (K < KP): K_hi = 1,
+// K_lo = 0 outside the real block (denominators stay > 0, padded scalings are exactly 0),
+// K (.) C_s = 0.
+__global__ void gibbs_prep_tc3_kernel(const float* __restrict__ cost, int K, float eps, int kp,
+                                      uint32_t* __restrict__ ghi, uint32_t* __restrict__ glo,
+                                      float* __restrict__ gc) {
+  const int64_t total = (int64_t)kp * kp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(idx / kp), k = (int)(idx % kp);
+    const bool in = n < K && k < K;
+    const double c = in ? (double)cost[(int64_t)n * K + k] : 0.0;
+    const double g = in ? exp(-c / (double)eps) : 1.0;   // P:183 K := exp(-C_s / eps)
+    const float g32 = (float)g;
+    const uint32_t h = tf32_rna_bits(g32);
+    const uint32_t off = sw128_kmajor_offset((uint32_t)n, (uint32_t)k, (uint32_t)kp) >> 2;
+    ghi[off] = h;
+    glo[off] = in ? __float_as_uint(g32 - __uint_as_float(h)) : 0u;
+    gc[idx] = in ? (float)(g * c) : 0.0f;
+  }
+}
+
+template <int KP>
+static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, const PairSink& out,
+                             const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
+                             const float* gc, int iters, cudaStream_t s) {
+  const size_t smem = Smem<KP>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(sinkhorn_tc3_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = n_tiles < sms ? n_tiles : sms;
+  if (grid < 1) return cudaSuccess;
+  sinkhorn_tc3_kernel<KP><<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+                                                                 ghi, glo, gc, iters);
+  return cudaGetLastError();
+}
+
+}  // namespace tc3
+
+bool sinkhorn_tc3_supported(int K) { return K >= 1 && K <= 128; }
+
+size_t sinkhorn_tc3_image_bytes(int K) {
+  const size_t kp = (size_t)kpad32(K);
+  return kp * kp * 4;
+}
+
+cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t* ghi, uint32_t* glo,
+                                  float* gc, cudaStream_t s) {
+  const int kp = kpad32(K);
+  const int64_t total = (int64_t)kp * kp;
+  tc3::gibbs_prep_tc3_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(cost, K, eps, kp, ghi, glo, gc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
+                                const float* gc, int iters, cudaStream_t s) {
+  const int64_t n_tiles = tile_end - tile_begin;
+  if (n_tiles <= 0) return cudaSuccess;
+  switch (kpad32(K)) {
+    case 32: return tc3::launch_kp<32>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
+    case 64: return tc3::launch_kp<64>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
+    case 96: return tc3::launch_kp<96>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
+    case 128: return tc3::launch_kp<128>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace asot
