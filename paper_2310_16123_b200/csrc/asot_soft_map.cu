@@ -18,6 +18,7 @@
 // point order (thread j owns bin j), so H is deterministic.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "asot_internal.cuh"
 
@@ -262,6 +263,236 @@ soft_map_kernel(Params P) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// ASOT-DL, register-tiled (K in {64, 128, 256}, d in {32, 64, 128}, dictionary SMEM-resident):
+// a tile of PT = 8192 / K points; per layer two CUDA-core GEMMs with register tiles
+//   R[p][k] = sum_j Z[p][j] Wd[j][k] - X[p][k]      thread: TP1 points x 4 dims
+//   G[p][j] = sum_k R[p][k] Wd[j][k]; z <- max(0, z - g - lambda_p)   thread: 4 points x 8 codes
+// with Z and R stored transposed (Zt[j][p], Rt[k][p]) and the dictionary stored twice
+// (Wd[j][k] for GEMM 1, WdT[k][j] for GEMM 2), so every inner step is two or three vector
+// shared-memory loads feeding 8-32 FMAs.  Same arithmetic as the generic kernel up to fp32
+// summation order.
+// ------------------------------------------------------------------------------------------
+template <int DP, int K>
+struct TiledDL {
+  static constexpr int PT = 8192 / K;            // points per tile
+  static constexpr int ZS = PT + 4;              // Zt / Rt row stride
+  static constexpr int WS = DP + 4;              // Wd row stride
+  static constexpr int TS = K + 4;               // WdT row stride
+  static constexpr int TP1 = PT * DP / 1024;     // GEMM-1 points per thread
+  static constexpr size_t kFloats(int hidden) {
+    return (size_t)K * WS + (size_t)DP * TS + (size_t)K * ZS + (size_t)DP * ZS + (size_t)PT * DP +
+           (size_t)PT * hidden + 3 * PT;
+  }
+  static constexpr size_t bytes(int hidden) { return (size_t)K * 8 + kFloats(hidden) * 4; }
+};
+
+template <int DP, int K>
+__global__ void __launch_bounds__(kThreads)
+soft_dl_tiled_kernel(Params P) {
+  using T = TiledDL<DP, K>;
+  constexpr int PT = T::PT, ZS = T::ZS, WS = T::WS, TS = T::TS, TP1 = T::TP1;
+  static_assert(TP1 >= 1 && (PT / 4) * (K / 8) == kThreads, "tile shape");
+  extern __shared__ double soft_smem[];
+  double* acc = soft_smem;                         // [K]
+  float* Wd = (float*)(acc + K);                   // [K][WS]
+  float* WdT = Wd + K * WS;                        // [DP][TS]
+  float* Zt = WdT + DP * TS;                       // [K][ZS]
+  float* Rt = Zt + K * ZS;                         // [DP][ZS]
+  float* Xs = Rt + DP * ZS;                        // [PT][DP]
+  float* Hs = Xs + PT * DP;                        // [PT][hidden]
+  float* lam = Hs + PT * P.hidden;
+  float* rs = lam + PT;
+  float* wts = rs + PT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i = blockIdx.x;
+  const int64_t s = P.offsets[i], e = P.offsets[i + 1];
+
+  for (int j = tid; j < K; j += kThreads) acc[j] = 0.0;
+  for (int x = tid; x < K * DP; x += kThreads) {
+    const int j = x / DP, k = x % DP;
+    const float w = k < P.dim ? P.dict[(int64_t)j * P.dim + k] : 0.0f;
+    Wd[j * WS + k] = w;
+    WdT[k * TS + j] = w;
+  }
+  bool nonfinite = false, negative = false;
+  double msum = 0.0;
+  // GEMM-1 ownership: dims k1..k1+3, points p1..p1+TP1-1
+  const int k1 = 4 * (tid % (DP / 4)), p1 = TP1 * (tid / (DP / 4));
+  // GEMM-2 ownership: codes j2..j2+7, points p2..p2+3
+  const int j2 = 8 * (tid % (K / 8)), p2 = 4 * (tid / (K / 8));
+
+  for (int64_t t0 = s; t0 < e; t0 += PT) {
+    const int np = (int)min((int64_t)PT, e - t0);
+    __syncthreads();
+    for (int x = tid; x < PT * DP; x += kThreads) {
+      const int p = x / DP, k = x % DP;
+      float v = 0.0f;
+      if (p < np && k < P.dim) {
+        v = P.points[(t0 + p) * P.dim + k];
+        nonfinite |= !isfinite(v);
+      }
+      Xs[x] = v;
+    }
+    for (int p = tid; p < PT; p += kThreads) {
+      const float w = p < np ? P.weights[t0 + p] : 0.0f;
+      if (p < np) {
+        nonfinite |= !isfinite(w);
+        negative |= w < 0.0f;
+        msum += (double)w;
+      }
+      wts[p] = w;
+    }
+    for (int x = tid; x < K * ZS; x += kThreads) Zt[x] = 0.0f;    // z^(0) = 0 (R#27)
+    __syncthreads();
+    // lambda-net hidden layer (thread = one hidden unit for all PT points)
+    for (int c = tid; c < P.hidden; c += kThreads) {
+      const float b = P.b1[c];
+      for (int p0 = 0; p0 < PT; p0 += 16) {
+        float a[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = b;
+        for (int k = 0; k < P.dim; ++k) {
+          const float w = __ldg(P.W1 + (int64_t)k * P.hidden + c);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) a[q] = fmaf(Xs[(p0 + q) * DP + k], w, a[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) Hs[(p0 + q) * P.hidden + c] = fmaxf(a[q], 0.0f);
+      }
+    }
+    __syncthreads();
+    for (int p = warp; p < PT; p += kThreads / 32) {
+      float sdot = 0.0f;
+      for (int c = lane; c < P.hidden; c += 32) sdot = fmaf(Hs[p * P.hidden + c], __ldg(P.W2 + c), sdot);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+      if (lane == 0) lam[p] = softplus_f(sdot + P.b2[0]);
+    }
+    __syncthreads();
+
+    for (int layer = 0; layer < P.n_layers; ++layer) {
+      // ---- GEMM 1: R = Z Wd - X
+      float r[TP1][4];
+#pragma unroll
+      for (int t = 0; t < TP1; ++t)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r[t][q] = 0.0f;
+#pragma unroll 4
+      for (int j = 0; j < K; ++j) {
+        const float4 w = *reinterpret_cast<const float4*>(Wd + j * WS + k1);
+        float z[TP1];
+        if constexpr (TP1 == 4) {
+          const float4 z4 = *reinterpret_cast<const float4*>(Zt + j * ZS + p1);
+          z[0] = z4.x; z[1] = z4.y; z[2] = z4.z; z[3] = z4.w;
+        } else if constexpr (TP1 == 2) {
+          const float2 z2 = *reinterpret_cast<const float2*>(Zt + j * ZS + p1);
+          z[0] = z2.x; z[1] = z2.y;
+        } else {
+#pragma unroll
+          for (int t = 0; t < TP1; ++t) z[t] = Zt[j * ZS + p1 + t];
+        }
+#pragma unroll
+        for (int t = 0; t < TP1; ++t) {
+          r[t][0] = fmaf(z[t], w.x, r[t][0]);
+          r[t][1] = fmaf(z[t], w.y, r[t][1]);
+          r[t][2] = fmaf(z[t], w.z, r[t][2]);
+          r[t][3] = fmaf(z[t], w.w, r[t][3]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < TP1; ++t)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Rt[(k1 + q) * ZS + p1 + t] = r[t][q] - Xs[(p1 + t) * DP + k1 + q];
+      __syncthreads();
+      // ---- GEMM 2 + update: g = W^T r, z <- max(0, z - g - lambda)
+      float g[4][8];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) g[t][q] = 0.0f;
+#pragma unroll 4
+      for (int k = 0; k < DP; ++k) {
+        const float4 rv = *reinterpret_cast<const float4*>(Rt + k * ZS + p2);
+        const float4 wa = *reinterpret_cast<const float4*>(WdT + k * TS + j2);
+        const float4 wb = *reinterpret_cast<const float4*>(WdT + k * TS + j2 + 4);
+        const float rr[4] = {rv.x, rv.y, rv.z, rv.w};
+        const float ww[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) g[t][q] = fmaf(rr[t], ww[q], g[t][q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 z4 = *reinterpret_cast<float4*>(Zt + (j2 + q) * ZS + p2);
+        z4.x = fmaxf(0.0f, (z4.x - g[0][q]) - lam[p2 + 0]);
+        z4.y = fmaxf(0.0f, (z4.y - g[1][q]) - lam[p2 + 1]);
+        z4.z = fmaxf(0.0f, (z4.z - g[2][q]) - lam[p2 + 2]);
+        z4.w = fmaxf(0.0f, (z4.w - g[3][q]) - lam[p2 + 3]);
+        *reinterpret_cast<float4*>(Zt + (j2 + q) * ZS + p2) = z4;
+      }
+      __syncthreads();
+    }
+    // ---- row sums (warp per point), normalisation, fp64 point-order accumulation
+    for (int p = warp; p < PT; p += kThreads / 32) {
+      float sum = 0.0f;
+      for (int j = lane; j < K; j += 32) sum += Zt[j * ZS + p];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) rs[p] = sum;
+    }
+    __syncthreads();
+    if (tid < np && !(rs[tid] > 0.0f)) atomicOr(P.status, ASOT_FLAG_SOFT_FALLBACK);
+    const float unif = 1.0f / (float)K;
+    for (int j = tid; j < K; j += kThreads) {
+      double a = acc[j];
+      for (int p = 0; p < np; ++p) {
+        const float z = rs[p] > 0.0f ? Zt[j * ZS + p] / rs[p] : unif;
+        if (P.codes) P.codes[(t0 + p) * K + j] = z;
+        a += (double)wts[p] * (double)z;
+      }
+      acc[j] = a;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < K; j += kThreads) P.H[i * K + j] = (float)acc[j];
+  if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(P.status, ASOT_FLAG_NONFINITE_INPUT);
+  if (__syncthreads_or(negative) && tid == 0) atomicOr(P.status, ASOT_FLAG_BAD_MASS);
+  // weights were read by threads p < PT: reduce their partial sums through the acc buffer
+  __syncthreads();
+  if (tid < PT) acc[tid] = msum;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int p = 0; p < PT && p < K; ++p) tot += acc[p];
+    if (e <= s) atomicOr(P.status, ASOT_FLAG_EMPTY_DIST);
+    else if (fabs(tot - 1.0) > 1e-5) atomicOr(P.status, ASOT_FLAG_BAD_MASS);
+  }
+}
+
+template <int DP, int K>
+cudaError_t launch_tiled_dl(const Params& P, cudaStream_t s, bool& done) {
+  const size_t smem = TiledDL<DP, K>::bytes(P.hidden);
+  if (smem > 220 * 1024 || TiledDL<DP, K>::PT > K) { done = false; return cudaSuccess; }
+  cudaError_t e = cudaFuncSetAttribute(soft_dl_tiled_kernel<DP, K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  soft_dl_tiled_kernel<DP, K><<<(unsigned)P.n_dist, kThreads, smem, s>>>(P);
+  done = true;
+  return cudaGetLastError();
+}
+
+// Picks the register-tiled DL kernel when (d, K) has an instantiation and it fits SMEM.
+template <int DP>
+cudaError_t try_tiled_dl(const Params& P, cudaStream_t s, bool& done) {
+  done = false;
+  if (P.K == 64) return launch_tiled_dl<DP, 64>(P, s, done);
+  if (P.K == 128) return launch_tiled_dl<DP, 128>(P, s, done);
+  if (P.K == 256) return launch_tiled_dl<DP, 256>(P, s, done);
+  return cudaSuccess;
+}
+
 size_t smem_bytes(int mode, int dp, int K, int hidden, int wrows) {
   size_t b = (size_t)K * 8 + (size_t)(2 * kPT * dp + kPT * hidden + kPT * K + 3 * kPT) * 4;
   if (mode == 1) b += (size_t)wrows * (dp + 1) * 4;
@@ -360,6 +591,13 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
                                cudaStream_t s) {
   soft::Params P{points, offsets, weights, n_dist, dim, K, hidden, V1, c1, v2, c2,
                  dict, n_layers, 0, H, codes, status};
+  if (!getenv("ASOT_SOFT_DL_GENERIC") && (dim == 32 || dim == 64 || dim == 128)) {
+    bool done = false;
+    cudaError_t e = dim == 32 ? soft::try_tiled_dl<32>(P, s, done)
+                  : dim == 64 ? soft::try_tiled_dl<64>(P, s, done)
+                              : soft::try_tiled_dl<128>(P, s, done);
+    if (e != cudaSuccess || done) return e;
+  }
   return soft::launch_mode<1>(P, s);
 }
 
