@@ -97,6 +97,19 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(float x) {
   return r;
 }
 
+// Two fp32 products in one FMUL2 (Blackwell's paired fp32 pipe op, PTX mul.rn.f32x2): each lane
+// is rounded exactly like a scalar FMUL, so results are bitwise those of two scalar multiplies.
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 c;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rc, ra, rb;\n\t"
+      "mov.b64 {%0, %1}, rc;\n\t}"
+      : "=f"(c.x), "=f"(c.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return c;
+}
+
 // Byte offset of element (row n, k) in the K-major SWIZZLE_128B UMMA operand image of an
 // [rows x kpad] fp32 matrix: k-blocks of 32 elements (128 B) stored one after another, each
 // [rows][128 B] with 8-row / 1024 B swizzle atoms (16-byte chunk index XOR row%8).

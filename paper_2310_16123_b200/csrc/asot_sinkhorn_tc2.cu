@@ -246,8 +246,9 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             const float m0 = (e & 2) ? mq.z : mq.x, m1 = (e & 2) ? mq.w : mq.y;
             const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
             const float r = rcp_approx(d0 * d1);
-            o[e] = tf32_rna_pre((m0 * d1) * r);
-            o[e + 1] = tf32_rna_pre((m1 * d0) * r);
+            const float2 x = fmul2(fmul2(make_float2(m0, m1), make_float2(d1, d0)), make_float2(r, r));
+            o[e] = tf32_rna_pre(x.x);
+            o[e + 1] = tf32_rna_pre(x.y);
           }
           tmem_st16(rd + c * 16, o);  // in place: the new scaling replaces D
           if (c + 1 < 4) {

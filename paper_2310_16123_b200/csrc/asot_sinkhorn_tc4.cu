@@ -298,8 +298,9 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                 for (int e = 0; e < 16; e += 2) {
                   const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
                   const float r = rcp_approx(d0 * d1);
-                  o[e] = tf32_rna_pre((m[e] * d1) * r);
-                  o[e + 1] = tf32_rna_pre((m[e + 1] * d0) * r);
+                  const float2 x = fmul2(fmul2(make_float2(m[e], m[e + 1]), make_float2(d1, d0)), make_float2(r, r));
+                  o[e] = tf32_rna_pre(x.x);
+                  o[e + 1] = tf32_rna_pre(x.y);
                 }
 #pragma unroll
                 for (int e = 0; e < 16; e += 4) stg128(xout + x_offset(p, k0 + e), o[e], o[e + 1], o[e + 2], o[e + 3]);
