@@ -120,9 +120,9 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
     b.GC = (float*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
-  } else {
-    b.G = (float*)cv.take((size_t)K * K * 4);
-    b.GC = (float*)cv.take((size_t)K * K * 4);
+  } else {  // CUDA-core kernel: row-padded fp32 K and K (.) C_s [K][simt_kpad(K)]
+    b.G = (float*)cv.take((size_t)K * asot::simt_kpad(K) * 4);
+    b.GC = (float*)cv.take((size_t)K * asot::simt_kpad(K) * 4);
   }
   return b;
 }
@@ -173,9 +173,11 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 3) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc3(cost, K, eps, gb.g_img, gb.gc_img, gb.GC, s));
+  } else if (kind == 1) {
+    ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, nullptr, nullptr, gb.g_img, gb.gc_img,
+                                        asot::kpad32(K), s));
   } else {
-    ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, gb.G, gb.GC, gb.g_img, gb.gc_img,
-                                        kind == 1 ? asot::kpad32(K) : K, s));
+    ASOT_LAUNCH(asot::launch_gibbs_prep_simt(cost, K, eps, gb.G, gb.GC, s));
   }
   ProfScope prof(ASOT_PROF_SINKHORN, s);
   if (kind == 4) {
