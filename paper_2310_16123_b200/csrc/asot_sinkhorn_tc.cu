@@ -471,8 +471,19 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
           const float2 x = fmul2(fmul2(make_float2(m0, m1), make_float2(d1, d0)), make_float2(r, r));
           o[e] = tf32_rna_pre(x.x);
           o[e + 1] = tf32_rna_pre(x.y);
+          if (DBG == 4) {  // diagnostics: TMEM traffic without the arithmetic
+            o[e] = dc[e];
+            o[e + 1] = dc[e + 1];
+          }
         }
-        tmem_st16(dst + c * 16, o);
+        if (DBG == 5) {  // diagnostics: arithmetic and loads without the TMEM stores
+          uint32_t acc5 = 0;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc5 ^= o[e];
+          if (acc5 == 0x12345678u && iters < 0) g_tc_trace[0][0][0] = acc5;
+        } else {
+          tmem_st16(dst + c * 16, o);
+        }
         if (c + 1 < NC) {
           tmem_wait_ld();
           reg_fence16(d[(c + 1) & 1]);
@@ -535,7 +546,8 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   const size_t smem = Smem<KP>::kBytes;
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = dbg == 1 ? sinkhorn_tc_kernel<KP, 1> : dbg == 2 ? sinkhorn_tc_kernel<KP, 2>
-            : dbg == 3 ? sinkhorn_tc_kernel<KP, 3> : sinkhorn_tc_kernel<KP, 0>;
+            : dbg == 3 ? sinkhorn_tc_kernel<KP, 3> : dbg == 4 ? sinkhorn_tc_kernel<KP, 4>
+            : dbg == 5 ? sinkhorn_tc_kernel<KP, 5> : sinkhorn_tc_kernel<KP, 0>;
   cudaError_t e = cudaFuncSetAttribute(kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
