@@ -255,6 +255,10 @@ def main():
                     help="NEXT-4: also time entropic OT on the original point sets (the paper's "
                          "eOT / BDS-eOT comparison) on a seeded pair sample, on the same GPU")
     ap.add_argument("--eot-pairs", type=int, default=20000)
+    ap.add_argument("--exact", action="store_true",
+                    help="NEXT-3: also solve exact anchor-space OT on a seeded pair sample and report "
+                         "its pairs/s and the eASOT-vs-exact gap")
+    ap.add_argument("--exact-pairs", type=int, default=20000)
     ap.add_argument("--mapping", default="onehot", choices=["onehot", "ml", "dl"],
                     help="P: one-hot nearest anchor (the north-star path), or the NEXT-1 soft "
                          "mappings ASOT-ML / ASOT-DL (seeded parameters)")
@@ -559,6 +563,35 @@ def main():
                              "asot_vs_eot_rel_p90": float(np.quantile(rel, 0.9)),
                              "eot_mean_distance": float(de.mean())})
 
+    # ---- NEXT-3: exact ASOT (eps -> 0 limit) on a pair sample, same GPU
+    exact = None
+    if args.exact and rank == 0 and world == 1:
+        from asot_inputs import random_pairs
+        _, Hx, _ = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+        xi, xj = random_pairs(inp.n_dist, min(args.exact_pairs, inp.n_pairs), seed=78)
+        xi_d, xj_d = t(xi.astype(np.int32)), t(xj.astype(np.int32))
+        xst = asot.asot.new_status(dev)
+        asot.exact_asot_pairs(Hx, cst, xi_d, xj_d, status=xst)      # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d_ex = asot.exact_asot_pairs(Hx, cst, xi_d, xj_d, status=xst)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        dx = d_ex.cpu().numpy()
+        ok = np.isfinite(dx)
+        da = Dres.cpu().numpy()[xi, xj].astype(np.float64)
+        rel = np.abs(da[ok] - dx[ok]) / np.maximum(dx[ok], 1e-3)
+        exact = {"kernel": "exact_pairs_kernel (fp64 successive-shortest-path min-cost flow on the "
+                           "histogram supports, warp per pair)",
+                 "sample_pairs": int(len(xi)), "solved": int(ok.sum()), "ms": ms,
+                 "pairs_per_s": len(xi) / (ms / 1e3),
+                 "easot_vs_exact_rmse": float(np.sqrt(np.mean((da[ok] - dx[ok]) ** 2))) if ok.any() else None,
+                 "easot_vs_exact_rel_p50": float(np.median(rel)) if ok.any() else None,
+                 "easot_vs_exact_rel_p90": float(np.quantile(rel, 0.9)) if ok.any() else None,
+                 "support_limit": "128 bins per side (larger: NaN, flagged)"}
+
     # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
     # distributed public API with H2D / D2H inside the timed region (N > 1)
     e2e = None
@@ -649,6 +682,7 @@ def main():
             "data": "synthetic",
             "config": workload_config(inp, args, world),
             "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "eot_baseline": eot_base,
+            "exact_asot": exact,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
             "wall_s_timed_region": wall,

@@ -69,6 +69,7 @@ typedef enum {
 #define ASOT_FLAG_DENOM_CLAMPED    8u  /* a Sinkhorn denominator < FLT_MIN was clamped     */
 #define ASOT_FLAG_NONFINITE_OUTPUT 16u /* a distance came out NaN/Inf                            */
 #define ASOT_FLAG_SOFT_FALLBACK    32u /* a soft code was all zero -> uniform row (warning) */
+#define ASOT_FLAG_EXACT_TOO_LARGE  64u /* exact ASOT: a histogram support > 128 bins (result NaN) */
 
 /* Distance-matrix tiling (step a4).  Distributions are grouped in blocks of 16; block pairs
  * (bi <= bj) are enumerated row-major over the upper triangle of the block grid; each block
@@ -232,6 +233,18 @@ asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const in
                            int64_t n_pairs, float* dist_out, uint32_t* status, void* workspace,
                            size_t workspace_bytes, void* stream);
 size_t asot_eot_workspace_bytes(int64_t n_dist, const int64_t* offsets_host, int64_t n_pairs);
+
+/* ---- EXACT anchor-space OT per pair (Def. 3 / Eq. (4)) ----
+ * dist_out[p] = min <T, C_s> over T in U(a', b'), a' = hist[pair_i[p]], b' = hist[pair_j[p]]
+ * renormalised to unit mass in fp64 (R#14), solved exactly (successive-shortest-path min-cost flow
+ * on the two histogram supports, fp64) -- the eps -> 0 limit of asot_pairwise_sinkhorn.  Supports
+ * of up to 128 bins per side; larger ones give NaN and ASOT_FLAG_EXACT_TOO_LARGE.  hist [n_dist,
+ * n_anchors] f32, cost [n_anchors, n_anchors] f32, pair_i / pair_j [n_pairs] i32, dist_out
+ * [n_pairs] f64: device pointers; workspace: n_pairs device bytes. */
+asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_anchors, const float* cost,
+                                  const int32_t* pair_i, const int32_t* pair_j, int64_t n_pairs,
+                                  double* dist_out, uint32_t* status, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 
 /* Precision actually used for a given K and request (TF32 covers 32 <= K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);

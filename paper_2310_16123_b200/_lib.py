@@ -52,6 +52,8 @@ _SIGS = {
                                c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_eot_workspace_bytes": (c_size, [c_i64, c_vp, c_i64]),
     "asot_sinkhorn_kernel_kind": (c_i32, [c_i32, c_i32]),
+    "asot_exact_asot_pairs": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                      c_size, c_vp]),
     "asot_profile_enable": (c_i32, [c_i32]),
     "asot_profile_read": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "asot_profile_read_kernel": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),

@@ -25,6 +25,7 @@ FLAG_NONFINITE_INPUT = 4
 FLAG_DENOM_CLAMPED = 8
 FLAG_NONFINITE_OUTPUT = 16
 FLAG_SOFT_FALLBACK = 32
+FLAG_EXACT_TOO_LARGE = 64
 
 _STATUS_EXC = {1: ValueError, 2: ValueError, 3: FloatingPointError, 4: RuntimeError,
                5: NotImplementedError, 6: MemoryError}
@@ -122,7 +123,7 @@ def new_status(device=None) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device or "cuda")
 
 
-def check_status(status, allow: int = FLAG_DENOM_CLAMPED | FLAG_SOFT_FALLBACK) -> int:
+def check_status(status, allow: int = FLAG_DENOM_CLAMPED | FLAG_SOFT_FALLBACK | FLAG_EXACT_TOO_LARGE) -> int:
     """Raise on data-dependent failures the kernels flagged (call after synchronising)."""
     v = int(status.item()) if isinstance(status, torch.Tensor) else int(status)
     bad = v & ~allow
@@ -299,6 +300,23 @@ def eot_pairs(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor
                             int(points.shape[1]), float(cost_scale), float(eps), int(iters),
                             _ptr(pair_i), _ptr(pair_j), n, _ptr(out), _ptr(st), _ptr(ws),
                             ws.numel(), _stream(stream)))
+    return out[:n]
+
+
+def exact_asot_pairs(H: torch.Tensor, cost: torch.Tensor, pair_i: torch.Tensor, pair_j: torch.Tensor,
+                     status: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
+                     stream=None) -> torch.Tensor:
+    """NEXT-3: exact anchor-space OT W_AS for explicit pairs (fp64 min-cost flow on the histogram
+    supports).  Returns dist [n_pairs] f64 (NaN where a support exceeds 128 bins)."""
+    _need_cuda(H, cost, pair_i, pair_j)
+    _need_f32(H, cost)
+    N, K = H.shape
+    n = int(pair_i.numel())
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=H.device)
+    st = new_status(H.device) if status is None else status
+    ws = _ws(workspace, H.device).get(max(n, 1))
+    _check(_lib_handle().asot_exact_asot_pairs(_ptr(H), N, int(K), _ptr(cost), _ptr(pair_i), _ptr(pair_j),
+                                               n, _ptr(out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))
     return out[:n]
 
 

@@ -414,6 +414,21 @@ asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const in
   return ASOT_OK;
 }
 
+asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_anchors, const float* cost,
+                                  const int32_t* pair_i, const int32_t* pair_j, int64_t n_pairs,
+                                  double* dist_out, uint32_t* status, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(hist && cost && pair_i && pair_j && dist_out && status, "null pointer argument");
+  ASOT_CHECK_ARG(n_dist >= 1 && n_anchors >= 1 && n_pairs >= 0, "bad sizes");
+  if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
+  if (n_pairs == 0) return ASOT_OK;
+  if (!workspace || workspace_bytes < (size_t)n_pairs) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  ASOT_LAUNCH(asot::launch_exact_pairs(hist, n_dist, n_anchors, cost, pair_i, pair_j, n_pairs, dist_out,
+                                       (uint8_t*)workspace, status, device_sms(), (cudaStream_t)stream));
+  return ASOT_OK;
+}
+
 size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
   Carver cv{nullptr, 0};
   (void)prec;

@@ -130,6 +130,9 @@ cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const flo
 cudaError_t launch_histograms(const int32_t* assign, const float* weights, const int64_t* offsets,
                               int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s);
 int simt_kpad(int K);
+cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const float* cost, const int32_t* pi,
+                               const int32_t* pj, int64_t n_pairs, double* out, uint8_t* pending,
+                               uint32_t* status, int sms, cudaStream_t s);
 cudaError_t launch_gibbs_prep_simt(const float* cost, int K, float eps, float* Gp, float* GCp, cudaStream_t s);
 cudaError_t launch_sinkhorn_simt(const PairSource& ps, const PairSink& out, const float* H, int K,
                                  const float* G, const float* GC, int iters, cudaStream_t s);
