@@ -30,14 +30,42 @@ constexpr int kSmallKS = kSmallN + 1;             // padded K row stride (odd: c
 constexpr int kSmallFloats = kSmallN * kSmallKS + 4 * kSmallN;   // K + u, v, a, b per warp
 constexpr size_t kSmemBytes = 200 * 1024;
 
-__device__ __forceinline__ float point_cost(const float* __restrict__ x, const float* __restrict__ y,
-                                            int d, float scale) {
-  float acc = 0.0f;
-  for (int k = 0; k < d; ++k) {
-    const float t = x[k] - y[k];
-    acc = fmaf(t, t, acc);
+// Squared distances of the 2 x 2 block (rows r0, r0+1 of X; rows c0, c0+1 of Y), times scale.
+// Rows past nr / nc repeat the last valid row (their results are discarded).  Same per-entry op
+// order everywhere (difference, then fma-accumulate in dimension order), so the cost pass
+// reproduces the kernel pass's C bitwise.
+__device__ __forceinline__ void cost2x2(const float* __restrict__ X, const float* __restrict__ Y, int dim,
+                                        int r0, int c0, int nr, int nc, float scale, float (&o)[4]) {
+  const float* x0 = X + (int64_t)r0 * dim;
+  const float* x1 = X + (int64_t)min(r0 + 1, nr - 1) * dim;
+  const float* y0 = Y + (int64_t)c0 * dim;
+  const float* y1 = Y + (int64_t)min(c0 + 1, nc - 1) * dim;
+  float a00 = 0.0f, a01 = 0.0f, a10 = 0.0f, a11 = 0.0f;
+  if ((dim & 3) == 0) {
+    for (int k = 0; k < dim; k += 4) {
+      const float4 p0 = *reinterpret_cast<const float4*>(x0 + k), p1 = *reinterpret_cast<const float4*>(x1 + k);
+      const float4 q0 = *reinterpret_cast<const float4*>(y0 + k), q1 = *reinterpret_cast<const float4*>(y1 + k);
+      const float xa[2][4] = {{p0.x, p0.y, p0.z, p0.w}, {p1.x, p1.y, p1.z, p1.w}};
+      const float ya[2][4] = {{q0.x, q0.y, q0.z, q0.w}, {q1.x, q1.y, q1.z, q1.w}};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float t;
+        t = xa[0][e] - ya[0][e]; a00 = fmaf(t, t, a00);
+        t = xa[0][e] - ya[1][e]; a01 = fmaf(t, t, a01);
+        t = xa[1][e] - ya[0][e]; a10 = fmaf(t, t, a10);
+        t = xa[1][e] - ya[1][e]; a11 = fmaf(t, t, a11);
+      }
+    }
+  } else {
+    for (int k = 0; k < dim; ++k) {
+      float t;
+      t = x0[k] - y0[k]; a00 = fmaf(t, t, a00);
+      t = x0[k] - y1[k]; a01 = fmaf(t, t, a01);
+      t = x1[k] - y0[k]; a10 = fmaf(t, t, a10);
+      t = x1[k] - y1[k]; a11 = fmaf(t, t, a11);
+    }
   }
-  return scale * acc;
+  o[0] = scale * a00; o[1] = scale * a01; o[2] = scale * a10; o[3] = scale * a11;
 }
 
 struct PairView {
@@ -74,9 +102,16 @@ __device__ void solve_small(const PairView& P, int dim, float scale, float inv_e
   float* v = u + kSmallN;
   float* a = v + kSmallN;
   float* b = a + kSmallN;
-  for (int e = lane; e < P.ni * P.nj; e += 32) {
-    const int r = e / P.nj, c = e % P.nj;
-    K[r * kSmallKS + c] = expf(-point_cost(P.X + (int64_t)r * dim, P.Y + (int64_t)c * dim, dim, scale) * inv_eps);
+  const int rb = (P.ni + 1) >> 1, cb = (P.nj + 1) >> 1;
+  for (int e = lane; e < rb * cb; e += 32) {
+    const int r0 = 2 * (e / cb), c0 = 2 * (e % cb);
+    float cc[4];
+    cost2x2(P.X, P.Y, dim, r0, c0, P.ni, P.nj, scale, cc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + (q >> 1), c = c0 + (q & 1);
+      if (r < P.ni && c < P.nj) K[r * kSmallKS + c] = expf(-cc[q] * inv_eps);
+    }
   }
   for (int r = lane; r < kSmallN; r += 32) {
     a[r] = r < P.ni ? P.a[r] : 0.0f;
@@ -99,10 +134,15 @@ __device__ void solve_small(const PairView& P, int dim, float scale, float inv_e
     __syncwarp();
   }
   double acc = 0.0;                                 // <diag(u) K diag(v), C>
-  for (int e = lane; e < P.ni * P.nj; e += 32) {
-    const int r = e / P.nj, c = e % P.nj;
-    const float C = point_cost(P.X + (int64_t)r * dim, P.Y + (int64_t)c * dim, dim, scale);
-    acc += (double)(u[r] * K[r * kSmallKS + c]) * (double)C * (double)v[c];
+  for (int e = lane; e < rb * cb; e += 32) {
+    const int r0 = 2 * (e / cb), c0 = 2 * (e % cb);
+    float cc[4];
+    cost2x2(P.X, P.Y, dim, r0, c0, P.ni, P.nj, scale, cc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + (q >> 1), c = c0 + (q & 1);
+      if (r < P.ni && c < P.nj) acc += (double)(u[r] * K[r * kSmallKS + c]) * (double)cc[q] * (double)v[c];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -121,9 +161,16 @@ __device__ void solve_large(const PairView& P, int dim, float scale, float inv_e
   float* Ks = v + max_n;
   const int64_t nk = (int64_t)P.ni * P.nj;
   float* K = nk <= sm_k_cap ? Ks : slot;
-  for (int64_t e = tid; e < nk; e += kThreads) {
-    const int r = (int)(e / P.nj), c = (int)(e % P.nj);
-    K[e] = expf(-point_cost(P.X + (int64_t)r * dim, P.Y + (int64_t)c * dim, dim, scale) * inv_eps);
+  const int rb = (P.ni + 1) >> 1, cb = (P.nj + 1) >> 1;
+  for (int64_t e = tid; e < (int64_t)rb * cb; e += kThreads) {
+    const int r0 = 2 * (int)(e / cb), c0 = 2 * (int)(e % cb);
+    float cc[4];
+    cost2x2(P.X, P.Y, dim, r0, c0, P.ni, P.nj, scale, cc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + (q >> 1), c = c0 + (q & 1);
+      if (r < P.ni && c < P.nj) K[(int64_t)r * P.nj + c] = expf(-cc[q] * inv_eps);
+    }
   }
   for (int c = tid; c < P.nj; c += kThreads) v[c] = 1.0f;
   __syncthreads();
@@ -164,10 +211,16 @@ __device__ void solve_large(const PairView& P, int dim, float scale, float inv_e
     __syncthreads();
   }
   double acc = 0.0;
-  for (int64_t e = tid; e < nk; e += kThreads) {
-    const int r = (int)(e / P.nj), c = (int)(e % P.nj);
-    const float C = point_cost(P.X + (int64_t)r * dim, P.Y + (int64_t)c * dim, dim, scale);
-    acc += (double)(u[r] * K[e]) * (double)C * (double)v[c];
+  for (int64_t e = tid; e < (int64_t)rb * cb; e += kThreads) {
+    const int r0 = 2 * (int)(e / cb), c0 = 2 * (int)(e % cb);
+    float cc[4];
+    cost2x2(P.X, P.Y, dim, r0, c0, P.ni, P.nj, scale, cc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + (q >> 1), c = c0 + (q & 1);
+      if (r < P.ni && c < P.nj)
+        acc += (double)(u[r] * K[(int64_t)r * P.nj + c]) * (double)cc[q] * (double)v[c];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
