@@ -310,6 +310,7 @@ def main():
     n_tiles = asot.num_tiles(inp.n_dist)
     launches = [0]
 
+    exchange_note = ["single GPU: no exchange"]
     if (args.mapping != "onehot" or args.anchors != "seeded") and world > 1:
         raise SystemExit("--mapping ml/dl and --anchors kmeans are single-GPU in this build")
     km_events = []
@@ -382,9 +383,22 @@ def main():
             return inner
 
         steps_impl = D_.DistSteps(counted(steps_impl.map_range), counted(steps_impl.tiles),
-                                  counted(steps_impl.unpack), counted(steps_impl.zero_diag))
+                                  counted(steps_impl.unpack), counted(steps_impl.zero_diag),
+                                  counted(steps_impl.tiles_into))
+        # result exchange: NVLink stores from the Sinkhorn epilogue into rank 0's symmetric-memory
+        # matrix (one kernel does compute + "gather"); NCCL all-gather + unpack as the fallback
+        p2p = None
+        if os.environ.get("ASOT_RESULT_EXCHANGE", "p2p") == "p2p":
+            try:
+                p2p = D_.P2PResult(inp.n_dist, dev)
+                exchange_note[0] = "p2p: NVLink stores into rank 0's symmetric-memory matrix"
+            except Exception as exc:  # noqa: BLE001 - report and fall back
+                exchange_note[0] = f"nccl all-gather + unpack (symmetric memory unavailable: {exc!s:.80})"
 
         def step():
+            if p2p is not None:
+                return D_.distance_matrix_distributed_p2p(inp.n_dist, inp.n_anchors, inp.offsets,
+                                                          n_tiles, steps_impl, p2p, device=dev)
             return D_.distance_matrix_distributed(inp.n_dist, inp.n_anchors, inp.offsets, n_tiles,
                                                   steps_impl, device=dev)
 
@@ -681,6 +695,7 @@ def main():
             "dtype": "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind == 3 else "f32"),
             "data": "synthetic",
             "config": workload_config(inp, args, world),
+            "result_exchange": exchange_note[0],
             "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "eot_baseline": eot_base,
             "exact_asot": exact,
             "cpu_baseline": cpu, "e2e": e2e,

@@ -348,9 +348,12 @@ def distance_matrix(points: Optional[torch.Tensor], offsets: Optional[torch.Tens
                     assign_out: Optional[torch.Tensor] = None, hist_out: Optional[torch.Tensor] = None,
                     offsets_host: Optional[np.ndarray] = None, cost_max: Optional[float] = None,
                     status: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
-                    stream=None):
+                    stream=None, out_ptr: Optional[int] = None):
     """Full pipeline a1-a6.  Returns the N x N matrix (when want_matrix) and/or fills `packed`
-    ([(tile_end - tile_begin) * 128] slot-ordered results) for the tile range."""
+    ([(tile_end - tile_begin) * 128] slot-ordered results) for the tile range.  `out_ptr` (with
+    want_matrix=False) is a raw device address of an N x N f32 matrix to write the range's pairs
+    into -- e.g. a peer GPU's symmetric-memory buffer, so the results travel as NVLink stores
+    straight from the Sinkhorn epilogue (distributed.py)."""
     _need_cuda(cost, hist, points, offsets, weights, anchors)
     _need_f32(cost, hist, points, weights, anchors)
     L = _lib_handle()
@@ -375,9 +378,10 @@ def distance_matrix(points: Optional[torch.Tensor], offsets: Optional[torch.Tens
     cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
     st = new_status(dev) if status is None else status
     ws = _ws(workspace, dev).get(L.asot_distance_matrix_workspace_bytes(N, T, K, int(precision)))
+    out_addr = _ptr(out) if out is not None else out_ptr
     _check(L.asot_distance_matrix(
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, d, _ptr(anchors), K, _ptr(cost),
-        cmax, float(eps), int(iters), int(precision), _ptr(hist), t0, t1, _ptr(out), _ptr(packed),
+        cmax, float(eps), int(iters), int(precision), _ptr(hist), t0, t1, out_addr, _ptr(packed),
         _ptr(assign_out), _ptr(hist_out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))
     return out
 

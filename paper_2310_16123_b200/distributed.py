@@ -1,5 +1,13 @@
 """Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL) process groups.
 
+Result exchange, two forms:
+  * "p2p" (default on GPUs): rank 0's N x N matrix is a torch symmetric-memory buffer; every rank
+    passes rank 0's buffer address as the Sinkhorn kernel's output, so each pair's distance leaves
+    the epilogue as an NVLink store into rank 0's matrix -- the compute and the "gather" are one
+    kernel, no packed buffers, no collective, no unpack; a barrier then publishes the matrix.
+  * "nccl": packed slot-ordered tiles, NCCL all-gather, KN6 unpack on rank 0 (also the CPU/gloo
+    test form, and the fallback when symmetric memory is unavailable).
+
 The pair set (Def. 1) is embarrassingly parallel: rank r owns a contiguous range of
 the upper-triangular pair tiles (step a4; every tile costs the same 2L+1 dense MMA phases, so
 equal tile counts are equal work).  There are exactly two exchanges:
@@ -47,6 +55,51 @@ def partition_by_points(offsets: np.ndarray, world: int) -> list[tuple[int, int]
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
+class P2PResult:
+    """Rank 0's N x N result matrix in torch symmetric memory, mapped into every rank."""
+
+    def __init__(self, n_dist: int, device: torch.device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.D = symm_mem.empty(n_dist, n_dist, dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self.D, group if group is not None else dist.group.WORLD)
+        self.root_ptr = int(self.handle.buffer_ptrs[0])
+
+
+def distance_matrix_distributed_p2p(n_dist: int, n_anchors: int, offsets_host: np.ndarray,
+                                    n_tiles: int, steps: "DistSteps", result: P2PResult, group=None,
+                                    device: Optional[torch.device] = None,
+                                    hist: Optional[torch.Tensor] = None):
+    """As distance_matrix_distributed, but every rank's Sinkhorn epilogue stores its pairs straight
+    into rank 0's symmetric-memory matrix (NVLink stores); returns that matrix on rank 0."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    H = _gather_hist(n_anchors, offsets_host, steps, world, rank, dev, group) if hist is None else hist
+    t0, t1 = partition_even(n_tiles, world)[rank]
+    if t1 > t0:
+        steps.tiles_into(H, t0, t1, result.root_ptr)
+    torch.cuda.current_stream().synchronize()   # this rank's stores have landed
+    dist.barrier(group=group)                    # ... and every other rank's
+    if rank != 0:
+        return None
+    steps.zero_diag(result.D)
+    return result.D
+
+
+def _gather_hist(n_anchors, offsets_host, steps, world, rank, dev, group):
+    """Exchange 1: partitioned mapping + NCCL all-gather of H (rows padded to equal counts)."""
+    ranges = partition_by_points(offsets_host, world)
+    rows = max(b - a for a, b in ranges)
+    lo, hi = ranges[rank]
+    H_local = torch.zeros((rows, n_anchors), dtype=torch.float32, device=dev)
+    if hi > lo:
+        H_local[: hi - lo] = steps.map_range(lo, hi)
+    H_all = torch.empty((world * rows, n_anchors), dtype=torch.float32, device=dev)
+    dist.all_gather_into_tensor(H_all, H_local, group=group)
+    return torch.cat([H_all[r * rows: r * rows + (b - a)] for r, (a, b) in enumerate(ranges)])
+
+
 @dataclass
 class DistSteps:
     """Compute steps used by distance_matrix_distributed (device or test stand-ins)."""
@@ -54,6 +107,7 @@ class DistSteps:
     tiles: Callable[[torch.Tensor, int, int], torch.Tensor]  # (H, t0, t1) -> packed [(t1-t0)*128]
     unpack: Callable[[torch.Tensor, int, int, torch.Tensor], None]  # (packed, t0, t1, D) in place
     zero_diag: Callable[[torch.Tensor], None]
+    tiles_into: Optional[Callable[[torch.Tensor, int, int, int], None]] = None  # (H, t0, t1, D address)
 
 
 def distance_matrix_distributed(n_dist: int, n_anchors: int, offsets_host: np.ndarray,
@@ -66,18 +120,7 @@ def distance_matrix_distributed(n_dist: int, n_anchors: int, offsets_host: np.nd
     dev = device if device is not None else torch.device("cpu")
 
     # exchange 1: partitioned mapping + all-gather of H (rows padded to equal counts)
-    if hist is None:
-        ranges = partition_by_points(offsets_host, world)
-        rows = max(b - a for a, b in ranges)
-        lo, hi = ranges[rank]
-        H_local = torch.zeros((rows, n_anchors), dtype=torch.float32, device=dev)
-        if hi > lo:
-            H_local[: hi - lo] = steps.map_range(lo, hi)
-        H_all = torch.empty((world * rows, n_anchors), dtype=torch.float32, device=dev)
-        dist.all_gather_into_tensor(H_all, H_local, group=group)
-        H = torch.cat([H_all[r * rows: r * rows + (b - a)] for r, (a, b) in enumerate(ranges)])
-    else:
-        H = hist
+    H = _gather_hist(n_anchors, offsets_host, steps, world, rank, dev, group) if hist is None else hist
 
     # the rank's contiguous share of the upper-triangular tiles
     tranges = partition_even(n_tiles, world)
@@ -131,4 +174,9 @@ def cuda_steps(points: torch.Tensor, offsets: torch.Tensor, offsets_host: np.nda
     def zero_diag(D: torch.Tensor) -> None:  # KN6 with an empty tile range: diagonal only
         A.unpack_tiles(D, D.shape[0], 0, 0, D, zero_diag=True)
 
-    return DistSteps(map_range, tiles, unpack, zero_diag)
+    def tiles_into(H: torch.Tensor, t0: int, t1: int, d_addr: int) -> None:
+        A.distance_matrix(None, None, None, None, cost, eps, iters, precision=precision, hist=H,
+                          tile_range=(t0, t1), want_matrix=False, out_ptr=d_addr,
+                          cost_max=cost_max, status=status, workspace=workspace)
+
+    return DistSteps(map_range, tiles, unpack, zero_diag, tiles_into)

@@ -266,6 +266,14 @@ def test_distributed_path_single_rank_nccl(asot, cfg, n):
                                             asot.num_tiles(inp.n_dist), steps, device=torch.device("cuda", 0))
         torch.cuda.synchronize()
         assert torch.equal(D1, D2)
+        # p2p form: the Sinkhorn epilogue stores into rank 0's symmetric-memory matrix
+        res = D_.P2PResult(inp.n_dist, torch.device("cuda", 0))
+        res.D.fill_(-1.0)
+        D3 = D_.distance_matrix_distributed_p2p(inp.n_dist, inp.n_anchors, inp.offsets,
+                                                asot.num_tiles(inp.n_dist), steps, res,
+                                                device=torch.device("cuda", 0))
+        torch.cuda.synchronize()
+        assert torch.equal(D1, D3)
     finally:
         if created:
             dist.destroy_process_group()
