@@ -461,7 +461,7 @@ def main():
     pairs_per_launch = P if world == 1 else -(-P // world)
     peaks = measured_peaks()
     kind = asot.asot.sinkhorn_kernel_kind(inp.n_anchors, prec)
-    if kind == 3:
+    if kind in (3, 5):
         peak = peaks["bf16_tflops"] * TF32_OVER_BF16 / 3
         bound, peak_note = "tensor", (f"3xTF32: dense TF32 ({peaks['_source']} bf16 {peaks['bf16_tflops']} "
                                       f"TFLOP/s burst x 1.1/2.25) / 3 MMAs per algorithmic product")
@@ -692,7 +692,7 @@ def main():
             "metric": baseline_metric(), "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind == 3 else "f32"),
+            "dtype": "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind in (3, 5) else "f32"),
             "data": "synthetic",
             "config": workload_config(inp, args, world),
             "result_exchange": exchange_note[0],

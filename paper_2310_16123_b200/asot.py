@@ -88,11 +88,13 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 1: "sinkhorn_tc_kernel (TF32, 1 SM, M=128)",
                 2: "sinkhorn_tc2_kernel (TF32, CTA pair, cta_group::2, M=256)",
                 3: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128)",
-                4: "sinkhorn_tc4_kernel (TF32, streamed GEMM form, CTA pair, M=N=256)"}
+                4: "sinkhorn_tc4_kernel (TF32, streamed GEMM form, CTA pair, M=N=256)",
+                5: "sinkhorn_tc5_kernel (3xTF32 fp32-accurate, streamed GEMM form, CTA pair, M=N=256)"}
 
 
 def sinkhorn_kernel_kind(n_anchors: int, precision: int) -> int:
-    """0 SIMT fp32, 1 TF32 1-SM, 2 TF32 CTA pair, 3 3xTF32, 4 TF32 streamed (see asot.h)."""
+    """0 SIMT fp32, 1 TF32 1-SM, 2 TF32 CTA pair, 3 3xTF32 1-SM, 4 TF32 streamed, 5 3xTF32
+    streamed (see asot.h)."""
     return int(_lib_handle().asot_sinkhorn_kernel_kind(int(n_anchors), int(precision)))
 
 

@@ -68,14 +68,16 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 
 // Tensor-core kernel selection: 0 = none (fp32 SIMT), 1 = single-CTA resident TF32 (K <= 128),
 // 2 = CTA-pair resident TF32 (128 < K <= 256), 4 = CTA-pair streamed TF32 (K <= 1024),
-// 3 = single-CTA resident 3xTF32 for fp32-accurate requests (K <= 128).
+// 3 = single-CTA resident 3xTF32 for fp32-accurate requests (K <= 128), 5 = CTA-pair streamed
+// 3xTF32 for fp32-accurate requests (128 < K <= 1024).
 // K < 32 stays on the fp32 kernel: the per-iteration TF32 rounding of u / v dominates the TF32
 // error (R#23) and a dot product over fewer than 32 anchors barely averages it out
 // (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
 constexpr int32_t kMinTcAnchors = 32;
 int tc_kind(int32_t K, asot_precision prec) {
   if (K < kMinTcAnchors) return 0;
-  if (prec == ASOT_PREC_FP32) return asot::sinkhorn_tc3_supported(K) ? 3 : 0;
+  if (prec == ASOT_PREC_FP32)
+    return asot::sinkhorn_tc3_supported(K) ? 3 : asot::sinkhorn_tc5_supported(K) ? 5 : 0;
   if (prec != ASOT_PREC_TF32) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
@@ -105,7 +107,10 @@ struct GibbsBufs {
 GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   GibbsBufs b;
   b.kind = kind;
-  if (kind == 4) {
+  if (kind == 5) {  // K_hi, K_lo, (K (.) C_s)_hi, (K (.) C_s)_lo images + marginals / X scratch
+    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc5_image_bytes(K));
+    b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc5_scratch_bytes(K, n_dist, device_sms()) + 1024);
+  } else if (kind == 4) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes());
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes());
     b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc4_scratch_bytes(n_dist, device_sms()) + 1024);
@@ -167,7 +172,9 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
                          cudaStream_t s) {
   const int kind = gb.kind;
-  if (kind == 4) {
+  if (kind == 5) {
+    ASOT_LAUNCH(asot::launch_gibbs_prep_tc5(cost, K, eps, (uint8_t*)gb.g_img, s));
+  } else if (kind == 4) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc4(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
@@ -180,7 +187,10 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_simt(cost, K, eps, gb.G, gb.GC, s));
   }
   ProfScope prof(ASOT_PROF_SINKHORN, s);
-  if (kind == 4) {
+  if (kind == 5) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc5(tile_begin, tile_end, ps.n_dist, sink, H, K, (const uint8_t*)gb.g_img,
+                                          (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
+  } else if (kind == 4) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img,
                                           (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
@@ -240,8 +250,8 @@ int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {
 }
 
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
-  return tc_kind(n_anchors, requested) == 0 || tc_kind(n_anchors, requested) == 3 ? ASOT_PREC_FP32
-                                                                                 : ASOT_PREC_TF32;
+  const int kind = tc_kind(n_anchors, requested);
+  return kind == 0 || kind == 3 || kind == 5 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;
 }
 
 asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,

@@ -174,6 +174,13 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
 cudaError_t launch_mahalanobis_cost(const float* anchors, int K, int d, const float* M, int h,
                                     bool normalize, float* Y, float* C, cudaStream_t s);
 cudaError_t launch_normalize_by_max(float* C, int64_t n, cudaStream_t s);
+bool sinkhorn_tc5_supported(int K);
+size_t sinkhorn_tc5_image_bytes(int K);
+size_t sinkhorn_tc5_scratch_bytes(int K, int64_t n_dist, int sms);
+cudaError_t launch_gibbs_prep_tc5(const float* cost, int K, float eps, uint8_t* img, cudaStream_t s);
+cudaError_t launch_sinkhorn_tc5(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint8_t* img, uint8_t* scratch, int iters,
+                                cudaStream_t s);
 bool sinkhorn_tc3_supported(int K);
 size_t sinkhorn_tc3_image_bytes(int K);
 cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t* ghi, uint32_t* glo,
