@@ -259,6 +259,9 @@ def main():
                     help="NEXT-3: also solve exact anchor-space OT on a seeded pair sample and report "
                          "its pairs/s and the eASOT-vs-exact gap")
     ap.add_argument("--exact-pairs", type=int, default=20000)
+    ap.add_argument("--pairs-api", action="store_true",
+                    help="also time asot_pairwise_sinkhorn (SPEC batched_sinkhorn_fixed) on the whole "
+                         "upper triangle given as an explicit (shuffled) pair list")
     ap.add_argument("--mapping", default="onehot", choices=["onehot", "ml", "dl"],
                     help="P: one-hot nearest anchor (the north-star path), or the NEXT-1 soft "
                          "mappings ASOT-ML / ASOT-DL (seeded parameters)")
@@ -577,6 +580,31 @@ def main():
                              "asot_vs_eot_rel_p90": float(np.quantile(rel, 0.9)),
                              "eot_mean_distance": float(de.mean())})
 
+    # ---- the explicit pair-list entry point on the same work (shuffled list of all i < j)
+    pairs_api = None
+    if args.pairs_api and rank == 0 and world == 1:
+        _, Hq, _ = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+        iu, ju = np.triu_indices(inp.n_dist, k=1)
+        perm = np.random.default_rng(5).permutation(iu.shape[0])
+        qi, qj = t(iu[perm].astype(np.int32)), t(ju[perm].astype(np.int32))
+        qst = asot.asot.new_status(dev)
+        asot.pairwise_sinkhorn(Hq, cst, float(inp.eps), inp.iters, qi, qj, precision=prec, cost_max=cmax,
+                               status=qst, workspace=ws)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dq = asot.pairwise_sinkhorn(Hq, cst, float(inp.eps), inp.iters, qi, qj, precision=prec,
+                                    cost_max=cmax, status=qst, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        asot.check_status(qst)
+        ms = e0.elapsed_time(e1)
+        same = Dres[qi.long(), qj.long()]
+        pairs_api = {"api": "asot_pairwise_sinkhorn (explicit shuffled list of all pairs)",
+                     "ms": ms, "pairs_per_s": inp.n_pairs / (ms / 1e3),
+                     "tflops": flops_per_pair * inp.n_pairs / (ms / 1e3) / 1e12,
+                     "max_rel_diff_vs_tile_path": float(((dq - same).abs() / same.clamp_min(1e-3)).max())}
+
     # ---- NEXT-3: exact ASOT (eps -> 0 limit) on a pair sample, same GPU
     exact = None
     if args.exact and rank == 0 and world == 1:
@@ -697,7 +725,7 @@ def main():
             "config": workload_config(inp, args, world),
             "result_exchange": exchange_note[0],
             "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "eot_baseline": eot_base,
-            "exact_asot": exact,
+            "exact_asot": exact, "pairs_api": pairs_api,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
             "wall_s_timed_region": wall,

@@ -96,7 +96,11 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
                                 int32_t n_anchors, int32_t* assign_out, float* hist_out,
                                 uint32_t* status, void* stream);
 
-/* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed):
+/* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed).
+ * K >= 32: the streamed tcgen05 kernel in pair-list mode (ASOT_PREC_TF32: one TF32 pass;
+ * ASOT_PREC_FP32: 3xTF32), tiles of 128 consecutive list entries, marginals read from the
+ * L2-resident H rows; K < 32: the fp32 CUDA-core kernel.  Workspace from
+ * asot_pairwise_workspace_bytes(n_dist, n_anchors, prec).  Arguments:
  *   hist     [n_dist, n_anchors] f32 device (rows are a' / b')
  *   cost     [n_anchors, n_anchors] f32 device: C_s symmetric, >= 0, zero diagonal
  *   eps > 0 (max(C_s)/eps <= 80 is checked against cost_max, a host value the caller supplies:
@@ -109,7 +113,7 @@ asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_
                                    const int32_t* pair_j, int64_t n_pairs, float* dist_out,
                                    uint32_t* status, void* workspace, size_t workspace_bytes,
                                    void* stream);
-size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec);
+size_t asot_pairwise_workspace_bytes(int64_t n_dist, int32_t n_anchors, asot_precision prec);
 
 /* Full pipeline a1-a6 on the tile range [tile_begin, tile_end) (device buffers):
  *   hist_in  NULL: map + histogram all distributions into the workspace first (needs points,
@@ -253,7 +257,8 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
 /* Which Sinkhorn kernel asot_distance_matrix runs for (K, request): 0 = fp32 CUDA-core kernel,
  * 1 = TF32 1-SM resident (K <= 128), 2 = TF32 CTA pair (K <= 256), 3 = 3xTF32 fp32-accurate
  * 1-SM resident (ASOT_PREC_FP32, 32 <= K <= 128), 4 = TF32 CTA-pair streamed (K <= 1024),
- * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024). */
+ * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024),
+ * 6 = one-pass TF32 CTA-pair streamed with K padded to 512 (256 < K <= 512). */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 
 /* Optional kernel timing (bench.py's roofline): while enabled on this thread, the library records

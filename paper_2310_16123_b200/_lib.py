@@ -29,7 +29,7 @@ _SIGS = {
                                     c_vp, c_vp]),
     "asot_pairwise_sinkhorn": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_f32, c_f32, c_i32, c_i32, c_vp,
                                        c_vp, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
-    "asot_pairwise_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "asot_pairwise_workspace_bytes": (c_size, [c_i64, c_i32, c_i32]),
     "asot_distance_matrix": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_f32,
                                      c_f32, c_i32, c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                      c_vp, c_vp, c_vp, c_size, c_vp]),

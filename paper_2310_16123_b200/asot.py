@@ -89,7 +89,8 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 2: "sinkhorn_tc2_kernel (TF32, CTA pair, cta_group::2, M=256)",
                 3: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128)",
                 4: "sinkhorn_tc4_kernel (TF32, streamed GEMM form, CTA pair, M=N=256)",
-                5: "sinkhorn_tc5_kernel (3xTF32 fp32-accurate, streamed GEMM form, CTA pair, M=N=256)"}
+                5: "sinkhorn_tc5_kernel (3xTF32 fp32-accurate, streamed GEMM form, CTA pair, M=N=256)",
+                6: "sinkhorn_tc5_kernel (TF32, streamed GEMM form, K padded to 512, CTA pair, M=N=256)"}
 
 
 def sinkhorn_kernel_kind(n_anchors: int, precision: int) -> int:
@@ -334,7 +335,7 @@ def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: in
     cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
     st = new_status(H.device) if status is None else status
     L = _lib_handle()
-    ws = _ws(workspace, H.device).get(L.asot_pairwise_workspace_bytes(int(K), int(precision)))
+    ws = _ws(workspace, H.device).get(L.asot_pairwise_workspace_bytes(int(N), int(K), int(precision)))
     _check(L.asot_pairwise_sinkhorn(
         _ptr(H), N, int(K), _ptr(cost), cmax, float(eps), int(iters), int(precision),
         _ptr(pair_i), _ptr(pair_j), n, _ptr(out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))

@@ -69,7 +69,8 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 // Tensor-core kernel selection: 0 = none (fp32 SIMT), 1 = single-CTA resident TF32 (K <= 128),
 // 2 = CTA-pair resident TF32 (128 < K <= 256), 4 = CTA-pair streamed TF32 (K <= 1024),
 // 3 = single-CTA resident 3xTF32 for fp32-accurate requests (K <= 128), 5 = CTA-pair streamed
-// 3xTF32 for fp32-accurate requests (128 < K <= 1024).
+// 3xTF32 for fp32-accurate requests (128 < K <= 1024), 6 = CTA-pair streamed one-pass TF32 with
+// K padded to 512 (256 < K <= 512; kind 4 pads to 1024).
 // K < 32 stays on the fp32 kernel: the per-iteration TF32 rounding of u / v dominates the TF32
 // error (R#23) and a dot product over fewer than 32 anchors barely averages it out
 // (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
@@ -81,8 +82,15 @@ int tc_kind(int32_t K, asot_precision prec) {
   if (prec != ASOT_PREC_TF32) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
+  if (K <= 512) return 6;
   if (asot::sinkhorn_tc4_supported(K)) return 4;
   return 0;
+}
+// Explicit pair lists (asot_pairwise_sinkhorn): the streamed kernel in pair-list mode (3xTF32 for
+// fp32 requests, one TF32 pass otherwise) for K >= 32, the CUDA-core kernel below.
+int pair_kind(int32_t K, asot_precision prec) {
+  if (K < kMinTcAnchors || K > asot::kMaxAnchors) return 0;
+  return prec == ASOT_PREC_FP32 ? 5 : 6;
 }
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
 
@@ -107,7 +115,7 @@ struct GibbsBufs {
 GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   GibbsBufs b;
   b.kind = kind;
-  if (kind == 5) {  // K_hi, K_lo, (K (.) C_s)_hi, (K (.) C_s)_lo images + marginals / X scratch
+  if (kind == 5 || kind == 6) {  // K_hi, K_lo, (K (.) C_s)_hi, _lo images + marginals / X scratch
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc5_image_bytes(K));
     b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc5_scratch_bytes(K, n_dist, device_sms()) + 1024);
   } else if (kind == 4) {
@@ -172,7 +180,7 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
                          cudaStream_t s) {
   const int kind = gb.kind;
-  if (kind == 5) {
+  if (kind == 5 || kind == 6) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc5(cost, K, eps, (uint8_t*)gb.g_img, s));
   } else if (kind == 4) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc4(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
@@ -187,9 +195,13 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_simt(cost, K, eps, gb.G, gb.GC, s));
   }
   ProfScope prof(ASOT_PROF_SINKHORN, s);
-  if (kind == 5) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc5(tile_begin, tile_end, ps.n_dist, sink, H, K, (const uint8_t*)gb.g_img,
-                                          (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
+  if (kind == 5 || kind == 6) {
+    const bool expl = ps.pi != nullptr;   // pair-list mode: tiles of 128 list entries
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc5(expl ? 0 : tile_begin,
+                                          expl ? (ps.n_slots + asot::kTileSlots - 1) / asot::kTileSlots : tile_end,
+                                          ps.n_dist, sink, ps, H, K, (const uint8_t*)gb.g_img,
+                                          (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters,
+                                          kind == 5, s));
   } else if (kind == 4) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img,
@@ -251,7 +263,7 @@ int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {
 
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
   const int kind = tc_kind(n_anchors, requested);
-  return kind == 0 || kind == 3 || kind == 5 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;
+  return kind == 0 || kind == 3 || kind == 5 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;   // (6: TF32)
 }
 
 asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
@@ -439,10 +451,9 @@ asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_a
   return ASOT_OK;
 }
 
-size_t asot_pairwise_workspace_bytes(int32_t n_anchors, asot_precision prec) {
+size_t asot_pairwise_workspace_bytes(int64_t n_dist, int32_t n_anchors, asot_precision prec) {
   Carver cv{nullptr, 0};
-  (void)prec;
-  carve_gibbs(cv, n_anchors, 0, 0);  // explicit pair lists run on the fp32 SIMT kernel
+  carve_gibbs(cv, n_anchors, pair_kind(n_anchors, prec), n_dist);
   return cv.used;
 }
 
@@ -458,9 +469,8 @@ asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_
   if (st != ASOT_OK) return st;
   ASOT_CHECK_ARG(n_pairs >= 0, "n_pairs must be >= 0");
   if (n_pairs == 0) return ASOT_OK;
-  (void)prec;
   Carver cv{(char*)workspace, workspace_bytes};
-  GibbsBufs gb = carve_gibbs(cv, n_anchors, 0, 0);
+  GibbsBufs gb = carve_gibbs(cv, n_anchors, pair_kind(n_anchors, prec), n_dist);
   if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
   asot::PairSource ps{pair_i, pair_j, n_pairs, 0, n_dist};
   asot::PairSink sink{dist_out, nullptr, n_dist, status};

@@ -179,8 +179,8 @@ size_t sinkhorn_tc5_image_bytes(int K);
 size_t sinkhorn_tc5_scratch_bytes(int K, int64_t n_dist, int sms);
 cudaError_t launch_gibbs_prep_tc5(const float* cost, int K, float eps, uint8_t* img, cudaStream_t s);
 cudaError_t launch_sinkhorn_tc5(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
-                                const float* H, int K, const uint8_t* img, uint8_t* scratch, int iters,
-                                cudaStream_t s);
+                                const PairSource& ps, const float* H, int K, const uint8_t* img,
+                                uint8_t* scratch, int iters, bool split3, cudaStream_t s);
 bool sinkhorn_tc3_supported(int K);
 size_t sinkhorn_tc3_image_bytes(int K);
 cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t* ghi, uint32_t* glo,

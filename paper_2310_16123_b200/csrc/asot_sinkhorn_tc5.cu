@@ -13,6 +13,11 @@
 // flag like the fp32 kernel), splits it and writes X_hi / X_lo of the next phase to per-CTA
 // ping-pong images in global memory (L2-resident for KP = 256: 0.5 MB per CTA); the last phase
 // multiplies v_L by K (.) C_s and reduces against u_L = hi + lo read back from global.
+//
+// Template variants: SPLIT = 3 (the fp32-accurate path above) or 1 (one TF32 pass: stages [X | K],
+// 6 deep; the TF32 path for 256 < K <= 512 without padding to 1024), and EXPLICIT (pairs from an
+// explicit (pair_i, pair_j) list -- SPEC batched_sinkhorn_fixed, asot_pairwise_sinkhorn -- with
+// the marginals read per thread from the L2-resident padded H rows instead of staged per tile).
 #include <cfloat>
 #include <cstdlib>
 
@@ -27,9 +32,14 @@ using namespace ::asot::ptx;
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = kEpiThreads + 64;   // + producer warp + MMA (leader) / relay (peer) warp
-constexpr int kStages = 3;
 constexpr uint32_t kChunk = 16384;           // 128 rows x 128 B (32 anchors, fp32)
-constexpr uint32_t kStageBytes = 4 * kChunk; // A_hi, A_lo, B_hi, B_lo
+constexpr uint32_t kStageRegion = 196608;    // 192 KB of stages: 3 x [A_hi|A_lo|B_hi|B_lo] or 6 x [A|B]
+
+template <int SPLIT>
+struct Pipe {
+  static constexpr uint32_t kStageBytes = (SPLIT == 3 ? 4u : 2u) * kChunk;
+  static constexpr int kStages = (int)(kStageRegion / kStageBytes);
+};
 
 template <int KP>
 struct Cfg {
@@ -42,10 +52,10 @@ struct Cfg {
 struct Smem {
   static constexpr int kMRS = 256 + 4;                                   // marginal row stride
   static constexpr size_t kOffStage = 0;
-  static constexpr size_t kOffMarg = (size_t)kStages * kStageBytes;      // [16 rows][260] floats
+  static constexpr size_t kOffMarg = kStageRegion;                        // [16 rows][260] floats
   static constexpr size_t kOffRed = kOffMarg;                            // [4][128] (aliases marg)
   static constexpr size_t kOffBar = kOffMarg + (size_t)16 * kMRS * 4;
-  static constexpr size_t kBytes = kOffBar + 256 + 1024;
+  static constexpr size_t kBytes = kOffBar + 512 + 1024;
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
@@ -70,20 +80,22 @@ __host__ __device__ inline uint32_t b_offset(uint32_t pass, uint32_t r, uint32_t
   return (pass * (uint32_t)Cfg<KP>::KC + (k >> 5)) * kChunk + sw_rows(r, k & 31);
 }
 
-template <int KP>
+template <int KP, int SPLIT, bool EXPLICIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
+sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out, PairSource ps,
                     const float* __restrict__ Hp, int K, const uint8_t* __restrict__ g_hi,
                     const uint8_t* __restrict__ g_lo, const uint8_t* __restrict__ gc_hi,
                     const uint8_t* __restrict__ gc_lo, uint8_t* __restrict__ xbuf, int iters) {
   using S = Smem;
   using C = Cfg<KP>;
+  constexpr int kStages = Pipe<SPLIT>::kStages;
+  constexpr uint32_t kStageBytes = Pipe<SPLIT>::kStageBytes;
   constexpr uint32_t kIdesc = make_idesc_tf32(256, 256);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
   constexpr int S3 = 3 * kStages;
-  static_assert((S3 + 4) * 8 <= 256, "barrier area");
+  static_assert((S3 + 4) * 8 <= 512, "barrier area");
   uint32_t* tmem_holder = (uint32_t*)(bars + S3 + 3);
   const uint32_t bar_full = smem_u32(&bars[0]), bar_empty = smem_u32(&bars[kStages]);
   const uint32_t bar_peer = smem_u32(&bars[2 * kStages]), bar_done = smem_u32(&bars[S3]);
@@ -143,10 +155,15 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
               const uint32_t st = stage0 + s * kStageBytes;
               const size_t boff = (size_t)(pass * C::KC + kc) * kChunk;
               mbar_expect_tx(bar_full + 8 * s, kStageBytes);
-              bulk_g2s(st, xin_hi + kc * kChunk, kChunk, bar_full + 8 * s);
-              bulk_g2s(st + kChunk, xin_lo + kc * kChunk, kChunk, bar_full + 8 * s);
-              bulk_g2s(st + 2 * kChunk, bh + boff, kChunk, bar_full + 8 * s);
-              bulk_g2s(st + 3 * kChunk, bl + boff, kChunk, bar_full + 8 * s);
+              if (SPLIT == 3) {
+                bulk_g2s(st, xin_hi + kc * kChunk, kChunk, bar_full + 8 * s);
+                bulk_g2s(st + kChunk, xin_lo + kc * kChunk, kChunk, bar_full + 8 * s);
+                bulk_g2s(st + 2 * kChunk, bh + boff, kChunk, bar_full + 8 * s);
+                bulk_g2s(st + 3 * kChunk, bl + boff, kChunk, bar_full + 8 * s);
+              } else {
+                bulk_g2s(st, xin_hi + kc * kChunk, kChunk, bar_full + 8 * s);
+                bulk_g2s(st + kChunk, bh + boff, kChunk, bar_full + 8 * s);
+              }
             }
           }
         }
@@ -178,13 +195,16 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             if (elect_one()) {
               const uint32_t st = stage0 + s * kStageBytes;
               const uint64_t ahi = make_noswz_desc(st), alo = make_noswz_desc(st + kChunk);
-              const uint64_t bhi = make_sw128_desc(st + 2 * kChunk), blo = make_sw128_desc(st + 3 * kChunk);
+              const uint64_t bhi = make_sw128_desc(st + (SPLIT == 3 ? 2 : 1) * kChunk);
+              const uint64_t blo = make_sw128_desc(st + 3 * kChunk);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
                 const uint64_t ao = (uint64_t)((ks * 4096) >> 4), bo = (uint64_t)((ks * 32) >> 4);
                 mma2_tf32_ss(tmem_base, ahi + ao, bhi + bo, kIdesc, (kc | ks) ? 1u : 0u);
-                mma2_tf32_ss(tmem_base, alo + ao, bhi + bo, kIdesc, 1u);
-                mma2_tf32_ss(tmem_base, ahi + ao, blo + bo, kIdesc, 1u);
+                if (SPLIT == 3) {
+                  mma2_tf32_ss(tmem_base, alo + ao, bhi + bo, kIdesc, 1u);
+                  mma2_tf32_ss(tmem_base, ahi + ao, blo + bo, kIdesc, 1u);
+                }
               }
               mma2_commit_mc(bar_empty + 8 * s);
               if (kc == C::KC - 1) mma2_commit_mc(bar_done);
@@ -206,20 +226,30 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
       const int64_t t = 2 * b + rank;
       const bool t_in = t >= tile_begin && t < tile_end;
-      int ii, jj;
-      const bool valid = tile_slot_pair(t, p, n_dist, ii, jj) && t_in;
-      int64_t bi, bj;
-      block_pair_decode(b, num_blocks(n_dist), bi, bj);
-      const int64_t i0 = bi * kBlockDist + rank * 8, j0 = bj * kBlockDist;
-      // invalid slots read row 0 of the staged side (finite, discarded: MMA rows are independent)
+      int ii = 0, jj = 0;
+      bool valid;
+      int64_t i0 = 0, j0 = 0;
+      if (EXPLICIT) {
+        valid = t_in && decode_slot(ps, (t - tile_begin) * kTileSlots + p, ii, jj);
+      } else {
+        valid = tile_slot_pair(t, p, n_dist, ii, jj) && t_in;
+        int64_t bi, bj;
+        block_pair_decode(b, num_blocks(n_dist), bi, bj);
+        i0 = bi * kBlockDist + rank * 8;
+        j0 = bj * kBlockDist;
+      }
+      // invalid slots read row 0 of the staged side / the dummy row (finite, discarded: MMA rows
+      // are independent)
       const int arow_s = valid ? (p >> 4) : 0, brow_s = valid ? (p & 15) : 0;
+      const float* ha = Hp + (size_t)(valid ? ii : n_dist) * KP;   // EXPLICIT: padded H rows
+      const float* hb = Hp + (size_t)(valid ? jj : n_dist) * KP;
       // tile init: X of phase 0 = v0 = 1 on real anchors (hi = 1, lo = 0), anchors [g*KP/4, ...)
       for (int k = g * (KP / 4); k < (g + 1) * (KP / 4); k += 4) {
         uint32_t v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = (k + e < K) ? 0x3f800000u : 0u;
         stg128(ximg(0, 0) + x_offset(p, k), v[0], v[1], v[2], v[3]);
-        stg128(ximg(0, 1) + x_offset(p, k), 0u, 0u, 0u, 0u);
+        if (SPLIT == 3) stg128(ximg(0, 1) + x_offset(p, k), 0u, 0u, 0u, 0u);
       }
       fence_proxy_async_global();
       named_bar_sync(1, kEpiThreads);
@@ -231,7 +261,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         const int64_t row0 = (f & 1) ? j0 : i0;
         const float* mrow = marg + ((f & 1) ? brow_s : arow_s) * S::kMRS;
         for (int pass = 0; pass < C::NP; ++pass) {
-          if (!cost_phase) {
+          if (!cost_phase && !EXPLICIT) {
             // stage this pass's 256 marginal columns (<= 16 KB) while the pass's MMAs run
             for (int e = threadIdx.x; e < nrows * 64; e += kEpiThreads) {
               const int r = e >> 6, c4 = (e & 63) * 4;
@@ -248,6 +278,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
           const uint32_t col0 = (uint32_t)(pass * 256 + g * 64);   // anchor index of my first column
           uint8_t* xo_hi = ximg((f + 1) & 1, 0);
           uint8_t* xo_lo = ximg((f + 1) & 1, 1);
+          const float* hrow = (f & 1) ? hb : ha;   // EXPLICIT marginal row of this phase
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t d[16];
@@ -259,7 +290,8 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
               uint32_t hi[16], lo[16];
 #pragma unroll
               for (int e = 0; e < 16; e += 4) {
-                const float4 mq = *reinterpret_cast<const float4*>(mrow + g * 64 + c * 16 + e);
+                const float4 mq = EXPLICIT ? __ldg(reinterpret_cast<const float4*>(hrow + k0 + e))
+                                           : *reinterpret_cast<const float4*>(mrow + g * 64 + c * 16 + e);
                 const float mm[4] = {mq.x, mq.y, mq.z, mq.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -269,26 +301,36 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                     den = FLT_MIN;
                   }
                   const float x = mm[u] * rcp_approx(den);   // m = 0 -> exactly 0 (R#11)
-                  const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
-                  hi[e + u] = xh;
-                  lo[e + u] = __float_as_uint(x - __uint_as_float(xh));
+                  if (SPLIT == 3) {
+                    const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
+                    hi[e + u] = xh;
+                    lo[e + u] = __float_as_uint(x - __uint_as_float(xh));
+                  } else {
+                    hi[e + u] = tf32_rna_pre(x);   // the MMA truncates: RNA (read back masked)
+                    lo[e + u] = 0u;
+                  }
                 }
               }
 #pragma unroll
               for (int e = 0; e < 16; e += 4) {
                 stg128(xo_hi + x_offset(p, k0 + e), hi[e], hi[e + 1], hi[e + 2], hi[e + 3]);
-                stg128(xo_lo + x_offset(p, k0 + e), lo[e], lo[e + 1], lo[e + 2], lo[e + 3]);
+                if (SPLIT == 3) stg128(xo_lo + x_offset(p, k0 + e), lo[e], lo[e + 1], lo[e + 2], lo[e + 3]);
               }
             } else {
               // cost: D = v_L (K (.) C_s); u_L (side 1) = hi + lo
 #pragma unroll
               for (int e = 0; e < 16; e += 4) {
                 const float4 uh = *reinterpret_cast<const float4*>(ximg(1, 0) + x_offset(p, k0 + e));
-                const float4 ul = *reinterpret_cast<const float4*>(ximg(1, 1) + x_offset(p, k0 + e));
-                acc = fmaf(uh.x + ul.x, __uint_as_float(d[e]), acc);
-                acc = fmaf(uh.y + ul.y, __uint_as_float(d[e + 1]), acc);
-                acc = fmaf(uh.z + ul.z, __uint_as_float(d[e + 2]), acc);
-                acc = fmaf(uh.w + ul.w, __uint_as_float(d[e + 3]), acc);
+                float uu[4] = {uh.x, uh.y, uh.z, uh.w};
+                if (SPLIT == 3) {
+                  const float4 ul = *reinterpret_cast<const float4*>(ximg(1, 1) + x_offset(p, k0 + e));
+                  uu[0] += ul.x; uu[1] += ul.y; uu[2] += ul.z; uu[3] += ul.w;
+                } else {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) uu[u] = tf32_mask(uu[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = fmaf(uu[u], __uint_as_float(d[e + u]), acc);
               }
             }
           }
@@ -304,8 +346,9 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       float* red = (float*)(smem + S::kOffRed);
       red[g * 128 + p] = acc;
       named_bar_sync(1, kEpiThreads);
-      if (g == 0 && t_in)
-        write_result(out, (t - tile_begin) * kTileSlots + p, valid, ii, jj,
+      const int64_t slot = (t - tile_begin) * kTileSlots + p;
+      if (g == 0 && t_in && (!EXPLICIT || slot < ps.n_slots))
+        write_result(out, slot, valid, ii, jj,
                      (red[p] + red[128 + p]) + (red[256 + p] + red[384 + p]));
       named_bar_sync(1, kEpiThreads);  // red (aliases the marginal rows) reused by the next tile
     }
@@ -351,9 +394,10 @@ __global__ void pad_marginals_tc5_kernel(const float* __restrict__ H, int64_t n_
   }
 }
 
-template <int KP>
-cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out, const float* H,
-                      int K, const uint8_t* img, uint8_t* scratch, int iters, cudaStream_t s) {
+template <int KP, int SPLIT, bool EXPLICIT>
+cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                      const PairSource& ps, const float* H, int K, const uint8_t* img, uint8_t* scratch,
+                      int iters, cudaStream_t s) {
   using C = Cfg<KP>;
   float* Hp = (float*)scratch;
   uint8_t* xbuf = scratch + (((size_t)(n_dist + 1) * KP * 4 + 1023) & ~(size_t)1023);
@@ -361,7 +405,8 @@ cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dist, cons
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = Smem::kBytes;
-  e = cudaFuncSetAttribute(sinkhorn_tc5_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(sinkhorn_tc5_kernel<KP, SPLIT, EXPLICIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -370,9 +415,9 @@ cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dist, cons
   int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
   if (clusters < 1) clusters = 1;
   const size_t img_bytes = 2 * C::kImgRankBytes;
-  sinkhorn_tc5_kernel<KP><<<(unsigned)(2 * clusters), kThreads, smem, s>>>(
-      tile_begin, tile_end, n_dist, out, Hp, K, img, img + img_bytes, img + 2 * img_bytes, img + 3 * img_bytes, xbuf,
-      iters);
+  sinkhorn_tc5_kernel<KP, SPLIT, EXPLICIT><<<(unsigned)(2 * clusters), kThreads, smem, s>>>(
+      tile_begin, tile_end, n_dist, out, ps, Hp, K, img, img + img_bytes, img + 2 * img_bytes,
+      img + 3 * img_bytes, xbuf, iters);
   return cudaGetLastError();
 }
 
@@ -399,15 +444,30 @@ cudaError_t launch_gibbs_prep_tc5(const float* cost, int K, float eps, uint8_t* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_sinkhorn_tc5(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
-                                const float* H, int K, const uint8_t* img, uint8_t* scratch, int iters,
-                                cudaStream_t s) {
-  if (tile_end <= tile_begin) return cudaSuccess;
+template <int SPLIT, bool EXPLICIT>
+static cudaError_t launch_split(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const PairSource& ps, const float* H, int K, const uint8_t* img,
+                                uint8_t* scratch, int iters, cudaStream_t s) {
   switch (tc5_kpad(K)) {
-    case 256: return tc5::launch_kp<256>(tile_begin, tile_end, n_dist, out, H, K, img, scratch, iters, s);
-    case 512: return tc5::launch_kp<512>(tile_begin, tile_end, n_dist, out, H, K, img, scratch, iters, s);
-    default: return tc5::launch_kp<1024>(tile_begin, tile_end, n_dist, out, H, K, img, scratch, iters, s);
+    case 256: return tc5::launch_kp<256, SPLIT, EXPLICIT>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s);
+    case 512: return tc5::launch_kp<512, SPLIT, EXPLICIT>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s);
+    default: return tc5::launch_kp<1024, SPLIT, EXPLICIT>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s);
   }
+}
+
+// Tile mode (ps.pi == nullptr): tiles [tile_begin, tile_end) of the upper triangle.  Explicit mode:
+// tiles of 128 consecutive entries of the pair list (tile_begin = 0, tile_end = ceil(n / 128)).
+cudaError_t launch_sinkhorn_tc5(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const PairSource& ps, const float* H, int K, const uint8_t* img,
+                                uint8_t* scratch, int iters, bool split3, cudaStream_t s) {
+  if (tile_end <= tile_begin) return cudaSuccess;
+  const bool expl = ps.pi != nullptr;
+  if (split3) {
+    return expl ? launch_split<3, true>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s)
+                : launch_split<3, false>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s);
+  }
+  return expl ? launch_split<1, true>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s)
+              : launch_split<1, false>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s);
 }
 
 }  // namespace asot
