@@ -36,6 +36,46 @@ def test_exports_every_header_symbol(lib):
     assert lib.asot_abi_version() == 1
 
 
+def header_param_types():
+    """{function: [C parameter types]} parsed from include/asot.h (comments stripped)."""
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(asot_[a-z0-9_]+)\s*\(([^;{)]*)\)\s*;", src):
+        params = [p.strip() for p in m.group(2).split(",") if p.strip() and p.strip() != "void"]
+        out[m.group(1)] = params
+    return out
+
+
+def _ctype_for(decl: str):
+    decl = " ".join(decl.split())
+    if "*" in decl:
+        return ctypes.c_void_p
+    base = decl.rsplit(" ", 1)[0] if " " in decl else decl
+    base = base.replace("const ", "")
+    return {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32, "float": ctypes.c_float,
+            "size_t": ctypes.c_size_t, "asot_precision": ctypes.c_int32, "uint32_t": ctypes.c_uint32,
+            "double": ctypes.c_double}[base]
+
+
+def test_binding_signatures_match_header():
+    """Every ctypes signature in _lib has the header's parameter count and scalar types (a
+    mismatch would silently shift arguments)."""
+    from paper_2310_16123_b200 import _lib
+    hdr = header_param_types()
+    for name, (_, args) in _lib._SIGS.items():
+        assert name in hdr, name
+        params = hdr[name]
+        assert len(args) == len(params), f"{name}: binding {len(args)} args, header {len(params)}"
+        for a, decl in zip(args, params):
+            want = _ctype_for(decl)
+            if want is ctypes.c_void_p:
+                assert a is ctypes.c_void_p or (hasattr(a, "_type_") and isinstance(a._type_, type)), (name, decl)
+            else:
+                assert a is want or (ctypes.sizeof(a) == ctypes.sizeof(want) and
+                                     (a is ctypes.c_float) == (want is ctypes.c_float) and
+                                     (a is ctypes.c_double) == (want is ctypes.c_double)), (name, decl, a)
+
+
 def test_num_tiles_and_enumeration(lib):
     import paper_2310_16123_b200 as asot
     for n in (1, 2, 15, 16, 17, 33, 64, 100, 1000):
