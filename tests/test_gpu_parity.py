@@ -284,3 +284,32 @@ def test_distributed_path_single_rank_nccl(asot, cfg, n):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,prec,npairs", [("c4", 1, 200), ("c3", 0, 200), ("c5", 1, 40), ("c5", 0, 24)])
+def test_full_size_sampled_parity_more(asot, cfg, prec, npairs):
+    """Full-size c4 (N = 8000, Dirichlet weights), c3 at fp32 (3xTF32 streamed kernel) and c5
+    (K = 1024, streamed kernels) in bench.py's launch configuration: sampled pairs against the
+    oracle evaluated pair by pair on the histograms of the touched distributions."""
+    inp = make_inputs(cfg)
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                             offsets_host=inp.offsets, cost_max=1.0, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    pi, pj = random_pairs(inp.n_dist, npairs, seed=23)
+    n = inp.n_dist
+    pi = np.concatenate([pi, [0, 15, n - 2]]).astype(np.int32)     # block boundary, ragged tail
+    pj = np.concatenate([pj, [n - 1, 16, n - 1]]).astype(np.int32)
+    touched = np.unique(np.concatenate([pi, pj]))
+    H_o = np.zeros((n, inp.n_anchors))
+    for d in touched:
+        s, e = int(inp.offsets[d]), int(inp.offsets[d + 1])
+        _, h = O.map_and_histogram(inp.points[s:e], np.array([0, e - s]), inp.weights[s:e], inp.anchors)
+        H_o[d] = h[0]
+    c_o, _ = O.pair_costs(H_o, inp.cost, inp.eps, inp.iters, pi.astype(np.int64), pj.astype(np.int64))
+    Dg = D.cpu().numpy()
+    r = rel_err(Dg[pi, pj], c_o, 1.0)
+    assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)], r.max()
+    assert np.all(np.diag(Dg) == 0) and np.array_equal(Dg[pi, pj], Dg[pj, pi])
