@@ -120,15 +120,18 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
     __syncthreads();
     for (int jj = q; jj < nc; jj += kLanesPerPoint) {
       const float4* w4 = reinterpret_cast<const float4*>(Ws + jj * RS);
-      float acc = 0.0f;
+      // four partial sums (coordinates k mod 4): a 4x shorter dependent FMA chain; the bound
+      // below holds for any summation order of the d non-negative rounded terms
+      float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
 #pragma unroll
       for (int k4 = 0; k4 < DP / 4; ++k4) {
         const float4 w = w4[k4];
-        float t = x[4 * k4 + 0] - w.x; acc = fmaf(t, t, acc);
-        t = x[4 * k4 + 1] - w.y; acc = fmaf(t, t, acc);
-        t = x[4 * k4 + 2] - w.z; acc = fmaf(t, t, acc);
-        t = x[4 * k4 + 3] - w.w; acc = fmaf(t, t, acc);
+        float t = x[4 * k4 + 0] - w.x; a0 = fmaf(t, t, a0);
+        t = x[4 * k4 + 1] - w.y; a1 = fmaf(t, t, a1);
+        t = x[4 * k4 + 2] - w.z; a2 = fmaf(t, t, a2);
+        t = x[4 * k4 + 3] - w.w; a3 = fmaf(t, t, a3);
       }
+      const float acc = (a0 + a1) + (a2 + a3);
       const int j = j0 + jj;  // increasing per lane: strict < keeps the lowest index
       if (acc < bt.best) {
         bt.second = bt.best;
