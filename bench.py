@@ -387,14 +387,15 @@ def main():
 
         steps_impl = D_.DistSteps(counted(steps_impl.map_range), counted(steps_impl.tiles),
                                   counted(steps_impl.unpack), counted(steps_impl.zero_diag),
-                                  counted(steps_impl.tiles_into))
+                                  counted(steps_impl.tiles_into), counted(steps_impl.map_range_bcast))
         # result exchange: NVLink stores from the Sinkhorn epilogue into rank 0's symmetric-memory
         # matrix (one kernel does compute + "gather"); NCCL all-gather + unpack as the fallback
         p2p = None
         if os.environ.get("ASOT_RESULT_EXCHANGE", "p2p") == "p2p":
             try:
-                p2p = D_.P2PResult(inp.n_dist, dev)
-                exchange_note[0] = "p2p: NVLink stores into rank 0's symmetric-memory matrix"
+                p2p = D_.P2PResult(inp.n_dist, dev, n_anchors=inp.n_anchors)
+                exchange_note[0] = ("p2p: histogram rows stored into every rank's symmetric-memory H, "
+                                    "distances stored into rank 0's symmetric-memory matrix (NVLink)")
             except Exception as exc:  # noqa: BLE001 - report and fall back
                 exchange_note[0] = f"nccl all-gather + unpack (symmetric memory unavailable: {exc!s:.80})"
 

@@ -96,6 +96,18 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
                                 int32_t n_anchors, int32_t* assign_out, float* hist_out,
                                 uint32_t* status, void* stream);
 
+/* Multi-GPU form of asot_map_to_anchors: additionally stores every histogram row i of this
+ * call into each of the n_peers full [N_total, n_anchors] matrices hist_peers[d] (a device array
+ * of device pointers -- e.g. every rank's symmetric-memory H, so the rows travel as NVLink stores
+ * and the all-gather of H is fused into the histogram kernel) at row row_base + i.  The caller
+ * synchronises and barriers before reading the peers' matrices. */
+asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offsets,
+                                      const int64_t* offsets_host, const float* weights,
+                                      int64_t n_dist, int32_t dim, const float* anchors,
+                                      int32_t n_anchors, int32_t* assign_out, float* hist_out,
+                                      float* const* hist_peers, int32_t n_peers, int64_t row_base,
+                                      uint32_t* status, void* stream);
+
 /* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed).
  * K >= 32: the streamed tcgen05 kernel in pair-list mode (ASOT_PREC_TF32: one TF32 pass;
  * ASOT_PREC_FP32: 3xTF32), tiles of 128 consecutive list entries, marginals read from the

@@ -54,6 +54,8 @@ _SIGS = {
     "asot_sinkhorn_kernel_kind": (c_i32, [c_i32, c_i32]),
     "asot_exact_asot_pairs": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                       c_size, c_vp]),
+    "asot_map_to_anchors_bcast": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp,
+                                          c_vp, c_i32, c_i64, c_vp, c_vp]),
     "asot_profile_enable": (c_i32, [c_i32]),
     "asot_profile_read": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "asot_profile_read_kernel": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),

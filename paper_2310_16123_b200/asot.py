@@ -187,6 +187,28 @@ def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.T
     return assign[:T], H, st
 
 
+def map_to_anchors_bcast(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
+                         anchors: torch.Tensor, peer_ptrs: torch.Tensor, row_base: int,
+                         offsets_host: Optional[np.ndarray] = None,
+                         status: Optional[torch.Tensor] = None, stream=None):
+    """map_to_anchors that also stores each H row into every matrix of `peer_ptrs` (int64 device
+    tensor of device addresses of full [N_total, K] H buffers) at row row_base + i."""
+    _need_cuda(points, offsets, weights, anchors, peer_ptrs)
+    _need_f32(points, weights, anchors)
+    oh = _host_offsets(offsets, offsets_host)
+    N = oh.shape[0] - 1
+    T = int(oh[-1])
+    K, d = anchors.shape
+    assign = torch.empty(max(T, 1), dtype=torch.int32, device=points.device)
+    H = torch.empty((N, K), dtype=torch.float32, device=points.device)
+    st = new_status(points.device) if status is None else status
+    _check(_lib_handle().asot_map_to_anchors_bcast(
+        _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(anchors), int(K),
+        _ptr(assign), _ptr(H), _ptr(peer_ptrs), int(peer_ptrs.numel()), int(row_base), _ptr(st),
+        _stream(stream)))
+    return assign[:T], H, st
+
+
 def _soft_common(points, offsets, weights, offsets_host, K, status, want_codes):
     _need_cuda(points, offsets, weights)
     oh = _host_offsets(offsets, offsets_host)

@@ -266,11 +266,36 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
   return kind == 0 || kind == 3 || kind == 5 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;   // (6: TF32)
 }
 
+static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,
+                            const float* weights, int64_t n_dist, int32_t dim, const float* anchors,
+                            int32_t n_anchors, int32_t* assign_out, float* hist_out, uint32_t* status,
+                            void* stream, float* const* peers, int32_t n_peers, int64_t row_base);
+
 asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
                                 const int64_t* offsets_host, const float* weights,
                                 int64_t n_dist, int32_t dim, const float* anchors,
                                 int32_t n_anchors, int32_t* assign_out, float* hist_out,
                                 uint32_t* status, void* stream) {
+  return map_impl(points, offsets, offsets_host, weights, n_dist, dim, anchors, n_anchors, assign_out,
+                  hist_out, status, stream, nullptr, 0, 0);
+}
+
+asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offsets,
+                                      const int64_t* offsets_host, const float* weights,
+                                      int64_t n_dist, int32_t dim, const float* anchors,
+                                      int32_t n_anchors, int32_t* assign_out, float* hist_out,
+                                      float* const* hist_peers, int32_t n_peers, int64_t row_base,
+                                      uint32_t* status, void* stream) {
+  ASOT_CHECK_ARG(n_peers >= 0 && (n_peers == 0 || hist_peers), "hist_peers required when n_peers > 0");
+  ASOT_CHECK_ARG(row_base >= 0, "row_base must be >= 0");
+  return map_impl(points, offsets, offsets_host, weights, n_dist, dim, anchors, n_anchors, assign_out,
+                  hist_out, status, stream, hist_peers, n_peers, row_base);
+}
+
+static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,
+                            const float* weights, int64_t n_dist, int32_t dim, const float* anchors,
+                            int32_t n_anchors, int32_t* assign_out, float* hist_out, uint32_t* status,
+                            void* stream, float* const* peers, int32_t n_peers, int64_t row_base) {
   g_launches = 0;
   ASOT_CHECK_ARG(points && offsets && offsets_host && weights && anchors && assign_out &&
                      hist_out && status,
@@ -289,7 +314,8 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
     ProfScope prof(ASOT_PROF_MAP, s);
     ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
   }
-  ASOT_LAUNCH(asot::launch_histograms(assign_out, weights, offsets, n_dist, n_anchors, hist_out, status, s));
+  ASOT_LAUNCH(asot::launch_histograms(assign_out, weights, offsets, n_dist, n_anchors, hist_out, status, s,
+                                      peers, n_peers, row_base));
   return ASOT_OK;
 }
 

@@ -224,7 +224,8 @@ constexpr int kHistWarps = 4;
 __global__ void __launch_bounds__(kHistWarps * 32)
 histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ weights,
                  const int64_t* __restrict__ offsets, int64_t n_dist, int K,
-                 float* __restrict__ H, uint32_t* __restrict__ status) {
+                 float* __restrict__ H, uint32_t* __restrict__ status,
+                 float* const* __restrict__ peers, int n_peers, int64_t row_base) {
   extern __shared__ double hist_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kHistWarps + warp;
@@ -264,17 +265,24 @@ histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ w
     atomicOr(status, ASOT_FLAG_BAD_MASS);
   }
   __syncwarp();
-  for (int r = lane; r < K; r += 32) H[i * K + r] = (float)h[r];
+  for (int r = lane; r < K; r += 32) {
+    const float v = (float)h[r];
+    H[i * K + r] = v;
+    // multi-GPU: the same row straight into every rank's full H (NVLink stores into symmetric
+    // memory) -- the all-gather of the mapped marginals fused into the kernel that makes them
+    for (int d = 0; d < n_peers; ++d) peers[d][(row_base + i) * K + r] = v;
+  }
 }
 
 cudaError_t launch_histograms(const int32_t* assign, const float* weights, const int64_t* offsets,
-                              int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s) {
+                              int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s,
+                              float* const* peers, int n_peers, int64_t row_base) {
   if (n_dist == 0) return cudaSuccess;
   const size_t smem = (size_t)kHistWarps * K * sizeof(double);
   cudaFuncSetAttribute(histogram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = (n_dist + kHistWarps - 1) / kHistWarps;
   histogram_kernel<<<(unsigned)blocks, kHistWarps * 32, smem, s>>>(assign, weights, offsets, n_dist,
-                                                                  K, H, status);
+                                                                  K, H, status, peers, n_peers, row_base);
   return cudaGetLastError();
 }
 

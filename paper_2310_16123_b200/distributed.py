@@ -1,10 +1,12 @@
 """Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL) process groups.
 
-Result exchange, two forms:
-  * "p2p" (default on GPUs): rank 0's N x N matrix is a torch symmetric-memory buffer; every rank
-    passes rank 0's buffer address as the Sinkhorn kernel's output, so each pair's distance leaves
-    the epilogue as an NVLink store into rank 0's matrix -- the compute and the "gather" are one
-    kernel, no packed buffers, no collective, no unpack; a barrier then publishes the matrix.
+Exchanges, two forms:
+  * "p2p" (default on GPUs): H and rank 0's N x N matrix are torch symmetric-memory buffers.  Each
+    rank's histogram kernel stores its rows into every rank's H (the all-gather fused into the
+    kernel that produces the rows), and every rank passes rank 0's matrix address as the Sinkhorn
+    kernel's output, so each pair's distance leaves the epilogue as an NVLink store into rank 0's
+    matrix -- no packed buffers, no collective on the data path, no unpack; stream syncs and
+    barriers publish H and the matrix.
   * "nccl": packed slot-ordered tiles, NCCL all-gather, KN6 unpack on rank 0 (also the CPU/gloo
     test form, and the fallback when symmetric memory is unavailable).
 
@@ -56,14 +58,24 @@ def partition_by_points(offsets: np.ndarray, world: int) -> list[tuple[int, int]
 
 
 class P2PResult:
-    """Rank 0's N x N result matrix in torch symmetric memory, mapped into every rank."""
+    """Symmetric-memory buffers mapped into every rank: rank 0's N x N result matrix (written by
+    every rank's Sinkhorn epilogue) and, when n_anchors is given, each rank's full N x K H
+    (written by every rank's histogram kernel: the all-gather of H fused into the mapping)."""
 
-    def __init__(self, n_dist: int, device: torch.device, group=None):
+    def __init__(self, n_dist: int, device: torch.device, group=None, n_anchors: Optional[int] = None):
         import torch.distributed._symmetric_memory as symm_mem
 
+        grp = group if group is not None else dist.group.WORLD
         self.D = symm_mem.empty(n_dist, n_dist, dtype=torch.float32, device=device)
-        self.handle = symm_mem.rendezvous(self.D, group if group is not None else dist.group.WORLD)
+        self.handle = symm_mem.rendezvous(self.D, grp)
         self.root_ptr = int(self.handle.buffer_ptrs[0])
+        self.H = None
+        self.h_peers = None
+        if n_anchors is not None:
+            self.H = symm_mem.empty(n_dist, n_anchors, dtype=torch.float32, device=device)
+            self.h_handle = symm_mem.rendezvous(self.H, grp)
+            self.h_peers = torch.tensor([int(x) for x in self.h_handle.buffer_ptrs], dtype=torch.int64,
+                                        device=device)
 
 
 def distance_matrix_distributed_p2p(n_dist: int, n_anchors: int, offsets_host: np.ndarray,
@@ -75,7 +87,18 @@ def distance_matrix_distributed_p2p(n_dist: int, n_anchors: int, offsets_host: n
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    H = _gather_hist(n_anchors, offsets_host, steps, world, rank, dev, group) if hist is None else hist
+    if hist is not None:
+        H = hist
+    elif result.h_peers is not None and steps.map_range_bcast is not None:
+        # exchange 1 fused: this rank's histogram rows are stored into every rank's H directly
+        lo, hi = partition_by_points(offsets_host, world)[rank]
+        if hi > lo:
+            steps.map_range_bcast(lo, hi, result.h_peers)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)
+        H = result.H
+    else:
+        H = _gather_hist(n_anchors, offsets_host, steps, world, rank, dev, group)
     t0, t1 = partition_even(n_tiles, world)[rank]
     if t1 > t0:
         steps.tiles_into(H, t0, t1, result.root_ptr)
@@ -108,6 +131,7 @@ class DistSteps:
     unpack: Callable[[torch.Tensor, int, int, torch.Tensor], None]  # (packed, t0, t1, D) in place
     zero_diag: Callable[[torch.Tensor], None]
     tiles_into: Optional[Callable[[torch.Tensor, int, int, int], None]] = None  # (H, t0, t1, D address)
+    map_range_bcast: Optional[Callable[[int, int, torch.Tensor], None]] = None  # (lo, hi, H peer addresses)
 
 
 def distance_matrix_distributed(n_dist: int, n_anchors: int, offsets_host: np.ndarray,
@@ -174,9 +198,16 @@ def cuda_steps(points: torch.Tensor, offsets: torch.Tensor, offsets_host: np.nda
     def zero_diag(D: torch.Tensor) -> None:  # KN6 with an empty tile range: diagonal only
         A.unpack_tiles(D, D.shape[0], 0, 0, D, zero_diag=True)
 
+    def map_range_bcast(lo: int, hi: int, peers: torch.Tensor) -> None:
+        s, e = int(offs_h[lo]), int(offs_h[hi])
+        sub_off_h = offs_h[lo: hi + 1] - s
+        sub_off = torch.from_numpy(sub_off_h).to(points.device, non_blocking=True)
+        A.map_to_anchors_bcast(points[s:e].contiguous(), sub_off, weights[s:e].contiguous(), anchors,
+                               peers, lo, offsets_host=sub_off_h, status=status)
+
     def tiles_into(H: torch.Tensor, t0: int, t1: int, d_addr: int) -> None:
         A.distance_matrix(None, None, None, None, cost, eps, iters, precision=precision, hist=H,
                           tile_range=(t0, t1), want_matrix=False, out_ptr=d_addr,
                           cost_max=cost_max, status=status, workspace=workspace)
 
-    return DistSteps(map_range, tiles, unpack, zero_diag, tiles_into)
+    return DistSteps(map_range, tiles, unpack, zero_diag, tiles_into, map_range_bcast)

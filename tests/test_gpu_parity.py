@@ -274,8 +274,9 @@ def test_distributed_path_single_rank_nccl(asot, cfg, n):
         torch.cuda.synchronize()
         assert torch.equal(D1, D2)
         # p2p form: the Sinkhorn epilogue stores into rank 0's symmetric-memory matrix
-        res = D_.P2PResult(inp.n_dist, torch.device("cuda", 0))
+        res = D_.P2PResult(inp.n_dist, torch.device("cuda", 0), n_anchors=inp.n_anchors)
         res.D.fill_(-1.0)
+        res.H.fill_(-1.0)
         D3 = D_.distance_matrix_distributed_p2p(inp.n_dist, inp.n_anchors, inp.offsets,
                                                 asot.num_tiles(inp.n_dist), steps, res,
                                                 device=torch.device("cuda", 0))
