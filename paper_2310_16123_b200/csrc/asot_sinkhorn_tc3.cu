@@ -38,19 +38,6 @@ constexpr int kEpiThreads = kEpiWarps * 32;   // 512
 constexpr int kThreads = kEpiThreads + 32;    // + the MMA issuer warp
 constexpr uint32_t kTmemCols = 512;
 
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -91,9 +78,9 @@ __device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint3
     const uint32_t boff = (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32) + row0;
     const uint64_t dhi = make_sw128_desc(ghi + boff), dlo = make_sw128_desc(glo + boff);
     const uint32_t acc0 = (kh > 0 || s > 0) ? 1u : 0u;
-    mma_ts(d, a_reg + 8 * ks, dhi, idesc, acc0);         // x_hi K_hi
-    mma_ts(d, a_reg + KP + 8 * ks, dhi, idesc, 1u);      // x_lo K_hi
-    mma_ts(d, a_reg + 8 * ks, dlo, idesc, 1u);           // x_hi K_lo
+    mma1_tf32_ts(d, a_reg + 8 * ks, dhi, idesc, acc0);         // x_hi K_hi
+    mma1_tf32_ts(d, a_reg + KP + 8 * ks, dhi, idesc, 1u);      // x_lo K_hi
+    mma1_tf32_ts(d, a_reg + 8 * ks, dlo, idesc, 1u);           // x_hi K_lo
   }
 }
 
@@ -167,9 +154,9 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
         tc_fence_after();
         if (elect_one()) {
           issue_part<KP>(a_reg, d_reg, ghi, glo, 1, 0);
-          mma_commit(bar_d0);
+          mma1_commit(bar_d0);
           issue_part<KP>(a_reg, d_reg, ghi, glo, 1, 1);
-          mma_commit(bar_d1);
+          mma1_commit(bar_d1);
         }
         __syncwarp();
         xpar ^= 1u;

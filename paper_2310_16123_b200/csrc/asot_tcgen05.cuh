@@ -1,6 +1,5 @@
 // asot_tcgen05.cuh -- thin inline-PTX wrappers for tcgen05 (MMA, TMEM ld/st, alloc), mbarriers,
-// TMA bulk copies and clusters on sm_100a.  Shared by the CTA-pair (asot_sinkhorn_tc2.cu) and the
-// streamed (asot_sinkhorn_tc4.cu) Sinkhorn kernels.
+// TMA bulk copies and clusters on sm_100a.  Shared by every tensor-core Sinkhorn kernel.
 #pragma once
 
 #include <cstdint>
@@ -136,6 +135,21 @@ __device__ __forceinline__ float rcp_approx(float x) {
 __device__ __forceinline__ uint32_t tf32_rna_pre(float x) { return __float_as_uint(x) + 0x1000u; }
 __device__ __forceinline__ float tf32_mask(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
+
+// Single-CTA (cta_group::1) MMA with A from TMEM, and its commit.
+__device__ __forceinline__ void mma1_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma1_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
 
 // SS-form MMA (A and B from shared-memory descriptors), CTA pair.
 __device__ __forceinline__ void mma2_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
