@@ -54,13 +54,13 @@ typedef enum {
 } asot_status;
 
 typedef enum {
-  ASOT_PREC_FP32 = 0, /* fp32-accurate: 3xTF32 tcgen05 (32 <= K <= 1024), else CUDA cores;
-                         target rel. err <= 1e-4                                            */
+  ASOT_PREC_FP32 = 0, /* fp32-accurate: 3xTF32 tcgen05 (tiles: any K <= 1024; pair lists:
+                         K >= 32), else CUDA cores; target rel. err <= 1e-4                 */
   ASOT_PREC_TF32 = 1  /* tcgen05 kind::tf32 MMA (RNA-rounded G and U/V, fp32 accumulate):
                          target rel. err <= 2e-3; 32 <= K <= 1024 runs on tcgen05
                          (resident kernels for K <= 256, streamed above); K < 32 runs the
-                         ASOT_PREC_FP32 kernel (TF32 rounding of u/v over < 32 terms can
-                         exceed 2e-3; reported by asot_effective_precision)                 */
+                         fp32-accurate 3xTF32 kernel (TF32 rounding of u/v over < 32 terms
+                         can exceed 2e-3; reported by asot_effective_precision)             */
 } asot_precision;
 
 /* Bits OR-ed into the caller's device status word. */
@@ -268,7 +268,8 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
 
 /* Which Sinkhorn kernel asot_distance_matrix runs for (K, request): 0 = fp32 CUDA-core kernel,
  * 1 = TF32 1-SM resident (K <= 128), 2 = TF32 CTA pair (K <= 256), 3 = 3xTF32 fp32-accurate
- * 1-SM resident (ASOT_PREC_FP32, 32 <= K <= 128), 4 = TF32 CTA-pair streamed (K <= 1024),
+ * 1-SM resident (ASOT_PREC_FP32 with K <= 128, and every request with K < 32), 4 = TF32 CTA-pair
+ * streamed (K <= 1024),
  * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024),
  * 6 = one-pass TF32 CTA-pair streamed with K padded to 512 (256 < K <= 512). */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);

@@ -76,7 +76,9 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 // (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
 constexpr int32_t kMinTcAnchors = 32;
 int tc_kind(int32_t K, asot_precision prec) {
-  if (K < kMinTcAnchors) return 0;
+  // K < 32: the fp32-accurate 3xTF32 kernel (K padded to 32) for both requests -- TF32 rounding
+  // is not accurate enough there (R#23) and 3xTF32 is still ~20x the CUDA-core kernel
+  if (K < kMinTcAnchors) return K >= 1 && (prec == ASOT_PREC_FP32 || prec == ASOT_PREC_TF32) ? 3 : 0;
   if (prec == ASOT_PREC_FP32)
     return asot::sinkhorn_tc3_supported(K) ? 3 : asot::sinkhorn_tc5_supported(K) ? 5 : 0;
   if (prec != ASOT_PREC_TF32) return 0;
