@@ -269,9 +269,9 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
 /* Which Sinkhorn kernel asot_distance_matrix runs for (K, request): 0 = fp32 CUDA-core kernel,
  * 1 = TF32 1-SM resident (K <= 128), 2 = TF32 CTA pair (K <= 256), 3 = 3xTF32 fp32-accurate
  * 1-SM resident (ASOT_PREC_FP32 with K <= 128, and every request with K < 32), 4 = TF32 CTA-pair
- * streamed (K <= 1024),
- * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024),
- * 6 = one-pass TF32 CTA-pair streamed with K padded to 512 (256 < K <= 512). */
+ * streamed (256 < K <= 1024, K padded to 512 or 1024),
+ * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024).
+ * (Pair lists use the streamed kernel's pair-list mode: 3xTF32 or one-pass TF32.) */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 
 /* Optional kernel timing (bench.py's roofline): while enabled on this thread, the library records

@@ -90,7 +90,7 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 3: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128)",
                 4: "sinkhorn_tc4_kernel (TF32, streamed GEMM form, CTA pair, M=N=256)",
                 5: "sinkhorn_tc5_kernel (3xTF32 fp32-accurate, streamed GEMM form, CTA pair, M=N=256)",
-                6: "sinkhorn_tc5_kernel (TF32, streamed GEMM form, K padded to 512, CTA pair, M=N=256)"}
+                6: "sinkhorn_tc5_kernel (TF32 one-pass, streamed GEMM form, pair-list mode, CTA pair)"}
 
 
 def sinkhorn_kernel_kind(n_anchors: int, precision: int) -> int:

@@ -69,8 +69,8 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 // Tensor-core kernel selection: 0 = none (fp32 SIMT), 1 = single-CTA resident TF32 (K <= 128),
 // 2 = CTA-pair resident TF32 (128 < K <= 256), 4 = CTA-pair streamed TF32 (K <= 1024),
 // 3 = single-CTA resident 3xTF32 for fp32-accurate requests (K <= 128), 5 = CTA-pair streamed
-// 3xTF32 for fp32-accurate requests (128 < K <= 1024), 6 = CTA-pair streamed one-pass TF32 with
-// K padded to 512 (256 < K <= 512; kind 4 pads to 1024).
+// 3xTF32 for fp32-accurate requests (128 < K <= 1024), 6 = CTA-pair streamed one-pass TF32 in
+// pair-list mode (explicit pairs only).
 // K < 32 stays on the fp32 kernel: the per-iteration TF32 rounding of u / v dominates the TF32
 // error (R#23) and a dot product over fewer than 32 anchors barely averages it out
 // (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
@@ -84,7 +84,6 @@ int tc_kind(int32_t K, asot_precision prec) {
   if (prec != ASOT_PREC_TF32) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
-  if (K <= 512) return 6;
   if (asot::sinkhorn_tc4_supported(K)) return 4;
   return 0;
 }
@@ -121,9 +120,9 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc5_image_bytes(K));
     b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc5_scratch_bytes(K, n_dist, device_sms()) + 1024);
   } else if (kind == 4) {
-    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes());
-    b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes());
-    b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc4_scratch_bytes(n_dist, device_sms()) + 1024);
+    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes(K));
+    b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc4_image_bytes(K));
+    b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc4_scratch_bytes(K, n_dist, device_sms()) + 1024);
   } else if (kind == 2) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());

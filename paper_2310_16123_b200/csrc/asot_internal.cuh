@@ -153,8 +153,8 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
 // Streamed tcgen05 cta_group::2 kernel for 256 < K <= 1024 (tile mode; images 2 x 2 MB; scratch:
 // padded marginals + per-CTA ping-pong X buffers).
 bool sinkhorn_tc4_supported(int K);
-size_t sinkhorn_tc4_image_bytes();
-size_t sinkhorn_tc4_scratch_bytes(int64_t n_dist, int sms);
+size_t sinkhorn_tc4_image_bytes(int K);
+size_t sinkhorn_tc4_scratch_bytes(int K, int64_t n_dist, int sms);
 cudaError_t launch_gibbs_prep_tc4(const float* cost, int K, float eps, uint8_t* g_img, uint8_t* gc_img,
                                   cudaStream_t s);
 cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,

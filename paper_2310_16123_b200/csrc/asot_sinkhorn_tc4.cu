@@ -27,7 +27,14 @@ namespace tc4 {
 
 using namespace ::asot::ptx;
 
-constexpr int kKP = 1024;
+// KP = K padded to 512 or 1024: NH = KP/512 passes per phase (N = 512 each), KC = KP/32 chunks
+template <int KP>
+struct Cfg {
+  static constexpr int NH = KP / 512;
+  static constexpr int KC = KP / 32;
+  static constexpr uint32_t kXBytes = 128u * KP * 4u;             // one X buffer: 128 rows x KP x 4 B
+  static constexpr size_t kImgRankBytes = (size_t)KP * KP * 2;    // one rank's half of a K image
+};
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = kEpiThreads + 64;  // + producer warp + MMA (leader) / relay (peer) warp
@@ -35,9 +42,6 @@ constexpr int kStages = 4;
 constexpr uint32_t kAChunk = 16384;          // 128 pair rows x 128 B (32 anchors)
 constexpr uint32_t kBChunk = 32768;          // 2 N-subs x 128 anchor rows x 128 B
 constexpr uint32_t kStageBytes = kAChunk + kBChunk;
-constexpr int kKC = kKP / 32;                // 32 K-chunks per pass
-constexpr uint32_t kXBytes = 512 * 1024;     // one X buffer: 128 rows x 1024 x 4 B
-constexpr size_t kImgRankBytes = (size_t)2 * 1024 * 1024;  // one rank's half of a K image
 
 struct Smem {
   static constexpr int kMRS = 512 + 4;  // marginal half-row stride (floats), 16-byte shift per row
@@ -66,9 +70,10 @@ __device__ __forceinline__ uint64_t make_noswz_desc(uint32_t saddr) {
   d |= (uint64_t)1u << 46;            // version (sm_100); layout type 0 = SWIZZLE_NONE
   return d;
 }
-// K image of one rank: [nh 2][kc 32][ns 2][128 rows][128 B]; output anchor n = nh*512 + ns*256 + rank*128 + r
+// K image of one rank: [nh NH][kc KC][ns 2][128 rows][128 B]; output anchor n = nh*512 + ns*256 + rank*128 + r
+template <int KP>
 __host__ __device__ inline uint32_t b_offset(uint32_t nh, uint32_t ns, uint32_t r, uint32_t k) {
-  return ((nh * 32u + (k >> 5)) * 2u + ns) * 16384u + sw_rows(r, k & 31);
+  return ((nh * (uint32_t)Cfg<KP>::KC + (k >> 5)) * 2u + ns) * 16384u + sw_rows(r, k & 31);
 }
 
 // 16 consecutive anchors [k0, k0+16) (k0 % 4 == 0) of pair row p in an X image: four 16-byte chunks
@@ -85,12 +90,15 @@ __device__ __forceinline__ void x_load16(const uint8_t* xb, uint32_t p, uint32_t
 //   2 epilogue woke (D ready), 3 epilogue done (after the barrier), 4 producer: first load issued
 __device__ long long g_tc4_trace[5][256];
 
-template <int DBG>
+template <int KP, int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
                     const float* __restrict__ Hp, int K, const uint8_t* __restrict__ g_img,
                     const uint8_t* __restrict__ gc_img, uint8_t* __restrict__ xbuf, int iters) {
   using S = Smem;
+  constexpr int NH = Cfg<KP>::NH, kKC = Cfg<KP>::KC;
+  constexpr uint32_t kXBytes = Cfg<KP>::kXBytes;
+  constexpr size_t kImgRankBytes = Cfg<KP>::kImgRankBytes;
   constexpr uint32_t kIdesc = make_idesc_tf32(256, 256);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -145,7 +153,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
           mbar_wait(bar_xr, xr_par);  // X_in fully written (previous phase / tile init)
           xr_par ^= 1u;
           fence_proxy_async_global();
-          for (int nh = 0; nh < 2; ++nh) {
+          for (int nh = 0; nh < NH; ++nh) {
             for (int kc = 0; kc < kKC; ++kc, ++it) {
               const int s = (int)(it % kStages);
               if (it >= kStages) mbar_wait(bar_empty + 8 * s, (uint32_t)((it / kStages - 1) & 1));
@@ -167,7 +175,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     bool first = true;
     for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
       for (int f = 0; f < phases; ++f) {
-        for (int nh = 0; nh < 2; ++nh) {
+        for (int nh = 0; nh < NH; ++nh) {
           if (rank == 0 && !first) {
             mbar_wait(bar_free, free_par);  // both CTAs drained D of the previous pass
             free_par ^= 1u;
@@ -227,7 +235,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       float* marg = (float*)(smem + S::kOffMarg);
       // tile init: X_in of phase 0 = V^T = 1 on real anchors (padding stays 0), my row, anchors
       // [g*256, g*256+256)
-      for (int k = g * 256; k < g * 256 + 256; k += 4) {
+      for (int k = g * (KP / 4); k < (g + 1) * (KP / 4); k += 4) {
         uint32_t v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = (k + e < K) ? 0x3f800000u : 0u;
@@ -245,7 +253,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         const int nrows = (f & 1) ? 16 : 8;
         const int64_t row0 = (f & 1) ? j0 : i0;
         const float* mrow = marg + ((f & 1) ? brow_s : arow_s) * S::kMRS;
-        for (int nh = 0; nh < 2; ++nh) {
+        for (int nh = 0; nh < NH; ++nh) {
           if (!cost_phase) {
             // stage this pass's marginal half-rows (<= 32 KB) while the pass's MMAs run; the
             // previous epilogue's barrier guarantees nobody still reads the buffer
@@ -253,7 +261,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
               const int r = e >> 7, c4 = (e & 127) * 4;
               const int64_t row = row0 + r < n_dist ? row0 + r : n_dist;
               *reinterpret_cast<float4*>(marg + r * S::kMRS + c4) =
-                  *reinterpret_cast<const float4*>(Hp + (size_t)row * kKP + nh * 512 + c4);
+                  *reinterpret_cast<const float4*>(Hp + (size_t)row * KP + nh * 512 + c4);
             }
             named_bar_sync(1, kEpiThreads);
           }
@@ -316,14 +324,14 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
               }
             }
           }
-          if (!cost_phase && nh == 1) fence_proxy_async_global();
+          if (!cost_phase && nh == NH - 1) fence_proxy_async_global();
           tc_fence_before();
           named_bar_sync(1, kEpiThreads);
           if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && threadIdx.x == 0 && 2 * f + nh < 256)
             g_tc4_trace[3][2 * f + nh] = clock64();
           if (threadIdx.x == 0) {
             mbar_arrive_cluster(free_remote);
-            if (!cost_phase && nh == 1) mbar_arrive_local(bar_xr);
+            if (!cost_phase && nh == NH - 1) mbar_arrive_local(bar_xr);
           }
         }
       }
@@ -342,28 +350,30 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
 }
 
 // ----------------------------------------------------------------------------- prep kernels
+template <int KP>
 __global__ void gibbs_prep_tc4_kernel(const float* __restrict__ cost, int K, float eps, uint8_t* __restrict__ g_img,
                                       uint8_t* __restrict__ gc_img) {
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < kKP * kKP; idx += gridDim.x * blockDim.x) {
-    const int n = idx / kKP, k = idx % kKP;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < KP * KP; idx += gridDim.x * blockDim.x) {
+    const int n = idx / KP, k = idx % KP;
     const bool in = n < K && k < K;
     const double c = in ? (double)cost[(int64_t)n * K + k] : 0.0;
     const double gv = in ? exp(-c / (double)eps) : 0.0;               // P:183  K := exp(-C_s / eps)
     const uint32_t gb = in ? tf32_rna_bits((float)gv) : 0x3f800000u;  // padding = 1 (R#12)
     const uint32_t gcb = in ? tf32_rna_bits((float)(gv * c)) : 0u;
     const uint32_t nh = n >> 9, ns = (n >> 8) & 1, rk = (n >> 7) & 1, r = n & 127;
-    const size_t off = (size_t)rk * kImgRankBytes + b_offset(nh, ns, r, k);
+    const size_t off = (size_t)rk * Cfg<KP>::kImgRankBytes + b_offset<KP>(nh, ns, r, k);
     *(uint32_t*)(g_img + off) = gb;
     *(uint32_t*)(gc_img + off) = gcb;
   }
 }
 
 // Marginal rows padded to 1024 anchors, plus a dummy row (index N) for invalid pair slots.
+template <int KP>
 __global__ void pad_marginals_kernel(const float* __restrict__ H, int64_t n_dist, int K, float* __restrict__ Hp) {
-  const int64_t total = (n_dist + 1) * kKP;
+  const int64_t total = (n_dist + 1) * KP;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = idx / kKP;
-    const int c = (int)(idx % kKP);
+    const int64_t row = idx / KP;
+    const int c = (int)(idx % KP);
     float v = 0.0f;
     if (c < K) v = row < n_dist ? H[row * K + c] : 1.0f / (float)K;
     Hp[idx] = v;
@@ -372,31 +382,35 @@ __global__ void pad_marginals_kernel(const float* __restrict__ H, int64_t n_dist
 
 }  // namespace tc4
 
+int tc4_kpad(int K) { return K <= 512 ? 512 : 1024; }
 bool sinkhorn_tc4_supported(int K) { return K > 256 && K <= 1024; }
-size_t sinkhorn_tc4_image_bytes() { return 2 * tc4::kImgRankBytes; }
-size_t sinkhorn_tc4_scratch_bytes(int64_t n_dist, int sms) {
-  return (size_t)(n_dist + 1) * tc4::kKP * 4 + (size_t)sms * 2 * tc4::kXBytes;
+size_t sinkhorn_tc4_image_bytes(int K) { const size_t kp = tc4_kpad(K); return kp * kp * 4; }
+size_t sinkhorn_tc4_scratch_bytes(int K, int64_t n_dist, int sms) {
+  const size_t kp = tc4_kpad(K);
+  return (size_t)(n_dist + 1) * kp * 4 + 1024 + (size_t)sms * 2 * 128 * kp * 4;
 }
 
 cudaError_t launch_gibbs_prep_tc4(const float* cost, int K, float eps, uint8_t* g_img, uint8_t* gc_img,
                                   cudaStream_t s) {
-  tc4::gibbs_prep_tc4_kernel<<<1024, 256, 0, s>>>(cost, K, eps, g_img, gc_img);
+  if (tc4_kpad(K) == 512) tc4::gibbs_prep_tc4_kernel<512><<<512, 256, 0, s>>>(cost, K, eps, g_img, gc_img);
+  else tc4::gibbs_prep_tc4_kernel<1024><<<1024, 256, 0, s>>>(cost, K, eps, g_img, gc_img);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
-                                const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
-                                int iters, cudaStream_t s) {
-  if (tile_end <= tile_begin) return cudaSuccess;
+namespace tc4 {
+template <int KP>
+static cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                             const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
+                             int iters, cudaStream_t s) {
   float* Hp = (float*)scratch;
-  uint8_t* xbuf = scratch + (((size_t)(n_dist + 1) * tc4::kKP * 4 + 1023) & ~(size_t)1023);
-  tc4::pad_marginals_kernel<<<512, 256, 0, s>>>(H, n_dist, K, Hp);
+  uint8_t* xbuf = scratch + (((size_t)(n_dist + 1) * KP * 4 + 1023) & ~(size_t)1023);
+  pad_marginals_kernel<KP><<<512, 256, 0, s>>>(H, n_dist, K, Hp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
-  auto kern = dbg == 1 ? tc4::sinkhorn_tc4_kernel<1> : dbg == 2 ? tc4::sinkhorn_tc4_kernel<2>
-            : dbg == 3 ? tc4::sinkhorn_tc4_kernel<3> : tc4::sinkhorn_tc4_kernel<0>;
-  const size_t smem = tc4::Smem::kBytes;
+  auto kern = dbg == 1 ? sinkhorn_tc4_kernel<KP, 1> : dbg == 2 ? sinkhorn_tc4_kernel<KP, 2>
+            : dbg == 3 ? sinkhorn_tc4_kernel<KP, 3> : sinkhorn_tc4_kernel<KP, 0>;
+  const size_t smem = Smem::kBytes;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -405,9 +419,19 @@ cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_
   const int64_t n_bp = ((tile_end + 1) >> 1) - (tile_begin >> 1);
   int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
   if (clusters < 1) clusters = 1;
-  kern<<<(unsigned)(2 * clusters), tc4::kThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, Hp, K, g_img,
-                                                             gc_img, xbuf, iters);
+  kern<<<(unsigned)(2 * clusters), kThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, Hp, K, g_img, gc_img,
+                                                        xbuf, iters);
   return cudaGetLastError();
+}
+}  // namespace tc4
+
+cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
+                                int iters, cudaStream_t s) {
+  if (tile_end <= tile_begin) return cudaSuccess;
+  if (tc4_kpad(K) == 512)
+    return tc4::launch_kp<512>(tile_begin, tile_end, n_dist, out, H, K, g_img, gc_img, scratch, iters, s);
+  return tc4::launch_kp<1024>(tile_begin, tile_end, n_dist, out, H, K, g_img, gc_img, scratch, iters, s);
 }
 
 }  // namespace asot
