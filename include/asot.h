@@ -26,9 +26,13 @@
  *   - asot_last_error() returns a thread-local message for the last non-OK return.
  *   - Floating point: inputs are fp32.  Mapping decisions are taken in fp64 wherever fp32
  *     cannot decide them (bit-exact against the fp64 definition); histograms are accumulated in
- *     fp64 in point order and rounded to fp32; Sinkhorn runs in fp32 (ASOT_PREC_FP32, CUDA
- *     cores, IEEE division) or on tcgen05 tensor cores with TF32 operands and fp32
- *     accumulation (ASOT_PREC_TF32).
+ *     fp64 in point order and rounded to fp32; Sinkhorn runs on tcgen05 tensor cores with fp32
+ *     accumulation, either fp32-accurate (ASOT_PREC_FP32: 3xTF32 split operands, target 1e-4;
+ *     CUDA cores for pair lists with K < 32) or with one TF32 pass (ASOT_PREC_TF32, target 2e-3).
+ *
+ * Beyond the hot path: soft mappings ASOT-ML / ASOT-DL (NEXT-1), mini-batch
+ * k-means anchors (NEXT-2), exact anchor-space OT per pair (NEXT-3), entropic OT on the original
+ * point sets as the comparison baseline (NEXT-4), and a multi-GPU broadcast form of the mapping.
  */
 #ifndef ASOT_H_
 #define ASOT_H_
