@@ -66,14 +66,15 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
   return ASOT_OK;
 }
 
-// Tensor-core kernel selection: 0 = none (fp32 SIMT), 1 = single-CTA resident TF32 (K <= 128),
-// 2 = CTA-pair resident TF32 (128 < K <= 256), 4 = CTA-pair streamed TF32 (K <= 1024),
-// 3 = single-CTA resident 3xTF32 for fp32-accurate requests (K <= 128), 5 = CTA-pair streamed
-// 3xTF32 for fp32-accurate requests (128 < K <= 1024), 6 = CTA-pair streamed one-pass TF32 in
-// pair-list mode (explicit pairs only).
-// K < 32 stays on the fp32 kernel: the per-iteration TF32 rounding of u / v dominates the TF32
+// Tensor-core kernel selection: 0 = none (fp32 CUDA cores; only explicit pair lists with K < 32),
+// 1 = single-CTA resident TF32 (32 <= K <= 128), 2 = CTA-pair resident TF32 (128 < K <= 256),
+// 4 = CTA-pair streamed TF32 (256 < K <= 1024), 3 = single-CTA resident 3xTF32 (fp32-accurate
+// requests with K <= 128, and every request with K < 32), 5 = CTA-pair streamed 3xTF32 for
+// fp32-accurate requests (128 < K <= 1024; also explicit fp32 pair lists), 6 = CTA-pair streamed
+// one-pass TF32 in pair-list mode (explicit TF32 pair lists).
+// K < 32 never uses one-pass TF32: the per-iteration TF32 rounding of u / v dominates the TF32
 // error (R#23) and a dot product over fewer than 32 anchors barely averages it out
-// (K = 7: 2.3e-3 > the 2e-3 bar), while the 32-wide MMA tile would be mostly padding anyway.
+// (K = 7: 2.3e-3 > the 2e-3 bar), so those requests run the 3xTF32 kernel.
 constexpr int32_t kMinTcAnchors = 32;
 int tc_kind(int32_t K, asot_precision prec) {
   // K < 32: the fp32-accurate 3xTF32 kernel (K padded to 32) for both requests -- TF32 rounding
