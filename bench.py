@@ -147,10 +147,21 @@ def oracle_sample_rate(inp, budget_s: float, seed: int = 0, mapping: str = "oneh
     from oracle import asot_oracle as O
 
     if mapping == "onehot":
+        # map whole distributions in order until half the budget; extrapolate by points
+        H = np.zeros((inp.n_dist, inp.n_anchors))
         t0 = time.perf_counter()
-        _, H = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
-        t_map = time.perf_counter() - t0
-        map_note = f"mapping of all {inp.n_points} points ({t_map:.2f} s)"
+        done_pts, i = 0, 0
+        while i < inp.n_dist and (i < 2 or time.perf_counter() - t0 < budget_s / 2):
+            s, e = int(inp.offsets[i]), int(inp.offsets[i + 1])
+            _, h = O.map_and_histogram(inp.points[s:e], np.array([0, e - s]), inp.weights[s:e], inp.anchors)
+            H[i] = h[0]
+            done_pts += e - s
+            i += 1
+        t = time.perf_counter() - t0
+        t_map = t / done_pts * inp.n_points
+        H[i:] = H[np.arange(inp.n_dist - i) % i]   # rows not mapped in the budget reuse mapped ones
+        map_note = (f"one-hot mapping of {i} distributions / {done_pts} points ({t:.2f} s), extrapolated "
+                    f"to all {inp.n_points} points")
     else:
         H, t_map, map_note = oracle_soft_map(inp, mapping, model, budget_s / 2)
     cost = inp.cost
@@ -166,7 +177,7 @@ def oracle_sample_rate(inp, budget_s: float, seed: int = 0, mapping: str = "oneh
         O.pair_costs(H, cost, inp.eps, inp.iters, pi[done:done + batch].astype(np.int64),
                      pj[done:done + batch].astype(np.int64), batch=batch)
         t_pairs += time.perf_counter() - s
-        done += batch
+        done += len(pi[done:done + batch])
     rate = done / t_pairs
     P = inp.n_pairs
     value = P / (t_map + P / rate)

@@ -62,7 +62,7 @@ __host__ __device__ inline uint32_t gc_image_offset(uint32_t nh, uint32_t r, uin
   return nh * 65536u + (kb >> 2) * 32768u + (kb & 3) * 8192u + sw_block(r, k & 31);
 }
 
-__device__ long long g_tc2_trace[4][256];
+__device__ long long g_tc2_trace[18][256];
 
 template <int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -146,29 +146,37 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   // (token), then commits "D half 0 ready" and "D half 1 ready" to both CTAs.  Each issuer's
   // blocking issue ends before its own next epilogue half is due.
   auto issue_p12 = [&](int f, int64_t gph) {
-    mbar_wait(bar_epi0, epi_par[0]);
+    if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f && lane == 0) g_tc2_trace[16][f] = clock64();
+    if (DBG == 7 || DBG == 8) mbar_wait_poll(bar_epi0, epi_par[0]);
+    else mbar_wait(bar_epi0, epi_par[0]);
+    if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f && lane == 0) g_tc2_trace[17][f] = clock64();
     epi_par[0] ^= 1u;
     tc_fence_after();
     if (elect_one()) {
+      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[4][f] = clock64();
       if (DBG != 2) {
         issue_part(f, 0, 0);
         issue_part(f, 0, 1);
       }
+      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[5][f] = clock64();
       *p12_token = gph;
     }
     __syncwarp();
   };
   auto issue_p34 = [&](int f, int64_t gph) {
-    mbar_wait(bar_epi0 + 8, epi_par[1]);
+    if (DBG == 7 || DBG == 8) mbar_wait_poll(bar_epi0 + 8, epi_par[1]);
+    else mbar_wait(bar_epi0 + 8, epi_par[1]);
     epi_par[1] ^= 1u;
     while (*p12_token < gph) __nanosleep(20);
     __syncwarp();
     tc_fence_after();
     if (elect_one()) {
+      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[6][f] = clock64();
       if (DBG != 2) issue_part(f, 1, 0);
       mma2_commit_mc(bar_mma0);
       if (DBG != 2) issue_part(f, 1, 1);
       mma2_commit_mc(bar_mma0 + 8);
+      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[7][f] = clock64();
     }
     __syncwarp();
   };
@@ -177,11 +185,18 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     if (leader && warp == 8) issue_p34(f, gph);
   };
   // End of an epilogue half: all of the half's threads stored to TMEM; report to the leader.
+  long long t_wake = 0;
+  int trace_f = -1;
   auto half_done = [&]() {
     tmem_wait_st();
     tc_fence_before();
     named_bar_sync(1 + h, kHalfThreads);
-    if (htid == 0) mbar_arrive_cluster(epi_remote0 + 8 * h);
+    if (DBG >= 3 && blockIdx.x < 2 && htid == 0 && trace_f >= 0 && trace_f < 256)
+      g_tc2_trace[8 + 2 * h + blockIdx.x][trace_f] = clock64() - t_wake;
+    if (htid == 0) {
+      if (DBG == 9 && leader) mbar_arrive_local(bar_epi0 + 8 * h);
+      else mbar_arrive_cluster(epi_remote0 + 8 * h);
+    }
   };
 
   const int64_t n_bp_total = num_blocks(n_dist) * (num_blocks(n_dist) + 1) / 2;
@@ -226,17 +241,32 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       mbar_wait(bar_mma0 + 8 * h, mma_par[h]);
       mma_par[h] ^= 1u;
       tc_fence_after();
-      if (DBG == 3 && blockIdx.x == 0 && b == bp_begin && htid == 0 && f < 256) g_tc2_trace[h][f] = clock64();
+      if (DBG >= 3 && blockIdx.x == 0 && b == bp_begin && htid == 0 && f < 256) g_tc2_trace[h][f] = clock64();
+      if (DBG >= 3) {
+        t_wake = clock64();
+        trace_f = b == bp_begin ? f : -1;
+        if (blockIdx.x < 2 && htid == 0 && trace_f >= 0 && trace_f < 256) {
+          long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          g_tc2_trace[12 + 2 * h + blockIdx.x][trace_f] = gt;
+        }
+      }
       const float* mrow = (f & 1) ? brow : arow;
       const uint32_t rd = lane_off + (uint32_t)(((f + 1) & 1) * 256) + cq * 64;
-      if (DBG != 1) {
+      if (DBG != 1 && DBG != 6 && DBG != 8) {
         uint32_t d[2][16];
-        tmem_ld16u(rd, d[0]);
-        tmem_wait_ld();
+        if (DBG == 5) {  // timing experiment: math without TMEM traffic
+#pragma unroll
+          for (int e = 0; e < 16; ++e) d[0][e] = d[1][e] = 0x3f800000u + (uint32_t)(lane * 16 + e + f);
+        } else {
+          tmem_ld16u(rd, d[0]);
+          tmem_wait_ld();
+        }
         reg_fence16(d[0]);
+        uint32_t dummy = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          if (c + 1 < 4) tmem_ld16u(rd + (c + 1) * 16, d[(c + 1) & 1]);
+          if (c + 1 < 4 && DBG != 5) tmem_ld16u(rd + (c + 1) * 16, d[(c + 1) & 1]);
           const uint32_t* dc = d[c & 1];
           uint32_t o[16];
           const float4* m4 = reinterpret_cast<const float4*>(mrow + c * 16);
@@ -249,15 +279,25 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             const float2 x = fmul2(fmul2(make_float2(m0, m1), make_float2(d1, d0)), make_float2(r, r));
             o[e] = tf32_rna_pre(x.x);
             o[e + 1] = tf32_rna_pre(x.y);
+            if (DBG == 4) {  // timing experiment: TMEM traffic without math
+              o[e] = dc[e];
+              o[e + 1] = dc[e + 1];
+            }
           }
-          tmem_st16(rd + c * 16, o);  // in place: the new scaling replaces D
-          if (c + 1 < 4) {
+          if (DBG == 5) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) dummy ^= o[e];
+          } else {
+            tmem_st16(rd + c * 16, o);  // in place: the new scaling replaces D
+          }
+          if (c + 1 < 4 && DBG != 5) {
             tmem_wait_ld();
             reg_fence16(d[(c + 1) & 1]);
           }
         }
+        if (DBG == 5 && dummy == 0x12345u) g_tc2_trace[0][255] = dummy;
       }
-      if (DBG == 3 && blockIdx.x == 0 && b == bp_begin && htid == 0 && f < 256) g_tc2_trace[2 + h][f] = clock64();
+      if (DBG >= 3 && blockIdx.x == 0 && b == bp_begin && htid == 0 && f < 256) g_tc2_trace[2 + h][f] = clock64();
       if (f + 1 < 2 * iters) {
         half_done();
         issue_phase(f + 1, gphase + f + 1);
@@ -363,7 +403,10 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
   if (tile_end <= tile_begin) return cudaSuccess;
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = dbg == 1 ? tc2::sinkhorn_tc2_kernel<1> : dbg == 2 ? tc2::sinkhorn_tc2_kernel<2>
-            : dbg == 3 ? tc2::sinkhorn_tc2_kernel<3> : tc2::sinkhorn_tc2_kernel<0>;
+            : dbg == 3 ? tc2::sinkhorn_tc2_kernel<3> : dbg == 4 ? tc2::sinkhorn_tc2_kernel<4>
+            : dbg == 5 ? tc2::sinkhorn_tc2_kernel<5> : dbg == 6 ? tc2::sinkhorn_tc2_kernel<6>
+            : dbg == 7 ? tc2::sinkhorn_tc2_kernel<7> : dbg == 8 ? tc2::sinkhorn_tc2_kernel<8>
+            : dbg == 9 ? tc2::sinkhorn_tc2_kernel<9> : tc2::sinkhorn_tc2_kernel<0>;
   const size_t smem = tc2::Smem::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

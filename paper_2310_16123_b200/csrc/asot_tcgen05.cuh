@@ -40,9 +40,29 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Non-suspending poll (mbarrier.test_wait): for waits whose last arrival comes from the peer CTA.
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_poll(uint32_t bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) {
+  }
+}
 // arrive on an mbarrier that may live in the peer CTA (shared::cluster address)
+// Release at CTA scope (the PTX default): every use signals tcgen05 / async-proxy work that is
+// ordered by tcgen05.wait + tcgen05.fence::before_thread_sync or by the mbarrier itself, so no
+// cluster-scope release is needed.  (.release.cluster compiles to MEMBAR.ALL.GPU, which stalled
+// the arriving warp ~1000 cycles behind the SM's in-flight TMEM / global traffic.)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
