@@ -4,19 +4,20 @@
 // v0 = 1, L iterations, d = sum_r u_r ((K (.) C_s) v)_r.  K (256 x 256 TF32 = 256 KB) does not fit
 // one SM's shared memory, so a cluster of two CTAs computes M = 256 pairs per MMA
 // (tcgen05.mma.cta_group::2.kind::tf32, A from TMEM): CTA c owns the 128-slot tile 2b+c of block
-// pair b, keeps its 128 pairs' scalings in its own TMEM, and holds the output-anchor half
-// {Nh*128 + c*64 + [0,64)} (Nh = 0, 1) of K in its SMEM (the B operand is split N-wise across
-// the pair).  Two warps of the leader CTA issue every MMA for both CTAs (see issue_p12/p34);
-// commits multicast to both CTAs' mbarriers; epilogue completion is reported to the leader by
-// remote mbarrier arrives.
+// pair b, keeps its 128 pairs' scalings in its own TMEM, and holds rows {nc*64 + c*32 + [0,32)}
+// (nc = 0..3) of K in its SMEM (the B operand is split N-wise across the pair).  A dedicated MMA
+// warp of the leader CTA issues every MMA for both CTAs; commits multicast to both CTAs'
+// mbarriers; epilogue completion is reported to the leader by remote mbarrier arrives.
 //
 // TMEM (per CTA, 512 columns): R0 = [0,256), R1 = [256,512).  Phase f reads A from R[f%2] and
 // writes D into R[(f+1)%2]; the epilogue writes the new scaling IN PLACE over D, so the roles
-// swap every phase.  Each phase's product is issued as four parts (K-half, N-half) in the order
-// (0,0), (0,1), (1,0), (1,1): N-half 0 of D is complete after part 3, so the epilogue of anchor
-// half 0 overlaps part 4, and the next phase's parts 1-2 (which only need K-half 0 of the new
-// scaling) overlap the epilogue of anchor half 1.  The tensor pipe never waits for a whole
-// epilogue.
+// swap every phase.  The anchors are cut into four 64-wide chunks.  A phase is issued as 16 parts
+// (kc, nc) = (input chunk, output chunk), kc-major, each 8 MMAs of M=256 x N=64 x k=8: the parts
+// of input chunk kc wait only for the epilogue of chunk kc of the previous phase, and output
+// chunk nc is complete (commit) after part (3, nc).  So the next phase's first parts wait for the
+// epilogue of ONE chunk (all 16 epilogue warps, 16 anchors per thread) that starts three parts
+// (~780 cycles) before the tensor pipe runs dry: the epilogue latency is hidden, not just
+// overlapped with half a phase.
 //
 // Cost (a6): v_L is written in place into D; u_L stays in A.  K (.) C_s is streamed through a
 // 32 KB SMEM staging buffer in four (N-half, K-half) sub-parts (once per tile: < 1% of a tile),
@@ -30,9 +31,11 @@ namespace asot {
 namespace tc2 {
 
 constexpr int kKP = 256;
-constexpr int kWarps = 16;
+constexpr int kChunk = 64;                  // anchors per epilogue chunk / MMA part
+constexpr int kNChunks = kKP / kChunk;
+constexpr int kWarps = 16;                  // epilogue warps
 constexpr int kThreads = kWarps * 32;
-constexpr int kHalfThreads = kThreads / 2;
+constexpr int kAllThreads = kThreads + 32;  // + the MMA warp
 
 using namespace ::asot::ptx;
 
@@ -40,7 +43,7 @@ using namespace ::asot::ptx;
 struct Smem {
   static constexpr int kRS = kKP + 4;
   static constexpr int kRows = 25;
-  static constexpr size_t kOffG = 0;                          // 128 KB: [kb 8][Nh 2][64 rows][128 B]
+  static constexpr size_t kOffG = 0;                          // 128 KB: [kb 8][nc 4][32 rows][128 B]
   static constexpr size_t kOffStage = 128 * 1024;             // 32 KB:  [kb_in 4][64 rows][128 B]
   static constexpr size_t kOffMarg = kOffStage + 32 * 1024;   // 25 x 260 floats
   static constexpr size_t kOffRed = kOffMarg + (size_t)kRows * kRS * 4;  // [4][128] floats
@@ -49,57 +52,58 @@ struct Smem {
 };
 
 // Global image offsets (bytes) within one rank's image; element (output anchor n, k), n and k in
-// [0, 256).  Output anchors are split as n = Nh*128 + rank*64 + r.
-__host__ __device__ inline uint32_t sw_block(uint32_t r, uint32_t kin) {  // [64 or 128 rows][128 B]
+// [0, 256).  K (the Sinkhorn B operand): n = nc*64 + rank*32 + r, blocks [kb 8][nc 4][32 rows][128 B]
+// (an N = 64 part of chunk nc takes 32 rows from each CTA).  K (.) C_s (the cost B operand, N = 128
+// sub-parts): n = Nh*128 + rank*64 + r, blocks [Nh 2][kb 8][64 rows][128 B].
+__host__ __device__ inline uint32_t sw_block(uint32_t r, uint32_t kin) {  // [rows][128 B], SW128
   const uint32_t lin = r * 128u + kin * 4u;
   return lin ^ (((lin >> 7) & 7u) << 4);
 }
-__host__ __device__ inline uint32_t g_image_offset(uint32_t nh, uint32_t r, uint32_t k) {
-  return (k >> 5) * 16384u + nh * 8192u + sw_block(r, k & 31);
+__host__ __device__ inline uint32_t g_image_offset(uint32_t nc, uint32_t r, uint32_t k) {
+  return (k >> 5) * 16384u + nc * 4096u + sw_block(r, k & 31);
 }
 __host__ __device__ inline uint32_t gc_image_offset(uint32_t nh, uint32_t r, uint32_t k) {
   const uint32_t kb = k >> 5;
   return nh * 65536u + (kb >> 2) * 32768u + (kb & 3) * 8192u + sw_block(r, k & 31);
 }
 
-__device__ long long g_tc2_trace[18][256];
+__device__ long long g_tc2_trace[4][256];
 
 template <int DBG>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAllThreads, 1)
 sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
                     const float* __restrict__ H, int K, const uint8_t* __restrict__ g_img,
                     const uint8_t* __restrict__ gc_img, int iters) {
   using S = Smem;
-  constexpr uint32_t kIdescPart = make_idesc_tf32(256, 128);
+  constexpr uint32_t kIdescPart = make_idesc_tf32(256, kChunk);   // Sinkhorn parts: N = 64
+  constexpr uint32_t kIdescCost = make_idesc_tf32(256, 128);      // cost sub-parts: N = 128
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* mrows = (float*)(smem + S::kOffMarg);
   float* red = (float*)(smem + S::kOffRed);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
-  // bars: 0 g_loaded, 1-2 mma_done[h], 3-4 epi_done[h] (leader only used), 5 cost_done
-  uint32_t* tmem_holder = (uint32_t*)(bars + 8);
-  volatile long long* p12_token = (volatile long long*)(bars + 9);  // last phase whose parts 1-2 are issued
+  // bars: 0 g_loaded, 1-4 mma_done[c] (D chunk c complete), 5-8 epi_done[c] (leader only used:
+  // scaling chunk c written by both CTAs), 9 cost_done
+  uint32_t* tmem_holder = (uint32_t*)(bars + 12);
   const uint32_t bar_g = smem_u32(&bars[0]);
   const uint32_t bar_mma0 = smem_u32(&bars[1]);
-  const uint32_t bar_epi0 = smem_u32(&bars[3]);
-  const uint32_t bar_cost = smem_u32(&bars[5]);
+  const uint32_t bar_epi0 = smem_u32(&bars[5]);
+  const uint32_t bar_cost = smem_u32(&bars[9]);
   static_assert(Smem::kOffBar % 8 == 0, "barrier alignment");
 
   const uint32_t rank = cluster_rank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool epi_warp = warp < kWarps;
   const int q = warp & 3;            // TMEM lane quarter
-  const int cq = warp >> 2;          // anchor (column) quarter: columns [cq*64, cq*64+64)
-  const int h = cq >> 1;             // anchor half handled by this warp in the Sinkhorn phases
+  const int cq = (warp >> 2) & 3;    // column group: 16 columns of every 64-anchor chunk
   const int p = q * 32 + lane;       // pair slot within this CTA's tile == TMEM lane
-  const int htid = threadIdx.x - h * kHalfThreads;  // 0..255 within the half's warps
 
   if (threadIdx.x == 0) {
-    *p12_token = -1;
     mbar_init(bar_g, 1);
-    mbar_init(bar_mma0, 1);
-    mbar_init(bar_mma0 + 8, 1);
-    mbar_init(bar_epi0, 2);
-    mbar_init(bar_epi0 + 8, 2);
+    for (int c = 0; c < kNChunks; ++c) {
+      mbar_init(bar_mma0 + 8 * c, 1);
+      mbar_init(bar_epi0 + 8 * c, 2);
+    }
     mbar_init(bar_cost, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -124,87 +128,32 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
   const uint32_t epi_remote0 = mapa(bar_epi0, 0);  // leader's epi_done[0] (cluster address)
   const bool leader = rank == 0;
-  const bool issuer = leader && warp == 0;  // also issues the cost MMAs
-  int64_t gphase = 0;                        // phases issued before this tile (token namespace)
+  const bool issuer = leader && warp == kWarps;    // the MMA warp (Sinkhorn parts and cost)
 
-  uint32_t mma_par[2] = {0, 0}, epi_par[2] = {0, 0}, cost_par = 0;
+  uint32_t mma_par = 0, epi_par = 0, cost_par = 0;   // one parity bit per barrier family (all
+                                                     // chunks of a family complete once per phase)
   bool g_ready = false;
 
-  // Issue one part (Kh, Nh) of phase f: D(R_d)[:, Nh] (+)= A(R_a)[:, Kh] x K[Kh, Nh]
-  auto issue_part = [&](int f, int kh, int nh) {
-    const uint32_t ra = (uint32_t)((f & 1) * 256), rd = (uint32_t)(((f + 1) & 1) * 256);
-    const uint64_t desc0 = make_sw128_desc(g_base + (uint32_t)(kh * 4 * 16384 + nh * 8192));
+  // Part (kc, nc) of phase f: D(R_d)[:, nc*64 +: 64] (+)= A(R_a)[:, kc*64 +: 64] x K[kc, nc]
+  // The MMA warp's per-part instruction stream is kept minimal (it shares its SM sub-partition
+  // with four busy epilogue warps): one descriptor base per input chunk, constant offsets.
+  const uint64_t gdesc0 = make_sw128_desc(g_base);
+  auto issue_part = [&](uint32_t a_col, uint32_t d_col, uint64_t desc, uint32_t acc0) {
 #pragma unroll
-    for (int ks = 0; ks < 16; ++ks) {
-      const uint64_t desc = desc0 + (uint64_t)(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4);
-      mma2_tf32_ts(rd + nh * 128, ra + kh * 128 + 8 * ks, desc, kIdescPart, (kh > 0 || ks > 0) ? 1u : 0u);
-    }
+    for (int ks = 0; ks < kChunk / 8; ++ks)
+      mma2_tf32_ts(d_col, a_col + 8 * ks, desc + (uint64_t)((((ks >> 2) * 16384) + (ks & 3) * 32) >> 4), kIdescPart,
+                   ks > 0 ? 1u : acc0);
   };
-  // Two issuers in the leader CTA.  Warp 0 (anchor half 0) issues parts 1-2 of phase f as soon
-  // as both CTAs finished epilogue half 0 (they only need K-half 0 of the new scaling); warp 8
-  // (anchor half 1) issues parts 3-4 after epilogue half 1 and after parts 1-2 are in the queue
-  // (token), then commits "D half 0 ready" and "D half 1 ready" to both CTAs.  Each issuer's
-  // blocking issue ends before its own next epilogue half is due.
-  auto issue_p12 = [&](int f, int64_t gph) {
-    if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f && lane == 0) g_tc2_trace[16][f] = clock64();
-    if (DBG == 7 || DBG == 8) mbar_wait_poll(bar_epi0, epi_par[0]);
-    else mbar_wait(bar_epi0, epi_par[0]);
-    if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f && lane == 0) g_tc2_trace[17][f] = clock64();
-    epi_par[0] ^= 1u;
-    tc_fence_after();
-    if (elect_one()) {
-      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[4][f] = clock64();
-      if (DBG != 2) {
-        issue_part(f, 0, 0);
-        issue_part(f, 0, 1);
-      }
-      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[5][f] = clock64();
-      *p12_token = gph;
-    }
-    __syncwarp();
-  };
-  auto issue_p34 = [&](int f, int64_t gph) {
-    if (DBG == 7 || DBG == 8) mbar_wait_poll(bar_epi0 + 8, epi_par[1]);
-    else mbar_wait(bar_epi0 + 8, epi_par[1]);
-    epi_par[1] ^= 1u;
-    while (*p12_token < gph) __nanosleep(20);
-    __syncwarp();
-    tc_fence_after();
-    if (elect_one()) {
-      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[6][f] = clock64();
-      if (DBG != 2) issue_part(f, 1, 0);
-      mma2_commit_mc(bar_mma0);
-      if (DBG != 2) issue_part(f, 1, 1);
-      mma2_commit_mc(bar_mma0 + 8);
-      if (DBG >= 3 && blockIdx.x == 0 && f < 256 && gph == f) g_tc2_trace[7][f] = clock64();
-    }
-    __syncwarp();
-  };
-  auto issue_phase = [&](int f, int64_t gph) {
-    if (leader && warp == 0) issue_p12(f, gph);
-    if (leader && warp == 8) issue_p34(f, gph);
-  };
-  // End of an epilogue half: all of the half's threads stored to TMEM; report to the leader.
-  long long t_wake = 0;
-  int trace_f = -1;
-  auto half_done = [&]() {
+  // End of an epilogue chunk: every epilogue thread of this CTA stored its part of chunk c;
+  // report to the leader's epi_done[c].
+  auto chunk_done = [&](int c) {
     tmem_wait_st();
     tc_fence_before();
-    named_bar_sync(1 + h, kHalfThreads);
-    if (DBG >= 3 && blockIdx.x < 2 && htid == 0 && trace_f >= 0 && trace_f < 256)
-      g_tc2_trace[8 + 2 * h + blockIdx.x][trace_f] = clock64() - t_wake;
-    if (htid == 0) {
-      if (DBG == 9 && leader) mbar_arrive_local(bar_epi0 + 8 * h);
-      else mbar_arrive_cluster(epi_remote0 + 8 * h);
-    }
+    named_bar_sync(1, kThreads);
+    if (threadIdx.x == 0) mbar_arrive_cluster(epi_remote0 + 8 * c);
   };
 
-  const int64_t n_bp_total = num_blocks(n_dist) * (num_blocks(n_dist) + 1) / 2;
-  const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
-  const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  (void)n_bp_total;
-
-  for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+  for (int64_t b = (tile_begin >> 1) + (blockIdx.x >> 1); b < ((tile_end + 1) >> 1); b += gridDim.x >> 1) {
     const int64_t t = 2 * b + rank;          // this CTA's tile
     const bool t_in = t >= tile_begin && t < tile_end;
     // ---- tile init
@@ -212,7 +161,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     block_pair_decode(b, num_blocks(n_dist), bi, bj);
     const int64_t i0 = bi * kBlockDist + rank * 8, j0 = bj * kBlockDist;
     __syncthreads();  // previous tile's readers are done with mrows / red
-    for (int e = threadIdx.x; e < S::kRows * kKP; e += kThreads) {
+    for (int e = threadIdx.x; e < S::kRows * kKP; e += kAllThreads) {
       const int r = e / kKP, c = e % kKP;
       const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
       float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
@@ -220,100 +169,112 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       mrows[r * S::kRS + c] = v;
     }
     int ii, jj;
-    const bool valid = tile_slot_pair(t, p, n_dist, ii, jj) && t_in;
-    const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS + cq * 64;
-    const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS + cq * 64;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {  // V^T = 1 into R0 (phase 0's A operand)
-      uint32_t ones[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) ones[e] = (cq * 64 + c * 16 + e < K) ? 0x3f800000u : 0u;
-      tmem_st16(lane_off + cq * 64 + c * 16, ones);
-    }
+    // TMEM lane p holds tile slot ps: a warp's 32 lanes then touch 8 distinct i-rows and 4
+    // distinct j-rows of the marginals (one SMEM wavefront per 16-byte load, not two)
+    const int ps = ((p & 7) << 4) | (p >> 3);
+    const bool valid = tile_slot_pair(t, ps, n_dist, ii, jj) && t_in;
+    const float* arow = mrows + (valid ? (ps >> 4) : 24) * S::kRS + cq * 16;
+    const float* brow = mrows + (valid ? 8 + (ps & 15) : 24) * S::kRS + cq * 16;
     if (!g_ready) {
-      mbar_wait(bar_g, 0);  // (the leader's first issue depends on both CTAs' arrivals below)
+      mbar_wait(bar_g, 0);
       g_ready = true;
     }
-    half_done();
-    issue_phase(0, gphase);
-
-    for (int f = 0; f < 2 * iters; ++f) {
-      mbar_wait(bar_mma0 + 8 * h, mma_par[h]);
-      mma_par[h] ^= 1u;
-      tc_fence_after();
-      if (DBG >= 3 && blockIdx.x == 0 && b == bp_begin && htid == 0 && f < 256) g_tc2_trace[h][f] = clock64();
-      if (DBG >= 3) {
-        t_wake = clock64();
-        trace_f = b == bp_begin ? f : -1;
-        if (blockIdx.x < 2 && htid == 0 && trace_f >= 0 && trace_f < 256) {
-          long long gt;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          g_tc2_trace[12 + 2 * h + blockIdx.x][trace_f] = gt;
-        }
+    if (epi_warp) {
+#pragma unroll
+      for (int c = 0; c < kNChunks; ++c) {  // V^T = 1 into R0 (phase 0's A operand)
+        uint32_t ones[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) ones[e] = (c * kChunk + cq * 16 + e < K) ? 0x3f800000u : 0u;
+        tmem_st16(lane_off + c * kChunk + cq * 16, ones);
       }
-      const float* mrow = (f & 1) ? brow : arow;
-      const uint32_t rd = lane_off + (uint32_t)(((f + 1) & 1) * 256) + cq * 64;
-      if (DBG != 1 && DBG != 6 && DBG != 8) {
-        uint32_t d[2][16];
-        if (DBG == 5) {  // timing experiment: math without TMEM traffic
+      tmem_wait_st();
+      tc_fence_before();
+      named_bar_sync(1, kThreads);
+      if (threadIdx.x == 0)
+        for (int c = 0; c < kNChunks; ++c) mbar_arrive_cluster(epi_remote0 + 8 * c);
+
+      // marginal values of the next chunk are prefetched into registers right after the
+      // current chunk's stores, so the SMEM reads stay off the chunk's critical path
+      float mk[16];
+      auto load_m = [&](int f, int c) {
+        const float4* m4 = reinterpret_cast<const float4*>(((f & 1) ? brow : arow) + c * kChunk);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) d[0][e] = d[1][e] = 0x3f800000u + (uint32_t)(lane * 16 + e + f);
-        } else {
-          tmem_ld16u(rd, d[0]);
-          tmem_wait_ld();
+        for (int e = 0; e < 4; ++e) {
+          const float4 mq = m4[e];
+          mk[4 * e] = mq.x; mk[4 * e + 1] = mq.y; mk[4 * e + 2] = mq.z; mk[4 * e + 3] = mq.w;
         }
-        reg_fence16(d[0]);
-        uint32_t dummy = 0;
+      };
+      load_m(0, 0);
+      for (int f = 0; f < 2 * iters; ++f) {
+        const uint32_t rd = lane_off + (uint32_t)(((f + 1) & 1) * 256) + cq * 16;
+        const bool last = f + 1 == 2 * iters;
+#pragma unroll 1
+        for (int c = 0; c < kNChunks; ++c) {
+          mbar_wait(bar_mma0 + 8 * c, mma_par);
+          tc_fence_after();
+          if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && threadIdx.x == 0 && f < 64)
+            g_tc2_trace[0][f * 4 + c] = clock64();
+          if (DBG != 1 && DBG != 4) {
+            uint32_t d[16];
+            tmem_ld16u(rd + c * kChunk, d);
+            tmem_wait_ld();
+            reg_fence16(d);
+            uint32_t o[16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c + 1 < 4 && DBG != 5) tmem_ld16u(rd + (c + 1) * 16, d[(c + 1) & 1]);
-          const uint32_t* dc = d[c & 1];
-          uint32_t o[16];
-          const float4* m4 = reinterpret_cast<const float4*>(mrow + c * 16);
+            for (int e = 0; e < 16; e += 2) {
+              const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
+              const float r = rcp_approx(d0 * d1);
+              const float2 x = fmul2(fmul2(make_float2(mk[e], mk[e + 1]), make_float2(d1, d0)), make_float2(r, r));
+              o[e] = tf32_rna_pre(x.x);
+              o[e + 1] = tf32_rna_pre(x.y);
+            }
+            tmem_st16(rd + c * kChunk, o);  // in place: the new scaling replaces D
+            if (c + 1 < kNChunks) load_m(f, c + 1);
+            else if (!last) load_m(f + 1, 0);
+          }
+          if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && threadIdx.x == 0 && f < 64)
+            g_tc2_trace[1][f * 4 + c] = clock64();
+          if (!last) chunk_done(c);
+        }
+        mma_par ^= 1u;
+        if (last) tmem_wait_st();
+      }
+    } else if (issuer) {
+      for (int f = 0; f < 2 * iters; ++f) {
+#pragma unroll 1
+        for (int kc = 0; kc < kNChunks; ++kc) {
+          mbar_wait(bar_epi0 + 8 * kc, epi_par);
+          tc_fence_after();
+          if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && lane == 0 && f < 64)
+            g_tc2_trace[2][f * 4 + kc] = clock64();
+          if (elect_one()) {
+            // part (kc, nc): D(R_d)[:, nc*64 +: 64] (+)= A(R_a)[:, kc*64 +: 64] x K[kc, nc]
+            const uint32_t a_col = (uint32_t)((f & 1) * 256 + kc * kChunk);
+            const uint32_t d_col = (uint32_t)(((f + 1) & 1) * 256);
+            const uint64_t desc = gdesc0 + (uint64_t)((kc * 2 * 16384) >> 4);
+            const uint32_t acc0 = kc > 0 ? 1u : 0u;
 #pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            const float4 mq = m4[e >> 2];
-            const float m0 = (e & 2) ? mq.z : mq.x, m1 = (e & 2) ? mq.w : mq.y;
-            const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
-            const float r = rcp_approx(d0 * d1);
-            const float2 x = fmul2(fmul2(make_float2(m0, m1), make_float2(d1, d0)), make_float2(r, r));
-            o[e] = tf32_rna_pre(x.x);
-            o[e + 1] = tf32_rna_pre(x.y);
-            if (DBG == 4) {  // timing experiment: TMEM traffic without math
-              o[e] = dc[e];
-              o[e + 1] = dc[e + 1];
+            for (int nc = 0; nc < kNChunks; ++nc) {
+              if (DBG != 2) issue_part(a_col, d_col + nc * kChunk, desc + (uint64_t)((nc * 4096) >> 4), acc0);
+              if (kc == kNChunks - 1) mma2_commit_mc(bar_mma0 + 8 * nc);
             }
           }
-          if (DBG == 5) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) dummy ^= o[e];
-          } else {
-            tmem_st16(rd + c * 16, o);  // in place: the new scaling replaces D
-          }
-          if (c + 1 < 4 && DBG != 5) {
-            tmem_wait_ld();
-            reg_fence16(d[(c + 1) & 1]);
-          }
+          __syncwarp();
         }
-        if (DBG == 5 && dummy == 0x12345u) g_tc2_trace[0][255] = dummy;
+        epi_par ^= 1u;
       }
-      if (DBG >= 3 && blockIdx.x == 0 && b == bp_begin && htid == 0 && f < 256) g_tc2_trace[2 + h][f] = clock64();
-      if (f + 1 < 2 * iters) {
-        half_done();
-        issue_phase(f + 1, gphase + f + 1);
-      } else {
-        tmem_wait_st();
-      }
-    }
+    }  // (the peer's MMA warp idles until the cost)
 
     // ---- cost: u_L in R_a = R[(2L-1)%2] = R1, v_L in R_d = R0 (both as RNA-pre bits)
-    const uint32_t ra = lane_off + 256, rdv = 256 - 256;  // A-operand (v_L) region base = R0
+    const uint32_t ra = lane_off + 256, rdv = 0;  // A-operand (v_L) region base = R0
     float ust[32];
+    if (epi_warp) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld8(ra + cq * 32 + 8 * c, &ust[8 * c]);
-    tmem_wait_ld();
+      for (int c = 0; c < 4; ++c) tmem_ld8(ra + cq * 32 + 8 * c, &ust[8 * c]);
+      tmem_wait_ld();
 #pragma unroll
-    for (int e = 0; e < 32; ++e) ust[e] = tf32_mask(ust[e]);
+      for (int e = 0; e < 32; ++e) ust[e] = tf32_mask(ust[e]);
+    }
     float acc = 0.0f;
     for (int sp = 0; sp < 4; ++sp) {  // sub-parts (Nh, Kh) = (sp >> 1, sp & 1)
       const int nh = sp >> 1, kh = sp & 1;
@@ -321,7 +282,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       const float4* src = reinterpret_cast<const float4*>(gc_img + (size_t)rank * (128 * 1024) +
                                                           (size_t)nh * 65536 + (size_t)kh * 32768);
       float4* dst = reinterpret_cast<float4*>(smem + S::kOffStage);
-      for (int e = threadIdx.x; e < 32768 / 16; e += kThreads) dst[e] = src[e];
+      for (int e = threadIdx.x; e < 32768 / 16; e += kAllThreads) dst[e] = src[e];
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       cluster_sync();
@@ -331,7 +292,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
           const uint64_t desc = desc0 + (uint64_t)(((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
-          mma2_tf32_ts(256, rdv + kh * 128 + 8 * ks, desc, kIdescPart, (kh > 0 || ks > 0) ? 1u : 0u);
+          mma2_tf32_ts(256, rdv + kh * 128 + 8 * ks, desc, kIdescCost, (kh > 0 || ks > 0) ? 1u : 0u);
         }
         mma2_commit_mc(bar_cost);
       }
@@ -339,7 +300,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       mbar_wait(bar_cost, cost_par);
       cost_par ^= 1u;
       tc_fence_after();
-      if (kh == 1) {
+      if (kh == 1 && epi_warp) {
         // (K (.) C_s) v for anchors [nh*128, nh*128+128) now sits in R1 columns [0, 128)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -358,11 +319,10 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       cluster_sync();  // staging buffer and R1 columns free for the next sub-part / tile
       tc_fence_after();
     }
-    gphase += 2 * iters;
-    red[cq * 128 + p] = acc;
+    if (epi_warp) red[cq * 128 + p] = acc;
     __syncthreads();
-    if (cq == 0 && t_in)
-      write_result(out, (t - tile_begin) * kTileSlots + p, valid, ii, jj,
+    if (warp < 4 && t_in)
+      write_result(out, (t - tile_begin) * kTileSlots + ps, valid, ii, jj,
                    red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
   }
   tc_fence_before();
@@ -380,8 +340,9 @@ __global__ void gibbs_prep_tc2_kernel(const float* __restrict__ cost, int K, flo
     const double g = in ? exp(-c / (double)eps) : 0.0;  // P:183  K := exp(-C_s / eps)
     const uint32_t gb = in ? tf32_rna_bits((float)g) : 0x3f800000u;  // padding = 1 (R#12)
     const uint32_t gcb = in ? tf32_rna_bits((float)(g * c)) : 0u;
+    const uint32_t nc = n >> 6, rg = (n >> 5) & 1, r32 = n & 31;
+    *(uint32_t*)(g_img + (size_t)rg * (128 * 1024) + g_image_offset(nc, r32, k)) = gb;
     const uint32_t nh = n >> 7, within = n & 127, rk = within >> 6, r = within & 63;
-    *(uint32_t*)(g_img + (size_t)rk * (128 * 1024) + g_image_offset(nh, r, k)) = gb;
     *(uint32_t*)(gc_img + (size_t)rk * (128 * 1024) + gc_image_offset(nh, r, k)) = gcb;
   }
 }
@@ -404,9 +365,7 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = dbg == 1 ? tc2::sinkhorn_tc2_kernel<1> : dbg == 2 ? tc2::sinkhorn_tc2_kernel<2>
             : dbg == 3 ? tc2::sinkhorn_tc2_kernel<3> : dbg == 4 ? tc2::sinkhorn_tc2_kernel<4>
-            : dbg == 5 ? tc2::sinkhorn_tc2_kernel<5> : dbg == 6 ? tc2::sinkhorn_tc2_kernel<6>
-            : dbg == 7 ? tc2::sinkhorn_tc2_kernel<7> : dbg == 8 ? tc2::sinkhorn_tc2_kernel<8>
-            : dbg == 9 ? tc2::sinkhorn_tc2_kernel<9> : tc2::sinkhorn_tc2_kernel<0>;
+            : tc2::sinkhorn_tc2_kernel<0>;
   const size_t smem = tc2::Smem::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -416,7 +375,7 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
   const int64_t n_bp = ((tile_end + 1) >> 1) - (tile_begin >> 1);
   int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
   if (clusters < 1) clusters = 1;
-  kern<<<(unsigned)(2 * clusters), tc2::kThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, H, K, g_img,
+  kern<<<(unsigned)(2 * clusters), tc2::kAllThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, H, K, g_img,
                                                              gc_img, iters);
   return cudaGetLastError();
 }
