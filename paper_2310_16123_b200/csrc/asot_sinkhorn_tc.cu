@@ -11,19 +11,26 @@
 // (K-major SWIZZLE_128B image staged once per CTA by a TMA bulk copy), and the fp32 accumulator
 // D in TMEM.  The scalings of a tile never leave the SM for all 2L+1 MMA phases.
 //
-// Warp roles (512 threads): warps 0-7 own slot 0 and warps 8-15 slot 1 (one pair tile each);
-// warp w reads TMEM lane quarter w%4 and the column half (w%8)/4, so each SMSP runs two
-// independent instruction streams per slot.  After a slot barrier one elected thread issues
-// that slot's tcgen05.mma chain and commits it to the slot's mbarrier.  While the tensor core
-// computes one slot's product, the other slot's warps turn their accumulator into the next
-// scaling (tcgen05.ld x16, double-buffered -> u = a / D with one MUFU.RCP per two anchors ->
-// RNA rounding to TF32 (add half an ulp; the MMA truncates) -> tcgen05.st), so MMA and the elementwise divide overlap (ping-pong).
-// Each pair lives in one TMEM lane; its two column halves are reduced in-thread and summed
-// through SMEM once per tile.  The cost (a6): the last v-update writes v_L in place into D, two
-// N = K/2 MMAs apply K (.) C_s to it (output into the consumed half of A), and the threads
-// reduce sum_r u_r ((K (.) C_s) v)_r.
+// Two pair tiles (slots) per CTA keep the tensor pipe busy: while it runs one slot's product
+// ("chain"), the other slot's warps turn their accumulator into the next scaling.  Each slot has
+// two TMEM regions of KP columns; phase f reads A from R[f%2] and writes D into R[(f+1)%2], and
+// the epilogue writes the new scaling IN PLACE over D, so the roles swap every phase.  The
+// input anchors are cut into two chunks of CH = KP/2: a chain is issued as two halves of N = KP
+// MMAs (k-steps of chunk 0, then chunk 1), each gated by the epilogue of that chunk of the
+// previous phase, so the next chain of a slot waits only for the epilogue of chunk 0 -- which
+// hides behind the other slot's chain -- instead of the whole epilogue.  (N = KP/2 parts with
+// early output chunks were slower: M=128 x N=64 MMAs run at 55 cycles, not 32, in this pattern.)
 //
-// TMEM map (columns): slot s: A at 2s*KP, D at 2s*KP + KP.  SMEM: [K image | KC image |
+// Warp roles (576 threads): warps 0-7 slot 0, warps 8-15 slot 1 (warp w reads TMEM lane quarter
+// w%4 and the column half (w%8)/4 of every chunk); warps 16 / 17 issue the MMAs of slot 0 / 1,
+// alternating chains through a turn token, gated per (slot, chunk) by mbarriers the epilogue arrives
+// on, and commits once per chain.  Epilogue: tcgen05.ld -> u = a / D with one MUFU.RCP per
+// two anchors -> RNA rounding to TF32 (add half an ulp; the MMA truncates) -> tcgen05.st.
+// Cost (a6): the last v-update leaves v_L in place in R0 (u_L in R1); two N = KP/2 chains apply
+// K (.) C_s to it (output into the consumed half of R1), and the threads reduce
+// sum_r u_r ((K (.) C_s) v)_r; the two column halves meet in SMEM once per tile.
+//
+// TMEM map (columns): slot s: R0 at 2s*KP, R1 at 2s*KP + KP.  SMEM: [K image | KC image |
 // marginal rows (8 a-rows, 16 b-rows, 1 dummy row) per slot | partial costs | mbarriers].
 #include <cfloat>
 #include <cstdlib>
@@ -35,32 +42,14 @@ namespace asot {
 namespace tc {
 
 // Debug timeline (ASOT_TC_DEBUG_MODE=3): slot, event, phase -> clock64 for CTA 0's first tile.
+// events: 0 / 1 = epilogue woke for chunk 0 / 1, 2 / 3 = MMA warp passed the chunk 0 / 1 gate
 __device__ long long g_tc_trace[2][4][512];
 
 constexpr int kWarpsPerSlot = 8;
-constexpr int kThreads = 2 * kWarpsPerSlot * 32;  // 512
+constexpr int kThreads = 2 * kWarpsPerSlot * 32;  // epilogue threads
+constexpr int kAllThreads = kThreads + 64;        // + one MMA warp per slot
 
 using namespace ::asot::ptx;
-
-// One slot's MMA chain with compile-time TMEM addresses (TMEM base is 0) and descriptors formed
-// from the uniform SMEM base plus constant offsets.
-//   MODE 0:    D_S = A_S (x) B          (N = KP, B = K image)
-//   MODE 1, 2: A_S[:, 0:KP/2] = D_S (x) B[rows (MODE-1)*KP/2 ...]   (N = KP/2, B = K (.) C_s)
-template <int KP, int S, int MODE>
-__device__ __forceinline__ void issue_chain(uint32_t b_base) {
-  constexpr uint32_t a0 = 2u * S * KP, d0 = a0 + KP;
-  constexpr uint32_t idesc = make_idesc_tf32(128, MODE == 0 ? KP : KP / 2);
-  constexpr uint32_t row0 = MODE == 0 ? 0u : (uint32_t)((MODE - 1) * (KP / 2) * 128);
-  const uint64_t desc0 = make_sw128_desc(b_base + row0);
-#pragma unroll
-  for (int ks = 0; ks < KP / 8; ++ks) {
-    const uint64_t desc = desc0 + (uint64_t)(((ks >> 2) * KP * 128 + (ks & 3) * 32) >> 4);
-    if (MODE == 0)
-      mma1_tf32_ts(d0, a0 + 8 * ks, desc, idesc, ks > 0 ? 1u : 0u);
-    else
-      mma1_tf32_ts(a0, d0 + 8 * ks, desc, idesc, ks > 0 ? 1u : 0u);
-  }
-}
 
 template <int KP>
 struct Smem {
@@ -73,47 +62,74 @@ struct Smem {
   static constexpr size_t kOffMarg = 2 * kImg;
   static constexpr size_t kOffRed = kOffMarg + 2 * kMarg;     // [2 slots][128] partial costs
   static constexpr size_t kOffBar = kOffRed + 2 * 128 * 4;
-  static constexpr size_t kBytes = kOffBar + 64 + 1024;      // + alignment slack
+  static constexpr size_t kBytes = kOffBar + 128 + 1024;     // + alignment slack
 };
 
-// Per-thread view: thread = (slot s, TMEM lane quarter, column half h).  Columns are processed
-// in chunks of 16 with the next chunk's tcgen05.ld in flight while the current one is computed.
+// Loads / stores of W columns (W = 8, 16, 24 or 32) of one TMEM lane quarter.
+template <int W>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[W]) {
+  static_assert(W % 8 == 0, "width");
+  if constexpr (W % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < W / 16; ++c) tmem_ld16u(taddr + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(&r[16 * c]));
+  } else {
+#pragma unroll
+    for (int c = 0; c < W / 8; ++c) {
+      float v[8];
+      tmem_ld8(taddr + 8 * c, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) r[8 * c + e] = __float_as_uint(v[e]);
+    }
+  }
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+template <int W>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)[W]) {
+  if constexpr (W % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < W / 16; ++c) tmem_st16(taddr + 16 * c, *reinterpret_cast<const uint32_t(*)[16]>(&r[16 * c]));
+  } else {
+#pragma unroll
+    for (int c = 0; c < W / 8; ++c) tmem_st8(taddr + 8 * c, &r[8 * c]);
+  }
+}
+
 template <int KP, int DBG>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kAllThreads, 1)
 sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                    const float* __restrict__ H, int K, const uint32_t* __restrict__ g_img,
                    const uint32_t* __restrict__ gc_img, int iters) {
   using S = Smem<KP>;
   // All 512 columns: the allocation then necessarily starts at column 0 (one CTA per SM), so
-  // every TMEM address below is a compile-time constant per slot and the MMA operands live in
-  // uniform registers (no per-instruction R2UR / ELECT loops in the issue path).
+  // every TMEM address below is a compile-time constant per slot.
   constexpr uint32_t kTmemCols = 512;
+  constexpr int CH = KP / 2;    // anchors per chunk
+  constexpr int W = CH / 2;     // columns per thread per chunk
+  constexpr int CQ = KP / 4;    // columns per thread in each cost half
+  constexpr int kWG = kWarpsPerSlot * 32;
   constexpr uint32_t kIdesc = make_idesc_tf32(128, KP);
   constexpr uint32_t kIdescHalf = make_idesc_tf32(128, KP / 2);
-  constexpr int kWG = kWarpsPerSlot * 32;
-  constexpr int CW = KP / 2;    // columns per thread in the Sinkhorn phases
-  constexpr int NC = CW / 16;   // x16 chunks per phase
-  constexpr int CQ = KP / 4;    // columns per thread in each cost half
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte aligned base derived from smem_raw by pointer arithmetic, so the compiler keeps
-  // the shared address space (LDS, not generic loads) for everything carved from it
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* marg = (float*)(smem + S::kOffMarg);
   float* red = (float*)(smem + S::kOffRed);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
-  uint32_t* tmem_holder = (uint32_t*)(bars + 6);
-  // Tensor-pipe turn token: the two slots issue their MMA chains strictly alternately, so one
-  // slot's chain finishes while the other's is still queued and the epilogues interleave with
-  // MMAs instead of both slots running in lockstep (issue blocks for about the chain's duration).
-  volatile int* turn = (volatile int*)(bars + 7);
+  // bars: 0 g_loaded, 1 + 2s + c mma_done[s][c], 5 + 2s + c go[s][c]
+  uint32_t* tmem_holder = (uint32_t*)(bars + 10);
+  volatile int* turn = (volatile int*)(bars + 11);
   volatile int* slot_done = turn + 1;  // [2]
   const uint32_t bar_g = smem_u32(&bars[0]);
-  const uint32_t bar_mma0 = smem_u32(&bars[1]);  // +8*s
+  const uint32_t bar_mma0 = smem_u32(&bars[1]);
+  const uint32_t bar_go0 = smem_u32(&bars[5]);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = warp / kWarpsPerSlot;          // slot (pair tile) owned by this warpgroup pair
+  const int s = warp / kWarpsPerSlot;          // slot (pair tile) of an epilogue warp; 2 = MMA warps
   const int sub = warp & 3;                    // TMEM lane quarter this warp may access
-  const int h = (warp % kWarpsPerSlot) >> 2;   // column half
+  const int h = (warp % kWarpsPerSlot) >> 2;   // column half of every chunk
   const int p = sub * 32 + lane;               // pair slot within the tile == TMEM lane
   const int wg_tid = threadIdx.x - s * kWG;
 
@@ -122,8 +138,10 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     slot_done[0] = 0;
     slot_done[1] = 0;
     mbar_init(bar_g, 1);
-    mbar_init(bar_mma0, 1);
-    mbar_init(bar_mma0 + 8, 1);
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(bar_mma0 + 8 * b, 1);
+      mbar_init(bar_go0 + 8 * b, 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -137,201 +155,231 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-  if (tmem_base != 0) __trap();  // cannot happen with a full 512-column allocation
+  if (*tmem_holder != 0) __trap();  // cannot happen with a full 512-column allocation
   if (threadIdx.x == 0) {  // stage K and K (.) C_s once per CTA (TMA bulk copies)
     mbar_expect_tx(bar_g, (uint32_t)(2 * S::kImg));
-    constexpr uint32_t kChunk = 32768;
-    for (uint32_t off = 0; off < S::kImg; off += kChunk) {
-      const uint32_t n = (uint32_t)((S::kImg - off) < kChunk ? (S::kImg - off) : kChunk);
+    constexpr uint32_t kChunkBytes = 32768;
+    for (uint32_t off = 0; off < S::kImg; off += kChunkBytes) {
+      const uint32_t n = (uint32_t)((S::kImg - off) < kChunkBytes ? (S::kImg - off) : kChunkBytes);
       bulk_g2s(smem_u32(smem + S::kOffG + off), (const uint8_t*)g_img + off, n, bar_g);
       bulk_g2s(smem_u32(smem + S::kOffGC + off), (const uint8_t*)gc_img + off, n, bar_g);
     }
   }
-
-  float* mrows = marg + (size_t)s * S::kRows * S::kRS;
-  const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
-  const uint32_t a_col = (uint32_t)(2 * s * KP);
-  const uint32_t a_tmem = tmem_base + lane_off + a_col;   // this thread's lane of A
-  const uint32_t d_tmem = a_tmem + KP;                    // this thread's lane of D
-  const uint32_t bar_mma = bar_mma0 + 8 * s;
-  const uint32_t g_base = smem_u32(smem + S::kOffG), gc_base = smem_u32(smem + S::kOffGC);
-  uint32_t mma_par = 0;
-  bool g_ready = false;
-
-  // Slot barrier, then one elected thread issues this slot's MMA chain and commits it.
-  //   mode 0:    D = A K                  (N = KP; A = V^T or U^T in TMEM, K in SMEM)
-  //   mode 1, 2: A[:, 0:KP/2] = D (K (.) C_s)[:, half]   (N = KP/2; D holds v_L^T as the
-  //              A operand, the output overwrites the half of u_L already consumed)
-  auto issue_mma = [&](int mode, int fdbg) {
-    tc_fence_before();
-    named_bar_sync(1 + s, kWG);
-    if (wg_tid < 32) {  // the slot's first warp, converged: one elected lane issues
-      if (DBG == 3 && blockIdx.x == 0 && fdbg >= 0 && fdbg < 512 && lane == 0) g_tc_trace[s][3][fdbg] = clock64();
-      if (!g_ready) {
-        mbar_wait(bar_g, 0);
-        g_ready = true;
-      }
-      while (*turn != s && !slot_done[s ^ 1]) __nanosleep(32);
-      __syncwarp();
-      if (DBG == 3 && blockIdx.x == 0 && fdbg >= 0 && fdbg < 512 && lane == 0) g_tc_trace[s][1][fdbg] = clock64();
-      tc_fence_after();
-      if (elect_one()) {
-        if (DBG != 2) {
-          if (s == 0) {
-            if (mode == 0) issue_chain<KP, 0, 0>(g_base);
-            else if (mode == 1) issue_chain<KP, 0, 1>(gc_base);
-            else issue_chain<KP, 0, 2>(gc_base);
-          } else {
-            if (mode == 0) issue_chain<KP, 1, 0>(g_base);
-            else if (mode == 1) issue_chain<KP, 1, 1>(gc_base);
-            else issue_chain<KP, 1, 2>(gc_base);
-          }
-        }
-        mma1_commit(bar_mma);
-        *turn = s ^ 1;
-      }
-      __syncwarp();
-    }
+  // tiles of slot s: tk = s, s+2, ... with tr = blockIdx.x + tk * gridDim.x < n_tiles
+  auto slot_tiles = [&](int slot) -> int64_t {
+    const int64_t per = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tk = 0..per-1
+    return per <= slot ? 0 : (per - slot + 1) / 2;
   };
-  auto wait_mma = [&]() {
-    mbar_wait(bar_mma, mma_par);
-    mma_par ^= 1u;
-    tc_fence_after();
-  };
+  const int chains_per_tile = 2 * iters + 2;   // 2L Sinkhorn phases + 2 cost halves
 
-  for (int64_t tk = s;; tk += 2) {
-    const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
-    if (tr >= n_tiles) {
-      if (wg_tid == 0) {
-        slot_done[s] = 1;
-        *turn = s ^ 1;
-      }
-      break;
-    }
-    const int64_t t = tile_begin + tr;
-    // ---- tile init: marginal rows -> SMEM, V^T = 1 -> TMEM (A operand)
-    int64_t bi, bj;
-    block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
-    const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
-    named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows / red
-    for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
-      const int r = e / KP, c = e % KP;
-      const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
-      float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
-      if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
-      mrows[r * S::kRS + c] = v;
-    }
-    int ii, jj;
-    const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
-    const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS + h * CW;
-    const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS + h * CW;
+  if (warp >= 2 * kWarpsPerSlot) {
+    // ------------------------------------------------------------------------ MMA warps
+    // One per slot; a turn token makes the two slots' chains alternate in the tensor pipe, and
+    // the waiting slot's warp is already spinning on it while the other issues, so the handoff
+    // overlaps the MMAs still queued.
+    const int ss = warp - 2 * kWarpsPerSlot;
+    const uint32_t g_base = smem_u32(smem + S::kOffG), gc_base = smem_u32(smem + S::kOffGC);
+    const uint64_t gdesc0 = make_sw128_desc(g_base);
+    const uint32_t r0 = (uint32_t)(2 * ss * KP);
+    const uint32_t go = bar_go0 + 16 * ss, mma = bar_mma0 + 16 * ss;
+    const int64_t n_chains = slot_tiles(ss) * chains_per_tile;
+    uint32_t go_par = 0;
+    int f = 0;   // chain index within the current tile
+    mbar_wait(bar_g, 0);
+    for (int64_t j = 0; j < n_chains; ++j) {
+      if (f < 2 * iters) {
+        // Sinkhorn phase f: A = R[f%2], D = R[(f+1)%2]; two halves of the k-steps
+        const uint32_t ra = r0 + (uint32_t)((f & 1) * KP), rd = r0 + (uint32_t)(((f + 1) & 1) * KP);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      uint32_t ones[16];
+        for (int kc = 0; kc < 2; ++kc) {
+          mbar_wait(go + 8 * kc, go_par);
+          if (kc == 0)
+            while (*turn != ss && !slot_done[ss ^ 1]) __nanosleep(20);
+          __syncwarp();
+          tc_fence_after();
+          if (DBG >= 3 && blockIdx.x == 0 && j < chains_per_tile && lane == 0 && f < 512)
+            g_tc_trace[ss][2 + kc][f] = clock64();
+          if (elect_one()) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) ones[e] = (h * CW + c * 16 + e < K) ? 0x3f800000u : 0u;
-      tmem_st16(a_tmem + h * CW + c * 16, ones);
-    }
-    tmem_wait_st();
-    issue_mma(0, -1);  // (its barrier also publishes mrows to the slot's warps)
-
-    for (int f = 0; f < 2 * iters; ++f) {
-      wait_mma();
-      if (DBG == 3 && blockIdx.x == 0 && tk < 2 && wg_tid == 0 && f < 512) g_tc_trace[s][0][f] = clock64();
-      const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
-      // u / v scalings go back to A (next MMA operand); the last v_L goes into D in place
-      const uint32_t dst = ((f == 2 * iters - 1) ? d_tmem : a_tmem) + h * CW;
-      const uint32_t src = d_tmem + h * CW;
-      if (DBG == 1) {
-        if (f != 2 * iters - 1) issue_mma(0, -1);
-        continue;
-      }
-      uint32_t d[2][16];
-      tmem_ld16u(src, d[0]);
-      tmem_wait_ld();
-      reg_fence16(d[0]);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (c + 1 < NC) tmem_ld16u(src + (c + 1) * 16, d[(c + 1) & 1]);
-        const uint32_t* dc = d[c & 1];
-        uint32_t o[16];
-        const float4* m4 = reinterpret_cast<const float4*>(mrow + c * 16);
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          const float4 mq = m4[e >> 2];
-          const float m0 = (e & 2) ? mq.z : mq.x, m1 = (e & 2) ? mq.w : mq.y;
-          // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r, m1/D1 = m1 D0 r.
-          // D > 0 by construction (padded K = 1, dummy marginals); m = 0 gives exactly 0 (R#11).
-          const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
-          const float r = rcp_approx(d0 * d1);
-          const float2 x = fmul2(fmul2(make_float2(m0, m1), make_float2(d1, d0)), make_float2(r, r));
-          o[e] = tf32_rna_pre(x.x);
-          o[e + 1] = tf32_rna_pre(x.y);
-          if (DBG == 4) {  // diagnostics: TMEM traffic without the arithmetic
-            o[e] = dc[e];
-            o[e + 1] = dc[e + 1];
+            for (int kk = 0; kk < CH / 8; ++kk) {
+              const int ks = kc * (CH / 8) + kk;
+              const uint64_t desc = gdesc0 + (uint64_t)((((ks >> 2) * KP * 128) + (ks & 3) * 32) >> 4);
+              if (DBG != 2) mma1_tf32_ts(rd, ra + 8 * ks, desc, kIdesc, (kc > 0 || kk > 0) ? 1u : 0u);
+            }
+            if (kc == 1) {
+              mma1_commit(mma);
+              mma1_commit(mma + 8);
+              *turn = ss ^ 1;
+            }
           }
+          __syncwarp();
         }
-        if (DBG == 5) {  // diagnostics: arithmetic and loads without the TMEM stores
-          uint32_t acc5 = 0;
+      } else {
+        // cost half m = f - 2L: R1[:, 0:KP/2] = R0 (v_L) x (K (.) C_s)[rows m*KP/2 ...]
+        const int m = f - 2 * iters;
+        mbar_wait(go, go_par);
+        mbar_wait(go + 8, go_par);
+        while (*turn != ss && !slot_done[ss ^ 1]) __nanosleep(20);
+        __syncwarp();
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t desc0 = make_sw128_desc(gc_base + (uint32_t)(m * (KP / 2) * 128));
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc5 ^= o[e];
-          if (acc5 == 0x12345678u && iters < 0) g_tc_trace[0][0][0] = acc5;
-        } else {
-          tmem_st16(dst + c * 16, o);
+          for (int ks = 0; ks < KP / 8; ++ks) {
+            const uint64_t desc = desc0 + (uint64_t)(((ks >> 2) * KP * 128 + (ks & 3) * 32) >> 4);
+            mma1_tf32_ts(r0 + KP, r0 + 8 * ks, desc, kIdescHalf, ks > 0 ? 1u : 0u);
+          }
+          mma1_commit(mma);
+          mma1_commit(mma + 8);
+          *turn = ss ^ 1;
         }
-        if (c + 1 < NC) {
-          tmem_wait_ld();
-          reg_fence16(d[(c + 1) & 1]);
-        }
+        __syncwarp();
       }
+      go_par ^= 1u;
+      f = f + 1 == chains_per_tile ? 0 : f + 1;
+    }
+    if (lane == 0) {
+      slot_done[ss] = 1;
+      *turn = ss ^ 1;
+    }
+  } else {
+    // ------------------------------------------------------------------------ epilogue warps
+    float* mrows = marg + (size_t)s * S::kRows * S::kRS;
+    const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+    const uint32_t r0 = lane_off + (uint32_t)(2 * s * KP);   // this thread's lane of R0; R1 = r0 + KP
+    const uint32_t bar_mma = bar_mma0 + 16 * s, bar_go = bar_go0 + 16 * s;
+    uint32_t mma_par = 0;
+    // chunk c of this slot's columns is ready: every thread of the slot stored its part
+    auto go = [&](int c) {
       tmem_wait_st();
-      if (f != 2 * iters - 1) issue_mma(0, (DBG == 3 && tk < 2) ? f : -1);
-      if (DBG == 3 && blockIdx.x == 0 && tk < 2 && wg_tid == 0 && f < 512) g_tc_trace[s][2][f] = clock64();
-    }
-    // ---- cost (a6): d = sum_r u_r ((K (.) C_s) v)_r with u_L in A and v_L in D, in two halves
-    // of N = KP/2 so the product can land in the already-consumed half of A.  Thread half h
-    // covers columns [h KP/4, (h+1) KP/4) of each half; the two partials meet in SMEM.
-    float ust[CQ];
+      tc_fence_before();
+      named_bar_sync(1 + s, kWG);
+      if (wg_tid == 0) mbar_arrive_local(bar_go + 8 * c);
+    };
+    const int64_t my_tiles = slot_tiles(s);
+    for (int64_t tk2 = 0; tk2 < my_tiles; ++tk2) {
+      const int64_t tk = s + 2 * tk2;
+      const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
+      const int64_t t = tile_begin + tr;
+      // ---- tile init: marginal rows -> SMEM, V^T = 1 -> R0 (phase 0's A operand)
+      int64_t bi, bj;
+      block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
+      const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
+      named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows / red
+      for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
+        const int r = e / KP, c = e % KP;
+        const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
+        float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+        if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
+        mrows[r * S::kRS + c] = v;
+      }
+      int ii, jj;
+      const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
+      const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS + h * W;
+      const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS + h * W;
 #pragma unroll
-    for (int c = 0; c < CQ / 8; ++c) tmem_ld8(a_tmem + h * CQ + 8 * c, &ust[8 * c]);
-    tmem_wait_ld();
+      for (int c = 0; c < 2; ++c) {
+        uint32_t ones[W];
 #pragma unroll
-    for (int e = 0; e < CQ; ++e) ust[e] = tf32_mask(ust[e]);
-    issue_mma(1, -1);
-    wait_mma();
-    float acc = 0.0f;
+        for (int e = 0; e < W; ++e) ones[e] = (c * CH + h * W + e < K) ? 0x3f800000u : 0u;
+        tmem_st_cols<W>(r0 + c * CH + h * W, ones);
+      }
+      go(0);  // (its barrier also publishes mrows to the slot's warps)
+      if (wg_tid == 0) mbar_arrive_local(bar_go + 8);
+
+      for (int f = 0; f < 2 * iters; ++f) {
+        const float* mrow = (f & 1) ? brow : arow;  // u-update: a = H[i]; v-update: b = H[j]
+        const uint32_t rd = r0 + (uint32_t)(((f + 1) & 1) * KP) + h * W;
+        const bool last = f + 1 == 2 * iters;
 #pragma unroll
-    for (int c = 0; c < CQ / 8; ++c) {
-      float g[8];
-      tmem_ld8(a_tmem + h * CQ + 8 * c, g);
+        for (int c = 0; c < 2; ++c) {
+          mbar_wait(bar_mma + 8 * c, mma_par);
+          tc_fence_after();
+          if (DBG >= 3 && blockIdx.x == 0 && tk < 2 && wg_tid == 0 && f < 512) g_tc_trace[s][c][f] = clock64();
+          if (DBG != 1 && DBG != 4) {
+            uint32_t d[W];
+            tmem_ld_cols<W>(rd + c * CH, d);
+            float m[W];
+            const float4* m4 = reinterpret_cast<const float4*>(mrow + c * CH);
+#pragma unroll
+            for (int e = 0; e < W / 4; ++e) {
+              const float4 mq = m4[e];
+              m[4 * e] = mq.x; m[4 * e + 1] = mq.y; m[4 * e + 2] = mq.z; m[4 * e + 3] = mq.w;
+            }
+            tmem_wait_ld();
+            uint32_t o[W];
+#pragma unroll
+            for (int e = 0; e < W; e += 2) {
+              // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r, m1/D1 = m1 D0 r.
+              // D > 0 by construction (padded K = 1, dummy marginals); m = 0 gives exactly 0 (R#11).
+              const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
+              const float r = rcp_approx(d0 * d1);
+              const float2 x = fmul2(fmul2(make_float2(m[e], m[e + 1]), make_float2(d1, d0)), make_float2(r, r));
+              o[e] = tf32_rna_pre(x.x);
+              o[e + 1] = tf32_rna_pre(x.y);
+            }
+            tmem_st_cols<W>(rd + c * CH, o);  // in place: the new scaling replaces D
+          }
+          if (!last) go(c);
+        }
+        mma_par ^= 1u;
+        if (last) tmem_wait_st();
+      }
+      // ---- cost (a6): u_L in R1, v_L in R0.  Thread half h covers columns [h KP/4, (h+1) KP/4)
+      // of each cost half; the two partials meet in SMEM.
+      const uint32_t r1 = r0 + KP;
+      float ust[CQ];
+#pragma unroll
+      for (int c = 0; c < CQ / 8; ++c) tmem_ld8(r1 + h * CQ + 8 * c, &ust[8 * c]);
       tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc = fmaf(ust[8 * c + e], g[e], acc);
-    }
-    issue_mma(2, -1);
-    wait_mma();
+      for (int e = 0; e < CQ; ++e) ust[e] = tf32_mask(ust[e]);
+      go(0);
+      if (wg_tid == 0) mbar_arrive_local(bar_go + 8);
+      mbar_wait(bar_mma, mma_par);
+      mbar_wait(bar_mma + 8, mma_par);
+      mma_par ^= 1u;
+      tc_fence_after();
+      float acc = 0.0f;
 #pragma unroll
-    for (int c = 0; c < CQ / 8; ++c) {
-      float g[8], u[8];
-      tmem_ld8(a_tmem + h * CQ + 8 * c, g);
-      tmem_ld8(a_tmem + KP / 2 + h * CQ + 8 * c, u);
-      tmem_wait_ld();
+      for (int c = 0; c < CQ / 8; ++c) {
+        float g[8];
+        tmem_ld8(r1 + h * CQ + 8 * c, g);
+        tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc = fmaf(tf32_mask(u[e]), g[e], acc);
+        for (int e = 0; e < 8; ++e) acc = fmaf(ust[8 * c + e], g[e], acc);
+      }
+      tc_fence_before();
+      named_bar_sync(1 + s, kWG);   // everyone consumed the first half's product
+      if (wg_tid == 0) {
+        mbar_arrive_local(bar_go);
+        mbar_arrive_local(bar_go + 8);
+      }
+      mbar_wait(bar_mma, mma_par);
+      mbar_wait(bar_mma + 8, mma_par);
+      mma_par ^= 1u;
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < CQ / 8; ++c) {
+        float g[8], u[8];
+        tmem_ld8(r1 + h * CQ + 8 * c, g);
+        tmem_ld8(r1 + KP / 2 + h * CQ + 8 * c, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = fmaf(tf32_mask(u[e]), g[e], acc);
+      }
+      float* rs = red + s * 128;
+      if (h == 1) rs[p] = acc;
+      tc_fence_before();
+      named_bar_sync(1 + s, kWG);   // (also: R1 reads done before the next tile's phase-0 MMA)
+      if (h == 0) write_result(out, tr * kTileSlots + p, valid, ii, jj, acc + rs[p]);
     }
-    float* rs = red + s * 128;
-    if (h == 1) rs[p] = acc;
-    named_bar_sync(1 + s, kWG);
-    if (h == 0) write_result(out, tr * kTileSlots + p, valid, ii, jj, acc + rs[p]);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(0u), "r"(kTmemCols)
                  : "memory");
   }
 }
@@ -344,7 +392,7 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = dbg == 1 ? sinkhorn_tc_kernel<KP, 1> : dbg == 2 ? sinkhorn_tc_kernel<KP, 2>
             : dbg == 3 ? sinkhorn_tc_kernel<KP, 3> : dbg == 4 ? sinkhorn_tc_kernel<KP, 4>
-            : dbg == 5 ? sinkhorn_tc_kernel<KP, 5> : sinkhorn_tc_kernel<KP, 0>;
+            : sinkhorn_tc_kernel<KP, 0>;
   cudaError_t e = cudaFuncSetAttribute(kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -354,7 +402,7 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   int64_t grid = (n_tiles + 1) / 2;
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
-  kern<<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+  kern<<<(unsigned)grid, kAllThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
                                                                g_img, gc_img, iters);
   return cudaGetLastError();
 }

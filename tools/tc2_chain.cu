@@ -123,6 +123,87 @@ void run(long long* d, int delay) {
          (double)h / phases, (double)h / phases / 64);
 }
 
+
+// cta_group::1 variants of the 1-SM kernel's chains (asot_sinkhorn_tc.cu): per chain either
+// 4 parts of 8 MMAs (M=128, N=64) with commits after parts 3 and 4 (VAR 10), the same with both
+// commits at the end (VAR 11), or 16 MMAs of N=128 and one commit (VAR 12).  Back to back.
+__device__ __forceinline__ void mma1(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+               ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void commit1(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+template <int VAR>
+__global__ void chain1_kernel(int chains, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t holder;
+  __shared__ __align__(8) uint64_t bars[2];
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[b])) : "memory");
+  }
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((uint32_t*)smem)[i] = 0x3c000000u;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&holder)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = holder;
+  const uint32_t b0 = smem_u32(&bars[0]), b1 = smem_u32(&bars[1]);
+  if (warp == 0) {
+    const uint64_t bd0 = make_sw128_desc(smem_u32(smem));
+    const long long t0 = clock64();
+    for (int c = 0; c < chains; ++c) {
+      const uint32_t base = tm + 256u * (c & 1);
+      const uint32_t ra = base + 128u * ((c >> 1) & 1), rd = base + 128u * (1 - ((c >> 1) & 1));
+      if (threadIdx.x == 0) {
+        if (VAR == 12) {
+          for (int k = 0; k < 16; ++k)
+            mma1(rd, ra + 8 * k, bd0 + (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4), idesc(128, 128), k > 0);
+          commit1(b0);
+        } else {
+          for (int part = 0; part < 4; ++part) {
+            const int kc = part >> 1, nc = part & 1;
+            for (int k = 0; k < 8; ++k)
+              mma1(rd + 64 * nc, ra + 64 * kc + 8 * k,
+                   bd0 + (uint64_t)((((kc * 8 + k) >> 2) * 16384 + nc * 8192 + (k & 3) * 32) >> 4), idesc(128, 64),
+                   (kc > 0 || k > 0));
+            if (VAR == 10 && part >= 2) commit1(part == 2 ? b0 : b1);
+          }
+          if (VAR == 11) {
+            commit1(b0);
+            commit1(b1);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
+template <int VAR>
+void run1(long long* d) {
+  const int chains = 256;
+  auto k = chain1_kernel<VAR>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
+  long long h = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    k<<<1, 128, 70 * 1024>>>(chains, d);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("error\n"); return; }
+  }
+  cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("1-SM variant %d: %7.1f issue cycles/chain (ideal 1034 at 64.6 per N=128 MMA)\n", VAR, (double)h / chains);
+}
+
 int main() {
   long long* d;
   cudaMalloc(&d, 16);
@@ -130,5 +211,8 @@ int main() {
   run<1>(d, 0);
   run<2>(d, 0);
   for (int delay : {200, 400, 600, 800, 1000, 1200}) run<3>(d, delay);
+  run1<10>(d);
+  run1<11>(d);
+  run1<12>(d);
   return 0;
 }
