@@ -126,13 +126,22 @@ void run(long long* d, int delay) {
 
 // cta_group::1 variants of the 1-SM kernel's chains (asot_sinkhorn_tc.cu): per chain either
 // 4 parts of 8 MMAs (M=128, N=64) with commits after parts 3 and 4 (VAR 10), the same with both
-// commits at the end (VAR 11), or 16 MMAs of N=128 and one commit (VAR 12).  Back to back.
+// commits at the end (VAR 11), or 16 MMAs of N=128 and one commit (VAR 12); 13-18 are N=64
+// operand-pattern variants.  Back to back, issued by elect.sync in a converged warp (issuing
+// from `if (threadIdx.x == 0)` instead makes ptxas wrap every MMA in an ELECT loop: ~50 cycles
+// per MMA, which once read here as "N = 64 MMAs are slow").
 __device__ __forceinline__ void mma1(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
                ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc) : "memory");
 }
 __device__ __forceinline__ void commit1(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool elect1() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\telect.sync rx|px, %1;\n\t@px mov.s32 %0, 1;\n\t}"
+               : "+r"(pred) : "r"(0xffffffffu));
+  return pred != 0;
 }
 template <int VAR>
 __global__ void chain1_kernel(int chains, long long* out) {
@@ -160,8 +169,36 @@ __global__ void chain1_kernel(int chains, long long* out) {
     for (int c = 0; c < chains; ++c) {
       const uint32_t base = tm + 256u * (c & 1);
       const uint32_t ra = base + 128u * ((c >> 1) & 1), rd = base + 128u * (1 - ((c >> 1) & 1));
-      if (threadIdx.x == 0) {
-        if (VAR == 12) {
+      if (elect1()) {  // converged warp + elect.sync: no per-MMA ELECT/R2UR loop
+        if (VAR == 13) {         // N = 64, one D range, A marching over 32 k-steps
+          for (int k = 0; k < 32; ++k)
+            mma1(rd, base + 8 * (k & 15), bd0 + (uint64_t)((((k >> 2) & 3) * 16384 + (k & 3) * 32) >> 4), idesc(128, 64), k > 0);
+          commit1(b0);
+        } else if (VAR == 14) {  // N = 64, D alternating between two column ranges every 8 MMAs
+          for (int part = 0; part < 4; ++part)
+            for (int k = 0; k < 8; ++k)
+              mma1(rd + 64 * (part & 1), base + 8 * k, bd0 + (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4),
+                   idesc(128, 64), part > 1 || k > 0);
+          commit1(b0);
+        } else if (VAR == 15) {  // N = 64, D alternating every MMA
+          for (int k = 0; k < 32; ++k)
+            mma1(rd + 64 * (k & 1), base + 8 * (k >> 1 & 7), bd0 + (uint64_t)((((k >> 1) >> 2 & 1) * 16384 + ((k >> 1) & 3) * 32) >> 4),
+                 idesc(128, 64), k > 1);
+          commit1(b0);
+        } else if (VAR == 16) {  // cg2_rate's pattern: fixed D, A = tm+256+8(k&15), B in one 16 KB block
+          for (int k = 0; k < 32; ++k)
+            mma1(tm, tm + 256 + 8 * (k & 15), bd0 + (uint64_t)(((k & 3) * 32) >> 4), idesc(128, 64), k > 0);
+          commit1(b0);
+        } else if (VAR == 17) {  // as 16, B marching over 4 blocks of 16 KB like the kernels
+          for (int k = 0; k < 32; ++k)
+            mma1(tm, tm + 256 + 8 * (k & 15), bd0 + (uint64_t)((((k >> 2) & 3) * 16384 + (k & 3) * 32) >> 4),
+                 idesc(128, 64), k > 0);
+          commit1(b0);
+        } else if (VAR == 18) {  // as 16 but D alternating between two tiles every chain (c)
+          for (int k = 0; k < 32; ++k)
+            mma1(tm + 128 * (c & 1), tm + 256 + 8 * (k & 15), bd0 + (uint64_t)(((k & 3) * 32) >> 4), idesc(128, 64), k > 0);
+          commit1(b0);
+        } else if (VAR == 12) {
           for (int k = 0; k < 16; ++k)
             mma1(rd, ra + 8 * k, bd0 + (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4), idesc(128, 128), k > 0);
           commit1(b0);
@@ -214,5 +251,11 @@ int main() {
   run1<10>(d);
   run1<11>(d);
   run1<12>(d);
+  run1<13>(d);
+  run1<14>(d);
+  run1<15>(d);
+  run1<16>(d);
+  run1<17>(d);
+  run1<18>(d);
   return 0;
 }
