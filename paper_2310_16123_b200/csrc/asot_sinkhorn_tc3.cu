@@ -65,8 +65,10 @@ struct Smem {
 
 // One part of a phase: D[:, nh*KP/2 ...] (+)= sum over K-half kh of
 // (A_hi K_hi + A_lo K_hi + A_hi K_lo), N = KP/2.
+// (The descriptors are the per-image base descriptor plus a constant offset: the issuing warp
+// shares its SM sub-partition with four busy epilogue warps, so its stream is kept short.)
 template <int KP>
-__device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint32_t ghi, uint32_t glo,
+__device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint64_t ghi_desc, uint64_t glo_desc,
                                            int kh, int nh) {
   constexpr int NH = KP / 2;
   constexpr uint32_t idesc = make_idesc_tf32(128, NH);
@@ -76,7 +78,7 @@ __device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint3
   for (int s = 0; s < KP / 16; ++s) {
     const int ks = kh * (KP / 16) + s;  // 8-wide k step
     const uint32_t boff = (uint32_t)((ks >> 2) * KP * 128 + (ks & 3) * 32) + row0;
-    const uint64_t dhi = make_sw128_desc(ghi + boff), dlo = make_sw128_desc(glo + boff);
+    const uint64_t dhi = ghi_desc + (uint64_t)(boff >> 4), dlo = glo_desc + (uint64_t)(boff >> 4);
     const uint32_t acc0 = (kh > 0 || s > 0) ? 1u : 0u;
     mma1_tf32_ts(d, a_reg + 8 * ks, dhi, idesc, acc0);         // x_hi K_hi
     mma1_tf32_ts(d, a_reg + KP + 8 * ks, dhi, idesc, 1u);      // x_lo K_hi
@@ -137,7 +139,8 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
 
   if (warp == kEpiWarps) {
     // ------------------------------------------------------------------ MMA issuer warp
-    const uint32_t ghi = smem_u32(smem + S::kOffGhi), glo = smem_u32(smem + S::kOffGlo);
+    const uint64_t ghi = make_sw128_desc(smem_u32(smem + S::kOffGhi));
+    const uint64_t glo = make_sw128_desc(smem_u32(smem + S::kOffGlo));
     mbar_wait(bar_g, 0);
     uint32_t xpar = 0;
     for (int64_t tr = blockIdx.x; tr < n_tiles; tr += gridDim.x) {

@@ -126,8 +126,13 @@ def test_pairwise_explicit_pairs(asot, cfg, n, npairs, prec):
     assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)], r.max()
 
 
-def test_tile_ranges_and_determinism(asot):
-    inp, _, _, _ = oracle_full("c2", 90)
+@pytest.mark.parametrize("cfg,n", [("c2", 90), ("c3", 70), ("c5", 40)])
+def test_tile_ranges_and_determinism(asot, cfg, n):
+    """D must be bitwise identical for every rank partition (each pair's arithmetic
+    is independent of the tile range that computes it) -- for every resident / streamed kernel
+    (c2: 1-SM and 3xTF32 kernels; c3: CTA-pair and streamed 3xTF32; c5: streamed TF32 / 3xTF32),
+    with cuts at odd tiles so CTA pairs straddle range boundaries."""
+    inp = make_inputs(cfg, n_dist=n)
     pts, offs, w, anc, cst = dev_inputs(inp)
     for prec in (0, 1):
         D1 = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
