@@ -188,36 +188,55 @@ def oracle_sample_rate(inp, budget_s: float, seed: int = 0, mapping: str = "oneh
 
 
 def run_reference(args, inp, rank, world):
-    """--impl reference: the oracle as it stands, each step a bounded sample of the workload."""
+    """--impl reference: the oracle as it stands, each step a bounded sample of the workload.
+
+    Same metric as our arm -- whole-job pairs/s for the N x N matrix -- extrapolated the same
+    way as cpu_baseline: each step maps a seeded sample of distributions (mapping time per point
+    -> all points) and runs the fp64 Sinkhorn on a seeded sample of pairs among them (time per
+    pair -> all P pairs); value = P / (t_map_all + P * t_pair) over the pooled timings."""
     if rank != 0:
         return
-    from asot_inputs import random_pairs
     from oracle import asot_oracle as O
 
     cores = len(os.sched_getaffinity(0))
+    m = max(2, args.ref_dists)
     n_sample = args.ref_pairs
 
     def ref_step(k):
-        pi, pj = random_pairs(inp.n_dist, n_sample, seed=1000 + k)
-        dists = np.unique(np.concatenate([pi, pj]))
-        # map + histogram the distributions the sample touches, then Sinkhorn on the sample
+        rng = np.random.default_rng(1000 + k)
+        dists = np.sort(rng.choice(inp.n_dist, size=min(m, inp.n_dist), replace=False))
         H = np.zeros((inp.n_dist, inp.n_anchors))
+        t0 = time.perf_counter()
+        pts = 0
         for d in dists:
-            s, e = inp.offsets[d], inp.offsets[d + 1]
+            s, e = int(inp.offsets[d]), int(inp.offsets[d + 1])
             _, h = O.map_and_histogram(inp.points[s:e], np.array([0, e - s]), inp.weights[s:e],
                                        inp.anchors)
             H[d] = h[0]
-        O.pair_costs(H, inp.cost, inp.eps, inp.iters, pi.astype(np.int64), pj.astype(np.int64))
+            pts += e - s
+        t_map = time.perf_counter() - t0
+        iu, ju = np.triu_indices(len(dists), k=1)
+        sel = rng.choice(len(iu), size=min(n_sample, len(iu)), replace=False)
+        pi, pj = dists[iu[sel]].astype(np.int64), dists[ju[sel]].astype(np.int64)
+        t0 = time.perf_counter()
+        O.pair_costs(H, inp.cost, inp.eps, inp.iters, pi, pj)
+        return t_map, pts, time.perf_counter() - t0, len(pi)
 
     for k in range(args.warmup):
         ref_step(-1 - k)
+    tm = tp = 0.0
+    npts = npairs = 0
     t0 = time.perf_counter()
     for k in range(args.steps):
-        ref_step(k)
+        a, b, c, d = ref_step(k)
+        tm, npts, tp, npairs = tm + a, npts + b, tp + c, npairs + d
     dt = time.perf_counter() - t0
-    value = n_sample * args.steps / dt
-    sample = (f"per step: {n_sample} seeded random pairs of {inp.name} (mapping of the touched "
-              f"distributions + fp64 Sinkhorn, L={inp.iters})")
+    P = inp.n_pairs
+    value = P / (tm / npts * inp.n_points + P * tp / npairs)
+    sample = (f"per step: mapping of {m} seeded distributions + fp64 Sinkhorn (L={inp.iters}) on "
+              f"{min(n_sample, m * (m - 1) // 2)} seeded pairs among them; whole-job pairs/s "
+              f"extrapolated from the pooled times ({npts} points mapped in {tm:.2f} s, {npairs} "
+              f"pairs in {tp:.2f} s) to all {inp.n_points} points and {P} pairs")
     line = {
         "impl": "reference", "metric": baseline_metric(), "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -279,6 +298,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-pairs", type=int, default=256)
+    ap.add_argument("--ref-dists", type=int, default=24, help="distributions mapped per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n-dist", type=int, default=None,
                     help="shrink N (profiling runs only; bench lines use the full config)")
