@@ -86,7 +86,12 @@ __device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint6
   }
 }
 
-template <int KP>
+// Debug timeline (ASOT_TC_DEBUG_MODE=3, CTA 0's first tile): event, phase -> clock64.
+// events: 0 / 1 = epilogue woke for D half 0 / 1, 2 / 3 = its x half 0 / 1 arrive,
+// 4 / 5 = issuer passed the x half 0 / 1 gate
+__device__ long long g_tc3_trace[6][256];
+
+template <int KP, int DBG>
 __global__ void __launch_bounds__(kThreads, 1)
 sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                     const float* __restrict__ H, int K, const uint32_t* __restrict__ ghi_img,
@@ -148,6 +153,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
         const uint32_t a_reg = (uint32_t)((f & 1) * 2 * KP), d_reg = (uint32_t)(((f + 1) & 1) * 2 * KP);
         mbar_wait(bar_x0, xpar);
         tc_fence_after();
+        if (DBG == 3 && blockIdx.x == 0 && tr == blockIdx.x && lane == 0 && f < 256) g_tc3_trace[4][f] = clock64();
         if (elect_one()) {
           issue_part<KP>(a_reg, d_reg, ghi, glo, 0, 0);
           issue_part<KP>(a_reg, d_reg, ghi, glo, 0, 1);
@@ -155,6 +161,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
         __syncwarp();
         mbar_wait(bar_x1, xpar);
         tc_fence_after();
+        if (DBG == 3 && blockIdx.x == 0 && tr == blockIdx.x && lane == 0 && f < 256) g_tc3_trace[5][f] = clock64();
         if (elect_one()) {
           issue_part<KP>(a_reg, d_reg, ghi, glo, 1, 0);
           mma1_commit(bar_d0);
@@ -217,6 +224,8 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
         for (int h = 0; h < 2; ++h) {
           mbar_wait(h == 0 ? bar_d0 : bar_d1, dpar);
           tc_fence_after();
+          if (DBG == 3 && blockIdx.x == 0 && tr == blockIdx.x && threadIdx.x == 0 && f < 256)
+            g_tc3_trace[h][f] = clock64();
 #pragma unroll
           for (int c4 = 0; c4 < CPT; c4 += 4) {
             const int c = h * NH + cg * CPT + c4;
@@ -245,6 +254,8 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_local(h == 0 ? bar_x0 : bar_x1);
+            if (DBG == 3 && blockIdx.x == 0 && tr == blockIdx.x && threadIdx.x == 0 && f < 256)
+              g_tc3_trace[2 + h][f] = clock64();
           }
         }
         dpar ^= 1u;
@@ -334,7 +345,9 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
                              const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
                              const float* gc, int iters, cudaStream_t s) {
   const size_t smem = Smem<KP>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(sinkhorn_tc3_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
+  auto kern = dbg == 3 ? sinkhorn_tc3_kernel<KP, 3> : sinkhorn_tc3_kernel<KP, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -342,7 +355,7 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t grid = n_tiles < sms ? n_tiles : sms;
   if (grid < 1) return cudaSuccess;
-  sinkhorn_tc3_kernel<KP><<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+  kern<<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
                                                                  ghi, glo, gc, iters);
   return cudaGetLastError();
 }
@@ -379,3 +392,7 @@ cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_
 }
 
 }  // namespace asot
+
+extern "C" int asot_debug_tc3_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, asot::tc3::g_tc3_trace, sizeof(asot::tc3::g_tc3_trace));
+}
