@@ -90,11 +90,38 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
   extern __shared__ float4 map_smem4[];
   float* Ws = reinterpret_cast<float*>(map_smem4);  // [chunk][DP + 4]
   constexpr int RS = DP + 4;                        // row stride: 16-byte shift per row
-  const int lane = threadIdx.x & 31;
   const int q = threadIdx.x & (kLanesPerPoint - 1);
-  const int64_t p = (int64_t)blockIdx.x * kPointsPerBlock + (threadIdx.x >> 2);
-  const bool valid = p < T;
 
+  // anchors are checked for non-finite values once (block 0), not at every staging
+  if (blockIdx.x == 0) {
+    bool bad = false;
+    for (int64_t e = threadIdx.x; e < (int64_t)K * dim; e += kMapThreads) bad |= !isfinite(anchors[e]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
+  }
+  const bool vec = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0);
+  auto stage = [&](int j0, int nc) {  // anchors [j0, j0+nc) -> Ws rows (16-byte vector loads)
+    __syncthreads();
+    if (vec) {
+      for (int e = threadIdx.x; e < nc * (DP / 4); e += kMapThreads) {
+        const int jj = e / (DP / 4), k = 4 * (e % (DP / 4));
+        const float4 v = k < dim ? *reinterpret_cast<const float4*>(anchors + (int64_t)(j0 + jj) * dim + k)
+                                 : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        *reinterpret_cast<float4*>(Ws + jj * RS + k) = v;
+      }
+    } else {
+      for (int e = threadIdx.x; e < nc * DP; e += kMapThreads) {
+        const int jj = e / DP, k = e % DP;
+        Ws[jj * RS + k] = k < dim ? anchors[(int64_t)(j0 + jj) * dim + k] : 0.0f;
+      }
+    }
+    __syncthreads();
+  };
+  const bool single = K <= chunk;   // all anchors resident: staged once for every point group
+  if (single) stage(0, K);
+  const int64_t n_groups = (T + kPointsPerBlock - 1) / kPointsPerBlock;
+  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {   // persistent over point groups
+  const int64_t p = g * kPointsPerBlock + (threadIdx.x >> 2);
+  const bool valid = p < T;
   // point p of this launch is row gather[p] of `points` (k-means batches) or row p
   const int64_t row = valid ? (gather ? gather[p] : p) : 0;
   float x[DP];
@@ -110,28 +137,21 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
   BestTriple bt{INFINITY, INFINITY, 0x7fffffff};
   for (int j0 = 0; j0 < K; j0 += chunk) {
     const int nc = min(chunk, K - j0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nc * DP; e += kMapThreads) {
-      const int jj = e / DP, k = e % DP;
-      const float v = k < dim ? anchors[(int64_t)(j0 + jj) * dim + k] : 0.0f;
-      if (!isfinite(v)) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
-      Ws[jj * RS + k] = v;
-    }
-    __syncthreads();
+    if (!single) stage(j0, nc);
     for (int jj = q; jj < nc; jj += kLanesPerPoint) {
       const float4* w4 = reinterpret_cast<const float4*>(Ws + jj * RS);
-      // four partial sums (coordinates k mod 4): a 4x shorter dependent FMA chain; the bound
-      // below holds for any summation order of the d non-negative rounded terms
-      float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+      // (paired f32x2 subtract / FMA: two coordinates per instruction; the bound below holds
+      // for any summation order of the d non-negative rounded terms)
+      float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int k4 = 0; k4 < DP / 4; ++k4) {
         const float4 w = w4[k4];
-        float t = x[4 * k4 + 0] - w.x; a0 = fmaf(t, t, a0);
-        t = x[4 * k4 + 1] - w.y; a1 = fmaf(t, t, a1);
-        t = x[4 * k4 + 2] - w.z; a2 = fmaf(t, t, a2);
-        t = x[4 * k4 + 3] - w.w; a3 = fmaf(t, t, a3);
+        const float2 t01 = fsub2(make_float2(x[4 * k4 + 0], x[4 * k4 + 1]), make_float2(w.x, w.y));
+        const float2 t23 = fsub2(make_float2(x[4 * k4 + 2], x[4 * k4 + 3]), make_float2(w.z, w.w));
+        a01 = ffma2(t01, t01, a01);
+        a23 = ffma2(t23, t23, a23);
       }
-      const float acc = (a0 + a1) + (a2 + a3);
+      const float acc = (a01.x + a01.y) + (a23.x + a23.y);
       const int j = j0 + jj;  // increasing per lane: strict < keeps the lowest index
       if (acc < bt.best) {
         bt.second = bt.best;
@@ -188,8 +208,8 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
     }
     if (refine) bt.idx = bi;
   }
-  (void)lane;
   if (valid && q == 0) assign[p] = bt.idx;
+  }  // point groups
 }
 
 template <int DP>
@@ -201,8 +221,14 @@ static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int
   if (chunk > K) chunk = K;
   const size_t smem = (size_t)chunk * rs_bytes;
   cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t blocks = (T + kPointsPerBlock - 1) / kPointsPerBlock;
+  int64_t blocks = (T + kPointsPerBlock - 1) / kPointsPerBlock;
   if (blocks == 0) return cudaSuccess;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, map_assign_kernel<DP>, kMapThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;   // persistent grid
   map_assign_kernel<DP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, gather, T, dim, anchors,
                                                                    K, chunk, assign, status);
   return cudaGetLastError();
