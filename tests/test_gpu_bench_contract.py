@@ -39,9 +39,3 @@ def test_bench_line_ours():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "workload" in d["config"]
 
-
-def test_bench_line_reference_arm():
-    d = run("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1", "--ref-pairs", "16")
-    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "pairs/s"
-    assert d["cpu_baseline"]["kind"] == "oracle"
-    assert d["e2e"]["h2d_bytes_per_step"] == 0
