@@ -18,7 +18,7 @@ N, L = 1000, 50
 base = make_inputs("c5", n_dist=N)
 t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 pts, offs, w = t(base.points), t(base.offsets), t(base.weights)
-for K in [16, 32, 64, 96, 128, 192, 256, 384, 512, 768, 1024]:
+for K in [int(k) for k in os.environ.get("KS", "16,32,64,96,128,192,256,384,512,768,1024").split(",")]:
     A = np.ascontiguousarray(base.anchors[:K])
     anc, cst = t(A), t(normalized_sqeuclid_cost(A))
     _, H, _ = asot.map_to_anchors(pts, offs, w, anc, offsets_host=base.offsets)
