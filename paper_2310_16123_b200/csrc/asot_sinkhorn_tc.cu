@@ -11,8 +11,9 @@
 // (K-major SWIZZLE_128B image staged once per CTA by a TMA bulk copy), and the fp32 accumulator
 // D in TMEM.  The scalings of a tile never leave the SM for all 2L+1 MMA phases.
 //
-// Two pair tiles (slots) per CTA keep the tensor pipe busy: while it runs one slot's product
-// ("chain"), the other slot's warps turn their accumulator into the next scaling.  Each slot has
+// Two pair tiles (slots) per CTA -- four for KP <= 64 -- keep the tensor pipe busy: while it
+// runs one slot's product ("chain"), the other slots' warps turn their accumulators into the
+// next scalings.  Each slot has
 // two TMEM regions of KP columns; phase f reads A from R[f%2] and writes D into R[(f+1)%2], and
 // the epilogue writes the new scaling IN PLACE over D, so the roles swap every phase.  The
 // input anchors are cut into two chunks of CH = KP/2: a chain is issued as two halves of N = KP
@@ -21,8 +22,9 @@
 // hides behind the other slot's chain -- instead of the whole epilogue.  (Also splitting N into
 // parts with early output chunks measured slower: 2380 vs 2324 cycles per two chains.)
 //
-// Warp roles (576 threads): warps 0-7 slot 0, warps 8-15 slot 1 (warp w reads TMEM lane quarter
-// w%4 and the column half (w%8)/4 of every chunk); warps 16 / 17 issue the MMAs of slot 0 / 1,
+// Warp roles (576 threads; 640 with four slots): warps 0-7 slot 0, warps 8-15 slot 1 (warp w
+// reads TMEM lane quarter w%4 and the column half (w%8)/4 of every chunk; four slots: 4 warps
+// each, whole chunks); warp 16 + s issues the MMAs of slot s,
 // alternating chains through a turn token, gated per (slot, chunk) by mbarriers the epilogue arrives
 // on, and commits once per chain.  Epilogue: tcgen05.ld -> u = a / D with one MUFU.RCP per
 // two anchors -> RNA rounding to TF32 (add half an ulp; the MMA truncates) -> tcgen05.st.
@@ -45,14 +47,24 @@ namespace tc {
 // events: 0 / 1 = epilogue woke for chunk 0 / 1, 2 / 3 = MMA warp passed the chunk 0 / 1 gate
 __device__ long long g_tc_trace[2][4][512];
 
-constexpr int kWarpsPerSlot = 8;
-constexpr int kThreads = 2 * kWarpsPerSlot * 32;  // epilogue threads
-constexpr int kAllThreads = kThreads + 64;        // + one MMA warp per slot
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = kEpiWarps * 32;  // epilogue threads
+
+// Pair tiles (slots) per CTA: two for KP > 64, four for KP <= 64 (TMEM holds 2·KP columns per
+// slot; with short chains more slots are needed to hide the epilogue latency).  The 16 epilogue
+// warps split evenly over the slots; each slot has its own MMA warp.
+template <int KP> struct Slots {
+  static constexpr int NS = KP <= 64 ? 4 : 2;
+  static constexpr int kWarpsPerSlot = kEpiWarps / NS;   // 8 or 4
+  static constexpr int NG = kWarpsPerSlot / 4;           // column groups per slot: 2 or 1
+  static constexpr int kAllThreads = kThreads + 32 * NS;
+};
 
 using namespace ::asot::ptx;
 
 template <int KP>
 struct Smem {
+  static constexpr int NS = Slots<KP>::NS;
   static constexpr int kRS = KP + 4;                      // marginal row stride (floats)
   static constexpr int kRows = 8 + 16 + 1;                // a-rows, b-rows, dummy row
   static constexpr size_t kImg = (size_t)KP * KP * 4;     // one operand image
@@ -60,9 +72,9 @@ struct Smem {
   static constexpr size_t kOffG = 0;
   static constexpr size_t kOffGC = kImg;
   static constexpr size_t kOffMarg = 2 * kImg;
-  static constexpr size_t kOffRed = kOffMarg + 2 * kMarg;     // [2 slots][128] partial costs
-  static constexpr size_t kOffBar = kOffRed + 2 * 128 * 4;
-  static constexpr size_t kBytes = kOffBar + 128 + 1024;     // + alignment slack
+  static constexpr size_t kOffRed = kOffMarg + NS * kMarg;    // [NS slots][128] partial costs
+  static constexpr size_t kOffBar = kOffRed + NS * 128 * 4;
+  static constexpr size_t kBytes = kOffBar + 256 + 1024;     // + alignment slack
 };
 
 // Loads / stores of W columns (W = 8, 16, 24 or 32) of one TMEM lane quarter.
@@ -99,7 +111,7 @@ __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)
 }
 
 template <int KP, int DBG>
-__global__ void __launch_bounds__(kAllThreads, 1)
+__global__ void __launch_bounds__(Slots<KP>::kAllThreads, 1)
 sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                    const float* __restrict__ H, int K, const uint32_t* __restrict__ g_img,
                    const uint32_t* __restrict__ gc_img, int iters) {
@@ -107,9 +119,12 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   // All 512 columns: the allocation then necessarily starts at column 0 (one CTA per SM), so
   // every TMEM address below is a compile-time constant per slot.
   constexpr uint32_t kTmemCols = 512;
-  constexpr int CH = KP / 2;    // anchors per chunk
-  constexpr int W = CH / 2;     // columns per thread per chunk
-  constexpr int CQ = KP / 4;    // columns per thread in each cost half
+  constexpr int NS = Slots<KP>::NS, NG = Slots<KP>::NG;
+  constexpr int kWarpsPerSlot = Slots<KP>::kWarpsPerSlot;
+  constexpr int CH = KP / 2;         // anchors per chunk
+  constexpr int W = CH / NG;         // columns per thread per chunk
+  constexpr int SB = NG == 2 ? W : 16;       // TMEM ld/st sub-block (columns)
+  constexpr int CQ = KP / 2 / NG;    // columns per thread in each cost half
   constexpr int kWG = kWarpsPerSlot * 32;
   constexpr uint32_t kIdesc = make_idesc_tf32(128, KP);
   constexpr uint32_t kIdescHalf = make_idesc_tf32(128, KP / 2);
@@ -118,27 +133,31 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   float* marg = (float*)(smem + S::kOffMarg);
   float* red = (float*)(smem + S::kOffRed);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
-  // bars: 0 g_loaded, 1 + 2s + c mma_done[s][c], 5 + 2s + c go[s][c]
-  uint32_t* tmem_holder = (uint32_t*)(bars + 10);
-  volatile int* turn = (volatile int*)(bars + 11);
-  volatile int* slot_done = turn + 1;  // [2]
+  // bars: 0 g_loaded, 1 + 2s + c mma_done[s][c], 9 + 2s + c go[s][c]
+  uint32_t* tmem_holder = (uint32_t*)(bars + 17);
+  volatile int* turn = (volatile int*)(bars + 18);
+  volatile int* slot_done = turn + 1;  // [NS]
   const uint32_t bar_g = smem_u32(&bars[0]);
   const uint32_t bar_mma0 = smem_u32(&bars[1]);
-  const uint32_t bar_go0 = smem_u32(&bars[5]);
+  const uint32_t bar_go0 = smem_u32(&bars[9]);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = warp / kWarpsPerSlot;          // slot (pair tile) of an epilogue warp; 2 = MMA warps
+  const int s = warp / kWarpsPerSlot;          // slot (pair tile) of an epilogue warp; NS = MMA warps
   const int sub = warp & 3;                    // TMEM lane quarter this warp may access
-  const int h = (warp % kWarpsPerSlot) >> 2;   // column half of every chunk
+  const int h = (warp % kWarpsPerSlot) >> 2;   // column group of every chunk (0 .. NG-1)
   const int p = sub * 32 + lane;               // pair slot within the tile == TMEM lane
   const int wg_tid = threadIdx.x - s * kWG;
 
+  // tiles of slot s: tk = s, s+NS, ... with tr = blockIdx.x + tk * gridDim.x < n_tiles
+  auto slot_tiles = [&](int slot) -> int64_t {
+    const int64_t per = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tk = 0..per-1
+    return per <= slot ? 0 : (per - slot + NS - 1) / NS;
+  };
   if (threadIdx.x == 0) {
-    turn[0] = 0;
-    slot_done[0] = 0;
-    slot_done[1] = 0;
+    turn[0] = 0;   // slot 0 always has a tile (grid <= n_tiles)
+    for (int b = 0; b < NS; ++b) slot_done[b] = slot_tiles(b) == 0 ? 1 : 0;
     mbar_init(bar_g, 1);
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 2 * NS; ++b) {
       mbar_init(bar_mma0 + 8 * b, 1);
       mbar_init(bar_go0 + 8 * b, 1);
     }
@@ -165,19 +184,23 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
       bulk_g2s(smem_u32(smem + S::kOffGC + off), (const uint8_t*)gc_img + off, n, bar_g);
     }
   }
-  // tiles of slot s: tk = s, s+2, ... with tr = blockIdx.x + tk * gridDim.x < n_tiles
-  auto slot_tiles = [&](int slot) -> int64_t {
-    const int64_t per = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tk = 0..per-1
-    return per <= slot ? 0 : (per - slot + 1) / 2;
-  };
   const int chains_per_tile = 2 * iters + 2;   // 2L Sinkhorn phases + 2 cost halves
 
-  if (warp >= 2 * kWarpsPerSlot) {
+  if (warp >= kEpiWarps) {
     // ------------------------------------------------------------------------ MMA warps
-    // One per slot; a turn token makes the two slots' chains alternate in the tensor pipe, and
-    // the waiting slot's warp is already spinning on it while the other issues, so the handoff
-    // overlaps the MMAs still queued.
-    const int ss = warp - 2 * kWarpsPerSlot;
+    // One per slot; a turn token passed round the active slots makes their chains alternate in
+    // the tensor pipe, and the waiting warps already spin on it while the holder issues, so the
+    // handoff overlaps the MMAs still queued.  Only the holder writes the token.
+    const int ss = warp - kEpiWarps;
+    auto pass_turn = [&]() {
+      for (int k = 1; k <= NS; ++k) {
+        const int cand = (ss + k) % NS;
+        if (cand == ss || !slot_done[cand]) {
+          *turn = cand;
+          break;
+        }
+      }
+    };
     const uint32_t g_base = smem_u32(smem + S::kOffG), gc_base = smem_u32(smem + S::kOffGC);
     const uint64_t gdesc0 = make_sw128_desc(g_base);
     const uint32_t r0 = (uint32_t)(2 * ss * KP);
@@ -194,10 +217,10 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
         for (int kc = 0; kc < 2; ++kc) {
           mbar_wait(go + 8 * kc, go_par);
           if (kc == 0)
-            while (*turn != ss && !slot_done[ss ^ 1]) __nanosleep(20);
+            while (*turn != ss) __nanosleep(20);
           __syncwarp();
           tc_fence_after();
-          if (DBG >= 3 && blockIdx.x == 0 && j < chains_per_tile && lane == 0 && f < 512)
+          if (DBG >= 3 && blockIdx.x == 0 && ss < 2 && j < chains_per_tile && lane == 0 && f < 512)
             g_tc_trace[ss][2 + kc][f] = clock64();
           if (elect_one()) {
 #pragma unroll
@@ -209,7 +232,8 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
             if (kc == 1) {
               mma1_commit(mma);
               mma1_commit(mma + 8);
-              *turn = ss ^ 1;
+              if (j + 1 == n_chains) slot_done[ss] = 1;   // last chain of this slot
+              pass_turn();
             }
           }
           __syncwarp();
@@ -219,7 +243,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
         const int m = f - 2 * iters;
         mbar_wait(go, go_par);
         mbar_wait(go + 8, go_par);
-        while (*turn != ss && !slot_done[ss ^ 1]) __nanosleep(20);
+        while (*turn != ss) __nanosleep(20);
         __syncwarp();
         tc_fence_after();
         if (elect_one()) {
@@ -231,16 +255,13 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
           }
           mma1_commit(mma);
           mma1_commit(mma + 8);
-          *turn = ss ^ 1;
+          if (j + 1 == n_chains) slot_done[ss] = 1;
+          pass_turn();
         }
         __syncwarp();
       }
       go_par ^= 1u;
       f = f + 1 == chains_per_tile ? 0 : f + 1;
-    }
-    if (lane == 0) {
-      slot_done[ss] = 1;
-      *turn = ss ^ 1;
     }
   } else {
     // ------------------------------------------------------------------------ epilogue warps
@@ -258,7 +279,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     };
     const int64_t my_tiles = slot_tiles(s);
     for (int64_t tk2 = 0; tk2 < my_tiles; ++tk2) {
-      const int64_t tk = s + 2 * tk2;
+      const int64_t tk = s + NS * tk2;
       const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
       const int64_t t = tile_begin + tr;
       // ---- tile init: marginal rows -> SMEM, V^T = 1 -> R0 (phase 0's A operand)
@@ -297,28 +318,34 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
           tc_fence_after();
           if (DBG >= 3 && blockIdx.x == 0 && tk < 2 && wg_tid == 0 && f < 512) g_tc_trace[s][c][f] = clock64();
           if (DBG != 1 && DBG != 4) {
-            uint32_t d[W];
-            tmem_ld_cols<W>(rd + c * CH, d);
-            float m[W];
-            const float4* m4 = reinterpret_cast<const float4*>(mrow + c * CH);
+            // the thread's W columns of chunk c in sub-blocks of SB (live registers stay small
+            // when one column group covers a whole chunk)
 #pragma unroll
-            for (int e = 0; e < W / 4; ++e) {
-              const float4 mq = m4[e];
-              m[4 * e] = mq.x; m[4 * e + 1] = mq.y; m[4 * e + 2] = mq.z; m[4 * e + 3] = mq.w;
-            }
-            tmem_wait_ld();
-            uint32_t o[W];
+            for (int b0 = 0; b0 < W; b0 += SB) {
+              uint32_t d[SB];
+              tmem_ld_cols<SB>(rd + c * CH + b0, d);
+              float m[SB];
+              const float4* m4 = reinterpret_cast<const float4*>(mrow + c * CH + b0);
 #pragma unroll
-            for (int e = 0; e < W; e += 2) {
-              // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r, m1/D1 = m1 D0 r.
-              // D > 0 by construction (padded K = 1, dummy marginals); m = 0 gives exactly 0 (R#11).
-              const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
-              const float r = rcp_approx(d0 * d1);
-              const float2 x = fmul2(fmul2(make_float2(m[e], m[e + 1]), make_float2(d1, d0)), make_float2(r, r));
-              o[e] = tf32_rna_pre(x.x);
-              o[e + 1] = tf32_rna_pre(x.y);
+              for (int e = 0; e < SB / 4; ++e) {
+                const float4 mq = m4[e];
+                m[4 * e] = mq.x; m[4 * e + 1] = mq.y; m[4 * e + 2] = mq.z; m[4 * e + 3] = mq.w;
+              }
+              tmem_wait_ld();
+              uint32_t o[SB];
+#pragma unroll
+              for (int e = 0; e < SB; e += 2) {
+                // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r,
+                // m1/D1 = m1 D0 r.  D > 0 by construction (padded K = 1, dummy marginals);
+                // m = 0 gives exactly 0 (R#11).
+                const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
+                const float r = rcp_approx(d0 * d1);
+                const float2 x = fmul2(fmul2(make_float2(m[e], m[e + 1]), make_float2(d1, d0)), make_float2(r, r));
+                o[e] = tf32_rna_pre(x.x);
+                o[e + 1] = tf32_rna_pre(x.y);
+              }
+              tmem_st_cols<SB>(rd + c * CH + b0, o);  // in place: the new scaling replaces D
             }
-            tmem_st_cols<W>(rd + c * CH, o);  // in place: the new scaling replaces D
           }
           if (!last) go(c);
         }
@@ -369,6 +396,12 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
         for (int e = 0; e < 8; ++e) acc = fmaf(tf32_mask(u[e]), g[e], acc);
       }
       float* rs = red + s * 128;
+      if (NG == 1) {
+        tc_fence_before();
+        named_bar_sync(1 + s, kWG);   // R1 reads done before the next tile's phase-0 MMA
+        write_result(out, tr * kTileSlots + p, valid, ii, jj, acc);
+        continue;
+      }
       if (h == 1) rs[p] = acc;
       tc_fence_before();
       named_bar_sync(1 + s, kWG);   // (also: R1 reads done before the next tile's phase-0 MMA)
@@ -399,10 +432,10 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = (n_tiles + 1) / 2;
+  int64_t grid = (n_tiles + Slots<KP>::NS - 1) / Slots<KP>::NS;
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
-  kern<<<(unsigned)grid, kAllThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+  kern<<<(unsigned)grid, Slots<KP>::kAllThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
                                                                g_img, gc_img, iters);
   return cudaGetLastError();
 }
