@@ -35,7 +35,17 @@ using namespace ptx;
 
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;   // 512
-constexpr int kThreads = kEpiThreads + 32;    // + the MMA issuer warp
+
+// Pair tiles (slots) per CTA: TMEM holds 4·KP columns per slot (two [x_hi | x_lo] regions), so
+// KP = 64 fits two slots and KP = 32 four; the 16 epilogue warps split evenly over the slots
+// and each slot has its own MMA warp.  With short phases the other slots' MMAs hide a slot's
+// epilogue latency.
+template <int KP> struct Slots {
+  static constexpr int NS = KP <= 32 ? 4 : (KP <= 64 ? 2 : 1);
+  static constexpr int kWarpsPerSlot = kEpiWarps / NS;
+  static constexpr int NCG = kWarpsPerSlot / 4;      // column groups per slot
+  static constexpr int kThreads = kEpiThreads + 32 * NS;
+};
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
@@ -57,10 +67,11 @@ struct Smem {
   static constexpr size_t kOffGhi = 0;
   static constexpr size_t kOffGlo = kImg;
   static constexpr size_t kOffGC = 2 * kImg;
-  static constexpr size_t kOffMarg = 3 * kImg;
-  static constexpr size_t kOffRed = kOffMarg + (size_t)kRows * kRS * 4;   // [4][128] partial costs
-  static constexpr size_t kOffBar = kOffRed + 4 * 128 * 4;
-  static constexpr size_t kBytes = kOffBar + 64 + 1024;
+  static constexpr int NS = Slots<KP>::NS;
+  static constexpr size_t kOffMarg = 3 * kImg;                             // [NS][kRows][kRS]
+  static constexpr size_t kOffRed = kOffMarg + (size_t)NS * kRows * kRS * 4;   // [NS][NCG][128]
+  static constexpr size_t kOffBar = kOffRed + (size_t)NS * Slots<KP>::NCG * 128 * 4;
+  static constexpr size_t kBytes = kOffBar + 256 + 1024;
 };
 
 // One part of a phase: D[:, nh*KP/2 ...] (+)= sum over K-half kh of
@@ -92,32 +103,45 @@ __device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint6
 __device__ long long g_tc3_trace[6][256];
 
 template <int KP, int DBG>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Slots<KP>::kThreads, 1)
 sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                     const float* __restrict__ H, int K, const uint32_t* __restrict__ ghi_img,
                     const uint32_t* __restrict__ glo_img, const float* __restrict__ gc_plain, int iters) {
   using S = Smem<KP>;
+  constexpr int NS = Slots<KP>::NS, NCG = Slots<KP>::NCG;
+  constexpr int kWPS = Slots<KP>::kWarpsPerSlot, kWG = kWPS * 32;
   constexpr int NH = KP / 2;          // columns per N-half
-  constexpr int CPT = NH / 4;         // columns per epilogue thread per half (4 column groups)
-  constexpr int CQ = KP / 4;          // columns per thread in the cost
+  constexpr int CPT = NH / NCG;       // columns per epilogue thread per half
+  constexpr int CQ = KP / NCG;        // columns per thread in the cost
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* marg = (float*)(smem + S::kOffMarg);
   float* red = (float*)(smem + S::kOffRed);
   const float* gcs = (const float*)(smem + S::kOffGC);
   uint64_t* bars = (uint64_t*)(smem + S::kOffBar);
-  uint32_t* tmem_holder = (uint32_t*)(bars + 7);
+  // bars: 0 g_loaded; slot s: 1 + 4s D-half-0 done, +1 D-half-1 done, +2 x-half-0 ready, +3 x-half-1
+  uint32_t* tmem_holder = (uint32_t*)(bars + 17);
+  volatile int* turn = (volatile int*)(bars + 18);
+  volatile int* slot_done = turn + 1;  // [NS]
   const uint32_t bar_g = smem_u32(&bars[0]);
-  const uint32_t bar_d0 = smem_u32(&bars[1]), bar_d1 = smem_u32(&bars[2]);   // D halves done
-  const uint32_t bar_x0 = smem_u32(&bars[3]), bar_x1 = smem_u32(&bars[4]);   // x halves ready
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // tiles of slot s: tk = s, s+NS, ... with tr = blockIdx.x + tk * gridDim.x < n_tiles
+  auto slot_tiles = [&](int slot) -> int64_t {
+    const int64_t per = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    return per <= slot ? 0 : (per - slot + NS - 1) / NS;
+  };
   if (threadIdx.x == 0) {
+    turn[0] = 0;   // slot 0 always has a tile (grid <= n_tiles)
+    for (int b = 0; b < NS; ++b) slot_done[b] = slot_tiles(b) == 0 ? 1 : 0;
     mbar_init(bar_g, 1);
-    mbar_init(bar_d0, 1);
-    mbar_init(bar_d1, 1);
-    mbar_init(bar_x0, kEpiWarps);
-    mbar_init(bar_x1, kEpiWarps);
+    for (int b = 0; b < NS; ++b) {
+      const uint32_t sb = smem_u32(&bars[1 + 4 * b]);
+      mbar_init(sb, 1);
+      mbar_init(sb + 8, 1);
+      mbar_init(sb + 16, kWPS);
+      mbar_init(sb + 24, kWPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -142,16 +166,36 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
     }
   }
 
-  if (warp == kEpiWarps) {
-    // ------------------------------------------------------------------ MMA issuer warp
+  if (warp >= kEpiWarps) {
+    // ------------------------------------------------------------------ MMA warps (one per slot)
+    // A turn token passed round the active slots orders whole phases of the slots in the tensor
+    // pipe; only the holder writes it.
+    const int ss = warp - kEpiWarps;
+    const uint32_t sb = (uint32_t)(ss * 4 * KP);   // this slot's TMEM columns
+    const uint32_t bar_d0 = smem_u32(&bars[1 + 4 * ss]), bar_d1 = bar_d0 + 8;
+    const uint32_t bar_x0 = bar_d0 + 16, bar_x1 = bar_d0 + 24;
+    auto pass_turn = [&]() {
+      for (int k = 1; k <= NS; ++k) {
+        const int cand = (ss + k) % NS;
+        if (cand == ss || !slot_done[cand]) {
+          *turn = cand;
+          break;
+        }
+      }
+    };
     const uint64_t ghi = make_sw128_desc(smem_u32(smem + S::kOffGhi));
     const uint64_t glo = make_sw128_desc(smem_u32(smem + S::kOffGlo));
     mbar_wait(bar_g, 0);
     uint32_t xpar = 0;
-    for (int64_t tr = blockIdx.x; tr < n_tiles; tr += gridDim.x) {
+    const int64_t my_tiles = slot_tiles(ss);
+    for (int64_t k2 = 0; k2 < my_tiles; ++k2) {
+      const int64_t tr = blockIdx.x + (ss + NS * k2) * (int64_t)gridDim.x;
       for (int f = 0; f < 2 * iters; ++f) {
-        const uint32_t a_reg = (uint32_t)((f & 1) * 2 * KP), d_reg = (uint32_t)(((f + 1) & 1) * 2 * KP);
+        const uint32_t a_reg = sb + (uint32_t)((f & 1) * 2 * KP), d_reg = sb + (uint32_t)(((f + 1) & 1) * 2 * KP);
         mbar_wait(bar_x0, xpar);
+        if (NS > 1)
+          while (*turn != ss) __nanosleep(20);
+        __syncwarp();
         tc_fence_after();
         if (DBG == 3 && blockIdx.x == 0 && tr == blockIdx.x && lane == 0 && f < 256) g_tc3_trace[4][f] = clock64();
         if (elect_one()) {
@@ -167,6 +211,10 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
           mma1_commit(bar_d0);
           issue_part<KP>(a_reg, d_reg, ghi, glo, 1, 1);
           mma1_commit(bar_d1);
+          if (NS > 1) {
+            if (k2 + 1 == my_tiles && f + 1 == 2 * iters) slot_done[ss] = 1;
+            pass_turn();
+          }
         }
         __syncwarp();
         xpar ^= 1u;
@@ -174,18 +222,26 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
     }
   } else {
     // ------------------------------------------------------------------ epilogue warps
-    const int q = warp & 3, cg = warp >> 2;   // TMEM lane quarter, column group
+    const int s = warp / kWPS;                // slot
+    const int q = warp & 3, cg = (warp % kWPS) >> 2;   // TMEM lane quarter, column group
     const int p = q * 32 + lane;              // pair slot == TMEM lane
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int wg_tid = threadIdx.x - s * kWG;
+    const uint32_t lane_off = ((uint32_t)(q * 32) << 16) + (uint32_t)(s * 4 * KP);   // + slot columns
+    const uint32_t bar_d0 = smem_u32(&bars[1 + 4 * s]), bar_d1 = bar_d0 + 8;
+    const uint32_t bar_x0 = bar_d0 + 16, bar_x1 = bar_d0 + 24;
+    marg += (size_t)s * S::kRows * S::kRS;
+    red += (size_t)s * NCG * 128;
     uint32_t dpar = 0;
     bool clamped = false;
-    for (int64_t tr = blockIdx.x; tr < n_tiles; tr += gridDim.x) {
+    const int64_t my_tiles = slot_tiles(s);
+    for (int64_t k2 = 0; k2 < my_tiles; ++k2) {
+      const int64_t tr = blockIdx.x + (s + NS * k2) * (int64_t)gridDim.x;
       const int64_t t = tile_begin + tr;
       int64_t bi, bj;
       block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
       const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
-      named_bar_sync(1, kEpiThreads);  // previous tile's cost readers are done (marg, red, R0)
-      for (int e = threadIdx.x; e < S::kRows * KP; e += kEpiThreads) {
+      named_bar_sync(1 + s, kWG);  // previous tile's cost readers are done (marg, red, R0)
+      for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
         const int r = e / KP, c = e % KP;
         const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
         float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
@@ -210,7 +266,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
         }
       }
       tmem_wait_st();
-      named_bar_sync(1, kEpiThreads);  // marginals visible to every epilogue thread
+      named_bar_sync(1 + s, kWG);  // marginals visible to every epilogue thread of the slot
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -264,12 +320,12 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
       // t_c = sum_r (K (.) C_s)[r][c] u_r for its CQ columns, partial = sum_c v_c t_c.
       // Every thread reads all columns of its lane, written by the other column groups' warps.
       tc_fence_before();
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(1 + s, kWG);
       tc_fence_after();
       float tacc[CQ];
 #pragma unroll
       for (int c = 0; c < CQ; ++c) tacc[c] = 0.0f;
-      const uint32_t r1 = lane_off + (uint32_t)(2 * KP);
+      const uint32_t r1 = lane_off + (uint32_t)(2 * KP);   // (lane_off includes the slot base)
       for (int r0 = 0; r0 < KP; r0 += 4) {
         uint32_t uh[4], ul[4];
         tmem_ld4(r1 + (uint32_t)r0, uh);
@@ -301,9 +357,12 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
           part = fmaf(__uint_as_float(vh[e]) + __uint_as_float(vl[e]), tacc[c4 + e], part);
       }
       red[cg * 128 + p] = part;
-      named_bar_sync(1, kEpiThreads);
+      named_bar_sync(1 + s, kWG);
       if (cg == 0) {
-        const float dsum = (red[p] + red[128 + p]) + (red[256 + p] + red[384 + p]);
+        float dsum;
+        if (NCG == 4) dsum = (red[p] + red[128 + p]) + (red[256 + p] + red[384 + p]);
+        else if (NCG == 2) dsum = red[p] + red[128 + p];
+        else dsum = red[p];
         write_result(out, tr * kTileSlots + p, valid, ii, jj, dsum);
       }
       tc_fence_before();
@@ -353,9 +412,10 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = n_tiles < sms ? n_tiles : sms;
+  int64_t grid = (n_tiles + Slots<KP>::NS - 1) / Slots<KP>::NS;
+  if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
-  kern<<<(unsigned)grid, kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
+  kern<<<(unsigned)grid, Slots<KP>::kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
                                                                  ghi, glo, gc, iters);
   return cudaGetLastError();
 }
