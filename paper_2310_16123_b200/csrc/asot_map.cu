@@ -99,6 +99,7 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
   }
   const bool vec = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0);
+  const bool pvec = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(points) & 15u) == 0);
   auto stage = [&](int j0, int nc) {  // anchors [j0, j0+nc) -> Ws rows (16-byte vector loads)
     __syncthreads();
     if (vec) {
@@ -126,11 +127,21 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
   const int64_t row = valid ? (gather ? gather[p] : p) : 0;
   float x[DP];
   bool finite = true;
+  if (pvec) {   // 16-byte loads of the point row
 #pragma unroll
-  for (int k = 0; k < DP; ++k) {
-    const float v = (valid && k < dim) ? points[row * dim + k] : 0.0f;
-    finite &= isfinite(v);
-    x[k] = v;
+    for (int k = 0; k < DP; k += 4) {
+      const float4 v = (valid && k < dim) ? __ldg(reinterpret_cast<const float4*>(points + row * dim + k))
+                                          : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+      x[k] = v.x; x[k + 1] = v.y; x[k + 2] = v.z; x[k + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < DP; ++k) {
+      const float v = (valid && k < dim) ? points[row * dim + k] : 0.0f;
+      finite &= isfinite(v);
+      x[k] = v;
+    }
   }
   if (!finite) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
 
@@ -138,21 +149,9 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
   for (int j0 = 0; j0 < K; j0 += chunk) {
     const int nc = min(chunk, K - j0);
     if (!single) stage(j0, nc);
-    for (int jj = q; jj < nc; jj += kLanesPerPoint) {
-      const float4* w4 = reinterpret_cast<const float4*>(Ws + jj * RS);
-      // (paired f32x2 subtract / FMA: two coordinates per instruction; the bound below holds
-      // for any summation order of the d non-negative rounded terms)
-      float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (int k4 = 0; k4 < DP / 4; ++k4) {
-        const float4 w = w4[k4];
-        const float2 t01 = fsub2(make_float2(x[4 * k4 + 0], x[4 * k4 + 1]), make_float2(w.x, w.y));
-        const float2 t23 = fsub2(make_float2(x[4 * k4 + 2], x[4 * k4 + 3]), make_float2(w.z, w.w));
-        a01 = ffma2(t01, t01, a01);
-        a23 = ffma2(t23, t23, a23);
-      }
-      const float acc = (a01.x + a01.y) + (a23.x + a23.y);
-      const int j = j0 + jj;  // increasing per lane: strict < keeps the lowest index
+    // two anchors per iteration (rows jj and jj + 4): two independent FMA chains per coordinate
+    // pair, so the shared-memory loads of one row overlap the arithmetic of the other
+    auto update = [&](float acc, int j) {  // j increasing per lane: strict < keeps the lowest index
       if (acc < bt.best) {
         bt.second = bt.best;
         bt.best = acc;
@@ -160,6 +159,29 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
       } else if (acc < bt.second) {
         bt.second = acc;
       }
+    };
+    for (int jj = q; jj < nc; jj += 2 * kLanesPerPoint) {
+      const bool two = jj + kLanesPerPoint < nc;
+      const float4* wa = reinterpret_cast<const float4*>(Ws + jj * RS);
+      const float4* wb = reinterpret_cast<const float4*>(Ws + (two ? jj + kLanesPerPoint : jj) * RS);
+      // (paired f32x2 subtract / FMA: two coordinates per instruction; the bound below holds
+      // for any summation order of the d non-negative rounded terms)
+      float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+      float2 b01 = make_float2(0.0f, 0.0f), b23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int k4 = 0; k4 < DP / 4; ++k4) {
+        const float4 w = wa[k4], v = wb[k4];
+        const float2 x01 = make_float2(x[4 * k4 + 0], x[4 * k4 + 1]);
+        const float2 x23 = make_float2(x[4 * k4 + 2], x[4 * k4 + 3]);
+        const float2 t01 = fsub2(x01, make_float2(w.x, w.y)), t23 = fsub2(x23, make_float2(w.z, w.w));
+        const float2 u01 = fsub2(x01, make_float2(v.x, v.y)), u23 = fsub2(x23, make_float2(v.z, v.w));
+        a01 = ffma2(t01, t01, a01);
+        a23 = ffma2(t23, t23, a23);
+        b01 = ffma2(u01, u01, b01);
+        b23 = ffma2(u23, u23, b23);
+      }
+      update((a01.x + a01.y) + (a23.x + a23.y), j0 + jj);
+      if (two) update((b01.x + b01.y) + (b23.x + b23.y), j0 + jj + kLanesPerPoint);
     }
   }
   // warp-shuffle argmin across the 4 lanes that share this point
