@@ -94,7 +94,7 @@ def distance_matrix_distributed_p2p(n_dist: int, n_anchors: int, offsets_host: n
         lo, hi = partition_by_points(offsets_host, world)[rank]
         if hi > lo:
             steps.map_range_bcast(lo, hi, result.h_peers)
-        torch.cuda.current_stream().synchronize()
+        _sync(dev)
         dist.barrier(group=group)
         H = result.H
     else:
@@ -102,12 +102,19 @@ def distance_matrix_distributed_p2p(n_dist: int, n_anchors: int, offsets_host: n
     t0, t1 = partition_even(n_tiles, world)[rank]
     if t1 > t0:
         steps.tiles_into(H, t0, t1, result.root_ptr)
-    torch.cuda.current_stream().synchronize()   # this rank's stores have landed
+    _sync(dev)                                   # this rank's stores have landed
     dist.barrier(group=group)                    # ... and every other rank's
     if rank != 0:
         return None
     steps.zero_diag(result.D)
     return result.D
+
+
+def _sync(dev):
+    """Wait for this rank's device work (its peer stores) before a barrier; no-op off-GPU (the
+    gloo tests' stand-in steps are synchronous)."""
+    if dev.type == "cuda":
+        torch.cuda.current_stream(dev).synchronize()
 
 
 def _gather_hist(n_anchors, offsets_host, steps, world, rank, dev, group):

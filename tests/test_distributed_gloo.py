@@ -89,6 +89,75 @@ def test_distributed_matches_single_process(world):
     assert np.all(np.diag(D) == 0)
 
 
+class _SharedP2P:
+    """Stand-in for P2PResult: the 'symmetric memory' is CPU shared memory visible to both
+    processes; h_peers / root_ptr are the peer tensors themselves (the stand-in steps below
+    interpret them)."""
+
+    def __init__(self, H_list, D, rank):
+        self.H = H_list[rank]
+        self.h_peers = H_list
+        self.root_ptr = D
+        self.D = D
+
+
+def _p2p_worker(rank, world, port, q, H_list, D):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2310_16123_b200 as asot
+        from paper_2310_16123_b200.distributed import distance_matrix_distributed_p2p
+
+        inp = make_inputs("c1", n_dist=37)
+        steps = _oracle_steps(inp)
+
+        def map_range_bcast(lo, hi, peers):      # this rank's rows -> every rank's H
+            rows = steps.map_range(lo, hi)
+            for Hp in peers:
+                Hp[lo:hi] = rows
+
+        def tiles_into(H, t0, t1, Droot):        # this rank's pairs -> rank 0's matrix
+            packed = steps.tiles(H, t0, t1)
+            steps.unpack(packed, t0, t1, Droot)
+
+        steps.map_range_bcast = map_range_bcast
+        steps.tiles_into = tiles_into
+        out = distance_matrix_distributed_p2p(inp.n_dist, inp.n_anchors, inp.offsets,
+                                              asot.num_tiles(inp.n_dist), steps,
+                                              _SharedP2P(H_list, D, rank), device=torch.device("cpu"))
+        q.put((rank, None if out is None else out.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_p2p_orchestration(world):
+    """The fused-exchange path (histogram rows stored into every rank's H, pair results stored into
+    rank 0's matrix, barriers, rank-0 diagonal) under gloo with shared-memory stand-ins."""
+    inp = make_inputs("c1", n_dist=37)
+    H_list = [torch.zeros((inp.n_dist, inp.n_anchors), dtype=torch.float32).share_memory_()
+              for _ in range(world)]
+    D = torch.full((inp.n_dist, inp.n_dist), -1.0, dtype=torch.float32).share_memory_()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, H_list, D)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(res[r] is None for r in range(1, world))
+    Do, _, H_o = O.distance_matrix(inp.points, inp.offsets, inp.weights, inp.anchors, inp.cost,
+                                   inp.eps, inp.iters)
+    for Hr in H_list:                             # every rank holds the full H
+        np.testing.assert_array_equal(Hr.numpy(), H_o.astype(np.float32))
+    np.testing.assert_allclose(res[0], Do.astype(np.float32), rtol=1e-6, atol=0)
+    assert np.all(np.diag(res[0]) == 0)
+
+
 def test_partitions():
     from paper_2310_16123_b200.distributed import partition_by_points, partition_even
     for n in (0, 1, 7, 100):
