@@ -483,6 +483,232 @@ cudaError_t launch_tiled_dl(const Params& P, cudaStream_t s, bool& done) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// ASOT-DL, dictionary streamed (d in {64, 128} = DP, K a multiple of 64 that the resident
+// kernels cannot hold, e.g. c5: K = 1024, d = 128): same tile of kPT points and the same
+// arithmetic order as the generic kernel (bitwise the same codes), but every layer streams the
+// dictionary through SMEM in 64-row chunks with 16-byte cp.async copies, double-buffered, and
+// both products are register-tiled so each shared-memory load feeds several FMAs:
+//   R[p][k] = sum_j Z[p][j] W[j][k] - X[p][k]   warp w: dims [w DP/8, +DP/8), lane: point p =
+//                                                lane % 16 x DP/16 dims; Z rows read as float4
+//   G[p][j] = sum_k R[p][k] W[j][k]              warp w: chunk rows [8w, 8w+8), lane: point p x
+//                                                4 rows; z <- max(0, z - g - lambda_p)
+// ------------------------------------------------------------------------------------------
+template <int DP>
+struct StreamDL {
+  static constexpr int CR = 64;          // dictionary rows per chunk
+  static constexpr int WS = DP + 4;      // chunk row stride (floats; 16-byte aligned rows)
+  static constexpr int RS = DP + 4;      // R row stride
+  static constexpr size_t bytes(int K, int hidden) {
+    return (size_t)K * 8 + ((size_t)kPT * DP + (size_t)kPT * RS + (size_t)kPT * hidden +
+                            (size_t)kPT * (K + 4) + 3 * kPT + 2 * (size_t)CR * WS) * 4 + 16;
+  }
+};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int DP>
+__global__ void __launch_bounds__(kThreads, 1)
+soft_dl_stream_kernel(Params P) {
+  using C = StreamDL<DP>;
+  constexpr int CR = C::CR, WS = C::WS, RS = C::RS;
+  constexpr int ND = DP / 16;              // GEMM-1 dims per thread
+  extern __shared__ double soft_smem[];
+  const int K = P.K, ZS = K + 4;
+  double* acc = soft_smem;                        // [K] fp64 per-bin sums
+  float* Xs = (float*)(acc + K);                  // [kPT][DP]
+  float* Rs = Xs + kPT * DP;                      // [kPT][RS]
+  float* Hs = Rs + kPT * RS;                      // [kPT][hidden]
+  float* Zs = Hs + kPT * P.hidden;                // [kPT][K + 4]
+  float* misc = Zs + kPT * ZS;
+  float* lam = misc;
+  float* rs = misc + kPT;
+  float* wts = misc + 2 * kPT;
+  float* Wb = (float*)(((uintptr_t)(misc + 3 * kPT) + 15) & ~(uintptr_t)15);   // [2][CR][WS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i = blockIdx.x;
+  const int64_t s = P.offsets[i], e = P.offsets[i + 1];
+  const int nchunks = K / CR;
+
+  // chunk c of the dictionary -> buffer b (16-byte async copies; rows padded to WS floats)
+  auto stage = [&](int c, int b) {
+    float* dst = Wb + (size_t)b * CR * WS;
+    const float* src = P.dict + (int64_t)c * CR * DP;
+    for (int x = tid; x < CR * (DP / 4); x += kThreads) {
+      const int r = x / (DP / 4), k4 = x % (DP / 4);
+      cp_async16(dst + r * WS + 4 * k4, src + (int64_t)r * DP + 4 * k4);
+    }
+    cp_async_commit();
+  };
+
+  for (int j = tid; j < K; j += kThreads) acc[j] = 0.0;
+  bool nonfinite = false, negative = false;
+  double msum = 0.0;
+  const int p = lane & 15;                         // point of this lane in both products
+  const int d0 = warp * (DP / 8) + (lane >> 4) * ND;   // GEMM-1 dims [d0, d0 + ND)
+  const int jr0 = warp * 8 + (lane >> 4) * 4;           // GEMM-2 chunk rows [jr0, jr0 + 4)
+
+  for (int64_t t0 = s; t0 < e; t0 += kPT) {
+    const int np = (int)min((int64_t)kPT, e - t0);
+    __syncthreads();  // previous tile's readers are done
+    for (int x = tid; x < kPT * DP; x += kThreads) {
+      const int pp = x / DP, k = x % DP;
+      float v = 0.0f;
+      if (pp < np) {
+        v = P.points[(t0 + pp) * DP + k];
+        nonfinite |= !isfinite(v);
+      }
+      Xs[x] = v;
+    }
+    if (tid < kPT) {
+      float w = tid < np ? P.weights[t0 + tid] : 0.0f;
+      if (tid < np) {
+        nonfinite |= !isfinite(w);
+        negative |= w < 0.0f;
+        msum += (double)w;
+      }
+      wts[tid] = w;
+    }
+    __syncthreads();
+    hidden_layer<DP>(P, Xs, Hs);
+    __syncthreads();
+    // lambda_p = softplus(v2 . h_p + c2), warp per point
+    for (int pp = warp; pp < kPT; pp += kThreads / 32) {
+      float sdot = 0.0f;
+      for (int c = lane; c < P.hidden; c += 32) sdot = fmaf(Hs[pp * P.hidden + c], __ldg(P.W2 + c), sdot);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+      if (lane == 0) lam[pp] = softplus_f(sdot + P.b2[0]);
+    }
+    for (int x = tid; x < kPT * ZS; x += kThreads) Zs[x] = 0.0f;   // z^(0) = 0 (R#27)
+    // the dictionary stream: per layer one pass for R, one for G; chunk sequence number g
+    int g = 0;
+    stage(0, 0);
+    for (int layer = 0; layer < P.n_layers; ++layer) {
+      for (int pass = 0; pass < 2; ++pass) {
+        float racc[ND];
+#pragma unroll
+        for (int q = 0; q < ND; ++q) racc[q] = 0.0f;
+        for (int c = 0; c < nchunks; ++c, ++g) {
+          // prefetch the next chunk of the stream (next pass / layer wraps to chunk 0)
+          const bool more = !(layer + 1 == P.n_layers && pass == 1 && c + 1 == nchunks);
+          if (more) {
+            stage(c + 1 < nchunks ? c + 1 : 0, (g + 1) & 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncthreads();   // chunk g visible; (pass 1) R complete; (pass 0) Z updated
+          const float* W = Wb + (size_t)(g & 1) * CR * WS;
+          const int c0 = c * CR;
+          if (pass == 0) {
+            // R[p][d0 + q] += sum_j Z[p][c0 + j] W[j][d0 + q]  (j in order)
+            const float* zr = Zs + p * ZS + c0;
+#pragma unroll 4
+            for (int j = 0; j < CR; j += 4) {
+              const float4 z4 = *reinterpret_cast<const float4*>(zr + j);
+              const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const float* wr = W + (j + jj) * WS + d0;
+#pragma unroll
+                for (int q4 = 0; q4 < ND; q4 += 4) {
+                  const float4 w4 = *reinterpret_cast<const float4*>(wr + q4);
+                  racc[q4 + 0] = fmaf(zz[jj], w4.x, racc[q4 + 0]);
+                  racc[q4 + 1] = fmaf(zz[jj], w4.y, racc[q4 + 1]);
+                  racc[q4 + 2] = fmaf(zz[jj], w4.z, racc[q4 + 2]);
+                  racc[q4 + 3] = fmaf(zz[jj], w4.w, racc[q4 + 3]);
+                }
+              }
+            }
+          } else {
+            // G[p][c0 + jr] = sum_k R[p][k] W[jr][k] (k in order); z update in place
+            float gacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const float* rr = Rs + p * RS;
+#pragma unroll 4
+            for (int k = 0; k < DP; k += 4) {
+              const float4 r4 = *reinterpret_cast<const float4*>(rr + k);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 w4 = *reinterpret_cast<const float4*>(W + (jr0 + q) * WS + k);
+                gacc[q] = fmaf(r4.x, w4.x, gacc[q]);
+                gacc[q] = fmaf(r4.y, w4.y, gacc[q]);
+                gacc[q] = fmaf(r4.z, w4.z, gacc[q]);
+                gacc[q] = fmaf(r4.w, w4.w, gacc[q]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float* z = &Zs[p * ZS + c0 + jr0 + q];
+              *z = fmaxf(0.0f, (*z - gacc[q]) - lam[p]);
+            }
+          }
+          __syncthreads();   // buffer g & 1 may be refilled two chunks later
+        }
+        if (pass == 0) {   // r = W z - x
+#pragma unroll
+          for (int q = 0; q < ND; ++q) Rs[p * RS + d0 + q] = racc[q] - Xs[p * DP + d0 + q];
+        }
+      }
+    }
+    __syncthreads();
+    // row sums (warp per point), normalisation, codes, the fp64 point-order H accumulation
+    for (int pp = warp; pp < kPT; pp += kThreads / 32) {
+      float sm = 0.0f;
+      for (int j = lane; j < K; j += 32) sm += Zs[pp * ZS + j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      if (lane == 0) rs[pp] = sm;
+    }
+    __syncthreads();
+    if (tid < np && !(rs[tid] > 0.0f)) atomicOr(P.status, ASOT_FLAG_SOFT_FALLBACK);
+    const float unif = 1.0f / (float)K;
+    for (int j = tid; j < K; j += kThreads) {
+      double a = acc[j];
+      for (int pp = 0; pp < np; ++pp) {  // point order
+        const float z = rs[pp] > 0.0f ? Zs[pp * ZS + j] / rs[pp] : unif;
+        if (P.codes) P.codes[(t0 + pp) * K + j] = z;
+        a += (double)wts[pp] * (double)z;
+      }
+      acc[j] = a;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < K; j += kThreads) P.H[i * K + j] = (float)acc[j];
+  if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(P.status, ASOT_FLAG_NONFINITE_INPUT);
+  if (__syncthreads_or(negative) && tid == 0) atomicOr(P.status, ASOT_FLAG_BAD_MASS);
+  if (tid < kPT) {  // threads < kPT hold the weight partial sums
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) msum += __shfl_xor_sync(0x0000ffffu, msum, o, 16);
+    if (tid == 0) {
+      if (e <= s) atomicOr(P.status, ASOT_FLAG_EMPTY_DIST);
+      else if (fabs(msum - 1.0) > 1e-5) atomicOr(P.status, ASOT_FLAG_BAD_MASS);
+    }
+  }
+}
+
+template <int DP>
+cudaError_t try_stream_dl(const Params& P, cudaStream_t s, bool& done) {
+  done = false;
+  const size_t smem = StreamDL<DP>::bytes(P.K, P.hidden);
+  if (P.dim != DP || P.K % StreamDL<DP>::CR != 0 || smem > 220 * 1024 ||
+      (reinterpret_cast<uintptr_t>(P.dict) & 15u) != 0)
+    return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(soft_dl_stream_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  soft_dl_stream_kernel<DP><<<(unsigned)P.n_dist, kThreads, smem, s>>>(P);
+  done = true;
+  return cudaGetLastError();
+}
+
 // Picks the register-tiled DL kernel when (d, K) has an instantiation and it fits SMEM.
 template <int DP>
 cudaError_t try_tiled_dl(const Params& P, cudaStream_t s, bool& done) {
@@ -597,6 +823,10 @@ cudaError_t launch_soft_map_dl(const float* points, const int64_t* offsets, cons
                   : dim == 64 ? soft::try_tiled_dl<64>(P, s, done)
                               : soft::try_tiled_dl<128>(P, s, done);
     if (e != cudaSuccess || done) return e;
+    if (dim == 64 || dim == 128) {   // dictionary too large for the resident kernels: streamed
+      e = dim == 64 ? soft::try_stream_dl<64>(P, s, done) : soft::try_stream_dl<128>(P, s, done);
+      if (e != cudaSuccess || done) return e;
+    }
   }
   return soft::launch_mode<1>(P, s);
 }
