@@ -521,6 +521,13 @@ def main():
                 "flops_per_pair": flops_per_pair, "pairs_per_launch": pairs_per_launch,
                 "peak_note": peak_note,
                 "peak_sustained_based": peaks.get("bf16_tflops_sustained", 0) * (TF32_OVER_BF16 if eff == asot.TF32 else 0) or None}
+    if bound == "tensor":
+        # context: the hardware's nominal dense TF32 rate (2048 MAC/clk/SM, tools/cg2_rate.cu) at the
+        # median SM clock sampled during the timed region (3xTF32: one third of it)
+        mhz = (clk or {}).get("sm_mhz") or 1965.0
+        nominal = 2048 * 2 * 148 * mhz * 1e6 / 1e12 / (3 if kind in (3, 5) else 1)
+        roofline["nominal_peak_at_clock"] = nominal
+        roofline["frac_of_nominal"] = achieved / nominal
 
     # ---- mapping step (a2): the north star's "achieved HBM GB/s for mapping", next to the
     # FP32-pipe fraction that actually bounds it; live CUDA-event timing
