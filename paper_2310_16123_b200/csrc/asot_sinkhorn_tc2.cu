@@ -265,6 +265,8 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       }
     }  // (the peer's MMA warp idles until the cost)
 
+    long long t_cost0 = 0;
+    if (DBG >= 3) t_cost0 = clock64();
     // ---- cost: u_L in R_a = R[(2L-1)%2] = R1, v_L in R_d = R0 (both as RNA-pre bits)
     const uint32_t ra = lane_off + 256, rdv = 0;  // A-operand (v_L) region base = R0
     float ust[32];
@@ -318,6 +320,10 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       tc_fence_before();
       cluster_sync();  // staging buffer and R1 columns free for the next sub-part / tile
       tc_fence_after();
+    }
+    if (DBG >= 3 && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t k = (b - (tile_begin >> 1)) / (gridDim.x >> 1);
+      if (k < 64) g_tc2_trace[3][k] = clock64() - t_cost0;
     }
     if (epi_warp) red[cq * 128 + p] = acc;
     __syncthreads();

@@ -26,3 +26,4 @@ print("ideal MMA cycles per phase (128 x M256 N64 k8 at 32.7):", 128 * 32.7)
 for f in range(20, 24):
     base = wake[f, 0]
     print(f, "wake", wake[f] - base, "done", done[f] - base, "| next-phase issue", issue[f + 1] - base)
+print("cost section per tile (cycles, CTA 0, first tiles):", buf[3][:8], "phase period x 2L:", np.mean(np.diff(wake[10:60, 0])) * 2 * inp.iters)
