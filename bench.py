@@ -429,6 +429,12 @@ def main():
                                     "distances stored into rank 0's symmetric-memory matrix (NVLink)")
             except Exception as exc:  # noqa: BLE001 - report and fall back
                 exchange_note[0] = f"nccl all-gather + unpack (symmetric memory unavailable: {exc!s:.80})"
+            # every rank must take the same exchange: fall back everywhere if any rank failed
+            ok = torch.tensor([1 if p2p is not None else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0 and p2p is not None:
+                p2p = None
+                exchange_note[0] = "nccl all-gather + unpack (symmetric memory unavailable on a peer rank)"
 
         def step():
             if p2p is not None:
