@@ -88,10 +88,12 @@ int tc_kind(int32_t K, asot_precision prec) {
   if (asot::sinkhorn_tc4_supported(K)) return 4;
   return 0;
 }
-// Explicit pair lists (asot_pairwise_sinkhorn): the streamed kernel in pair-list mode (3xTF32 for
-// fp32 requests, one TF32 pass otherwise) for K >= 32, the CUDA-core kernel below.
+// Explicit pair lists (asot_pairwise_sinkhorn): TF32 with 32 <= K <= 128 -> the resident 1-SM
+// kernel in pair-list mode (7); otherwise the streamed kernel in pair-list mode (3xTF32 for fp32
+// requests, one TF32 pass otherwise) for K >= 32; the CUDA-core kernel below 32.
 int pair_kind(int32_t K, asot_precision prec) {
   if (K < kMinTcAnchors || K > asot::kMaxAnchors) return 0;
+  if (prec != ASOT_PREC_FP32 && asot::sinkhorn_tc_supported(K)) return 7;
   return prec == ASOT_PREC_FP32 ? 5 : 6;
 }
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
@@ -127,10 +129,11 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   } else if (kind == 2) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
-  } else if (kind == 1) {
+  } else if (kind == 1 || kind == 7) {
     const size_t kp = (size_t)asot::kpad32(K);
     b.g_img = (uint32_t*)cv.take(kp * kp * 4);
     b.gc_img = (uint32_t*)cv.take(kp * kp * 4);
+    if (kind == 7) b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc_pairs_scratch_bytes(n_dist, K));
   } else if (kind == 3) {  // K_hi image, K_lo image, plain K (.) C_s
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
@@ -190,7 +193,7 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 3) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc3(cost, K, eps, gb.g_img, gb.gc_img, gb.GC, s));
-  } else if (kind == 1) {
+  } else if (kind == 1 || kind == 7) {
     ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, nullptr, nullptr, gb.g_img, gb.gc_img,
                                         asot::kpad32(K), s));
   } else {
@@ -214,6 +217,9 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   } else if (kind == 1) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                          gb.gc_img, iters, s));
+  } else if (kind == 7) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
+                                               gb.gc_img, (float*)gb.scratch, iters, s));
   } else if (kind == 3) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                           gb.gc_img, gb.GC, iters, s));

@@ -158,11 +158,17 @@ cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const floa
 cudaError_t launch_gibbs_prep_simt(const float* cost, int K, float eps, float* Gp, float* GCp, cudaStream_t s);
 cudaError_t launch_sinkhorn_simt(const PairSource& ps, const PairSink& out, const float* H, int K,
                                  const float* G, const float* GC, int iters, cudaStream_t s);
-// tcgen05 TF32 kernel, tile mode only, K <= 128 (images padded to kpad = roundup(K, 32)).
+// tcgen05 TF32 kernel, K <= 128 (images padded to kpad = roundup(K, 32)): tile mode, and the
+// pair-list mode (list entries in tiles of 128; marginals from a padded copy Hp [(n_dist+1)][kpad]
+// of scratch, sinkhorn_tc_pairs_scratch_bytes).
 bool sinkhorn_tc_supported(int K);
 cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_dist,
                                const PairSink& out, const float* H, int K, const uint32_t* g_img,
                                const uint32_t* gc_img, int iters, cudaStream_t s);
+size_t sinkhorn_tc_pairs_scratch_bytes(int64_t n_dist, int K);
+cudaError_t launch_sinkhorn_tc_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
+                                     const PairSink& out, const float* H, int K, const uint32_t* g_img,
+                                     const uint32_t* gc_img, float* Hp, int iters, cudaStream_t s);
 // tcgen05 cta_group::2 kernel for 128 < K <= 256 (tile mode; images: 2 ranks x 128 KB each).
 bool sinkhorn_tc2_supported(int K);
 size_t sinkhorn_tc2_image_bytes();

@@ -110,11 +110,16 @@ __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)
   }
 }
 
-template <int KP, int DBG>
+// EX (pair-list mode, asot_pairwise_sinkhorn): tile tr holds list entries [128 tr, 128 tr + 128);
+// each slot's marginal rows come straight from the padded copy Hp [(n_dist + 1)][KP] (row n_dist
+// = uniform, for invalid entries), prefetched a chunk ahead into registers, instead of the
+// tile's 25 shared rows in SMEM.
+template <int KP, int DBG, bool EX>
 __global__ void __launch_bounds__(Slots<KP>::kAllThreads, 1)
 sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                    const float* __restrict__ H, int K, const uint32_t* __restrict__ g_img,
-                   const uint32_t* __restrict__ gc_img, int iters) {
+                   const uint32_t* __restrict__ gc_img, int iters, const int32_t* __restrict__ pair_i,
+                   const int32_t* __restrict__ pair_j, int64_t n_pairs, const float* __restrict__ Hp) {
   using S = Smem<KP>;
   // All 512 columns: the allocation then necessarily starts at column 0 (one CTA per SM), so
   // every TMEM address below is a compile-time constant per slot.
@@ -283,21 +288,49 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
       const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
       const int64_t t = tile_begin + tr;
       // ---- tile init: marginal rows -> SMEM, V^T = 1 -> R0 (phase 0's A operand)
-      int64_t bi, bj;
-      block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
-      const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
       named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows / red
-      for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
-        const int r = e / KP, c = e % KP;
-        const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
-        float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
-        if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
-        mrows[r * S::kRS + c] = v;
+      int ii = 0, jj = 0;
+      bool valid;
+      const float* arow;
+      const float* brow;
+      if constexpr (EX) {
+        const int64_t q = tr * kTileSlots + p;   // list entry of this lane
+        valid = q < n_pairs;
+        if (valid) {
+          ii = pair_i[q];
+          jj = pair_j[q];
+          valid = ii >= 0 && jj >= 0 && ii < n_dist && jj < n_dist;
+        }
+        arow = Hp + (valid ? (int64_t)ii : n_dist) * KP + h * W;
+        brow = Hp + (valid ? (int64_t)jj : n_dist) * KP + h * W;
+      } else {
+        int64_t bi, bj;
+        block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
+        const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
+        for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
+          const int r = e / KP, c = e % KP;
+          const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
+          float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+          if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
+          mrows[r * S::kRS + c] = v;
+        }
+        valid = tile_slot_pair(t, p, n_dist, ii, jj);
+        arow = mrows + (valid ? (p >> 4) : 24) * S::kRS + h * W;
+        brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS + h * W;
       }
-      int ii, jj;
-      const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
-      const float* arow = mrows + (valid ? (p >> 4) : 24) * S::kRS + h * W;
-      const float* brow = mrows + (valid ? 8 + (p & 15) : 24) * S::kRS + h * W;
+      // (EX) marginal values of the current chunk, prefetched from L2 one chunk ahead
+      float mk[EX ? W : 1];
+      auto load_mk = [&](int f, int c) {
+        if constexpr (EX) {
+          const float4* m4 = reinterpret_cast<const float4*>(((f & 1) ? brow : arow) + c * CH);
+#pragma unroll
+          for (int e = 0; e < W / 4; ++e) {
+            const float4 mq = __ldg(m4 + e);
+            mk[4 * e] = mq.x; mk[4 * e + 1] = mq.y; mk[4 * e + 2] = mq.z; mk[4 * e + 3] = mq.w;
+          }
+        }
+      };
+      load_mk(0, 0);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t ones[W];
@@ -325,11 +358,16 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
               uint32_t d[SB];
               tmem_ld_cols<SB>(rd + c * CH + b0, d);
               float m[SB];
-              const float4* m4 = reinterpret_cast<const float4*>(mrow + c * CH + b0);
+              if constexpr (EX) {
 #pragma unroll
-              for (int e = 0; e < SB / 4; ++e) {
-                const float4 mq = m4[e];
-                m[4 * e] = mq.x; m[4 * e + 1] = mq.y; m[4 * e + 2] = mq.z; m[4 * e + 3] = mq.w;
+                for (int e = 0; e < SB; ++e) m[e] = mk[b0 + e];
+              } else {
+                const float4* m4 = reinterpret_cast<const float4*>(mrow + c * CH + b0);
+#pragma unroll
+                for (int e = 0; e < SB / 4; ++e) {
+                  const float4 mq = m4[e];
+                  m[4 * e] = mq.x; m[4 * e + 1] = mq.y; m[4 * e + 2] = mq.z; m[4 * e + 3] = mq.w;
+                }
               }
               tmem_wait_ld();
               uint32_t o[SB];
@@ -346,6 +384,8 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
               }
               tmem_st_cols<SB>(rd + c * CH + b0, o);  // in place: the new scaling replaces D
             }
+            if (c == 0) load_mk(f, 1);
+            else if (!last) load_mk(f + 1, 0);
           }
           if (!last) go(c);
         }
@@ -420,12 +460,14 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
 template <int KP>
 static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, const PairSink& out,
                              const float* H, int K, const uint32_t* g_img, const uint32_t* gc_img,
-                             int iters, cudaStream_t s) {
+                             int iters, cudaStream_t s, const int32_t* pi = nullptr,
+                             const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr) {
   const size_t smem = Smem<KP>::kBytes;
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
-  auto kern = dbg == 1 ? sinkhorn_tc_kernel<KP, 1> : dbg == 2 ? sinkhorn_tc_kernel<KP, 2>
-            : dbg == 3 ? sinkhorn_tc_kernel<KP, 3> : dbg == 4 ? sinkhorn_tc_kernel<KP, 4>
-            : sinkhorn_tc_kernel<KP, 0>;
+  auto kern = pi != nullptr ? sinkhorn_tc_kernel<KP, 0, true>
+            : dbg == 1 ? sinkhorn_tc_kernel<KP, 1, false> : dbg == 2 ? sinkhorn_tc_kernel<KP, 2, false>
+            : dbg == 3 ? sinkhorn_tc_kernel<KP, 3, false> : dbg == 4 ? sinkhorn_tc_kernel<KP, 4, false>
+            : sinkhorn_tc_kernel<KP, 0, false>;
   cudaError_t e = cudaFuncSetAttribute(kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -436,8 +478,23 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
   kern<<<(unsigned)grid, Slots<KP>::kAllThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
-                                                               g_img, gc_img, iters);
+                                                               g_img, gc_img, iters, pi, pj, n_pairs, Hp);
   return cudaGetLastError();
+}
+
+// Padded marginal rows for the pair-list mode: Hp[r][c] = H[r][c] (c < K), 0 (K <= c < KP);
+// row n_dist = uniform 1/K (the dummy for invalid list entries).
+__global__ void pad_marginals_tc_kernel(const float* __restrict__ H, int64_t n_dist, int K, int kp,
+                                        float* __restrict__ Hp) {
+  const int64_t total = (n_dist + 1) * kp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / kp;
+    const int c = (int)(idx % kp);
+    float v = 0.0f;
+    if (c < K) v = row < n_dist ? H[row * K + c] : 1.0f / (float)K;
+    Hp[idx] = v;
+  }
 }
 
 }  // namespace tc
@@ -454,6 +511,28 @@ cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_d
     case 64: return tc::launch_kp<64>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
     case 96: return tc::launch_kp<96>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
     case 128: return tc::launch_kp<128>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+size_t sinkhorn_tc_pairs_scratch_bytes(int64_t n_dist, int K) {
+  return (size_t)(n_dist + 1) * kpad32(K) * 4;
+}
+
+cudaError_t launch_sinkhorn_tc_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
+                                     const PairSink& out, const float* H, int K, const uint32_t* g_img,
+                                     const uint32_t* gc_img, float* Hp, int iters, cudaStream_t s) {
+  if (n_pairs <= 0) return cudaSuccess;
+  const int kp = kpad32(K);
+  tc::pad_marginals_tc_kernel<<<512, 256, 0, s>>>(H, n_dist, K, kp, Hp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t n_tiles = (n_pairs + kTileSlots - 1) / kTileSlots;
+  switch (kp) {
+    case 32: return tc::launch_kp<32>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
+    case 64: return tc::launch_kp<64>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
+    case 96: return tc::launch_kp<96>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
+    case 128: return tc::launch_kp<128>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
     default: return cudaErrorNotSupported;
   }
 }
