@@ -126,6 +126,39 @@ def test_pairwise_explicit_pairs(asot, cfg, n, npairs, prec):
     assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)], r.max()
 
 
+@pytest.mark.parametrize("K", [32, 50, 64, 96, 128])
+def test_pairwise_resident_pair_mode(asot, K):
+    """TF32 pair lists with K <= 128 run the resident 1-SM kernel in pair-list mode (2 and 4 slots
+    per CTA): every i < j entry equals the tile path's value for that pair bitwise (same kernel
+    arithmetic), invalid entries (out-of-range indices) give 0, and all values (reversed
+    orientations included) are within the TF32 bar of the oracle."""
+    inp = make_inputs("c2", n_dist=45)
+    A = np.ascontiguousarray(inp.anchors[:K])
+    C = (((A[:, None, :].astype(np.float64) - A[None, :, :]) ** 2).sum(-1))
+    C = (C / C.max()).astype(np.float32)
+    pts, offs, w, _, _ = dev_inputs(inp)
+    anc, cst = torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda()
+    _, H, _ = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+    D = asot.distance_matrix(None, None, None, None, cst, float(inp.eps), inp.iters, precision=asot.TF32,
+                             hist=H, cost_max=1.0)
+    pi, pj = random_pairs(inp.n_dist, 700, seed=11)
+    pi = np.concatenate([pi, pj[:40], [-1, 3, inp.n_dist]]).astype(np.int32)   # reversed + invalid
+    pj = np.concatenate([pj, pi[:40], [2, inp.n_dist + 5, 1]]).astype(np.int32)
+    st = asot.asot.new_status()
+    d = asot.pairwise_sinkhorn(H, cst, float(inp.eps), inp.iters, torch.from_numpy(pi).cuda(),
+                               torch.from_numpy(pj).cuda(), precision=asot.TF32, status=st, cost_max=1.0)
+    torch.cuda.synchronize()
+    d = d.cpu().numpy()
+    Dn = D.cpu().numpy()
+    ok = (pi >= 0) & (pj >= 0) & (pi < inp.n_dist) & (pj < inp.n_dist)
+    assert np.all(d[~ok] == 0.0)
+    fwd = ok & (pi < pj)   # the tile path computes i < j with a = H[i] on the u side (R#10)
+    np.testing.assert_array_equal(d[fwd], Dn[pi[fwd], pj[fwd]])
+    c_o, _ = O.pair_costs(H.cpu().numpy().astype(np.float64), C.astype(np.float64), inp.eps, inp.iters,
+                          pi[ok].astype(np.int64), pj[ok].astype(np.int64))
+    assert rel_err(d[ok], c_o, 1.0).max() <= TOL[asot.TF32]
+
+
 @pytest.mark.parametrize("cfg,n", [("c2", 90), ("c3", 70), ("c5", 40)])
 def test_tile_ranges_and_determinism(asot, cfg, n):
     """D must be bitwise identical for every rank partition (each pair's arithmetic
