@@ -58,9 +58,12 @@ def test_padded_anchor_counts(asot, K, prec):
     np.testing.assert_array_equal(Dg, Dg.T)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 17])
-def test_tiny_n(asot, n):
-    inp = make_inputs("c2", n_dist=n, iters=5)
+@pytest.mark.parametrize("cfg,n", [("c2", 1), ("c2", 2), ("c2", 3), ("c2", 17), ("c3", 1), ("c3", 2),
+                                   ("c3", 17), ("c5", 2), ("c5", 17), ("c1", 2)])
+def test_tiny_n(asot, cfg, n):
+    """N = 1 (no pairs), 2 (one pair, one tile), 3, 17 (a ragged second block) on every kernel family:
+    1-SM (c2), CTA pair (c3), streamed (c5), 3xTF32 at K < 32 (c1), both precisions."""
+    inp = make_inputs(cfg, n_dist=n, iters=5)
     for prec in (0, 1):
         Dg, Do, st = run_both(asot, inp, prec)
         assert st == 0 and Dg.shape == (n, n)
