@@ -113,11 +113,12 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
                                       uint32_t* status, void* stream);
 
 /* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed).
- * ASOT_PREC_TF32 with 32 <= K <= 128: the resident 1-SM tcgen05 kernel in pair-list mode
- * (bitwise the values of the tile path); other K >= 32: the streamed tcgen05 kernel in pair-list
- * mode (ASOT_PREC_TF32: one TF32 pass; ASOT_PREC_FP32: 3xTF32); both take tiles of 128
- * consecutive list entries and read each entry's marginal rows from a padded copy of H in the
- * workspace (L2-resident); K < 32: the fp32 CUDA-core kernel.  Workspace from
+ * K <= 128: the resident 1-SM tcgen05 kernels in pair-list mode (ASOT_PREC_TF32 with K >= 32:
+ * TF32; ASOT_PREC_FP32, and every K < 32: 3xTF32), bitwise the values of the tile path; K > 128:
+ * the streamed tcgen05 kernel in pair-list mode (TF32: one pass; FP32: 3xTF32).  All take tiles
+ * of 128 consecutive list entries and read each entry's marginal rows from a padded copy of H in
+ * the workspace (L2-resident).  (Environment ASOT_PAIR_KERNEL=simt selects the fp32 CUDA-core
+ * kernel instead, for cross-checks.)  Invalid entries (index out of range) give 0.  Workspace from
  * asot_pairwise_workspace_bytes(n_dist, n_anchors, prec).  Arguments:
  *   hist     [n_dist, n_anchors] f32 device (rows are a' / b')
  *   cost     [n_anchors, n_anchors] f32 device: C_s symmetric, >= 0, zero diagonal
@@ -277,8 +278,7 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
  * 1-SM resident (ASOT_PREC_FP32 with K <= 128, and every request with K < 32), 4 = TF32 CTA-pair
  * streamed (256 < K <= 1024, K padded to 512 or 1024),
  * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024).
- * (Pair lists: TF32 with K <= 128 the 1-SM kernel's pair-list mode, else the streamed kernel's
- * pair-list mode, 3xTF32 or one-pass TF32.) */
+ * (Pair lists: K <= 128 the 1-SM kernels' pair-list modes, else the streamed kernel's.) */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 
 /* Optional kernel timing (bench.py's roofline): while enabled on this thread, the library records

@@ -91,7 +91,8 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 4: "sinkhorn_tc4_kernel (TF32, streamed GEMM form, CTA pair, M=N=256)",
                 5: "sinkhorn_tc5_kernel (3xTF32 fp32-accurate, streamed GEMM form, CTA pair, M=N=256)",
                 6: "sinkhorn_tc5_kernel (TF32 one-pass, streamed GEMM form, pair-list mode, CTA pair)",
-                7: "sinkhorn_tc_kernel (TF32, 1 SM, M=128, pair-list mode)"}
+                7: "sinkhorn_tc_kernel (TF32, 1 SM, M=128, pair-list mode)",
+                8: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128, pair-list mode)"}
 
 
 def sinkhorn_kernel_kind(n_anchors: int, precision: int) -> int:

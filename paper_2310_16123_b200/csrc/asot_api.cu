@@ -88,12 +88,17 @@ int tc_kind(int32_t K, asot_precision prec) {
   if (asot::sinkhorn_tc4_supported(K)) return 4;
   return 0;
 }
-// Explicit pair lists (asot_pairwise_sinkhorn): TF32 with 32 <= K <= 128 -> the resident 1-SM
-// kernel in pair-list mode (7); otherwise the streamed kernel in pair-list mode (3xTF32 for fp32
-// requests, one TF32 pass otherwise) for K >= 32; the CUDA-core kernel below 32.
+// Explicit pair lists (asot_pairwise_sinkhorn): K <= 128 -> the resident 1-SM kernels in
+// pair-list mode (TF32: 7; fp32 requests and every K < 32: 3xTF32, 8); above, the streamed
+// kernel in pair-list mode (3xTF32 for fp32 requests, one TF32 pass otherwise).
 int pair_kind(int32_t K, asot_precision prec) {
-  if (K < kMinTcAnchors || K > asot::kMaxAnchors) return 0;
-  if (prec != ASOT_PREC_FP32 && asot::sinkhorn_tc_supported(K)) return 7;
+  if (K < 1 || K > asot::kMaxAnchors) return 0;
+  // ASOT_PAIR_KERNEL=simt: the fp32 CUDA-core kernel for pair lists (cross-checks of the tensor-core
+  // pair-list modes against an independent fp32 implementation)
+  static const bool simt = getenv("ASOT_PAIR_KERNEL") && std::string(getenv("ASOT_PAIR_KERNEL")) == "simt";
+  if (simt) return 0;
+  if (K < kMinTcAnchors) return 8;   // the 3xTF32 1-SM kernel's pair-list mode (as tile requests, R#23)
+  if (asot::sinkhorn_tc_supported(K)) return prec == ASOT_PREC_FP32 ? 8 : 7;
   return prec == ASOT_PREC_FP32 ? 5 : 6;
 }
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
@@ -134,10 +139,11 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
     b.g_img = (uint32_t*)cv.take(kp * kp * 4);
     b.gc_img = (uint32_t*)cv.take(kp * kp * 4);
     if (kind == 7) b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc_pairs_scratch_bytes(n_dist, K));
-  } else if (kind == 3) {  // K_hi image, K_lo image, plain K (.) C_s
+  } else if (kind == 3 || kind == 8) {  // K_hi image, K_lo image, plain K (.) C_s (+ padded H)
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
     b.GC = (float*)cv.take(asot::sinkhorn_tc3_image_bytes(K));
+    if (kind == 8) b.scratch = (uint8_t*)cv.take(asot::sinkhorn_tc3_pairs_scratch_bytes(n_dist, K));
   } else {  // CUDA-core kernel: row-padded fp32 K and K (.) C_s [K][simt_kpad(K)]
     b.G = (float*)cv.take((size_t)K * asot::simt_kpad(K) * 4);
     b.GC = (float*)cv.take((size_t)K * asot::simt_kpad(K) * 4);
@@ -191,7 +197,7 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc4(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
-  } else if (kind == 3) {
+  } else if (kind == 3 || kind == 8) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc3(cost, K, eps, gb.g_img, gb.gc_img, gb.GC, s));
   } else if (kind == 1 || kind == 7) {
     ASOT_LAUNCH(asot::launch_gibbs_prep(cost, K, eps, nullptr, nullptr, gb.g_img, gb.gc_img,
@@ -223,6 +229,9 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   } else if (kind == 3) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                           gb.gc_img, gb.GC, iters, s));
+  } else if (kind == 8) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc3_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
+                                                gb.gc_img, gb.GC, (float*)gb.scratch, iters, s));
   } else {
     ASOT_LAUNCH(asot::launch_sinkhorn_simt(ps, sink, H, K, gb.G, gb.GC, iters, s));
   }

@@ -213,6 +213,10 @@ bool sinkhorn_tc3_supported(int K);
 size_t sinkhorn_tc3_image_bytes(int K);
 cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t* ghi, uint32_t* glo,
                                   float* gc, cudaStream_t s);
+size_t sinkhorn_tc3_pairs_scratch_bytes(int64_t n_dist, int K);
+cudaError_t launch_sinkhorn_tc3_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
+                                      const PairSink& out, const float* H, int K, const uint32_t* ghi,
+                                      const uint32_t* glo, const float* gc, float* Hp, int iters, cudaStream_t s);
 cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
                                 const float* gc, int iters, cudaStream_t s);

@@ -102,11 +102,16 @@ __device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint6
 // 4 / 5 = issuer passed the x half 0 / 1 gate
 __device__ long long g_tc3_trace[6][256];
 
-template <int KP, int DBG>
+// EX (pair-list mode): tile tr holds list entries [128 tr, 128 tr + 128); each lane's marginal rows
+// come from the padded copy Hp [(n_dist + 1)][KP] (row n_dist = uniform, for invalid entries),
+// prefetched half a phase ahead into registers, instead of the tile's 25 rows in SMEM.
+template <int KP, int DBG, bool EX>
 __global__ void __launch_bounds__(Slots<KP>::kThreads, 1)
 sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                     const float* __restrict__ H, int K, const uint32_t* __restrict__ ghi_img,
-                    const uint32_t* __restrict__ glo_img, const float* __restrict__ gc_plain, int iters) {
+                    const uint32_t* __restrict__ glo_img, const float* __restrict__ gc_plain, int iters,
+                    const int32_t* __restrict__ pair_i, const int32_t* __restrict__ pair_j, int64_t n_pairs,
+                    const float* __restrict__ Hp) {
   using S = Smem<KP>;
   constexpr int NS = Slots<KP>::NS, NCG = Slots<KP>::NCG;
   constexpr int kWPS = Slots<KP>::kWarpsPerSlot, kWG = kWPS * 32;
@@ -237,21 +242,49 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
     for (int64_t k2 = 0; k2 < my_tiles; ++k2) {
       const int64_t tr = blockIdx.x + (s + NS * k2) * (int64_t)gridDim.x;
       const int64_t t = tile_begin + tr;
-      int64_t bi, bj;
-      block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
-      const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
       named_bar_sync(1 + s, kWG);  // previous tile's cost readers are done (marg, red, R0)
-      for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
-        const int r = e / KP, c = e % KP;
-        const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
-        float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
-        if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
-        marg[r * S::kRS + c] = v;
+      int ii = 0, jj = 0;
+      bool valid;
+      const float* arow;
+      const float* brow;
+      if constexpr (EX) {
+        const int64_t q = tr * kTileSlots + p;   // list entry of this lane
+        valid = q < n_pairs;
+        if (valid) {
+          ii = pair_i[q];
+          jj = pair_j[q];
+          valid = ii >= 0 && jj >= 0 && ii < n_dist && jj < n_dist;
+        }
+        arow = Hp + (valid ? (int64_t)ii : n_dist) * KP;
+        brow = Hp + (valid ? (int64_t)jj : n_dist) * KP;
+      } else {
+        int64_t bi, bj;
+        block_pair_decode(t >> 1, num_blocks(n_dist), bi, bj);
+        const int64_t i0 = bi * kBlockDist + (t & 1) * 8, j0 = bj * kBlockDist;
+        for (int e = wg_tid; e < S::kRows * KP; e += kWG) {
+          const int r = e / KP, c = e % KP;
+          const int64_t row = r < 8 ? i0 + r : (r < 24 ? j0 + (r - 8) : n_dist);
+          float v = (row < n_dist && c < K) ? H[row * K + c] : 0.0f;
+          if (r == 24) v = c < K ? 1.0f / (float)K : 0.0f;  // dummy marginal for invalid slots
+          marg[r * S::kRS + c] = v;
+        }
+        valid = tile_slot_pair(t, p, n_dist, ii, jj);
+        arow = marg + (valid ? (p >> 4) : 24) * S::kRS;
+        brow = marg + (valid ? 8 + (p & 15) : 24) * S::kRS;
       }
-      int ii, jj;
-      const bool valid = tile_slot_pair(t, p, n_dist, ii, jj);
-      const float* arow = marg + (valid ? (p >> 4) : 24) * S::kRS;
-      const float* brow = marg + (valid ? 8 + (p & 15) : 24) * S::kRS;
+      // (EX) the lane's CPT marginal values of the next half, prefetched from L2
+      float mk[EX ? CPT : 1];
+      auto load_mk = [&](int f, int h) {
+        if constexpr (EX) {
+          const float4* m4 = reinterpret_cast<const float4*>(((f & 1) ? brow : arow) + h * NH + cg * CPT);
+#pragma unroll
+          for (int e = 0; e < CPT / 4; ++e) {
+            const float4 mq = __ldg(m4 + e);
+            mk[4 * e] = mq.x; mk[4 * e + 1] = mq.y; mk[4 * e + 2] = mq.z; mk[4 * e + 3] = mq.w;
+          }
+        }
+      };
+      load_mk(0, 0);
       // x^(0) = v0 = 1 on the real anchors, hi = 1, lo = 0, into R0 (both halves)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -288,8 +321,13 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
             uint32_t dv[4], hi[4], lo[4];
             tmem_ld4(lane_off + d_reg + (uint32_t)c, dv);
             tmem_wait_ld();
-            const float4 m4 = *reinterpret_cast<const float4*>(mrow + c);
-            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+            float mm[4];
+            if constexpr (EX) {
+              mm[0] = mk[c4]; mm[1] = mk[c4 + 1]; mm[2] = mk[c4 + 2]; mm[3] = mk[c4 + 3];
+            } else {
+              const float4 m4 = *reinterpret_cast<const float4*>(mrow + c);
+              mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               float den = __uint_as_float(dv[e]);
@@ -305,6 +343,8 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
             tmem_st4(lane_off + d_reg + (uint32_t)c, hi);
             tmem_st4(lane_off + d_reg + (uint32_t)(KP + c), lo);
           }
+          if (h == 0) load_mk(f, 1);
+          else if (f + 1 < 2 * iters) load_mk(f + 1, 0);
           tmem_wait_st();
           if (f + 1 < 2 * iters) {
             tc_fence_before();
@@ -402,10 +442,12 @@ __global__ void gibbs_prep_tc3_kernel(const float* __restrict__ cost, int K, flo
 template <int KP>
 static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, const PairSink& out,
                              const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
-                             const float* gc, int iters, cudaStream_t s) {
+                             const float* gc, int iters, cudaStream_t s, const int32_t* pi = nullptr,
+                             const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr) {
   const size_t smem = Smem<KP>::kBytes;
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
-  auto kern = dbg == 3 ? sinkhorn_tc3_kernel<KP, 3> : sinkhorn_tc3_kernel<KP, 0>;
+  auto kern = pi != nullptr ? sinkhorn_tc3_kernel<KP, 0, true>
+            : dbg == 3 ? sinkhorn_tc3_kernel<KP, 3, false> : sinkhorn_tc3_kernel<KP, 0, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -416,8 +458,22 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
   kern<<<(unsigned)grid, Slots<KP>::kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
-                                                                 ghi, glo, gc, iters);
+                                                                 ghi, glo, gc, iters, pi, pj, n_pairs, Hp);
   return cudaGetLastError();
+}
+
+// Padded marginal rows for the pair-list mode (row n_dist = uniform 1/K, the invalid-entry dummy).
+__global__ void pad_marginals_tc3_kernel(const float* __restrict__ H, int64_t n_dist, int K, int kp,
+                                         float* __restrict__ Hp) {
+  const int64_t total = (n_dist + 1) * kp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / kp;
+    const int c = (int)(idx % kp);
+    float v = 0.0f;
+    if (c < K) v = row < n_dist ? H[row * K + c] : 1.0f / (float)K;
+    Hp[idx] = v;
+  }
 }
 
 }  // namespace tc3
@@ -451,6 +507,28 @@ cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_
   }
 }
 
+}  // namespace asot
+
+namespace asot {
+size_t sinkhorn_tc3_pairs_scratch_bytes(int64_t n_dist, int K) { return (size_t)(n_dist + 1) * kpad32(K) * 4; }
+
+cudaError_t launch_sinkhorn_tc3_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
+                                      const PairSink& out, const float* H, int K, const uint32_t* ghi,
+                                      const uint32_t* glo, const float* gc, float* Hp, int iters, cudaStream_t s) {
+  if (n_pairs <= 0) return cudaSuccess;
+  const int kp = kpad32(K);
+  tc3::pad_marginals_tc3_kernel<<<512, 256, 0, s>>>(H, n_dist, K, kp, Hp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t n_tiles = (n_pairs + kTileSlots - 1) / kTileSlots;
+  switch (kp) {
+    case 32: return tc3::launch_kp<32>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
+    case 64: return tc3::launch_kp<64>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
+    case 96: return tc3::launch_kp<96>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
+    case 128: return tc3::launch_kp<128>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
+    default: return cudaErrorNotSupported;
+  }
+}
 }  // namespace asot
 
 extern "C" int asot_debug_tc3_trace(long long* host) {

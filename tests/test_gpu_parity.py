@@ -352,3 +352,54 @@ def test_full_size_sampled_parity_more(asot, cfg, prec, npairs):
     r = rel_err(Dg[pi, pj], c_o, 1.0)
     assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)], r.max()
     assert np.all(np.diag(Dg) == 0) and np.array_equal(Dg[pi, pj], Dg[pj, pi])
+
+
+@pytest.mark.parametrize("K", [16, 64, 128])
+def test_pair_modes_vs_cuda_core_kernel(K):
+    """fp32 pair lists: the 3xTF32 1-SM kernel's pair-list mode (K <= 128, and all K < 32) against
+    the independent fp32 CUDA-core kernel (ASOT_PAIR_KERNEL=simt, a separate process) and the
+    oracle, on the same list with reversed and invalid entries."""
+    import os
+    import subprocess
+    import sys
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import numpy as np, torch, sys
+sys.path.insert(0, {ROOT!r})
+from asot_inputs import make_inputs, random_pairs
+import paper_2310_16123_b200 as asot
+inp = make_inputs('c2', n_dist=40)
+A = np.ascontiguousarray(inp.anchors[:{K}])
+C = (((A[:, None, :].astype(np.float64) - A[None, :, :]) ** 2).sum(-1)); C = (C / C.max()).astype(np.float32)
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+_, H, _ = asot.map_to_anchors(t(inp.points), t(inp.offsets), t(inp.weights), t(A), offsets_host=inp.offsets)
+pi, pj = random_pairs(inp.n_dist, 300, seed=5)
+pi = np.concatenate([pi, pj[:20], [-1]]).astype(np.int32); pj = np.concatenate([pj, pi[:20], [3]]).astype(np.int32)
+d = asot.pairwise_sinkhorn(H, t(C), float(inp.eps), inp.iters, t(pi), t(pj), precision=asot.FP32, cost_max=1.0)
+np.save(sys.argv[1], d.cpu().numpy()); np.save(sys.argv[2], H.cpu().numpy()); np.save(sys.argv[3], np.stack([pi, pj]))
+"""
+    import tempfile
+    outs = {}
+    with tempfile.TemporaryDirectory() as td:
+        for mode in ("tc", "simt"):
+            env = dict(os.environ)
+            env.pop("ASOT_PAIR_KERNEL", None)
+            if mode == "simt":
+                env["ASOT_PAIR_KERNEL"] = "simt"
+            f = [os.path.join(td, f"{mode}_{k}.npy") for k in ("d", "h", "p")]
+            r = subprocess.run([sys.executable, "-c", code, *f], env=env, capture_output=True, text=True,
+                               timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs[mode] = [np.load(x) for x in f]
+    d_tc, H, (pi, pj) = outs["tc"]
+    d_simt = outs["simt"][0]
+    inp = make_inputs("c2", n_dist=40)
+    A = inp.anchors[:K].astype(np.float64)
+    C = ((A[:, None, :] - A[None, :, :]) ** 2).sum(-1)
+    C = (C / C.max()).astype(np.float32)
+    ok = (pi >= 0) & (pj >= 0)
+    assert np.all(d_tc[~ok] == 0.0) and np.all(d_simt[~ok] == 0.0)
+    c_o, _ = O.pair_costs(H.astype(np.float64), C.astype(np.float64), inp.eps, inp.iters,
+                          pi[ok].astype(np.int64), pj[ok].astype(np.int64))
+    assert rel_err(d_tc[ok], c_o, 1.0).max() <= TOL[0]      # ASOT_PREC_FP32
+    assert rel_err(d_simt[ok], c_o, 1.0).max() <= TOL[0]
