@@ -85,6 +85,28 @@ def test_mapping_adversarial_ties(asot):
     assert assign.cpu().numpy()[-2] == 3
 
 
+@pytest.mark.parametrize("d,K", [(7, 40), (13, 300), (100, 9), (100, 400)])
+def test_mapping_odd_dims_unaligned(asot, d, K):
+    """Dimensions that are not a multiple of 4 and point / anchor buffers that are not 16-byte
+    aligned take the mapping kernel's scalar load paths; K > one SMEM chunk re-stages anchors per
+    point group.  Assignments bit-exact, H bit-identical."""
+    rng = np.random.default_rng(d * 1000 + K)
+    sizes = rng.integers(1, 40, size=25)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    X = rng.normal(size=(off[-1], d)).astype(np.float32)
+    W = rng.normal(size=(K, d)).astype(np.float32)
+    wts = np.concatenate([np.full(n, 1.0 / n) for n in sizes]).astype(np.float32)
+    # one-float offsets make the device buffers 4- but not 16-byte aligned
+    Xb = torch.from_numpy(np.concatenate([[0.0], X.ravel()]).astype(np.float32)).cuda()[1:].view(-1, d)
+    Wb = torch.from_numpy(np.concatenate([[0.0], W.ravel()]).astype(np.float32)).cuda()[1:].view(-1, d)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    assign, H, st = asot.map_to_anchors(Xb, t(off), t(wts), Wb, offsets_host=off)
+    torch.cuda.synchronize()
+    a_o, H_o = O.map_and_histogram(X, off, wts, W)
+    np.testing.assert_array_equal(assign.cpu().numpy(), a_o)
+    np.testing.assert_array_equal(H.cpu().numpy(), H_o.astype(np.float32))
+
+
 # ------------------------------------------------------------------ distances (whole pipeline)
 @pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("cfg,n", [("c1", 64), ("c2", 90), ("c3", 36), ("c4", 50), ("c5", 18)])
