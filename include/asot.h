@@ -262,9 +262,12 @@ size_t asot_eot_workspace_bytes(int64_t n_dist, const int64_t* offsets_host, int
  * dist_out[p] = min <T, C_s> over T in U(a', b'), a' = hist[pair_i[p]], b' = hist[pair_j[p]]
  * renormalised to unit mass in fp64 (R#14), solved exactly (successive-shortest-path min-cost flow
  * on the two histogram supports, fp64) -- the eps -> 0 limit of asot_pairwise_sinkhorn.  Supports
- * of up to 128 bins per side; larger ones give NaN and ASOT_FLAG_EXACT_TOO_LARGE.  hist [n_dist,
- * n_anchors] f32, cost [n_anchors, n_anchors] f32, pair_i / pair_j [n_pairs] i32, dist_out
- * [n_pairs] f64: device pointers; workspace: n_pairs device bytes. */
+ * of up to 128 bins per side run one warp per pair, larger ones (n_anchors > 128) one CTA per
+ * pair with the flow matrix in the workspace.  Invalid indices or an empty support give NaN.
+ * hist [n_dist, n_anchors] f32, cost [n_anchors, n_anchors] f32, pair_i / pair_j [n_pairs] i32,
+ * dist_out [n_pairs] f64: device pointers; workspace: asot_exact_asot_workspace_bytes(n_pairs,
+ * n_anchors) device bytes (n_pairs flags, plus #SMs x n_anchors^2 f64 when n_anchors > 128). */
+size_t asot_exact_asot_workspace_bytes(int64_t n_pairs, int32_t n_anchors);
 asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_anchors, const float* cost,
                                   const int32_t* pair_i, const int32_t* pair_j, int64_t n_pairs,
                                   double* dist_out, uint32_t* status, void* workspace,

@@ -334,14 +334,15 @@ def exact_asot_pairs(H: torch.Tensor, cost: torch.Tensor, pair_i: torch.Tensor, 
                      status: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
                      stream=None) -> torch.Tensor:
     """NEXT-3: exact anchor-space OT W_AS for explicit pairs (fp64 min-cost flow on the histogram
-    supports).  Returns dist [n_pairs] f64 (NaN where a support exceeds 128 bins)."""
+    supports; a warp per pair up to 128-bin supports, a CTA per pair above).  Returns dist [n_pairs]
+    f64 (NaN for invalid indices or an empty support)."""
     _need_cuda(H, cost, pair_i, pair_j)
     _need_f32(H, cost)
     N, K = H.shape
     n = int(pair_i.numel())
     out = torch.empty(max(n, 1), dtype=torch.float64, device=H.device)
     st = new_status(H.device) if status is None else status
-    ws = _ws(workspace, H.device).get(max(n, 1))
+    ws = _ws(workspace, H.device).get(int(_lib_handle().asot_exact_asot_workspace_bytes(n, int(K))))
     _check(_lib_handle().asot_exact_asot_pairs(_ptr(H), N, int(K), _ptr(cost), _ptr(pair_i), _ptr(pair_j),
                                                n, _ptr(out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))
     return out[:n]

@@ -479,6 +479,10 @@ asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const in
   return ASOT_OK;
 }
 
+size_t asot_exact_asot_workspace_bytes(int64_t n_pairs, int32_t n_anchors) {
+  return asot::exact_pairs_workspace_bytes(n_pairs, n_anchors, device_sms());
+}
+
 asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_anchors, const float* cost,
                                   const int32_t* pair_i, const int32_t* pair_j, int64_t n_pairs,
                                   double* dist_out, uint32_t* status, void* workspace,
@@ -488,7 +492,8 @@ asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_a
   ASOT_CHECK_ARG(n_dist >= 1 && n_anchors >= 1 && n_pairs >= 0, "bad sizes");
   if (n_anchors > asot::kMaxAnchors) return fail(ASOT_ERR_UNSUPPORTED, "n_anchors > 1024");
   if (n_pairs == 0) return ASOT_OK;
-  if (!workspace || workspace_bytes < (size_t)n_pairs) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  if (!workspace || workspace_bytes < asot::exact_pairs_workspace_bytes(n_pairs, n_anchors, device_sms()))
+    return fail(ASOT_ERR_WORKSPACE, "workspace too small (asot_exact_asot_workspace_bytes)");
   ASOT_LAUNCH(asot::launch_exact_pairs(hist, n_dist, n_anchors, cost, pair_i, pair_j, n_pairs, dist_out,
                                        (uint8_t*)workspace, status, device_sms(), (cudaStream_t)stream));
   return ASOT_OK;

@@ -8,8 +8,8 @@
 // augmentation along the path to the nearest sink with remaining demand.  Everything in fp64.
 // One warp per pair: nodes are spread over the lanes for the arg-min and the arc relaxations;
 // the flow matrix of the supports lives in the warp's slice of shared memory.  Pairs whose
-// supports exceed 64 bins run in a second launch with 128-bin slices; above 128 the pair gets NaN
-// and ASOT_FLAG_EXACT_TOO_LARGE.
+// supports exceed 64 bins run in a second launch with 128-bin slices; above 128 a third launch
+// runs one CTA per pair (block-wide arg-min / relaxations, flow matrix in a global scratch).
 #include <cfloat>
 #include <cmath>
 
@@ -225,8 +225,7 @@ __global__ void exact_pairs_kernel(const float* __restrict__ H, int64_t n_dist, 
     const double d = solve_pair<MAXS>(H + (int64_t)i * K, H + (int64_t)j * K, K, cost, sm, ok);
     if (lane == 0) {
       out[q] = d;
-      if (MAXS <= 64) pending[q] = ok ? 0 : 1;
-      else if (!ok) atomicOr(status, ASOT_FLAG_EXACT_TOO_LARGE);
+      pending[q] = ok ? 0 : 1;   // still pending: the next (larger) launch takes it
     }
   }
 }
@@ -247,7 +246,220 @@ cudaError_t launch_maxs(const float* H, int64_t n_dist, int K, const float* cost
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Supports above 128 bins (e.g. c5, ~380 of 1024): one CTA per pair, the same successive-shortest-
+// path algorithm with block-wide arg-min and relaxations; node arrays in SMEM, the flow matrix
+// [sa][sb] f64 in a per-CTA global scratch (L2-resident).
+constexpr int kBlockThreads = 256;
+constexpr int kBlockMaxS = 1024;
+
+struct BlockSmem {
+  double dist[2 * kBlockMaxS], pot[2 * kBlockMaxS], rem[2 * kBlockMaxS];
+  int pred[2 * kBlockMaxS], done[2 * kBlockMaxS], sidx[2 * kBlockMaxS];
+  double red_v[kBlockThreads / 32];
+  int red_i[kBlockThreads / 32];
+  int sa, sb, target, cnt;
+  double bcast;
+};
+
+// Block-wide (value, index) arg-min (lowest index on ties); result in every thread.
+__device__ void block_argmin(BlockSmem& S, double& v, int& idx) {
+  warp_argmin(v, idx);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) {
+    S.red_v[warp] = v;
+    S.red_i[warp] = idx;
+  }
+  __syncthreads();
+  v = lane < kBlockThreads / 32 ? S.red_v[lane] : INFINITY;
+  idx = lane < kBlockThreads / 32 ? S.red_i[lane] : 0x7fffffff;
+  warp_argmin(v, idx);   // every warp reduces the same partials
+}
+
+__device__ double block_sum(BlockSmem& S, double v) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) S.red_v[warp] = v;
+  __syncthreads();
+  v = lane < kBlockThreads / 32 ? S.red_v[lane] : 0.0;
+  return warp_sum(v);
+}
+
+__global__ void __launch_bounds__(kBlockThreads)
+exact_pairs_block_kernel(const float* __restrict__ H, int64_t n_dist, int K, const float* __restrict__ cost,
+                         const int32_t* __restrict__ pi, const int32_t* __restrict__ pj, int64_t n_pairs,
+                         double* __restrict__ out, const uint8_t* __restrict__ pending, double* __restrict__ flow_all,
+                         uint32_t* status) {
+  extern __shared__ __align__(16) uint8_t exact_block_smem[];
+  BlockSmem& S = *reinterpret_cast<BlockSmem*>(exact_block_smem);
+  const int tid = threadIdx.x;
+  double* F = flow_all + (size_t)blockIdx.x * K * K;   // [sa][sb] row-major, row stride sb
+  for (int64_t q = blockIdx.x; q < n_pairs; q += gridDim.x) {
+    if (!pending[q]) continue;
+    const int i0 = pi[q], j0 = pj[q];
+    if (i0 < 0 || j0 < 0 || i0 >= n_dist || j0 >= n_dist) {
+      if (tid == 0) out[q] = NAN;
+      continue;
+    }
+    // ---- supports (order-preserving compaction by warp 0) and fp64 masses
+    if (tid < 32) {
+      const int lane = tid;
+      for (int side = 0; side < 2; ++side) {
+        const float* h = H + (int64_t)(side == 0 ? i0 : j0) * K;
+        int cnt = 0;
+        for (int k0 = 0; k0 < K; k0 += 32) {
+          const int k = k0 + lane;
+          const float w = k < K ? h[k] : 0.0f;
+          const bool nz = w > 0.0f;
+          const unsigned m = __ballot_sync(0xffffffffu, nz);
+          const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+          if (nz && pos < kBlockMaxS) {
+            S.sidx[side * kBlockMaxS + pos] = k;
+            S.rem[side * kBlockMaxS + pos] = (double)w;
+          }
+          cnt += __popc(m);
+        }
+        if (lane == 0) (side == 0 ? S.sa : S.sb) = cnt;
+      }
+    }
+    __syncthreads();
+    const int sa = S.sa, sb = S.sb;
+    const int M = kBlockMaxS;
+    if (sa == 0 || sb == 0) {
+      if (tid == 0) out[q] = NAN;
+      __syncthreads();
+      continue;
+    }
+    double ma = 0.0, mb = 0.0;
+    for (int x = tid; x < sa; x += kBlockThreads) ma += S.rem[x];
+    ma = block_sum(S, ma);
+    for (int x = tid; x < sb; x += kBlockThreads) mb += S.rem[M + x];
+    mb = block_sum(S, mb);
+    for (int x = tid; x < sa; x += kBlockThreads) S.rem[x] /= ma;      // renormalise (R#14)
+    for (int x = tid; x < sb; x += kBlockThreads) S.rem[M + x] /= mb;
+    auto C = [&](int i, int j) { return (double)cost[(int64_t)S.sidx[i] * K + S.sidx[M + j]]; };
+    for (int64_t e = tid; e < (int64_t)sa * sb; e += kBlockThreads) F[e] = 0.0;
+    for (int i = tid; i < sa; i += kBlockThreads) S.pot[i] = 0.0;
+    for (int j = tid; j < sb; j += kBlockThreads) {
+      double m = INFINITY;
+      for (int i = 0; i < sa; ++i) m = fmin(m, C(i, j));
+      S.pot[M + j] = m;
+    }
+    __syncthreads();
+    const int V = 2 * M;
+    for (int iter = 0; iter < 4 * (sa + sb) + 16; ++iter) {
+      double left = 0.0;
+      for (int i = tid; i < sa; i += kBlockThreads) left += S.rem[i];
+      left = block_sum(S, left);
+      if (left <= 1e-13) break;
+      // ---- Dijkstra from every source with remaining supply (node ids: i, M + j)
+      for (int v = tid; v < V; v += kBlockThreads) {
+        const bool exists = v < M ? v < sa : (v - M) < sb;
+        const bool src = v < M && v < sa && S.rem[v] > kMassEps;
+        S.dist[v] = src ? 0.0 : INFINITY;
+        S.pred[v] = -1;
+        S.done[v] = exists ? 0 : 1;
+      }
+      if (tid == 0) S.target = -1;
+      __syncthreads();
+      for (int step = 0; step < sa + sb; ++step) {
+        double best = INFINITY;
+        int bi = 0x7fffffff;
+        for (int v = tid; v < V; v += kBlockThreads)
+          if (!S.done[v] && S.dist[v] < best) {
+            best = S.dist[v];
+            bi = v;
+          }
+        block_argmin(S, best, bi);
+        if (best == INFINITY) break;
+        __syncthreads();
+        if (tid == 0) S.done[bi] = 1;
+        if (bi >= M && S.rem[bi] > kMassEps) {   // nearest sink with remaining demand
+          if (tid == 0) S.target = bi;
+          __syncthreads();
+          break;
+        }
+        if (bi >= M) {
+          const int j = bi - M;   // backward arcs j -> i (flow on (i, j))
+          for (int i = tid; i < sa; i += kBlockThreads) {
+            if (!S.done[i] && F[(int64_t)i * sb + j] > kMassEps) {
+              const double nd = best + fmax(0.0, -(C(i, j) + S.pot[i] - S.pot[bi]));
+              if (nd < S.dist[i]) {
+                S.dist[i] = nd;
+                S.pred[i] = bi;
+              }
+            }
+          }
+        } else {
+          const int i = bi;
+          for (int j = tid; j < sb; j += kBlockThreads) {
+            const int v = M + j;
+            if (!S.done[v]) {
+              const double nd = best + fmax(0.0, C(i, j) + S.pot[i] - S.pot[v]);
+              if (nd < S.dist[v]) {
+                S.dist[v] = nd;
+                S.pred[v] = i;
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      const int target = S.target;
+      if (target < 0) break;  // cannot happen for balanced masses
+      const double Dt = S.dist[target];
+      for (int v = tid; v < V; v += kBlockThreads) {
+        const bool exists = v < M ? v < sa : (v - M) < sb;
+        if (exists) S.pot[v] += fmin(S.dist[v], Dt);
+      }
+      __syncthreads();
+      if (tid == 0) {   // augment along the path
+        double delta = S.rem[target];
+        int v = target, src = -1;
+        while (v >= 0) {
+          const int u = S.pred[v];
+          if (u < 0) {
+            src = v;
+            break;
+          }
+          if (v < M) delta = fmin(delta, F[(int64_t)v * sb + (u - M)]);  // backward arc u=sink -> v=source
+          v = u;
+        }
+        delta = fmin(delta, S.rem[src]);
+        v = target;
+        while (true) {
+          const int u = S.pred[v];
+          if (u < 0) break;
+          if (v >= M) F[(int64_t)u * sb + (v - M)] += delta;   // forward arc source u -> sink v
+          else F[(int64_t)v * sb + (u - M)] -= delta;          // backward: cancel flow on (v, u)
+          v = u;
+        }
+        S.rem[src] -= delta;
+        S.rem[target] -= delta;
+      }
+      __syncthreads();
+    }
+    double tot = 0.0;
+    for (int64_t e = tid; e < (int64_t)sa * sb; e += kBlockThreads) {
+      const double fe = F[e];
+      if (fe != 0.0) tot += fe * C((int)(e / sb), (int)(e % sb));
+    }
+    tot = block_sum(S, tot);
+    if (tid == 0) out[q] = tot;
+    __syncthreads();
+  }
+  (void)status;
+}
+
 }  // namespace exact
+
+size_t exact_pairs_workspace_bytes(int64_t n_pairs, int K, int sms) {
+  size_t b = ((size_t)(n_pairs > 0 ? n_pairs : 1) + 255) & ~(size_t)255;   // pending flags
+  if (K > 128) b += (size_t)sms * K * K * 8;                                 // per-CTA flow matrices
+  return b;
+}
 
 cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const float* cost, const int32_t* pi,
                                const int32_t* pj, int64_t n_pairs, double* out, uint8_t* pending,
@@ -255,7 +467,16 @@ cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const floa
   if (n_pairs <= 0) return cudaSuccess;
   cudaError_t e = exact::launch_maxs<64>(H, n_dist, K, cost, pi, pj, n_pairs, out, pending, status, sms, s);
   if (e != cudaSuccess) return e;
-  return exact::launch_maxs<128>(H, n_dist, K, cost, pi, pj, n_pairs, out, pending, status, sms, s);
+  e = exact::launch_maxs<128>(H, n_dist, K, cost, pi, pj, n_pairs, out, pending, status, sms, s);
+  if (e != cudaSuccess || K <= 128) return e;
+  // supports above 128 bins: one CTA per pair (flow matrices after the pending flags)
+  double* flow = (double*)(pending + (((size_t)n_pairs + 255) & ~(size_t)255));
+  const size_t smem = sizeof(exact::BlockSmem);
+  e = cudaFuncSetAttribute(exact::exact_pairs_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  exact::exact_pairs_block_kernel<<<(unsigned)sms, exact::kBlockThreads, smem, s>>>(
+      H, n_dist, K, cost, pi, pj, n_pairs, out, pending, flow, status);
+  return cudaGetLastError();
 }
 
 }  // namespace asot

@@ -152,6 +152,7 @@ cudaError_t launch_histograms(const int32_t* assign, const float* weights, const
                               int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s,
                               float* const* peers = nullptr, int n_peers = 0, int64_t row_base = 0);
 int simt_kpad(int K);
+size_t exact_pairs_workspace_bytes(int64_t n_pairs, int K, int sms);
 cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const float* cost, const int32_t* pi,
                                const int32_t* pj, int64_t n_pairs, double* out, uint8_t* pending,
                                uint32_t* status, int sms, cudaStream_t s);

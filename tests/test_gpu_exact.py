@@ -44,15 +44,23 @@ def test_exact_asot_vs_lp(asot, cfg, n, npairs):
     assert np.all(d[-2:] == 0.0) or np.allclose(d[-2:], 0.0, atol=1e-12)   # self pairs
 
 
-def test_exact_asot_supports_too_large(asot):
-    inp = make_inputs("c5", n_dist=3)
+def test_exact_asot_large_supports(asot):
+    """c5 (K = 1024, supports of ~380 bins): the CTA-per-pair solver, against the oracle LP, plus
+    a mixed list (a K = 1024 histogram pair next to an invalid index)."""
+    inp = make_inputs("c5", n_dist=4)
     _, H = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
     H32 = H.astype(np.float32)
+    assert (H32 > 0).sum(1).max() > 128
+    pi = np.array([0, 1, 2, 3, -1], np.int32)
+    pj = np.array([1, 2, 3, 0, 2], np.int32)
     st = asot.asot.new_status()
-    d = asot.exact_asot_pairs(dev(H32), dev(inp.cost), dev(np.array([0, 1], np.int32)),
-                              dev(np.array([1, 2], np.int32)), status=st).cpu().numpy()
+    d = asot.exact_asot_pairs(dev(H32), dev(inp.cost), dev(pi), dev(pj), status=st).cpu().numpy()
     torch.cuda.synchronize()
-    supp = (H32 > 0).sum(1)
-    if supp.max() > 128:
-        assert int(st.item()) & asot.asot.FLAG_EXACT_TOO_LARGE
-        assert np.isnan(d).any()
+    assert int(st.item()) == 0
+    assert np.isnan(d[-1])
+    C = inp.cost.astype(np.float64)
+    for q in range(4):
+        a, b = H32[pi[q]].astype(np.float64), H32[pj[q]].astype(np.float64)
+        sa, sb = a > 0, b > 0
+        ref = O.solve_exact(a[sa], b[sb], C[np.ix_(sa, sb)])
+        assert abs(d[q] - ref) <= 1e-9 + 1e-9 * abs(ref), (q, d[q], ref)
