@@ -74,7 +74,7 @@ typedef enum {
 #define ASOT_FLAG_DENOM_CLAMPED    8u  /* a Sinkhorn denominator < FLT_MIN was clamped     */
 #define ASOT_FLAG_NONFINITE_OUTPUT 16u /* a distance came out NaN/Inf                            */
 #define ASOT_FLAG_SOFT_FALLBACK    32u /* a soft code was all zero -> uniform row (warning) */
-#define ASOT_FLAG_EXACT_TOO_LARGE  64u /* exact ASOT: a histogram support > 128 bins (result NaN) */
+#define ASOT_FLAG_EXACT_TOO_LARGE  64u /* reserved (exact ASOT now solves every support; never raised) */
 
 /* Distance-matrix tiling (step a4).  Distributions are grouped in blocks of 16; block pairs
  * (bi <= bj) are enumerated row-major over the upper triangle of the block grid; each block
