@@ -190,7 +190,8 @@ sinkhorn_simt_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
     const int g = tid / kTP, q = tid % kTP;
     float d = 0.0f;
     for (int w = 0; w < WPG; ++w) d += red[g * WPG + w][q];
-    write_result(out, slot0 + tid, s_i[tid] >= 0, s_i[tid], s_j[tid], d);
+    if (slot0 + tid < ps.n_slots)   // the last CTA's slots past the list / range are not outputs
+      write_result(out, slot0 + tid, s_i[tid] >= 0, s_i[tid], s_j[tid], d);
   }
 }
 

@@ -439,13 +439,15 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
       if (NG == 1) {
         tc_fence_before();
         named_bar_sync(1 + s, kWG);   // R1 reads done before the next tile's phase-0 MMA
-        write_result(out, tr * kTileSlots + p, valid, ii, jj, acc);
+        if (!EX || tr * kTileSlots + p < n_pairs)   // (pair lists: no slot past the list)
+          write_result(out, tr * kTileSlots + p, valid, ii, jj, acc);
         continue;
       }
       if (h == 1) rs[p] = acc;
       tc_fence_before();
       named_bar_sync(1 + s, kWG);   // (also: R1 reads done before the next tile's phase-0 MMA)
-      if (h == 0) write_result(out, tr * kTileSlots + p, valid, ii, jj, acc + rs[p]);
+      if (h == 0 && (!EX || tr * kTileSlots + p < n_pairs))
+        write_result(out, tr * kTileSlots + p, valid, ii, jj, acc + rs[p]);
     }
   }
   tc_fence_before();

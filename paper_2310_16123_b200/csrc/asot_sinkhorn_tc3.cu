@@ -403,7 +403,8 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
         if (NCG == 4) dsum = (red[p] + red[128 + p]) + (red[256 + p] + red[384 + p]);
         else if (NCG == 2) dsum = red[p] + red[128 + p];
         else dsum = red[p];
-        write_result(out, tr * kTileSlots + p, valid, ii, jj, dsum);
+        if (!EX || tr * kTileSlots + p < n_pairs)   // (pair lists: no slot past the list)
+          write_result(out, tr * kTileSlots + p, valid, ii, jj, dsum);
       }
       tc_fence_before();
     }

@@ -425,3 +425,34 @@ np.save(sys.argv[1], d.cpu().numpy()); np.save(sys.argv[2], H.cpu().numpy()); np
                           pi[ok].astype(np.int64), pj[ok].astype(np.int64))
     assert rel_err(d_tc[ok], c_o, 1.0).max() <= TOL[0]      # ASOT_PREC_FP32
     assert rel_err(d_simt[ok], c_o, 1.0).max() <= TOL[0]
+
+
+@pytest.mark.parametrize("K,prec", [(128, 1), (64, 0), (16, 1), (256, 1), (256, 0)])
+def test_pair_list_writes_stay_in_bounds(asot, K, prec):
+    """Pair lists whose length is not a multiple of the 128-entry tile: the kernels must write
+    exactly n_pairs results (a guard region after dist_out stays untouched) -- resident pair-list
+    modes (K <= 128, TF32 and 3xTF32) and the streamed one (K = 256)."""
+    from paper_2310_16123_b200 import _lib
+    inp = make_inputs("c5", n_dist=30)
+    A = np.ascontiguousarray(inp.anchors[:K])
+    C = (((A[:, None, :].astype(np.float64) - A[None, :, :]) ** 2).sum(-1))
+    C = (C / C.max()).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    _, H, _ = asot.map_to_anchors(t(inp.points), t(inp.offsets), t(inp.weights), t(A), offsets_host=inp.offsets)
+    pi, pj = random_pairs(inp.n_dist, 200, seed=3)
+    n = 131   # one full tile + 3
+    pi, pj = t(pi[:n].astype(np.int32)), t(pj[:n].astype(np.int32))
+    guard = 1024
+    out = torch.full((n + guard,), -7.0, dtype=torch.float32, device="cuda")
+    st = asot.asot.new_status()
+    L = _lib.load()
+    nbytes = int(L.asot_pairwise_workspace_bytes(inp.n_dist, K, prec))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+    rc = L.asot_pairwise_sinkhorn(H.data_ptr(), inp.n_dist, K, t(C).data_ptr(), 1.0, float(inp.eps), 20, prec,
+                                  pi.data_ptr(), pj.data_ptr(), n, out.data_ptr(), st.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), None)
+    torch.cuda.synchronize()
+    assert rc == 0
+    o = out.cpu().numpy()
+    assert np.all(o[n:] == -7.0), "write past dist_out[n_pairs]"
+    assert np.all(np.isfinite(o[:n])) and np.all(o[:n] >= 0.0)
