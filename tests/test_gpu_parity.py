@@ -456,3 +456,42 @@ def test_pair_list_writes_stay_in_bounds(asot, K, prec):
     o = out.cpu().numpy()
     assert np.all(o[n:] == -7.0), "write past dist_out[n_pairs]"
     assert np.all(np.isfinite(o[:n])) and np.all(o[:n] >= 0.0)
+
+
+@pytest.mark.parametrize("cfg,prec,nrand,pool", [("c3", 1, 10000, None), ("c4", 1, 10000, None),
+                                                ("c5", 1, 2000, 100)])
+def test_survey_parity_subsets(asot, cfg, prec, nrand, pool):
+    """SURVEY 8(d)'s parity subset at full size in bench.py's launch configuration: a seeded set of
+    random pairs (>= 10,000 for c3 / c4; for c5, whose oracle mapping runs ~2 distributions/s, 2,000
+    among the first 100 distributions), every pair inside the first 64 distributions, and the pairs
+    of the tiles on both sides of every rank boundary of the 2-, 4- and 8-GPU partitions -- each
+    against the oracle evaluated pair by pair."""
+    from paper_2310_16123_b200.distributed import partition_even
+    inp = make_inputs(cfg)
+    n = inp.n_dist
+    pts, offs, w, anc, cst = dev_inputs(inp)
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(pts, offs, w, anc, cst, float(inp.eps), inp.iters, precision=prec,
+                             offsets_host=inp.offsets, cost_max=1.0, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    pi, pj = random_pairs(n if pool is None else pool, nrand, seed=29)
+    fi, fj = np.triu_indices(64, k=1)
+    bi, bj = [], []
+    nt = asot.num_tiles(n)
+    for world in (2, 4, 8):
+        for (a, b) in partition_even(nt, world)[1:]:
+            i, j, v = asot.tile_pairs(n, max(a - 1, 0), min(a + 1, nt))   # tiles a-1 and a
+            bi.append(i[v]); bj.append(j[v])
+    pi = np.concatenate([pi, fi, *bi]).astype(np.int64)
+    pj = np.concatenate([pj, fj, *bj]).astype(np.int64)
+    touched = np.unique(np.concatenate([pi, pj]))
+    H_o = np.zeros((n, inp.n_anchors))
+    for d in touched:
+        s, e = int(inp.offsets[d]), int(inp.offsets[d + 1])
+        _, h = O.map_and_histogram(inp.points[s:e], np.array([0, e - s]), inp.weights[s:e], inp.anchors)
+        H_o[d] = h[0]
+    c_o, _ = O.pair_costs(H_o, inp.cost, inp.eps, inp.iters, pi, pj)
+    Dg = D.cpu().numpy()
+    r = rel_err(Dg[pi, pj], c_o, 1.0)
+    assert r.max() <= TOL[asot.effective_precision(inp.n_anchors, prec)], r.max()
