@@ -129,6 +129,9 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   const uint32_t epi_remote0 = mapa(bar_epi0, 0);  // leader's epi_done[0] (cluster address)
   const bool leader = rank == 0;
   const bool issuer = leader && warp == kWarps;    // the MMA warp (Sinkhorn parts and cost)
+  // 64-anchor chunks holding real anchors: K <= 192 skips the all-padding fourth chunk in every
+  // Sinkhorn phase (9 of the 16 parts); the padded scalings stay exactly 0 there
+  const int NCH = (K + kChunk - 1) / kChunk;
 
   uint32_t mma_par = 0, epi_par = 0, cost_par = 0;   // one parity bit per barrier family (all
                                                      // chunks of a family complete once per phase)
@@ -186,6 +189,12 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
 #pragma unroll
         for (int e = 0; e < 16; ++e) ones[e] = (c * kChunk + cq * 16 + e < K) ? 0x3f800000u : 0u;
         tmem_st16(lane_off + c * kChunk + cq * 16, ones);
+        if (c >= NCH) {   // skipped chunk: R1's copy is read by the cost, so it must be 0 too
+          uint32_t zeros[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) zeros[e] = 0u;
+          tmem_st16(lane_off + 256 + c * kChunk + cq * 16, zeros);
+        }
       }
       tmem_wait_st();
       tc_fence_before();
@@ -209,7 +218,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         const uint32_t rd = lane_off + (uint32_t)(((f + 1) & 1) * 256) + cq * 16;
         const bool last = f + 1 == 2 * iters;
 #pragma unroll 1
-        for (int c = 0; c < kNChunks; ++c) {
+        for (int c = 0; c < NCH; ++c) {
           mbar_wait(bar_mma0 + 8 * c, mma_par);
           tc_fence_after();
           if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && threadIdx.x == 0 && f < 64)
@@ -229,7 +238,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
               o[e + 1] = tf32_rna_pre(x.y);
             }
             tmem_st16(rd + c * kChunk, o);  // in place: the new scaling replaces D
-            if (c + 1 < kNChunks) load_m(f, c + 1);
+            if (c + 1 < NCH) load_m(f, c + 1);
             else if (!last) load_m(f + 1, 0);
           }
           if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && threadIdx.x == 0 && f < 64)
@@ -242,7 +251,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     } else if (issuer) {
       for (int f = 0; f < 2 * iters; ++f) {
 #pragma unroll 1
-        for (int kc = 0; kc < kNChunks; ++kc) {
+        for (int kc = 0; kc < NCH; ++kc) {
           mbar_wait(bar_epi0 + 8 * kc, epi_par);
           tc_fence_after();
           if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && lane == 0 && f < 64)
@@ -255,8 +264,10 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             const uint32_t acc0 = kc > 0 ? 1u : 0u;
 #pragma unroll
             for (int nc = 0; nc < kNChunks; ++nc) {
-              if (DBG != 2) issue_part(a_col, d_col + nc * kChunk, desc + (uint64_t)((nc * 4096) >> 4), acc0);
-              if (kc == kNChunks - 1) mma2_commit_mc(bar_mma0 + 8 * nc);
+              if (nc < NCH) {
+                if (DBG != 2) issue_part(a_col, d_col + nc * kChunk, desc + (uint64_t)((nc * 4096) >> 4), acc0);
+                if (kc == NCH - 1) mma2_commit_mc(bar_mma0 + 8 * nc);
+              }
             }
           }
           __syncwarp();

@@ -43,7 +43,7 @@ def run_both(asot, inp, prec):
     return D.cpu().numpy(), Do, int(st.item())
 
 
-@pytest.mark.parametrize("K", [1, 7, 31, 32, 33, 70, 100, 129, 200, 257, 300, 700])
+@pytest.mark.parametrize("K", [1, 7, 31, 32, 33, 70, 100, 129, 192, 200, 257, 300, 700])
 @pytest.mark.parametrize("prec", [0, 1])
 def test_padded_anchor_counts(asot, K, prec):
     """K off the 32 / 256 / 1024 tile grids exercises the padding of every kernel
