@@ -140,6 +140,9 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int phases = 2 * iters + 1;
+  // 32-anchor input chunks holding real anchors: padded chunks (x = 0 there) are neither loaded
+  // nor multiplied (K = 384: 12 of 16, K = 768: 24 of 32)
+  const int kcn = (K + 31) / 32 < kKC ? (K + 31) / 32 : kKC;
 
   if (warp == kEpiWarps) {
     // ------------------------------------------------------------------ producer (TMA)
@@ -154,7 +157,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
           xr_par ^= 1u;
           fence_proxy_async_global();
           for (int nh = 0; nh < NH; ++nh) {
-            for (int kc = 0; kc < kKC; ++kc, ++it) {
+            for (int kc = 0; kc < kcn; ++kc, ++it) {
               const int s = (int)(it % kStages);
               if (it >= kStages) mbar_wait(bar_empty + 8 * s, (uint32_t)((it / kStages - 1) & 1));
               if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && kc == 0 && 2 * f + nh < 256)
@@ -181,7 +184,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             free_par ^= 1u;
           }
           first = false;
-          for (int kc = 0; kc < kKC; ++kc, ++it) {
+          for (int kc = 0; kc < kcn; ++kc, ++it) {
             const int s = (int)(it % kStages);
             const uint32_t par = (uint32_t)((it / kStages) & 1);
             mbar_wait(bar_full + 8 * s, par);
@@ -191,7 +194,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             }
             mbar_wait(bar_peer + 8 * s, par);
             tc_fence_after();
-            if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && lane == 0 && (kc == 0 || kc == kKC - 1) &&
+            if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && lane == 0 && (kc == 0 || kc == kcn - 1) &&
                 2 * f + nh < 256)
               g_tc4_trace[kc == 0 ? 0 : 1][2 * f + nh] = clock64();
             if (elect_one()) {
@@ -207,7 +210,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                 }
               }
               mma2_commit_mc(bar_empty + 8 * s);
-              if (kc == kKC - 1) mma2_commit_mc(bar_done);
+              if (kc == kcn - 1) mma2_commit_mc(bar_done);
             }
             __syncwarp();
           }

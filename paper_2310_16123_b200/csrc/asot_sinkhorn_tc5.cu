@@ -132,6 +132,8 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int phases = 2 * iters + 1;
+  // 32-anchor input chunks holding real anchors: padded chunks (x = 0 there) are skipped
+  const int kcn = (K + 31) / 32 < C::KC ? (K + 31) / 32 : C::KC;
 
   if (warp == kEpiWarps) {
     // ------------------------------------------------------------------ producer (TMA)
@@ -149,7 +151,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
           xr_par ^= 1u;
           fence_proxy_async_global();
           for (int pass = 0; pass < C::NP; ++pass) {
-            for (int kc = 0; kc < C::KC; ++kc, ++it) {
+            for (int kc = 0; kc < kcn; ++kc, ++it) {
               const int s = (int)(it % kStages);
               if (it >= kStages) mbar_wait(bar_empty + 8 * s, (uint32_t)((it / kStages - 1) & 1));
               const uint32_t st = stage0 + s * kStageBytes;
@@ -182,7 +184,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             free_par ^= 1u;
           }
           first = false;
-          for (int kc = 0; kc < C::KC; ++kc, ++it) {
+          for (int kc = 0; kc < kcn; ++kc, ++it) {
             const int s = (int)(it % kStages);
             const uint32_t par = (uint32_t)((it / kStages) & 1);
             mbar_wait(bar_full + 8 * s, par);
@@ -207,7 +209,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                 }
               }
               mma2_commit_mc(bar_empty + 8 * s);
-              if (kc == C::KC - 1) mma2_commit_mc(bar_done);
+              if (kc == kcn - 1) mma2_commit_mc(bar_done);
             }
             __syncwarp();
           }
