@@ -17,7 +17,7 @@
 // chunk nc is complete (commit) after part (3, nc).  So the next phase's first parts wait for the
 // epilogue of ONE chunk (all 16 epilogue warps, 16 anchors per thread) that starts three parts
 // (~780 cycles) before the tensor pipe runs dry: the epilogue latency is hidden, not just
-// overlapped with half a phase.
+// overlapped with half a phase.  For K <= 192 the all-padding fourth chunk is skipped (9 parts).
 //
 // Cost (a6): v_L is written in place into D; u_L stays in A.  K (.) C_s is streamed through a
 // 32 KB SMEM staging buffer in four (N-half, K-half) sub-parts (once per tile: < 1% of a tile),

@@ -15,7 +15,9 @@
 //   - each phase is two passes over N (512 anchors each, D = 512 TMEM columns); after a pass the
 //     16 epilogue warps compute x = m / D (one MUFU per two anchors), RNA-round to TF32 and
 //     write the next X to global; the last phase multiplies by K (.) C_s and reduces
-//     sum_r u_r ((K (.) C_s) v)_r against u_L read back from global.
+//     sum_r u_r ((K (.) C_s) v)_r against u_L read back from global;
+//   - K-chunks made only of padding anchors (K not a multiple of 32 * KC) are neither loaded
+//     nor multiplied (x = 0 there).
 #include <cfloat>
 #include <cstdlib>
 
