@@ -117,6 +117,53 @@ def test_sinkhorn_general_2x2_converged_closed_form():
         assert abs(c[0] - off * (p - x + q - x)) < 1e-12
 
 
+def test_sinkhorn_separable_cost_any_L():
+    """Finite-L pin (not a convergence statement).  C_s(i, j) = f_i + f_j makes the Gibbs kernel
+    rank one, G = g g^T with g = exp(-f / eps), so the first u-update already gives
+    T = diag(u) G diag(v) = a b^T after the first v-update: for every L >= 1 the plan is the
+    product coupling and d = sum_i a_i f_i + sum_j b_j f_j exactly (up to rounding)."""
+    rng = np.random.default_rng(21)
+    K, P = 7, 5
+    f = rng.uniform(0.0, 1.0, K)
+    Cs = f[:, None] + f[None, :]
+    A = rng.dirichlet(np.ones(K), P).T
+    B = rng.dirichlet(np.ones(K), P).T
+    A[2, 0] = 0.0
+    A[:, 0] /= A[:, 0].sum()
+    for eps in (0.1, 0.5):
+        G, GC = O.gibbs(Cs, eps)
+        for L in (1, 2, 9):
+            c, U, V, flags = O.sinkhorn_batch(A, B, G, GC, L)
+            assert not flags.any()
+            for p in range(P):
+                T = U[:, p][:, None] * G * V[:, p][None, :]
+                np.testing.assert_allclose(T, np.outer(A[:, p], B[:, p]), atol=1e-14)
+                assert abs(c[p] - (A[:, p] @ f + B[:, p] @ f)) <= 1e-13
+
+
+def test_sinkhorn_2x2_one_iteration_closed_form():
+    """Finite-L pin away from convergence.  C = [[0, c], [c, 0]], G = [[1, k], [k, 1]] with
+    k = exp(-c / eps); a = (p, 1-p), b = (q, 1-q), v0 = 1.  One iteration by hand:
+    u = a / (1 + k), v_1 = q (1 + k) / (p + k (1-p)), v_2 = (1-q)(1 + k) / (k p + 1 - p), and the
+    cost <T, C> = c k (u_1 v_2 + u_2 v_1) =
+        c k [ p (1-q) / (k p + 1 - p) + (1-p) q / (p + k (1-p)) ]."""
+    rng = np.random.default_rng(22)
+    for _ in range(20):
+        p, q = rng.uniform(0.05, 0.95, 2)
+        cst = rng.uniform(0.1, 2.0)
+        eps = rng.uniform(0.2, 2.0)
+        k = math.exp(-cst / eps)
+        G, GC = O.gibbs(np.array([[0.0, cst], [cst, 0.0]]), eps)
+        c, U, V, _ = O.sinkhorn_batch(np.array([[p], [1 - p]]), np.array([[q], [1 - q]]), G, GC, 1)
+        exact = cst * k * (p * (1 - q) / (k * p + 1 - p) + (1 - p) * q / (p + k * (1 - p)))
+        assert abs(c[0] - exact) <= 1e-14 * max(exact, 1.0)
+        np.testing.assert_allclose(U[:, 0], [p / (1 + k), (1 - p) / (1 + k)], rtol=1e-14)
+        # the row marginals are NOT met after one iteration unless p = q (a non-converged value)
+        T = U[:, 0][:, None] * G * V[:, 0][None, :]
+        if abs(p - q) > 0.05:
+            assert abs(T.sum(1)[0] - p) > 1e-6
+
+
 def test_sinkhorn_one_hot_marginals_exact():
     """a = e_u, b = e_v  =>  the plan is the single entry (u, v) => d = C_s(u, v) for any eps, L."""
     rng = np.random.default_rng(3)
