@@ -139,3 +139,61 @@ def test_rejects_cpu_tensors_and_bad_args(asot):
     with pytest.raises(ValueError):   # eps such that max(C)/eps > 80 (R#12)
         asot.distance_matrix(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors),
                              dev(inp.cost), 0.001, 2, offsets_host=inp.offsets)
+
+
+@pytest.mark.parametrize("K", [16, 100, 200, 700])
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("L", [1, 5])
+def test_separable_cost_closed_form(asot, K, prec, L):
+    """Oracle-free finite-L check through the C ABI: C_s(i, j) = f_i + f_j has a rank-one Gibbs
+    kernel, so after one iteration the plan is a b^T and d = a.f + b.f for every L (the pin of
+    test_oracle_pins.test_sinkhorn_separable_cost_any_L), on every kernel family (K = 16: 3xTF32
+    1-SM, 100: 1-SM, 200 / 700: streamed pair-list kernels)."""
+    rng = np.random.default_rng(K + 10 * L + 100 * prec)
+    N, n = 40, 300
+    f = rng.uniform(0.0, 0.5, K).astype(np.float32)
+    C = (f[:, None] + f[None, :]).astype(np.float32)
+    H = rng.dirichlet(np.ones(K), N).astype(np.float32)
+    H[rng.uniform(size=H.shape) < 0.2] = 0.0
+    H[:, 0] += 1e-3
+    H /= H.sum(1, keepdims=True)
+    H = H.astype(np.float32)
+    pi = rng.integers(0, N, n).astype(np.int32)
+    pj = rng.integers(0, N, n).astype(np.int32)
+    st = asot.asot.new_status()
+    d = asot.pairwise_sinkhorn(dev(H), dev(C), 0.25, L, dev(pi), dev(pj), precision=prec, status=st,
+                               cost_max=float(C.max()))
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    Hd = H.astype(np.float64)
+    fd = f.astype(np.float64)
+    exact = Hd[pi] @ fd + Hd[pj] @ fd
+    r = np.abs(d.cpu().numpy().astype(np.float64) - exact) / exact
+    eff = asot.effective_precision(K, prec)
+    assert r.max() <= TOL[eff], f"K={K} prec={eff} L={L} max rel {r.max():.3e}"
+
+
+@pytest.mark.parametrize("K", [16, 100, 200, 700])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_separable_cost_closed_form_tiles(asot, K, prec):
+    """The same oracle-free closed form through the tile-mode kernels (distance_matrix: 1-SM, CTA
+    pair, streamed), L = 3: D[i, j] = H_i.f + H_j.f off the diagonal, with H from the oracle's
+    (bit-exact) mapping."""
+    base = make_inputs("c5", n_dist=19, iters=3)
+    inp = with_anchors(base, K, dim=37)
+    rng = np.random.default_rng(K)
+    f = rng.uniform(0.0, 0.5, K).astype(np.float32)
+    C = (f[:, None] + f[None, :]).astype(np.float32)
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors),
+                             dev(C), 0.25, 3, precision=prec, offsets_host=inp.offsets, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    _, H = O.map_and_histogram(inp.points, inp.offsets, inp.weights, inp.anchors)
+    m = H.astype(np.float64) @ f.astype(np.float64)
+    exact = m[:, None] + m[None, :]
+    np.fill_diagonal(exact, 0.0)
+    Dg = D.cpu().numpy().astype(np.float64)
+    eff = asot.effective_precision(K, prec)
+    r = np.abs(Dg - exact) / np.maximum(exact, 1e-3)
+    assert r.max() <= TOL[eff], f"K={K} prec={eff} max rel {r.max():.3e}"
