@@ -550,6 +550,17 @@ def main():
         nominal = 2048 * 2 * 148 * mhz * 1e6 / 1e12 / (3 if kind in (3, 5) else 1)
         roofline["nominal_peak_at_clock"] = nominal
         roofline["frac_of_nominal"] = achieved / nominal
+        # the clock the last timed launch actually ran at (in-kernel %clock64 / %globaltimer
+        # probe; under power capping it sits below the clock nvidia-smi reports)
+        try:
+            emhz = asot.asot.profile_clock(kind)
+        except Exception:  # noqa: BLE001 -- kind without a probe
+            emhz = None
+        if emhz:
+            enominal = 2048 * 2 * 148 * emhz * 1e6 / 1e12 / (3 if kind in (3, 5) else 1)
+            roofline["effective_sm_mhz"] = emhz
+            roofline["nominal_peak_at_effective_clock"] = enominal
+            roofline["frac_of_nominal_effective"] = achieved / enominal
 
     # ---- mapping step (a2): the north star's "achieved HBM GB/s for mapping", next to the
     # FP32-pipe fraction that actually bounds it; live CUDA-event timing

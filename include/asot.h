@@ -295,6 +295,12 @@ int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 asot_status asot_profile_enable(int32_t on);
 asot_status asot_profile_read_kernel(int32_t which, double* ms_out, int64_t* launches, int32_t reset);
 asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset);
+/* Effective SM clock (MHz) of the most recent launch of tensor-core Sinkhorn kernel `kind`
+ * (asot_sinkhorn_kernel_kind's numbering, 1..8): CTA 0 records %clock64 and %globaltimer after
+ * its setup and at its end, and the clock is their ratio -- the clock the kernel ran at under
+ * power capping, for the roofline's nominal peak at clock.  Synchronises the device.
+ * ASOT_ERR_INVALID_ARGUMENT for kind 0 (CUDA cores) or a kind not launched yet. */
+asot_status asot_profile_clock(int32_t kind, double* sm_mhz);
 
 /* Number of kernel launches the last distance_matrix / pairwise call on this thread issued. */
 int32_t asot_last_launch_count(void);

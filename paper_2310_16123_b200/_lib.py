@@ -59,6 +59,7 @@ _SIGS = {
                                           c_vp, c_i32, c_i64, c_vp, c_vp]),
     "asot_profile_enable": (c_i32, [c_i32]),
     "asot_profile_read": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
+    "asot_profile_clock": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double)]),
     "asot_profile_read_kernel": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),
                                          c_i32]),
 }

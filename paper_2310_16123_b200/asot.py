@@ -124,6 +124,14 @@ def profile_read(reset: bool = True, kernel: int = PROF_SINKHORN) -> tuple[float
     return float(ms.value), int(n.value)
 
 
+def profile_clock(kind: int) -> float:
+    """Effective SM clock (MHz) of the last launch of Sinkhorn kernel `kind` (in-kernel
+    %clock64 / %globaltimer probe; see asot_profile_clock)."""
+    mhz = ctypes.c_double(0.0)
+    _check(_lib_handle().asot_profile_clock(int(kind), ctypes.byref(mhz)))
+    return float(mhz.value)
+
+
 def new_status(device=None) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device or "cuda")
 

@@ -272,6 +272,23 @@ asot_status asot_profile_read_kernel(int32_t which, double* ms_out, int64_t* lau
 asot_status asot_profile_read(double* sinkhorn_ms, int64_t* launches, int32_t reset) {
   return asot_profile_read_kernel(ASOT_PROF_SINKHORN, sinkhorn_ms, launches, reset);
 }
+asot_status asot_profile_clock(int32_t kind, double* sm_mhz) {
+  ASOT_CHECK_ARG(sm_mhz, "null pointer argument");
+  long long c[4] = {0, 0, 0, 0};
+  cudaError_t e;
+  switch (kind) {
+    case 1: case 7: e = asot::read_kernel_clock_tc(c); break;
+    case 2: e = asot::read_kernel_clock_tc2(c); break;
+    case 3: case 8: e = asot::read_kernel_clock_tc3(c); break;
+    case 4: e = asot::read_kernel_clock_tc4(c); break;
+    case 5: case 6: e = asot::read_kernel_clock_tc5(c); break;
+    default: return fail(ASOT_ERR_INVALID_ARGUMENT, "no clock probe for this kernel kind");
+  }
+  ASOT_CUDA(e);
+  if (c[3] <= c[1] || c[2] <= c[0]) return fail(ASOT_ERR_INVALID_ARGUMENT, "kernel kind not launched yet");
+  *sm_mhz = (double)(c[2] - c[0]) / (double)(c[3] - c[1]) * 1000.0;
+  return ASOT_OK;
+}
 int64_t asot_num_tiles(int64_t n_dist) { return n_dist < 1 ? 0 : asot::num_tiles(n_dist); }
 
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {

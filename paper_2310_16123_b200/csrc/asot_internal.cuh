@@ -238,4 +238,23 @@ cudaError_t launch_kmeans_update(const float* points, int dim, const int64_t* ba
 
 inline int kpad32(int K) { return (K + 31) & ~31; }
 
+
+// Effective-clock probe (asot_profile_clock): CTA 0's thread 0 records (%clock64, %globaltimer)
+// once the kernel's setup is done and again at its end; dclock / dns over the launch is the SM
+// clock the kernel actually ran at (nvidia-smi samples read the requested clock, not the
+// power-capped one under tensor load).
+__device__ __forceinline__ void clock_probe(long long* p, int at_end) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p[2 * at_end] = clock64();
+    p[2 * at_end + 1] = t;
+  }
+}
+cudaError_t read_kernel_clock_tc(long long* host4);
+cudaError_t read_kernel_clock_tc2(long long* host4);
+cudaError_t read_kernel_clock_tc3(long long* host4);
+cudaError_t read_kernel_clock_tc4(long long* host4);
+cudaError_t read_kernel_clock_tc5(long long* host4);
+
 }  // namespace asot

@@ -46,6 +46,7 @@ namespace tc {
 // Debug timeline (ASOT_TC_DEBUG_MODE=3): slot, event, phase -> clock64 for CTA 0's first tile.
 // events: 0 / 1 = epilogue woke for chunk 0 / 1, 2 / 3 = MMA warp passed the chunk 0 / 1 gate
 __device__ long long g_tc_trace[2][4][512];
+__device__ long long g_tc_clock[4];  // clock_probe: (clock64, globaltimer) at start / end
 
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = kEpiWarps * 32;  // epilogue threads
@@ -179,6 +180,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  clock_probe(g_tc_clock, 0);
   if (*tmem_holder != 0) __trap();  // cannot happen with a full 512-column allocation
   if (threadIdx.x == 0) {  // stage K and K (.) C_s once per CTA (TMA bulk copies)
     mbar_expect_tx(bar_g, (uint32_t)(2 * S::kImg));
@@ -452,6 +454,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
   }
   tc_fence_before();
   __syncthreads();
+  clock_probe(g_tc_clock, 1);
   tc_fence_after();
   if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(0u), "r"(kTmemCols)
@@ -544,3 +547,9 @@ cudaError_t launch_sinkhorn_tc_pairs(const int32_t* pi, const int32_t* pj, int64
 extern "C" int asot_debug_tc_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, asot::tc::g_tc_trace, sizeof(asot::tc::g_tc_trace));
 }
+
+namespace asot {
+cudaError_t read_kernel_clock_tc(long long* host4) {
+  return cudaMemcpyFromSymbol(host4, tc::g_tc_clock, 4 * sizeof(long long));
+}
+}  // namespace asot

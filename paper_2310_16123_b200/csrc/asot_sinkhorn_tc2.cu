@@ -68,6 +68,7 @@ __host__ __device__ inline uint32_t gc_image_offset(uint32_t nh, uint32_t r, uin
 }
 
 __device__ long long g_tc2_trace[4][256];
+__device__ long long g_tc2_clock[4];  // clock_probe: (clock64, globaltimer) at start / end
 
 template <int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAllThreads, 1)
@@ -116,6 +117,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  clock_probe(g_tc2_clock, 0);
   if (*tmem_holder != 0) __trap();  // full 512-column allocation starts at column 0
   if (threadIdx.x == 0) {          // this CTA's half of K, once (TMA bulk copies)
     const uint8_t* src = g_img + (size_t)rank * (128 * 1024);
@@ -344,6 +346,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   }
   tc_fence_before();
   cluster_sync();
+  clock_probe(g_tc2_clock, 1);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(0u) : "memory");
 }
 
@@ -402,3 +405,9 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
 extern "C" int asot_debug_tc2_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, asot::tc2::g_tc2_trace, sizeof(asot::tc2::g_tc2_trace));
 }
+
+namespace asot {
+cudaError_t read_kernel_clock_tc2(long long* host4) {
+  return cudaMemcpyFromSymbol(host4, tc2::g_tc2_clock, 4 * sizeof(long long));
+}
+}  // namespace asot

@@ -101,6 +101,7 @@ __device__ __forceinline__ void issue_part(uint32_t a_reg, uint32_t d_reg, uint6
 // events: 0 / 1 = epilogue woke for D half 0 / 1, 2 / 3 = its x half 0 / 1 arrive,
 // 4 / 5 = issuer passed the x half 0 / 1 gate
 __device__ long long g_tc3_trace[6][256];
+__device__ long long g_tc3_clock[4];  // clock_probe: (clock64, globaltimer) at start / end
 
 // EX (pair-list mode): tile tr holds list entries [128 tr, 128 tr + 128); each lane's marginal rows
 // come from the padded copy Hp [(n_dist + 1)][KP] (row n_dist = uniform, for invalid entries),
@@ -159,6 +160,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  clock_probe(g_tc3_clock, 0);
   if (*tmem_holder != 0) __trap();  // full allocation starts at column 0 (one CTA per SM)
   if (threadIdx.x == 0) {           // K_hi, K_lo images and the GC copy, once per CTA (TMA bulk)
     mbar_expect_tx(bar_g, (uint32_t)(3 * S::kImg));
@@ -412,6 +414,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
   }
   tc_fence_before();
   __syncthreads();
+  clock_probe(g_tc3_clock, 1);
   tc_fence_after();
   if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(0u), "r"(kTmemCols) : "memory");
@@ -535,3 +538,9 @@ cudaError_t launch_sinkhorn_tc3_pairs(const int32_t* pi, const int32_t* pj, int6
 extern "C" int asot_debug_tc3_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, asot::tc3::g_tc3_trace, sizeof(asot::tc3::g_tc3_trace));
 }
+
+namespace asot {
+cudaError_t read_kernel_clock_tc3(long long* host4) {
+  return cudaMemcpyFromSymbol(host4, tc3::g_tc3_clock, 4 * sizeof(long long));
+}
+}  // namespace asot

@@ -91,6 +91,7 @@ __device__ __forceinline__ void x_load16(const uint8_t* xb, uint32_t p, uint32_t
 //   0 issuer: first MMA of the pass issued, 1 issuer: last MMA issued,
 //   2 epilogue woke (D ready), 3 epilogue done (after the barrier), 4 producer: first load issued
 __device__ long long g_tc4_trace[5][256];
+__device__ long long g_tc4_clock[4];  // clock_probe: (clock64, globaltimer) at start / end
 
 template <int KP, int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -136,6 +137,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  clock_probe(g_tc4_clock, 0);
   if (*tmem_holder != 0) __trap();
 
   uint8_t* xb = xbuf + (size_t)blockIdx.x * (2 * kXBytes);
@@ -351,6 +353,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   }
   tc_fence_before();
   cluster_sync();
+  clock_probe(g_tc4_clock, 1);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(0u) : "memory");
 }
 
@@ -444,3 +447,9 @@ cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_
 extern "C" int asot_debug_tc4_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, asot::tc4::g_tc4_trace, sizeof(asot::tc4::g_tc4_trace));
 }
+
+namespace asot {
+cudaError_t read_kernel_clock_tc4(long long* host4) {
+  return cudaMemcpyFromSymbol(host4, tc4::g_tc4_clock, 4 * sizeof(long long));
+}
+}  // namespace asot

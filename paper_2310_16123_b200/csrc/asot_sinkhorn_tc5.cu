@@ -29,6 +29,8 @@ namespace tc5 {
 
 using namespace ::asot::ptx;
 
+__device__ long long g_tc5_clock[4];  // clock_probe: (clock64, globaltimer) at start / end
+
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = kEpiThreads + 64;   // + producer warp + MMA (leader) / relay (peer) warp
@@ -124,6 +126,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  clock_probe(g_tc5_clock, 0);
   const uint32_t tmem_base = *tmem_holder;
 
   // per-CTA X images: [side 2][hi, lo]
@@ -358,6 +361,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   }
   tc_fence_before();
   cluster_sync();
+  clock_probe(g_tc5_clock, 1);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem_base) : "memory");
 }
 
@@ -472,4 +476,10 @@ cudaError_t launch_sinkhorn_tc5(int64_t tile_begin, int64_t tile_end, int64_t n_
               : launch_split<1, false>(tile_begin, tile_end, n_dist, out, ps, H, K, img, scratch, iters, s);
 }
 
+}  // namespace asot
+
+namespace asot {
+cudaError_t read_kernel_clock_tc5(long long* host4) {
+  return cudaMemcpyFromSymbol(host4, tc5::g_tc5_clock, 4 * sizeof(long long));
+}
 }  // namespace asot
