@@ -197,3 +197,19 @@ def test_separable_cost_closed_form_tiles(asot, K, prec):
     eff = asot.effective_precision(K, prec)
     r = np.abs(Dg - exact) / np.maximum(exact, 1e-3)
     assert r.max() <= TOL[eff], f"K={K} prec={eff} max rel {r.max():.3e}"
+
+
+def test_profile_clock_probe(asot):
+    """asot_profile_clock: after a launch of a tensor-core kernel kind its in-kernel clock probe
+    gives a plausible SM clock; kind 0 (CUDA cores) has no probe."""
+    inp = make_inputs("c2", n_dist=300)
+    run = asot.distance_matrix(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors),
+                               dev(inp.cost), float(inp.eps), inp.iters, precision=1,
+                               offsets_host=inp.offsets)
+    torch.cuda.synchronize()
+    assert run.shape == (300, 300)
+    kind = asot.asot.sinkhorn_kernel_kind(inp.n_anchors, 1)
+    mhz = asot.asot.profile_clock(kind)
+    assert 300.0 < mhz < 2500.0, mhz
+    with pytest.raises(Exception):
+        asot.asot.profile_clock(0)
