@@ -69,17 +69,19 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
 // Tensor-core kernel selection: 0 = none (fp32 CUDA cores; only explicit pair lists with K < 32),
 // 1 = single-CTA resident TF32 (32 <= K <= 128), 2 = CTA-pair resident TF32 (128 < K <= 256),
 // 4 = CTA-pair streamed TF32 (256 < K <= 1024), 3 = single-CTA resident 3xTF32 (fp32-accurate
-// requests with K <= 128, and every request with K < 32), 5 = CTA-pair streamed 3xTF32 for
-// fp32-accurate requests (128 < K <= 1024; also explicit fp32 pair lists), 6 = CTA-pair streamed
-// one-pass TF32 in pair-list mode (explicit TF32 pair lists).
+// requests with 32 <= K <= 128), 5 = CTA-pair streamed 3xTF32 for fp32-accurate requests
+// (128 < K <= 1024; also explicit fp32 pair lists), 6 = CTA-pair streamed one-pass TF32 in
+// pair-list mode (explicit TF32 pair lists), 9 = fp32 lane-per-anchor kernel (every request with
+// K < 32, tiles and pair lists).
 // K < 32 never uses one-pass TF32: the per-iteration TF32 rounding of u / v dominates the TF32
 // error (R#23) and a dot product over fewer than 32 anchors barely averages it out
-// (K = 7: 2.3e-3 > the 2e-3 bar), so those requests run the 3xTF32 kernel.
+// (K = 7: 2.3e-3 > the 2e-3 bar), so those requests run in fp32.
 constexpr int32_t kMinTcAnchors = 32;
 int tc_kind(int32_t K, asot_precision prec) {
-  // K < 32: the fp32-accurate 3xTF32 kernel (K padded to 32) for both requests -- TF32 rounding
-  // is not accurate enough there (R#23) and 3xTF32 is still ~20x the CUDA-core kernel
-  if (K < kMinTcAnchors) return K >= 1 && (prec == ASOT_PREC_FP32 || prec == ASOT_PREC_TF32) ? 3 : 0;
+  // K < 32: fp32 for both requests -- TF32 rounding is not accurate enough there (R#23) -- on
+  // the lane-per-anchor kernel: a pair's state is < 32 floats, so one lane group per pair keeps
+  // every SM busy where 128-pair tensor-core tiles leave c1 on 16 SMs (latency-bound)
+  if (K < kMinTcAnchors) return K >= 1 && (prec == ASOT_PREC_FP32 || prec == ASOT_PREC_TF32) ? 9 : 0;
   if (prec == ASOT_PREC_FP32)
     return asot::sinkhorn_tc3_supported(K) ? 3 : asot::sinkhorn_tc5_supported(K) ? 5 : 0;
   if (prec != ASOT_PREC_TF32) return 0;
@@ -97,7 +99,7 @@ int pair_kind(int32_t K, asot_precision prec) {
   // pair-list modes against an independent fp32 implementation)
   static const bool simt = getenv("ASOT_PAIR_KERNEL") && std::string(getenv("ASOT_PAIR_KERNEL")) == "simt";
   if (simt) return 0;
-  if (K < kMinTcAnchors) return 8;   // the 3xTF32 1-SM kernel's pair-list mode (as tile requests, R#23)
+  if (K < kMinTcAnchors) return 9;   // fp32 lane-per-anchor kernel (as tile requests, R#23)
   if (asot::sinkhorn_tc_supported(K)) return prec == ASOT_PREC_FP32 ? 8 : 7;
   return prec == ASOT_PREC_FP32 ? 5 : 6;
 }
@@ -232,6 +234,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   } else if (kind == 8) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc3_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
                                                 gb.gc_img, gb.GC, (float*)gb.scratch, iters, s));
+  } else if (kind == 9) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_warp(ps, sink, H, K, gb.G, gb.GC, iters, s));
   } else {
     ASOT_LAUNCH(asot::launch_sinkhorn_simt(ps, sink, H, K, gb.G, gb.GC, iters, s));
   }
@@ -297,7 +301,7 @@ int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {
 
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
   const int kind = tc_kind(n_anchors, requested);
-  return kind == 0 || kind == 3 || kind == 5 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;   // (6: TF32)
+  return kind == 0 || kind == 3 || kind == 5 || kind == 9 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;   // (6: TF32)
 }
 
 static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,

@@ -157,6 +157,9 @@ cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const floa
                                const int32_t* pj, int64_t n_pairs, double* out, uint8_t* pending,
                                uint32_t* status, int sms, cudaStream_t s);
 cudaError_t launch_gibbs_prep_simt(const float* cost, int K, float eps, float* Gp, float* GCp, cudaStream_t s);
+bool sinkhorn_warp_supported(int K);
+cudaError_t launch_sinkhorn_warp(const PairSource& ps, const PairSink& out, const float* H, int K,
+                                 const float* Gp, const float* GCp, int iters, cudaStream_t s);
 cudaError_t launch_sinkhorn_simt(const PairSource& ps, const PairSink& out, const float* H, int K,
                                  const float* G, const float* GC, int iters, cudaStream_t s);
 // tcgen05 TF32 kernel, K <= 128 (images padded to kpad = roundup(K, 32)): tile mode, and the
