@@ -27,8 +27,9 @@
  *   - Floating point: inputs are fp32.  Mapping decisions are taken in fp64 wherever fp32
  *     cannot decide them (bit-exact against the fp64 definition); histograms are accumulated in
  *     fp64 in point order and rounded to fp32; Sinkhorn runs on tcgen05 tensor cores with fp32
- *     accumulation, either fp32-accurate (ASOT_PREC_FP32: 3xTF32 split operands, target 1e-4;
- *     CUDA cores for pair lists with K < 32) or with one TF32 pass (ASOT_PREC_TF32, target 2e-3).
+ *     accumulation, either fp32-accurate (ASOT_PREC_FP32: 3xTF32 split operands, target 1e-4)
+ *     or with one TF32 pass (ASOT_PREC_TF32, target 2e-3); K < 32 runs in fp32 on CUDA cores
+ *     (one lane per anchor) for both requests.
  *
  * Beyond the hot path: soft mappings ASOT-ML / ASOT-DL (NEXT-1), mini-batch
  * k-means anchors (NEXT-2), exact anchor-space OT per pair (NEXT-3), entropic OT on the original
@@ -58,13 +59,13 @@ typedef enum {
 } asot_status;
 
 typedef enum {
-  ASOT_PREC_FP32 = 0, /* fp32-accurate: 3xTF32 tcgen05 (tiles: any K <= 1024; pair lists:
-                         K >= 32), else CUDA cores; target rel. err <= 1e-4                 */
+  ASOT_PREC_FP32 = 0, /* fp32-accurate: 3xTF32 tcgen05 for 32 <= K <= 1024, fp32 CUDA cores
+                         (lane per anchor) for K < 32; target rel. err <= 1e-4              */
   ASOT_PREC_TF32 = 1  /* tcgen05 kind::tf32 MMA (RNA-rounded G and U/V, fp32 accumulate):
                          target rel. err <= 2e-3; 32 <= K <= 1024 runs on tcgen05
-                         (resident kernels for K <= 256, streamed above); K < 32 runs the
-                         fp32-accurate 3xTF32 kernel (TF32 rounding of u/v over < 32 terms
-                         can exceed 2e-3; reported by asot_effective_precision)             */
+                         (resident kernels for K <= 256, streamed above); K < 32 runs in
+                         fp32 (TF32 rounding of u/v over < 32 terms can exceed 2e-3;
+                         reported by asot_effective_precision)                              */
 } asot_precision;
 
 /* Bits OR-ed into the caller's device status word. */
@@ -113,8 +114,9 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
                                       uint32_t* status, void* stream);
 
 /* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed).
- * K <= 128: the resident 1-SM tcgen05 kernels in pair-list mode (ASOT_PREC_TF32 with K >= 32:
- * TF32; ASOT_PREC_FP32, and every K < 32: 3xTF32), bitwise the values of the tile path; K > 128:
+ * 32 <= K <= 128: the resident 1-SM tcgen05 kernels in pair-list mode (ASOT_PREC_TF32: TF32;
+ * ASOT_PREC_FP32: 3xTF32), bitwise the values of the tile path; K < 32: the fp32 lane-per-anchor
+ * kernel (the tile path's kernel, which takes pair lists natively); K > 128:
  * the streamed tcgen05 kernel in pair-list mode (TF32: one pass; FP32: 3xTF32).  All take tiles
  * of 128 consecutive list entries and read each entry's marginal rows from a padded copy of H in
  * the workspace (L2-resident).  (Environment ASOT_PAIR_KERNEL=simt selects the fp32 CUDA-core
@@ -278,9 +280,10 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
 
 /* Which Sinkhorn kernel asot_distance_matrix runs for (K, request): 0 = fp32 CUDA-core kernel,
  * 1 = TF32 1-SM resident (K <= 128), 2 = TF32 CTA pair (K <= 256), 3 = 3xTF32 fp32-accurate
- * 1-SM resident (ASOT_PREC_FP32 with K <= 128, and every request with K < 32), 4 = TF32 CTA-pair
+ * 1-SM resident (ASOT_PREC_FP32 with 32 <= K <= 128), 4 = TF32 CTA-pair
  * streamed (256 < K <= 1024, K padded to 512 or 1024),
- * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024).
+ * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024),
+ * 9 = fp32 lane-per-anchor CUDA-core kernel (every request with K < 32).
  * (Pair lists: K <= 128 the 1-SM kernels' pair-list modes, else the streamed kernel's.) */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 

@@ -66,7 +66,7 @@ asot_status check_common(int64_t n_dist, int32_t n_anchors, float eps, int32_t i
   return ASOT_OK;
 }
 
-// Tensor-core kernel selection: 0 = none (fp32 CUDA cores; only explicit pair lists with K < 32),
+// Sinkhorn kernel selection: 0 = the fp32 CUDA-core GEMM kernel (only via ASOT_PAIR_KERNEL=simt),
 // 1 = single-CTA resident TF32 (32 <= K <= 128), 2 = CTA-pair resident TF32 (128 < K <= 256),
 // 4 = CTA-pair streamed TF32 (256 < K <= 1024), 3 = single-CTA resident 3xTF32 (fp32-accurate
 // requests with 32 <= K <= 128), 5 = CTA-pair streamed 3xTF32 for fp32-accurate requests
@@ -91,7 +91,7 @@ int tc_kind(int32_t K, asot_precision prec) {
   return 0;
 }
 // Explicit pair lists (asot_pairwise_sinkhorn): K <= 128 -> the resident 1-SM kernels in
-// pair-list mode (TF32: 7; fp32 requests and every K < 32: 3xTF32, 8); above, the streamed
+// pair-list mode (TF32: 7; fp32 requests: 3xTF32, 8; K < 32: the lane-per-anchor kernel, 9); above, the streamed
 // kernel in pair-list mode (3xTF32 for fp32 requests, one TF32 pass otherwise).
 int pair_kind(int32_t K, asot_precision prec) {
   if (K < 1 || K > asot::kMaxAnchors) return 0;

@@ -1,5 +1,5 @@
-// asot_sinkhorn_simt.cu -- steps a5 + a6 on CUDA cores in fp32: the ASOT_PREC_FP32 path where the
-// 3xTF32 tensor kernel does not apply (K < 32 or K > 128) and the explicit pair-list API.
+// asot_sinkhorn_simt.cu -- steps a5 + a6 on CUDA cores in fp32 as a batched GEMM: the first fp32
+// path, now the independent cross-check of the tensor-core pair-list modes (ASOT_PAIR_KERNEL=simt).
 //
 // Batched Sinkhorn on the shared Gibbs kernel:
 //   U = A / (K V),  V = B / (K^T U),  V^(0) = 1 (R#4), exactly L iterations (R#5),
