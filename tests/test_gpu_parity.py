@@ -378,9 +378,11 @@ def test_full_size_sampled_parity_more(asot, cfg, prec, npairs):
 
 @pytest.mark.parametrize("K", [16, 64, 128])
 def test_pair_modes_vs_cuda_core_kernel(K):
-    """fp32 pair lists: the 3xTF32 1-SM kernel's pair-list mode (K <= 128, and all K < 32) against
-    the independent fp32 CUDA-core kernel (ASOT_PAIR_KERNEL=simt, a separate process) and the
-    oracle, on the same list with reversed and invalid entries."""
+    """fp32 pair lists: the 3xTF32 1-SM kernel's pair-list mode (32 <= K <= 128) or the fp32
+    lane-per-anchor kernel (K < 32) against the independent fp32 CUDA-core GEMM kernel
+    (ASOT_PAIR_KERNEL=simt, a separate process) and the oracle, on the same list with reversed and
+    invalid entries.  At K < 32 both are fp32 CUDA-core kernels with the same dot-product order
+    (u, v bitwise equal): only the final reduction over anchors differs."""
     import os
     import subprocess
     import sys
@@ -425,6 +427,8 @@ np.save(sys.argv[1], d.cpu().numpy()); np.save(sys.argv[2], H.cpu().numpy()); np
                           pi[ok].astype(np.int64), pj[ok].astype(np.int64))
     assert rel_err(d_tc[ok], c_o, 1.0).max() <= TOL[0]      # ASOT_PREC_FP32
     assert rel_err(d_simt[ok], c_o, 1.0).max() <= TOL[0]
+    if K < 32:
+        assert np.abs(d_tc[ok].astype(np.float64) - d_simt[ok]).max() <= 2e-6 * np.abs(d_simt[ok]).max()
 
 
 @pytest.mark.parametrize("K,prec", [(128, 1), (64, 0), (16, 1), (256, 1), (256, 0)])
