@@ -11,10 +11,11 @@
 // (N = 64: 2,016 pairs = 16 tiles) on 16 SMs running 2L dependent phases of ~3.4k cycles each.
 // Here lane r of a pair's group owns anchor r: its column of K and of K (.) C_s sit in registers
 // for the whole call, the current scaling is exchanged through LP floats of shared memory
-// (one store, LP/4 broadcast float4 loads) and each half-iteration is LP FMAs per lane -- a few
-// hundred cycles, with thousands of pairs in flight across all SMs.  The dot products run in the
-// CUDA-core kernel's order (c = 0 .. K-1, fmaf from 0), so u and v match it bit for bit; only
-// the final reduction over anchors is ordered differently.
+// (one store, LP/4 broadcast float4 loads) and each half-iteration is LP FMAs and one
+// reciprocal per lane -- ~260 cycles, with thousands of pairs in flight across all SMs.  The dot
+// products run in the CUDA-core kernel's order (c = 0 .. K-1, fmaf from 0); the divide is
+// m * rcp.approx(den) (<= 1 ulp, as in the tensor-core epilogues) instead of the IEEE divide,
+// which alone took a third of the time at c1.
 #include <cfloat>
 
 #include "asot_internal.cuh"
@@ -53,7 +54,9 @@ sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
       clamped |= m > 0.0f;
       den = FLT_MIN;
     }
-    return m > 0.0f ? m / den : 0.0f;
+    float rc;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));   // den >= FLT_MIN: no FTZ effect
+    return m > 0.0f ? m * rc : 0.0f;
   };
   // y = sum_c col[c] * x_c over the group's shared vector, c = 0 .. LP-1 in order
   auto dot = [&](const float (&col)[LP]) {

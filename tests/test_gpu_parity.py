@@ -381,8 +381,9 @@ def test_pair_modes_vs_cuda_core_kernel(K):
     """fp32 pair lists: the 3xTF32 1-SM kernel's pair-list mode (32 <= K <= 128) or the fp32
     lane-per-anchor kernel (K < 32) against the independent fp32 CUDA-core GEMM kernel
     (ASOT_PAIR_KERNEL=simt, a separate process) and the oracle, on the same list with reversed and
-    invalid entries.  At K < 32 both are fp32 CUDA-core kernels with the same dot-product order
-    (u, v bitwise equal): only the final reduction over anchors differs."""
+    invalid entries.  At K < 32 both are fp32 CUDA-core kernels with the same dot-product order;
+    they differ only in the divide (rcp.approx vs IEEE, <= 1 ulp per step) and the final
+    reduction order."""
     import os
     import subprocess
     import sys
