@@ -62,7 +62,7 @@ def test_padded_anchor_counts(asot, K, prec):
                                    ("c3", 17), ("c5", 2), ("c5", 17), ("c1", 2)])
 def test_tiny_n(asot, cfg, n):
     """N = 1 (no pairs), 2 (one pair, one tile), 3, 17 (a ragged second block) on every kernel family:
-    1-SM (c2), CTA pair (c3), streamed (c5), 3xTF32 at K < 32 (c1), both precisions."""
+    1-SM (c2), CTA pair (c3), streamed (c5), fp32 lane-per-anchor kernel at K < 32 (c1), both precisions."""
     inp = make_inputs(cfg, n_dist=n, iters=5)
     for prec in (0, 1):
         Dg, Do, st = run_both(asot, inp, prec)
