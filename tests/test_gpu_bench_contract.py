@@ -38,4 +38,8 @@ def test_bench_line_ours():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "workload" in d["config"]
+    # tensor-core kernels: the in-kernel clock probe gives the clock the timed launches ran at
+    assert rf["bound"] == "tensor"
+    assert 300.0 < rf["effective_sm_mhz"] < 2500.0
+    assert abs(rf["frac_of_nominal_effective"] * rf["nominal_peak_at_effective_clock"] - rf["achieved"]) < 1e-6 * rf["achieved"]
 
