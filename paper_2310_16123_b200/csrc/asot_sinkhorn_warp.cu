@@ -29,10 +29,11 @@ template <int LP>
 __global__ void __launch_bounds__(kThreads)
 sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, int K,
                      const float* __restrict__ Gp, const float* __restrict__ GCp, int kp, int iters) {
-  __shared__ __align__(16) float xs[kThreads];
+  __shared__ __align__(16) float xs[2][kThreads];   // double-buffered: one __syncwarp per step
   const int r = threadIdx.x % LP;                                  // anchor owned by this lane
   const int64_t slot = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / LP;
-  float* xg = xs + (threadIdx.x - r);                              // this pair's LP floats
+  float* xg0 = &xs[0][threadIdx.x - r];                            // this pair's LP floats
+  float* xg1 = &xs[1][threadIdx.x - r];
   const bool in = r < K;
 
   // columns r of K and K (.) C_s (row-padded images Gp[c][r], c < K; zeros past K)
@@ -59,7 +60,7 @@ sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
     return m > 0.0f ? m * rc : 0.0f;
   };
   // y = sum_c col[c] * x_c over the group's shared vector, c = 0 .. LP-1 in order
-  auto dot = [&](const float (&col)[LP]) {
+  auto dot = [&](const float* xg, const float (&col)[LP]) {
     float y = 0.0f;
 #pragma unroll
     for (int c4 = 0; c4 < LP; c4 += 4) {
@@ -74,21 +75,21 @@ sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
 
   float v = in ? 1.0f : 0.0f;   // v0 = 1 on real anchors (R#4)
   float u = 0.0f;
+  // buffer 0 carries v, buffer 1 carries u: a buffer is rewritten only after the __syncwarp that
+  // follows the other buffer's store, which every lane passes after finishing its reads
   for (int it = 0; it < iters; ++it) {
-    xg[r] = v;
+    xg0[r] = v;
     __syncwarp();
-    u = divide(a, dot(g));
-    __syncwarp();
+    u = divide(a, dot(xg0, g));
     if (it + 1 == iters) break;
-    xg[r] = u;
+    xg1[r] = u;
     __syncwarp();
-    v = divide(b, dot(g));
-    __syncwarp();
+    v = divide(b, dot(xg1, g));
   }
   // last v-update fused with the cost: part_r = v_r ((K (.) C_s) u)_r
-  xg[r] = u;
+  xg1[r] = u;
   __syncwarp();
-  float part = divide(b, dot(g)) * dot(gc);
+  float part = divide(b, dot(xg1, g)) * dot(xg1, gc);
 #pragma unroll
   for (int o = LP / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
