@@ -35,6 +35,43 @@ TF32_OVER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense tf32 / bf16
 FP32_ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max SM clock
 
 
+DEBUG_ENV = ("ASOT_TC_DEBUG_MODE", "ASOT_PAIR_KERNEL", "ASOT_SOFT_DL_GENERIC")
+
+
+def asot_env() -> dict:
+    """Every ASOT_* environment variable of this run (recorded in the JSON line)."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("ASOT_")}
+
+
+def cublas_tf32_tflops(dev) -> float:
+    """Measured dense TF32 GEMM rate of this GPU through cuBLAS (torch.matmul 8192^3, TF32
+    allowed; best of 3 x 5): context for the roofline denominator, which stays the
+    MEASURED_PEAKS bf16 figure x the nominal tf32/bf16 ratio."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(2):
+            a @ b
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 5 * 2 * n ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
+        del a, b
+        return best
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def baseline_metric() -> str:
     with open(os.path.join(ROOT, "BASELINE.json")) as f:
         return json.load(f)["metric"]
@@ -289,6 +326,10 @@ def main():
                     help="NEXT-3: also solve exact anchor-space OT on a seeded pair sample and report "
                          "its pairs/s and the eASOT-vs-exact gap")
     ap.add_argument("--exact-pairs", type=int, default=0, help="exact-ASOT sample (0: 20000, 1000 if K > 128)")
+    ap.add_argument("--bounds", action="store_true",
+                    help="NEXT-3: Prop. 1 / Prop. 2 bound terms, exact W_AS and exact W_1 on the original "
+                         "points (Euclidean metric) on a pair sample, with violation counts")
+    ap.add_argument("--bounds-pairs", type=int, default=20000)
     ap.add_argument("--pairs-api", action="store_true",
                     help="also time asot_pairwise_sinkhorn (SPEC batched_sinkhorn_fixed) on the whole "
                          "upper triangle given as an explicit (shuffled) pair list")
@@ -304,6 +345,12 @@ def main():
                     help="shrink N (profiling runs only; bench lines use the full config)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # diagnostic kernel selection must never reach a bench line: the
+    # epilogue/MMA-skipping variants exist only in ASOT_DEBUG_BUILD libraries, and the
+    # cross-check kernel switches are for tests
+    bad_env = [k for k in DEBUG_ENV if os.environ.get(k)]
+    if bad_env:
+        raise SystemExit(f"bench.py refuses to run with diagnostic kernel selection set: {bad_env}")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -469,7 +516,9 @@ def main():
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
+            torch.cuda.nvtx.range_push(f"asot step {k}")
             Dres = step()
+            torch.cuda.nvtx.range_pop()
             evs[k][1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -530,11 +579,16 @@ def main():
         peak = FP32_ALU_PEAK_TFLOPS
         bound, peak_note = "alu", "FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz"
     achieved = flops_per_pair * pairs_per_launch / (kern_avg_ms / 1e3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(f"{inp.name}:{args.precision}")
+    # ncu evidence for this kernel and workload (profiles/ncu_summary.json, written from the
+    # committed `ncu --set full` captures by tools/summarize_ncu.py: a run under ncu is never
+    # the bench run, so these are the capture's per-launch numbers, named with their source)
+    traffic, ncu_ev = None, None
+    spath = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(spath):
+        with open(spath) as f:
+            ncu_ev = json.load(f).get(f"{inp.name}:{args.precision}")
+        if ncu_ev:
+            traffic = ncu_ev.get("dram_bytes_per_launch")
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": asot.asot.KERNEL_NAMES[kind],
@@ -542,7 +596,12 @@ def main():
                 "kernel_share_of_step": kern_avg_ms * kern_n / max(tot_ms, 1e-9) if world == 1 else None,
                 "flops_per_pair": flops_per_pair, "pairs_per_launch": pairs_per_launch,
                 "peak_note": peak_note,
-                "peak_sustained_based": peaks.get("bf16_tflops_sustained", 0) * (TF32_OVER_BF16 if eff == asot.TF32 else 0) or None}
+                "peak_sustained_based": peaks.get("bf16_tflops_sustained", 0) * (TF32_OVER_BF16 if eff == asot.TF32 else 0) or None,
+                "ncu": ncu_ev}
+    if bound == "tensor" and rank == 0:
+        ct = cublas_tf32_tflops(dev)
+        roofline["cublas_tf32_measured_tflops"] = ct
+        roofline["frac_of_cublas_tf32"] = achieved / (ct / (3 if kind in (3, 5) else 1))
     if bound == "tensor":
         # context: the hardware's nominal dense TF32 rate (2048 MAC/clk/SM, tools/cg2_rate.cu) at the
         # median SM clock sampled during the timed region (3xTF32: one third of it)
@@ -709,6 +768,48 @@ def main():
                  "easot_vs_exact_rel_p90": float(np.quantile(rel, 0.9)) if ok.any() else None,
                  "support_limit": "none (K <= 1024)"}
 
+    # ---- NEXT-3 bound checks: the paper's guarantee |W_AS - W_1| <= Prop. 1 / Prop. 2 bounds,
+    # per pair at scale, all terms on the GPU (Euclidean C_s and C, R#7; one-hot P_o)
+    bounds = None
+    if args.bounds and rank == 0 and world == 1:
+        from asot_inputs import random_pairs
+        bi, bj = random_pairs(inp.n_dist, min(args.bounds_pairs, inp.n_pairs), seed=79)
+        bi_d, bj_d = t(bi.astype(np.int32)), t(bj.astype(np.int32))
+        bst = asot.asot.new_status(dev)
+        asg, Hb, _ = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+        CsE = asot.mahalanobis_cost(anc, torch.eye(inp.dim, dtype=torch.float32, device=dev), normalize=False)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        w_as = asot.exact_asot_pairs(Hb, CsE, bi_d, bj_d, status=bst)
+        ev[1].record()
+        w1 = asot.exact_w1_points(pts, offs, w, bi_d, bj_d, status=bst)
+        ev[2].record()
+        l1, linf, p2 = asot.bound_terms(pts, offs, anc, asg, CsE, bi_d, bj_d, status=bst)
+        ev[3].record()
+        torch.cuda.synchronize()
+        st_b = int(bst.item())
+        w_as, w1 = w_as.cpu().numpy(), w1.cpu().numpy()
+        l1, linf, p2 = l1.cpu().numpy(), linf.cpu().numpy(), p2.cpu().numpy()
+        ok = np.isfinite(w1) & np.isfinite(w_as)
+        gap = np.abs(w_as - w1)[ok]
+        ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(3)]
+        bounds = {
+            "metric": "Euclidean C_s = ||w_u - w_v||_2 and C = ||x - y||_2 (R#7), one-hot P_o",
+            "sample_pairs": int(len(bi)), "checked_pairs": int(ok.sum()),
+            "skipped_w1_support_gt_64": int((~np.isfinite(w1)).sum()), "status_flags": st_b,
+            "violations_prop1_l1": int((gap > l1[ok] + 1e-9).sum()),
+            "violations_prop1_max": int((gap > linf[ok] + 1e-9).sum()),
+            "violations_prop2": int((gap > p2[ok] + 1e-9).sum()),
+            "gap_mean": float(gap.mean()) if ok.any() else None,
+            "gap_over_prop1_max_median": float(np.median(gap / linf[ok])) if ok.any() else None,
+            "gap_over_prop1_l1_median": float(np.median(gap / l1[ok])) if ok.any() else None,
+            "gap_over_prop2_median": float(np.median(gap / p2[ok])) if ok.any() else None,
+            "ms": {"exact_w_as": ms[0], "exact_w1_points": ms[1], "bound_terms": ms[2]},
+            "pairs_per_s": {"exact_w_as": len(bi) / (ms[0] / 1e3), "exact_w1_points": len(bi) / (ms[1] / 1e3),
+                            "bound_terms": len(bi) / (ms[2] / 1e3)},
+        }
+
     # ---- e2e: host buffers through the public C-ABI host entry point (N = 1), or the
     # distributed public API with H2D / D2H inside the timed region (N > 1)
     e2e = None
@@ -800,10 +901,11 @@ def main():
             "config": workload_config(inp, args, world),
             "result_exchange": exchange_note[0],
             "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "eot_baseline": eot_base,
-            "exact_asot": exact, "pairs_api": pairs_api,
+            "exact_asot": exact, "pairs_api": pairs_api, "bounds": bounds,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
             "wall_s_timed_region": wall,
+            "env": asot_env(),
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
         }
         print(json.dumps(line), flush=True)

@@ -72,10 +72,15 @@ typedef enum {
 #define ASOT_FLAG_EMPTY_DIST       1u  /* a distribution with n_i = 0 (S:24 requires n >= 1)      */
 #define ASOT_FLAG_BAD_MASS         2u  /* negative weight or |sum w - 1| > 1e-5 (fp32)     */
 #define ASOT_FLAG_NONFINITE_INPUT  4u  /* NaN/Inf in points, weights or anchors                  */
-#define ASOT_FLAG_DENOM_CLAMPED    8u  /* a Sinkhorn denominator < FLT_MIN was clamped     */
+#define ASOT_FLAG_DENOM_CLAMPED    8u  /* a Sinkhorn denominator on an anchor with mass left
+                                          [FLT_MIN, 2^126] and was clamped into it (
+                                          a warning: the distance is that of the clamped run) */
 #define ASOT_FLAG_NONFINITE_OUTPUT 16u /* a distance came out NaN/Inf                            */
 #define ASOT_FLAG_SOFT_FALLBACK    32u /* a soft code was all zero -> uniform row (warning) */
-#define ASOT_FLAG_EXACT_TOO_LARGE  64u /* reserved (exact ASOT now solves every support; never raised) */
+#define ASOT_FLAG_EXACT_TOO_LARGE  64u /* asot_exact_w1_points: a support above 64 points (NaN out);
+                                          exact ASOT itself solves every support              */
+#define ASOT_FLAG_BAD_INDEX       128u /* an explicit pair-list entry had i or j outside [0, n_dist):
+                                          its output is NaN (asot_pairwise_sinkhorn)             */
 
 /* Distance-matrix tiling (step a4).  Distributions are grouped in blocks of 16; block pairs
  * (bi <= bj) are enumerated row-major over the upper triangle of the block grid; each block
@@ -120,8 +125,11 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
  * the streamed tcgen05 kernel in pair-list mode (TF32: one pass; FP32: 3xTF32).  All take tiles
  * of 128 consecutive list entries and read each entry's marginal rows from a padded copy of H in
  * the workspace (L2-resident).  (Environment ASOT_PAIR_KERNEL=simt selects the fp32 CUDA-core
- * kernel instead, for cross-checks.)  Invalid entries (index out of range) give 0.  Workspace from
- * asot_pairwise_workspace_bytes(n_dist, n_anchors, prec).  Arguments:
+ * kernel instead, for cross-checks.)  Invalid entries (an index outside [0, n_dist)) give NaN
+ * and raise ASOT_FLAG_BAD_INDEX.  n_pairs = 0 returns ASOT_OK at once (pair_i, pair_j and
+ * dist_out may then be NULL).  Workspace from asot_pairwise_workspace_bytes(n_dist, n_anchors,
+ * prec).  Status: the call's flags are OR-ed into ONE word for the whole list (DESIGN R#33:
+ * no per-pair flag array; a flagged run is re-run on a sub-list to locate pairs).  Arguments:
  *   hist     [n_dist, n_anchors] f32 device (rows are a' / b')
  *   cost     [n_anchors, n_anchors] f32 device: C_s symmetric, >= 0, zero diagonal
  *   eps > 0 (max(C_s)/eps <= 80 is checked against cost_max, a host value the caller supplies:
@@ -274,6 +282,36 @@ asot_status asot_exact_asot_pairs(const float* hist, int64_t n_dist, int32_t n_a
                                   const int32_t* pair_i, const int32_t* pair_j, int64_t n_pairs,
                                   double* dist_out, uint32_t* status, void* workspace,
                                   size_t workspace_bytes, void* stream);
+
+/* ---- NEXT-3 bound checks at scale: the paper's guarantees per pair ------------
+ * asot_exact_w1_points: EXACT W_1 on the ORIGINAL point sets (Eq. (1)) with the Euclidean
+ * ground metric of Prop. 2 (R#7): dist_out[p] = min <T, C> over T in U(a, b), C(r, c) =
+ * ||x_r - y_c||_2 in fp64 from the f32 points, a / b = the point weights of distributions
+ * pair_i[p] / pair_j[p] renormalised in fp64 (R#14); successive-shortest-path min-cost flow on the
+ * supports (points with weight > 0), one warp per pair, supports of up to 64 points per side
+ * (graph-sized distributions, c1 / c2).  Larger supports: NaN and ASOT_FLAG_EXACT_TOO_LARGE;
+ * invalid indices: NaN and ASOT_FLAG_BAD_INDEX.  points [T, dim] f32, offsets [n_dist+1] i64,
+ * weights [T] f32, pair_i / pair_j [n_pairs] i32, dist_out [n_pairs] f64: device pointers.
+ *
+ * asot_bound_terms: per pair the right-hand sides of Prop. 1 (Eq. (7)) and
+ * Prop. 2 for the one-hot mapping P_o:
+ *   prop1_l1[p]   = sum_{r,c} |C_hat(r, c) - C(r, c)|, C_hat(r, c) = cost[u_r][v_c] (Z_x C_s Z_y^T
+ *                   for one-hot Z), C(r, c) = ||x_r - y_c||_2;
+ *   prop1_max[p]  = max_{r,c} |C_hat(r, c) - C(r, c)| (the tighter bound the proof gives, R#16);
+ *   prop2[p]      = m sum_r ||w_{u_r} - x_r||_2 + n sum_c ||w_{v_c} - y_c||_2 (n, m = point counts).
+ * u = assign (the mapping's output, asot_map_to_anchors), cost = the C_s the caller's W_AS used
+ * (Euclidean anchor distances for Prop. 2: asot_mahalanobis_cost with M = I, normalize = 0).
+ * All terms accumulate in fp64.  anchors [n_anchors, dim] f32, assign [T] i32, cost
+ * [n_anchors, n_anchors] f32, outputs [n_pairs] f64: device pointers.  One CTA per pair. */
+asot_status asot_exact_w1_points(const float* points, const int64_t* offsets, const float* weights,
+                                 int64_t n_dist, int32_t dim, const int32_t* pair_i,
+                                 const int32_t* pair_j, int64_t n_pairs, double* dist_out,
+                                 uint32_t* status, void* stream);
+asot_status asot_bound_terms(const float* points, const int64_t* offsets, int64_t n_dist, int32_t dim,
+                             const float* anchors, int32_t n_anchors, const int32_t* assign,
+                             const float* cost, const int32_t* pair_i, const int32_t* pair_j,
+                             int64_t n_pairs, double* prop1_l1, double* prop1_max, double* prop2,
+                             uint32_t* status, void* stream);
 
 /* Precision actually used for a given K and request (TF32 covers 32 <= K <= 1024). */
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested);

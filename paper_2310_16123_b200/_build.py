@@ -15,6 +15,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+# ASOT_DEBUG_BUILD=1 adds the diagnostic kernel variants the tools/ timelines select through
+# ASOT_TC_DEBUG_MODE (epilogue or MMAs skipped, clock traces).  The product library never has them.
+if os.environ.get("ASOT_DEBUG_BUILD") == "1":
+    FLAGS.append("-DASOT_DEBUG_KERNELS")
 
 
 def _compile(src: str) -> tuple[str, str]:

@@ -55,6 +55,9 @@ _SIGS = {
     "asot_exact_asot_pairs": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                       c_size, c_vp]),
     "asot_exact_asot_workspace_bytes": (c_size, [c_i64, c_i32]),
+    "asot_exact_w1_points": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "asot_bound_terms": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                 c_vp, c_vp, c_vp, c_vp, c_vp]),
     "asot_map_to_anchors_bcast": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp,
                                           c_vp, c_i32, c_i64, c_vp, c_vp]),
     "asot_profile_enable": (c_i32, [c_i32]),

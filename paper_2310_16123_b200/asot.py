@@ -15,7 +15,8 @@ import torch
 
 from . import _lib
 
-FP32 = 0  # ASOT_PREC_FP32: CUDA-core fp32, IEEE divide (rel. err <= 1e-4 target)
+FP32 = 0  # ASOT_PREC_FP32: fp32-accurate -- 3xTF32 tcgen05 (K >= 32), fp32 CUDA cores (K < 32);
+          # rel. err <= 1e-4 target
 TF32 = 1  # ASOT_PREC_TF32: tcgen05 kind::tf32 MMA, fp32 accumulate (rel. err <= 2e-3 target)
 TILE_SLOTS = 128
 
@@ -26,6 +27,7 @@ FLAG_DENOM_CLAMPED = 8
 FLAG_NONFINITE_OUTPUT = 16
 FLAG_SOFT_FALLBACK = 32
 FLAG_EXACT_TOO_LARGE = 64
+FLAG_BAD_INDEX = 128
 
 _STATUS_EXC = {1: ValueError, 2: ValueError, 3: FloatingPointError, 4: RuntimeError,
                5: NotImplementedError, 6: MemoryError}
@@ -74,6 +76,26 @@ def _need_f32(*ts):
     for t in ts:
         if t is not None and t.dtype != torch.float32:
             raise ValueError(f"float32 tensors are required (got {t.dtype})")
+
+
+def _pair_list(pair_i, pair_j) -> int:
+    """Explicit pair lists are two 1-D int32 device tensors of one length (the ABI reads i32:
+    an int64 tensor would be read as (low, high) word pairs).  Returns the length."""
+    for t in (pair_i, pair_j):
+        if t.dtype != torch.int32:
+            raise ValueError(f"pair_i / pair_j must be int32 tensors (got {t.dtype})")
+        if t.dim() != 1:
+            raise ValueError("pair_i / pair_j must be 1-D")
+    if pair_i.numel() != pair_j.numel():
+        raise ValueError(f"pair_i has {pair_i.numel()} entries, pair_j {pair_j.numel()}")
+    return int(pair_i.numel())
+
+
+def _hist_cost(H, cost):
+    """H [N, K] and C_s [K, K], both f32."""
+    _need_f32(H, cost)
+    if H.dim() != 2 or cost.dim() != 2 or cost.shape[0] != cost.shape[1] or cost.shape[0] != H.shape[1]:
+        raise ValueError(f"need H [N, K] and cost [K, K] (got {tuple(H.shape)}, {tuple(cost.shape)})")
 
 
 def num_tiles(n_dist: int) -> int:
@@ -143,6 +165,8 @@ def check_status(status, allow: int = FLAG_DENOM_CLAMPED | FLAG_SOFT_FALLBACK | 
     bad = v & ~allow
     if bad & (FLAG_EMPTY_DIST | FLAG_BAD_MASS):
         raise ValueError(f"infeasible mass (status flags {v:#x})")
+    if bad & FLAG_BAD_INDEX:
+        raise ValueError(f"pair-list index outside [0, n_dist) (status flags {v:#x})")
     if bad & (FLAG_NONFINITE_INPUT | FLAG_NONFINITE_OUTPUT):
         raise FloatingPointError(f"non-finite values (status flags {v:#x})")
     return v
@@ -325,9 +349,11 @@ def eot_pairs(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor
     cost_scale * ||x - y||^2).  Returns dist [n_pairs] f32."""
     _need_cuda(points, offsets, weights, pair_i, pair_j)
     _need_f32(points, weights)
+    n = _pair_list(pair_i, pair_j)
+    if n == 0:
+        return torch.empty(0, dtype=torch.float32, device=points.device)
     oh = _host_offsets(offsets, offsets_host)
     N = oh.shape[0] - 1
-    n = int(pair_i.numel())
     out = torch.empty(max(n, 1), dtype=torch.float32, device=points.device)
     st = new_status(points.device) if status is None else status
     L = _lib_handle()
@@ -345,10 +371,12 @@ def exact_asot_pairs(H: torch.Tensor, cost: torch.Tensor, pair_i: torch.Tensor, 
     """NEXT-3: exact anchor-space OT W_AS for explicit pairs (fp64 min-cost flow on the histogram
     supports; a warp per pair up to 128-bin supports, a CTA per pair above).  Returns dist [n_pairs]
     f64 (NaN for invalid indices or an empty support)."""
+    _hist_cost(H, cost)
+    n = _pair_list(pair_i, pair_j)
     _need_cuda(H, cost, pair_i, pair_j)
-    _need_f32(H, cost)
+    if n == 0:
+        return torch.empty(0, dtype=torch.float64, device=H.device)
     N, K = H.shape
-    n = int(pair_i.numel())
     out = torch.empty(max(n, 1), dtype=torch.float64, device=H.device)
     st = new_status(H.device) if status is None else status
     ws = _ws(workspace, H.device).get(int(_lib_handle().asot_exact_asot_workspace_bytes(n, int(K))))
@@ -357,14 +385,58 @@ def exact_asot_pairs(H: torch.Tensor, cost: torch.Tensor, pair_i: torch.Tensor, 
     return out[:n]
 
 
+def exact_w1_points(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
+                    pair_i: torch.Tensor, pair_j: torch.Tensor, status: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    """NEXT-3 bound checks: exact W_1 on the original point sets with the Euclidean ground metric
+    (supports <= 64 points per side; larger: NaN + FLAG_EXACT_TOO_LARGE).  Returns [n_pairs] f64."""
+    _need_f32(points, weights)
+    n = _pair_list(pair_i, pair_j)
+    _need_cuda(points, offsets, weights, pair_i, pair_j)
+    out = torch.empty(n, dtype=torch.float64, device=points.device)
+    if n == 0:
+        return out
+    st = new_status(points.device) if status is None else status
+    _check(_lib_handle().asot_exact_w1_points(_ptr(points), _ptr(offsets), _ptr(weights),
+                                              int(offsets.numel()) - 1, int(points.shape[1]), _ptr(pair_i),
+                                              _ptr(pair_j), n, _ptr(out), _ptr(st), _stream(stream)))
+    return out
+
+
+def bound_terms(points: torch.Tensor, offsets: torch.Tensor, anchors: torch.Tensor, assign: torch.Tensor,
+                cost: torch.Tensor, pair_i: torch.Tensor, pair_j: torch.Tensor,
+                status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-3: per pair (Prop. 1 ||C_hat - C||_1, max |C_hat - C|, Prop. 2 residual bound), each
+    [n_pairs] f64, for the one-hot assignments `assign` and the anchor cost `cost` (C_s of W_AS)."""
+    _need_f32(points, anchors, cost)
+    if assign.dtype != torch.int32:
+        raise ValueError("assign must be int32")
+    n = _pair_list(pair_i, pair_j)
+    _need_cuda(points, offsets, anchors, assign, cost, pair_i, pair_j)
+    outs = [torch.empty(n, dtype=torch.float64, device=points.device) for _ in range(3)]
+    if n == 0:
+        return tuple(outs)
+    st = new_status(points.device) if status is None else status
+    _check(_lib_handle().asot_bound_terms(_ptr(points), _ptr(offsets), int(offsets.numel()) - 1,
+                                          int(points.shape[1]), _ptr(anchors), int(anchors.shape[0]),
+                                          _ptr(assign), _ptr(cost), _ptr(pair_i), _ptr(pair_j), n,
+                                          _ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), _ptr(st),
+                                          _stream(stream)))
+    return tuple(outs)
+
+
 def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: int,
                       pair_i: torch.Tensor, pair_j: torch.Tensor, precision: int = TF32,
                       cost_max: Optional[float] = None, status: Optional[torch.Tensor] = None,
                       workspace: Optional[Workspace] = None, stream=None) -> torch.Tensor:
-    """Steps a1 + a5 + a6 on explicit pairs (a = H[pair_i] on the u side)."""
+    """Steps a1 + a5 + a6 on explicit pairs (a = H[pair_i] on the u side).  pair_i / pair_j:
+    int32 device tensors of one length; an entry outside [0, N) gives NaN and FLAG_BAD_INDEX."""
+    _hist_cost(H, cost)
+    n = _pair_list(pair_i, pair_j)
     _need_cuda(H, cost, pair_i, pair_j)
+    if n == 0:
+        return torch.empty(0, dtype=torch.float32, device=H.device)
     N, K = H.shape
-    n = int(pair_i.numel())
     out = torch.empty(n, dtype=torch.float32, device=H.device)
     cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
     st = new_status(H.device) if status is None else status

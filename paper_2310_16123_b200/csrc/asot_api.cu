@@ -6,6 +6,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "asot_internal.cuh"
 
 namespace {
@@ -153,6 +155,15 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   return b;
 }
 
+// NVTX ranges per hot-path phase (SURVEY §5 tracing): host-side push/pop around each phase's
+// launches, visible in Nsight Systems / ncu --nvtx; no cost without an attached tool.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+
 // Profiling (asot_profile_*): event pairs recorded around each launch of the Sinkhorn kernel
 // (ASOT_PROF_SINKHORN) and of the mapping kernel (ASOT_PROF_MAP).
 thread_local bool g_prof_on = false;
@@ -193,6 +204,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
                          cudaStream_t s) {
   const int kind = gb.kind;
+  {
+  Nvtx range("asot a1 gibbs_prep");
   if (kind == 5 || kind == 6) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc5(cost, K, eps, (uint8_t*)gb.g_img, s));
   } else if (kind == 4) {
@@ -207,6 +220,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   } else {
     ASOT_LAUNCH(asot::launch_gibbs_prep_simt(cost, K, eps, gb.G, gb.GC, s));
   }
+  }
+  Nvtx range("asot a5+a6 sinkhorn+cost");
   ProfScope prof(ASOT_PROF_SINKHORN, s);
   if (kind == 5 || kind == 6) {
     const bool expl = ps.pi != nullptr;   // pair-list mode: tiles of 128 list entries
@@ -349,9 +364,11 @@ static asot_status map_impl(const float* points, const int64_t* offsets, const i
   const int64_t T = offsets_host[n_dist];
   cudaStream_t s = (cudaStream_t)stream;
   if (T > 0) {
+    Nvtx range("asot a2 map_assign");
     ProfScope prof(ASOT_PROF_MAP, s);
     ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
   }
+  Nvtx range("asot a3 histograms");
   ASOT_LAUNCH(asot::launch_histograms(assign_out, weights, offsets, n_dist, n_anchors, hist_out, status, s,
                                       peers, n_peers, row_base));
   return ASOT_OK;
@@ -500,6 +517,41 @@ asot_status asot_eot_pairs(const float* points, const int64_t* offsets, const in
   return ASOT_OK;
 }
 
+asot_status asot_exact_w1_points(const float* points, const int64_t* offsets, const float* weights,
+                                 int64_t n_dist, int32_t dim, const int32_t* pair_i,
+                                 const int32_t* pair_j, int64_t n_pairs, double* dist_out,
+                                 uint32_t* status, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(n_pairs >= 0 && n_dist >= 1 && dim >= 1, "bad sizes");
+  ASOT_CHECK_ARG(points && offsets && weights && status && (n_pairs == 0 || (pair_i && pair_j && dist_out)),
+                 "null pointer argument");
+  if (n_pairs == 0) return ASOT_OK;
+  Nvtx range("asot next3 exact_w1_points");
+  ASOT_LAUNCH(asot::launch_w1_points(points, offsets, weights, n_dist, dim, pair_i, pair_j, n_pairs, dist_out,
+                                     status, device_sms(), (cudaStream_t)stream));
+  return ASOT_OK;
+}
+
+asot_status asot_bound_terms(const float* points, const int64_t* offsets, int64_t n_dist, int32_t dim,
+                             const float* anchors, int32_t n_anchors, const int32_t* assign,
+                             const float* cost, const int32_t* pair_i, const int32_t* pair_j,
+                             int64_t n_pairs, double* prop1_l1, double* prop1_max, double* prop2,
+                             uint32_t* status, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(n_pairs >= 0 && n_dist >= 1 && n_anchors >= 1, "bad sizes");
+  ASOT_CHECK_ARG(dim >= 1, "dim must be >= 1");
+  if (dim > asot::kMaxDim) return fail(ASOT_ERR_UNSUPPORTED, "dim > 128 is not supported");
+  ASOT_CHECK_ARG(points && offsets && anchors && assign && cost && status &&
+                     (n_pairs == 0 || (pair_i && pair_j && prop1_l1 && prop1_max && prop2)),
+                 "null pointer argument");
+  if (n_pairs == 0) return ASOT_OK;
+  Nvtx range("asot next3 bound_terms");
+  ASOT_LAUNCH(asot::launch_bound_terms(points, offsets, n_dist, dim, anchors, n_anchors, assign, cost, pair_i,
+                                       pair_j, n_pairs, prop1_l1, prop1_max, prop2, status, device_sms(),
+                                       (cudaStream_t)stream));
+  return ASOT_OK;
+}
+
 size_t asot_exact_asot_workspace_bytes(int64_t n_pairs, int32_t n_anchors) {
   return asot::exact_pairs_workspace_bytes(n_pairs, n_anchors, device_sms());
 }
@@ -533,16 +585,17 @@ asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_
                                    uint32_t* status, void* workspace, size_t workspace_bytes,
                                    void* stream) {
   g_launches = 0;
-  ASOT_CHECK_ARG(hist && cost && pair_i && pair_j && dist_out && status, "null pointer argument");
+  ASOT_CHECK_ARG(n_pairs >= 0, "n_pairs must be >= 0");
+  ASOT_CHECK_ARG(hist && cost && status && (n_pairs == 0 || (pair_i && pair_j && dist_out)),
+                 "null pointer argument");
   asot_status st = check_common(n_dist, n_anchors, eps, iters, cost_max);
   if (st != ASOT_OK) return st;
-  ASOT_CHECK_ARG(n_pairs >= 0, "n_pairs must be >= 0");
-  if (n_pairs == 0) return ASOT_OK;
+  if (n_pairs == 0) return ASOT_OK;   // (pair_i, pair_j, dist_out may be null)
   Carver cv{(char*)workspace, workspace_bytes};
   GibbsBufs gb = carve_gibbs(cv, n_anchors, pair_kind(n_anchors, prec), n_dist);
   if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
   asot::PairSource ps{pair_i, pair_j, n_pairs, 0, n_dist};
-  asot::PairSink sink{dist_out, nullptr, n_dist, status};
+  asot::PairSink sink{dist_out, nullptr, n_dist, status, 1};
   return run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, gb, 0, 0,
                       (cudaStream_t)stream);
 }
@@ -600,10 +653,13 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
     Huse = Hw;
   }
   asot::PairSource ps{nullptr, nullptr, (tile_end - tile_begin) * asot::kTileSlots, tile_begin, n_dist};
-  asot::PairSink sink{packed_out, dist_out, n_dist, status};
+  asot::PairSink sink{packed_out, dist_out, n_dist, status, 0};
   st = run_sinkhorn(ps, sink, Huse, cost, eps, n_anchors, iters, gb, tile_begin, tile_end, s);
   if (st != ASOT_OK) return st;
-  if (dist_out && tile_begin == 0 && tile_end == n_tiles) ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, s));
+  if (dist_out && tile_begin == 0 && tile_end == n_tiles) {
+    Nvtx range("asot a6 zero_diag");
+    ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, s));
+  }
   return ASOT_OK;
 }
 
@@ -648,17 +704,21 @@ asot_status asot_distance_matrix_host(const float* points_host, const int64_t* o
   const size_t rest_bytes = workspace_bytes - cv.used;
 
   // one cudaMemcpyAsync per buffer (no batched-copy APIs)
+  {
+  Nvtx range("asot e2e h2d");
   ASOT_CUDA(cudaMemcpyAsync(d_points, points_host, (size_t)T * dim * 4, cudaMemcpyHostToDevice, s));
   ASOT_CUDA(cudaMemcpyAsync(d_offsets, offsets_host, (size_t)(n_dist + 1) * 8, cudaMemcpyHostToDevice, s));
   ASOT_CUDA(cudaMemcpyAsync(d_weights, weights_host, (size_t)T * 4, cudaMemcpyHostToDevice, s));
   ASOT_CUDA(cudaMemcpyAsync(d_anchors, anchors_host, (size_t)n_anchors * dim * 4, cudaMemcpyHostToDevice, s));
   ASOT_CUDA(cudaMemcpyAsync(d_cost, cost_host, (size_t)n_anchors * n_anchors * 4, cudaMemcpyHostToDevice, s));
   ASOT_CUDA(cudaMemsetAsync(d_status, 0, 4, s));
+  }
   asot_status st = asot_distance_matrix(d_points, d_offsets, offsets_host, d_weights, n_dist, dim,
                                         d_anchors, n_anchors, d_cost, cmax, eps, iters, prec,
                                         nullptr, 0, asot::num_tiles(n_dist), d_D, nullptr,
                                         nullptr, nullptr, d_status, rest, rest_bytes, stream);
   if (st != ASOT_OK) return st;
+  Nvtx range("asot e2e d2h");
   ASOT_CUDA(cudaMemcpyAsync(dist_host, d_D, (size_t)n_dist * n_dist * 4, cudaMemcpyDeviceToHost, s));
   ASOT_CUDA(cudaMemcpyAsync(status_host, d_status, 4, cudaMemcpyDeviceToHost, s));
   ASOT_CUDA(cudaStreamSynchronize(s));

@@ -48,10 +48,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Returns W_AS of one pair; `sm` is the warp's SMEM slice.  ok = false if a support is too large.
-template <int MAXS>
-__device__ double solve_pair(const float* __restrict__ ha, const float* __restrict__ hb, int K,
-                             const float* __restrict__ cost, uint8_t* sm, bool& ok) {
+// Exact OT on prefilled supports by successive shortest paths (one warp): sources 0..sa-1 with
+// supplies rem[0..sa), sinks 0..sb-1 with demands rem[MAXS..MAXS+sb) (both renormalised to unit
+// mass), cost C(i, j) (fp64).  `sm` is the warp's slice (Slice<MAXS> layout).  Returns <F, C>.
+template <int MAXS, class CostF>
+__device__ double ssp_warp(int sa, int sb, uint8_t* sm, CostF C) {
   constexpr int V = 2 * MAXS;
   const int lane = threadIdx.x & 31;
   double* F = (double*)sm;                                  // [MAXS][MAXS]
@@ -60,40 +61,6 @@ __device__ double solve_pair(const float* __restrict__ ha, const float* __restri
   double* rem = pot + V;                                    // [V]
   int* pred = (int*)(rem + V);                              // [V]
   int* done = pred + V;                                     // [V]
-  int* sidx = done + V;                                     // [V] anchor index of each node
-  // ---- supports (order-preserving compaction with ballots) and fp64 masses
-  int sa = 0, sb = 0;
-  double ma = 0.0, mb = 0.0;
-  for (int side = 0; side < 2; ++side) {
-    const float* h = side == 0 ? ha : hb;
-    int cnt = 0;
-    for (int k0 = 0; k0 < K; k0 += 32) {
-      const int k = k0 + lane;
-      const float w = k < K ? h[k] : 0.0f;
-      const bool nz = w > 0.0f;
-      const unsigned m = __ballot_sync(0xffffffffu, nz);
-      const int pos = cnt + __popc(m & ((1u << lane) - 1u));
-      if (nz && pos < MAXS) {
-        sidx[side * MAXS + pos] = k;
-        rem[side * MAXS + pos] = (double)w;
-      }
-      if (nz) {
-        if (side == 0) ma += (double)w;
-        else mb += (double)w;
-      }
-      cnt += __popc(m);
-    }
-    if (side == 0) sa = cnt;
-    else sb = cnt;
-  }
-  ok = sa <= MAXS && sb <= MAXS && sa > 0 && sb > 0;
-  if (!ok) return NAN;
-  ma = warp_sum(ma);
-  mb = warp_sum(mb);
-  __syncwarp();
-  for (int i = lane; i < sa; i += 32) rem[i] /= ma;                 // renormalise (R#14)
-  for (int j = lane; j < sb; j += 32) rem[MAXS + j] /= mb;
-  auto C = [&](int i, int j) { return (double)cost[(int64_t)sidx[i] * K + sidx[MAXS + j]]; };
   for (int e = lane; e < MAXS * MAXS; e += 32) F[e] = 0.0;
   // initial potentials: sources 0, sinks min_i C[i][j] (all forward reduced costs >= 0)
   for (int i = lane; i < sa; i += 32) pot[i] = 0.0;
@@ -204,6 +171,56 @@ __device__ double solve_pair(const float* __restrict__ ha, const float* __restri
     if (i < sa && j < sb && F[e] != 0.0) tot += F[e] * C(i, j);
   }
   return warp_sum(tot);
+}
+
+// Returns W_AS of one pair; `sm` is the warp's SMEM slice.  ok = false if a support is too large.
+template <int MAXS>
+__device__ double solve_pair(const float* __restrict__ ha, const float* __restrict__ hb, int K,
+                             const float* __restrict__ cost, uint8_t* sm, bool& ok) {
+  constexpr int V = 2 * MAXS;
+  const int lane = threadIdx.x & 31;
+  double* F = (double*)sm;                                  // [MAXS][MAXS]
+  double* dist = F + MAXS * MAXS;                           // [V]
+  double* pot = dist + V;                                   // [V]
+  double* rem = pot + V;                                    // [V]
+  int* pred = (int*)(rem + V);                              // [V]
+  int* done = pred + V;                                     // [V]
+  int* sidx = done + V;                                     // [V] anchor index of each node
+  // ---- supports (order-preserving compaction with ballots) and fp64 masses
+  int sa = 0, sb = 0;
+  double ma = 0.0, mb = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    const float* h = side == 0 ? ha : hb;
+    int cnt = 0;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      const int k = k0 + lane;
+      const float w = k < K ? h[k] : 0.0f;
+      const bool nz = w > 0.0f;
+      const unsigned m = __ballot_sync(0xffffffffu, nz);
+      const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+      if (nz && pos < MAXS) {
+        sidx[side * MAXS + pos] = k;
+        rem[side * MAXS + pos] = (double)w;
+      }
+      if (nz) {
+        if (side == 0) ma += (double)w;
+        else mb += (double)w;
+      }
+      cnt += __popc(m);
+    }
+    if (side == 0) sa = cnt;
+    else sb = cnt;
+  }
+  ok = sa <= MAXS && sb <= MAXS && sa > 0 && sb > 0;
+  if (!ok) return NAN;
+  ma = warp_sum(ma);
+  mb = warp_sum(mb);
+  __syncwarp();
+  for (int i = lane; i < sa; i += 32) rem[i] /= ma;                 // renormalise (R#14)
+  for (int j = lane; j < sb; j += 32) rem[MAXS + j] /= mb;
+  return ssp_warp<MAXS>(sa, sb, sm, [&](int i, int j) {
+    return (double)cost[(int64_t)sidx[i] * K + sidx[MAXS + j]];
+  });
 }
 
 template <int MAXS>
@@ -453,6 +470,90 @@ exact_pairs_block_kernel(const float* __restrict__ H, int64_t n_dist, int K, con
   (void)status;
 }
 
+// ---------------------------------------------------------------------------------------------
+// NEXT-3 bound checks: EXACT W_1 on the ORIGINAL point sets (Eq. (1)) with the Euclidean
+// ground metric d_E of Prop. 2 (R#7): C(r, c) = ||x_r - y_c||_2 in fp64 from the f32
+// points, marginals = the point weights renormalised in fp64 (R#14), solved by the same warp SSP
+// on the supports (points with weight > 0, <= 64 per side: graph-sized distributions such as c1 /
+// c2).  The n x m cost matrix lives next to the warp's flow matrix in shared memory.
+constexpr int kW1MaxS = 64;
+constexpr int kW1Warps = 3;
+constexpr size_t kW1SliceBytes = Slice<kW1MaxS>::kBytes + (size_t)kW1MaxS * kW1MaxS * 8;
+
+__global__ void w1_points_kernel(const float* __restrict__ points, const int64_t* __restrict__ offsets,
+                                 const float* __restrict__ weights, int64_t n_dist, int dim,
+                                 const int32_t* __restrict__ pi, const int32_t* __restrict__ pj,
+                                 int64_t n_pairs, double* __restrict__ out, uint32_t* status) {
+  extern __shared__ __align__(16) uint8_t w1_smem[];
+  constexpr int M = kW1MaxS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sm = w1_smem + (size_t)warp * kW1SliceBytes;
+  double* rem = (double*)sm + M * M + 2 * (2 * M);            // Slice layout: F, dist, pot, rem
+  int* sidx = (int*)(rem + 2 * M) + 2 * (2 * M);              // pred, done, sidx
+  double* Cm = (double*)(sm + Slice<M>::kBytes);              // [M][M]
+  for (int64_t q = (int64_t)blockIdx.x * kW1Warps + warp; q < n_pairs; q += (int64_t)gridDim.x * kW1Warps) {
+    const int i = pi[q], j = pj[q];
+    if (i < 0 || j < 0 || i >= n_dist || j >= n_dist) {
+      if (lane == 0) {
+        out[q] = NAN;
+        atomicOr(status, ASOT_FLAG_BAD_INDEX);
+      }
+      continue;
+    }
+    // supports: points with weight > 0, in point order (ballot compaction); fp64 masses
+    int cnt[2];
+    double mass[2] = {0.0, 0.0};
+    for (int side = 0; side < 2; ++side) {
+      const int64_t d = side == 0 ? i : j;
+      const int64_t b = offsets[d], e = offsets[d + 1];
+      int c = 0;
+      for (int64_t p0 = b; p0 < e; p0 += 32) {
+        const int64_t p = p0 + lane;
+        const float w = p < e ? weights[p] : 0.0f;
+        const unsigned m = __ballot_sync(0xffffffffu, w > 0.0f);
+        const int pos = c + __popc(m & ((1u << lane) - 1u));
+        if (w > 0.0f && pos < M) {
+          sidx[side * M + pos] = (int)(p - b);
+          rem[side * M + pos] = (double)w;
+        }
+        if (w > 0.0f) mass[side] += (double)w;
+        c += __popc(m);
+      }
+      cnt[side] = c;
+    }
+    const int sa = cnt[0], sb = cnt[1];
+    if (sa == 0 || sb == 0 || sa > M || sb > M) {
+      if (lane == 0) {
+        out[q] = NAN;
+        if (sa > M || sb > M) atomicOr(status, ASOT_FLAG_EXACT_TOO_LARGE);
+      }
+      __syncwarp();
+      continue;
+    }
+    const double ma = warp_sum(mass[0]), mb = warp_sum(mass[1]);
+    __syncwarp();
+    for (int r = lane; r < sa; r += 32) rem[r] /= ma;            // renormalise (R#14)
+    for (int c = lane; c < sb; c += 32) rem[M + c] /= mb;
+    const float* X = points + offsets[i] * dim;
+    const float* Y = points + offsets[j] * dim;
+    for (int e = lane; e < sa * sb; e += 32) {                   // C(r, c) = ||x_r - y_c||_2, fp64
+      const int r = e / sb, c = e % sb;
+      const float* x = X + (int64_t)sidx[r] * dim;
+      const float* y = Y + (int64_t)sidx[M + c] * dim;
+      double acc = 0.0;
+      for (int k = 0; k < dim; ++k) {
+        const double t = (double)x[k] - (double)y[k];
+        acc = fma(t, t, acc);
+      }
+      Cm[r * M + c] = sqrt(acc);
+    }
+    __syncwarp();
+    const double w1 = ssp_warp<M>(sa, sb, sm, [&](int r, int c) { return Cm[r * M + c]; });
+    if (lane == 0) out[q] = w1;
+    __syncwarp();
+  }
+}
+
 }  // namespace exact
 
 size_t exact_pairs_workspace_bytes(int64_t n_pairs, int K, int sms) {
@@ -476,6 +577,20 @@ cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const floa
   if (e != cudaSuccess) return e;
   exact::exact_pairs_block_kernel<<<(unsigned)sms, exact::kBlockThreads, smem, s>>>(
       H, n_dist, K, cost, pi, pj, n_pairs, out, pending, flow, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_w1_points(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist,
+                             int dim, const int32_t* pi, const int32_t* pj, int64_t n_pairs, double* out,
+                             uint32_t* status, int sms, cudaStream_t s) {
+  if (n_pairs <= 0) return cudaSuccess;
+  const size_t smem = (size_t)exact::kW1Warps * exact::kW1SliceBytes;
+  cudaError_t e = cudaFuncSetAttribute(exact::w1_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t grid = (n_pairs + exact::kW1Warps - 1) / exact::kW1Warps;
+  if (grid > (int64_t)sms * 4) grid = (int64_t)sms * 4;
+  exact::w1_points_kernel<<<(unsigned)grid, exact::kW1Warps * 32, smem, s>>>(points, offsets, weights, n_dist, dim,
+                                                                            pi, pj, n_pairs, out, status);
   return cudaGetLastError();
 }
 

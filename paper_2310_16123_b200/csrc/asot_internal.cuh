@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cfloat>
+
 #include "asot.h"
 
 namespace asot {
@@ -75,8 +77,11 @@ struct PairSink {
   float* mat;     // [n_dist, n_dist] or null (both triangles written)
   int64_t n_dist;
   uint32_t* status;
+  int32_t list;   // explicit pair list: an invalid entry is an argument error, not tile padding
 };
 
+// Invalid slots: tile padding (i >= j or j >= N) stores 0 in the packed vector; an explicit-list
+// entry with an index outside [0, N) stores NaN and raises ASOT_FLAG_BAD_INDEX.
 __device__ inline void write_result(const PairSink& out, int64_t s, bool valid, int i, int j, float d) {
   if (valid) {
     if (!isfinite(d)) atomicOr(out.status, ASOT_FLAG_NONFINITE_OUTPUT);
@@ -85,6 +90,9 @@ __device__ inline void write_result(const PairSink& out, int64_t s, bool valid, 
       out.mat[(int64_t)i * out.n_dist + j] = d;
       out.mat[(int64_t)j * out.n_dist + i] = d;
     }
+  } else if (out.list) {
+    atomicOr(out.status, ASOT_FLAG_BAD_INDEX);
+    if (out.vec) out.vec[s] = __int_as_float(0x7fc00000);
   } else if (out.vec) {
     out.vec[s] = 0.0f;
   }
@@ -110,11 +118,89 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return c;
 }
 
+// ---- the Sinkhorn divide x = m / D with SPEC's clamp + flag (R#12).
+// D is clamped into [FLT_MIN, 2^126] -- below, 1/D overflows; above, rcp.approx.ftz returns a
+// flushed subnormal -- and the clamp raises DENOM_CLAMPED when the anchor carries mass (m > 0).
+// A NaN D is left alone (it comes from non-finite inputs and surfaces as NONFINITE_OUTPUT).
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float div_clamped(float m, float den, bool& clamped) {
+  if (!(den >= FLT_MIN) && den == den) {
+    clamped |= m > 0.0f;
+    den = FLT_MIN;
+  } else if (den > 0x1p126f) {
+    clamped |= m > 0.0f;
+    den = 0x1p126f;
+  }
+  return m * rcp_ftz(den);   // m = 0 -> exactly 0 (R#11)
+}
+// The TF32 epilogues' divide over a thread's N (even) anchors of one chunk: o = the RNA-pre-
+// rounded TF32 bits of m / D, m = 0 -> exactly 0 (R#11), one MUFU per two anchors:
+//   p = D0 D1,  r = 1/p,  q = (D1 r, D0 r) = (1/D0, 1/D1),  x = m q.
+// The form is exact up to rounding whenever p lies in [2^-126, 2^126), where rcp.approx.ftz
+// returns a finite normal r.  p leaves that range once max(C_s)/eps exceeds ~44, so the fast
+// pass also tracks min / max of p over the chunk (3-input FMNMX on the products, off the
+// MUFU's dependency chain) and reports the thread as `bad`; the caller then reloads D from TMEM
+// (not yet overwritten) in sub-blocks of 8 and epi_div_fix8 replaces the bad thread's values by
+// per-anchor clamped reciprocals (S:62 clamp + flag).  Other threads keep their fast values, so
+// a pair's result never depends on the other pairs of its warp.
+__device__ __forceinline__ uint32_t tf32_rna_pre_bits(float x) { return __float_as_uint(x) + 0x1000u; }
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+template <int N>
+__device__ __forceinline__ bool epi_div_fast(const float* m, const uint32_t (&d)[N], uint32_t (&o)[N]) {
+  static_assert(N % 4 == 0, "chunk");
+  float lo = INFINITY, hi = 0.0f;
+#pragma unroll
+  for (int e = 0; e < N; e += 4) {
+    const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
+    const float d2 = __uint_as_float(d[e + 2]), d3 = __uint_as_float(d[e + 3]);
+    const float pa = d0 * d1, pb = d2 * d3;
+    const float ra = rcp_ftz(pa), rb = rcp_ftz(pb);
+    lo = fmin3(lo, pa, pb);
+    hi = fmax3(hi, pa, pb);
+    // q = (D1 r, D0 r) = (1/D0, 1/D1) first, then x = m q: no intermediate can underflow while
+    // the result is representable (m D1 could, when D0 and D1 lie far apart)
+    const float2 xa = fmul2(make_float2(m[e], m[e + 1]), fmul2(make_float2(d1, d0), make_float2(ra, ra)));
+    const float2 xb = fmul2(make_float2(m[e + 2], m[e + 3]), fmul2(make_float2(d3, d2), make_float2(rb, rb)));
+    o[e] = tf32_rna_pre_bits(xa.x);
+    o[e + 1] = tf32_rna_pre_bits(xa.y);
+    o[e + 2] = tf32_rna_pre_bits(xb.x);
+    o[e + 3] = tf32_rna_pre_bits(xb.y);
+  }
+  return !(lo >= 0x1p-126f && hi < 0x1p126f);
+}
+__device__ __forceinline__ void epi_div_fix8(const float* m, const uint32_t (&d)[8], uint32_t* o, bool& clamped) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) o[e] = tf32_rna_pre_bits(div_clamped(m[e], __uint_as_float(d[e]), clamped));
+}
+
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   float2 c;
   asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
       "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
       "sub.rn.f32x2 rc, ra, rb;\n\t"
+      "mov.b64 {%0, %1}, rc;\n\t}"
+      : "=f"(c.x), "=f"(c.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return c;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 c;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rc, ra, rb;\n\t"
       "mov.b64 {%0, %1}, rc;\n\t}"
       : "=f"(c.x), "=f"(c.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
@@ -153,6 +239,13 @@ cudaError_t launch_histograms(const int32_t* assign, const float* weights, const
                               float* const* peers = nullptr, int n_peers = 0, int64_t row_base = 0);
 int simt_kpad(int K);
 size_t exact_pairs_workspace_bytes(int64_t n_pairs, int K, int sms);
+cudaError_t launch_w1_points(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist,
+                             int dim, const int32_t* pi, const int32_t* pj, int64_t n_pairs, double* out,
+                             uint32_t* status, int sms, cudaStream_t s);
+cudaError_t launch_bound_terms(const float* points, const int64_t* offsets, int64_t n_dist, int dim,
+                               const float* anchors, int K, const int32_t* assign, const float* cost,
+                               const int32_t* pi, const int32_t* pj, int64_t n_pairs, double* l1,
+                               double* linf, double* prop2, uint32_t* status, int sms, cudaStream_t s);
 cudaError_t launch_exact_pairs(const float* H, int64_t n_dist, int K, const float* cost, const int32_t* pi,
                                const int32_t* pj, int64_t n_pairs, double* out, uint8_t* pending,
                                uint32_t* status, int sms, cudaStream_t s);

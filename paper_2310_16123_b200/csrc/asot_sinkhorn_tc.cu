@@ -277,6 +277,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     const uint32_t r0 = lane_off + (uint32_t)(2 * s * KP);   // this thread's lane of R0; R1 = r0 + KP
     const uint32_t bar_mma = bar_mma0 + 16 * s, bar_go = bar_go0 + 16 * s;
     uint32_t mma_par = 0;
+    bool clamped = false;   // a denominator left [FLT_MIN, 2^126] on an anchor with mass
     // chunk c of this slot's columns is ready: every thread of the slot stored its part
     auto go = [&](int c) {
       tmem_wait_st();
@@ -372,17 +373,19 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
                 }
               }
               tmem_wait_ld();
+              // x = m / D, one MUFU per two anchors while the sub-block's D lie in
+              // [2^-62, 2^62], else one clamped reciprocal each (S:62 clamp + flag); m = 0 gives
+              // exactly 0 (R#11).
               uint32_t o[SB];
+              const bool bad = epi_div_fast<SB>(m, d, o);
+              if (__builtin_expect(__any_sync(0xffffffffu, bad), 0)) {   // a product D0 D1 out of fp32 range (rare)
 #pragma unroll
-              for (int e = 0; e < SB; e += 2) {
-                // x = m / D for two anchors with one MUFU: r = 1/(D0 D1), m0/D0 = m0 D1 r,
-                // m1/D1 = m1 D0 r.  D > 0 by construction (padded K = 1, dummy marginals);
-                // m = 0 gives exactly 0 (R#11).
-                const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
-                const float r = rcp_approx(d0 * d1);
-                const float2 x = fmul2(fmul2(make_float2(m[e], m[e + 1]), make_float2(d1, d0)), make_float2(r, r));
-                o[e] = tf32_rna_pre(x.x);
-                o[e + 1] = tf32_rna_pre(x.y);
+                for (int s8 = 0; s8 < SB; s8 += 8) {
+                  uint32_t d8[8];
+                  tmem_ld8u(rd + c * CH + b0 + s8, d8);
+                  tmem_wait_ld();
+                  if (bad) epi_div_fix8(m + s8, d8, o + s8, clamped);
+                }
               }
               tmem_st_cols<SB>(rd + c * CH + b0, o);  // in place: the new scaling replaces D
             }
@@ -451,6 +454,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
       if (h == 0 && (!EX || tr * kTileSlots + p < n_pairs))
         write_result(out, tr * kTileSlots + p, valid, ii, jj, acc + rs[p]);
     }
+    if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
   }
   tc_fence_before();
   __syncthreads();
@@ -468,11 +472,15 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
                              int iters, cudaStream_t s, const int32_t* pi = nullptr,
                              const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr) {
   const size_t smem = Smem<KP>::kBytes;
+#ifdef ASOT_DEBUG_KERNELS   // diagnostic variants (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = pi != nullptr ? sinkhorn_tc_kernel<KP, 0, true>
             : dbg == 1 ? sinkhorn_tc_kernel<KP, 1, false> : dbg == 2 ? sinkhorn_tc_kernel<KP, 2, false>
             : dbg == 3 ? sinkhorn_tc_kernel<KP, 3, false> : dbg == 4 ? sinkhorn_tc_kernel<KP, 4, false>
             : sinkhorn_tc_kernel<KP, 0, false>;
+#else
+  auto kern = pi != nullptr ? sinkhorn_tc_kernel<KP, 0, true> : sinkhorn_tc_kernel<KP, 0, false>;
+#endif
   cudaError_t e = cudaFuncSetAttribute(kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -158,6 +158,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     if (threadIdx.x == 0) mbar_arrive_cluster(epi_remote0 + 8 * c);
   };
 
+  bool clamped = false;   // a denominator left [FLT_MIN, 2^126] on an anchor with mass
   for (int64_t b = (tile_begin >> 1) + (blockIdx.x >> 1); b < ((tile_end + 1) >> 1); b += gridDim.x >> 1) {
     const int64_t t = 2 * b + rank;          // this CTA's tile
     const bool t_in = t >= tile_begin && t < tile_end;
@@ -230,14 +231,18 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             tmem_ld16u(rd + c * kChunk, d);
             tmem_wait_ld();
             reg_fence16(d);
+            // x = m / D, one MUFU per two anchors; a product D0 D1 out of fp32 range (rare):
+            // reload D, per-anchor clamped reciprocals on that thread (S:62 clamp + flag)
             uint32_t o[16];
+            const bool bad = epi_div_fast<16>(mk, d, o);
+            if (__builtin_expect(__any_sync(0xffffffffu, bad), 0)) {   // a product D0 D1 out of fp32 range (rare)
 #pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
-              const float r = rcp_approx(d0 * d1);
-              const float2 x = fmul2(fmul2(make_float2(mk[e], mk[e + 1]), make_float2(d1, d0)), make_float2(r, r));
-              o[e] = tf32_rna_pre(x.x);
-              o[e + 1] = tf32_rna_pre(x.y);
+              for (int s8 = 0; s8 < 16; s8 += 8) {
+                uint32_t d8[8];
+                tmem_ld8u(rd + c * kChunk + s8, d8);
+                tmem_wait_ld();
+                if (bad) epi_div_fix8(mk + s8, d8, o + s8, clamped);
+              }
             }
             tmem_st16(rd + c * kChunk, o);  // in place: the new scaling replaces D
             if (c + 1 < NCH) load_m(f, c + 1);
@@ -344,6 +349,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       write_result(out, (t - tile_begin) * kTileSlots + ps, valid, ii, jj,
                    red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
   }
+  if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
   tc_fence_before();
   cluster_sync();
   clock_probe(g_tc2_clock, 1);
@@ -382,10 +388,14 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
                                 cudaStream_t s) {
   if (tile_end <= tile_begin) return cudaSuccess;
+#ifdef ASOT_DEBUG_KERNELS   // diagnostic variants (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = dbg == 1 ? tc2::sinkhorn_tc2_kernel<1> : dbg == 2 ? tc2::sinkhorn_tc2_kernel<2>
             : dbg == 3 ? tc2::sinkhorn_tc2_kernel<3> : dbg == 4 ? tc2::sinkhorn_tc2_kernel<4>
             : tc2::sinkhorn_tc2_kernel<0>;
+#else
+  auto kern = tc2::sinkhorn_tc2_kernel<0>;
+#endif
   const size_t smem = tc2::Smem::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

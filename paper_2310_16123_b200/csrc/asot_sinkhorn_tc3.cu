@@ -332,12 +332,8 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              float den = __uint_as_float(dv[e]);
-              if (den < FLT_MIN) {          // S:62 clamp + flag (cannot happen for real rows)
-                clamped |= mm[e] > 0.0f;
-                den = FLT_MIN;
-              }
-              const float x = mm[e] * rcp_approx(den);     // m = 0 -> exactly 0 (R#11)
+              // S:62 clamp into [FLT_MIN, 2^126] + flag; m = 0 -> exactly 0 (R#11)
+              const float x = div_clamped(mm[e], __uint_as_float(dv[e]), clamped);
               const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;  // RNA to TF32
               hi[e] = xh;
               lo[e] = __float_as_uint(x - __uint_as_float(xh));
@@ -449,9 +445,13 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
                              const float* gc, int iters, cudaStream_t s, const int32_t* pi = nullptr,
                              const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr) {
   const size_t smem = Smem<KP>::kBytes;
+#ifdef ASOT_DEBUG_KERNELS   // diagnostic variant (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = pi != nullptr ? sinkhorn_tc3_kernel<KP, 0, true>
             : dbg == 3 ? sinkhorn_tc3_kernel<KP, 3, false> : sinkhorn_tc3_kernel<KP, 0, false>;
+#else
+  auto kern = pi != nullptr ? sinkhorn_tc3_kernel<KP, 0, true> : sinkhorn_tc3_kernel<KP, 0, false>;
+#endif
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

@@ -228,6 +228,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t free_remote = mapa(bar_free, 0);
     uint32_t done_par = 0;
+    bool clamped = false;   // a denominator left [FLT_MIN, 2^126] on an anchor with mass
     for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
       const int64_t t = 2 * b + rank;
       const bool t_in = t >= tile_begin && t < tile_end;
@@ -308,14 +309,18 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                   const float4 q4 = mq[c & 1][e];
                   m[4 * e] = q4.x; m[4 * e + 1] = q4.y; m[4 * e + 2] = q4.z; m[4 * e + 3] = q4.w;
                 }
+                // x = m / D (one MUFU per two anchors; S:62 clamp + flag outside [2^-62, 2^62];
+                // m = 0 -> exactly 0, R#11)
                 uint32_t o[16];
+                const bool bad = epi_div_fast<16>(m, *reinterpret_cast<const uint32_t(*)[16]>(dc), o);
+                if (__builtin_expect(__any_sync(0xffffffffu, bad), 0)) {   // a product D0 D1 out of fp32 range (rare)
 #pragma unroll
-                for (int e = 0; e < 16; e += 2) {
-                  const float d0 = __uint_as_float(dc[e]), d1 = __uint_as_float(dc[e + 1]);
-                  const float r = rcp_approx(d0 * d1);
-                  const float2 x = fmul2(fmul2(make_float2(m[e], m[e + 1]), make_float2(d1, d0)), make_float2(r, r));
-                  o[e] = tf32_rna_pre(x.x);
-                  o[e + 1] = tf32_rna_pre(x.y);
+                  for (int s8 = 0; s8 < 16; s8 += 8) {
+                    uint32_t d8[8];
+                    tmem_ld8u(tcol + c * 16 + s8, d8);
+                    tmem_wait_ld();
+                    if (bad) epi_div_fix8(m + s8, d8, o + s8, clamped);
+                  }
                 }
 #pragma unroll
                 for (int e = 0; e < 16; e += 4) stg128(xout + x_offset(p, k0 + e), o[e], o[e + 1], o[e + 2], o[e + 3]);
@@ -350,6 +355,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                      red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
       named_bar_sync(1, kEpiThreads);  // red reused by the next tile
     }
+    if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
   }
   tc_fence_before();
   cluster_sync();
@@ -415,9 +421,13 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dis
   pad_marginals_kernel<KP><<<512, 256, 0, s>>>(H, n_dist, K, Hp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+#ifdef ASOT_DEBUG_KERNELS   // diagnostic variants (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
   auto kern = dbg == 1 ? sinkhorn_tc4_kernel<KP, 1> : dbg == 2 ? sinkhorn_tc4_kernel<KP, 2>
             : dbg == 3 ? sinkhorn_tc4_kernel<KP, 3> : sinkhorn_tc4_kernel<KP, 0>;
+#else
+  auto kern = sinkhorn_tc4_kernel<KP, 0>;
+#endif
   const size_t smem = Smem::kBytes;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

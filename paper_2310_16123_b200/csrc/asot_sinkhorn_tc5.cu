@@ -300,12 +300,8 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                 const float mm[4] = {mq.x, mq.y, mq.z, mq.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                  float den = __uint_as_float(d[e + u]);
-                  if (den < FLT_MIN) {       // S:62 clamp + flag (as the fp32 CUDA-core kernel)
-                    clamped |= mm[u] > 0.0f;
-                    den = FLT_MIN;
-                  }
-                  const float x = mm[u] * rcp_approx(den);   // m = 0 -> exactly 0 (R#11)
+                  // S:62 clamp into [FLT_MIN, 2^126] + flag; m = 0 -> exactly 0 (R#11)
+                  const float x = div_clamped(mm[u], __uint_as_float(d[e + u]), clamped);
                   if (SPLIT == 3) {
                     const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
                     hi[e + u] = xh;

@@ -3,7 +3,7 @@
 //
 // Same recurrence and conventions as the fp32 CUDA-core kernel (asot_sinkhorn_simt.cu; P:179-183,
 // S:61-62, R#4, R#5, R#11, R#12): v0 = 1, exactly L iterations of u = a / (K v), v = b / (K^T u)
-// with 0/x = 0 and denominators below FLT_MIN clamped and flagged, then
+// with 0/x = 0 and denominators clamped into [FLT_MIN, 2^126] and flagged, then
 // d = sum_c v_c ((K (.) C_s) u)_c with the last v-update fused (K and C_s symmetric).
 //
 // Why a separate kernel: at K < 32 one pair's whole state is K floats, so the batched GEMM form
@@ -15,7 +15,9 @@
 // reciprocal per lane -- ~260 cycles, with thousands of pairs in flight across all SMs.  The dot
 // products run in the CUDA-core kernel's order (c = 0 .. K-1, fmaf from 0); the divide is
 // m * rcp.approx(den) (<= 1 ulp, as in the tensor-core epilogues) instead of the IEEE divide,
-// which alone took a third of the time at c1.
+// which alone took a third of the time at c1.  (Above 2^126 the approximate reciprocal would be
+// flushed to 0 where the IEEE divide returns a subnormal: such denominators are clamped to 2^126
+// and flagged, as in every tensor-core kernel.)
 #include <cfloat>
 
 #include "asot_internal.cuh"
@@ -51,13 +53,8 @@ sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
 
   bool clamped = false;
   auto divide = [&](float m, float den) {   // 0/x = 0 (R#11); clamp + flag (R#12)
-    if (!(den >= FLT_MIN)) {
-      clamped |= m > 0.0f;
-      den = FLT_MIN;
-    }
-    float rc;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));   // den >= FLT_MIN: no FTZ effect
-    return m > 0.0f ? m * rc : 0.0f;
+    // den clamped into [FLT_MIN, 2^126]: rcp.approx.ftz then never overflows or flushes
+    return m > 0.0f ? div_clamped(m, den, clamped) : 0.0f;
   };
   // y = sum_c col[c] * x_c over the group's shared vector, c = 0 .. LP-1 in order
   auto dot = [&](const float* xg, const float (&col)[LP]) {

@@ -114,6 +114,9 @@ def test_host_argument_errors(lib):
     rc = lib.asot_pairwise_sinkhorn(fake, 10, 16, fake, 1.0, 0.05, 10, 1, fake, fake, 5, fake, fake,
                                     fake, 16, None)
     assert rc == 6                                         # workspace too small
+    rc = lib.asot_pairwise_sinkhorn(fake, 10, 16, fake, 1.0, 0.05, 10, 1, None, None, 0, None, fake,
+                                    None, 0, None)
+    assert rc == 0                                         # empty pair list: nothing to do
     rc = lib.asot_distance_matrix(None, None, None, None, 10, 4, None, 16, fake, 1.0, 0.05, 10, 1,
                                   None, 0, 10**6, fake, None, None, None, fake, fake, 1 << 20, None)
     assert rc == 1 and b"tile range" in lib.asot_last_error()
@@ -134,3 +137,25 @@ def test_product_path_has_no_oracle_or_cpu_fallback():
             src = open(os.path.join(pkg, name)).read()
             assert "oracle" not in src.replace("never imports oracle", ""), name
             assert "torch.exp" not in src and "np.exp" not in src and "matmul" not in src, name
+
+
+def test_binding_rejects_malformed_pair_lists():
+    """The binding validates pair lists and shapes before any device call: int64 index
+    tensors (the ABI reads i32), unequal lengths, a cost of the wrong size, non-f32 histograms."""
+    import torch
+    import paper_2310_16123_b200 as asot
+    H = torch.zeros(10, 16)
+    C = torch.zeros(16, 16)
+    i32 = torch.zeros(5, dtype=torch.int32)
+    with pytest.raises(ValueError, match="int32"):
+        asot.pairwise_sinkhorn(H, C, 0.05, 10, torch.zeros(5, dtype=torch.int64), i32)
+    with pytest.raises(ValueError, match="entries"):
+        asot.pairwise_sinkhorn(H, C, 0.05, 10, i32, torch.zeros(4, dtype=torch.int32))
+    with pytest.raises(ValueError, match="cost"):
+        asot.pairwise_sinkhorn(H, torch.zeros(15, 15), 0.05, 10, i32, i32)
+    with pytest.raises(ValueError, match="float32"):
+        asot.pairwise_sinkhorn(H.double(), C, 0.05, 10, i32, i32)
+    with pytest.raises(ValueError, match="int32"):
+        asot.exact_asot_pairs(H, C, i32.long(), i32)
+    with pytest.raises(ValueError, match="cuda"):   # well-formed CPU tensors: no CPU path
+        asot.pairwise_sinkhorn(H, C, 0.05, 10, i32, i32)

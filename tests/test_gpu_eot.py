@@ -28,8 +28,8 @@ def test_eot_pairs_vs_oracle(asot, cfg, n, iters):
     inp = make_inputs(cfg, n_dist=n)
     s = anchor_sqdist_scale(inp.anchors)
     pi, pj = O.upper_pairs(n)
-    pi = np.concatenate([pi, pj[:5]]).astype(np.int32)      # + a few reversed pairs
-    pj = np.concatenate([pj, pi[:5]]).astype(np.int32)
+    pi, pj = (np.concatenate([pi, pj[:5]]).astype(np.int32),   # + a few reversed pairs
+              np.concatenate([pj, pi[:5]]).astype(np.int32))
     st = asot.asot.new_status()
     d = asot.eot_pairs(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(pi), dev(pj),
                        float(inp.eps), iters, float(s), offsets_host=inp.offsets, status=st)

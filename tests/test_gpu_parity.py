@@ -152,7 +152,7 @@ def test_pairwise_explicit_pairs(asot, cfg, n, npairs, prec):
 def test_pairwise_resident_pair_mode(asot, K):
     """TF32 pair lists with K <= 128 run the resident 1-SM kernel in pair-list mode (2 and 4 slots
     per CTA): every i < j entry equals the tile path's value for that pair bitwise (same kernel
-    arithmetic), invalid entries (out-of-range indices) give 0, and all values (reversed
+    arithmetic), invalid entries (out-of-range indices) give NaN and raise FLAG_BAD_INDEX, and all values (reversed
     orientations included) are within the TF32 bar of the oracle."""
     inp = make_inputs("c2", n_dist=45)
     A = np.ascontiguousarray(inp.anchors[:K])
@@ -173,7 +173,10 @@ def test_pairwise_resident_pair_mode(asot, K):
     d = d.cpu().numpy()
     Dn = D.cpu().numpy()
     ok = (pi >= 0) & (pj >= 0) & (pi < inp.n_dist) & (pj < inp.n_dist)
-    assert np.all(d[~ok] == 0.0)
+    assert np.all(np.isnan(d[~ok])) and np.all(np.isfinite(d[ok]))
+    assert int(st.item()) == asot.asot.FLAG_BAD_INDEX
+    with pytest.raises(ValueError):
+        asot.check_status(st)
     fwd = ok & (pi < pj)   # the tile path computes i < j with a = H[i] on the u side (R#10)
     np.testing.assert_array_equal(d[fwd], Dn[pi[fwd], pj[fwd]])
     c_o, _ = O.pair_costs(H.cpu().numpy().astype(np.float64), C.astype(np.float64), inp.eps, inp.iters,
@@ -423,7 +426,7 @@ np.save(sys.argv[1], d.cpu().numpy()); np.save(sys.argv[2], H.cpu().numpy()); np
     C = ((A[:, None, :] - A[None, :, :]) ** 2).sum(-1)
     C = (C / C.max()).astype(np.float32)
     ok = (pi >= 0) & (pj >= 0)
-    assert np.all(d_tc[~ok] == 0.0) and np.all(d_simt[~ok] == 0.0)
+    assert np.all(np.isnan(d_tc[~ok])) and np.all(np.isnan(d_simt[~ok]))
     c_o, _ = O.pair_costs(H.astype(np.float64), C.astype(np.float64), inp.eps, inp.iters,
                           pi[ok].astype(np.int64), pj[ok].astype(np.int64))
     assert rel_err(d_tc[ok], c_o, 1.0).max() <= TOL[0]      # ASOT_PREC_FP32

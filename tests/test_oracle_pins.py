@@ -219,6 +219,28 @@ def test_sinkhorn_invariants():
     np.testing.assert_allclose(cs, cl, rtol=1e-9)
 
 
+def test_sinkhorn_underflow_floor_branch():
+    """S:62 / S:79 (R#12): a denominator below underflow_floor = 1e-300 is clamped to the floor and
+    flagged.  K = 2, C = [[0, 1], [1, 0]], a = 1e-200 e_0, b = e_1, G off-diagonal g, v0 = 1.
+    Hand computation of one iteration: G v0 = (1 + g, 1 + g) -> u = (1e-200 / (1 + g), 0);
+    G^T u = (u_0, g u_0).
+      g = 1e-120: (G^T u)_1 = 1e-320 < 1e-300 -> clamped: v_1 = 1 / 1e-300 (unclamped it would be
+        1e320 = inf in fp64), flag set, cost = u_0 g C_01 v_1 = 1e-20;
+      g = 1e-90: (G^T u)_1 = 1e-290 >= floor -> v_1 = 1 / (g u_0), no flag, and the cost is the
+        one-hot closed form C_01 = 1 (the plan moves all of b's mass across)."""
+    C = np.array([[0.0, 1.0], [1.0, 0.0]])
+    A = np.array([[1e-200], [0.0]])
+    B = np.array([[0.0], [1.0]])
+    for g, flagged, v1, cost in ((1e-120, True, 1e300, 1e-20), (1e-90, False, 1e290, 1.0)):
+        G = np.array([[1.0, g], [g, 1.0]])
+        c, U, V, fl = O.sinkhorn_batch(A, B, G, G * C, 1)
+        assert bool(fl[0]) is flagged
+        assert V[0, 0] == 0.0                      # b_0 = 0 -> v_0 = 0 (0/x = 0, R#11)
+        assert math.isclose(V[1, 0], v1, rel_tol=1e-12)
+        assert np.isfinite(c[0]) and math.isclose(c[0], cost, rel_tol=1e-12)
+    assert O.UNDERFLOW_FLOOR == 1e-300             # S:79 default
+
+
 def test_batched_equals_per_pair():
     """batched column p == single-pair Sinkhorn on (a_p, b_p)."""
     rng = np.random.default_rng(5)

@@ -1,7 +1,7 @@
 """Summarise ncu artefacts into profiles/ (run here, on the CPU box, after a gpurun call).
 
   python tools/summarize_ncu.py launches <launches.csv> <out.md>
-  python tools/summarize_ncu.py full <prof.ncu-rep> <out.json> [traffic-key]
+  python tools/summarize_ncu.py full <prof.ncu-rep> <out.json> [summary-key, e.g. c3:tf32]
 """
 import collections
 import csv
@@ -82,10 +82,25 @@ def full(rep, out_json, traffic_key=None):
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))
     if traffic_key:
-        tpath = os.path.join(ROOT, 'profiles', 'ncu_traffic.json')
-        t = json.load(open(tpath)) if os.path.exists(tpath) else {}
-        t[traffic_key] = traffic
-        json.dump(t, open(tpath, 'w'), indent=1)
+        # profiles/ncu_summary.json: what bench.py quotes next to its live roofline (per launch)
+        spath = os.path.join(ROOT, 'profiles', 'ncu_summary.json')
+        t = json.load(open(spath)) if os.path.exists(spath) else {}
+
+        def pct(k):
+            return float(v[h.index(k)].replace(',', '')) if k in h else None
+        t[traffic_key] = {
+            'source': os.path.relpath(out_json, ROOT),
+            'kernel': out['kernel'][:120] if out['kernel'] else None,
+            'gpu_time_ms': num('gpu__time_duration.sum') / 1e6 if u[h.index('gpu__time_duration.sum')] == 'nsecond'
+            else num('gpu__time_duration.sum') * {'usecond': 1e-3, 'msecond': 1.0, 'second': 1e3}.get(
+                u[h.index('gpu__time_duration.sum')], 1.0),
+            'dram_bytes_per_launch': traffic,
+            'tensor_pipe_active_pct': pct('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'),
+            'fma_pipe_active_pct': pct('sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active'),
+            'issue_active_pct': pct('sm__issue_active.avg.pct_of_peak_sustained_elapsed'),
+            'sm_clock_hz': num('sm__cycles_elapsed.avg.per_second') if 'sm__cycles_elapsed.avg.per_second' in h else None,
+        }
+        json.dump(t, open(spath, 'w'), indent=1)
 
 
 if __name__ == '__main__':
