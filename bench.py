@@ -567,7 +567,13 @@ def main():
     pairs_per_launch = P if world == 1 else -(-P // world)
     peaks = measured_peaks()
     kind = asot.asot.sinkhorn_kernel_kind(inp.n_anchors, prec)
-    if kind in (3, 5):
+    # hardware MAC rate of the kernel's MMA kind (per SM per clock) and MMAs per algorithmic product
+    mac_clk, per_product = {10: (4096, 3), 3: (2048, 3), 5: (2048, 3)}.get(kind, (2048, 1))
+    if kind == 10:
+        peak = peaks["bf16_tflops"] / 3
+        bound, peak_note = "tensor", (f"BF16x3: dense BF16 ({peaks['_source']} {peaks['bf16_tflops']} TFLOP/s "
+                                      f"burst) / 3 MMAs per algorithmic product")
+    elif kind in (3, 5):
         peak = peaks["bf16_tflops"] * TF32_OVER_BF16 / 3
         bound, peak_note = "tensor", (f"3xTF32: dense TF32 ({peaks['_source']} bf16 {peaks['bf16_tflops']} "
                                       f"TFLOP/s burst x 1.1/2.25) / 3 MMAs per algorithmic product")
@@ -601,12 +607,12 @@ def main():
     if bound == "tensor" and rank == 0:
         ct = cublas_tf32_tflops(dev)
         roofline["cublas_tf32_measured_tflops"] = ct
-        roofline["frac_of_cublas_tf32"] = achieved / (ct / (3 if kind in (3, 5) else 1))
+        roofline["frac_of_cublas_tf32"] = achieved / (ct / (3 if kind in (3, 5) else 1)) if kind != 10 else None
     if bound == "tensor":
         # context: the hardware's nominal dense TF32 rate (2048 MAC/clk/SM, tools/cg2_rate.cu) at the
         # median SM clock sampled during the timed region (3xTF32: one third of it)
         mhz = (clk or {}).get("sm_mhz") or 1965.0
-        nominal = 2048 * 2 * 148 * mhz * 1e6 / 1e12 / (3 if kind in (3, 5) else 1)
+        nominal = mac_clk * 2 * 148 * mhz * 1e6 / 1e12 / per_product
         roofline["nominal_peak_at_clock"] = nominal
         roofline["frac_of_nominal"] = achieved / nominal
         # the clock the last timed launch actually ran at (in-kernel %clock64 / %globaltimer
@@ -616,7 +622,7 @@ def main():
         except Exception:  # noqa: BLE001 -- kind without a probe
             emhz = None
         if emhz:
-            enominal = 2048 * 2 * 148 * emhz * 1e6 / 1e12 / (3 if kind in (3, 5) else 1)
+            enominal = mac_clk * 2 * 148 * emhz * 1e6 / 1e12 / per_product
             roofline["effective_sm_mhz"] = emhz
             roofline["nominal_peak_at_effective_clock"] = enominal
             roofline["frac_of_nominal_effective"] = achieved / enominal
@@ -896,7 +902,8 @@ def main():
             "metric": baseline_metric(), "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind in (3, 5) else "f32"),
+            "dtype": "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind in (3, 5) else
+                                                      "f32 (bf16x3)" if kind == 10 else "f32"),
             "data": "synthetic",
             "config": workload_config(inp, args, world),
             "result_exchange": exchange_note[0],

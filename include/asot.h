@@ -59,7 +59,8 @@ typedef enum {
 } asot_status;
 
 typedef enum {
-  ASOT_PREC_FP32 = 0, /* fp32-accurate: 3xTF32 tcgen05 for 32 <= K <= 1024, fp32 CUDA cores
+  ASOT_PREC_FP32 = 0, /* fp32-accurate: 3xTF32 tcgen05 for 32 <= K <= 128 and 256 < K <= 1024,
+                         BF16x3 tcgen05 for 128 < K <= 256 (tile path), fp32 CUDA cores
                          (lane per anchor) for K < 32; target rel. err <= 1e-4              */
   ASOT_PREC_TF32 = 1  /* tcgen05 kind::tf32 MMA (RNA-rounded G and U/V, fp32 accumulate):
                          target rel. err <= 2e-3; 32 <= K <= 1024 runs on tcgen05
@@ -320,8 +321,9 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
  * 1 = TF32 1-SM resident (K <= 128), 2 = TF32 CTA pair (K <= 256), 3 = 3xTF32 fp32-accurate
  * 1-SM resident (ASOT_PREC_FP32 with 32 <= K <= 128), 4 = TF32 CTA-pair
  * streamed (256 < K <= 1024, K padded to 512 or 1024),
- * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 128 < K <= 1024),
- * 9 = fp32 lane-per-anchor CUDA-core kernel (every request with K < 32).
+ * 5 = 3xTF32 fp32-accurate CTA-pair streamed (ASOT_PREC_FP32, 256 < K <= 1024),
+ * 9 = fp32 lane-per-anchor CUDA-core kernel (every request with K < 32),
+ * 10 = BF16x3 fp32-accurate CTA-pair resident (ASOT_PREC_FP32, 128 < K <= 256).
  * (Pair lists: K <= 128 the 1-SM kernels' pair-list modes, else the streamed kernel's.) */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
 

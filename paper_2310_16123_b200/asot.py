@@ -115,7 +115,8 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 6: "sinkhorn_tc5_kernel (TF32 one-pass, streamed GEMM form, pair-list mode, CTA pair)",
                 7: "sinkhorn_tc_kernel (TF32, 1 SM, M=128, pair-list mode)",
                 8: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128, pair-list mode)",
-                9: "sinkhorn_warp_kernel (fp32 CUDA cores, lane per anchor, K < 32)"}
+                9: "sinkhorn_warp_kernel (fp32 CUDA cores, lane per anchor, K < 32)",
+                10: "sinkhorn_tc6_kernel (BF16x3 fp32-accurate, resident, CTA pair, cta_group::2, M=256)"}
 
 
 def sinkhorn_kernel_kind(n_anchors: int, precision: int) -> int:

@@ -85,7 +85,8 @@ int tc_kind(int32_t K, asot_precision prec) {
   // every SM busy where 128-pair tensor-core tiles leave c1 on 16 SMs (latency-bound)
   if (K < kMinTcAnchors) return K >= 1 && (prec == ASOT_PREC_FP32 || prec == ASOT_PREC_TF32) ? 9 : 0;
   if (prec == ASOT_PREC_FP32)
-    return asot::sinkhorn_tc3_supported(K) ? 3 : asot::sinkhorn_tc5_supported(K) ? 5 : 0;
+    return asot::sinkhorn_tc3_supported(K) ? 3 : asot::sinkhorn_tc6_supported(K) ? 10
+         : asot::sinkhorn_tc5_supported(K) ? 5 : 0;
   if (prec != ASOT_PREC_TF32) return 0;
   if (asot::sinkhorn_tc_supported(K)) return 1;
   if (asot::sinkhorn_tc2_supported(K)) return 2;
@@ -138,6 +139,9 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
   } else if (kind == 2) {
     b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
     b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc2_image_bytes());
+  } else if (kind == 10) {   // BF16 hi / lo images of K and K (.) C_s, both ranks
+    b.g_img = (uint32_t*)cv.take(asot::sinkhorn_tc6_image_bytes());
+    b.gc_img = (uint32_t*)cv.take(asot::sinkhorn_tc6_image_bytes());
   } else if (kind == 1 || kind == 7) {
     const size_t kp = (size_t)asot::kpad32(K);
     b.g_img = (uint32_t*)cv.take(kp * kp * 4);
@@ -212,6 +216,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc4(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc2(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
+  } else if (kind == 10) {
+    ASOT_LAUNCH(asot::launch_gibbs_prep_tc6(cost, K, eps, (uint8_t*)gb.g_img, (uint8_t*)gb.gc_img, s));
   } else if (kind == 3 || kind == 8) {
     ASOT_LAUNCH(asot::launch_gibbs_prep_tc3(cost, K, eps, gb.g_img, gb.gc_img, gb.GC, s));
   } else if (kind == 1 || kind == 7) {
@@ -236,6 +242,9 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                                           (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink, H, K,
+                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
+  } else if (kind == 10) {
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc6(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
   } else if (kind == 1) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
@@ -301,6 +310,7 @@ asot_status asot_profile_clock(int32_t kind, double* sm_mhz) {
     case 3: case 8: e = asot::read_kernel_clock_tc3(c); break;
     case 4: e = asot::read_kernel_clock_tc4(c); break;
     case 5: case 6: e = asot::read_kernel_clock_tc5(c); break;
+    case 10: e = asot::read_kernel_clock_tc6(c); break;
     default: return fail(ASOT_ERR_INVALID_ARGUMENT, "no clock probe for this kernel kind");
   }
   ASOT_CUDA(e);
@@ -316,7 +326,8 @@ int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {
 
 asot_precision asot_effective_precision(int32_t n_anchors, asot_precision requested) {
   const int kind = tc_kind(n_anchors, requested);
-  return kind == 0 || kind == 3 || kind == 5 || kind == 9 ? ASOT_PREC_FP32 : ASOT_PREC_TF32;   // (6: TF32)
+  return kind == 0 || kind == 3 || kind == 5 || kind == 9 || kind == 10 ? ASOT_PREC_FP32
+                                                                        : ASOT_PREC_TF32;   // (6: TF32)
 }
 
 static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,

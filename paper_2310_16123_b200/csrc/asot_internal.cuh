@@ -349,6 +349,15 @@ __device__ __forceinline__ void clock_probe(long long* p, int at_end) {
 }
 cudaError_t read_kernel_clock_tc(long long* host4);
 cudaError_t read_kernel_clock_tc2(long long* host4);
+// BF16x3 fp32-accurate CTA-pair resident kernel (128 < K <= 256): asot_sinkhorn_tc6.cu
+bool sinkhorn_tc6_supported(int K);
+size_t sinkhorn_tc6_image_bytes();
+cudaError_t launch_gibbs_prep_tc6(const float* cost, int K, float eps, uint8_t* g_img, uint8_t* gc_img,
+                                  cudaStream_t s);
+cudaError_t launch_sinkhorn_tc6(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
+                                const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
+                                cudaStream_t s);
+cudaError_t read_kernel_clock_tc6(long long* host4);
 cudaError_t read_kernel_clock_tc3(long long* host4);
 cudaError_t read_kernel_clock_tc4(long long* host4);
 cudaError_t read_kernel_clock_tc5(long long* host4);

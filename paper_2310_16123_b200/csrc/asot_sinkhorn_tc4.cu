@@ -5,8 +5,9 @@
 // phase is a GEMM  D[256 pairs x 1024] = X[256 x 1024] . K[1024 x 1024]  per CTA pair
 // (tcgen05.mma.cta_group::2.kind::tf32, M = 256, N = 256 per instruction, both operands from
 // SMEM) with the divide fused into the epilogue:
-//   - X (the current scaling, TF32 bits in the K-major SW128 operand layout) lives in a
-//     per-CTA ping-pong buffer in global memory (L2 / HBM); K and K (.) C_s live in global
+//   - X (the current scaling, TF32 bits in the no-swizzle K-major operand layout) lives in
+//     per-CTA buffers in global memory (L2-resident: a rotation over three half-buffers at
+//     K = 1024, see xhalf); K and K (.) C_s live in global
 //     images pre-arranged so each (K-chunk, N-half) operand slice is one contiguous block;
 //   - a producer warp streams 48 KB stages (A: 128 pairs x 32 anchors of X; B: this CTA's 256
 //     output anchors x 32) with TMA bulk copies into a 4-stage mbarrier pipeline; the leader's
@@ -144,6 +145,22 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int phases = 2 * iters + 1;
+  // Where half h (anchors [512 h, 512 h + 512)) of X_f, the input of phase f, lives.  KP = 512:
+  // ping-pong of whole buffers.  KP = 1024: a rotation over three half-buffers -- pass 0's
+  // epilogue writes X_{f+1} half 0 into the third buffer while pass 1 still reads X_f; pass 1's
+  // epilogue (after its MMAs completed) writes X_{f+1} half 1 over X_f half 0 -- so the working
+  // set is 3 x 256 KB per CTA (111 MB over 148 CTAs: L2-resident) instead of 4 x 256 KB
+  // (148 MB, spilling to HBM).  The last phase's half 1 goes to a fourth half-buffer: the cost
+  // phase reads u_L (X_{2L-1}) next to v_L (X_{2L}).
+  auto xhalf = [&](int f, int h) -> uint8_t* {
+    if constexpr (NH == 1) {
+      return xb + (f & 1) * kXBytes;
+    } else {
+      const int idx = (f == phases - 1 && h == 1) ? 3 : (2 * f + h) % 3;
+      return xb + (size_t)idx * (kXBytes / 2);
+    }
+  };
+  constexpr int kHalfChunks = kKC / NH;   // 32-anchor chunks per half-buffer
   // 32-anchor input chunks holding real anchors: padded chunks (x = 0 there) are neither loaded
   // nor multiplied (K = 384: 12 of 16, K = 768: 24 of 32)
   const int kcn = (K + 31) / 32 < kKC ? (K + 31) / 32 : kKC;
@@ -155,7 +172,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       uint32_t xr_par = 0;
       for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
         for (int f = 0; f < phases; ++f) {
-          const uint8_t* xin = xb + (f & 1) * kXBytes;
+
           const uint8_t* img = (f < phases - 1 ? g_img : gc_img) + rank * kImgRankBytes;
           mbar_wait(bar_xr, xr_par);  // X_in fully written (previous phase / tile init)
           xr_par ^= 1u;
@@ -167,7 +184,8 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
               if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && kc == 0 && 2 * f + nh < 256)
                 g_tc4_trace[4][2 * f + nh] = clock64();
               mbar_expect_tx(bar_full + 8 * s, kStageBytes);
-              bulk_g2s(stage0 + s * kStageBytes, xin + kc * kAChunk, kAChunk, bar_full + 8 * s);
+              bulk_g2s(stage0 + s * kStageBytes, xhalf(f, kc / kHalfChunks) + (kc % kHalfChunks) * kAChunk, kAChunk,
+                       bar_full + 8 * s);
               bulk_g2s(stage0 + s * kStageBytes + kAChunk, img + (size_t)(nh * kKC + kc) * kBChunk, kBChunk,
                        bar_full + 8 * s);
             }
@@ -247,7 +265,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         uint32_t v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = (k + e < K) ? 0x3f800000u : 0u;
-        stg128(xb + x_offset(p, k), v[0], v[1], v[2], v[3]);
+        stg128(xhalf(0, k / 512) + x_offset(p, k % 512), v[0], v[1], v[2], v[3]);
       }
       fence_proxy_async_global();
       named_bar_sync(1, kEpiThreads);
@@ -255,8 +273,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       float acc = 0.0f;
       for (int f = 0; f < phases; ++f) {
         const bool cost_phase = f == phases - 1;
-        uint8_t* xout = xb + ((f + 1) & 1) * kXBytes;
-        const uint8_t* ubuf = xb + kXBytes;  // u_L (read in the cost phase only)
+
         // u-update: a = H[i] (8 rows); v-update: b = H[j] (16 rows)
         const int nrows = (f & 1) ? 16 : 8;
         const int64_t row0 = (f & 1) ? j0 : i0;
@@ -279,6 +296,8 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
           if (DBG == 3 && blockIdx.x == 0 && b == bp_begin + cluster_id && threadIdx.x == 0 && 2 * f + nh < 256)
             g_tc4_trace[2][2 * f + nh] = clock64();
           const uint32_t col0 = (uint32_t)(nh * 512 + g * 128);   // global anchor index of my first column
+          uint8_t* xout = xhalf(f + 1, nh);                         // half nh of the next X
+          const uint8_t* ubuf = xhalf(phases - 2, nh);              // u_L (cost phase only)
           const uint32_t tcol = lane_off + (uint32_t)(g * 128);   // my TMEM columns (N-subs = g>>1)
           if (DBG != 1) {
             uint32_t d[2][16];
@@ -301,7 +320,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                 }
               }
               const uint32_t* dc = d[c & 1];
-              const uint32_t k0 = col0 + c * 16;
+              const uint32_t k0 = col0 - (uint32_t)(nh * 512) + c * 16;   // anchor within half nh
               if (!cost_phase) {
                 float m[16];
 #pragma unroll
@@ -309,8 +328,8 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                   const float4 q4 = mq[c & 1][e];
                   m[4 * e] = q4.x; m[4 * e + 1] = q4.y; m[4 * e + 2] = q4.z; m[4 * e + 3] = q4.w;
                 }
-                // x = m / D (one MUFU per two anchors; S:62 clamp + flag outside [2^-62, 2^62];
-                // m = 0 -> exactly 0, R#11)
+                // x = m / D, one MUFU per two anchors (epi_div_fast; S:62 clamp + flag when a
+                // product D0 D1 leaves fp32 range; m = 0 -> exactly 0, R#11)
                 uint32_t o[16];
                 const bool bad = epi_div_fast<16>(m, *reinterpret_cast<const uint32_t(*)[16]>(dc), o);
                 if (__builtin_expect(__any_sync(0xffffffffu, bad), 0)) {   // a product D0 D1 out of fp32 range (rare)
