@@ -1,7 +1,7 @@
 """Summarise ncu artefacts into profiles/ (run here, on the CPU box, after a gpurun call).
 
   python tools/summarize_ncu.py launches <launches.csv> <out.md>
-  python tools/summarize_ncu.py full <prof.ncu-rep> <out.json> [summary-key, e.g. c3:tf32]
+  python tools/summarize_ncu.py full <prof.ncu-rep> <out.json> [summary-key, e.g. c3:tf32] [kernel-name substring]
 """
 import collections
 import csv
@@ -52,10 +52,13 @@ def launches(csv_path, out_md):
     print("\n".join(lines))
 
 
-def full(rep, out_json, traffic_key=None):
+def full(rep, out_json, traffic_key=None, kernel=None):
     raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    h, u, v = rows[0], rows[1], rows[2]
+    h, u = rows[0], rows[1]
+    ki = h.index('Kernel Name')
+    cand = [r for r in rows[2:] if kernel is None or kernel in r[ki]]
+    v = cand[0]
     out = {'kernel': v[h.index('Kernel Name')] if 'Kernel Name' in h else None}
     for k in KEYS:
         if k in h:
@@ -74,7 +77,8 @@ def full(rep, out_json, traffic_key=None):
 
     def num(k):
         i = h.index(k)
-        scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}.get(u[i], 1)
+        scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'hz': 1, 'Khz': 1e3, 'Mhz': 1e6,
+                 'Ghz': 1e9}.get(u[i], 1)
         return float(v[i].replace(',', '')) * scale
     traffic = num('dram__bytes_read.sum') + num('dram__bytes_write.sum')
     out['dram_bytes_per_launch'] = traffic
@@ -107,4 +111,5 @@ if __name__ == '__main__':
     if sys.argv[1] == 'launches':
         launches(sys.argv[2], sys.argv[3])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None,
+             sys.argv[5] if len(sys.argv) > 5 else None)
