@@ -137,16 +137,20 @@ __device__ __forceinline__ float div_clamped(float m, float den, bool& clamped) 
   }
   return m * rcp_ftz(den);   // m = 0 -> exactly 0 (R#11)
 }
-// The TF32 epilogues' divide over a thread's N (even) anchors of one chunk: o = the RNA-pre-
-// rounded TF32 bits of m / D, m = 0 -> exactly 0 (R#11), one MUFU per two anchors:
-//   p = D0 D1,  r = 1/p,  q = (D1 r, D0 r) = (1/D0, 1/D1),  x = m q.
-// The form is exact up to rounding whenever p lies in [2^-126, 2^126), where rcp.approx.ftz
-// returns a finite normal r.  p leaves that range once max(C_s)/eps exceeds ~44, so the fast
-// pass also tracks min / max of p over the chunk (3-input FMNMX on the products, off the
-// MUFU's dependency chain) and reports the thread as `bad`; the caller then reloads D from TMEM
-// (not yet overwritten) in sub-blocks of 8 and epi_div_fix8 replaces the bad thread's values by
-// per-anchor clamped reciprocals (S:62 clamp + flag).  Other threads keep their fast values, so
-// a pair's result never depends on the other pairs of its warp.
+// The TF32 epilogues' divide over a thread's N (multiple of 4) anchors of one chunk: o = the
+// RNA-pre-rounded TF32 bits of m / D, m = 0 -> exactly 0 (R#11), one MUFU per two anchors.
+// Anchors (e, e+2) and (e+1, e+3) share a reciprocal, so every product and scaling step is a
+// paired f32x2 op on consecutive registers:
+//   (pa, pb) = (D0 D2, D1 D3),  r = (1/pa, 1/pb),  q = (D2, D3) r = (1/D0, 1/D1),
+//   (D0, D1) r = (1/D2, 1/D3),  x = m q.
+// The form is exact up to rounding whenever each product lies in [2^-126, 2^126), where
+// rcp.approx.ftz returns a finite normal r.  Products leave that range once max(C_s)/eps exceeds
+// ~44: the fast pass accumulates t = p r (= 1 up to 2^-22 when valid; 0, inf or NaN
+// otherwise) over the chunk in one FFMA2 per four anchors and reports the thread as `bad` unless
+// the sum is N/2; the caller then reloads D from TMEM (not yet overwritten) in sub-blocks of 8 and
+// epi_div_fix8 replaces the bad thread's values by per-anchor clamped reciprocals (S:62 clamp +
+// flag).  Other threads keep their fast values, so a pair's result never depends on the other
+// pairs of its warp.
 __device__ __forceinline__ uint32_t tf32_rna_pre_bits(float x) { return __float_as_uint(x) + 0x1000u; }
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
   float r;
@@ -158,28 +162,30 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c);
+// x[e .. e+4) = m / D for one group of four anchors; t += (pa ra, pb rb)
+__device__ __forceinline__ void epi_div4(const float* m, float d0, float d1, float d2, float d3, float* x, float2& t) {
+  const float2 p = fmul2(make_float2(d0, d1), make_float2(d2, d3));
+  const float2 r = make_float2(rcp_ftz(p.x), rcp_ftz(p.y));
+  t = ffma2(p, r, t);
+  const float2 x01 = fmul2(make_float2(m[0], m[1]), fmul2(make_float2(d2, d3), r));
+  const float2 x23 = fmul2(make_float2(m[2], m[3]), fmul2(make_float2(d0, d1), r));
+  x[0] = x01.x; x[1] = x01.y; x[2] = x23.x; x[3] = x23.y;
+}
+__device__ __forceinline__ bool epi_div_bad(float2 t, int n) { return !(fabsf((t.x + t.y) - 0.5f * n) < 0.25f); }
 template <int N>
 __device__ __forceinline__ bool epi_div_fast(const float* m, const uint32_t (&d)[N], uint32_t (&o)[N]) {
   static_assert(N % 4 == 0, "chunk");
-  float lo = INFINITY, hi = 0.0f;
+  float2 t = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int e = 0; e < N; e += 4) {
-    const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
-    const float d2 = __uint_as_float(d[e + 2]), d3 = __uint_as_float(d[e + 3]);
-    const float pa = d0 * d1, pb = d2 * d3;
-    const float ra = rcp_ftz(pa), rb = rcp_ftz(pb);
-    lo = fmin3(lo, pa, pb);
-    hi = fmax3(hi, pa, pb);
-    // q = (D1 r, D0 r) = (1/D0, 1/D1) first, then x = m q: no intermediate can underflow while
-    // the result is representable (m D1 could, when D0 and D1 lie far apart)
-    const float2 xa = fmul2(make_float2(m[e], m[e + 1]), fmul2(make_float2(d1, d0), make_float2(ra, ra)));
-    const float2 xb = fmul2(make_float2(m[e + 2], m[e + 3]), fmul2(make_float2(d3, d2), make_float2(rb, rb)));
-    o[e] = tf32_rna_pre_bits(xa.x);
-    o[e + 1] = tf32_rna_pre_bits(xa.y);
-    o[e + 2] = tf32_rna_pre_bits(xb.x);
-    o[e + 3] = tf32_rna_pre_bits(xb.y);
+    float x[4];
+    epi_div4(m + e, __uint_as_float(d[e]), __uint_as_float(d[e + 1]), __uint_as_float(d[e + 2]),
+             __uint_as_float(d[e + 3]), x, t);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[e + k] = tf32_rna_pre_bits(x[k]);
   }
-  return !(lo >= 0x1p-126f && hi < 0x1p126f);
+  return epi_div_bad(t, N);
 }
 __device__ __forceinline__ void epi_div_fix8(const float* m, const uint32_t (&d)[8], uint32_t* o, bool& clamped) {
 #pragma unroll

@@ -28,7 +28,7 @@
 //     K = 16): (x_hi, K_hi), (x_lo, K_hi), (x_hi, K_lo).  Output chunk nc is committed after part
 //     (3, nc); parts of input chunk kc wait only for the epilogue of chunk kc of the previous phase.
 //   Epilogue (16 warps, 16 anchors per thread per chunk): x = m / D with one MUFU per two anchors
-//     (epi_div_f32_fast: the product range check of the TF32 kernels, S:62 clamp + flag on the rare
+//     (epi_div4: the product range check of the TF32 kernels, S:62 clamp + flag on the rare
 //     out-of-range chunk), then the BF16 split packed with cvt.rn.bf16x2.
 //   Cost (a6): v_L (R0, split) against K (.) C_s, also split and streamed in four (N-half, K-half)
 //     sub-parts of [hi | lo] x 64 rows x 128 anchors (32 KB); the fp32 products land in the
@@ -88,25 +88,17 @@ __device__ __forceinline__ uint32_t cvt_bf16x2(float hi_elem, float lo_elem) {
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-// x = m / D for a thread's 16 anchors (fp32; one MUFU per two anchors, the TF32 kernels' product
-// range check, q-first order so no intermediate underflows), then the BF16 split:
+// x = m / D for a thread's 16 anchors (fp32; one MUFU per two anchors and the product range check
+// of the TF32 kernels, epi_div4), then the BF16 split:
 // o[0..8) = x_hi pairs, o[8..16) = x_lo pairs.  Returns true if a product D0 D1 left
 // [2^-126, 2^126) -- the caller then redoes the thread's values with clamped reciprocals.
 __device__ __forceinline__ bool epi_split_fast(const float* m, const uint32_t (&d)[16], float (&x)[16]) {
-  float lo = INFINITY, hi = 0.0f;
+  float2 t = make_float2(0.0f, 0.0f);
 #pragma unroll
-  for (int e = 0; e < 16; e += 4) {
-    const float d0 = __uint_as_float(d[e]), d1 = __uint_as_float(d[e + 1]);
-    const float d2 = __uint_as_float(d[e + 2]), d3 = __uint_as_float(d[e + 3]);
-    const float pa = d0 * d1, pb = d2 * d3;
-    const float ra = rcp_ftz(pa), rb = rcp_ftz(pb);
-    lo = fmin3(lo, pa, pb);
-    hi = fmax3(hi, pa, pb);
-    const float2 xa = fmul2(make_float2(m[e], m[e + 1]), fmul2(make_float2(d1, d0), make_float2(ra, ra)));
-    const float2 xb = fmul2(make_float2(m[e + 2], m[e + 3]), fmul2(make_float2(d3, d2), make_float2(rb, rb)));
-    x[e] = xa.x; x[e + 1] = xa.y; x[e + 2] = xb.x; x[e + 3] = xb.y;
-  }
-  return !(lo >= 0x1p-126f && hi < 0x1p126f);
+  for (int e = 0; e < 16; e += 4)
+    epi_div4(m + e, __uint_as_float(d[e]), __uint_as_float(d[e + 1]), __uint_as_float(d[e + 2]),
+             __uint_as_float(d[e + 3]), x + e, t);
+  return epi_div_bad(t, 16);
 }
 __device__ __forceinline__ void split16(const float (&x)[16], uint32_t (&o)[16]) {
 #pragma unroll
