@@ -4,13 +4,13 @@
 // a2 (P:214 one-hot P_o; "P_o is the clustering operator"; S:378 argmin, lowest index on
 // ties).  The decision must be bit-exact against the fp64 definition (reading R#8):
 // D_pj = sum_k (x_pk - w_jk)^2 accumulated sequentially in k in fp64 with every op rounded.
-// Kernel: a point x anchor distance tile.  Each point is held in registers by 4 lanes; each lane
-// scans every 4th anchor of the SMEM-staged anchor chunk in fp32 (direct differences, FMA), the
-// 4 lanes merge (best, index, second-best) with warp shuffles.  fp32 with a rigorous bound:
+// Kernel: a point x anchor distance tile, register-blocked (4 points x 4 anchors per thread, both
+// staged in shared memory), fp32 direct differences (f32x2 FSUB / FFMA), the 16 lanes sharing a
+// point merge (best, index, second-best) with warp shuffles.  fp32 with a rigorous bound:
 // for d non-negative rounded terms, |D32 - D| <= gamma_{d+2} D (gamma_n = n u / (1 - n u),
-// u = 2^-24).  If the runner-up D32 exceeds best * (1 + 5 gamma) (+ an absolute underflow
-// slack) the fp32 winner provably is the fp64 winner; otherwise the 4 lanes recompute all K
-// distances with the fp64 op sequence above and take the (value, index) minimum.
+// u = 2^-24), for any summation order.  If the runner-up D32 exceeds best * (1 + 5 gamma) (+ an
+// absolute underflow slack) the fp32 winner provably is the fp64 winner; otherwise the 16 lanes
+// recompute all K distances with the fp64 op sequence above and take the (value, index) minimum.
 //
 // a3 (Eq. (5) P:100 with the 1/n factor dropped, R#1; Lemma 1 proof a' = Z^T a P:145, P:417;
 // S:196).  One warp per distribution builds H[i, :] in shared memory in fp64: points are
@@ -61,9 +61,19 @@ cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, flo
 }
 
 // ------------------------------------------------------------------------------ a2: mapping
+// Point x anchor distance tile, register-blocked like a GEMM: a CTA stages a tile of 64 points
+// and a chunk of anchors in shared memory (rows padded to DP + 4 floats: 16-byte vector loads,
+// consecutive anchor rows 16 bytes apart in the bank space); thread (warp w, lane l) owns the 4
+// points 4 (2w + l/16) + [0, 4) and, per group of 64 anchors, the 4 anchors 16a + l%16
+// (a = 0..3).  Per 4 coordinates it loads 4 point float4 (broadcast across the 16 lanes that share
+// them) and 4 anchor float4, and issues 16 x (2 FSUB2 + 2 FFMA2): each staged value feeds 4
+// distances (the round-1 kernel held one point per lane, so every anchor load fed one point).
+// fp32 squared distances with the rigorous near-tie test of R#8, then the 16 lanes sharing a
+// point merge (best, index, second) with shuffles; ambiguous points are recomputed in fp64 in the
+// oracle's op order by those 16 lanes.
 constexpr int kMapThreads = 256;
-constexpr int kLanesPerPoint = 4;
-constexpr int kPointsPerBlock = kMapThreads / kLanesPerPoint;  // 64
+constexpr int kTilePoints = 64;                 // points per tile (16 groups of 4)
+constexpr int kMapAnchorGroup = 64;             // anchors per register pass (16 lanes x 4)
 
 struct BestTriple {
   float best;
@@ -83,14 +93,17 @@ __device__ __forceinline__ void merge_triple(BestTriple& a, float ob, float os, 
 }
 
 template <int DP>
-__global__ void __launch_bounds__(kMapThreads)
+__global__ void __launch_bounds__(kMapThreads, 2)
 map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ gather, int64_t T,
                   int dim, const float* __restrict__ anchors, int K, int chunk,
                   int32_t* __restrict__ assign, uint32_t* __restrict__ status) {
   extern __shared__ float4 map_smem4[];
-  float* Ws = reinterpret_cast<float*>(map_smem4);  // [chunk][DP + 4]
-  constexpr int RS = DP + 4;                        // row stride: 16-byte shift per row
-  const int q = threadIdx.x & (kLanesPerPoint - 1);
+  constexpr int RS = DP + 4;                        // row stride (floats)
+  float* Xs = reinterpret_cast<float*>(map_smem4);  // [64][RS] points of the tile
+  float* Ws = Xs + kTilePoints * RS;                // [chunk][RS] anchors
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = lane & 15;                         // anchor slot
+  const int pg = 2 * warp + (lane >> 4);            // point group: points 4 pg + [0, 4)
 
   // anchors are checked for non-finite values once (block 0), not at every staging
   if (blockIdx.x == 0) {
@@ -98,140 +111,155 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
     for (int64_t e = threadIdx.x; e < (int64_t)K * dim; e += kMapThreads) bad |= !isfinite(anchors[e]);
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
   }
-  const bool vec = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0);
+  const bool avec = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(anchors) & 15u) == 0);
   const bool pvec = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(points) & 15u) == 0);
-  auto stage = [&](int j0, int nc) {  // anchors [j0, j0+nc) -> Ws rows (16-byte vector loads)
-    __syncthreads();
+  // rows [0, n) of src (row r of src = row map(r)) -> dst rows, zero-padded to DP; 16-byte
+  // loads when the source allows
+  auto stage_rows = [&](float* dst, int n, int n_alloc, const float* src, bool vec, auto map) {
     if (vec) {
-      for (int e = threadIdx.x; e < nc * (DP / 4); e += kMapThreads) {
-        const int jj = e / (DP / 4), k = 4 * (e % (DP / 4));
-        const float4 v = k < dim ? *reinterpret_cast<const float4*>(anchors + (int64_t)(j0 + jj) * dim + k)
-                                 : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        *reinterpret_cast<float4*>(Ws + jj * RS + k) = v;
+      for (int e = threadIdx.x; e < n_alloc * (DP / 4); e += kMapThreads) {
+        const int r = e / (DP / 4), k = 4 * (e % (DP / 4));
+        float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (r < n && k < dim) v = __ldg(reinterpret_cast<const float4*>(src + map(r) * dim + k));
+        *reinterpret_cast<float4*>(dst + r * RS + k) = v;
       }
     } else {
-      for (int e = threadIdx.x; e < nc * DP; e += kMapThreads) {
-        const int jj = e / DP, k = e % DP;
-        Ws[jj * RS + k] = k < dim ? anchors[(int64_t)(j0 + jj) * dim + k] : 0.0f;
+      for (int e = threadIdx.x; e < n_alloc * DP; e += kMapThreads) {
+        const int r = e / DP, k = e % DP;
+        dst[r * RS + k] = (r < n && k < dim) ? src[map(r) * dim + k] : 0.0f;
       }
     }
-    __syncthreads();
   };
-  const bool single = K <= chunk;   // all anchors resident: staged once for every point group
-  if (single) stage(0, K);
-  const int64_t n_groups = (T + kPointsPerBlock - 1) / kPointsPerBlock;
-  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {   // persistent over point groups
-  const int64_t p = g * kPointsPerBlock + (threadIdx.x >> 2);
-  const bool valid = p < T;
-  // point p of this launch is row gather[p] of `points` (k-means batches) or row p
-  const int64_t row = valid ? (gather ? gather[p] : p) : 0;
-  float x[DP];
-  bool finite = true;
-  if (pvec) {   // 16-byte loads of the point row
-#pragma unroll
-    for (int k = 0; k < DP; k += 4) {
-      const float4 v = (valid && k < dim) ? __ldg(reinterpret_cast<const float4*>(points + row * dim + k))
-                                          : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
-      x[k] = v.x; x[k + 1] = v.y; x[k + 2] = v.z; x[k + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < DP; ++k) {
-      const float v = (valid && k < dim) ? points[row * dim + k] : 0.0f;
-      finite &= isfinite(v);
-      x[k] = v;
-    }
+  const int K64 = (K + kMapAnchorGroup - 1) / kMapAnchorGroup * kMapAnchorGroup;
+  const bool single = K64 <= chunk;   // all anchors resident: staged once for every tile
+  if (single) {
+    stage_rows(Ws, K, K64, anchors, avec, [](int r) { return (int64_t)r; });
+    __syncthreads();
   }
-  if (!finite) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
-
-  BestTriple bt{INFINITY, INFINITY, 0x7fffffff};
-  for (int j0 = 0; j0 < K; j0 += chunk) {
-    const int nc = min(chunk, K - j0);
-    if (!single) stage(j0, nc);
-    // two anchors per iteration (rows jj and jj + 4): two independent FMA chains per coordinate
-    // pair, so the shared-memory loads of one row overlap the arithmetic of the other
-    auto update = [&](float acc, int j) {  // j increasing per lane: strict < keeps the lowest index
-      if (acc < bt.best) {
-        bt.second = bt.best;
-        bt.best = acc;
-        bt.idx = j;
-      } else if (acc < bt.second) {
-        bt.second = acc;
-      }
-    };
-    for (int jj = q; jj < nc; jj += 2 * kLanesPerPoint) {
-      const bool two = jj + kLanesPerPoint < nc;
-      const float4* wa = reinterpret_cast<const float4*>(Ws + jj * RS);
-      const float4* wb = reinterpret_cast<const float4*>(Ws + (two ? jj + kLanesPerPoint : jj) * RS);
-      // (paired f32x2 subtract / FMA: two coordinates per instruction; the bound below holds
-      // for any summation order of the d non-negative rounded terms)
-      float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
-      float2 b01 = make_float2(0.0f, 0.0f), b23 = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (int k4 = 0; k4 < DP / 4; ++k4) {
-        const float4 w = wa[k4], v = wb[k4];
-        const float2 x01 = make_float2(x[4 * k4 + 0], x[4 * k4 + 1]);
-        const float2 x23 = make_float2(x[4 * k4 + 2], x[4 * k4 + 3]);
-        const float2 t01 = fsub2(x01, make_float2(w.x, w.y)), t23 = fsub2(x23, make_float2(w.z, w.w));
-        const float2 u01 = fsub2(x01, make_float2(v.x, v.y)), u23 = fsub2(x23, make_float2(v.z, v.w));
-        a01 = ffma2(t01, t01, a01);
-        a23 = ffma2(t23, t23, a23);
-        b01 = ffma2(u01, u01, b01);
-        b23 = ffma2(u23, u23, b23);
-      }
-      update((a01.x + a01.y) + (a23.x + a23.y), j0 + jj);
-      if (two) update((b01.x + b01.y) + (b23.x + b23.y), j0 + jj + kLanesPerPoint);
-    }
-  }
-  // warp-shuffle argmin across the 4 lanes that share this point
-#pragma unroll
-  for (int off = 1; off < kLanesPerPoint; off <<= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, bt.best, off);
-    const float os = __shfl_xor_sync(0xffffffffu, bt.second, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, bt.idx, off);
-    merge_triple(bt, ob, os, oi);
-  }
-
-  // near-tie test with the rigorous fp32 bound (gamma_{d+2}, 5x slack incl. rounding of thr)
   const float u = 5.9604645e-8f;  // 2^-24
   const float nd = (float)(dim + 2);
   const float gamma = nd * u / (1.0f - nd * u);
-  const float thr = bt.best * (1.0f + 5.0f * gamma) + 1e-35f;
-  const bool refine = valid && K > 1 && (bt.second <= thr);
-  if (__any_sync(0xffffffffu, refine)) {
-    // fp64 recomputation in the pinned op order: t = x - w; sq = t*t; acc = acc + sq (no FMA)
-    double bd = INFINITY;
-    int bi = 0x7fffffff;
-    if (refine) {
-      for (int j = q; j < K; j += kLanesPerPoint) {
-        const float* wr = anchors + (int64_t)j * dim;
-        double acc = 0.0;
+  const int64_t n_tiles = (T + kTilePoints - 1) / kTilePoints;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {   // persistent over tiles
+    const int64_t p0 = tile * kTilePoints;
+    const int np = (int)((T - p0) < kTilePoints ? (T - p0) : kTilePoints);
+    __syncthreads();   // previous tile's readers are done with Xs
+    stage_rows(Xs, np, kTilePoints, points, pvec,
+               [&](int r) { return gather ? gather[p0 + r] : p0 + r; });
+    __syncthreads();
+    {   // non-finite coordinates of this thread's points (each point checked by its 16 lanes)
+      bool finite = true;
+      for (int q = 0; q < 4; ++q)
+        for (int k = tx; k < DP; k += 16) finite &= isfinite(Xs[(4 * pg + q) * RS + k]);
+      if (!finite) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
+    }
+    BestTriple bt[4];
 #pragma unroll
-        for (int k = 0; k < DP; ++k) {
-          const double w = k < dim ? (double)wr[k] : 0.0;
-          const double t = __dsub_rn((double)x[k], w);
-          acc = __dadd_rn(acc, __dmul_rn(t, t));
+    for (int q = 0; q < 4; ++q) bt[q] = BestTriple{INFINITY, INFINITY, 0x7fffffff};
+    const float* xr = Xs + 4 * pg * RS;
+    for (int j0 = 0; j0 < K; j0 += chunk) {
+      const int nc = min(chunk, K - j0);
+      const int nc64 = (nc + kMapAnchorGroup - 1) / kMapAnchorGroup * kMapAnchorGroup;
+      if (!single) {
+        __syncthreads();
+        stage_rows(Ws, nc, nc64, anchors + (int64_t)j0 * dim, avec, [](int r) { return (int64_t)r; });
+        __syncthreads();
+      }
+      for (int g0 = 0; g0 < nc64; g0 += kMapAnchorGroup) {
+        const float* wr = Ws + (g0 + tx) * RS;
+        float2 acc[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int a = 0; a < 4; ++a) acc[q][a] = make_float2(0.0f, 0.0f);
+#pragma unroll 2
+        for (int k = 0; k < DP; k += 4) {
+          float4 xv[4], wv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) xv[q] = *reinterpret_cast<const float4*>(xr + q * RS + k);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) wv[a] = *reinterpret_cast<const float4*>(wr + 16 * a * RS + k);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const float2 t01 = fsub2(make_float2(xv[q].x, xv[q].y), make_float2(wv[a].x, wv[a].y));
+              const float2 t23 = fsub2(make_float2(xv[q].z, xv[q].w), make_float2(wv[a].z, wv[a].w));
+              acc[q][a] = ffma2(t01, t01, acc[q][a]);
+              acc[q][a] = ffma2(t23, t23, acc[q][a]);
+            }
         }
-        if (acc < bd) {
-          bd = acc;
-          bi = j;
+        // anchors j increase along a within a lane: strict < keeps the lowest index
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int j = j0 + g0 + tx + 16 * a;
+          if (j < K) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float dq = acc[q][a].x + acc[q][a].y;
+              if (dq < bt[q].best) {
+                bt[q].second = bt[q].best;
+                bt[q].best = dq;
+                bt[q].idx = j;
+              } else if (dq < bt[q].second) {
+                bt[q].second = dq;
+              }
+            }
+          }
         }
       }
     }
+    // merge across the 16 lanes that share the points (lane groups of 16 within the warp)
 #pragma unroll
-    for (int off = 1; off < kLanesPerPoint; off <<= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, bd, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ob < bd || (ob == bd && oi < bi)) {
-        bd = ob;
-        bi = oi;
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, bt[q].best, off);
+        const float os = __shfl_xor_sync(0xffffffffu, bt[q].second, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bt[q].idx, off);
+        merge_triple(bt[q], ob, os, oi);
       }
     }
-    if (refine) bt.idx = bi;
-  }
-  if (valid && q == 0) assign[p] = bt.idx;
-  }  // point groups
+    // near-tie test with the rigorous fp32 bound (gamma_{d+2}, 5x slack incl. rounding of thr);
+    // ambiguous points: fp64 recomputation in the pinned op order t = x - w; acc = acc + t*t
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int pl = 4 * pg + q;
+      const bool valid = pl < np;
+      const float thr = bt[q].best * (1.0f + 5.0f * gamma) + 1e-35f;
+      const bool refine = valid && K > 1 && (bt[q].second <= thr);
+      if (__any_sync(0xffffffffu, refine)) {
+        double bd = INFINITY;
+        int bi = 0x7fffffff;
+        if (refine) {
+          const float* xp = Xs + pl * RS;
+          for (int j = tx; j < K; j += 16) {
+            const float* wj = anchors + (int64_t)j * dim;
+            double accd = 0.0;
+            for (int k = 0; k < dim; ++k) {
+              const double t = __dsub_rn((double)xp[k], (double)wj[k]);
+              accd = __dadd_rn(accd, __dmul_rn(t, t));
+            }
+            if (accd < bd) {
+              bd = accd;
+              bi = j;
+            }
+          }
+        }
+#pragma unroll
+        for (int off = 1; off < 16; off <<= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, bd, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (ob < bd || (ob == bd && oi < bi)) {
+            bd = ob;
+            bi = oi;
+          }
+        }
+        if (refine) bt[q].idx = bi;
+      }
+      if (valid && tx == 0) assign[p0 + pl] = bt[q].idx;
+    }
+  }  // tiles
 }
 
 template <int DP>
@@ -239,11 +267,14 @@ static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int
                                  const float* anchors, int K, int32_t* assign, uint32_t* status,
                                  cudaStream_t s) {
   const int rs_bytes = (DP + 4) * 4;
-  int chunk = (96 * 1024) / rs_bytes;
-  if (chunk > K) chunk = K;
-  const size_t smem = (size_t)chunk * rs_bytes;
-  cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int64_t blocks = (T + kPointsPerBlock - 1) / kPointsPerBlock;
+  // anchor chunk: whole 64-anchor groups within ~96 KB (with the point tile: 2 CTAs per SM)
+  int chunk = ((96 * 1024) / rs_bytes) / kMapAnchorGroup * kMapAnchorGroup;
+  const int K64 = (K + kMapAnchorGroup - 1) / kMapAnchorGroup * kMapAnchorGroup;
+  if (chunk > K64) chunk = K64;
+  const size_t smem = (size_t)(chunk + kTilePoints) * rs_bytes;
+  cudaError_t e = cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (T + kTilePoints - 1) / kTilePoints;
   if (blocks == 0) return cudaSuccess;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
