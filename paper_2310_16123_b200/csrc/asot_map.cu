@@ -92,6 +92,8 @@ __device__ __forceinline__ void merge_triple(BestTriple& a, float ob, float os, 
   }
 }
 
+__device__ __forceinline__ uint32_t smem_u32_of(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 template <int DP>
 __global__ void __launch_bounds__(kMapThreads, 2)
 map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ gather, int64_t T,
@@ -99,8 +101,8 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
                   int32_t* __restrict__ assign, uint32_t* __restrict__ status) {
   extern __shared__ float4 map_smem4[];
   constexpr int RS = DP + 4;                        // row stride (floats)
-  float* Xs = reinterpret_cast<float*>(map_smem4);  // [64][RS] points of the tile
-  float* Ws = Xs + kTilePoints * RS;                // [chunk][RS] anchors
+  float* Xs2 = reinterpret_cast<float*>(map_smem4); // 2 x [64][RS] points: current and next tile
+  float* Ws = Xs2 + (DP <= 64 ? 2 : 1) * kTilePoints * RS;   // [chunk][RS] anchors
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = lane & 15;                         // anchor slot
   const int pg = 2 * warp + (lane >> 4);            // point group: points 4 pg + [0, 4)
@@ -140,13 +142,41 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
   const float nd = (float)(dim + 2);
   const float gamma = nd * u / (1.0f - nd * u);
   const int64_t n_tiles = (T + kTilePoints - 1) / kTilePoints;
+  // the next tile's points are copied (cp.async, 16 B, zero-filled past the end) while this one
+  // is computed; unaligned / odd-dim inputs are staged synchronously
+  auto prefetch = [&](int64_t tile, float* dst) {
+    const int64_t q0 = tile * kTilePoints;
+    const int nq = (int)((T - q0) < kTilePoints ? (T - q0) : kTilePoints);
+    for (int e = threadIdx.x; e < kTilePoints * (DP / 4); e += kMapThreads) {
+      const int r = e / (DP / 4), k = 4 * (e % (DP / 4));
+      const bool ok = r < nq && k < dim;
+      const float* src = ok ? points + (gather ? gather[q0 + r] : q0 + r) * dim + k : points;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32_of(dst + r * RS + k)),
+                   "l"(src), "r"(ok ? 16 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // (d = 128: a second point tile would cost the second CTA per SM -- staged synchronously)
+  constexpr bool kDbuf = DP <= 64;
+  const bool dbuf = kDbuf && pvec;
+  int buf = 0;
+  if (dbuf && blockIdx.x < n_tiles) prefetch(blockIdx.x, Xs2);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {   // persistent over tiles
     const int64_t p0 = tile * kTilePoints;
     const int np = (int)((T - p0) < kTilePoints ? (T - p0) : kTilePoints);
-    __syncthreads();   // previous tile's readers are done with Xs
-    stage_rows(Xs, np, kTilePoints, points, pvec,
-               [&](int r) { return gather ? gather[p0 + r] : p0 + r; });
-    __syncthreads();
+    float* Xs = Xs2 + buf * kTilePoints * RS;
+    if (dbuf) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();   // this tile landed; everyone is done with the other buffer
+      if (tile + gridDim.x < n_tiles) prefetch(tile + gridDim.x, Xs2 + (buf ^ 1) * kTilePoints * RS);
+    } else {
+      __syncthreads();   // previous tile's readers are done with Xs
+      stage_rows(Xs, np, kTilePoints, points, pvec,
+                 [&](int r) { return gather ? gather[p0 + r] : p0 + r; });
+      __syncthreads();
+    }
+    if (dbuf) buf ^= 1;
     {   // non-finite coordinates of this thread's points (each point checked by its 16 lanes)
       bool finite = true;
       for (int q = 0; q < 4; ++q)
@@ -267,11 +297,13 @@ static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int
                                  const float* anchors, int K, int32_t* assign, uint32_t* status,
                                  cudaStream_t s) {
   const int rs_bytes = (DP + 4) * 4;
-  // anchor chunk: whole 64-anchor groups within ~96 KB (with the point tile: 2 CTAs per SM)
-  int chunk = ((96 * 1024) / rs_bytes) / kMapAnchorGroup * kMapAnchorGroup;
+  // anchor chunk: whole 64-anchor groups such that the CTA (with its one or two point tiles)
+  // fits twice per SM
+  constexpr int kTiles = DP <= 64 ? 2 : 1;
+  int chunk = ((110 * 1024) / rs_bytes - kTiles * kTilePoints) / kMapAnchorGroup * kMapAnchorGroup;
   const int K64 = (K + kMapAnchorGroup - 1) / kMapAnchorGroup * kMapAnchorGroup;
   if (chunk > K64) chunk = K64;
-  const size_t smem = (size_t)(chunk + kTilePoints) * rs_bytes;
+  const size_t smem = (size_t)(chunk + kTiles * kTilePoints) * rs_bytes;
   cudaError_t e = cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t blocks = (T + kTilePoints - 1) / kTilePoints;
