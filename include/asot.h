@@ -219,7 +219,13 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
                              int32_t dim, const float* dictionary, int32_t n_anchors,
                              int32_t n_layers, int32_t hidden, const float* V1, const float* c1,
                              const float* v2, const float* c2, float* hist_out, float* codes_out,
-                             uint32_t* status, void* stream);
+                             uint32_t* status, void* workspace, size_t workspace_bytes,
+                             void* stream);
+/* Device workspace for asot_map_soft_dl: dim in {64, 128} with 256 <= n_anchors <= 1024
+ * (n_anchors % 64 == 0) runs the sparse-code kernel (asot_soft_dl_sparse.cu), which keeps each
+ * CTA's tile of codes in this scratch (#SMs x 64 x n_anchors floats, L2-resident); 0 otherwise.
+ * A smaller workspace (or NULL) selects the previous kernels. */
+size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors);
 
 /* ASOT-ML anchor cost: C_s[u, v] = ||M w_u - M w_v||_2, M [h, dim] row-major, anchors
  * [n_anchors, dim]; bitwise symmetric, zero diagonal.  normalize != 0 divides by the max entry

@@ -42,7 +42,8 @@ _SIGS = {
     "asot_map_soft_ml": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp]),
     "asot_map_soft_dl": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
-                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "asot_map_soft_dl_workspace_bytes": (c_size, [c_i32, c_i32]),
     "asot_mahalanobis_cost": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
     "asot_mahalanobis_workspace_bytes": (c_size, [c_i32, c_i32]),
     "asot_kmeans_minibatch": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp,

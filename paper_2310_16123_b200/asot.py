@@ -276,7 +276,8 @@ def map_soft_ml(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tens
 def map_soft_dl(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
                 dictionary: torch.Tensor, V1: torch.Tensor, c1: torch.Tensor, v2: torch.Tensor,
                 c2: torch.Tensor, n_layers: int = 20, offsets_host: Optional[np.ndarray] = None,
-                want_codes: bool = False, status: Optional[torch.Tensor] = None, stream=None):
+                want_codes: bool = False, status: Optional[torch.Tensor] = None,
+                workspace: Optional[Workspace] = None, stream=None):
     """NEXT-1 ASOT-DL near-one-hot encoder (Eq. (9), L layers) and H = Z^T a per distribution.
     Returns (H [N, K], codes [T, K] or None, status)."""
     _need_cuda(dictionary, V1, c1, v2, c2)
@@ -285,10 +286,13 @@ def map_soft_dl(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tens
     hidden = int(V1.shape[1])
     oh, N, T, H, codes, st = _soft_common(points, offsets, weights, offsets_host, int(K), status,
                                           want_codes)
-    _check(_lib_handle().asot_map_soft_dl(
+    L = _lib_handle()
+    nbytes = int(L.asot_map_soft_dl_workspace_bytes(int(d), int(K)))
+    ws = _ws(workspace, points.device).get(nbytes) if nbytes > 0 else None
+    _check(L.asot_map_soft_dl(
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(dictionary), int(K),
         int(n_layers), hidden, _ptr(V1), _ptr(c1), _ptr(v2), _ptr(c2), _ptr(H), _ptr(codes),
-        _ptr(st), _stream(stream)))
+        _ptr(st), _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)))
     return H, (codes[:T] if codes is not None else None), st
 
 

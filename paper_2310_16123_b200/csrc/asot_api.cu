@@ -423,7 +423,8 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
                              int32_t dim, const float* dictionary, int32_t n_anchors,
                              int32_t n_layers, int32_t hidden, const float* V1, const float* c1,
                              const float* v2, const float* c2, float* hist_out, float* codes_out,
-                             uint32_t* status, void* stream) {
+                             uint32_t* status, void* workspace, size_t workspace_bytes,
+                             void* stream) {
   g_launches = 0;
   asot_status st = check_soft(points, offsets, offsets_host, weights, n_dist, dim, n_anchors,
                               hidden, hist_out, status);
@@ -431,11 +432,26 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
   ASOT_CHECK_ARG(dictionary && V1 && c1 && v2 && c2, "null pointer argument");
   ASOT_CHECK_ARG(n_layers >= 1, "n_layers must be >= 1");
   cudaStream_t s = (cudaStream_t)stream;
+  Nvtx range("asot next1 map_soft_dl");
   ProfScope prof(ASOT_PROF_MAP, s);
+  const size_t need = asot_map_soft_dl_workspace_bytes(dim, n_anchors);
+  const bool aligned = ((uintptr_t)points & 15u) == 0 && ((uintptr_t)dictionary & 15u) == 0;
+  if (need > 0 && workspace && workspace_bytes >= need && aligned &&
+      !getenv("ASOT_SOFT_DL_GENERIC")) {
+    ASOT_LAUNCH(asot::launch_soft_dl_sparse(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
+                                            n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
+                                            (float*)workspace, status, device_sms(), s));
+    return ASOT_OK;
+  }
   ASOT_LAUNCH(asot::launch_soft_map_dl(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
                                        n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
                                        status, s));
   return ASOT_OK;
+}
+
+size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors) {
+  return asot::soft_dl_sparse_supported(dim, n_anchors)
+             ? asot::soft_dl_sparse_workspace_bytes(n_anchors, device_sms()) : 0;
 }
 
 size_t asot_mahalanobis_workspace_bytes(int32_t n_anchors, int32_t h) {
