@@ -222,9 +222,10 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
                              uint32_t* status, void* workspace, size_t workspace_bytes,
                              void* stream);
 /* Device workspace for asot_map_soft_dl: dim in {64, 128} with 256 <= n_anchors <= 1024
- * (n_anchors % 64 == 0) runs the sparse-code kernel (asot_soft_dl_sparse.cu), which keeps each
- * CTA's tile of codes in this scratch (#SMs x 64 x n_anchors floats, L2-resident); 0 otherwise.
- * A smaller workspace (or NULL) selects the previous kernels. */
+ * (n_anchors % 64 == 0) runs the tensor-core encoder (asot_soft_dl_tc.cu: the dense product
+ * g = W^T r on tcgen05 3xTF32, the sparse r = W z - x on CUDA cores), which keeps each CTA's tile
+ * of codes in this scratch (#SMs x 128 x n_anchors floats, L2-resident) next to the split
+ * dictionary images; 0 otherwise.  A smaller workspace (or NULL) selects the CUDA-core kernels. */
 size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors);
 
 /* ASOT-ML anchor cost: C_s[u, v] = ||M w_u - M w_v||_2, M [h, dim] row-major, anchors

@@ -436,12 +436,23 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
   ProfScope prof(ASOT_PROF_MAP, s);
   const size_t need = asot_map_soft_dl_workspace_bytes(dim, n_anchors);
   const bool aligned = ((uintptr_t)points & 15u) == 0 && ((uintptr_t)dictionary & 15u) == 0;
-  if (need > 0 && workspace && workspace_bytes >= need && aligned &&
-      !getenv("ASOT_SOFT_DL_GENERIC")) {
-    ASOT_LAUNCH(asot::launch_soft_dl_sparse(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
-                                            n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
-                                            (float*)workspace, status, device_sms(), s));
-    return ASOT_OK;
+  // large dictionaries: the tensor-core kernel (default) or, for cross-checks
+  // (ASOT_SOFT_DL_GENERIC=sparse), the sparse-code CUDA-core kernel; otherwise / without a
+  // workspace the resident, tiled or streamed CUDA-core kernels
+  const char* gen = getenv("ASOT_SOFT_DL_GENERIC");
+  if (need > 0 && workspace && workspace_bytes >= need && aligned) {
+    if (!gen) {
+      ASOT_LAUNCH(asot::launch_soft_dl_tc(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
+                                          n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
+                                          (uint8_t*)workspace, status, device_sms(), s));
+      return ASOT_OK;
+    }
+    if (std::string(gen) == "sparse") {
+      ASOT_LAUNCH(asot::launch_soft_dl_sparse(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
+                                              n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
+                                              (float*)workspace, status, device_sms(), s));
+      return ASOT_OK;
+    }
   }
   ASOT_LAUNCH(asot::launch_soft_map_dl(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
                                        n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
@@ -450,8 +461,10 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
 }
 
 size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors) {
-  return asot::soft_dl_sparse_supported(dim, n_anchors)
-             ? asot::soft_dl_sparse_workspace_bytes(n_anchors, device_sms()) : 0;
+  if (!asot::soft_dl_tc_supported(dim, n_anchors)) return 0;
+  const size_t a = asot::soft_dl_tc_workspace_bytes(dim, n_anchors, device_sms());
+  const size_t b = asot::soft_dl_sparse_workspace_bytes(n_anchors, device_sms());
+  return a > b ? a : b;
 }
 
 size_t asot_mahalanobis_workspace_bytes(int32_t n_anchors, int32_t h) {

@@ -1,0 +1,397 @@
+// asot_soft_dl_tc.cu -- SURVEY §8(f) NEXT-1 on the tensor cores: the ASOT-DL encoder (P:262-272
+// Eqs. (8)(9), appendix P:500-538 step size 1; R#26-R#28) with its dense product on tcgen05.
+//
+//   lambda_p = softplus(v2 . relu(V1^T x_p + c1) + c2),  z^(0) = 0,
+//   n_layers x { r = W z - x;  g = W^T r;  z <- max(0, z - g - lambda) },  then z / sum z
+//   (uniform fallback, flagged), H[i] = sum_p w_p z_p in fp64 in point order (Eq. (5), R#1).
+//
+// Per CTA a tile of 128 points of one distribution (persistent CTAs loop over distributions):
+//   * r = W z - x is a gather over the non-zero codes (near-one-hot: 8-16 of 1024 at c5, 15-61 of
+//     256 at c3; asot_soft_dl_sparse.cu) on the CUDA cores, split x = x_hi + x_lo with
+//     x_hi = RNA_tf32(x) (3xTF32, fp32-accurate: R#22's split) and stored into TMEM as the MMA's
+//     A operand: thread p of warp w (lane quarter w % 4) owns point p = TMEM lane p;
+//   * g = W^T r, [128 points x d] x [d x K], is `tcgen05.mma.cta_group::1.kind::tf32` with
+//     A = R from TMEM and B = 64-anchor chunks of the dictionary (pre-split K_hi / K_lo images,
+//     SW128 K-major, streamed by a TMA producer warp through a double-buffered SMEM ring), three
+//     MMAs per 8-wide k-step (r_hi W_hi, r_lo W_hi, r_hi W_lo), fp32 accumulators in two TMEM
+//     buffers of 64 columns so the epilogue of chunk c overlaps the MMAs of chunk c + 1;
+//   * epilogue (8 warps: lane quarter x column half): z <- max(0, z_old - g - lambda) with the
+//     dense codes of the tile in a per-CTA global scratch (L2) and a bitmap of their non-zeros
+//     in shared memory (each thread owns one bitmap word per chunk: no atomics).
+// TMEM: A_hi [0, d), A_lo [d, 2d), D0 [256, 320), D1 [320, 384).
+#include <cfloat>
+#include <cmath>
+
+#include "asot_internal.cuh"
+#include "asot_tcgen05.cuh"
+
+namespace asot {
+namespace dltc {
+
+using namespace ::asot::ptx;
+
+constexpr int kTP = 128;                 // points per tile (MMA M)
+constexpr int kCN = 64;                  // anchors per chunk (MMA N)
+constexpr int kCompWarps = 8;
+constexpr int kThreads = kCompWarps * 32 + 64;   // + MMA warp + TMA producer warp
+constexpr int kStages = 2;
+
+template <int DP>
+struct Cfg {
+  static constexpr uint32_t kImgBytes = (uint32_t)kCN * DP * 4;        // one chunk, one of hi / lo
+  static constexpr uint32_t kStageBytes = 2 * kImgBytes;               // hi | lo
+  static constexpr uint32_t kDCol0 = 256;                              // D buffers
+};
+
+struct Args {
+  const float* points;
+  const int64_t* offsets;
+  const float* weights;
+  int64_t n_dist;
+  int K;
+  int hidden;
+  const float* V1;
+  const float* c1;
+  const float* v2;
+  const float* c2;
+  const float* dict;        // [K, d] fp32
+  const uint8_t* img;       // [K / 64 chunks][hi | lo][d / 32 kb][64 rows][128 B]
+  int n_layers;
+  float* H;
+  float* codes;
+  float* zbuf;              // [gridDim.x][kTP][K]
+  uint32_t* status;
+};
+
+__device__ __forceinline__ float softplus_f(float t) { return t > 30.0f ? t : log1pf(expf(t)); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  tmem_st16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(&r[0]));
+  tmem_st16(taddr + 16, *reinterpret_cast<const uint32_t(*)[16]>(&r[16]));
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kThreads, 1)
+soft_dl_tc_kernel(Args A) {
+  using C = Cfg<DP>;
+  constexpr uint32_t kIdesc = make_idesc_tf32(kTP, kCN);
+  extern __shared__ uint8_t dl_smem_raw[];
+  uint8_t* smem = dl_smem_raw + ((1024u - (smem_u32(dl_smem_raw) & 1023u)) & 1023u);
+  const int K = A.K, KW = K / 32, nchunks = K / kCN;
+  uint8_t* stage_base = smem;                                        // kStages x kStageBytes
+  double* acc = (double*)(smem + kStages * C::kStageBytes);          // [K]
+  uint32_t* bm = (uint32_t*)(acc + K);                               // [kTP][KW]
+  float* lam = (float*)(bm + kTP * KW);                              // [kTP]
+  float* wts = lam + kTP;                                            // [kTP]
+  float* rsum = wts + kTP;                                           // [kTP]
+  uint64_t* bars = (uint64_t*)(((uintptr_t)(rsum + kTP) + 7) & ~(uintptr_t)7);
+  // bars: full[2], empty[2], dfull[2], dfree[2], a_ready
+  const uint32_t bar_full = smem_u32(&bars[0]), bar_empty = smem_u32(&bars[2]);
+  const uint32_t bar_dfull = smem_u32(&bars[4]), bar_dfree = smem_u32(&bars[6]);
+  const uint32_t bar_a = smem_u32(&bars[8]);
+  uint32_t* tmem_holder = (uint32_t*)&bars[10];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* Z = A.zbuf + (size_t)blockIdx.x * kTP * K;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+      mbar_init(bar_dfull + 8 * s, 1);
+      mbar_init(bar_dfree + 8 * s, kCompWarps);
+    }
+    mbar_init(bar_a, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_holder != 0) __trap();
+
+  // the work sequence every role walks: distributions i = blockIdx.x + k gridDim.x, their
+  // 128-point tiles, n_layers layers, nchunks chunks
+  auto n_tiles_of = [&](int64_t i) -> int { return (int)((A.offsets[i + 1] - A.offsets[i] + kTP - 1) / kTP); };
+
+  if (warp == kCompWarps + 1) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t i = blockIdx.x; i < A.n_dist; i += gridDim.x) {
+        const int nt = n_tiles_of(i);
+        for (int t = 0; t < nt * A.n_layers; ++t)
+          for (int c = 0; c < nchunks; ++c, ++it) {
+            const uint32_t s = it % kStages;
+            if (it >= kStages) mbar_wait(bar_empty + 8 * s, ((it / kStages) - 1) & 1);
+            mbar_expect_tx(bar_full + 8 * s, C::kStageBytes);
+            bulk_g2s(smem_u32(stage_base + s * C::kStageBytes), A.img + (size_t)c * C::kStageBytes, C::kStageBytes,
+                     bar_full + 8 * s);
+          }
+      }
+    }
+  } else if (warp == kCompWarps) {
+    // ------------------------------------------------------------------ MMA issuer
+    uint32_t it = 0, a_par = 0;
+    for (int64_t i = blockIdx.x; i < A.n_dist; i += gridDim.x) {
+      const int nt = n_tiles_of(i);
+      for (int t = 0; t < nt * A.n_layers; ++t) {
+        mbar_wait(bar_a, a_par);   // R (A operand) of this layer is in TMEM
+        a_par ^= 1u;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const uint32_t s = it % kStages, db = it & 1;
+          mbar_wait(bar_full + 8 * s, (it / kStages) & 1);
+          if (it >= 2) mbar_wait(bar_dfree + 8 * db, ((it >> 1) - 1) & 1);   // epilogue drained D[db]
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sb = smem_u32(stage_base + s * C::kStageBytes);
+            const uint64_t bhi = make_sw128_desc(sb), blo = make_sw128_desc(sb + C::kImgBytes);
+            const uint32_t dcol = C::kDCol0 + kCN * db;
+#pragma unroll
+            for (int ks = 0; ks < DP / 8; ++ks) {
+              const uint64_t o = (uint64_t)(((ks >> 2) * (kCN * 128) + (ks & 3) * 32) >> 4);
+              mma1_tf32_ts(dcol, (uint32_t)(8 * ks), bhi + o, kIdesc, ks > 0 ? 1u : 0u);
+              mma1_tf32_ts(dcol, (uint32_t)(DP + 8 * ks), bhi + o, kIdesc, 1u);
+              mma1_tf32_ts(dcol, (uint32_t)(8 * ks), blo + o, kIdesc, 1u);
+            }
+            mma1_commit(bar_empty + 8 * s);   // the stage can be refilled
+            mma1_commit(bar_dfull + 8 * db);  // D[db] ready for the epilogue
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ compute warps (0..7)
+    const int q = warp & 3, half = warp >> 2;
+    const int p = q * 32 + lane;                       // TMEM lane == point of the tile
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    constexpr int RD = DP / 2;                         // dims of r per thread (two threads per point)
+    uint32_t it = 0;
+    for (int64_t i = blockIdx.x; i < A.n_dist; i += gridDim.x) {
+      const int64_t s0 = A.offsets[i], e0 = A.offsets[i + 1];
+      named_bar_sync(1, kCompWarps * 32);
+      for (int j = tid; j < K; j += kCompWarps * 32) acc[j] = 0.0;
+      bool nonfinite = false, negative = false;
+      double msum = 0.0;
+      for (int64_t t0 = s0; t0 < e0; t0 += kTP) {
+        const int np = (int)min((int64_t)kTP, e0 - t0);
+        const bool pv = p < np;
+        const float* xp = A.points + (t0 + (pv ? p : 0)) * DP;
+        named_bar_sync(1, kCompWarps * 32);   // previous tile's final pass is done
+        for (int x = tid; x < kTP * KW; x += kCompWarps * 32) bm[x] = 0u;   // z^(0) = 0 (R#27)
+        {
+          // lambda_p = softplus(v2 . relu(V1^T x_p + c1) + c2): the two threads of a point split
+          // the hidden units, partial sums meet in rsum (free until the row sums)
+          float lsum = 0.0f;
+          const int hh = (A.hidden + 1) / 2, c_lo = half * hh, c_hi = min(A.hidden, c_lo + hh);
+          for (int c = c_lo; c < c_hi; ++c) {
+            float a = A.c1[c];
+            for (int k = 0; k < DP; ++k) a = fmaf(pv ? __ldg(xp + k) : 0.0f, __ldg(A.V1 + (int64_t)k * A.hidden + c), a);
+            lsum = fmaf(fmaxf(a, 0.0f), __ldg(A.v2 + c), lsum);
+          }
+          if (half == 1) rsum[p] = lsum;
+          named_bar_sync(1, kCompWarps * 32);
+          if (half == 0) lam[p] = softplus_f((rsum[p] + lsum) + A.c2[0]);
+        }
+        if (half == 0) {
+          bool nf = false;
+          for (int k = 0; k < DP; ++k) nf |= pv && !isfinite(__ldg(xp + k));
+          nonfinite |= nf;
+          const float w = pv ? A.weights[t0 + p] : 0.0f;
+          if (pv) {
+            nonfinite |= !isfinite(w);
+            negative |= w < 0.0f;
+            msum += (double)w;
+          }
+          wts[p] = w;
+        }
+        named_bar_sync(1, kCompWarps * 32);
+        for (int layer = 0; layer < A.n_layers; ++layer) {
+          // ---- r = W z - x (non-zero z_j in increasing j), split into TF32 hi / lo -> TMEM A
+          {
+            float r[RD];
+#pragma unroll
+            for (int k = 0; k < RD; ++k) r[k] = 0.0f;
+            if (layer > 0 && pv) {
+              for (int w = 0; w < KW; ++w) {
+                uint32_t bits = bm[p * KW + w];
+                while (bits) {
+                  const int j = 32 * w + __ffs(bits) - 1;
+                  bits &= bits - 1;
+                  const float zj = Z[(size_t)p * K + j];
+                  const float4* wr = reinterpret_cast<const float4*>(A.dict + (int64_t)j * DP + half * RD);
+#pragma unroll
+                  for (int k4 = 0; k4 < RD / 4; ++k4) {
+                    const float4 w4 = __ldg(wr + k4);
+                    r[4 * k4] = fmaf(zj, w4.x, r[4 * k4]);
+                    r[4 * k4 + 1] = fmaf(zj, w4.y, r[4 * k4 + 1]);
+                    r[4 * k4 + 2] = fmaf(zj, w4.z, r[4 * k4 + 2]);
+                    r[4 * k4 + 3] = fmaf(zj, w4.w, r[4 * k4 + 3]);
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int b = 0; b < RD; b += 32) {
+              uint32_t hi[32], lo[32];
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const float x = pv ? __ldg(xp + half * RD + b + k) : 0.0f;
+                const float v = r[b + k] - x;
+                const uint32_t h = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
+                hi[k] = h;
+                lo[k] = __float_as_uint(v - __uint_as_float(h));
+              }
+              tmem_st32(lane_off + (uint32_t)(half * RD + b), hi);
+              tmem_st32(lane_off + (uint32_t)(DP + half * RD + b), lo);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            named_bar_sync(1, kCompWarps * 32);   // (also: the bitmap reads above are done)
+            if (tid == 0) mbar_arrive_local(bar_a);
+          }
+          // ---- chunks: z <- max(0, z - g - lambda); bitmap words 2c + half rebuilt
+          const float lp = lam[p];
+          for (int c = 0; c < nchunks; ++c, ++it) {
+            const uint32_t db = it & 1;
+            mbar_wait(bar_dfull + 8 * db, (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t g[32];
+            const uint32_t dcol = C::kDCol0 + kCN * db + 32 * half;
+            tmem_ld16u(lane_off + dcol, *reinterpret_cast<uint32_t(*)[16]>(&g[0]));
+            tmem_ld16u(lane_off + dcol + 16, *reinterpret_cast<uint32_t(*)[16]>(&g[16]));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(bar_dfree + 8 * db);   // D[db] may be overwritten
+            const int j0 = c * kCN + 32 * half;
+            float4* zp = reinterpret_cast<float4*>(Z + (size_t)p * K + j0);
+            uint32_t mask = 0u;
+#pragma unroll
+            for (int e4 = 0; e4 < 8; ++e4) {
+              float4 zo = layer > 0 ? zp[e4] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+              float zn[4] = {zo.x, zo.y, zo.z, zo.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                zn[u] = fmaxf(0.0f, (zn[u] - __uint_as_float(g[4 * e4 + u])) - lp);
+                if (zn[u] > 0.0f) mask |= 1u << (4 * e4 + u);
+              }
+              zp[e4] = make_float4(zn[0], zn[1], zn[2], zn[3]);
+            }
+            bm[p * KW + (j0 >> 5)] = pv ? mask : 0u;
+          }
+          named_bar_sync(1, kCompWarps * 32);   // codes + bitmap of this layer complete
+        }
+        // ---- row sums in increasing j (non-zeros only), the uniform fallback
+        if (half == 0) {
+          float sm = 0.0f;
+          for (int w = 0; w < KW; ++w) {
+            uint32_t bits = bm[p * KW + w];
+            while (bits) {
+              const int j = 32 * w + __ffs(bits) - 1;
+              bits &= bits - 1;
+              sm += Z[(size_t)p * K + j];
+            }
+          }
+          rsum[p] = sm;
+          if (pv && !(sm > 0.0f)) atomicOr(A.status, ASOT_FLAG_SOFT_FALLBACK);
+        }
+        named_bar_sync(1, kCompWarps * 32);
+        // ---- codes (z / sum z) and the fp64 point-order histogram: thread per bin j
+        const float unif = 1.0f / (float)K;
+        for (int j = tid; j < K; j += kCompWarps * 32) {
+          double a = acc[j];
+          for (int pp = 0; pp < np; ++pp) {
+            float z;
+            if (!(rsum[pp] > 0.0f)) z = unif;
+            else z = (bm[pp * KW + (j >> 5)] >> (j & 31)) & 1u ? Z[(size_t)pp * K + j] / rsum[pp] : 0.0f;
+            if (A.codes) A.codes[(t0 + pp) * K + j] = z;
+            a += (double)wts[pp] * (double)z;
+          }
+          acc[j] = a;
+        }
+      }
+      named_bar_sync(1, kCompWarps * 32);
+      for (int j = tid; j < K; j += kCompWarps * 32) A.H[i * K + j] = (float)acc[j];
+      // flags: every compute thread reports its own; the weight sum lives in threads p < 128
+      if (nonfinite) atomicOr(A.status, ASOT_FLAG_NONFINITE_INPUT);
+      if (negative) atomicOr(A.status, ASOT_FLAG_BAD_MASS);
+      __shared__ double msh[kTP];
+      if (half == 0) msh[p] = msum;
+      named_bar_sync(1, kCompWarps * 32);
+      if (tid == 0) {
+        double m = 0.0;
+        for (int x = 0; x < kTP; ++x) m += msh[x];
+        if (e0 <= s0) atomicOr(A.status, ASOT_FLAG_EMPTY_DIST);
+        else if (fabs(m - 1.0) > 1e-5) atomicOr(A.status, ASOT_FLAG_BAD_MASS);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(0u) : "memory");
+}
+
+// Dictionary [K, d] -> per 64-anchor chunk [hi | lo] images, each [kb = d/32][64 rows][128 B] SW128
+// K-major (TF32 RNA hi, fp32 remainder lo: the MMA reads its TF32 truncation).
+template <int DP>
+__global__ void dl_image_kernel(const float* __restrict__ dict, int K, uint8_t* __restrict__ img) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < K * DP; idx += gridDim.x * blockDim.x) {
+    const int n = idx / DP, k = idx % DP;
+    const float v = dict[idx];
+    const uint32_t h = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;
+    const float lo = v - __uint_as_float(h);
+    const uint32_t c = n / kCN, r = n % kCN;
+    const uint32_t lin = (uint32_t)(k >> 5) * (kCN * 128) + r * 128u + (uint32_t)(k & 31) * 4u;
+    const uint32_t off = lin ^ (((lin >> 7) & 7u) << 4);
+    uint8_t* base = img + (size_t)c * Cfg<DP>::kStageBytes;
+    *(uint32_t*)(base + off) = h;
+    *(float*)(base + Cfg<DP>::kImgBytes + off) = lo;
+  }
+}
+
+template <int DP>
+size_t smem_bytes(int K) {
+  return 1024 + kStages * Cfg<DP>::kStageBytes + (size_t)K * 8 + (size_t)kTP * (K / 32) * 4 + 3 * kTP * 4 + 128;
+}
+
+}  // namespace dltc
+
+bool soft_dl_tc_supported(int dim, int K) { return (dim == 64 || dim == 128) && K >= 256 && K % 64 == 0 && K <= 1024; }
+
+size_t soft_dl_tc_workspace_bytes(int dim, int K, int sms) {
+  return (size_t)sms * dltc::kTP * K * 4 + (size_t)K * dim * 8 + 1024;   // codes scratch + images
+}
+
+cudaError_t launch_soft_dl_tc(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist, int dim,
+                              const float* dict, int K, int n_layers, int hidden, const float* V1, const float* c1,
+                              const float* v2, const float* c2, float* H, float* codes, uint8_t* ws, uint32_t* status,
+                              int sms, cudaStream_t s) {
+  const int grid = (int)(n_dist < sms ? n_dist : sms);
+  if (grid < 1) return cudaSuccess;
+  float* zbuf = (float*)ws;
+  uint8_t* img = (uint8_t*)(((uintptr_t)(ws + (size_t)sms * dltc::kTP * K * 4) + 1023) & ~(uintptr_t)1023);
+  dltc::Args A{points, offsets, weights, n_dist, K, hidden, V1, c1, v2, c2, dict, img, n_layers, H, codes, zbuf, status};
+  cudaError_t e;
+  if (dim == 64) {
+    dltc::dl_image_kernel<64><<<256, 256, 0, s>>>(dict, K, img);
+    const size_t smem = dltc::smem_bytes<64>(K);
+    e = cudaFuncSetAttribute(dltc::soft_dl_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dltc::soft_dl_tc_kernel<64><<<grid, dltc::kThreads, smem, s>>>(A);
+  } else {
+    dltc::dl_image_kernel<128><<<256, 256, 0, s>>>(dict, K, img);
+    const size_t smem = dltc::smem_bytes<128>(K);
+    e = cudaFuncSetAttribute(dltc::soft_dl_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dltc::soft_dl_tc_kernel<128><<<grid, dltc::kThreads, smem, s>>>(A);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace asot
