@@ -225,8 +225,8 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
  * (n_anchors % 64 == 0) runs the tensor-core encoder (asot_soft_dl_tc.cu: the dense product
  * g = W^T r on tcgen05 3xTF32, the sparse r = W z - x on CUDA cores), which keeps each CTA's tile
  * of codes in this scratch (#SMs x 128 x n_anchors floats, L2-resident) next to the split
- * dictionary images; 0 otherwise.  A smaller workspace (or NULL) selects the CUDA-core kernels. */
-size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors);
+ * dictionary images and lambda per point (n_points = offsets_host[n_dist]); 0 otherwise.  A smaller workspace (or NULL) selects the CUDA-core kernels. */
+size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors, int64_t n_points);
 
 /* ASOT-ML anchor cost: C_s[u, v] = ||M w_u - M w_v||_2, M [h, dim] row-major, anchors
  * [n_anchors, dim]; bitwise symmetric, zero diagonal.  normalize != 0 divides by the max entry

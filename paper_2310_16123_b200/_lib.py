@@ -43,7 +43,7 @@ _SIGS = {
                                  c_vp, c_vp, c_vp, c_vp, c_vp]),
     "asot_map_soft_dl": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
-    "asot_map_soft_dl_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "asot_map_soft_dl_workspace_bytes": (c_size, [c_i32, c_i32, c_i64]),
     "asot_mahalanobis_cost": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
     "asot_mahalanobis_workspace_bytes": (c_size, [c_i32, c_i32]),
     "asot_kmeans_minibatch": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp,

@@ -287,7 +287,7 @@ def map_soft_dl(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tens
     oh, N, T, H, codes, st = _soft_common(points, offsets, weights, offsets_host, int(K), status,
                                           want_codes)
     L = _lib_handle()
-    nbytes = int(L.asot_map_soft_dl_workspace_bytes(int(d), int(K)))
+    nbytes = int(L.asot_map_soft_dl_workspace_bytes(int(d), int(K), int(T)))
     ws = _ws(workspace, points.device).get(nbytes) if nbytes > 0 else None
     _check(L.asot_map_soft_dl(
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(dictionary), int(K),

@@ -434,7 +434,7 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
   cudaStream_t s = (cudaStream_t)stream;
   Nvtx range("asot next1 map_soft_dl");
   ProfScope prof(ASOT_PROF_MAP, s);
-  const size_t need = asot_map_soft_dl_workspace_bytes(dim, n_anchors);
+  const size_t need = asot_map_soft_dl_workspace_bytes(dim, n_anchors, offsets_host[n_dist]);
   const bool aligned = ((uintptr_t)points & 15u) == 0 && ((uintptr_t)dictionary & 15u) == 0;
   // large dictionaries: the tensor-core kernel (default) or, for cross-checks
   // (ASOT_SOFT_DL_GENERIC=sparse), the sparse-code CUDA-core kernel; otherwise / without a
@@ -444,7 +444,7 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
     if (!gen) {
       ASOT_LAUNCH(asot::launch_soft_dl_tc(points, offsets, weights, n_dist, dim, dictionary, n_anchors,
                                           n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
-                                          (uint8_t*)workspace, status, device_sms(), s));
+                                          (uint8_t*)workspace, status, device_sms(), offsets_host[n_dist], s));
       return ASOT_OK;
     }
     if (std::string(gen) == "sparse") {
@@ -460,9 +460,9 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
   return ASOT_OK;
 }
 
-size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors) {
+size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors, int64_t n_points) {
   if (!asot::soft_dl_tc_supported(dim, n_anchors)) return 0;
-  const size_t a = asot::soft_dl_tc_workspace_bytes(dim, n_anchors, device_sms());
+  const size_t a = asot::soft_dl_tc_workspace_bytes(dim, n_anchors, device_sms(), n_points);
   const size_t b = asot::soft_dl_sparse_workspace_bytes(n_anchors, device_sms());
   return a > b ? a : b;
 }

@@ -359,11 +359,11 @@ cudaError_t read_kernel_clock_tc2(long long* host4);
 bool soft_dl_sparse_supported(int dim, int K);
 size_t soft_dl_sparse_workspace_bytes(int K, int sms);
 bool soft_dl_tc_supported(int dim, int K);
-size_t soft_dl_tc_workspace_bytes(int dim, int K, int sms);
+size_t soft_dl_tc_workspace_bytes(int dim, int K, int sms, int64_t T);
 cudaError_t launch_soft_dl_tc(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist, int dim,
                               const float* dict, int K, int n_layers, int hidden, const float* V1, const float* c1,
                               const float* v2, const float* c2, float* H, float* codes, uint8_t* ws, uint32_t* status,
-                              int sms, cudaStream_t s);
+                              int sms, int64_t T, cudaStream_t s);
 cudaError_t launch_soft_dl_sparse(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist,
                                   int dim, const float* dict, int K, int n_layers, int hidden, const float* V1,
                                   const float* c1, const float* v2, const float* c2, float* H, float* codes,

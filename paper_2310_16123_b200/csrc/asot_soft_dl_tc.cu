@@ -32,7 +32,7 @@ using namespace ::asot::ptx;
 
 constexpr int kTP = 128;                 // points per tile (MMA M)
 constexpr int kCN = 64;                  // anchors per chunk (MMA N)
-constexpr int kCompWarps = 8;
+constexpr int kCompWarps = 16;
 constexpr int kThreads = kCompWarps * 32 + 64;   // + MMA warp + TMA producer warp
 constexpr int kStages = 2;
 
@@ -56,6 +56,7 @@ struct Args {
   const float* c2;
   const float* dict;        // [K, d] fp32
   const uint8_t* img;       // [K / 64 chunks][hi | lo][d / 32 kb][64 rows][128 B]
+  const float* lam;         // [T] lambda per point (dl_lambda_kernel)
   int n_layers;
   float* H;
   float* codes;
@@ -64,10 +65,6 @@ struct Args {
 };
 
 __device__ __forceinline__ float softplus_f(float t) { return t > 30.0f ? t : log1pf(expf(t)); }
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  tmem_st16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(&r[0]));
-  tmem_st16(taddr + 16, *reinterpret_cast<const uint32_t(*)[16]>(&r[16]));
-}
 
 template <int DP>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -97,7 +94,7 @@ soft_dl_tc_kernel(Args A) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
       mbar_init(bar_dfull + 8 * s, 1);
-      mbar_init(bar_dfree + 8 * s, kCompWarps);
+      mbar_init(bar_dfree + 8 * s, kCompWarps / 2);   // the 8 warps of D[s]'s epilogue group
     }
     mbar_init(bar_a, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -165,42 +162,31 @@ soft_dl_tc_kernel(Args A) {
       }
     }
   } else {
-    // ------------------------------------------------------------------ compute warps (0..7)
-    const int q = warp & 3, half = warp >> 2;
+    // ------------------------------------------------------------------ compute warps (0..15)
+    // warp w: TMEM lane quarter q = w % 4 (point p = 32 q + lane), group g = w / 4.  r phase: the
+    // four threads of a point own d/4 dims each.  Epilogue: group g handles the chunks that land
+    // in D[g / 2] (so two chunks are drained at once), 32 of their 64 columns (g % 2) = one
+    // bitmap word per thread and chunk.
+    const int q = warp & 3, g = warp >> 2;
     const int p = q * 32 + lane;                       // TMEM lane == point of the tile
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    constexpr int RD = DP / 2;                         // dims of r per thread (two threads per point)
+    constexpr int RD = DP / 4;
+    constexpr int kCT = kCompWarps * 32;
+    const int my_db = g >> 1, half = g & 1;
     uint32_t it = 0;
     for (int64_t i = blockIdx.x; i < A.n_dist; i += gridDim.x) {
       const int64_t s0 = A.offsets[i], e0 = A.offsets[i + 1];
-      named_bar_sync(1, kCompWarps * 32);
-      for (int j = tid; j < K; j += kCompWarps * 32) acc[j] = 0.0;
+      named_bar_sync(1, kCT);
+      for (int j = tid; j < K; j += kCT) acc[j] = 0.0;
       bool nonfinite = false, negative = false;
       double msum = 0.0;
       for (int64_t t0 = s0; t0 < e0; t0 += kTP) {
         const int np = (int)min((int64_t)kTP, e0 - t0);
         const bool pv = p < np;
         const float* xp = A.points + (t0 + (pv ? p : 0)) * DP;
-        named_bar_sync(1, kCompWarps * 32);   // previous tile's final pass is done
-        for (int x = tid; x < kTP * KW; x += kCompWarps * 32) bm[x] = 0u;   // z^(0) = 0 (R#27)
-        {
-          // lambda_p = softplus(v2 . relu(V1^T x_p + c1) + c2): the two threads of a point split
-          // the hidden units, partial sums meet in rsum (free until the row sums)
-          float lsum = 0.0f;
-          const int hh = (A.hidden + 1) / 2, c_lo = half * hh, c_hi = min(A.hidden, c_lo + hh);
-          for (int c = c_lo; c < c_hi; ++c) {
-            float a = A.c1[c];
-            for (int k = 0; k < DP; ++k) a = fmaf(pv ? __ldg(xp + k) : 0.0f, __ldg(A.V1 + (int64_t)k * A.hidden + c), a);
-            lsum = fmaf(fmaxf(a, 0.0f), __ldg(A.v2 + c), lsum);
-          }
-          if (half == 1) rsum[p] = lsum;
-          named_bar_sync(1, kCompWarps * 32);
-          if (half == 0) lam[p] = softplus_f((rsum[p] + lsum) + A.c2[0]);
-        }
-        if (half == 0) {
-          bool nf = false;
-          for (int k = 0; k < DP; ++k) nf |= pv && !isfinite(__ldg(xp + k));
-          nonfinite |= nf;
+        named_bar_sync(1, kCT);   // previous tile's final pass is done
+        for (int x = tid; x < kTP * KW; x += kCT) bm[x] = 0u;   // z^(0) = 0 (R#27)
+        if (g == 0) {
           const float w = pv ? A.weights[t0 + p] : 0.0f;
           if (pv) {
             nonfinite |= !isfinite(w);
@@ -208,8 +194,15 @@ soft_dl_tc_kernel(Args A) {
             msum += (double)w;
           }
           wts[p] = w;
+          lam[p] = pv ? A.lam[t0 + p] : 0.0f;
         }
-        named_bar_sync(1, kCompWarps * 32);
+        {
+          bool nf = false;
+          for (int k = g * RD; k < (g + 1) * RD; ++k) nf |= pv && !isfinite(__ldg(xp + k));
+          nonfinite |= nf;
+        }
+        named_bar_sync(1, kCT);
+        const float lp = lam[p];
         for (int layer = 0; layer < A.n_layers; ++layer) {
           // ---- r = W z - x (non-zero z_j in increasing j), split into TF32 hi / lo -> TMEM A
           {
@@ -223,71 +216,83 @@ soft_dl_tc_kernel(Args A) {
                   const int j = 32 * w + __ffs(bits) - 1;
                   bits &= bits - 1;
                   const float zj = Z[(size_t)p * K + j];
-                  const float4* wr = reinterpret_cast<const float4*>(A.dict + (int64_t)j * DP + half * RD);
+                  const float4* wr = reinterpret_cast<const float4*>(A.dict + (int64_t)j * DP + g * RD);
+                  float4 w4[RD / 4];
+#pragma unroll
+                  for (int k4 = 0; k4 < RD / 4; ++k4) w4[k4] = __ldg(wr + k4);
 #pragma unroll
                   for (int k4 = 0; k4 < RD / 4; ++k4) {
-                    const float4 w4 = __ldg(wr + k4);
-                    r[4 * k4] = fmaf(zj, w4.x, r[4 * k4]);
-                    r[4 * k4 + 1] = fmaf(zj, w4.y, r[4 * k4 + 1]);
-                    r[4 * k4 + 2] = fmaf(zj, w4.z, r[4 * k4 + 2]);
-                    r[4 * k4 + 3] = fmaf(zj, w4.w, r[4 * k4 + 3]);
+                    r[4 * k4] = fmaf(zj, w4[k4].x, r[4 * k4]);
+                    r[4 * k4 + 1] = fmaf(zj, w4[k4].y, r[4 * k4 + 1]);
+                    r[4 * k4 + 2] = fmaf(zj, w4[k4].z, r[4 * k4 + 2]);
+                    r[4 * k4 + 3] = fmaf(zj, w4[k4].w, r[4 * k4 + 3]);
                   }
                 }
               }
             }
 #pragma unroll
-            for (int b = 0; b < RD; b += 32) {
-              uint32_t hi[32], lo[32];
+            for (int b = 0; b < RD; b += 16) {
+              uint32_t hi[16], lo[16];
 #pragma unroll
-              for (int k = 0; k < 32; ++k) {
-                const float x = pv ? __ldg(xp + half * RD + b + k) : 0.0f;
+              for (int k = 0; k < 16; ++k) {
+                const float x = pv ? __ldg(xp + g * RD + b + k) : 0.0f;
                 const float v = r[b + k] - x;
                 const uint32_t h = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
                 hi[k] = h;
                 lo[k] = __float_as_uint(v - __uint_as_float(h));
               }
-              tmem_st32(lane_off + (uint32_t)(half * RD + b), hi);
-              tmem_st32(lane_off + (uint32_t)(DP + half * RD + b), lo);
+              tmem_st16(lane_off + (uint32_t)(g * RD + b), hi);
+              tmem_st16(lane_off + (uint32_t)(DP + g * RD + b), lo);
             }
             tmem_wait_st();
             tc_fence_before();
-            named_bar_sync(1, kCompWarps * 32);   // (also: the bitmap reads above are done)
+            named_bar_sync(1, kCT);   // (also: the bitmap reads above are done)
             if (tid == 0) mbar_arrive_local(bar_a);
           }
-          // ---- chunks: z <- max(0, z - g - lambda); bitmap words 2c + half rebuilt
-          const float lp = lam[p];
+          // ---- chunks: z <- max(0, z - g - lambda); each thread rewrites bitmap word 2c + half
+          // of its point.  Codes are stored only for words with a non-zero and read only for
+          // words that had one (the rest are exactly 0).
           for (int c = 0; c < nchunks; ++c, ++it) {
             const uint32_t db = it & 1;
+            if ((int)db != my_db) continue;
             mbar_wait(bar_dfull + 8 * db, (it >> 1) & 1);
             tc_fence_after();
-            uint32_t g[32];
+            uint32_t gv[32];
             const uint32_t dcol = C::kDCol0 + kCN * db + 32 * half;
-            tmem_ld16u(lane_off + dcol, *reinterpret_cast<uint32_t(*)[16]>(&g[0]));
-            tmem_ld16u(lane_off + dcol + 16, *reinterpret_cast<uint32_t(*)[16]>(&g[16]));
+            tmem_ld16u(lane_off + dcol, *reinterpret_cast<uint32_t(*)[16]>(&gv[0]));
+            tmem_ld16u(lane_off + dcol + 16, *reinterpret_cast<uint32_t(*)[16]>(&gv[16]));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_local(bar_dfree + 8 * db);   // D[db] may be overwritten
             const int j0 = c * kCN + 32 * half;
+            const int wi = p * KW + (j0 >> 5);
+            const uint32_t old = layer > 0 ? bm[wi] : 0u;
             float4* zp = reinterpret_cast<float4*>(Z + (size_t)p * K + j0);
+            float zn[32];
             uint32_t mask = 0u;
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
-              float4 zo = layer > 0 ? zp[e4] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-              float zn[4] = {zo.x, zo.y, zo.z, zo.w};
+              const float4 zo = old ? zp[e4] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+              const float zz[4] = {zo.x, zo.y, zo.z, zo.w};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                zn[u] = fmaxf(0.0f, (zn[u] - __uint_as_float(g[4 * e4 + u])) - lp);
-                if (zn[u] > 0.0f) mask |= 1u << (4 * e4 + u);
+                const float v = fmaxf(0.0f, (zz[u] - __uint_as_float(gv[4 * e4 + u])) - lp);
+                zn[4 * e4 + u] = v;
+                if (v > 0.0f) mask |= 1u << (4 * e4 + u);
               }
-              zp[e4] = make_float4(zn[0], zn[1], zn[2], zn[3]);
             }
-            bm[p * KW + (j0 >> 5)] = pv ? mask : 0u;
+            if (!pv) mask = 0u;
+            if (mask) {
+#pragma unroll
+              for (int e4 = 0; e4 < 8; ++e4) zp[e4] = make_float4(zn[4 * e4], zn[4 * e4 + 1], zn[4 * e4 + 2], zn[4 * e4 + 3]);
+            }
+            bm[wi] = mask;
           }
-          named_bar_sync(1, kCompWarps * 32);   // codes + bitmap of this layer complete
+          named_bar_sync(1, kCT);   // codes + bitmap of this layer complete
         }
         // ---- row sums in increasing j (non-zeros only), the uniform fallback
-        if (half == 0) {
+        if (g == 0) {
           float sm = 0.0f;
           for (int w = 0; w < KW; ++w) {
             uint32_t bits = bm[p * KW + w];
@@ -300,10 +305,10 @@ soft_dl_tc_kernel(Args A) {
           rsum[p] = sm;
           if (pv && !(sm > 0.0f)) atomicOr(A.status, ASOT_FLAG_SOFT_FALLBACK);
         }
-        named_bar_sync(1, kCompWarps * 32);
+        named_bar_sync(1, kCT);
         // ---- codes (z / sum z) and the fp64 point-order histogram: thread per bin j
         const float unif = 1.0f / (float)K;
-        for (int j = tid; j < K; j += kCompWarps * 32) {
+        for (int j = tid; j < K; j += kCT) {
           double a = acc[j];
           for (int pp = 0; pp < np; ++pp) {
             float z;
@@ -315,14 +320,14 @@ soft_dl_tc_kernel(Args A) {
           acc[j] = a;
         }
       }
-      named_bar_sync(1, kCompWarps * 32);
-      for (int j = tid; j < K; j += kCompWarps * 32) A.H[i * K + j] = (float)acc[j];
-      // flags: every compute thread reports its own; the weight sum lives in threads p < 128
+      named_bar_sync(1, kCT);
+      for (int j = tid; j < K; j += kCT) A.H[i * K + j] = (float)acc[j];
+      // flags: every compute thread reports its own; the weight sums live in group 0
       if (nonfinite) atomicOr(A.status, ASOT_FLAG_NONFINITE_INPUT);
       if (negative) atomicOr(A.status, ASOT_FLAG_BAD_MASS);
       __shared__ double msh[kTP];
-      if (half == 0) msh[p] = msum;
-      named_bar_sync(1, kCompWarps * 32);
+      if (g == 0) msh[p] = msum;
+      named_bar_sync(1, kCT);
       if (tid == 0) {
         double m = 0.0;
         for (int x = 0; x < kTP; ++x) m += msh[x];
@@ -335,6 +340,30 @@ soft_dl_tc_kernel(Args A) {
   __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(0u) : "memory");
+}
+
+// lambda_p = softplus(v2 . relu(V1^T x_p + c1) + c2) for every point (R#24, R#26): thread per
+// point, hidden units in order, V1 reads broadcast across the warp
+template <int DP>
+__global__ void dl_lambda_kernel(const float* __restrict__ points, int64_t T, const float* __restrict__ V1,
+                                 const float* __restrict__ c1, const float* __restrict__ v2,
+                                 const float* __restrict__ c2, int hidden, float* __restrict__ lam) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < T; p += (int64_t)gridDim.x * blockDim.x) {
+    float x[DP];
+#pragma unroll
+    for (int k4 = 0; k4 < DP / 4; ++k4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(points + p * DP) + k4);
+      x[4 * k4] = v.x; x[4 * k4 + 1] = v.y; x[4 * k4 + 2] = v.z; x[4 * k4 + 3] = v.w;
+    }
+    float lsum = 0.0f;
+    for (int c = 0; c < hidden; ++c) {
+      float a = __ldg(c1 + c);
+#pragma unroll
+      for (int k = 0; k < DP; ++k) a = fmaf(x[k], __ldg(V1 + (int64_t)k * hidden + c), a);
+      lsum = fmaf(fmaxf(a, 0.0f), __ldg(v2 + c), lsum);
+    }
+    lam[p] = softplus_f(lsum + c2[0]);
+  }
 }
 
 // Dictionary [K, d] -> per 64-anchor chunk [hi | lo] images, each [kb = d/32][64 rows][128 B] SW128
@@ -364,27 +393,33 @@ size_t smem_bytes(int K) {
 
 bool soft_dl_tc_supported(int dim, int K) { return (dim == 64 || dim == 128) && K >= 256 && K % 64 == 0 && K <= 1024; }
 
-size_t soft_dl_tc_workspace_bytes(int dim, int K, int sms) {
-  return (size_t)sms * dltc::kTP * K * 4 + (size_t)K * dim * 8 + 1024;   // codes scratch + images
+size_t soft_dl_tc_workspace_bytes(int dim, int K, int sms, int64_t T) {
+  // codes scratch + images + lambda per point
+  return (size_t)sms * dltc::kTP * K * 4 + (size_t)K * dim * 8 + 1024 + (size_t)(T > 0 ? T : 1) * 4 + 256;
 }
 
 cudaError_t launch_soft_dl_tc(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist, int dim,
                               const float* dict, int K, int n_layers, int hidden, const float* V1, const float* c1,
                               const float* v2, const float* c2, float* H, float* codes, uint8_t* ws, uint32_t* status,
-                              int sms, cudaStream_t s) {
+                              int sms, int64_t T, cudaStream_t s) {
   const int grid = (int)(n_dist < sms ? n_dist : sms);
   if (grid < 1) return cudaSuccess;
   float* zbuf = (float*)ws;
   uint8_t* img = (uint8_t*)(((uintptr_t)(ws + (size_t)sms * dltc::kTP * K * 4) + 1023) & ~(uintptr_t)1023);
-  dltc::Args A{points, offsets, weights, n_dist, K, hidden, V1, c1, v2, c2, dict, img, n_layers, H, codes, zbuf, status};
+  float* lam = (float*)(img + (size_t)K * dim * 8);
+  dltc::Args A{points, offsets, weights, n_dist, K, hidden, V1, c1, v2, c2, dict, img, lam, n_layers, H, codes, zbuf,
+               status};
+  const int lblocks = (int)((T + 255) / 256 < 4 * sms ? (T + 255) / 256 : 4 * sms);
   cudaError_t e;
   if (dim == 64) {
+    if (T > 0) dltc::dl_lambda_kernel<64><<<lblocks, 256, 0, s>>>(points, T, V1, c1, v2, c2, hidden, lam);
     dltc::dl_image_kernel<64><<<256, 256, 0, s>>>(dict, K, img);
     const size_t smem = dltc::smem_bytes<64>(K);
     e = cudaFuncSetAttribute(dltc::soft_dl_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dltc::soft_dl_tc_kernel<64><<<grid, dltc::kThreads, smem, s>>>(A);
   } else {
+    if (T > 0) dltc::dl_lambda_kernel<128><<<lblocks, 256, 0, s>>>(points, T, V1, c1, v2, c2, hidden, lam);
     dltc::dl_image_kernel<128><<<256, 256, 0, s>>>(dict, K, img);
     const size_t smem = dltc::smem_bytes<128>(K);
     e = cudaFuncSetAttribute(dltc::soft_dl_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
