@@ -256,29 +256,44 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         if (last) tmem_wait_st();
       }
     } else if (issuer) {
+      // Issue order: input chunks 0 .. NCH-3 for every output chunk; then (NCH-2, 0),
+      // (NCH-2, 1), (NCH-1, 0), (NCH-2, 2), (NCH-2, 3), (NCH-1, 1), (NCH-1, 2), (NCH-1, 3): output
+      // chunk 0 completes five parts before the phase ends (kc-major: three), so its epilogue --
+      // the one the next phase's first parts wait for -- has more cover.  Each output chunk still
+      // accumulates its input chunks in order.
+      auto part = [&](int f, int kc, int nc) {
+        const uint32_t a_col = (uint32_t)((f & 1) * 256 + kc * kChunk);
+        const uint32_t d_col = (uint32_t)(((f + 1) & 1) * 256);
+        const uint64_t desc = gdesc0 + (uint64_t)((kc * 2 * 16384 + nc * 4096) >> 4);
+        if (DBG != 2) issue_part(a_col, d_col + nc * kChunk, desc, kc > 0 ? 1u : 0u);
+        if (kc == NCH - 1) mma2_commit_mc(bar_mma0 + 8 * nc);
+      };
+      auto gate = [&](int f, int kc) {
+        mbar_wait(bar_epi0 + 8 * kc, epi_par);
+        tc_fence_after();
+        if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && lane == 0 && f < 64)
+          g_tc2_trace[2][f * 4 + kc] = clock64();
+      };
       for (int f = 0; f < 2 * iters; ++f) {
 #pragma unroll 1
-        for (int kc = 0; kc < NCH; ++kc) {
-          mbar_wait(bar_epi0 + 8 * kc, epi_par);
-          tc_fence_after();
-          if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && lane == 0 && f < 64)
-            g_tc2_trace[2][f * 4 + kc] = clock64();
+        for (int kc = 0; kc < NCH - 2; ++kc) {
+          gate(f, kc);
           if (elect_one()) {
-            // part (kc, nc): D(R_d)[:, nc*64 +: 64] (+)= A(R_a)[:, kc*64 +: 64] x K[kc, nc]
-            const uint32_t a_col = (uint32_t)((f & 1) * 256 + kc * kChunk);
-            const uint32_t d_col = (uint32_t)(((f + 1) & 1) * 256);
-            const uint64_t desc = gdesc0 + (uint64_t)((kc * 2 * 16384) >> 4);
-            const uint32_t acc0 = kc > 0 ? 1u : 0u;
-#pragma unroll
-            for (int nc = 0; nc < kNChunks; ++nc) {
-              if (nc < NCH) {
-                if (DBG != 2) issue_part(a_col, d_col + nc * kChunk, desc + (uint64_t)((nc * 4096) >> 4), acc0);
-                if (kc == NCH - 1) mma2_commit_mc(bar_mma0 + 8 * nc);
-              }
-            }
+            for (int nc = 0; nc < NCH; ++nc) part(f, kc, nc);
           }
           __syncwarp();
         }
+        const int a = NCH - 2, z = NCH - 1;
+        gate(f, a);
+        if (elect_one()) { part(f, a, 0); part(f, a, 1); }
+        __syncwarp();
+        gate(f, z);
+        if (elect_one()) {
+          part(f, z, 0);
+          for (int nc = 2; nc < NCH; ++nc) part(f, a, nc);
+          for (int nc = 1; nc < NCH; ++nc) part(f, z, nc);
+        }
+        __syncwarp();
         epi_par ^= 1u;
       }
     }  // (the peer's MMA warp idles until the cost)
