@@ -4,8 +4,9 @@ configuration (whole configs, one call):
 * assignments bit-exact for EVERY point of c3 (N = 2000, 349,010 points) and for a seeded 10% of
   c5's distributions (400 of 4000, ~240k points, K = 1024, d = 128), with their H rows
   bit-identical -- the oracle mapping (R#8) fanned out over the host cores (tests/oracle_par.py);
-* >= 2,000 sampled pairs at ASOT_PREC_FP32 (the north star's 1e-4 mode, 3xTF32 streamed kernel)
-  for c4 (N = 8000, Dirichlet weights) and c5 (pairs among the 10% sample), each against the
+* >= 2,000 sampled pairs at ASOT_PREC_FP32 (the north star's 1e-4 mode: BF16x3 resident kernel
+  at K = 256, 3xTF32 streamed at K = 1024) for c4 (N = 8000, Dirichlet weights) and c5 (pairs
+  among the 10% sample), each against the
   oracle evaluated pair by pair on the oracle's own histograms."""
 import numpy as np
 import pytest
@@ -89,7 +90,8 @@ def _fp32_pairs_check(asot, inp, pi, pj, H_o_rows, row_of):
                              offsets_host=inp.offsets, cost_max=1.0, status=st)
     torch.cuda.synchronize()
     asot.check_status(st)
-    assert asot.asot.sinkhorn_kernel_kind(inp.n_anchors, asot.FP32) == 5     # 3xTF32 streamed kernel
+    # K = 256: the BF16x3 resident CTA-pair kernel; K = 1024: the 3xTF32 streamed kernel
+    assert asot.asot.sinkhorn_kernel_kind(inp.n_anchors, asot.FP32) == (10 if inp.n_anchors <= 256 else 5)
     c_o, fl = O.pair_costs(H_o_rows, inp.cost, inp.eps, inp.iters, row_of[pi], row_of[pj])
     assert not fl.any()
     Dg = D.cpu().numpy()
