@@ -644,6 +644,30 @@ def main():
                 flops_pt = 2 * d_ * h_ + 2 * h_ + soft_model.n_layers * 4 * d_ * K_
                 kname = f"soft_map_kernel<DL> ({soft_model.n_layers} near-one-hot layers, fused a' = Z^T a)"
             bytes_ = T_rank * (4 * d_ + 4) + inp.n_dist * K_ * 4
+            dl_tc = (args.mapping == "dl" and not os.environ.get("ASOT_SOFT_DL_GENERIC")
+                     and asot.asot._lib_handle().asot_map_soft_dl_workspace_bytes(d_, K_, T_rank) > 0)
+            if dl_tc:
+                # g = W^T r on the tensor cores: 3 TF32 MMAs per product (3xTF32), the sparse r
+                # gather and the lambda MLP on the CUDA cores (asot_soft_dl_tc.cu)
+                L_ = soft_model.n_layers
+                g_flops = L_ * 2 * d_ * K_ * T_rank
+                tpeak = peaks["bf16_tflops"] * TF32_OVER_BF16
+                mapping = {
+                    "kernel": f"soft_dl_tc_kernel ({L_} near-one-hot layers; g = W^T r on tcgen05 3xTF32, "
+                              "sparse r = W z - x gather)",
+                    "ms_per_launch": map_avg_ms, "points_per_launch": T_rank,
+                    "g_flops_per_point": L_ * 2 * d_ * K_,
+                    "bound": "tensor",
+                    "g_tflops_algorithmic": g_flops / (map_avg_ms / 1e3) / 1e12,
+                    "tf32_issued_tflops": 3 * g_flops / (map_avg_ms / 1e3) / 1e12,
+                    "tf32_peak_tflops": tpeak,
+                    "tf32_frac": 3 * g_flops / (map_avg_ms / 1e3) / 1e12 / tpeak,
+                    "hbm_gbs": bytes_ / (map_avg_ms / 1e3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                    "share_of_step": map_ms / max(tot_ms, 1e-9),
+                    "note": "tf32_frac counts the three TF32 MMAs per product against dense TF32 "
+                            "(measured bf16 x 1.1/2.25); the r gather between layers leaves the "
+                            "tensor pipe idle (DESIGN.md, DL TC kernel)"}
+        if T_rank is not None and args.mapping != "onehot" and mapping is None:
             mapping = {
                 "kernel": kname, "ms_per_launch": map_avg_ms, "points_per_launch": T_rank,
                 "flops_per_point": flops_pt,
@@ -654,7 +678,7 @@ def main():
                 "share_of_step": map_ms / max(tot_ms, 1e-9),
                 "note": "CUDA-core fp32 GEMM-like tiles (16 points x weights from L2/SMEM); "
                         "bound: FP32 FFMA peak 148 x 128 x 2 x 1.965 GHz"}
-        elif T_rank is not None:
+        elif T_rank is not None and args.mapping == "onehot":
             d_, K_ = inp.dim, inp.n_anchors
             bytes_ = T_rank * (4 * d_ + 4) + K_ * d_ * 4     # points in, assignment out, anchors
             lane_ops = 2 * K_ * d_ * T_rank                   # FSUB + FFMA per (point, anchor, dim)

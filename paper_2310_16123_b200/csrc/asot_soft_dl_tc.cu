@@ -7,9 +7,11 @@
 //
 // Per CTA a tile of 128 points of one distribution (persistent CTAs loop over distributions):
 //   * r = W z - x is a gather over the non-zero codes (near-one-hot: 8-16 of 1024 at c5, 15-61 of
-//     256 at c3; asot_soft_dl_sparse.cu) on the CUDA cores, split x = x_hi + x_lo with
-//     x_hi = RNA_tf32(x) (3xTF32, fp32-accurate: R#22's split) and stored into TMEM as the MMA's
-//     A operand: thread p of warp w (lane quarter w % 4) owns point p = TMEM lane p;
+//     256 at c3; asot_soft_dl_sparse.cu) on the CUDA cores: warp per point, its non-zeros decoded
+//     lane-parallel from the bitmap, 32 / (d / 32) coalesced dictionary rows in flight, the row
+//     r - x staged in SMEM; then split x = x_hi + x_lo with x_hi = RNA_tf32(x) (3xTF32,
+//     fp32-accurate: R#22's split) and stored into TMEM as the MMA's A operand by thread p of
+//     warp w (lane quarter w % 4), which owns point p = TMEM lane p;
 //   * g = W^T r, [128 points x d] x [d x K], is `tcgen05.mma.cta_group::1.kind::tf32` with
 //     A = R from TMEM and B = 64-anchor chunks of the dictionary (pre-split K_hi / K_lo images,
 //     SW128 K-major, streamed by a TMA producer warp through a double-buffered SMEM ring), three
@@ -42,6 +44,8 @@ struct Cfg {
   static constexpr uint32_t kStageBytes = 2 * kImgBytes;               // hi | lo
   static constexpr uint32_t kDCol0 = 256;                              // D buffers
 };
+template <int DP>
+constexpr int kStgOf = DP + 4;           // staging row stride (floats): conflict-free LDS.128 by lane = point
 
 struct Args {
   const float* points;
@@ -70,6 +74,7 @@ template <int DP>
 __global__ void __launch_bounds__(kThreads, 1)
 soft_dl_tc_kernel(Args A) {
   using C = Cfg<DP>;
+  constexpr int kStg = kStgOf<DP>;
   constexpr uint32_t kIdesc = make_idesc_tf32(kTP, kCN);
   extern __shared__ uint8_t dl_smem_raw[];
   uint8_t* smem = dl_smem_raw + ((1024u - (smem_u32(dl_smem_raw) & 1023u)) & 1023u);
@@ -80,7 +85,8 @@ soft_dl_tc_kernel(Args A) {
   float* lam = (float*)(bm + kTP * KW);                              // [kTP]
   float* wts = lam + kTP;                                            // [kTP]
   float* rsum = wts + kTP;                                           // [kTP]
-  uint64_t* bars = (uint64_t*)(((uintptr_t)(rsum + kTP) + 7) & ~(uintptr_t)7);
+  float* stg = rsum + kTP;                                           // [kTP][kStg]: r - x rows
+  uint64_t* bars = (uint64_t*)(((uintptr_t)(stg + kTP * kStg) + 7) & ~(uintptr_t)7);
   // bars: full[2], empty[2], dfull[2], dfree[2], a_ready
   const uint32_t bar_full = smem_u32(&bars[0]), bar_empty = smem_u32(&bars[2]);
   const uint32_t bar_dfull = smem_u32(&bars[4]), bar_dfree = smem_u32(&bars[6]);
@@ -163,8 +169,9 @@ soft_dl_tc_kernel(Args A) {
     }
   } else {
     // ------------------------------------------------------------------ compute warps (0..15)
-    // warp w: TMEM lane quarter q = w % 4 (point p = 32 q + lane), group g = w / 4.  r phase: the
-    // four threads of a point own d/4 dims each.  Epilogue: group g handles the chunks that land
+    // warp w: TMEM lane quarter q = w % 4 (point p = 32 q + lane), group g = w / 4.  r gather:
+    // warp w owns points w + 16 s; TMEM store: the four threads of a point own d/4 dims each.
+    // Epilogue: group g handles the chunks that land
     // in D[g / 2] (so two chunks are drained at once), 32 of their 64 columns (g % 2) = one
     // bitmap word per thread and chunk.
     const int q = warp & 3, g = warp >> 2;
@@ -204,49 +211,138 @@ soft_dl_tc_kernel(Args A) {
         named_bar_sync(1, kCT);
         const float lp = lam[p];
         for (int layer = 0; layer < A.n_layers; ++layer) {
-          // ---- r = W z - x (non-zero z_j in increasing j), split into TF32 hi / lo -> TMEM A
+          // ---- r = W z - x (non-zero z_j in increasing j).  Warp w owns the kPW points
+          // pp = w + 16 s: their non-zeros form one warp-uniform stream (point-major, j increasing)
+          // of which kGB dictionary rows are in flight at a time; each lane owns DP / 32 dims, so a
+          // row is one coalesced 512 B (256 B) read.  The rows are staged through SMEM; the thread
+          // owning TMEM lane p then splits its d/4 slice into TF32 hi / lo for the A operand.
           {
-            float r[RD];
+            constexpr int VEC = DP / 32;
+            constexpr int kPW = kTP / kCompWarps;
+            constexpr int kGB = 32 / VEC;
+            auto row_of = [&](int sl) { return stg + (warp + kCompWarps * sl) * kStg + lane * VEC; };
+            auto store_row = [&](int sl, const float (&v)[VEC]) {
+              float* sr = row_of(sl);
+              if constexpr (VEC == 4) *reinterpret_cast<float4*>(sr) = make_float4(v[0], v[1], v[2], v[3]);
+              else *reinterpret_cast<float2*>(sr) = make_float2(v[0], v[1]);
+            };
+            {
+              const float zero[VEC] = {};
 #pragma unroll
-            for (int k = 0; k < RD; ++k) r[k] = 0.0f;
-            if (layer > 0 && pv) {
-              for (int w = 0; w < KW; ++w) {
-                uint32_t bits = bm[p * KW + w];
-                while (bits) {
-                  const int j = 32 * w + __ffs(bits) - 1;
-                  bits &= bits - 1;
-                  const float zj = Z[(size_t)p * K + j];
-                  const float4* wr = reinterpret_cast<const float4*>(A.dict + (int64_t)j * DP + g * RD);
-                  float4 w4[RD / 4];
+              for (int sl = 0; sl < kPW; ++sl) store_row(sl, zero);
+            }
+            if (layer > 0) {
+              for (int sl = 0; sl < kPW; ++sl) {
+                const int pp = warp + kCompWarps * sl;
+                if (pp >= np) break;
+                // decode the point's non-zeros lane-parallel: lane l holds bitmap word l; entry t of
+                // the (increasing-j) list is found by a shuffle binary search over the inclusive
+                // popcount scan, then __fns picks its bit
+                const uint32_t word = lane < KW ? bm[pp * KW + lane] : 0u;
+                const int cnt = __popc(word);
+                int incl = cnt;
 #pragma unroll
-                  for (int k4 = 0; k4 < RD / 4; ++k4) w4[k4] = __ldg(wr + k4);
+                for (int o = 1; o < 32; o <<= 1) {
+                  const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                  if (lane >= o) incl += t;
+                }
+                const int n = __shfl_sync(0xffffffffu, incl, 31);
+                if (n == 0) continue;
+                float ra[VEC] = {};
+                const float* zrow = Z + (size_t)pp * K;
+                for (int base = 0; base < n; base += 32) {
+                  const int t = base + lane;
+                  int own = 0;
 #pragma unroll
-                  for (int k4 = 0; k4 < RD / 4; ++k4) {
-                    r[4 * k4] = fmaf(zj, w4[k4].x, r[4 * k4]);
-                    r[4 * k4 + 1] = fmaf(zj, w4[k4].y, r[4 * k4 + 1]);
-                    r[4 * k4 + 2] = fmaf(zj, w4[k4].z, r[4 * k4 + 2]);
-                    r[4 * k4 + 3] = fmaf(zj, w4[k4].w, r[4 * k4 + 3]);
+                  for (int st = 16; st >= 1; st >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, incl, own + st - 1);
+                    if (v <= t) own += st;
+                  }
+                  const uint32_t ow = __shfl_sync(0xffffffffu, word, own);
+                  const int oe = __shfl_sync(0xffffffffu, incl - cnt, own);
+                  int jl = 0;
+                  float zl = 0.0f;
+                  if (t < n) {
+                    jl = 32 * own + (int)__fns(ow, 0u, t - oe + 1);
+                    zl = zrow[jl];
+                  }
+                  const int m = min(32, n - base);
+                  for (int u0 = 0; u0 < m; u0 += kGB) {
+                    float rv[kGB][VEC];
+#pragma unroll
+                    for (int u = 0; u < kGB; ++u) {
+                      const int j = __shfl_sync(0xffffffffu, jl, (u0 + u) & 31);
+                      if (u0 + u < m) {
+                        const float* wr = A.dict + (int64_t)j * DP + lane * VEC;
+                        if constexpr (VEC == 4) {
+                          const float4 q4 = __ldg(reinterpret_cast<const float4*>(wr));
+                          rv[u][0] = q4.x; rv[u][1] = q4.y; rv[u][2] = q4.z; rv[u][3] = q4.w;
+                        } else {
+                          const float2 q2 = __ldg(reinterpret_cast<const float2*>(wr));
+                          rv[u][0] = q2.x; rv[u][1] = q2.y;
+                        }
+                      }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kGB; ++u) {
+                      const float zu = __shfl_sync(0xffffffffu, zl, (u0 + u) & 31);   // after the row loads
+                      if (u0 + u < m) {
+#pragma unroll
+                        for (int k = 0; k < VEC; ++k) ra[k] = fmaf(zu, rv[u][k], ra[k]);
+                      }
+                    }
                   }
                 }
+                store_row(sl, ra);
               }
             }
+            // r - x for the warp's valid points (the x rows are coalesced reads, all in flight)
+            {
+              float xv[kPW][VEC];
+#pragma unroll
+              for (int sl = 0; sl < kPW; ++sl) {
+                const int pp = warp + kCompWarps * sl;
+                const float* xr = A.points + (t0 + (pp < np ? pp : 0)) * DP + lane * VEC;
+                if constexpr (VEC == 4) {
+                  const float4 t = __ldg(reinterpret_cast<const float4*>(xr));
+                  xv[sl][0] = t.x; xv[sl][1] = t.y; xv[sl][2] = t.z; xv[sl][3] = t.w;
+                } else {
+                  const float2 t = __ldg(reinterpret_cast<const float2*>(xr));
+                  xv[sl][0] = t.x; xv[sl][1] = t.y;
+                }
+              }
+#pragma unroll
+              for (int sl = 0; sl < kPW; ++sl) {
+                if (warp + kCompWarps * sl >= np) continue;
+                float* sr = row_of(sl);
+                float v[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) v[k] = sr[k] - xv[sl][k];
+                store_row(sl, v);
+              }
+            }
+            named_bar_sync(1, kCT);
 #pragma unroll
             for (int b = 0; b < RD; b += 16) {
               uint32_t hi[16], lo[16];
+              const float4* sp = reinterpret_cast<const float4*>(stg + p * kStg + g * RD + b);
 #pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const float x = pv ? __ldg(xp + g * RD + b + k) : 0.0f;
-                const float v = r[b + k] - x;
-                const uint32_t h = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
-                hi[k] = h;
-                lo[k] = __float_as_uint(v - __uint_as_float(h));
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const float4 v4 = sp[k4];
+                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const uint32_t h = (__float_as_uint(vv[e]) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
+                  hi[4 * k4 + e] = h;
+                  lo[4 * k4 + e] = __float_as_uint(vv[e] - __uint_as_float(h));
+                }
               }
               tmem_st16(lane_off + (uint32_t)(g * RD + b), hi);
               tmem_st16(lane_off + (uint32_t)(DP + g * RD + b), lo);
             }
             tmem_wait_st();
             tc_fence_before();
-            named_bar_sync(1, kCT);   // (also: the bitmap reads above are done)
+            named_bar_sync(1, kCT);   // (also: the bitmap / staging reads above are done)
             if (tid == 0) mbar_arrive_local(bar_a);
           }
           // ---- chunks: z <- max(0, z - g - lambda); each thread rewrites bitmap word 2c + half
@@ -386,7 +482,8 @@ __global__ void dl_image_kernel(const float* __restrict__ dict, int K, uint8_t* 
 
 template <int DP>
 size_t smem_bytes(int K) {
-  return 1024 + kStages * Cfg<DP>::kStageBytes + (size_t)K * 8 + (size_t)kTP * (K / 32) * 4 + 3 * kTP * 4 + 128;
+  return 1024 + kStages * Cfg<DP>::kStageBytes + (size_t)K * 8 + (size_t)kTP * (K / 32) * 4 + 3 * kTP * 4 +
+         (size_t)kTP * kStgOf<DP> * 4 + 128;
 }
 
 }  // namespace dltc
