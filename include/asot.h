@@ -128,8 +128,15 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
  * the workspace (L2-resident).  (Environment ASOT_PAIR_KERNEL=simt selects the fp32 CUDA-core
  * kernel instead, for cross-checks.)  Invalid entries (an index outside [0, n_dist)) give NaN
  * and raise ASOT_FLAG_BAD_INDEX.  n_pairs = 0 returns ASOT_OK at once (pair_i, pair_j and
- * dist_out may then be NULL).  Workspace from asot_pairwise_workspace_bytes(n_dist, n_anchors,
- * prec).  Status: the call's flags are OR-ed into ONE word for the whole list (DESIGN R#33:
+ * dist_out may then be NULL).  Workspace: asot_pairwise_workspace_bytes(n_dist, n_anchors, prec)
+ * runs the list as it is; the larger asot_pairwise_list_workspace_bytes(n_dist, n_anchors, prec,
+ * n_pairs) lets TF32 requests with 32 <= K <= 256 (n_pairs >= 1024, n_dist <= ~2.9e4) serve every
+ * tile of the upper triangle whose 8 x 16 block of i < j pairs the list covers COMPLETELY through
+ * the tile kernels (marginal rows staged in SMEM once per tile; asot_pairs_bucket.cu), the other
+ * entries (i >= j, repeats, partly covered tiles, invalid indices) through the pair-list mode --
+ * stream-ordered, no host synchronisation; the values are those of the tile path (K <= 128:
+ * bitwise the pair-list mode's; 128 < K <= 256: within the TF32 tolerance of either).
+ * (ASOT_PAIR_BUCKET=0 disables it.)  Status: the call's flags are OR-ed into ONE word for the whole list (DESIGN R#33:
  * no per-pair flag array; a flagged run is re-run on a sub-list to locate pairs).  Arguments:
  *   hist     [n_dist, n_anchors] f32 device (rows are a' / b')
  *   cost     [n_anchors, n_anchors] f32 device: C_s symmetric, >= 0, zero diagonal
@@ -144,6 +151,8 @@ asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_
                                    uint32_t* status, void* workspace, size_t workspace_bytes,
                                    void* stream);
 size_t asot_pairwise_workspace_bytes(int64_t n_dist, int32_t n_anchors, asot_precision prec);
+size_t asot_pairwise_list_workspace_bytes(int64_t n_dist, int32_t n_anchors, asot_precision prec,
+                                          int64_t n_pairs);
 
 /* Full pipeline a1-a6 on the tile range [tile_begin, tile_end) (device buffers):
  *   hist_in  NULL: map + histogram all distributions into the workspace first (needs points,

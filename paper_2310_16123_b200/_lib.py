@@ -30,6 +30,7 @@ _SIGS = {
     "asot_pairwise_sinkhorn": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_f32, c_f32, c_i32, c_i32, c_vp,
                                        c_vp, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_pairwise_workspace_bytes": (c_size, [c_i64, c_i32, c_i32]),
+    "asot_pairwise_list_workspace_bytes": (c_size, [c_i64, c_i32, c_i32, c_i64]),
     "asot_distance_matrix": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_f32,
                                      c_f32, c_i32, c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                      c_vp, c_vp, c_vp, c_size, c_vp]),

@@ -446,7 +446,8 @@ def pairwise_sinkhorn(H: torch.Tensor, cost: torch.Tensor, eps: float, iters: in
     cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
     st = new_status(H.device) if status is None else status
     L = _lib_handle()
-    ws = _ws(workspace, H.device).get(L.asot_pairwise_workspace_bytes(int(N), int(K), int(precision)))
+    ws = _ws(workspace, H.device).get(L.asot_pairwise_list_workspace_bytes(int(N), int(K), int(precision),
+                                                                           int(n)))
     _check(L.asot_pairwise_sinkhorn(
         _ptr(H), N, int(K), _ptr(cost), cmax, float(eps), int(iters), int(precision),
         _ptr(pair_i), _ptr(pair_j), n, _ptr(out), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)))

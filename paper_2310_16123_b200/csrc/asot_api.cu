@@ -107,6 +107,19 @@ int pair_kind(int32_t K, asot_precision prec) {
   return prec == ASOT_PREC_FP32 ? 5 : 6;
 }
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
+// Bucketed pair lists (asot_pairs_bucket.cu): the tile kernel that serves the fully covered tiles
+// of a list of pair_kind `lk` (TF32: 7 -> the 1-SM kernel's tile mode, 6 -> the CTA-pair kernel
+// when K <= 256), its unit (1: tiles, 2: block pairs); 0 = the list runs as it is.
+int bucket_tile_kind(int32_t K, asot_precision prec) {
+  static const bool off = getenv("ASOT_PAIR_BUCKET") && std::string(getenv("ASOT_PAIR_BUCKET")) == "0";
+  if (off) return 0;
+  const int lk = pair_kind(K, prec);
+  if (lk == 7) return 1;
+  if (lk == 6 && asot::sinkhorn_tc2_supported(K)) return 2;
+  return 0;
+}
+int bucket_upt(int tk) { return tk == 2 ? 2 : 1; }
+constexpr int64_t kMinBucketPairs = 1024;
 
 int device_sms() {
   int dev = 0, sms = 148;
@@ -242,16 +255,17 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                                           (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink, H, K,
-                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
+                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s,
+                                          ps.units, ps.n_dev));
   } else if (kind == 10) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc6(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
   } else if (kind == 1) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
-                                         gb.gc_img, iters, s));
+                                         gb.gc_img, iters, s, ps.units, ps.n_dev));
   } else if (kind == 7) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
-                                               gb.gc_img, (float*)gb.scratch, iters, s));
+                                               gb.gc_img, (float*)gb.scratch, iters, s, ps.n_dev));
   } else if (kind == 3) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                           gb.gc_img, gb.GC, iters, s));
@@ -266,6 +280,26 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   return ASOT_OK;
 }
 
+// the bucketed layout after the list kind's buffers: the tile kind's Gibbs images (kind 1 shares
+// kind 7's), then the bucket arrays
+struct BucketLayout {
+  GibbsBufs gbt;
+  uint8_t* base = nullptr;
+};
+BucketLayout carve_bucketed(Carver& cv, const GibbsBufs& gbl, int32_t K, int tk, int64_t n_dist, int64_t n_pairs) {
+  BucketLayout L;
+  if (tk == 1) {
+    L.gbt = gbl;
+    L.gbt.kind = 1;
+  } else {
+    L.gbt = carve_gibbs(cv, K, tk, n_dist);
+  }
+  L.base = (uint8_t*)cv.take(asot::pair_bucket_bytes(n_dist, n_pairs, bucket_upt(tk)));
+  return L;
+}
+bool bucketed(int32_t K, asot_precision prec, int64_t n_dist, int64_t n_pairs) {
+  return bucket_tile_kind(K, prec) != 0 && n_pairs >= kMinBucketPairs && asot::pair_bucket_supported(n_dist);
+}
 }  // namespace
 
 extern "C" {
@@ -618,6 +652,16 @@ size_t asot_pairwise_workspace_bytes(int64_t n_dist, int32_t n_anchors, asot_pre
   return cv.used;
 }
 
+
+size_t asot_pairwise_list_workspace_bytes(int64_t n_dist, int32_t n_anchors, asot_precision prec,
+                                          int64_t n_pairs) {
+  Carver cv{nullptr, 0};
+  const GibbsBufs gbl = carve_gibbs(cv, n_anchors, pair_kind(n_anchors, prec), n_dist);
+  if (bucketed(n_anchors, prec, n_dist, n_pairs))
+    carve_bucketed(cv, gbl, n_anchors, bucket_tile_kind(n_anchors, prec), n_dist, n_pairs);
+  return cv.used;
+}
+
 asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_anchors,
                                    const float* cost, float cost_max, float eps, int32_t iters,
                                    asot_precision prec, const int32_t* pair_i,
@@ -634,10 +678,38 @@ asot_status asot_pairwise_sinkhorn(const float* hist, int64_t n_dist, int32_t n_
   Carver cv{(char*)workspace, workspace_bytes};
   GibbsBufs gb = carve_gibbs(cv, n_anchors, pair_kind(n_anchors, prec), n_dist);
   if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (bucketed(n_anchors, prec, n_dist, n_pairs)) {
+    // the workspace of asot_pairwise_list_workspace_bytes: whole tiles on the tile path (the
+    // smaller asot_pairwise_workspace_bytes runs the list as it is)
+    Carver cvb = cv;
+    const int tk = bucket_tile_kind(n_anchors, prec), upt = bucket_upt(tk);
+    const BucketLayout L = carve_bucketed(cvb, gb, n_anchors, tk, n_dist, n_pairs);
+    if (!cvb.overflow) {
+      const int sms = device_sms();
+      const asot::PairBuckets w = asot::carve_pair_buckets(L.base, n_dist, n_pairs, upt);
+      ASOT_LAUNCH(asot::launch_pair_buckets(w, pair_i, pair_j, n_pairs, n_dist, sms, s));
+      const int64_t* n_units = (const int64_t*)&w.cnt[0];
+      const int64_t* n_left = (const int64_t*)&w.cnt[1];
+      asot::PairSource pt{nullptr, nullptr, 0, 0, n_dist};
+      pt.units = w.units;
+      pt.n_dev = n_units;
+      asot::PairSink rt{w.R, nullptr, n_dist, status, 0};
+      asot_status st = run_sinkhorn(pt, rt, hist, cost, eps, n_anchors, iters, L.gbt, 0, w.cap * upt, s);
+      if (st != ASOT_OK) return st;
+      asot::PairSource pl{w.li, w.lj, n_pairs, 0, n_dist};
+      pl.n_dev = n_left;
+      asot::PairSink rl{dist_out, nullptr, n_dist, status, 1};
+      rl.idx = w.lidx;
+      st = run_sinkhorn(pl, rl, hist, cost, eps, n_anchors, iters, gb, 0, 0, s);
+      if (st != ASOT_OK) return st;
+      ASOT_LAUNCH(asot::launch_pair_gather(w, pair_i, pair_j, n_pairs, n_dist, dist_out, sms, s));
+      return ASOT_OK;
+    }
+  }
   asot::PairSource ps{pair_i, pair_j, n_pairs, 0, n_dist};
   asot::PairSink sink{dist_out, nullptr, n_dist, status, 1};
-  return run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, gb, 0, 0,
-                      (cudaStream_t)stream);
+  return run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, gb, 0, 0, s);
 }
 
 size_t asot_distance_matrix_workspace_bytes(int64_t n_dist, int64_t n_points, int32_t n_anchors,

@@ -59,6 +59,11 @@ struct PairSource {
   int64_t n_slots;     // explicit: n_pairs; tile mode: (tile_end - tile_begin) * 128
   int64_t tile_begin;  // tile mode
   int64_t n_dist;
+  // Bucketed pair lists (asot_pairs_bucket.cu; both stay on the device, no host sync):
+  const int32_t* units = nullptr;   // tile mode: the tiles (1-SM kernels) / block pairs (CTA-pair
+                                    // kernels) to run, in this order, instead of a tile range
+  const int64_t* n_dev = nullptr;   // device count: of `units`, or of the explicit list's entries
+                                    // (an upper bound of either is the host-side size)
 };
 
 __device__ inline bool decode_slot(const PairSource& ps, int64_t s, int& i, int& j) {
@@ -78,11 +83,13 @@ struct PairSink {
   int64_t n_dist;
   uint32_t* status;
   int32_t list;   // explicit pair list: an invalid entry is an argument error, not tile padding
+  const int32_t* idx = nullptr;   // slot s is stored at vec[idx[s]] (a compacted sub-list)
 };
 
 // Invalid slots: tile padding (i >= j or j >= N) stores 0 in the packed vector; an explicit-list
 // entry with an index outside [0, N) stores NaN and raises ASOT_FLAG_BAD_INDEX.
 __device__ inline void write_result(const PairSink& out, int64_t s, bool valid, int i, int j, float d) {
+  if (out.idx) s = out.idx[s];
   if (valid) {
     if (!isfinite(d)) atomicOr(out.status, ASOT_FLAG_NONFINITE_OUTPUT);
     if (out.vec) out.vec[s] = d;
@@ -265,21 +272,51 @@ cudaError_t launch_sinkhorn_simt(const PairSource& ps, const PairSink& out, cons
 // pair-list mode (list entries in tiles of 128; marginals from a padded copy Hp [(n_dist+1)][kpad]
 // of scratch, sinkhorn_tc_pairs_scratch_bytes).
 bool sinkhorn_tc_supported(int K);
+// Bucketed explicit pair lists (asot_pairs_bucket.cu): units (upt = 1: tiles; 2: block pairs)
+// fully covered by the list run on the tile path into R; the rest form the sub-list (li, lj, lidx).
+struct PairBuckets {
+  uint32_t* mask;            // [n_units * upt][4] slot bits
+  int32_t* pos;              // [n_units] position in R, or -1
+  unsigned long long* cnt;   // [0] units to run, [1] sub-list length
+  int32_t* units;            // [cap]
+  int32_t* code;             // [n_pairs] tile of the entry, or -1
+  int32_t* li;
+  int32_t* lj;
+  int32_t* lidx;             // [n_pairs] sub-list
+  float* R;                  // [cap * upt * 128]
+  int64_t n_units, cap;
+  int upt;
+};
+bool pair_bucket_supported(int64_t n_dist);
+int64_t pair_bucket_cap(int64_t n_dist, int64_t n_pairs, int upt);
+size_t pair_bucket_bytes(int64_t n_dist, int64_t n_pairs, int upt);
+PairBuckets carve_pair_buckets(uint8_t* base, int64_t n_dist, int64_t n_pairs, int upt);
+cudaError_t launch_pair_buckets(const PairBuckets& w, const int32_t* pi, const int32_t* pj, int64_t n_pairs,
+                                int64_t n_dist, int sms, cudaStream_t s);
+cudaError_t launch_pair_gather(const PairBuckets& w, const int32_t* pi, const int32_t* pj, int64_t n_pairs,
+                               int64_t n_dist, float* dist, int sms, cudaStream_t s);
+// units / n_dev (optional): run the n_dev[0] tiles units[0..) instead of [tile_begin, tile_end)
+// (that range's length is then the host-side upper bound); slot p of units[k] -> vec[128 k + p].
 cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_dist,
                                const PairSink& out, const float* H, int K, const uint32_t* g_img,
-                               const uint32_t* gc_img, int iters, cudaStream_t s);
+                               const uint32_t* gc_img, int iters, cudaStream_t s,
+                               const int32_t* units = nullptr, const int64_t* n_dev = nullptr);
 size_t sinkhorn_tc_pairs_scratch_bytes(int64_t n_dist, int K);
+// n_dev (optional): the list length on the device (n_pairs is then its upper bound)
 cudaError_t launch_sinkhorn_tc_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
                                      const PairSink& out, const float* H, int K, const uint32_t* g_img,
-                                     const uint32_t* gc_img, float* Hp, int iters, cudaStream_t s);
+                                     const uint32_t* gc_img, float* Hp, int iters, cudaStream_t s,
+                                     const int64_t* n_dev = nullptr);
 // tcgen05 cta_group::2 kernel for 128 < K <= 256 (tile mode; images: 2 ranks x 128 KB each).
 bool sinkhorn_tc2_supported(int K);
 size_t sinkhorn_tc2_image_bytes();
 cudaError_t launch_gibbs_prep_tc2(const float* cost, int K, float eps, uint8_t* g_img, uint8_t* gc_img,
                                   cudaStream_t s);
+// units / n_dev (optional): the n_dev[0] block pairs units[0..) (tiles 2b, 2b + 1); slot p of
+// rank r of units[k] -> vec[128 (2k + r) + p].
 cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
-                                cudaStream_t s);
+                                cudaStream_t s, const int32_t* units = nullptr, const int64_t* n_dev = nullptr);
 // Streamed tcgen05 cta_group::2 kernel for 256 < K <= 1024 (tile mode; images 2 x 2 MB; scratch:
 // padded marginals + per-CTA ping-pong X buffers).
 bool sinkhorn_tc4_supported(int K);

@@ -120,8 +120,19 @@ __global__ void __launch_bounds__(Slots<KP>::kAllThreads, 1)
 sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink out,
                    const float* __restrict__ H, int K, const uint32_t* __restrict__ g_img,
                    const uint32_t* __restrict__ gc_img, int iters, const int32_t* __restrict__ pair_i,
-                   const int32_t* __restrict__ pair_j, int64_t n_pairs, const float* __restrict__ Hp) {
+                   const int32_t* __restrict__ pair_j, int64_t n_pairs, const float* __restrict__ Hp,
+                   const int32_t* __restrict__ units, const int64_t* __restrict__ n_dev) {
   using S = Smem<KP>;
+  // device-side counts (bucketed pair lists): the host passed upper bounds
+  if (n_dev != nullptr) {
+    const int64_t c = *n_dev;
+    if constexpr (EX) {
+      n_pairs = c < n_pairs ? c : n_pairs;
+      n_tiles = (n_pairs + kTileSlots - 1) / kTileSlots;
+    } else {
+      n_tiles = c < n_tiles ? c : n_tiles;
+    }
+  }
   // All 512 columns: the allocation then necessarily starts at column 0 (one CTA per SM), so
   // every TMEM address below is a compile-time constant per slot.
   constexpr uint32_t kTmemCols = 512;
@@ -289,7 +300,7 @@ sinkhorn_tc_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSink
     for (int64_t tk2 = 0; tk2 < my_tiles; ++tk2) {
       const int64_t tk = s + NS * tk2;
       const int64_t tr = blockIdx.x + tk * (int64_t)gridDim.x;  // tile index within the range
-      const int64_t t = tile_begin + tr;
+      const int64_t t = units != nullptr ? (int64_t)units[tr] : tile_begin + tr;
       // ---- tile init: marginal rows -> SMEM, V^T = 1 -> R0 (phase 0's A operand)
       named_bar_sync(1 + s, kWG);  // previous tile's readers are done with mrows / red
       int ii = 0, jj = 0;
@@ -470,7 +481,8 @@ template <int KP>
 static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, const PairSink& out,
                              const float* H, int K, const uint32_t* g_img, const uint32_t* gc_img,
                              int iters, cudaStream_t s, const int32_t* pi = nullptr,
-                             const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr) {
+                             const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr,
+                             const int32_t* units = nullptr, const int64_t* n_dev = nullptr) {
   const size_t smem = Smem<KP>::kBytes;
 #ifdef ASOT_DEBUG_KERNELS   // diagnostic variants (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
@@ -491,7 +503,8 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
   kern<<<(unsigned)grid, Slots<KP>::kAllThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
-                                                               g_img, gc_img, iters, pi, pj, n_pairs, Hp);
+                                                               g_img, gc_img, iters, pi, pj, n_pairs, Hp,
+                                                               units, n_dev);
   return cudaGetLastError();
 }
 
@@ -516,14 +529,19 @@ bool sinkhorn_tc_supported(int K) { return K >= 1 && K <= 128; }
 
 cudaError_t launch_sinkhorn_tc(int64_t tile_begin, int64_t tile_end, int64_t n_dist,
                                const PairSink& out, const float* H, int K, const uint32_t* g_img,
-                               const uint32_t* gc_img, int iters, cudaStream_t s) {
+                               const uint32_t* gc_img, int iters, cudaStream_t s, const int32_t* units,
+                               const int64_t* n_dev) {
   const int64_t n_tiles = tile_end - tile_begin;
   if (n_tiles <= 0) return cudaSuccess;
   switch (kpad32(K)) {
-    case 32: return tc::launch_kp<32>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
-    case 64: return tc::launch_kp<64>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
-    case 96: return tc::launch_kp<96>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
-    case 128: return tc::launch_kp<128>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s);
+#define ASOT_TC_CASE(KP)                                                                               \
+    case KP: return tc::launch_kp<KP>(tile_begin, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, \
+                                      nullptr, nullptr, 0, nullptr, units, n_dev);
+    ASOT_TC_CASE(32)
+    ASOT_TC_CASE(64)
+    ASOT_TC_CASE(96)
+    ASOT_TC_CASE(128)
+#undef ASOT_TC_CASE
     default: return cudaErrorNotSupported;
   }
 }
@@ -534,7 +552,8 @@ size_t sinkhorn_tc_pairs_scratch_bytes(int64_t n_dist, int K) {
 
 cudaError_t launch_sinkhorn_tc_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
                                      const PairSink& out, const float* H, int K, const uint32_t* g_img,
-                                     const uint32_t* gc_img, float* Hp, int iters, cudaStream_t s) {
+                                     const uint32_t* gc_img, float* Hp, int iters, cudaStream_t s,
+                                     const int64_t* n_dev) {
   if (n_pairs <= 0) return cudaSuccess;
   const int kp = kpad32(K);
   tc::pad_marginals_tc_kernel<<<512, 256, 0, s>>>(H, n_dist, K, kp, Hp);
@@ -542,10 +561,14 @@ cudaError_t launch_sinkhorn_tc_pairs(const int32_t* pi, const int32_t* pj, int64
   if (e != cudaSuccess) return e;
   const int64_t n_tiles = (n_pairs + kTileSlots - 1) / kTileSlots;
   switch (kp) {
-    case 32: return tc::launch_kp<32>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
-    case 64: return tc::launch_kp<64>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
-    case 96: return tc::launch_kp<96>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
-    case 128: return tc::launch_kp<128>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, n_pairs, Hp);
+#define ASOT_TC_CASE(KP)                                                                                \
+    case KP: return tc::launch_kp<KP>(0, n_tiles, n_dist, out, H, K, g_img, gc_img, iters, s, pi, pj, \
+                                      n_pairs, Hp, nullptr, n_dev);
+    ASOT_TC_CASE(32)
+    ASOT_TC_CASE(64)
+    ASOT_TC_CASE(96)
+    ASOT_TC_CASE(128)
+#undef ASOT_TC_CASE
     default: return cudaErrorNotSupported;
   }
 }

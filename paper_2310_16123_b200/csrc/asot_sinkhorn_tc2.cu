@@ -74,7 +74,8 @@ template <int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAllThreads, 1)
 sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
                     const float* __restrict__ H, int K, const uint8_t* __restrict__ g_img,
-                    const uint8_t* __restrict__ gc_img, int iters) {
+                    const uint8_t* __restrict__ gc_img, int iters, const int32_t* __restrict__ units,
+                    const int64_t* __restrict__ n_dev) {
   using S = Smem;
   constexpr uint32_t kIdescPart = make_idesc_tf32(256, kChunk);   // Sinkhorn parts: N = 64
   constexpr uint32_t kIdescCost = make_idesc_tf32(256, 128);      // cost sub-parts: N = 128
@@ -159,9 +160,13 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   };
 
   bool clamped = false;   // a denominator left [FLT_MIN, 2^126] on an anchor with mass
-  for (int64_t b = (tile_begin >> 1) + (blockIdx.x >> 1); b < ((tile_end + 1) >> 1); b += gridDim.x >> 1) {
+  // block pairs kb = 0, 1, ... of the range, or (bucketed pair lists) of the unit list
+  int64_t n_kb = ((tile_end + 1) >> 1) - (tile_begin >> 1);
+  if (units != nullptr && *n_dev < n_kb) n_kb = *n_dev;
+  for (int64_t kb = blockIdx.x >> 1; kb < n_kb; kb += gridDim.x >> 1) {
+    const int64_t b = units != nullptr ? (int64_t)units[kb] : (tile_begin >> 1) + kb;
     const int64_t t = 2 * b + rank;          // this CTA's tile
-    const bool t_in = t >= tile_begin && t < tile_end;
+    const bool t_in = units != nullptr || (t >= tile_begin && t < tile_end);
     // ---- tile init
     int64_t bi, bj;
     block_pair_decode(b, num_blocks(n_dist), bi, bj);
@@ -224,7 +229,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
         for (int c = 0; c < NCH; ++c) {
           mbar_wait(bar_mma0 + 8 * c, mma_par);
           tc_fence_after();
-          if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && threadIdx.x == 0 && f < 64)
+          if (DBG >= 3 && blockIdx.x == 0 && kb == 0 && threadIdx.x == 0 && f < 64)
             g_tc2_trace[0][f * 4 + c] = clock64();
           if (DBG != 1 && DBG != 4) {
             uint32_t d[16];
@@ -248,7 +253,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
             if (c + 1 < NCH) load_m(f, c + 1);
             else if (!last) load_m(f + 1, 0);
           }
-          if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && threadIdx.x == 0 && f < 64)
+          if (DBG >= 3 && blockIdx.x == 0 && kb == 0 && threadIdx.x == 0 && f < 64)
             g_tc2_trace[1][f * 4 + c] = clock64();
           if (!last) chunk_done(c);
         }
@@ -271,7 +276,7 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       auto gate = [&](int f, int kc) {
         mbar_wait(bar_epi0 + 8 * kc, epi_par);
         tc_fence_after();
-        if (DBG >= 3 && blockIdx.x == 0 && b == (tile_begin >> 1) && lane == 0 && f < 64)
+        if (DBG >= 3 && blockIdx.x == 0 && kb == 0 && lane == 0 && f < 64)
           g_tc2_trace[2][f * 4 + kc] = clock64();
       };
       for (int f = 0; f < 2 * iters; ++f) {
@@ -355,13 +360,13 @@ sinkhorn_tc2_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       tc_fence_after();
     }
     if (DBG >= 3 && blockIdx.x == 0 && threadIdx.x == 0) {
-      const int64_t k = (b - (tile_begin >> 1)) / (gridDim.x >> 1);
+      const int64_t k = kb / (gridDim.x >> 1);
       if (k < 64) g_tc2_trace[3][k] = clock64() - t_cost0;
     }
     if (epi_warp) red[cq * 128 + p] = acc;
     __syncthreads();
     if (warp < 4 && t_in)
-      write_result(out, (t - tile_begin) * kTileSlots + ps, valid, ii, jj,
+      write_result(out, (units != nullptr ? 2 * kb + rank : t - tile_begin) * kTileSlots + ps, valid, ii, jj,
                    red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
   }
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
@@ -401,7 +406,7 @@ cudaError_t launch_gibbs_prep_tc2(const float* cost, int K, float eps, uint8_t* 
 
 cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
-                                cudaStream_t s) {
+                                cudaStream_t s, const int32_t* units, const int64_t* n_dev) {
   if (tile_end <= tile_begin) return cudaSuccess;
 #ifdef ASOT_DEBUG_KERNELS   // diagnostic variants (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
@@ -421,7 +426,7 @@ cudaError_t launch_sinkhorn_tc2(int64_t tile_begin, int64_t tile_end, int64_t n_
   int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
   if (clusters < 1) clusters = 1;
   kern<<<(unsigned)(2 * clusters), tc2::kAllThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, H, K, g_img,
-                                                             gc_img, iters);
+                                                             gc_img, iters, units, n_dev);
   return cudaGetLastError();
 }
 

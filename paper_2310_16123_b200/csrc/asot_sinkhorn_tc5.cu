@@ -132,6 +132,11 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   // per-CTA X images: [side 2][hi, lo]
   uint8_t* xb = xbuf + (size_t)blockIdx.x * (4 * (size_t)C::kXBytes);
   auto ximg = [&](int side, int lo) { return xb + (size_t)(2 * side + lo) * C::kXBytes; };
+  if (EXPLICIT && ps.n_dev != nullptr) {   // bucketed pair lists: the list length on the device
+    if (*ps.n_dev < ps.n_slots) ps.n_slots = *ps.n_dev;
+    const int64_t te = (ps.n_slots + kTileSlots - 1) / kTileSlots;
+    if (te < tile_end) tile_end = te;
+  }
   const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int phases = 2 * iters + 1;
