@@ -130,12 +130,13 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
  * and raise ASOT_FLAG_BAD_INDEX.  n_pairs = 0 returns ASOT_OK at once (pair_i, pair_j and
  * dist_out may then be NULL).  Workspace: asot_pairwise_workspace_bytes(n_dist, n_anchors, prec)
  * runs the list as it is; the larger asot_pairwise_list_workspace_bytes(n_dist, n_anchors, prec,
- * n_pairs) lets TF32 requests with 32 <= K <= 256 (n_pairs >= 1024, n_dist <= ~2.9e4) serve every
+ * n_pairs) lets requests with 32 <= K <= 256 (n_pairs >= 1024, n_dist <= ~2.9e4) serve every
  * tile of the upper triangle whose 8 x 16 block of i < j pairs the list covers COMPLETELY through
  * the tile kernels (marginal rows staged in SMEM once per tile; asot_pairs_bucket.cu), the other
  * entries (i >= j, repeats, partly covered tiles, invalid indices) through the pair-list mode --
  * stream-ordered, no host synchronisation; the values are those of the tile path (K <= 128:
- * bitwise the pair-list mode's; 128 < K <= 256: within the TF32 tolerance of either).
+ * bitwise the pair-list mode's; 128 < K <= 256: another kernel -- TF32: the CTA-pair kernel,
+ * FP32: the BF16x3 one -- within the precision's tolerance, like the pair-list mode's).
  * (ASOT_PAIR_BUCKET=0 disables it.)  Status: the call's flags are OR-ed into ONE word for the whole list (DESIGN R#33:
  * no per-pair flag array; a flagged run is re-run on a sub-list to locate pairs).  Arguments:
  *   hist     [n_dist, n_anchors] f32 device (rows are a' / b')

@@ -109,16 +109,19 @@ int pair_kind(int32_t K, asot_precision prec) {
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
 // Bucketed pair lists (asot_pairs_bucket.cu): the tile kernel that serves the fully covered tiles
 // of a list of pair_kind `lk` (TF32: 7 -> the 1-SM kernel's tile mode, 6 -> the CTA-pair kernel
-// when K <= 256), its unit (1: tiles, 2: block pairs); 0 = the list runs as it is.
+// when K <= 256; fp32: 8 -> the 1-SM 3xTF32 kernel, 5 -> the BF16x3 CTA-pair kernel when
+// K <= 256), its unit (1: tiles, 2: block pairs); 0 = the list runs as it is.
 int bucket_tile_kind(int32_t K, asot_precision prec) {
   static const bool off = getenv("ASOT_PAIR_BUCKET") && std::string(getenv("ASOT_PAIR_BUCKET")) == "0";
   if (off) return 0;
   const int lk = pair_kind(K, prec);
   if (lk == 7) return 1;
+  if (lk == 8) return 3;
   if (lk == 6 && asot::sinkhorn_tc2_supported(K)) return 2;
+  if (lk == 5 && asot::sinkhorn_tc6_supported(K)) return 10;
   return 0;
 }
-int bucket_upt(int tk) { return tk == 2 ? 2 : 1; }
+int bucket_upt(int tk) { return tk == 2 || tk == 10 ? 2 : 1; }
 constexpr int64_t kMinBucketPairs = 1024;
 
 int device_sms() {
@@ -259,7 +262,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                                           ps.units, ps.n_dev));
   } else if (kind == 10) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc6(tile_begin, tile_end, ps.n_dist, sink, H, K,
-                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s));
+                                          (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s,
+                                          ps.units, ps.n_dev));
   } else if (kind == 1) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
                                          gb.gc_img, iters, s, ps.units, ps.n_dev));
@@ -268,10 +272,10 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
                                                gb.gc_img, (float*)gb.scratch, iters, s, ps.n_dev));
   } else if (kind == 3) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
-                                          gb.gc_img, gb.GC, iters, s));
+                                          gb.gc_img, gb.GC, iters, s, ps.units, ps.n_dev));
   } else if (kind == 8) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc3_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
-                                                gb.gc_img, gb.GC, (float*)gb.scratch, iters, s));
+                                                gb.gc_img, gb.GC, (float*)gb.scratch, iters, s, ps.n_dev));
   } else if (kind == 9) {
     ASOT_LAUNCH(asot::launch_sinkhorn_warp(ps, sink, H, K, gb.G, gb.GC, iters, s));
   } else {
@@ -288,9 +292,9 @@ struct BucketLayout {
 };
 BucketLayout carve_bucketed(Carver& cv, const GibbsBufs& gbl, int32_t K, int tk, int64_t n_dist, int64_t n_pairs) {
   BucketLayout L;
-  if (tk == 1) {
+  if (tk == 1 || tk == 3) {   // the pair-list kinds 7 / 8 carve the same images (+ padded H)
     L.gbt = gbl;
-    L.gbt.kind = 1;
+    L.gbt.kind = tk;
   } else {
     L.gbt = carve_gibbs(cv, K, tk, n_dist);
   }

@@ -356,10 +356,12 @@ cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t*
 size_t sinkhorn_tc3_pairs_scratch_bytes(int64_t n_dist, int K);
 cudaError_t launch_sinkhorn_tc3_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
                                       const PairSink& out, const float* H, int K, const uint32_t* ghi,
-                                      const uint32_t* glo, const float* gc, float* Hp, int iters, cudaStream_t s);
+                                      const uint32_t* glo, const float* gc, float* Hp, int iters, cudaStream_t s,
+                                      const int64_t* n_dev = nullptr);
 cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
-                                const float* gc, int iters, cudaStream_t s);
+                                const float* gc, int iters, cudaStream_t s, const int32_t* units = nullptr,
+                                const int64_t* n_dev = nullptr);
 size_t eot_slot_floats(int64_t max_n);
 int eot_grid(int64_t n_pairs, int sms);
 bool eot_supported(int64_t max_n);
@@ -412,7 +414,7 @@ cudaError_t launch_gibbs_prep_tc6(const float* cost, int K, float eps, uint8_t* 
                                   cudaStream_t s);
 cudaError_t launch_sinkhorn_tc6(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
-                                cudaStream_t s);
+                                cudaStream_t s, const int32_t* units = nullptr, const int64_t* n_dev = nullptr);
 cudaError_t read_kernel_clock_tc6(long long* host4);
 cudaError_t read_kernel_clock_tc3(long long* host4);
 cudaError_t read_kernel_clock_tc4(long long* host4);

@@ -112,8 +112,19 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
                     const float* __restrict__ H, int K, const uint32_t* __restrict__ ghi_img,
                     const uint32_t* __restrict__ glo_img, const float* __restrict__ gc_plain, int iters,
                     const int32_t* __restrict__ pair_i, const int32_t* __restrict__ pair_j, int64_t n_pairs,
-                    const float* __restrict__ Hp) {
+                    const float* __restrict__ Hp, const int32_t* __restrict__ units,
+                    const int64_t* __restrict__ n_dev) {
   using S = Smem<KP>;
+  // device-side counts (bucketed pair lists, asot_pairs_bucket.cu): the host passed upper bounds
+  if (n_dev != nullptr) {
+    const int64_t c = *n_dev;
+    if constexpr (EX) {
+      n_pairs = c < n_pairs ? c : n_pairs;
+      n_tiles = (n_pairs + kTileSlots - 1) / kTileSlots;
+    } else {
+      n_tiles = c < n_tiles ? c : n_tiles;
+    }
+  }
   constexpr int NS = Slots<KP>::NS, NCG = Slots<KP>::NCG;
   constexpr int kWPS = Slots<KP>::kWarpsPerSlot, kWG = kWPS * 32;
   constexpr int NH = KP / 2;          // columns per N-half
@@ -243,7 +254,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
     const int64_t my_tiles = slot_tiles(s);
     for (int64_t k2 = 0; k2 < my_tiles; ++k2) {
       const int64_t tr = blockIdx.x + (s + NS * k2) * (int64_t)gridDim.x;
-      const int64_t t = tile_begin + tr;
+      const int64_t t = units != nullptr ? (int64_t)units[tr] : tile_begin + tr;
       named_bar_sync(1 + s, kWG);  // previous tile's cost readers are done (marg, red, R0)
       int ii = 0, jj = 0;
       bool valid;
@@ -443,7 +454,8 @@ template <int KP>
 static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, const PairSink& out,
                              const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
                              const float* gc, int iters, cudaStream_t s, const int32_t* pi = nullptr,
-                             const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr) {
+                             const int32_t* pj = nullptr, int64_t n_pairs = 0, const float* Hp = nullptr,
+                             const int32_t* units = nullptr, const int64_t* n_dev = nullptr) {
   const size_t smem = Smem<KP>::kBytes;
 #ifdef ASOT_DEBUG_KERNELS   // diagnostic variant (tools/): only in debug builds
   static const int dbg = getenv("ASOT_TC_DEBUG_MODE") ? atoi(getenv("ASOT_TC_DEBUG_MODE")) : 0;
@@ -462,7 +474,8 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t n_tiles, int64_t n_dist
   if (grid > sms) grid = sms;
   if (grid < 1) return cudaSuccess;
   kern<<<(unsigned)grid, Slots<KP>::kThreads, smem, s>>>(tile_begin, n_tiles, n_dist, out, H, K,
-                                                                 ghi, glo, gc, iters, pi, pj, n_pairs, Hp);
+                                                                 ghi, glo, gc, iters, pi, pj, n_pairs, Hp,
+                                                                 units, n_dev);
   return cudaGetLastError();
 }
 
@@ -499,14 +512,19 @@ cudaError_t launch_gibbs_prep_tc3(const float* cost, int K, float eps, uint32_t*
 
 cudaError_t launch_sinkhorn_tc3(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint32_t* ghi, const uint32_t* glo,
-                                const float* gc, int iters, cudaStream_t s) {
+                                const float* gc, int iters, cudaStream_t s, const int32_t* units,
+                                const int64_t* n_dev) {
   const int64_t n_tiles = tile_end - tile_begin;
   if (n_tiles <= 0) return cudaSuccess;
   switch (kpad32(K)) {
-    case 32: return tc3::launch_kp<32>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
-    case 64: return tc3::launch_kp<64>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
-    case 96: return tc3::launch_kp<96>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
-    case 128: return tc3::launch_kp<128>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s);
+#define ASOT_TC3_CASE(KP)                                                                              \
+    case KP: return tc3::launch_kp<KP>(tile_begin, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, \
+                                       nullptr, nullptr, 0, nullptr, units, n_dev);
+    ASOT_TC3_CASE(32)
+    ASOT_TC3_CASE(64)
+    ASOT_TC3_CASE(96)
+    ASOT_TC3_CASE(128)
+#undef ASOT_TC3_CASE
     default: return cudaErrorNotSupported;
   }
 }
@@ -518,7 +536,8 @@ size_t sinkhorn_tc3_pairs_scratch_bytes(int64_t n_dist, int K) { return (size_t)
 
 cudaError_t launch_sinkhorn_tc3_pairs(const int32_t* pi, const int32_t* pj, int64_t n_pairs, int64_t n_dist,
                                       const PairSink& out, const float* H, int K, const uint32_t* ghi,
-                                      const uint32_t* glo, const float* gc, float* Hp, int iters, cudaStream_t s) {
+                                      const uint32_t* glo, const float* gc, float* Hp, int iters, cudaStream_t s,
+                                      const int64_t* n_dev) {
   if (n_pairs <= 0) return cudaSuccess;
   const int kp = kpad32(K);
   tc3::pad_marginals_tc3_kernel<<<512, 256, 0, s>>>(H, n_dist, K, kp, Hp);
@@ -526,10 +545,14 @@ cudaError_t launch_sinkhorn_tc3_pairs(const int32_t* pi, const int32_t* pj, int6
   if (e != cudaSuccess) return e;
   const int64_t n_tiles = (n_pairs + kTileSlots - 1) / kTileSlots;
   switch (kp) {
-    case 32: return tc3::launch_kp<32>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
-    case 64: return tc3::launch_kp<64>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
-    case 96: return tc3::launch_kp<96>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
-    case 128: return tc3::launch_kp<128>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, n_pairs, Hp);
+#define ASOT_TC3_CASE(KP)                                                                                \
+    case KP: return tc3::launch_kp<KP>(0, n_tiles, n_dist, out, H, K, ghi, glo, gc, iters, s, pi, pj, \
+                                       n_pairs, Hp, nullptr, n_dev);
+    ASOT_TC3_CASE(32)
+    ASOT_TC3_CASE(64)
+    ASOT_TC3_CASE(96)
+    ASOT_TC3_CASE(128)
+#undef ASOT_TC3_CASE
     default: return cudaErrorNotSupported;
   }
 }

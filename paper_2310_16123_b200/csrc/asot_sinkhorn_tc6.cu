@@ -115,7 +115,8 @@ __device__ long long g_tc6_clock[4];  // clock_probe: (clock64, globaltimer) at 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAllThreads, 1)
 sinkhorn_tc6_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
                     const float* __restrict__ H, int K, const uint8_t* __restrict__ g_img,
-                    const uint8_t* __restrict__ gc_img, int iters) {
+                    const uint8_t* __restrict__ gc_img, int iters, const int32_t* __restrict__ units,
+                    const int64_t* __restrict__ n_dev) {
   using S = Smem;
   constexpr uint32_t kIdescPart = make_idesc_bf16(256, kChunk);   // Sinkhorn parts: N = 64
   constexpr uint32_t kIdescCost = make_idesc_bf16(256, 128);      // cost sub-parts: N = 128
@@ -196,9 +197,13 @@ sinkhorn_tc6_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
   };
 
   bool clamped = false;   // a denominator left [FLT_MIN, 2^126] on an anchor with mass
-  for (int64_t b = (tile_begin >> 1) + (blockIdx.x >> 1); b < ((tile_end + 1) >> 1); b += gridDim.x >> 1) {
+  // block pairs kb = 0, 1, ... of the range, or (bucketed pair lists) of the unit list
+  int64_t n_kb = ((tile_end + 1) >> 1) - (tile_begin >> 1);
+  if (units != nullptr && *n_dev < n_kb) n_kb = *n_dev;
+  for (int64_t kb = blockIdx.x >> 1; kb < n_kb; kb += gridDim.x >> 1) {
+    const int64_t b = units != nullptr ? (int64_t)units[kb] : (tile_begin >> 1) + kb;
     const int64_t t = 2 * b + rank;
-    const bool t_in = t >= tile_begin && t < tile_end;
+    const bool t_in = units != nullptr || (t >= tile_begin && t < tile_end);
     int64_t bi, bj;
     block_pair_decode(b, num_blocks(n_dist), bi, bj);
     const int64_t i0 = bi * kBlockDist + rank * 8, j0 = bj * kBlockDist;
@@ -393,7 +398,7 @@ sinkhorn_tc6_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     if (epi_warp) red[cq * 128 + p] = acc;
     __syncthreads();
     if (warp < 4 && t_in)
-      write_result(out, (t - tile_begin) * kTileSlots + ps, valid, ii, jj,
+      write_result(out, (units != nullptr ? 2 * kb + rank : t - tile_begin) * kTileSlots + ps, valid, ii, jj,
                    red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
   }
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
@@ -444,7 +449,7 @@ cudaError_t launch_gibbs_prep_tc6(const float* cost, int K, float eps, uint8_t* 
 
 cudaError_t launch_sinkhorn_tc6(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, int iters,
-                                cudaStream_t s) {
+                                cudaStream_t s, const int32_t* units, const int64_t* n_dev) {
   if (tile_end <= tile_begin) return cudaSuccess;
   const size_t smem = tc6::Smem::kBytes;
   cudaError_t e = cudaFuncSetAttribute(tc6::sinkhorn_tc6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -456,7 +461,8 @@ cudaError_t launch_sinkhorn_tc6(int64_t tile_begin, int64_t tile_end, int64_t n_
   int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
   if (clusters < 1) clusters = 1;
   tc6::sinkhorn_tc6_kernel<<<(unsigned)(2 * clusters), tc6::kAllThreads, smem, s>>>(tile_begin, tile_end, n_dist, out,
-                                                                                  H, K, g_img, gc_img, iters);
+                                                                                  H, K, g_img, gc_img, iters,
+                                                                                  units, n_dev);
   return cudaGetLastError();
 }
 
