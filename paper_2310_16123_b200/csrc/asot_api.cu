@@ -109,19 +109,20 @@ int pair_kind(int32_t K, asot_precision prec) {
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
 // Bucketed pair lists (asot_pairs_bucket.cu): the tile kernel that serves the fully covered tiles
 // of a list of pair_kind `lk` (TF32: 7 -> the 1-SM kernel's tile mode, 6 -> the CTA-pair kernel
-// when K <= 256; fp32: 8 -> the 1-SM 3xTF32 kernel, 5 -> the BF16x3 CTA-pair kernel when
-// K <= 256), its unit (1: tiles, 2: block pairs); 0 = the list runs as it is.
+// for K <= 256, else the streamed one; fp32: 8 -> the 1-SM 3xTF32 kernel, 5 -> the BF16x3
+// CTA-pair kernel for K <= 256, else the streamed 3xTF32 kernel's tile mode), its unit (1: tiles,
+// 2: block pairs); 0 = the list runs as it is.
 int bucket_tile_kind(int32_t K, asot_precision prec) {
   static const bool off = getenv("ASOT_PAIR_BUCKET") && std::string(getenv("ASOT_PAIR_BUCKET")) == "0";
   if (off) return 0;
   const int lk = pair_kind(K, prec);
   if (lk == 7) return 1;
   if (lk == 8) return 3;
-  if (lk == 6 && asot::sinkhorn_tc2_supported(K)) return 2;
-  if (lk == 5 && asot::sinkhorn_tc6_supported(K)) return 10;
+  if (lk == 6) return asot::sinkhorn_tc2_supported(K) ? 2 : 4;
+  if (lk == 5) return asot::sinkhorn_tc6_supported(K) ? 10 : 5;
   return 0;
 }
-int bucket_upt(int tk) { return tk == 2 || tk == 10 ? 2 : 1; }
+int bucket_upt(int tk) { return tk == 1 || tk == 3 ? 1 : 2; }
 constexpr int64_t kMinBucketPairs = 1024;
 
 int device_sms() {
@@ -255,7 +256,8 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   } else if (kind == 4) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img,
-                                          (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s));
+                                          (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s,
+                                          ps.units, ps.n_dev));
   } else if (kind == 2) {
     ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s,
@@ -292,7 +294,7 @@ struct BucketLayout {
 };
 BucketLayout carve_bucketed(Carver& cv, const GibbsBufs& gbl, int32_t K, int tk, int64_t n_dist, int64_t n_pairs) {
   BucketLayout L;
-  if (tk == 1 || tk == 3) {   // the pair-list kinds 7 / 8 carve the same images (+ padded H)
+  if (tk == 1 || tk == 3 || tk == 5) {   // the pair-list kinds 7 / 8 / 5 carve the same images
     L.gbt = gbl;
     L.gbt.kind = tk;
   } else {

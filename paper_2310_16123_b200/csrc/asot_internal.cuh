@@ -326,7 +326,8 @@ cudaError_t launch_gibbs_prep_tc4(const float* cost, int K, float eps, uint8_t* 
                                   cudaStream_t s);
 cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
-                                int iters, cudaStream_t s);
+                                int iters, cudaStream_t s, const int32_t* units = nullptr,
+                                const int64_t* n_dev = nullptr);
 cudaError_t launch_unpack_tiles(const float* packed, int64_t n_dist, int64_t tile_begin,
                                 int64_t tile_end, float* mat, cudaStream_t s);
 cudaError_t launch_zero_diag(float* mat, int64_t n_dist, cudaStream_t s);

@@ -98,7 +98,8 @@ template <int KP, int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSink out,
                     const float* __restrict__ Hp, int K, const uint8_t* __restrict__ g_img,
-                    const uint8_t* __restrict__ gc_img, uint8_t* __restrict__ xbuf, int iters) {
+                    const uint8_t* __restrict__ gc_img, uint8_t* __restrict__ xbuf, int iters,
+                    const int32_t* __restrict__ units, const int64_t* __restrict__ n_dev) {
   using S = Smem;
   constexpr int NH = Cfg<KP>::NH, kKC = Cfg<KP>::KC;
   constexpr uint32_t kXBytes = Cfg<KP>::kXBytes;
@@ -143,6 +144,9 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
 
   uint8_t* xb = xbuf + (size_t)blockIdx.x * (2 * kXBytes);
   const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
+  // block pairs kb = 0, 1, ... of the range, or (bucketed pair lists, tile mode) of the unit list
+  int64_t n_kb = bp_end - bp_begin;
+  if (units != nullptr && *n_dev < n_kb) n_kb = *n_dev;
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int phases = 2 * iters + 1;
   // Where half h (anchors [512 h, 512 h + 512)) of X_f, the input of phase f, lives.  KP = 512:
@@ -173,7 +177,8 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     if (lane == 0) {
       int64_t it = 0;
       uint32_t xr_par = 0;
-      for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+      for (int64_t kb = cluster_id; kb < n_kb; kb += n_clusters) {
+        const int64_t b = units != nullptr ? (int64_t)units[kb] : bp_begin + kb;
         for (int f = 0; f < phases; ++f) {
 
           const uint8_t* img = (f < phases - 1 ? g_img : gc_img) + rank * kImgRankBytes;
@@ -201,7 +206,8 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     int64_t it = 0;
     uint32_t free_par = 0;
     bool first = true;
-    for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+    for (int64_t kb = cluster_id; kb < n_kb; kb += n_clusters) {
+        const int64_t b = units != nullptr ? (int64_t)units[kb] : bp_begin + kb;
       for (int f = 0; f < phases; ++f) {
         for (int nh = 0; nh < NH; ++nh) {
           if (rank == 0 && !first) {
@@ -250,9 +256,10 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     const uint32_t free_remote = mapa(bar_free, 0);
     uint32_t done_par = 0;
     bool clamped = false;   // a denominator left [FLT_MIN, 2^126] on an anchor with mass
-    for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+    for (int64_t kb = cluster_id; kb < n_kb; kb += n_clusters) {
+        const int64_t b = units != nullptr ? (int64_t)units[kb] : bp_begin + kb;
       const int64_t t = 2 * b + rank;
-      const bool t_in = t >= tile_begin && t < tile_end;
+      const bool t_in = units != nullptr || (t >= tile_begin && t < tile_end);
       int ii, jj;
       const bool valid = tile_slot_pair(t, p, n_dist, ii, jj) && t_in;
       // marginal rows of this tile: u side = distributions i0 + [0, 8), v side = j0 + [0, 16)
@@ -373,7 +380,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       red[g * 128 + p] = acc;
       named_bar_sync(1, kEpiThreads);
       if (g == 0 && t_in)
-        write_result(out, (t - tile_begin) * kTileSlots + p, valid, ii, jj,
+        write_result(out, (units != nullptr ? 2 * kb + rank : t - tile_begin) * kTileSlots + p, valid, ii, jj,
                      red[p] + red[128 + p] + red[256 + p] + red[384 + p]);
       named_bar_sync(1, kEpiThreads);  // red reused by the next tile
     }
@@ -437,7 +444,7 @@ namespace tc4 {
 template <int KP>
 static cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                              const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
-                             int iters, cudaStream_t s) {
+                             int iters, cudaStream_t s, const int32_t* units, const int64_t* n_dev) {
   float* Hp = (float*)scratch;
   uint8_t* xbuf = scratch + (((size_t)(n_dist + 1) * KP * 4 + 1023) & ~(size_t)1023);
   pad_marginals_kernel<KP><<<512, 256, 0, s>>>(H, n_dist, K, Hp);
@@ -460,18 +467,20 @@ static cudaError_t launch_kp(int64_t tile_begin, int64_t tile_end, int64_t n_dis
   int64_t clusters = n_bp < sms / 2 ? n_bp : sms / 2;
   if (clusters < 1) clusters = 1;
   kern<<<(unsigned)(2 * clusters), kThreads, smem, s>>>(tile_begin, tile_end, n_dist, out, Hp, K, g_img, gc_img,
-                                                        xbuf, iters);
+                                                        xbuf, iters, units, n_dev);
   return cudaGetLastError();
 }
 }  // namespace tc4
 
 cudaError_t launch_sinkhorn_tc4(int64_t tile_begin, int64_t tile_end, int64_t n_dist, const PairSink& out,
                                 const float* H, int K, const uint8_t* g_img, const uint8_t* gc_img, uint8_t* scratch,
-                                int iters, cudaStream_t s) {
+                                int iters, cudaStream_t s, const int32_t* units, const int64_t* n_dev) {
   if (tile_end <= tile_begin) return cudaSuccess;
   if (tc4_kpad(K) == 512)
-    return tc4::launch_kp<512>(tile_begin, tile_end, n_dist, out, H, K, g_img, gc_img, scratch, iters, s);
-  return tc4::launch_kp<1024>(tile_begin, tile_end, n_dist, out, H, K, g_img, gc_img, scratch, iters, s);
+    return tc4::launch_kp<512>(tile_begin, tile_end, n_dist, out, H, K, g_img, gc_img, scratch, iters, s, units,
+                               n_dev);
+  return tc4::launch_kp<1024>(tile_begin, tile_end, n_dist, out, H, K, g_img, gc_img, scratch, iters, s, units,
+                              n_dev);
 }
 
 }  // namespace asot

@@ -89,6 +89,8 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                     const uint8_t* __restrict__ g_lo, const uint8_t* __restrict__ gc_hi,
                     const uint8_t* __restrict__ gc_lo, uint8_t* __restrict__ xbuf, int iters) {
   using S = Smem;
+  const int32_t* units = EXPLICIT ? nullptr : ps.units;   // bucketed pair lists (tile mode)
+  const int64_t* n_dev = ps.n_dev;
   using C = Cfg<KP>;
   constexpr int kStages = Pipe<SPLIT>::kStages;
   constexpr uint32_t kStageBytes = Pipe<SPLIT>::kStageBytes;
@@ -138,6 +140,9 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     if (te < tile_end) tile_end = te;
   }
   const int64_t bp_begin = tile_begin >> 1, bp_end = (tile_end + 1) >> 1;
+  // block pairs kb = 0, 1, ... of the range, or (bucketed pair lists, tile mode) of the unit list
+  int64_t n_kb = bp_end - bp_begin;
+  if (units != nullptr && *n_dev < n_kb) n_kb = *n_dev;
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int phases = 2 * iters + 1;
   // 32-anchor input chunks holding real anchors: padded chunks (x = 0 there) are skipped
@@ -148,7 +153,8 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     if (lane == 0) {
       int64_t it = 0;
       uint32_t xr_par = 0;
-      for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+      for (int64_t kb = cluster_id; kb < n_kb; kb += n_clusters) {
+        const int64_t b = units != nullptr ? (int64_t)units[kb] : bp_begin + kb;
         for (int f = 0; f < phases; ++f) {
           const uint8_t* xin_hi = ximg(f & 1, 0);
           const uint8_t* xin_lo = ximg(f & 1, 1);
@@ -184,7 +190,8 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     int64_t it = 0;
     uint32_t free_par = 0;
     bool first = true;
-    for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+    for (int64_t kb = cluster_id; kb < n_kb; kb += n_clusters) {
+        const int64_t b = units != nullptr ? (int64_t)units[kb] : bp_begin + kb;
       for (int f = 0; f < phases; ++f) {
         for (int pass = 0; pass < C::NP; ++pass) {
           if (rank == 0 && !first) {
@@ -233,9 +240,10 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
     uint32_t done_par = 0;
     bool clamped = false;
     float* marg = (float*)(smem + S::kOffMarg);
-    for (int64_t b = bp_begin + cluster_id; b < bp_end; b += n_clusters) {
+    for (int64_t kb = cluster_id; kb < n_kb; kb += n_clusters) {
+        const int64_t b = units != nullptr ? (int64_t)units[kb] : bp_begin + kb;
       const int64_t t = 2 * b + rank;
-      const bool t_in = t >= tile_begin && t < tile_end;
+      const bool t_in = units != nullptr || (t >= tile_begin && t < tile_end);
       int ii = 0, jj = 0;
       bool valid;
       int64_t i0 = 0, j0 = 0;
@@ -352,7 +360,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
       float* red = (float*)(smem + S::kOffRed);
       red[g * 128 + p] = acc;
       named_bar_sync(1, kEpiThreads);
-      const int64_t slot = (t - tile_begin) * kTileSlots + p;
+      const int64_t slot = (units != nullptr ? 2 * kb + rank : t - tile_begin) * kTileSlots + p;
       if (g == 0 && t_in && (!EXPLICIT || slot < ps.n_slots))
         write_result(out, slot, valid, ii, jj,
                      (red[p] + red[128 + p]) + (red[256 + p] + red[384 + p]));

@@ -89,7 +89,7 @@ def valid_mask(pi, pj, n):
 
 
 @pytest.mark.parametrize("prec", [TF32, FP32])
-@pytest.mark.parametrize("cfg,n", [("c2", 150), ("c3", 90)])
+@pytest.mark.parametrize("cfg,n", [("c2", 150), ("c3", 90), ("c5", 40)])
 def test_complete_triangle_plus_extras(asot, cfg, n, prec):
     inp, H = setup(asot, cfg, n)
     pi, pj = mixed_list(n, seed=7)
@@ -101,8 +101,9 @@ def test_complete_triangle_plus_extras(asot, cfg, n, prec):
     D = tile_matrix(asot, inp, H, prec)
     up = ok & (pi < pj)
     tile_val = np.where(up, D[np.where(ok, pi, 0), np.where(ok, pj, 0)], np.nan)
-    if inp.n_anchors <= 128:
-        # the 1-SM kernel serves both paths: every entry bitwise the plain path's value
+    if inp.n_anchors <= 128 or (inp.n_anchors > 256 and prec == FP32):
+        # one kernel serves both paths (the 1-SM kernels; the streamed 3xTF32 kernel's tile and
+        # pair-list modes): every entry bitwise the plain path's value
         np.testing.assert_array_equal(b[ok], p[ok])
     # first occurrences of i < j are tile-served, every other entry stays on the list path;
     # which of two repeated entries the tile serves is unspecified: each is one of the two
@@ -110,7 +111,7 @@ def test_complete_triangle_plus_extras(asot, cfg, n, prec):
     assert np.all(either[ok]), f"{(~either[ok]).sum()} entries match neither path"
     uniq = np.unique(np.stack([pi[up], pj[up]]), axis=1)
     assert uniq.shape[1] == n * (n - 1) // 2
-    assert np.all(b[up] == tile_val[up]) or inp.n_anchors > 128
+    assert np.all(b[up] == tile_val[up]) or 128 < inp.n_anchors
     # the fp64 oracle on a sample of both kinds of entries
     Hd = H.cpu().numpy().astype(np.float64)
     idx = np.random.default_rng(3).choice(np.flatnonzero(ok), 60, replace=False)
@@ -130,7 +131,7 @@ def test_no_tile_covered(asot):
 
 
 @pytest.mark.parametrize("prec", [TF32, FP32])
-@pytest.mark.parametrize("cfg,n", [("c2", 70), ("c3", 70)])
+@pytest.mark.parametrize("cfg,n", [("c2", 70), ("c3", 70), ("c5", 70)])
 def test_partly_covered_tiles(asot, cfg, n, prec):
     """One block pair covered completely, a second one missing a single pair, plus the first
     16 distributions' pairs in both orientations: tile-served entries equal the tile path, the
