@@ -157,3 +157,25 @@ def test_partly_covered_tiles(asot, cfg, n, prec):
     else:
         tile_val = np.where(pi < pj, D[pi, pj], np.nan)
         assert np.all((b[rest] == p[rest]) | (b[rest] == tile_val[rest]))
+
+
+@pytest.mark.parametrize("prec", [TF32, FP32])
+@pytest.mark.parametrize("cfg,n", [("c2", 20), ("c3", 23)])
+def test_small_n_repeated_triangle(asot, cfg, n, prec):
+    """A small, ragged N whose whole triangle appears six times (shuffled): every tile covered,
+    five of six copies of each pair repeats on the list path; all copies of a pair agree with
+    the tile path or the list path and, within the precision, with each other."""
+    inp, H = setup(asot, cfg, n)
+    iu, ju = np.triu_indices(n, k=1)
+    perm = np.random.default_rng(17).permutation(6 * iu.size)
+    pi, pj = np.tile(iu, 6)[perm], np.tile(ju, 6)[perm]
+    assert pi.size >= 1024
+    b, _ = run_list(asot, inp, H, pi, pj, bucket=True, guard=128, prec=prec)
+    p, _ = run_list(asot, inp, H, pi, pj, bucket=False, prec=prec)
+    D = tile_matrix(asot, inp, H, prec)
+    tv = D[pi, pj]
+    assert np.all((b == tv) | (b == p))
+    rel = np.abs(b - tv) / np.maximum(tv, 1e-3 * float(inp.cost.max()))
+    assert rel.max() <= TOL[prec]
+    if inp.n_anchors <= 128:
+        np.testing.assert_array_equal(b, p)
