@@ -135,14 +135,15 @@ __device__ __forceinline__ float rcp_ftz(float x) {
   return y;
 }
 __device__ __forceinline__ float div_clamped(float m, float den, bool& clamped) {
-  if (!(den >= FLT_MIN) && den == den) {
-    clamped |= m > 0.0f;
-    den = FLT_MIN;
-  } else if (den > 0x1p126f) {
-    clamped |= m > 0.0f;
-    den = 0x1p126f;
-  }
-  return m * rcp_ftz(den);   // m = 0 -> exactly 0 (R#11)
+  // = m * rcp(clamp(den)) bitwise: the reciprocals of the two clamp values are exact powers of
+  // two (rcp(FLT_MIN) = 2^126, rcp(2^126) = 2^-126), so the reciprocal is taken of den itself and
+  // replaced by a select -- the range test runs beside the MUFU instead of in front of it
+  const bool lo = !(den >= FLT_MIN) && den == den;   // 0, subnormal or negative (not NaN)
+  const bool hi = den > 0x1p126f;
+  float r = rcp_ftz(den);
+  r = (lo || hi) ? (lo ? 0x1p126f : 0x1p-126f) : r;
+  clamped |= (lo || hi) && m > 0.0f;
+  return m * r;   // m = 0 -> exactly 0 (R#11)
 }
 // The TF32 epilogues' divide over a thread's N (multiple of 4) anchors of one chunk: o = the
 // RNA-pre-rounded TF32 bits of m / D, m = 0 -> exactly 0 (R#11), one MUFU per two anchors.

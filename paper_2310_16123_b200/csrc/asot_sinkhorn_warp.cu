@@ -27,8 +27,10 @@ namespace warp {
 
 constexpr int kThreads = 256;
 
+// (min 1 block per SM: c1's 2,016 pairs x 16 lanes fill fewer than 148 blocks anyway, and the
+// default register heuristic spilled the LP = 16 instance at 64 registers)
 template <int LP>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, int K,
                      const float* __restrict__ Gp, const float* __restrict__ GCp, int kp, int iters) {
   __shared__ __align__(16) float xs[2][kThreads];   // double-buffered: one __syncwarp per step
@@ -52,9 +54,11 @@ sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
   const float b = (valid && in) ? __ldg(H + (int64_t)j * K + r) : 0.0f;
 
   bool clamped = false;
-  auto divide = [&](float m, float den) {   // 0/x = 0 (R#11); clamp + flag (R#12)
+  const bool apos = a > 0.0f, bpos = b > 0.0f;   // loop-invariant: 0/x = 0 (R#11)
+  auto divide = [&](float m, bool mpos, float den) {   // clamp + flag (R#12)
     // den clamped into [FLT_MIN, 2^126]: rcp.approx.ftz then never overflows or flushes
-    return m > 0.0f ? div_clamped(m, den, clamped) : 0.0f;
+    const float q = div_clamped(m, den, clamped);
+    return mpos ? q : 0.0f;
   };
   // y = sum_c col[c] * x_c over the group's shared vector, c = 0 .. LP-1 in order
   auto dot = [&](const float* xg, const float (&col)[LP]) {
@@ -77,16 +81,16 @@ sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, i
   for (int it = 0; it < iters; ++it) {
     xg0[r] = v;
     __syncwarp();
-    u = divide(a, dot(xg0, g));
+    u = divide(a, apos, dot(xg0, g));
     if (it + 1 == iters) break;
     xg1[r] = u;
     __syncwarp();
-    v = divide(b, dot(xg1, g));
+    v = divide(b, bpos, dot(xg1, g));
   }
   // last v-update fused with the cost: part_r = v_r ((K (.) C_s) u)_r
   xg1[r] = u;
   __syncwarp();
-  float part = divide(b, dot(xg1, g)) * dot(xg1, gc);
+  float part = divide(b, bpos, dot(xg1, g)) * dot(xg1, gc);
 #pragma unroll
   for (int o = LP / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
