@@ -170,6 +170,33 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
+// NaN-propagating 3-input min / max (a NaN operand gives NaN: range checks then fail on NaN)
+__device__ __forceinline__ float fmin3n(float a, float b, float c) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3n(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// Four divides m / den as div_clamped, with the range test taken once for the four (and the warp):
+// when every den of the warp's lanes lies in [FLT_MIN, 2^126] (the rule) x = m * rcp(den), else
+// the clamped per-element form -- bitwise div_clamped either way.
+__device__ __forceinline__ void div4_clamped(const float (&m)[4], const float (&d)[4], float (&x)[4],
+                                             bool& clamped) {
+  const float mn = fmin3n(fmin3n(d[0], d[1], d[2]), d[3], d[3]);
+  const float mx = fmax3n(fmax3n(d[0], d[1], d[2]), d[3], d[3]);
+  const bool bad = !(mn >= FLT_MIN && mx <= 0x1p126f);
+  if (__builtin_expect(__any_sync(0xffffffffu, bad), 0)) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = div_clamped(m[e], d[e], clamped);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = m[e] * rcp_ftz(d[e]);
+  }
+}
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c);
 // x[e .. e+4) = m / D for one group of four anchors; t += (pa ra, pb rb)
 __device__ __forceinline__ void epi_div4(const float* m, float d0, float d1, float d2, float d3, float* x, float2& t) {

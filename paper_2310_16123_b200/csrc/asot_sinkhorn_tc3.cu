@@ -341,13 +341,17 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
               const float4 m4 = *reinterpret_cast<const float4*>(mrow + c);
               mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
             }
+            // S:62 clamp into [FLT_MIN, 2^126] + flag; m = 0 -> exactly 0 (R#11); one range
+            // test per four anchors (div4_clamped)
+            float xq[4];
+            const float dq[4] = {__uint_as_float(dv[0]), __uint_as_float(dv[1]), __uint_as_float(dv[2]),
+                                 __uint_as_float(dv[3])};
+            div4_clamped(mm, dq, xq, clamped);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              // S:62 clamp into [FLT_MIN, 2^126] + flag; m = 0 -> exactly 0 (R#11)
-              const float x = div_clamped(mm[e], __uint_as_float(dv[e]), clamped);
-              const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;  // RNA to TF32
+              const uint32_t xh = (__float_as_uint(xq[e]) + 0x1000u) & 0xFFFFE000u;  // RNA to TF32
               hi[e] = xh;
-              lo[e] = __float_as_uint(x - __uint_as_float(xh));
+              lo[e] = __float_as_uint(xq[e] - __uint_as_float(xh));
             }
             tmem_st4(lane_off + d_reg + (uint32_t)c, hi);
             tmem_st4(lane_off + d_reg + (uint32_t)(KP + c), lo);

@@ -311,10 +311,15 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                 const float4 mq = EXPLICIT ? __ldg(reinterpret_cast<const float4*>(hrow + k0 + e))
                                            : *reinterpret_cast<const float4*>(mrow + g * 64 + c * 16 + e);
                 const float mm[4] = {mq.x, mq.y, mq.z, mq.w};
+                // S:62 clamp into [FLT_MIN, 2^126] + flag; m = 0 -> exactly 0 (R#11); one range
+                // test per four anchors (div4_clamped)
+                const float dq[4] = {__uint_as_float(d[e]), __uint_as_float(d[e + 1]), __uint_as_float(d[e + 2]),
+                                     __uint_as_float(d[e + 3])};
+                float xq[4];
+                div4_clamped(mm, dq, xq, clamped);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                  // S:62 clamp into [FLT_MIN, 2^126] + flag; m = 0 -> exactly 0 (R#11)
-                  const float x = div_clamped(mm[u], __uint_as_float(d[e + u]), clamped);
+                  const float x = xq[u];
                   if (SPLIT == 3) {
                     const uint32_t xh = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;   // RNA to TF32
                     hi[e + u] = xh;
