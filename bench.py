@@ -920,6 +920,25 @@ def main():
         v, sample = oracle_sample_rate(inp, args.cpu_budget, mapping=args.mapping, model=soft_model)
         cpu = {"value": v, "unit": "pairs/s", "cores": len(os.sched_getaffinity(0)),
                "kind": "oracle", "sample": sample}
+        if eot_base is not None:
+            # the paper's CPU comparison system, one pair at a time (Table 2 "eOT (CPU)"):
+            # the fp64 eOT oracle on the GPU leg's seeded pairs until the budget, extrapolated
+            from oracle import eot_oracle as EO
+            done, t_eot = 0, 0.0
+            while t_eot < args.cpu_budget / 2 and done < len(ei):
+                s0 = time.perf_counter()
+                EO.eot_pair_costs(inp.points, inp.offsets, inp.weights, float(inp.eps), inp.iters,
+                                  ei[done:done + 16], ej[done:done + 16], scale)
+                t_eot += time.perf_counter() - s0
+                done += len(ei[done:done + 16])
+            r_cpu = done / t_eot
+            cpu["eot_one_by_one"] = {
+                "pairs_per_s": r_cpu, "sample_pairs": done, "seconds": t_eot,
+                "whole_job_s_extrapolated": inp.n_pairs / r_cpu,
+                "gpu_eot_speedup": eot_base["pairs_per_s"] / r_cpu,
+                "asot_speedup": value / r_cpu,
+                "note": "fp64 eOT oracle (per-pair n_i x n_j cost + Sinkhorn, L iterations) on the "
+                        "first pairs of the eOT leg's seeded sample"}
 
     if rank == 0:
         line = {

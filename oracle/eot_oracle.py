@@ -33,3 +33,43 @@ def eot_pair_costs(points, offsets, weights, eps, iters, pi, pj, scale) -> np.nd
         C = sqeuclid_point_cost(points[si:ei], points[sj:ej], scale)
         out[q], _ = sinkhorn(weights[si:ei], weights[sj:ej], C, eps, iters)
     return out
+
+
+# ------------------------------------------------------------------------------------------
+# The block-diagonal stacking strategy (BDS, Sec. 2.4; S:123-131 bds_sinkhorn): the
+# pairs' Gibbs kernels K_q = exp(-C_q / eps) placed along the diagonal of ONE sparse matrix
+# K_bd, the marginals and scalings stacked vertically, and ONE update sequence
+# u = a / (K_bd v), v = b / (K_bd^T u) run on the stacked system (v0 = 1, exactly L iterations);
+# pair q's cost is the sum over its block of u_r K_rc C_rc v_c.  Written independently of
+# eot_pair_costs (no shared helper beyond the input slicing), so the pins below can compare the
+# two.  Denominators are not clamped (the S:62 floor is the per-pair form's; BDS inputs in the
+# pins keep every denominator far above it).
+# ------------------------------------------------------------------------------------------
+def bds_eot_costs(points, offsets, weights, eps, iters, pi, pj, scale) -> np.ndarray:
+    import scipy.sparse as sp
+
+    blocks_K, blocks_C, a_parts, b_parts, rows, cols = [], [], [], [], [], []
+    for i, j in zip(pi, pj):
+        si, ei = int(offsets[i]), int(offsets[i + 1])
+        sj, ej = int(offsets[j]), int(offsets[j + 1])
+        X = np.asarray(points[si:ei], dtype=np.float64)
+        Y = np.asarray(points[sj:ej], dtype=np.float64)
+        C = float(scale) * ((X[:, None, :] - Y[None, :, :]) ** 2).sum(-1)
+        blocks_C.append(C)
+        blocks_K.append(np.exp(-C / float(eps)))
+        a_parts.append(np.asarray(weights[si:ei], dtype=np.float64))
+        b_parts.append(np.asarray(weights[sj:ej], dtype=np.float64))
+        rows.append(ei - si)
+        cols.append(ej - sj)
+    Kbd = sp.block_diag(blocks_K, format="csr")
+    KCbd = sp.block_diag([k * c for k, c in zip(blocks_K, blocks_C)], format="csr")
+    a = np.concatenate(a_parts)
+    b = np.concatenate(b_parts)
+    v = np.ones(b.shape[0])
+    u = np.zeros(a.shape[0])
+    for _ in range(iters):
+        u = a / (Kbd @ v)
+        v = b / (Kbd.T @ u)
+    per_row = u * (KCbd @ v)                       # u_r sum_c K_rc C_rc v_c, stacked rows
+    ends = np.cumsum(rows)
+    return np.add.reduceat(per_row, np.concatenate([[0], ends[:-1]])) if len(rows) else np.zeros(0)
