@@ -667,6 +667,27 @@ def main():
                     "note": "tf32_frac counts the three TF32 MMAs per product against dense TF32 "
                             "(measured bf16 x 1.1/2.25); the r gather between layers leaves the "
                             "tensor pipe idle (DESIGN.md, DL TC kernel)"}
+            ml_tc = (args.mapping == "ml"
+                     and asot.asot._lib_handle().asot_map_soft_ml_workspace_bytes(d_, h_, K_) > 0)
+            if ml_tc:
+                # both MLP layers on the tensor cores: 3 BF16 MMAs per product (BF16x3 split,
+                # asot_soft_ml_tc.cu), against the measured dense BF16 peak
+                flops = flops_pt * T_rank
+                bpeak = peaks["bf16_tflops"]
+                mapping = {
+                    "kernel": "soft_ml_tc_kernel (MLP d->2d->K on tcgen05 kind::f16, BF16x3 split; "
+                              "|.|/l1 and fp64 a' = Z^T a on the CUDA cores)",
+                    "ms_per_launch": map_avg_ms, "points_per_launch": T_rank,
+                    "flops_per_point": flops_pt, "bound": "tensor",
+                    "tflops_algorithmic": flops / (map_avg_ms / 1e3) / 1e12,
+                    "bf16_issued_tflops": 3 * flops / (map_avg_ms / 1e3) / 1e12,
+                    "bf16_peak_tflops": bpeak,
+                    "bf16_frac": 3 * flops / (map_avg_ms / 1e3) / 1e12 / bpeak,
+                    "hbm_gbs": bytes_ / (map_avg_ms / 1e3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                    "share_of_step": map_ms / max(tot_ms, 1e-9),
+                    "note": "bf16_frac counts the three BF16 MMAs per product; per 128-point tile the "
+                            "layers run back to back (relu/split epilogue between them) and a CUDA-core "
+                            "pass normalises the codes and sums the histogram"}
         if T_rank is not None and args.mapping != "onehot" and mapping is None:
             mapping = {
                 "kernel": kname, "ms_per_launch": map_avg_ms, "points_per_launch": T_rank,

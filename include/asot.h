@@ -216,7 +216,15 @@ asot_status asot_map_soft_ml(const float* points, const int64_t* offsets,
                              const int64_t* offsets_host, const float* weights, int64_t n_dist,
                              int32_t dim, int32_t n_anchors, int32_t hidden, const float* W1,
                              const float* b1, const float* W2, const float* b2, float* hist_out,
-                             float* codes_out, uint32_t* status, void* stream);
+                             float* codes_out, uint32_t* status, void* workspace,
+                             size_t workspace_bytes, void* stream);
+/* Device workspace for asot_map_soft_ml: dim in {32, 64, 128} (points 16-byte aligned), hidden a
+ * multiple of 64 up to 256 and n_anchors a multiple of 64 in [64, 1024] run both MLP layers on
+ * the tensor cores (asot_soft_ml_tc.cu: tcgen05 kind::f16 with BF16 hi + lo split operands,
+ * three MMAs per k-step; R#35), which keep their split weight images (BF16 hi + lo of W1 and
+ * W2, 4 (dim' hidden + hidden n_anchors) bytes, dim' = dim rounded up to 64) here; 0 for other
+ * shapes.  A smaller workspace (or NULL) selects the CUDA-core kernel. */
+size_t asot_map_soft_ml_workspace_bytes(int32_t dim, int32_t hidden, int32_t n_anchors);
 
 /* ASOT-DL near-one-hot encoder (Eqs. (8)(9); appendix; Table 4):
  *   lambda_p = softplus(relu(x V1 + c1) . v2 + c2[0]); z^(0) = 0; n_layers times

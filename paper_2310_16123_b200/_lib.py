@@ -41,7 +41,8 @@ _SIGS = {
     "asot_unpack_tiles": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i32, c_vp]),
     "asot_tile_pairs_host": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "asot_map_soft_ml": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
-                                 c_vp, c_vp, c_vp, c_vp, c_vp]),
+                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "asot_map_soft_ml_workspace_bytes": (c_size, [c_i32, c_i32, c_i32]),
     "asot_map_soft_dl": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_map_soft_dl_workspace_bytes": (c_size, [c_i32, c_i32, c_i64]),

@@ -259,17 +259,25 @@ def _soft_common(points, offsets, weights, offsets_host, K, status, want_codes):
 def map_soft_ml(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
                 W1: torch.Tensor, b1: torch.Tensor, W2: torch.Tensor, b2: torch.Tensor,
                 offsets_host: Optional[np.ndarray] = None, want_codes: bool = False,
-                status: Optional[torch.Tensor] = None, stream=None):
+                status: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
+                tensor_cores: bool = True, stream=None):
     """NEXT-1 ASOT-ML mapping: codes |MLP(x)| / l1 and H = Z^T a per distribution.
-    Returns (H [N, K], codes [T, K] or None, status)."""
+    ``tensor_cores=False`` passes no workspace, which selects the CUDA-core kernel (the
+    cross-check implementation).  Returns (H [N, K], codes [T, K] or None, status)."""
     _need_cuda(W1, b1, W2, b2)
     _need_f32(points, weights, W1, b1, W2, b2)
     d, hidden = W1.shape
     K = int(W2.shape[1])
+    if tuple(b1.shape) != (hidden,) or tuple(W2.shape) != (hidden, K) or tuple(b2.shape) != (K,):
+        raise ValueError("ML weights: W1 [d, h], b1 [h], W2 [h, K], b2 [K]")
     oh, N, T, H, codes, st = _soft_common(points, offsets, weights, offsets_host, K, status, want_codes)
-    _check(_lib_handle().asot_map_soft_ml(
+    L = _lib_handle()
+    nbytes = int(L.asot_map_soft_ml_workspace_bytes(int(d), int(hidden), K)) if tensor_cores else 0
+    ws = _ws(workspace, points.device).get(nbytes) if nbytes > 0 else None
+    _check(L.asot_map_soft_ml(
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), K, int(hidden), _ptr(W1),
-        _ptr(b1), _ptr(W2), _ptr(b2), _ptr(H), _ptr(codes), _ptr(st), _stream(stream)))
+        _ptr(b1), _ptr(W2), _ptr(b2), _ptr(H), _ptr(codes), _ptr(st), _ptr(ws),
+        0 if ws is None else ws.numel(), _stream(stream)))
     return H, (codes[:T] if codes is not None else None), st
 
 

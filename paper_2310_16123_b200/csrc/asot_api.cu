@@ -445,14 +445,25 @@ asot_status asot_map_soft_ml(const float* points, const int64_t* offsets,
                              const int64_t* offsets_host, const float* weights, int64_t n_dist,
                              int32_t dim, int32_t n_anchors, int32_t hidden, const float* W1,
                              const float* b1, const float* W2, const float* b2, float* hist_out,
-                             float* codes_out, uint32_t* status, void* stream) {
+                             float* codes_out, uint32_t* status, void* workspace,
+                             size_t workspace_bytes, void* stream) {
   g_launches = 0;
   asot_status st = check_soft(points, offsets, offsets_host, weights, n_dist, dim, n_anchors,
                               hidden, hist_out, status);
   if (st != ASOT_OK) return st;
   ASOT_CHECK_ARG(W1 && b1 && W2 && b2, "null pointer argument");
   cudaStream_t s = (cudaStream_t)stream;
+  Nvtx range("asot next1 map_soft_ml");
   ProfScope prof(ASOT_PROF_MAP, s);
+  // both MLP layers on tcgen05 (BF16x3) when the shapes allow and the workspace is given;
+  // otherwise the CUDA-core kernel (also the cross-check implementation)
+  const size_t need = asot_map_soft_ml_workspace_bytes(dim, hidden, n_anchors);
+  if (need > 0 && workspace && workspace_bytes >= need && ((uintptr_t)points & 15u) == 0) {
+    ASOT_LAUNCH(asot::launch_soft_ml_tc(points, offsets, weights, n_dist, dim, hidden, n_anchors, W1, b1,
+                                        W2, b2, hist_out, codes_out, (uint8_t*)workspace, status,
+                                        device_sms(), s));
+    return ASOT_OK;
+  }
   ASOT_LAUNCH(asot::launch_soft_map_ml(points, offsets, weights, n_dist, dim, n_anchors, hidden,
                                        W1, b1, W2, b2, hist_out, codes_out, status, s));
   return ASOT_OK;
@@ -498,6 +509,11 @@ asot_status asot_map_soft_dl(const float* points, const int64_t* offsets,
                                        n_layers, hidden, V1, c1, v2, c2, hist_out, codes_out,
                                        status, s));
   return ASOT_OK;
+}
+
+size_t asot_map_soft_ml_workspace_bytes(int32_t dim, int32_t hidden, int32_t n_anchors) {
+  if (!asot::soft_ml_tc_supported(dim, hidden, n_anchors)) return 0;
+  return asot::soft_ml_tc_workspace_bytes(dim, hidden, n_anchors, device_sms());
 }
 
 size_t asot_map_soft_dl_workspace_bytes(int32_t dim, int32_t n_anchors, int64_t n_points) {

@@ -426,6 +426,12 @@ cudaError_t read_kernel_clock_tc2(long long* host4);
 // NEXT-1 ASOT-DL encoder with sparse codes (asot_soft_dl_sparse.cu)
 bool soft_dl_sparse_supported(int dim, int K);
 size_t soft_dl_sparse_workspace_bytes(int K, int sms);
+bool soft_ml_tc_supported(int dim, int hidden, int K);
+size_t soft_ml_tc_workspace_bytes(int dim, int hidden, int K, int sms);
+cudaError_t launch_soft_ml_tc(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist,
+                              int dim, int hidden, int K, const float* W1, const float* b1, const float* W2,
+                              const float* b2, float* H, float* codes, uint8_t* ws, uint32_t* status, int sms,
+                              cudaStream_t s);
 bool soft_dl_tc_supported(int dim, int K);
 size_t soft_dl_tc_workspace_bytes(int dim, int K, int sms, int64_t T);
 cudaError_t launch_soft_dl_tc(const float* points, const int64_t* offsets, const float* weights, int64_t n_dist, int dim,

@@ -5,11 +5,11 @@
 // ties).  The decision must be bit-exact against the fp64 definition (reading R#8):
 // D_pj = sum_k (x_pk - w_jk)^2 accumulated sequentially in k in fp64 with every op rounded.
 // Kernel: a point x anchor distance tile, register-blocked (4 points x 4 anchors per thread, both
-// staged in shared memory), fp32 direct differences (f32x2 FSUB / FFMA), the 16 lanes sharing a
+// staged in shared memory), fp32 direct differences (f32x2 FSUB / FFMA), the 16 or 32 lanes sharing a
 // point merge (best, index, second-best) with warp shuffles.  fp32 with a rigorous bound:
 // for d non-negative rounded terms, |D32 - D| <= gamma_{d+2} D (gamma_n = n u / (1 - n u),
 // u = 2^-24), for any summation order.  If the runner-up D32 exceeds best * (1 + 5 gamma) (+ an
-// absolute underflow slack) the fp32 winner provably is the fp64 winner; otherwise the 16 lanes
+// absolute underflow slack) the fp32 winner provably is the fp64 winner; otherwise the lanes
 // recompute all K distances with the fp64 op sequence above and take the (value, index) minimum.
 //
 // a3 (Eq. (5) P:100 with the 1/n factor dropped, R#1; Lemma 1 proof a' = Z^T a P:145, P:417;
@@ -63,17 +63,19 @@ cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, flo
 // ------------------------------------------------------------------------------ a2: mapping
 // Point x anchor distance tile, register-blocked like a GEMM: a CTA stages a tile of 64 points
 // and a chunk of anchors in shared memory (rows padded to DP + 4 floats: 16-byte vector loads,
-// consecutive anchor rows 16 bytes apart in the bank space); thread (warp w, lane l) owns the 4
-// points 4 (2w + l/16) + [0, 4) and, per group of 64 anchors, the 4 anchors 16a + l%16
-// (a = 0..3).  Per 4 coordinates it loads 4 point float4 (broadcast across the 16 lanes that share
-// them) and 4 anchor float4, and issues 16 x (2 FSUB2 + 2 FFMA2): each staged value feeds 4
-// distances (the round-1 kernel held one point per lane, so every anchor load fed one point).
-// fp32 squared distances with the rigorous near-tie test of R#8, then the 16 lanes sharing a
+// consecutive anchor rows 16 bytes apart in the bank space); thread (warp w, lane l) owns 4
+// points and, per group of 4 LPP anchors, the 4 anchors LPP a + l % LPP (a = 0..3).  LPP = 16
+// (K < 128): the points 4 (2w + l/16) + [0, 4); LPP = 32 (K >= 128): all 32 lanes share the
+// points 4 (2w + pass) + [0, 4), two passes per tile, so a point float4 is one broadcast
+// shared-memory wavefront for the whole warp (LPP = 16 needs two per load and leaves the loop
+// bound by shared-memory wavefronts, 36 per 64 FP32 instructions, instead of the FMA pipe).  Per
+// 4 coordinates a thread loads 4 point float4 and 4 anchor float4 and issues 16 x (2 FSUB2 +
+// 2 FFMA2): each staged value feeds 4 distances.
+// fp32 squared distances with the rigorous near-tie test of R#8, then the LPP lanes sharing a
 // point merge (best, index, second) with shuffles; ambiguous points are recomputed in fp64 in the
-// oracle's op order by those 16 lanes.
+// oracle's op order by those LPP lanes.
 constexpr int kMapThreads = 256;
 constexpr int kTilePoints = 64;                 // points per tile (16 groups of 4)
-constexpr int kMapAnchorGroup = 64;             // anchors per register pass (16 lanes x 4)
 
 struct BestTriple {
   float best;
@@ -94,7 +96,7 @@ __device__ __forceinline__ void merge_triple(BestTriple& a, float ob, float os, 
 
 __device__ __forceinline__ uint32_t smem_u32_of(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int DP>
+template <int DP, int LPP>
 __global__ void __launch_bounds__(kMapThreads, 2)
 map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ gather, int64_t T,
                   int dim, const float* __restrict__ anchors, int K, int chunk,
@@ -103,9 +105,12 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
   constexpr int RS = DP + 4;                        // row stride (floats)
   float* Xs2 = reinterpret_cast<float*>(map_smem4); // 2 x [64][RS] points: current and next tile
   float* Ws = Xs2 + (DP <= 64 ? 2 : 1) * kTilePoints * RS;   // [chunk][RS] anchors
+  constexpr int kMapAnchorGroup = 4 * LPP;          // anchors per register pass
+  constexpr int kPass = LPP / 16;                   // point groups per thread
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tx = lane & 15;                         // anchor slot
-  const int pg = 2 * warp + (lane >> 4);            // point group: points 4 pg + [0, 4)
+  const int tx = lane % LPP;                        // anchor slot
+  // point group of pass ps: points 4 pg + [0, 4)
+  auto pg_of = [&](int ps) { return LPP == 16 ? 2 * warp + (lane >> 4) : 2 * warp + ps; };
 
   // anchors are checked for non-finite values once (block 0), not at every staging
   if (blockIdx.x == 0) {
@@ -177,16 +182,18 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
       __syncthreads();
     }
     if (dbuf) buf ^= 1;
-    {   // non-finite coordinates of this thread's points (each point checked by its 16 lanes)
+    {   // non-finite coordinates of this thread's points (each point checked by its LPP lanes)
       bool finite = true;
-      for (int q = 0; q < 4; ++q)
-        for (int k = tx; k < DP; k += 16) finite &= isfinite(Xs[(4 * pg + q) * RS + k]);
+      for (int ps = 0; ps < kPass; ++ps)
+        for (int q = 0; q < 4; ++q)
+          for (int k = tx; k < DP; k += LPP) finite &= isfinite(Xs[(4 * pg_of(ps) + q) * RS + k]);
       if (!finite) atomicOr(status, ASOT_FLAG_NONFINITE_INPUT);
     }
-    BestTriple bt[4];
+    BestTriple bt[kPass][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) bt[q] = BestTriple{INFINITY, INFINITY, 0x7fffffff};
-    const float* xr = Xs + 4 * pg * RS;
+    for (int ps = 0; ps < kPass; ++ps)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bt[ps][q] = BestTriple{INFINITY, INFINITY, 0x7fffffff};
     for (int j0 = 0; j0 < K; j0 += chunk) {
       const int nc = min(chunk, K - j0);
       const int nc64 = (nc + kMapAnchorGroup - 1) / kMapAnchorGroup * kMapAnchorGroup;
@@ -195,8 +202,11 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
         stage_rows(Ws, nc, nc64, anchors + (int64_t)j0 * dim, avec, [](int r) { return (int64_t)r; });
         __syncthreads();
       }
-      for (int g0 = 0; g0 < nc64; g0 += kMapAnchorGroup) {
+      for (int g0 = 0; g0 < nc64; g0 += kMapAnchorGroup)
+#pragma unroll
+      for (int ps = 0; ps < kPass; ++ps) {
         const float* wr = Ws + (g0 + tx) * RS;
+        const float* xr = Xs + 4 * pg_of(ps) * RS;
         float2 acc[4][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -208,7 +218,7 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
 #pragma unroll
           for (int q = 0; q < 4; ++q) xv[q] = *reinterpret_cast<const float4*>(xr + q * RS + k);
 #pragma unroll
-          for (int a = 0; a < 4; ++a) wv[a] = *reinterpret_cast<const float4*>(wr + 16 * a * RS + k);
+          for (int a = 0; a < 4; ++a) wv[a] = *reinterpret_cast<const float4*>(wr + LPP * a * RS + k);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -222,48 +232,54 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
         // anchors j increase along a within a lane: strict < keeps the lowest index
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          const int j = j0 + g0 + tx + 16 * a;
+          const int j = j0 + g0 + tx + LPP * a;
           if (j < K) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const float dq = acc[q][a].x + acc[q][a].y;
-              if (dq < bt[q].best) {
-                bt[q].second = bt[q].best;
-                bt[q].best = dq;
-                bt[q].idx = j;
-              } else if (dq < bt[q].second) {
-                bt[q].second = dq;
+              BestTriple& b = bt[ps][q];
+              if (dq < b.best) {
+                b.second = b.best;
+                b.best = dq;
+                b.idx = j;
+              } else if (dq < b.second) {
+                b.second = dq;
               }
             }
           }
         }
       }
     }
-    // merge across the 16 lanes that share the points (lane groups of 16 within the warp)
+    // merge across the LPP lanes that share the points
+#pragma unroll
+    for (int ps = 0; ps < kPass; ++ps)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
-      for (int off = 1; off < 16; off <<= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, bt[q].best, off);
-        const float os = __shfl_xor_sync(0xffffffffu, bt[q].second, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bt[q].idx, off);
-        merge_triple(bt[q], ob, os, oi);
+      for (int off = 1; off < LPP; off <<= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, bt[ps][q].best, off);
+        const float os = __shfl_xor_sync(0xffffffffu, bt[ps][q].second, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bt[ps][q].idx, off);
+        merge_triple(bt[ps][q], ob, os, oi);
       }
     }
     // near-tie test with the rigorous fp32 bound (gamma_{d+2}, 5x slack incl. rounding of thr);
     // ambiguous points: fp64 recomputation in the pinned op order t = x - w; acc = acc + t*t
 #pragma unroll
+    for (int ps = 0; ps < kPass; ++ps)
+#pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int pl = 4 * pg + q;
+      BestTriple& b = bt[ps][q];
+      const int pl = 4 * pg_of(ps) + q;
       const bool valid = pl < np;
-      const float thr = bt[q].best * (1.0f + 5.0f * gamma) + 1e-35f;
-      const bool refine = valid && K > 1 && (bt[q].second <= thr);
+      const float thr = b.best * (1.0f + 5.0f * gamma) + 1e-35f;
+      const bool refine = valid && K > 1 && (b.second <= thr);
       if (__any_sync(0xffffffffu, refine)) {
         double bd = INFINITY;
         int bi = 0x7fffffff;
         if (refine) {
           const float* xp = Xs + pl * RS;
-          for (int j = tx; j < K; j += 16) {
+          for (int j = tx; j < K; j += LPP) {
             const float* wj = anchors + (int64_t)j * dim;
             double accd = 0.0;
             for (int k = 0; k < dim; ++k) {
@@ -277,7 +293,7 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
           }
         }
 #pragma unroll
-        for (int off = 1; off < 16; off <<= 1) {
+        for (int off = 1; off < LPP; off <<= 1) {
           const double ob = __shfl_xor_sync(0xffffffffu, bd, off);
           const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
           if (ob < bd || (ob == bd && oi < bi)) {
@@ -285,17 +301,18 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
             bi = oi;
           }
         }
-        if (refine) bt[q].idx = bi;
+        if (refine) b.idx = bi;
       }
-      if (valid && tx == 0) assign[p0 + pl] = bt[q].idx;
+      if (valid && tx == 0) assign[p0 + pl] = b.idx;
     }
   }  // tiles
 }
 
-template <int DP>
+template <int DP, int LPP>
 static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int64_t T, int dim,
                                  const float* anchors, int K, int32_t* assign, uint32_t* status,
                                  cudaStream_t s) {
+  constexpr int kMapAnchorGroup = 4 * LPP;
   const int rs_bytes = (DP + 4) * 4;
   // anchor chunk: whole 64-anchor groups such that the CTA (with its one or two point tiles)
   // fits twice per SM
@@ -304,17 +321,17 @@ static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int
   const int K64 = (K + kMapAnchorGroup - 1) / kMapAnchorGroup * kMapAnchorGroup;
   if (chunk > K64) chunk = K64;
   const size_t smem = (size_t)(chunk + kTiles * kTilePoints) * rs_bytes;
-  cudaError_t e = cudaFuncSetAttribute(map_assign_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(map_assign_kernel<DP, LPP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t blocks = (T + kTilePoints - 1) / kTilePoints;
   if (blocks == 0) return cudaSuccess;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, map_assign_kernel<DP>, kMapThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, map_assign_kernel<DP, LPP>, kMapThreads, smem);
   if (per_sm < 1) per_sm = 1;
   if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;   // persistent grid
-  map_assign_kernel<DP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, gather, T, dim, anchors,
+  map_assign_kernel<DP, LPP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, gather, T, dim, anchors,
                                                                    K, chunk, assign, status);
   return cudaGetLastError();
 }
@@ -322,11 +339,18 @@ static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
                               int32_t* assign, uint32_t* status, cudaStream_t s,
                               const int64_t* gather) {
-  if (dim <= 8) return launch_map_dp<8>(points, gather, T, dim, anchors, K, assign, status, s);
-  if (dim <= 16) return launch_map_dp<16>(points, gather, T, dim, anchors, K, assign, status, s);
-  if (dim <= 32) return launch_map_dp<32>(points, gather, T, dim, anchors, K, assign, status, s);
-  if (dim <= 64) return launch_map_dp<64>(points, gather, T, dim, anchors, K, assign, status, s);
-  return launch_map_dp<128>(points, gather, T, dim, anchors, K, assign, status, s);
+  // K >= 128: 32 lanes share a thread's points (one broadcast wavefront per point load)
+  if (K >= 128 && dim > 8) {
+    if (dim <= 16) return launch_map_dp<16, 32>(points, gather, T, dim, anchors, K, assign, status, s);
+    if (dim <= 32) return launch_map_dp<32, 32>(points, gather, T, dim, anchors, K, assign, status, s);
+    if (dim <= 64) return launch_map_dp<64, 32>(points, gather, T, dim, anchors, K, assign, status, s);
+    return launch_map_dp<128, 32>(points, gather, T, dim, anchors, K, assign, status, s);
+  }
+  if (dim <= 8) return launch_map_dp<8, 16>(points, gather, T, dim, anchors, K, assign, status, s);
+  if (dim <= 16) return launch_map_dp<16, 16>(points, gather, T, dim, anchors, K, assign, status, s);
+  if (dim <= 32) return launch_map_dp<32, 16>(points, gather, T, dim, anchors, K, assign, status, s);
+  if (dim <= 64) return launch_map_dp<64, 16>(points, gather, T, dim, anchors, K, assign, status, s);
+  return launch_map_dp<128, 16>(points, gather, T, dim, anchors, K, assign, status, s);
 }
 
 // ------------------------------------------------------------------------------ a3: histograms

@@ -85,6 +85,39 @@ def test_mapping_adversarial_ties(asot):
     assert assign.cpu().numpy()[-2] == 3
 
 
+@pytest.mark.parametrize("case", ["offset", "tiny", "huge", "mixed"])
+@pytest.mark.parametrize("d,K", [(16, 64), (64, 256), (128, 1024)])
+def test_mapping_extreme_magnitudes(asot, case, d, K):
+    """The kernel decides in fp32 with the rigorous near-tie bound of R#8 and falls back to the
+    fp64 op sequence: a large common offset (|x| >> the distances), coordinates near 1e-20
+    (subnormal squares: the absolute slack), near 1e19 (fp32 overflow of the distances: every
+    point falls back to fp64) and a mix of scales within one batch.  The decision stays the
+    fp64 definition's, bit for bit."""
+    rng = np.random.default_rng(d + K + len(case))
+    C = max(K // 8, 1)
+    means = rng.normal(size=(C, d))
+    W = np.repeat(means, K // C, axis=0)[:K] + 0.2 * rng.normal(size=(K, d))
+    comp = rng.integers(0, C, size=3000)
+    X = means[comp] + 0.3 * rng.normal(size=(3000, d))
+    if case == "offset":
+        X, W = X + 1000.0, W + 1000.0
+    elif case == "tiny":
+        X, W = X * 1e-20, W * 1e-20
+    elif case == "huge":
+        X, W = X * 1e19, W * 1e19
+    else:
+        X = X * np.repeat(10.0 ** rng.integers(-6, 6, size=300), 10)[:, None]
+    X, W = X.astype(np.float32), W.astype(np.float32)
+    off = np.array([0, X.shape[0]], np.int64)
+    w = np.full(X.shape[0], np.float32(1.0 / X.shape[0]))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    assign, H, st = asot.map_to_anchors(t(X), t(off), t(w), t(W), offsets_host=off)
+    torch.cuda.synchronize()
+    a_o = O.map_assign(X, W)
+    a_g = assign.cpu().numpy()
+    assert np.array_equal(a_g, a_o), f"{(a_g != a_o).sum()} of {a_o.size} assignments differ"
+
+
 @pytest.mark.parametrize("d,K", [(7, 40), (13, 300), (100, 9), (100, 400)])
 def test_mapping_odd_dims_unaligned(asot, d, K):
     """Dimensions that are not a multiple of 4 and point / anchor buffers that are not 16-byte

@@ -136,3 +136,35 @@ def test_soft_distance_matrices_end_to_end(asot, prec):
     Do = np.zeros((dinp.n_dist, dinp.n_dist)); Do[pi, pj] = c; Do[pj, pi] = c
     eff = asot.effective_precision(dinp.n_anchors, prec)
     assert rel_err(D.cpu().numpy(), Do).max() <= TOL[eff]
+
+
+@pytest.mark.parametrize("d,h,K", [(32, 64, 64), (64, 128, 256), (64, 192, 128), (128, 256, 1024)])
+def test_soft_ml_tensor_core_ragged(asot, d, h, K):
+    """The tcgen05 ML kernel (BF16x3 split operands, R#35) on ragged distributions around its
+    128-point tile (1, 127, 128, 129, 300 points): codes and H within 1e-5 of the oracle and of
+    the CUDA-core kernel (tensor_cores=False), status clean."""
+    from asot_inputs.soft import make_ml_model
+    rng = np.random.default_rng(d + h + K)
+    sizes = np.array([1, 127, 128, 129, 300, 5])
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    X = rng.normal(0.0, 1.0, size=(off[-1], d)).astype(np.float32)
+    w = np.concatenate([rng.dirichlet(np.ones(n)) for n in sizes]).astype(np.float32)
+    m = make_ml_model(d, K)
+    W1 = rng.normal(0.0, np.sqrt(2.0 / d), size=(d, h)).astype(np.float32)
+    b1 = rng.normal(0.0, 0.1, size=h).astype(np.float32)
+    W2 = rng.normal(0.0, np.sqrt(1.0 / h), size=(h, K)).astype(np.float32)
+    b2 = m.b2
+    args = (dev(X), dev(off), dev(w), dev(W1), dev(b1), dev(W2), dev(b2))
+    assert asot.asot._lib_handle().asot_map_soft_ml_workspace_bytes(d, h, K) > 0
+    H, Z, st = asot.map_soft_ml(*args, offsets_host=off, want_codes=True)
+    Hc, Zc, stc = asot.map_soft_ml(*args, offsets_host=off, want_codes=True, tensor_cores=False)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    asot.check_status(stc)
+    Zo, flags = S.ml_encode(X, [(W1, b1), (W2, b2)])
+    assert not flags.any()
+    np.testing.assert_allclose(Z.cpu().numpy(), Zo, rtol=0, atol=CODE_TOL)
+    np.testing.assert_allclose(Z.cpu().numpy(), Zc.cpu().numpy(), rtol=0, atol=CODE_TOL)
+    Ho = S.soft_histograms(Zo, w, off)
+    np.testing.assert_allclose(H.cpu().numpy(), Ho, rtol=0, atol=CODE_TOL)
+    np.testing.assert_allclose(H.cpu().numpy(), Hc.cpu().numpy(), rtol=0, atol=CODE_TOL)

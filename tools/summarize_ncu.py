@@ -95,9 +95,9 @@ def full(rep, out_json, traffic_key=None, kernel=None):
         t[traffic_key] = {
             'source': os.path.relpath(out_json, ROOT),
             'kernel': out['kernel'][:120] if out['kernel'] else None,
-            'gpu_time_ms': num('gpu__time_duration.sum') / 1e6 if u[h.index('gpu__time_duration.sum')] == 'nsecond'
-            else num('gpu__time_duration.sum') * {'usecond': 1e-3, 'msecond': 1.0, 'second': 1e3}.get(
-                u[h.index('gpu__time_duration.sum')], 1.0),
+            'gpu_time_ms': num('gpu__time_duration.sum') * {
+                'ns': 1e-6, 'nsecond': 1e-6, 'us': 1e-3, 'usecond': 1e-3, 'ms': 1.0, 'msecond': 1.0,
+                's': 1e3, 'second': 1e3}.get(u[h.index('gpu__time_duration.sum')], 1.0),
             'dram_bytes_per_launch': traffic,
             'tensor_pipe_active_pct': pct('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'),
             'fma_pipe_active_pct': pct('sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active'),
