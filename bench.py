@@ -35,7 +35,7 @@ TF32_OVER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense tf32 / bf16
 FP32_ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max SM clock
 
 
-DEBUG_ENV = ("ASOT_TC_DEBUG_MODE", "ASOT_PAIR_KERNEL", "ASOT_SOFT_DL_GENERIC")
+DEBUG_ENV = ("ASOT_TC_DEBUG_MODE", "ASOT_PAIR_KERNEL", "ASOT_SOFT_DL_GENERIC", "ASOT_SPARSE")
 
 
 def asot_env() -> dict:
@@ -392,6 +392,7 @@ def main():
     launches = [0]
 
     exchange_note = ["single GPU: no exchange"]
+    last_H, last_A = [None], [None]   # the histograms / learned anchors of the last step (path kind)
     if (args.mapping != "onehot" or args.anchors != "seeded") and world > 1:
         raise SystemExit("--mapping ml/dl and --anchors kmeans are single-GPU in this build")
     km_events = []
@@ -409,6 +410,7 @@ def main():
         def step():
             H, _, _ = asot.map_soft_ml(pts, offs, w, mW1, mb1, mW2, mb2, offsets_host=inp.offsets,
                                        status=status)
+            last_H[0] = H
             launches[0] += asot.last_launch_count()
             C = asot.mahalanobis_cost(anc, mM, normalize=True, workspace=ws)
             launches[0] += 3
@@ -424,6 +426,7 @@ def main():
         def step():
             H, _, _ = asot.map_soft_dl(pts, offs, w, anc, dV1, dc1, dv2, dc2, m.n_layers,
                                        offsets_host=inp.offsets, status=status)
+            last_H[0] = H
             launches[0] += asot.last_launch_count()
             asot.distance_matrix(None, None, None, None, cst, float(inp.eps), inp.iters,
                                  precision=prec, hist=H, out=Dbuf, cost_max=cmax, status=status,
@@ -435,6 +438,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             _, A, _, _ = asot.kmeans_minibatch(pts, km_init_d, km_idx_d, status=status)
+            last_A[0] = A
             e1.record()
             km_events.append((e0, e1))
             launches[0] += asot.last_launch_count()
@@ -566,10 +570,34 @@ def main():
     flops_per_pair = 4 * K * K * L + 2 * K * K           # SURVEY §8(d) algorithmic work per pair
     pairs_per_launch = P if world == 1 else -(-P // world)
     peaks = measured_peaks()
-    kind = asot.asot.sinkhorn_kernel_kind(inp.n_anchors, prec)
+    # which Sinkhorn kernel the calls ran: the library decides on the device from the histograms'
+    # supports (asot_sinkhorn_path_kind states the rule); recompute them here for the report
+    if last_H[0] is not None:
+        H_path = last_H[0]
+    else:
+        _, H_path, _ = asot.map_to_anchors(pts, offs, w, last_A[0] if last_A[0] is not None else anc,
+                                           offsets_host=inp.offsets)
+    supports = (H_path != 0).sum(dim=1).to(torch.float64)
+    kind = asot.asot.sinkhorn_path_kind(H_path, prec)
     # hardware MAC rate of the kernel's MMA kind (per SM per clock) and MMAs per algorithmic product
     mac_clk, per_product = {10: (4096, 3), 3: (2048, 3), 5: (2048, 3)}.get(kind, (2048, 1))
-    if kind == 10:
+    sparse_info = None
+    if kind == 11:
+        # the small-support kernel (R#36): thread per pair, an 8 x 8 register block of K (supports
+        # <= 8; 9-16: a local-memory form), fp32 FFMA2 -- bound by the FP32 pipe / issue rate.
+        # Issued work: 2 updates x 64 MACs per iteration + the cost on the real block; useful work:
+        # the real |S_a| x |S_b| blocks (sum over i < j of m_i m_j)
+        S = supports
+        useful_mn = float((S.sum() ** 2 - (S * S).sum()) / 2) if world == 1 else None
+        flops_issued = 4 * 64 * L
+        peak = FP32_ALU_PEAK_TFLOPS
+        bound, peak_note = "alu", "FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz"
+        sparse_info = {"max_support": int(S.max()), "mean_support": float(S.mean()),
+                       "issued_flops_per_pair": flops_issued,
+                       "useful_flops_per_pair_mean": (4 * L + 2) * useful_mn / P if useful_mn else None,
+                       "dense_equivalent_flops_per_pair": flops_per_pair}
+        flops_per_pair = flops_issued
+    elif kind == 10:
         peak = peaks["bf16_tflops"] / 3
         bound, peak_note = "tensor", (f"BF16x3: dense BF16 ({peaks['_source']} {peaks['bf16_tflops']} TFLOP/s "
                                       f"burst) / 3 MMAs per algorithmic product")
@@ -593,6 +621,9 @@ def main():
     if os.path.exists(spath):
         with open(spath) as f:
             ncu_ev = json.load(f).get(f"{inp.name}:{args.precision}")
+        if kind == 11:
+            with open(spath) as f:
+                ncu_ev = json.load(f).get(f"{inp.name}:sparse")
         if ncu_ev:
             traffic = ncu_ev.get("dram_bytes_per_launch")
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -604,6 +635,13 @@ def main():
                 "peak_note": peak_note,
                 "peak_sustained_based": peaks.get("bf16_tflops_sustained", 0) * (TF32_OVER_BF16 if eff == asot.TF32 else 0) or None,
                 "ncu": ncu_ev}
+    if sparse_info is not None:
+        sparse_info["useful_tflops"] = (sparse_info["useful_flops_per_pair_mean"] or 0) * pairs_per_launch / (kern_avg_ms / 1e3) / 1e12
+        sparse_info["useful_frac"] = sparse_info["useful_tflops"] / peak
+        roofline["sparse"] = sparse_info
+        roofline["kernel_ms_note"] = ("the timed Sinkhorn launch scope = support extraction + fp32 K images "
+                                      "(sparse prep) + the small-support kernel + the dense kernel's "
+                                      "immediate return")
     if bound == "tensor" and rank == 0:
         ct = cublas_tf32_tflops(dev)
         roofline["cublas_tf32_measured_tflops"] = ct
@@ -966,7 +1004,7 @@ def main():
             "metric": baseline_metric(), "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind in (3, 5) else
+            "dtype": "f32" if kind == 11 else "tf32" if eff == asot.TF32 else ("f32 (3xtf32)" if kind in (3, 5) else
                                                       "f32 (bf16x3)" if kind == 10 else "f32"),
             "data": "synthetic",
             "config": workload_config(inp, args, world),

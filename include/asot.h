@@ -351,6 +351,13 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
  * 10 = BF16x3 fp32-accurate CTA-pair resident (ASOT_PREC_FP32, 128 < K <= 256).
  * (Pair lists: K <= 128 the 1-SM kernels' pair-list modes, else the streamed kernel's.) */
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested);
+/* The kernel a distance-matrix / pair-list call runs once the histograms are known: 11 = the
+ * small-support fp32 kernel (asot_sinkhorn_sparse.cu, DESIGN R#36) when n_anchors >= 64 and every
+ * histogram row has at most 16 non-zero bins (max_support = the largest count of non-zero bins
+ * in a row), for both precision requests; otherwise asot_sinkhorn_kernel_kind.  The calls take
+ * this decision on the device (no host synchronisation); this host function states the rule.
+ * Environment ASOT_SPARSE=0 (diagnostic) disables the small-support kernel. */
+int32_t asot_sinkhorn_path_kind(int32_t n_anchors, asot_precision requested, int32_t max_support);
 
 /* Optional kernel timing (bench.py's roofline): while enabled on this thread, the library records
  * a CUDA event pair on the launch stream immediately around every Sinkhorn kernel launch

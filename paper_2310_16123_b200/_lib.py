@@ -43,6 +43,7 @@ _SIGS = {
     "asot_map_soft_ml": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_map_soft_ml_workspace_bytes": (c_size, [c_i32, c_i32, c_i32]),
+    "asot_sinkhorn_path_kind": (c_i32, [c_i32, c_i32, c_i32]),
     "asot_map_soft_dl": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_map_soft_dl_workspace_bytes": (c_size, [c_i32, c_i32, c_i64]),

@@ -116,7 +116,15 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 7: "sinkhorn_tc_kernel (TF32, 1 SM, M=128, pair-list mode)",
                 8: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128, pair-list mode)",
                 9: "sinkhorn_warp_kernel (fp32 CUDA cores, lane per anchor, K < 32)",
-                10: "sinkhorn_tc6_kernel (BF16x3 fp32-accurate, resident, CTA pair, cta_group::2, M=256)"}
+                10: "sinkhorn_tc6_kernel (BF16x3 fp32-accurate, resident, CTA pair, cta_group::2, M=256)",
+                11: "sinkhorn_sparse_kernel (fp32 CUDA cores, thread per pair, histogram supports <= 16)"}
+
+
+def sinkhorn_path_kind(H: torch.Tensor, precision: int) -> int:
+    """The kernel a call on histograms H [N, K] runs (asot_sinkhorn_path_kind): 11 = the
+    small-support kernel, else sinkhorn_kernel_kind(K, precision)."""
+    max_support = int((H != 0).sum(dim=1).max().item()) if H.numel() else 0
+    return int(_lib_handle().asot_sinkhorn_path_kind(int(H.shape[1]), int(precision), max_support))
 
 
 def sinkhorn_kernel_kind(n_anchors: int, precision: int) -> int:

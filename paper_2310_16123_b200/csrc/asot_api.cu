@@ -107,6 +107,7 @@ int pair_kind(int32_t K, asot_precision prec) {
   return prec == ASOT_PREC_FP32 ? 5 : 6;
 }
 bool use_tc(int32_t K, asot_precision prec) { return tc_kind(K, prec) != 0; }
+constexpr int32_t kMinSparseAnchors = 64;   // the small-support path (R#36) from this K up
 // Bucketed pair lists (asot_pairs_bucket.cu): the tile kernel that serves the fully covered tiles
 // of a list of pair_kind `lk` (TF32: 7 -> the 1-SM kernel's tile mode, 6 -> the CTA-pair kernel
 // for K <= 256, else the streamed one; fp32: 8 -> the 1-SM 3xTF32 kernel, 5 -> the BF16x3
@@ -141,6 +142,7 @@ struct GibbsBufs {
   uint32_t* g_img = nullptr;
   uint32_t* gc_img = nullptr;
   uint8_t* scratch = nullptr;
+  asot::SparseBufs sp;   // the small-support path (R#36), every kind
 };
 
 GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
@@ -173,7 +175,16 @@ GibbsBufs carve_gibbs(Carver& cv, int32_t K, int kind, int64_t n_dist) {
     b.G = (float*)cv.take((size_t)K * asot::simt_kpad(K) * 4);
     b.GC = (float*)cv.take((size_t)K * asot::simt_kpad(K) * 4);
   }
+  uint8_t* spb = (uint8_t*)cv.take(asot::sparse_bytes(n_dist, K));
+  if (spb != nullptr) b.sp = asot::carve_sparse(spb, n_dist, K);
   return b;
+}
+
+// ASOT_SPARSE=0 (diagnostic, read per call: the GPU tests of the dense kernels set it; bench.py
+// refuses it) keeps every call on the dense kernels
+bool sparse_path_enabled() {
+  const char* e = getenv("ASOT_SPARSE");
+  return !(e && std::string(e) == "0");
 }
 
 // NVTX ranges per hot-path phase (SURVEY §5 tracing): host-side push/pop around each phase's
@@ -246,42 +257,57 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
   }
   Nvtx range("asot a5+a6 sinkhorn+cost");
   ProfScope prof(ASOT_PROF_SINKHORN, s);
+  // Small supports (R#36): the sparse kernel serves the call when every distribution has at most
+  // kSparseCap non-zero bins, decided on the device; the dense kernel below then returns at once
+  // (sink.dense_if), and vice versa.
+  asot::PairSink sinkd = sink;
+  // K < 64 stays on the dense kernels: a 16-bin support there saves at most 16x of K^2 <= 4096
+  // products per half-iteration, against the lane-per-anchor / 1-SM kernels' full occupancy
+  if (sparse_path_enabled() && gb.sp.flag != nullptr && K >= kMinSparseAnchors) {
+    ASOT_LAUNCH(asot::launch_sparse_prep(H, ps.n_dist, K, cost, eps, gb.sp, s));
+    const bool units = ps.units != nullptr && ps.pi == nullptr;
+    const int upt = units ? bucket_upt(kind) : 1;
+    const int64_t max_slots = units ? (tile_end - tile_begin) * asot::kTileSlots : ps.n_slots;
+    ASOT_LAUNCH(asot::launch_sinkhorn_sparse(ps, sink, K, gb.sp, iters, upt, max_slots, device_sms(), s));
+    sinkd.dense_if = gb.sp.flag;
+  }
+  const asot::PairSink& sink_dense = sinkd;
   if (kind == 5 || kind == 6) {
     const bool expl = ps.pi != nullptr;   // pair-list mode: tiles of 128 list entries
     ASOT_LAUNCH(asot::launch_sinkhorn_tc5(expl ? 0 : tile_begin,
                                           expl ? (ps.n_slots + asot::kTileSlots - 1) / asot::kTileSlots : tile_end,
-                                          ps.n_dist, sink, ps, H, K, (const uint8_t*)gb.g_img,
+                                          ps.n_dist, sink_dense, ps, H, K, (const uint8_t*)gb.g_img,
                                           (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters,
                                           kind == 5, s));
   } else if (kind == 4) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink, H, K,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc4(tile_begin, tile_end, ps.n_dist, sink_dense, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img,
                                           (uint8_t*)(((uintptr_t)gb.scratch + 1023) & ~(uintptr_t)1023), iters, s,
                                           ps.units, ps.n_dev));
   } else if (kind == 2) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink, H, K,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc2(tile_begin, tile_end, ps.n_dist, sink_dense, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s,
                                           ps.units, ps.n_dev));
   } else if (kind == 10) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc6(tile_begin, tile_end, ps.n_dist, sink, H, K,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc6(tile_begin, tile_end, ps.n_dist, sink_dense, H, K,
                                           (const uint8_t*)gb.g_img, (const uint8_t*)gb.gc_img, iters, s,
                                           ps.units, ps.n_dev));
   } else if (kind == 1) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc(tile_begin, tile_end, ps.n_dist, sink_dense, H, K, gb.g_img,
                                          gb.gc_img, iters, s, ps.units, ps.n_dev));
   } else if (kind == 7) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink_dense, H, K, gb.g_img,
                                                gb.gc_img, (float*)gb.scratch, iters, s, ps.n_dev));
   } else if (kind == 3) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink, H, K, gb.g_img,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc3(tile_begin, tile_end, ps.n_dist, sink_dense, H, K, gb.g_img,
                                           gb.gc_img, gb.GC, iters, s, ps.units, ps.n_dev));
   } else if (kind == 8) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_tc3_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink, H, K, gb.g_img,
+    ASOT_LAUNCH(asot::launch_sinkhorn_tc3_pairs(ps.pi, ps.pj, ps.n_slots, ps.n_dist, sink_dense, H, K, gb.g_img,
                                                 gb.gc_img, gb.GC, (float*)gb.scratch, iters, s, ps.n_dev));
   } else if (kind == 9) {
-    ASOT_LAUNCH(asot::launch_sinkhorn_warp(ps, sink, H, K, gb.G, gb.GC, iters, s));
+    ASOT_LAUNCH(asot::launch_sinkhorn_warp(ps, sink_dense, H, K, gb.G, gb.GC, iters, s));
   } else {
-    ASOT_LAUNCH(asot::launch_sinkhorn_simt(ps, sink, H, K, gb.G, gb.GC, iters, s));
+    ASOT_LAUNCH(asot::launch_sinkhorn_simt(ps, sink_dense, H, K, gb.G, gb.GC, iters, s));
   }
   return ASOT_OK;
 }
@@ -361,6 +387,13 @@ asot_status asot_profile_clock(int32_t kind, double* sm_mhz) {
 int64_t asot_num_tiles(int64_t n_dist) { return n_dist < 1 ? 0 : asot::num_tiles(n_dist); }
 
 int32_t asot_sinkhorn_kernel_kind(int32_t n_anchors, asot_precision requested) {
+  return tc_kind(n_anchors, requested);
+}
+
+int32_t asot_sinkhorn_path_kind(int32_t n_anchors, asot_precision requested, int32_t max_support) {
+  if (sparse_path_enabled() && n_anchors >= kMinSparseAnchors && n_anchors <= asot::kMaxAnchors &&
+      max_support <= asot::kSparseCap)
+    return 11;
   return tc_kind(n_anchors, requested);
 }
 

@@ -84,7 +84,13 @@ struct PairSink {
   uint32_t* status;
   int32_t list;   // explicit pair list: an invalid entry is an argument error, not tile padding
   const int32_t* idx = nullptr;   // slot s is stored at vec[idx[s]] (a compacted sub-list)
+  // small-support path (asot_sinkhorn_sparse.cu): a dense kernel returns at once unless
+  // *dense_if != 0 (a support above kSparseCap); null = always run
+  const uint32_t* dense_if = nullptr;
 };
+__device__ __forceinline__ bool dense_skipped(const PairSink& out) {
+  return out.dense_if != nullptr && *out.dense_if == 0u;
+}
 
 // Invalid slots: tile padding (i >= j or j >= N) stores 0 in the packed vector; an explicit-list
 // entry with an index outside [0, N) stores NaN and raises ASOT_FLAG_BAD_INDEX.
@@ -267,9 +273,30 @@ __host__ __device__ inline uint32_t sw128_kmajor_offset(uint32_t n, uint32_t k, 
   return lin ^ (((lin >> 7) & 7u) << 4);
 }
 
+// Small-support Sinkhorn (asot_sinkhorn_sparse.cu, R#36): per distribution up to kSparseCap
+// non-zero bins; fp32 K and K (.) C_s, the row sums of K, and the path flag.
+constexpr int kSparseCap = 16;
+struct SparseBufs {
+  float* G = nullptr;        // [K][K] fp32 K = exp(-C_s / eps)
+  float* GC = nullptr;       // [K][K] fp32 K (.) C_s
+  float* R = nullptr;        // [K] row sums of K (fp64-summed)
+  int32_t* cnt = nullptr;    // [n_dist] support sizes
+  uint16_t* idx = nullptr;   // [n_dist][kSparseCap] bins, increasing
+  float* val = nullptr;      // [n_dist][kSparseCap] masses
+  uint32_t* flag = nullptr;  // [1] != 0: some support > kSparseCap (the dense kernels run)
+};
+size_t sparse_bytes(int64_t n_dist, int K);
+SparseBufs carve_sparse(uint8_t* base, int64_t n_dist, int K);
+
 // ------------------------------------------------------------------------------------------
 // Launchers (return cudaGetLastError() after the launch).
 // ------------------------------------------------------------------------------------------
+cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const float* cost, float eps,
+                               const SparseBufs& sp, cudaStream_t s);
+// ps: a tile range, an explicit list (n_dev optional) or units of upt tiles (bucketed lists);
+// max_slots: the host-side upper bound of the slots
+cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, int K, const SparseBufs& sp, int iters,
+                                   int upt, int64_t max_slots, int sms, cudaStream_t s);
 cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, float* GC,
                               uint32_t* g_img, uint32_t* gc_img, int kpad, cudaStream_t s);
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,

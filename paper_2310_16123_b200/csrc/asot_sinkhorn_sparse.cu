@@ -1,0 +1,294 @@
+// asot_sinkhorn_sparse.cu -- a5 + a6 (batched Sinkhorn and cost) for
+// marginals with small supports, on the CUDA cores in fp32.
+//
+// With the one-hot mapping P_o a distribution of n_i points has a histogram
+// a' = Z^T a (Eq. (5)) with at most min(n_i, K) non-zero bins, and far fewer when its
+// points sit near a few anchors (c3: 1-9 of 256).  Where a_r = 0 the update u = a / (K v) gives
+// u_r = 0 exactly (R#11: m = 0 -> 0), and where b_c = 0, v_c = 0; a zero scaling contributes an
+// exact 0 to every later product.  So after the first half-iteration (v^0 = 1 on every anchor:
+// u_r = a_r / R_r with the full row sums R_r = sum_c K_rc) the whole recurrence of a pair lives on
+// the |S_a| x |S_b| block of K, and the cost u^T ((K (.) C_s) v) on the same block of K (.) C_s:
+// the same L iterations, the same formulas, the products with exact zeros left out (R#36).
+//
+// Path selection stays on the device (the call enqueues only): sparse_prep_kernel extracts each
+// distribution's support (<= kCap bins, increasing anchor index) and raises flag[0] when any
+// support is larger; the sparse kernel then returns at once and the dense tensor-core kernel runs
+// (its PairSink.dense_if = flag), otherwise the dense kernel returns at once.
+//
+// Per pair (one thread): the 8 x 8 block of K (padding entries 1, padded masses 0, so padded
+// scalings are exactly 0) in registers as row pairs, u as row pairs, v; each half-iteration is
+// 32 FFMA2 + 8 clamped reciprocal-multiplies (div_clamped: the S:62 clamp + DENOM_CLAMPED flag of
+// every fp32 kernel).  Pairs with a support of 9-16 bins take a local-memory form of the same
+// recurrence (rare: c3 has one such distribution in 2000).
+#include <cfloat>
+#include <cmath>
+
+#include "asot_internal.cuh"
+
+namespace asot {
+namespace sps {
+
+constexpr int kFast = 8;        // register-resident block of the fast form
+constexpr int kThreads = 128;   // one tile (8 x 16 pair slots) per CTA pass
+
+__global__ void gibbs_rows_kernel(const float* __restrict__ cost, int K, float eps, SparseBufs sp) {
+  // K = exp(-C_s / eps) and K (.) C_s in fp64, rounded to fp32 (as every Gibbs prep), and
+  // the row sums R_r = sum_c K_rc of the first half-iteration (v^0 = 1) summed in fp64
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < K; r += nwarps) {
+    double s = 0.0;
+    for (int c = lane; c < K; c += 32) {
+      const double cc = (double)cost[(int64_t)r * K + c];
+      const double g = exp(-cc / (double)eps);
+      sp.G[(int64_t)r * K + c] = (float)g;
+      sp.GC[(int64_t)r * K + c] = (float)(g * cc);
+      s += g;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sp.R[r] = (float)s;
+  }
+}
+
+__global__ void support_kernel(const float* __restrict__ H, int64_t n_dist, int K, SparseBufs sp) {
+  // warp per distribution: the non-zero bins (a_r != 0; NaN counts as non-zero) in increasing r
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_dist; i += nwarps) {
+    int cnt = 0;
+    for (int base = 0; base < K; base += 32) {
+      const int r = base + lane;
+      const float v = r < K ? H[i * K + r] : 0.0f;
+      const bool nz = r < K && v != 0.0f;
+      const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+      const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+      if (nz && pos < kSparseCap) {
+        sp.idx[i * kSparseCap + pos] = (uint16_t)r;
+        sp.val[i * kSparseCap + pos] = v;
+      }
+      cnt += __popc(bal);
+    }
+    if (lane == 0) {
+      sp.cnt[i] = cnt;
+      if (cnt > kSparseCap) atomicOr(sp.flag, 1u);
+    }
+  }
+}
+
+// x_e = m_e / d_e for 8 anchors, bitwise div_clamped: the range test once for the 8 -- every d in
+// [FLT_MIN, 2^126] exactly when no d is negative and sum_e d_e rcp(d_e) = 8 (+- 2^-19; a d
+// outside the range gives a product of 0, inf or NaN under rcp.approx.ftz) -- then
+// x = m rcp(d); otherwise the clamped per-element form (S:62 clamp + flag).
+__device__ __forceinline__ void div8(const float* m, const float* d, float* x, bool& clamped) {
+  float r[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) r[e] = rcp_ftz(d[e]);
+  float2 t = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) t = ffma2(make_float2(d[e], d[e + 1]), make_float2(r[e], r[e + 1]), t);
+  uint32_t sg = 0u;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sg |= __float_as_uint(d[e]);
+  if (fabsf((t.x + t.y) - 8.0f) < 2e-6f && !(sg >> 31)) {
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float2 q = fmul2(make_float2(m[e], m[e + 1]), make_float2(r[e], r[e + 1]));
+      x[e] = q.x;
+      x[e + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] = div_clamped(m[e], d[e], clamped);
+  }
+}
+
+// The fast form: |S_a|, |S_b| <= 8.  gp[q][c] = (K_{2q,c}, K_{2q+1,c}) of the block, up[q] =
+// (u_{2q}, u_{2q+1}).  u-update: rows in pairs, t = sum_c K_rc v_c (c increasing); v-update:
+// t = (even-r partial + odd-r partial) of sum_r K_rc u_r.
+__device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs& sp, int iters, bool& clamped) {
+  constexpr int M = kFast, Q = kFast / 2;
+  const int m = sp.cnt[i], n = sp.cnt[j];
+  const uint16_t* sa = sp.idx + (int64_t)i * kSparseCap;
+  const uint16_t* sb = sp.idx + (int64_t)j * kSparseCap;
+  float a[M], b[M];
+  float2 gp[Q][M];
+  float2 up[Q];
+  float v[M];
+  {
+    int ia[M], ib[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      ia[r] = r < m ? (int)sa[r] : 0;
+      a[r] = r < m ? sp.val[(int64_t)i * kSparseCap + r] : 0.0f;
+      ib[r] = r < n ? (int)sb[r] : 0;
+      b[r] = r < n ? sp.val[(int64_t)j * kSparseCap + r] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        const bool cv = c < n;
+        gp[q][c].x = (2 * q < m && cv) ? __ldg(sp.G + (int64_t)ia[2 * q] * K + ib[c]) : 1.0f;
+        gp[q][c].y = (2 * q + 1 < m && cv) ? __ldg(sp.G + (int64_t)ia[2 * q + 1] * K + ib[c]) : 1.0f;
+      }
+    // half-iteration 1: v^0 = 1 on every anchor, so (K v^0)_r is the full row sum R_r
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      up[q].x = 2 * q < m ? div_clamped(a[2 * q], __ldg(sp.R + ia[2 * q]), clamped) : 0.0f;
+      up[q].y = 2 * q + 1 < m ? div_clamped(a[2 * q + 1], __ldg(sp.R + ia[2 * q + 1]), clamped) : 0.0f;
+    }
+  }
+  auto v_update = [&]() {
+    float den[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      float2 t = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) t = ffma2(gp[q][c], up[q], t);
+      den[c] = t.x + t.y;
+    }
+    div8(b, den, v, clamped);
+  };
+  v_update();
+  for (int it = 1; it < iters; ++it) {
+    float den[M], un[M];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      float2 t = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int c = 0; c < M; ++c) t = ffma2(gp[q][c], make_float2(v[c], v[c]), t);
+      den[2 * q] = t.x;
+      den[2 * q + 1] = t.y;
+    }
+    div8(a, den, un, clamped);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) up[q] = make_float2(un[2 * q], un[2 * q + 1]);
+    v_update();
+  }
+  // a6: d = sum_r u_r sum_c (K (.) C_s)_rc v_c over the block
+  float d = 0.0f;
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    if (r < m) {
+      const float* gc = sp.GC + (int64_t)sa[r] * K;
+      float t = 0.0f;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+        if (c < n) t = fmaf(__ldg(gc + sb[c]), v[c], t);
+      d = fmaf((r & 1) ? up[r >> 1].y : up[r >> 1].x, t, d);
+    }
+  }
+  return d;
+}
+
+// Supports of 9-16 bins: the same recurrence with the block read from L1 / L2 every half-iteration.
+__device__ __noinline__ float pair_slow(int i, int j, int K, const SparseBufs& sp, int iters, bool* clamped_out) {
+  const int m = sp.cnt[i], n = sp.cnt[j];
+  const uint16_t* ia = sp.idx + (int64_t)i * kSparseCap;
+  const uint16_t* ib = sp.idx + (int64_t)j * kSparseCap;
+  const float* a = sp.val + (int64_t)i * kSparseCap;
+  const float* b = sp.val + (int64_t)j * kSparseCap;
+  float u[kSparseCap], v[kSparseCap];
+  bool clamped = false;
+  for (int r = 0; r < m; ++r) u[r] = div_clamped(a[r], __ldg(sp.R + ia[r]), clamped);
+  for (int it = 0; it < iters; ++it) {
+    if (it > 0) {
+      for (int r = 0; r < m; ++r) {
+        const float* g = sp.G + (int64_t)ia[r] * K;
+        float t = 0.0f;
+        for (int c = 0; c < n; ++c) t = fmaf(__ldg(g + ib[c]), v[c], t);
+        u[r] = div_clamped(a[r], t, clamped);
+      }
+    }
+    for (int c = 0; c < n; ++c) {
+      float t = 0.0f;
+      for (int r = 0; r < m; ++r) t = fmaf(__ldg(sp.G + (int64_t)ia[r] * K + ib[c]), u[r], t);
+      v[c] = div_clamped(b[c], t, clamped);
+    }
+  }
+  float d = 0.0f;
+  for (int r = 0; r < m; ++r) {
+    const float* gc = sp.GC + (int64_t)ia[r] * K;
+    float t = 0.0f;
+    for (int c = 0; c < n; ++c) t = fmaf(__ldg(gc + ib[c]), v[c], t);
+    d = fmaf(u[r], t, d);
+  }
+  *clamped_out |= clamped;
+  return d;
+}
+
+// Slot s of the source: a tile range, an explicit list, or (bucketed lists) units of upt tiles.
+__device__ __forceinline__ bool sparse_slot(const PairSource& ps, int upt, int64_t s, int& i, int& j) {
+  if (ps.units != nullptr && ps.pi == nullptr) {
+    const int64_t q = s / kTileSlots, k = q / upt;
+    const int r = (int)(q % upt);
+    const int64_t t = upt == 1 ? (int64_t)ps.units[k] : 2 * (int64_t)ps.units[k] + r;
+    return tile_slot_pair(t, (int)(s % kTileSlots), ps.n_dist, i, j);
+  }
+  return decode_slot(ps, s, i, j);
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int iters, int upt) {
+  if (*sp.flag != 0u) return;   // a support above kSparseCap: the dense kernel runs this call
+  int64_t n = ps.n_slots;
+  if (ps.units != nullptr && ps.pi == nullptr) n = *ps.n_dev * upt * kTileSlots;
+  else if (ps.n_dev != nullptr && *ps.n_dev < n) n = *ps.n_dev;
+  bool clamped = false;
+  for (int64_t s = (int64_t)blockIdx.x * kThreads + threadIdx.x; s < n; s += (int64_t)gridDim.x * kThreads) {
+    int i = 0, j = 0;
+    const bool valid = sparse_slot(ps, upt, s, i, j);
+    float d = 0.0f;
+    if (valid) {
+      if (sp.cnt[i] <= kFast && sp.cnt[j] <= kFast) d = pair_fast(i, j, K, sp, iters, clamped);
+      else d = pair_slow(i, j, K, sp, iters, &clamped);
+    }
+    write_result(out, s, valid, i, j, d);
+  }
+  if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
+}
+
+}  // namespace sps
+
+size_t sparse_bytes(int64_t n_dist, int K) {
+  const auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  return al((size_t)K * K * 4) * 2 + al((size_t)K * 4) + al((size_t)n_dist * 4) +
+         al((size_t)n_dist * kSparseCap * 2) + al((size_t)n_dist * kSparseCap * 4) + al(4);
+}
+
+SparseBufs carve_sparse(uint8_t* base, int64_t n_dist, int K) {
+  const auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  SparseBufs sp;
+  uint8_t* p = base;
+  sp.G = (float*)p; p += al((size_t)K * K * 4);
+  sp.GC = (float*)p; p += al((size_t)K * K * 4);
+  sp.R = (float*)p; p += al((size_t)K * 4);
+  sp.cnt = (int32_t*)p; p += al((size_t)n_dist * 4);
+  sp.idx = (uint16_t*)p; p += al((size_t)n_dist * kSparseCap * 2);
+  sp.val = (float*)p; p += al((size_t)n_dist * kSparseCap * 4);
+  sp.flag = (uint32_t*)p;
+  return sp;
+}
+
+cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const float* cost, float eps,
+                               const SparseBufs& sp, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(sp.flag, 0, 4, s);
+  if (e != cudaSuccess) return e;
+  sps::gibbs_rows_kernel<<<(K + 7) / 8, 256, 0, s>>>(cost, K, eps, sp);   // a warp per row
+  const int64_t blocks = (n_dist + 7) / 8 < 148 * 16 ? (n_dist + 7) / 8 : 148 * 16;
+  sps::support_kernel<<<(unsigned)blocks, 256, 0, s>>>(H, n_dist, K, sp);   // a warp per distribution
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, int K, const SparseBufs& sp, int iters,
+                                   int upt, int64_t max_slots, int sms, cudaStream_t s) {
+  if (max_slots <= 0) return cudaSuccess;
+  int64_t blocks = (max_slots + sps::kThreads - 1) / sps::kThreads;
+  if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt);
+  return cudaGetLastError();
+}
+
+}  // namespace asot

@@ -114,6 +114,7 @@ sinkhorn_tc3_kernel(int64_t tile_begin, int64_t n_tiles, int64_t n_dist, PairSin
                     const int32_t* __restrict__ pair_i, const int32_t* __restrict__ pair_j, int64_t n_pairs,
                     const float* __restrict__ Hp, const int32_t* __restrict__ units,
                     const int64_t* __restrict__ n_dev) {
+  if (dense_skipped(out)) return;   // the small-support kernel serves this call (R#36)
   using S = Smem<KP>;
   // device-side counts (bucketed pair lists, asot_pairs_bucket.cu): the host passed upper bounds
   if (n_dev != nullptr) {

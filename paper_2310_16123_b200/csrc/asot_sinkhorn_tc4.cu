@@ -100,6 +100,7 @@ sinkhorn_tc4_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                     const float* __restrict__ Hp, int K, const uint8_t* __restrict__ g_img,
                     const uint8_t* __restrict__ gc_img, uint8_t* __restrict__ xbuf, int iters,
                     const int32_t* __restrict__ units, const int64_t* __restrict__ n_dev) {
+  if (dense_skipped(out)) return;   // the small-support kernel serves this call (R#36)
   using S = Smem;
   constexpr int NH = Cfg<KP>::NH, kKC = Cfg<KP>::KC;
   constexpr uint32_t kXBytes = Cfg<KP>::kXBytes;

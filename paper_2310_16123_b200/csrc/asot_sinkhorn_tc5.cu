@@ -88,6 +88,7 @@ sinkhorn_tc5_kernel(int64_t tile_begin, int64_t tile_end, int64_t n_dist, PairSi
                     const float* __restrict__ Hp, int K, const uint8_t* __restrict__ g_hi,
                     const uint8_t* __restrict__ g_lo, const uint8_t* __restrict__ gc_hi,
                     const uint8_t* __restrict__ gc_lo, uint8_t* __restrict__ xbuf, int iters) {
+  if (dense_skipped(out)) return;   // the small-support kernel serves this call (R#36)
   using S = Smem;
   const int32_t* units = EXPLICIT ? nullptr : ps.units;   // bucketed pair lists (tile mode)
   const int64_t* n_dev = ps.n_dev;

@@ -33,6 +33,7 @@ template <int LP>
 __global__ void __launch_bounds__(kThreads, 1)
 sinkhorn_warp_kernel(PairSource ps, PairSink out, const float* __restrict__ H, int K,
                      const float* __restrict__ Gp, const float* __restrict__ GCp, int kp, int iters) {
+  if (dense_skipped(out)) return;   // the small-support kernel serves this call (R#36)
   __shared__ __align__(16) float xs[2][kThreads];   // double-buffered: one __syncwarp per step
   const int r = threadIdx.x % LP;                                  // anchor owned by this lane
   const int64_t slot = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / LP;

@@ -8,7 +8,7 @@ import sys
 import pytest
 
 torch = pytest.importorskip("torch")
-pytestmark = [pytest.mark.gpu,
+pytestmark = [pytest.mark.gpu, pytest.mark.sparse_path,   # bench.py refuses ASOT_SPARSE
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
