@@ -281,6 +281,7 @@ struct SparseBufs {
   float* GC = nullptr;       // [K][K] fp32 K (.) C_s
   float* R = nullptr;        // [K] row sums of K (fp64-summed)
   int32_t* cnt = nullptr;    // [n_dist] support sizes
+  int32_t* perm = nullptr;   // [n_dist] the distributions ordered by support size
   uint16_t* idx = nullptr;   // [n_dist][kSparseCap] bins, increasing
   float* val = nullptr;      // [n_dist][kSparseCap] masses
   uint32_t* flag = nullptr;  // [1] != 0: some support > kSparseCap (the dense kernels run)

@@ -77,38 +77,41 @@ __global__ void support_kernel(const float* __restrict__ H, int64_t n_dist, int 
   }
 }
 
-// x_e = m_e / d_e for 8 anchors, bitwise div_clamped: the range test once for the 8 -- every d in
-// [FLT_MIN, 2^126] exactly when no d is negative and sum_e d_e rcp(d_e) = 8 (+- 2^-19; a d
-// outside the range gives a product of 0, inf or NaN under rcp.approx.ftz) -- then
+// x_e = m_e / d_e for N (even) anchors, bitwise div_clamped: the range test once for the N --
+// every d in [FLT_MIN, 2^126] exactly when no d is negative and sum_e d_e rcp(d_e) = N (+- N 2^-22;
+// a d outside the range gives a product of 0, inf or NaN under rcp.approx.ftz) -- then
 // x = m rcp(d); otherwise the clamped per-element form (S:62 clamp + flag).
-__device__ __forceinline__ void div8(const float* m, const float* d, float* x, bool& clamped) {
-  float r[8];
+template <int N>
+__device__ __forceinline__ void divn(const float* m, const float* d, float* x, bool& clamped) {
+  float r[N];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) r[e] = rcp_ftz(d[e]);
+  for (int e = 0; e < N; ++e) r[e] = rcp_ftz(d[e]);
   float2 t = make_float2(0.0f, 0.0f);
 #pragma unroll
-  for (int e = 0; e < 8; e += 2) t = ffma2(make_float2(d[e], d[e + 1]), make_float2(r[e], r[e + 1]), t);
+  for (int e = 0; e < N; e += 2) t = ffma2(make_float2(d[e], d[e + 1]), make_float2(r[e], r[e + 1]), t);
   uint32_t sg = 0u;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) sg |= __float_as_uint(d[e]);
-  if (fabsf((t.x + t.y) - 8.0f) < 2e-6f && !(sg >> 31)) {
+  for (int e = 0; e < N; ++e) sg |= __float_as_uint(d[e]);
+  if (fabsf((t.x + t.y) - (float)N) < 2e-6f && !(sg >> 31)) {
 #pragma unroll
-    for (int e = 0; e < 8; e += 2) {
+    for (int e = 0; e < N; e += 2) {
       const float2 q = fmul2(make_float2(m[e], m[e + 1]), make_float2(r[e], r[e + 1]));
       x[e] = q.x;
       x[e + 1] = q.y;
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) x[e] = div_clamped(m[e], d[e], clamped);
+    for (int e = 0; e < N; ++e) x[e] = div_clamped(m[e], d[e], clamped);
   }
 }
 
-// The fast form: |S_a|, |S_b| <= 8.  gp[q][c] = (K_{2q,c}, K_{2q+1,c}) of the block, up[q] =
-// (u_{2q}, u_{2q+1}).  u-update: rows in pairs, t = sum_c K_rc v_c (c increasing); v-update:
-// t = (even-r partial + odd-r partial) of sum_r K_rc u_r.
+// The fast form for |S_a|, |S_b| <= S (S in {4, 6, 8}; the warp's largest support picks S).
+// gp[q][c] = (K_{2q,c}, K_{2q+1,c}) of the block, up[q] = (u_{2q}, u_{2q+1}); padding: K = 1,
+// masses 0, so padded scalings are exactly 0.  u-update: rows in pairs, t = sum_c K_rc v_c (c
+// increasing); v-update: t = (even-r partial + odd-r partial) of sum_r K_rc u_r.
+template <int S>
 __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs& sp, int iters, bool& clamped) {
-  constexpr int M = kFast, Q = kFast / 2;
+  constexpr int M = S, Q = S / 2;
   const int m = sp.cnt[i], n = sp.cnt[j];
   const uint16_t* sa = sp.idx + (int64_t)i * kSparseCap;
   const uint16_t* sb = sp.idx + (int64_t)j * kSparseCap;
@@ -149,7 +152,7 @@ __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs
       for (int q = 0; q < Q; ++q) t = ffma2(gp[q][c], up[q], t);
       den[c] = t.x + t.y;
     }
-    div8(b, den, v, clamped);
+    divn<M>(b, den, v, clamped);
   };
   v_update();
   for (int it = 1; it < iters; ++it) {
@@ -162,7 +165,7 @@ __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs
       den[2 * q] = t.x;
       den[2 * q + 1] = t.y;
     }
-    div8(a, den, un, clamped);
+    divn<M>(a, den, un, clamped);
 #pragma unroll
     for (int q = 0; q < Q; ++q) up[q] = make_float2(un[2 * q], un[2 * q + 1]);
     v_update();
@@ -230,22 +233,54 @@ __device__ __forceinline__ bool sparse_slot(const PairSource& ps, int upt, int64
   return decode_slot(ps, s, i, j);
 }
 
+// Whole triangle in support order: slot s enumerates the tiles of the distributions ordered by
+// support size (perm), so a warp's 32 pairs have nearly equal supports; the pair runs in its
+// original orientation (u side = the smaller original index, R#10) and is stored at its slot of
+// the original tiling (tile of (i, j), a4).
+__device__ __forceinline__ bool sorted_slot(const SparseBufs& sp, int64_t n_dist, int64_t s, int& i, int& j,
+                                            int64_t& s_out) {
+  int ip, jp;
+  if (!tile_slot_pair(s / kTileSlots, (int)(s % kTileSlots), n_dist, ip, jp)) return false;
+  i = sp.perm[ip];
+  j = sp.perm[jp];
+  if (i > j) {
+    const int t = i;
+    i = j;
+    j = t;
+  }
+  const int64_t nb = num_blocks(n_dist), bi = i / kBlockDist, bj = j / kBlockDist;
+  const int64_t b = bi * nb - bi * (bi - 1) / 2 + (bj - bi);   // row-major over bi <= bj (a4)
+  const int h = (i % kBlockDist) >> 3;
+  s_out = (2 * b + h) * kTileSlots + (((i & 7) << 4) | (j % kBlockDist));
+  return true;
+}
+
 __global__ void __launch_bounds__(kThreads, 4)
-sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int iters, int upt) {
+sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int iters, int upt, int sorted) {
   if (*sp.flag != 0u) return;   // a support above kSparseCap: the dense kernel runs this call
   int64_t n = ps.n_slots;
   if (ps.units != nullptr && ps.pi == nullptr) n = *ps.n_dev * upt * kTileSlots;
   else if (ps.n_dev != nullptr && *ps.n_dev < n) n = *ps.n_dev;
   bool clamped = false;
-  for (int64_t s = (int64_t)blockIdx.x * kThreads + threadIdx.x; s < n; s += (int64_t)gridDim.x * kThreads) {
+  for (int64_t s0 = (int64_t)blockIdx.x * kThreads; s0 < n; s0 += (int64_t)gridDim.x * kThreads) {
+    const int64_t s = s0 + threadIdx.x;
     int i = 0, j = 0;
-    const bool valid = sparse_slot(ps, upt, s, i, j);
+    int64_t s_out = s;
+    bool valid = false;
+    if (s < n) valid = sorted ? sorted_slot(sp, ps.n_dist, s, i, j, s_out) : sparse_slot(ps, upt, s, i, j);
+    const int m = valid ? sp.cnt[i] : 0, nn = valid ? sp.cnt[j] : 0;
+    const bool slow = m > kFast || nn > kFast;
+    // the warp's largest support picks the register form (warp-uniform)
+    const unsigned smax = __reduce_max_sync(0xffffffffu, slow ? 0u : (unsigned)(m > nn ? m : nn));
     float d = 0.0f;
-    if (valid) {
-      if (sp.cnt[i] <= kFast && sp.cnt[j] <= kFast) d = pair_fast(i, j, K, sp, iters, clamped);
-      else d = pair_slow(i, j, K, sp, iters, &clamped);
+    if (valid && !slow) {
+      if (smax <= 4) d = pair_fast<4>(i, j, K, sp, iters, clamped);
+      else if (smax <= 6) d = pair_fast<6>(i, j, K, sp, iters, clamped);
+      else d = pair_fast<8>(i, j, K, sp, iters, clamped);
+    } else if (valid) {
+      d = pair_slow(i, j, K, sp, iters, &clamped);
     }
-    write_result(out, s, valid, i, j, d);
+    if (s < n && (valid || !sorted)) write_result(out, s_out, valid, i, j, d);
   }
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
 }
@@ -254,7 +289,7 @@ sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int it
 
 size_t sparse_bytes(int64_t n_dist, int K) {
   const auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  return al((size_t)K * K * 4) * 2 + al((size_t)K * 4) + al((size_t)n_dist * 4) +
+  return al((size_t)K * K * 4) * 2 + al((size_t)K * 4) + al((size_t)n_dist * 4) * 2 +
          al((size_t)n_dist * kSparseCap * 2) + al((size_t)n_dist * kSparseCap * 4) + al(4);
 }
 
@@ -266,11 +301,40 @@ SparseBufs carve_sparse(uint8_t* base, int64_t n_dist, int K) {
   sp.GC = (float*)p; p += al((size_t)K * K * 4);
   sp.R = (float*)p; p += al((size_t)K * 4);
   sp.cnt = (int32_t*)p; p += al((size_t)n_dist * 4);
+  sp.perm = (int32_t*)p; p += al((size_t)n_dist * 4);
   sp.idx = (uint16_t*)p; p += al((size_t)n_dist * kSparseCap * 2);
   sp.val = (float*)p; p += al((size_t)n_dist * kSparseCap * 4);
   sp.flag = (uint32_t*)p;
   return sp;
 }
+
+namespace sps {
+// perm: the distributions ordered by support size (counting sort; the order within a size is
+// whatever the atomics give -- every pair's result is independent of where it runs)
+__global__ void support_order_kernel(int64_t n_dist, SparseBufs sp) {
+  __shared__ int hist[kSparseCap + 2];
+  for (int c = threadIdx.x; c < kSparseCap + 2; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n_dist; i += blockDim.x) {
+    const int c = sp.cnt[i] < kSparseCap + 1 ? sp.cnt[i] : kSparseCap + 1;
+    atomicAdd(&hist[c], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int c = 0; c < kSparseCap + 2; ++c) {
+      const int h = hist[c];
+      hist[c] = acc;
+      acc += h;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n_dist; i += blockDim.x) {
+    const int c = sp.cnt[i] < kSparseCap + 1 ? sp.cnt[i] : kSparseCap + 1;
+    sp.perm[atomicAdd(&hist[c], 1)] = (int32_t)i;
+  }
+}
+}  // namespace sps
 
 cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const float* cost, float eps,
                                const SparseBufs& sp, cudaStream_t s) {
@@ -279,6 +343,7 @@ cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const floa
   sps::gibbs_rows_kernel<<<(K + 7) / 8, 256, 0, s>>>(cost, K, eps, sp);   // a warp per row
   const int64_t blocks = (n_dist + 7) / 8 < 148 * 16 ? (n_dist + 7) / 8 : 148 * 16;
   sps::support_kernel<<<(unsigned)blocks, 256, 0, s>>>(H, n_dist, K, sp);   // a warp per distribution
+  sps::support_order_kernel<<<1, 1024, 0, s>>>(n_dist, sp);
   return cudaGetLastError();
 }
 
@@ -287,7 +352,10 @@ cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, in
   if (max_slots <= 0) return cudaSuccess;
   int64_t blocks = (max_slots + sps::kThreads - 1) / sps::kThreads;
   if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-  sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt);
+  // the whole triangle into the matrix only (no packed slots to zero) runs in support order
+  const int sorted = ps.pi == nullptr && ps.units == nullptr && ps.tile_begin == 0 &&
+                     ps.n_slots == num_tiles(ps.n_dist) * kTileSlots && out.vec == nullptr;
+  sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt, sorted);
   return cudaGetLastError();
 }
 
