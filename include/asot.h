@@ -29,7 +29,9 @@
  *     fp64 in point order and rounded to fp32; Sinkhorn runs on tcgen05 tensor cores with fp32
  *     accumulation, either fp32-accurate (ASOT_PREC_FP32: 3xTF32 split operands, target 1e-4)
  *     or with one TF32 pass (ASOT_PREC_TF32, target 2e-3); K < 32 runs in fp32 on CUDA cores
- *     (one lane per anchor) for both requests.
+ *     (one lane per anchor) for both requests; and when every histogram row has at most 16
+ *     non-zero bins (K >= 64) the calls run the exact recurrence on each pair's support block
+ *     in fp32 on CUDA cores for both requests (R#36, asot_sinkhorn_path_kind).
  *
  * Beyond the hot path: soft mappings ASOT-ML / ASOT-DL (NEXT-1), mini-batch
  * k-means anchors (NEXT-2), exact anchor-space OT per pair (NEXT-3), entropic OT on the original
