@@ -179,6 +179,22 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
 size_t asot_distance_matrix_workspace_bytes(int64_t n_dist, int64_t n_points, int32_t n_anchors,
                                             asot_precision prec);
 
+/* Steps a1, a5, a6 on part [part_begin, part_end) of the pair enumeration the call picks (the
+ * multi-GPU unit when results go straight into one matrix): on the small-support path (R#36)
+ * the tiles of the distributions ordered by support size -- homogeneous warps, as the whole
+ * triangle runs there -- otherwise the a4 tiles, exactly as asot_distance_matrix's tile range.
+ * Either way a partition of [0, asot_num_tiles(n_dist)) over calls with the same hist covers
+ * every pair i < j exactly once (each pair keeps its orientation, R#10).  hist [n_dist,
+ * n_anchors] f32 device (e.g. the all-gathered H); dist_out [n_dist, n_dist] f32 device (may be
+ * a peer GPU's memory): D[i,j] = D[j,i] for the part's pairs, the diagonal zeroed when the part
+ * is the whole range.  Workspace: asot_distance_matrix_workspace_bytes(n_dist, 0, n_anchors,
+ * prec). */
+asot_status asot_distance_matrix_partition(const float* hist, int64_t n_dist, int32_t n_anchors,
+                                           const float* cost, float cost_max, float eps, int32_t iters,
+                                           asot_precision prec, int64_t part_begin, int64_t part_end,
+                                           float* dist_out, uint32_t* status, void* workspace,
+                                           size_t workspace_bytes, void* stream);
+
 /* Same pipeline end to end from HOST buffers (the e2e entry point): copies points, offsets,
  * weights, anchors and cost host->device on `stream`, runs the whole triangle, copies the
  * N x N matrix (and status) back to `dist_host` / `status_host`, and synchronises `stream`.

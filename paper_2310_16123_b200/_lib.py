@@ -44,6 +44,8 @@ _SIGS = {
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_map_soft_ml_workspace_bytes": (c_size, [c_i32, c_i32, c_i32]),
     "asot_sinkhorn_path_kind": (c_i32, [c_i32, c_i32, c_i32]),
+    "asot_distance_matrix_partition": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_f32, c_f32, c_i32, c_i32, c_i64,
+                                               c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_map_soft_dl": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "asot_map_soft_dl_workspace_bytes": (c_size, [c_i32, c_i32, c_i64]),

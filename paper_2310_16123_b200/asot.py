@@ -517,6 +517,31 @@ def distance_matrix(points: Optional[torch.Tensor], offsets: Optional[torch.Tens
     return out
 
 
+def distance_matrix_partition(hist: torch.Tensor, cost: torch.Tensor, eps: float, iters: int,
+                              part: Sequence[int], precision: int = TF32,
+                              out: Optional[torch.Tensor] = None, out_ptr: Optional[int] = None,
+                              cost_max: Optional[float] = None, status: Optional[torch.Tensor] = None,
+                              workspace: Optional[Workspace] = None, stream=None):
+    """asot_distance_matrix_partition: part (p0, p1) of the pair enumeration the call picks
+    (support order on the small-support path, the a4 tiles otherwise), results into `out` [N, N]
+    or the raw device address `out_ptr` (e.g. a peer GPU's symmetric-memory matrix); a partition
+    of [0, num_tiles(N)) over calls covers every pair once.  Returns `out`."""
+    _hist_cost(hist, cost)
+    _need_cuda(hist, cost)
+    L = _lib_handle()
+    N, K = int(hist.shape[0]), int(hist.shape[1])
+    if out is None and out_ptr is None:
+        out = torch.empty((N, N), dtype=torch.float32, device=hist.device)
+    cmax = float(cost.max().item()) if cost_max is None else float(cost_max)
+    st = new_status(hist.device) if status is None else status
+    ws = _ws(workspace, hist.device).get(L.asot_distance_matrix_workspace_bytes(N, 0, K, int(precision)))
+    _check(L.asot_distance_matrix_partition(
+        _ptr(hist), N, K, _ptr(cost), cmax, float(eps), int(iters), int(precision), int(part[0]),
+        int(part[1]), _ptr(out) if out is not None else out_ptr, _ptr(st), _ptr(ws), ws.numel(),
+        _stream(stream)))
+    return out
+
+
 def host_workspace_bytes(n_dist: int, n_points: int, dim: int, n_anchors: int,
                          precision: int = TF32) -> int:
     return int(_lib_handle().asot_distance_matrix_host_workspace_bytes(

@@ -234,7 +234,7 @@ struct ProfScope {
 asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink, const float* H,
                          const float* cost, float eps, int32_t K, int32_t iters,
                          const GibbsBufs& gb, int64_t tile_begin, int64_t tile_end,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool ordered = false) {
   const int kind = gb.kind;
   {
   Nvtx range("asot a1 gibbs_prep");
@@ -268,7 +268,7 @@ asot_status run_sinkhorn(const asot::PairSource& ps, const asot::PairSink& sink,
     const bool units = ps.units != nullptr && ps.pi == nullptr;
     const int upt = units ? bucket_upt(kind) : 1;
     const int64_t max_slots = units ? (tile_end - tile_begin) * asot::kTileSlots : ps.n_slots;
-    ASOT_LAUNCH(asot::launch_sinkhorn_sparse(ps, sink, K, gb.sp, iters, upt, max_slots, device_sms(), s));
+    ASOT_LAUNCH(asot::launch_sinkhorn_sparse(ps, sink, K, gb.sp, iters, upt, max_slots, device_sms(), s, ordered));
     sinkd.dense_if = gb.sp.flag;
   }
   const asot::PairSink& sink_dense = sinkd;
@@ -826,6 +826,34 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
   if (dist_out && tile_begin == 0 && tile_end == n_tiles) {
     Nvtx range("asot a6 zero_diag");
     ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, s));
+  }
+  return ASOT_OK;
+}
+
+asot_status asot_distance_matrix_partition(const float* hist, int64_t n_dist, int32_t n_anchors,
+                                           const float* cost, float cost_max, float eps, int32_t iters,
+                                           asot_precision prec, int64_t part_begin, int64_t part_end,
+                                           float* dist_out, uint32_t* status, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  ASOT_CHECK_ARG(hist && cost && dist_out && status, "null pointer argument");
+  asot_status st = check_common(n_dist, n_anchors, eps, iters, cost_max);
+  if (st != ASOT_OK) return st;
+  const int64_t n_tiles = asot::num_tiles(n_dist);
+  ASOT_CHECK_ARG(0 <= part_begin && part_begin <= part_end && part_end <= n_tiles,
+                 "part range outside [0, asot_num_tiles(n_dist)]");
+  Carver cv{(char*)workspace, workspace_bytes};
+  cv.take((size_t)n_dist * n_anchors * 4);   // (the asot_distance_matrix layout)
+  GibbsBufs gb = carve_gibbs(cv, n_anchors, tc_kind(n_anchors, prec), n_dist);
+  if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
+  asot::PairSource ps{nullptr, nullptr, (part_end - part_begin) * asot::kTileSlots, part_begin, n_dist};
+  asot::PairSink sink{nullptr, dist_out, n_dist, status, 0};
+  st = run_sinkhorn(ps, sink, hist, cost, eps, n_anchors, iters, gb, part_begin, part_end,
+                    (cudaStream_t)stream, /*ordered=*/true);
+  if (st != ASOT_OK) return st;
+  if (part_begin == 0 && part_end == n_tiles) {
+    Nvtx range("asot a6 zero_diag");
+    ASOT_LAUNCH(asot::launch_zero_diag(dist_out, n_dist, (cudaStream_t)stream));
   }
   return ASOT_OK;
 }

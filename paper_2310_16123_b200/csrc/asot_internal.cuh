@@ -296,8 +296,9 @@ cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const floa
                                const SparseBufs& sp, cudaStream_t s);
 // ps: a tile range, an explicit list (n_dev optional) or units of upt tiles (bucketed lists);
 // max_slots: the host-side upper bound of the slots
+// ordered: a tile range of the support-ordered enumeration (matrix output only)
 cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, int K, const SparseBufs& sp, int iters,
-                                   int upt, int64_t max_slots, int sms, cudaStream_t s);
+                                   int upt, int64_t max_slots, int sms, cudaStream_t s, bool ordered = false);
 cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, float* GC,
                               uint32_t* g_img, uint32_t* gc_img, int kpad, cudaStream_t s);
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,

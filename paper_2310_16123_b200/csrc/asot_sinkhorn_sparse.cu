@@ -237,10 +237,10 @@ __device__ __forceinline__ bool sparse_slot(const PairSource& ps, int upt, int64
 // support size (perm), so a warp's 32 pairs have nearly equal supports; the pair runs in its
 // original orientation (u side = the smaller original index, R#10) and is stored at its slot of
 // the original tiling (tile of (i, j), a4).
-__device__ __forceinline__ bool sorted_slot(const SparseBufs& sp, int64_t n_dist, int64_t s, int& i, int& j,
-                                            int64_t& s_out) {
+__device__ __forceinline__ bool sorted_slot(const SparseBufs& sp, int64_t n_dist, int64_t tile_begin, int64_t s,
+                                            int& i, int& j, int64_t& s_out) {
   int ip, jp;
-  if (!tile_slot_pair(s / kTileSlots, (int)(s % kTileSlots), n_dist, ip, jp)) return false;
+  if (!tile_slot_pair(tile_begin + s / kTileSlots, (int)(s % kTileSlots), n_dist, ip, jp)) return false;
   i = sp.perm[ip];
   j = sp.perm[jp];
   if (i > j) {
@@ -267,7 +267,7 @@ sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int it
     int i = 0, j = 0;
     int64_t s_out = s;
     bool valid = false;
-    if (s < n) valid = sorted ? sorted_slot(sp, ps.n_dist, s, i, j, s_out) : sparse_slot(ps, upt, s, i, j);
+    if (s < n) valid = sorted ? sorted_slot(sp, ps.n_dist, ps.tile_begin, s, i, j, s_out) : sparse_slot(ps, upt, s, i, j);
     const int m = valid ? sp.cnt[i] : 0, nn = valid ? sp.cnt[j] : 0;
     const bool slow = m > kFast || nn > kFast;
     // the warp's largest support picks the register form (warp-uniform)
@@ -348,13 +348,14 @@ cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const floa
 }
 
 cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, int K, const SparseBufs& sp, int iters,
-                                   int upt, int64_t max_slots, int sms, cudaStream_t s) {
+                                   int upt, int64_t max_slots, int sms, cudaStream_t s, bool ordered) {
   if (max_slots <= 0) return cudaSuccess;
   int64_t blocks = (max_slots + sps::kThreads - 1) / sps::kThreads;
   if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-  // the whole triangle into the matrix only (no packed slots to zero) runs in support order
-  const int sorted = ps.pi == nullptr && ps.units == nullptr && ps.tile_begin == 0 &&
-                     ps.n_slots == num_tiles(ps.n_dist) * kTileSlots && out.vec == nullptr;
+  // support order: the whole triangle into the matrix only (no packed slots to zero), or a tile
+  // range of the support-ordered enumeration (asot_distance_matrix_partition)
+  const int sorted = ps.pi == nullptr && ps.units == nullptr && out.vec == nullptr &&
+                     (ordered || (ps.tile_begin == 0 && ps.n_slots == num_tiles(ps.n_dist) * kTileSlots));
   sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt, sorted);
   return cudaGetLastError();
 }

@@ -213,8 +213,11 @@ def cuda_steps(points: torch.Tensor, offsets: torch.Tensor, offsets_host: np.nda
                                peers, lo, offsets_host=sub_off_h, status=status)
 
     def tiles_into(H: torch.Tensor, t0: int, t1: int, d_addr: int) -> None:
-        A.distance_matrix(None, None, None, None, cost, eps, iters, precision=precision, hist=H,
-                          tile_range=(t0, t1), want_matrix=False, out_ptr=d_addr,
-                          cost_max=cost_max, status=status, workspace=workspace)
+        # part [t0, t1) of the enumeration the library picks (support order on the small-support
+        # path): the ranks' parts still cover every pair once, and each rank's warps stay as
+        # homogeneous as the single-GPU whole triangle
+        A.distance_matrix_partition(H, cost, eps, iters, (t0, t1), precision=precision,
+                                    out_ptr=d_addr, cost_max=cost_max, status=status,
+                                    workspace=workspace)
 
     return DistSteps(map_range, tiles, unpack, zero_diag, tiles_into, map_range_bcast)

@@ -231,3 +231,24 @@ def test_sparse_denominator_clamp_is_flagged(asot):
                            dev(np.array([1], np.int32)), precision=asot.FP32, cost_max=1.0, status=st2)
     torch.cuda.synchronize()
     assert int(st2.item()) == asot.asot.FLAG_DENOM_CLAMPED, f"flags {int(st2.item()):#x}"
+
+
+@pytest.mark.parametrize("cfg,n", [("c3", 80), ("c2", 60)])
+def test_partition_union_bitwise(asot, cfg, n):
+    """asot_distance_matrix_partition (the multi-GPU unit of distributed.py's NVLink path): parts
+    of [0, num_tiles) with odd cuts, run as separate calls into one matrix, reproduce the whole
+    matrix bitwise -- in support order on the small-support path (c3) and in the a4 tiling on the
+    dense one (c2)."""
+    inp, _, H = oracle_full(cfg, n)
+    D, _ = run_matrix(asot, inp, asot.TF32)
+    Hd = dev(H.astype(np.float32))
+    n_tiles = asot.num_tiles(inp.n_dist)
+    cuts = [0, 3, 17, 18, n_tiles - 5, n_tiles]
+    R = torch.zeros_like(D)
+    st = asot.asot.new_status()
+    for p0, p1 in zip(cuts[:-1], cuts[1:]):
+        asot.distance_matrix_partition(Hd, dev(inp.cost), float(inp.eps), inp.iters, (p0, p1),
+                                       precision=asot.TF32, out=R, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    assert torch.equal(R, D)
