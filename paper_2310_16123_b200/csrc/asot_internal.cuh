@@ -285,6 +285,7 @@ struct SparseBufs {
   uint16_t* idx = nullptr;   // [n_dist][kSparseCap] bins, increasing
   float* val = nullptr;      // [n_dist][kSparseCap] masses
   uint32_t* flag = nullptr;  // [1] != 0: some support > kSparseCap (the dense kernels run)
+  int32_t* bounds = nullptr; // [4] distributions with support <= 4, 6, 8, 16 (prefixes of perm)
 };
 size_t sparse_bytes(int64_t n_dist, int K);
 SparseBufs carve_sparse(uint8_t* base, int64_t n_dist, int K);

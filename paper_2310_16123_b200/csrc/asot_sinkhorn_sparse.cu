@@ -222,6 +222,65 @@ __device__ __noinline__ float pair_slow(int i, int j, int K, const SparseBufs& s
   return d;
 }
 
+// Supports of 9-16 bins in the support-ordered traversal: a half-warp per pair, lane r (= l % 16)
+// owns row r of the 16 x 16 block (in registers) and column r's mass.  v-update: the products
+// K_rc u_r of the 16 columns are reduced over the 16 rows by a butterfly (xor 8, 4, 2, 1; lane c
+// ends with column c's sum); u-update: lane r sums K_rc v_c with v_c broadcast from lane c.
+// Padding: K = 1, masses 0 (padded scalings exactly 0).  Returns the pair's cost on every lane.
+__device__ __forceinline__ float pair_half16(int i, int j, int K, const SparseBufs& sp, int iters, bool valid,
+                                             bool& clamped) {
+  const int l = threadIdx.x & 15;
+  const unsigned hm = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;   // this half-warp
+  const int m = valid ? sp.cnt[i] : 0, n = valid ? sp.cnt[j] : 0;
+  const int ia = l < m ? (int)sp.idx[(int64_t)i * kSparseCap + l] : 0;
+  const int ib = l < n ? (int)sp.idx[(int64_t)j * kSparseCap + l] : 0;
+  const float a = l < m ? sp.val[(int64_t)i * kSparseCap + l] : 0.0f;
+  const float b = l < n ? sp.val[(int64_t)j * kSparseCap + l] : 0.0f;
+  float g[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int ibc = __shfl_sync(hm, ib, c, 16);
+    g[c] = (l < m && c < n) ? __ldg(sp.G + (int64_t)ia * K + ibc) : 1.0f;
+  }
+  float u = l < m ? div_clamped(a, __ldg(sp.R + ia), clamped) : 0.0f;
+  float v = 0.0f;
+  for (int it = 0; it < iters; ++it) {
+    if (it > 0) {
+      float t = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) t = fmaf(g[c], __shfl_sync(hm, v, c, 16), t);
+      u = div_clamped(a, t, clamped);
+    }
+    float p[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) p[c] = g[c] * u;
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {   // 16 -> 8 -> 4 -> 2 -> 1 values per lane
+      const bool up = (l & w) != 0;
+#pragma unroll
+      for (int e = 0; e < w; ++e) {
+        const float send = up ? p[e] : p[e + w];
+        const float keep = up ? p[e + w] : p[e];
+        p[e] = keep + __shfl_xor_sync(hm, send, w, 16);
+      }
+    }
+    v = div_clamped(b, p[0], clamped);   // lane l holds column l's sum
+  }
+  // a6: sum_r u_r sum_c (K (.) C_s)_rc v_c
+  float t = 0.0f;
+  const float* gc = sp.GC + (int64_t)ia * K;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int ibc = __shfl_sync(hm, ib, c, 16);
+    const float vc = __shfl_sync(hm, v, c, 16);
+    if (l < m && c < n) t = fmaf(__ldg(gc + ibc), vc, t);
+  }
+  float d = l < m ? u * t : 0.0f;
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) d += __shfl_xor_sync(hm, d, o, 16);
+  return d;
+}
+
 // Slot s of the source: a tile range, an explicit list, or (bucketed lists) units of upt tiles.
 __device__ __forceinline__ bool sparse_slot(const PairSource& ps, int upt, int64_t s, int& i, int& j) {
   if (ps.units != nullptr && ps.pi == nullptr) {
@@ -285,6 +344,67 @@ sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int it
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
 }
 
+// The whole triangle (or a part of it) in support order, one kernel per support class.  Pairs of
+// the distributions in support order, enumerated column-major (k -> j' = the largest with
+// j'(j'-1)/2 <= k, i' = k - j'(j'-1)/2, i' < j'): since supp(perm[i']) <= supp(perm[j']), the
+// column alone fixes the class, so each class is one contiguous range of k and its kernel runs
+// one register form (S = 4, 6, 8; 0 = the 9-16 form) at the occupancy that form allows; a warp's
+// 32 consecutive k share (mostly) one column.  Each pair keeps its orientation (u side = the
+// smaller original index, R#10) and lands at (i, j) of the matrix; [k_lo, k_hi) bounds the part.
+template <int S>
+__global__ void __launch_bounds__(kThreads, S == 4 ? 8 : S == 6 ? 5 : 4)
+sinkhorn_sparse_class_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp, int iters, int64_t k_lo,
+                             int64_t k_hi) {
+  if (*sp.flag != 0u) return;
+  constexpr int cls = S == 4 ? 0 : S == 6 ? 1 : S == 8 ? 2 : 3;
+  const int64_t c0 = cls == 0 ? 0 : sp.bounds[cls - 1], c1 = sp.bounds[cls];
+  int64_t a = c0 * (c0 - 1) / 2, b = c1 * (c1 - 1) / 2;
+  if (a < k_lo) a = k_lo;
+  if (b > k_hi) b = k_hi;
+  bool clamped = false;
+  if constexpr (S == 0) {
+    // a half-warp per pair (warp-synchronous: both halves loop the same number of times)
+    const int64_t hw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 4, nhw = ((int64_t)gridDim.x * kThreads) >> 4;
+    for (int64_t k0 = a + (hw & ~(int64_t)1); k0 < b; k0 += nhw) {
+      const int64_t k = k0 + (hw & 1);
+      const bool valid = k < b;
+      int i = 0, j = 0;
+      if (valid) {
+        int64_t jp = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)k)) * 0.5);
+        while (jp * (jp - 1) / 2 > k) --jp;
+        while ((jp + 1) * jp / 2 <= k) ++jp;
+        const int64_t ip = k - jp * (jp - 1) / 2;
+        i = sp.perm[ip];
+        j = sp.perm[jp];
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+      }
+      const float d = pair_half16(i, j, K, sp, iters, valid, clamped);
+      if (valid && (threadIdx.x & 15) == 0) write_result(out, 0, true, i, j, d);
+    }
+    if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
+    return;
+  }
+  for (int64_t k = a + (int64_t)blockIdx.x * kThreads + threadIdx.x; k < b; k += (int64_t)gridDim.x * kThreads) {
+    int64_t jp = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)k)) * 0.5);
+    while (jp * (jp - 1) / 2 > k) --jp;
+    while ((jp + 1) * jp / 2 <= k) ++jp;
+    const int64_t ip = k - jp * (jp - 1) / 2;
+    int i = sp.perm[ip], j = sp.perm[jp];
+    if (i > j) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    const float d = pair_fast<S == 0 ? 4 : S>(i, j, K, sp, iters, clamped);
+    write_result(out, 0, true, i, j, d);
+  }
+  if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
+}
+
 }  // namespace sps
 
 size_t sparse_bytes(int64_t n_dist, int K) {
@@ -305,6 +425,7 @@ SparseBufs carve_sparse(uint8_t* base, int64_t n_dist, int K) {
   sp.idx = (uint16_t*)p; p += al((size_t)n_dist * kSparseCap * 2);
   sp.val = (float*)p; p += al((size_t)n_dist * kSparseCap * 4);
   sp.flag = (uint32_t*)p;
+  sp.bounds = (int32_t*)(p + 16);
   return sp;
 }
 
@@ -327,6 +448,12 @@ __global__ void support_order_kernel(int64_t n_dist, SparseBufs sp) {
       hist[c] = acc;
       acc += h;
     }
+    // the support classes of the class kernels: perm[0, b0) <= 4 bins, [b0, b1) 5-6, [b1, b2)
+    // 7-8, [b2, b3) 9-16
+    sp.bounds[0] = hist[5];
+    sp.bounds[1] = hist[7];
+    sp.bounds[2] = hist[9];
+    sp.bounds[3] = hist[kSparseCap + 1];
   }
   __syncthreads();
   for (int64_t i = threadIdx.x; i < n_dist; i += blockDim.x) {
@@ -352,11 +479,23 @@ cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, in
   if (max_slots <= 0) return cudaSuccess;
   int64_t blocks = (max_slots + sps::kThreads - 1) / sps::kThreads;
   if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-  // support order: the whole triangle into the matrix only (no packed slots to zero), or a tile
-  // range of the support-ordered enumeration (asot_distance_matrix_partition)
-  const int sorted = ps.pi == nullptr && ps.units == nullptr && out.vec == nullptr &&
-                     (ordered || (ps.tile_begin == 0 && ps.n_slots == num_tiles(ps.n_dist) * kTileSlots));
-  sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt, sorted);
+  // support order: the whole triangle into the matrix only (no packed slots to zero), or a part
+  // of the support-ordered enumeration (asot_distance_matrix_partition): the class kernels over
+  // pair range [k_lo, k_hi) = the part's share of the N(N-1)/2 pairs
+  const int64_t T = num_tiles(ps.n_dist);
+  const bool sorted = ps.pi == nullptr && ps.units == nullptr && out.vec == nullptr &&
+                      (ordered || (ps.tile_begin == 0 && ps.n_slots == T * kTileSlots));
+  if (sorted) {
+    const int64_t P = ps.n_dist * (ps.n_dist - 1) / 2;
+    const int64_t p0 = ps.tile_begin, p1 = ps.tile_begin + ps.n_slots / kTileSlots;
+    const int64_t k_lo = T > 0 ? p0 * P / T : 0, k_hi = T > 0 ? p1 * P / T : 0;
+    sps::sinkhorn_sparse_class_kernel<4><<<sms * 8, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_class_kernel<6><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_class_kernel<8><<<sms * 4, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_class_kernel<0><<<sms * 2, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    return cudaGetLastError();
+  }
+  sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt, 0);
   return cudaGetLastError();
 }
 
