@@ -406,7 +406,8 @@ asot_precision asot_effective_precision(int32_t n_anchors, asot_precision reques
 static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,
                             const float* weights, int64_t n_dist, int32_t dim, const float* anchors,
                             int32_t n_anchors, int32_t* assign_out, float* hist_out, uint32_t* status,
-                            void* stream, float* const* peers, int32_t n_peers, int64_t row_base);
+                            void* stream, float* const* peers, int32_t n_peers, int64_t row_base,
+                            uint8_t* tc_ws);
 
 asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
                                 const int64_t* offsets_host, const float* weights,
@@ -414,7 +415,7 @@ asot_status asot_map_to_anchors(const float* points, const int64_t* offsets,
                                 int32_t n_anchors, int32_t* assign_out, float* hist_out,
                                 uint32_t* status, void* stream) {
   return map_impl(points, offsets, offsets_host, weights, n_dist, dim, anchors, n_anchors, assign_out,
-                  hist_out, status, stream, nullptr, 0, 0);
+                  hist_out, status, stream, nullptr, 0, 0, nullptr);
 }
 
 asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offsets,
@@ -426,13 +427,14 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
   ASOT_CHECK_ARG(n_peers >= 0 && (n_peers == 0 || hist_peers), "hist_peers required when n_peers > 0");
   ASOT_CHECK_ARG(row_base >= 0, "row_base must be >= 0");
   return map_impl(points, offsets, offsets_host, weights, n_dist, dim, anchors, n_anchors, assign_out,
-                  hist_out, status, stream, hist_peers, n_peers, row_base);
+                  hist_out, status, stream, hist_peers, n_peers, row_base, nullptr);
 }
 
 static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,
                             const float* weights, int64_t n_dist, int32_t dim, const float* anchors,
                             int32_t n_anchors, int32_t* assign_out, float* hist_out, uint32_t* status,
-                            void* stream, float* const* peers, int32_t n_peers, int64_t row_base) {
+                            void* stream, float* const* peers, int32_t n_peers, int64_t row_base,
+                            uint8_t* tc_ws) {
   g_launches = 0;
   ASOT_CHECK_ARG(points && offsets && offsets_host && weights && anchors && assign_out &&
                      hist_out && status,
@@ -450,7 +452,14 @@ static asot_status map_impl(const float* points, const int64_t* offsets, const i
   if (T > 0) {
     Nvtx range("asot a2 map_assign");
     ProfScope prof(ASOT_PROF_MAP, s);
-    ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
+    // with a workspace (asot_distance_matrix): the products on the tensor cores and the exact
+    // kernel on the points they cannot decide (R#37); else the exact kernel on every point
+    if (tc_ws != nullptr && asot::map_tc_supported(dim, n_anchors) && ((uintptr_t)points & 15u) == 0) {
+      ASOT_LAUNCH(asot::launch_map_tc(points, T, dim, anchors, n_anchors, assign_out, status, tc_ws,
+                                      device_sms(), s));
+    } else {
+      ASOT_LAUNCH(asot::launch_map_assign(points, T, dim, anchors, n_anchors, assign_out, status, s));
+    }
   }
   Nvtx range("asot a3 histograms");
   ASOT_LAUNCH(asot::launch_histograms(assign_out, weights, offsets, n_dist, n_anchors, hist_out, status, s,
@@ -773,6 +782,7 @@ size_t asot_distance_matrix_workspace_bytes(int64_t n_dist, int64_t n_points, in
   cv.take((size_t)n_dist * n_anchors * 4);   // H
   cv.take((size_t)n_points * 4);             // assign scratch
   carve_gibbs(cv, n_anchors, tc_kind(n_anchors, prec), n_dist);
+  cv.take(asot::map_tc_workspace_bytes(n_points, n_anchors));   // tensor-core mapping (R#37)
   return cv.used;
 }
 
@@ -806,6 +816,7 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
   float* H = (float*)cv.take((size_t)n_dist * n_anchors * 4);
   int32_t* assign = (int32_t*)cv.take((size_t)T * 4);
   GibbsBufs gb = carve_gibbs(cv, n_anchors, tc_kind(n_anchors, prec), n_dist);
+  uint8_t* map_ws = (uint8_t*)cv.take(asot::map_tc_workspace_bytes(T, n_anchors));
   if (!workspace || cv.overflow) return fail(ASOT_ERR_WORKSPACE, "workspace too small");
 
   const float* Huse = hist_in;
@@ -813,8 +824,8 @@ asot_status asot_distance_matrix(const float* points, const int64_t* offsets,
     int32_t* asg = assign_out ? assign_out : assign;
     float* Hw = hist_out ? hist_out : H;
     const int32_t launches_before = g_launches;
-    st = asot_map_to_anchors(points, offsets, offsets_host, weights, n_dist, dim, anchors,
-                             n_anchors, asg, Hw, status, stream);
+    st = map_impl(points, offsets, offsets_host, weights, n_dist, dim, anchors, n_anchors, asg, Hw,
+                  status, stream, nullptr, 0, 0, map_ws);
     g_launches += launches_before;
     if (st != ASOT_OK) return st;
     Huse = Hw;

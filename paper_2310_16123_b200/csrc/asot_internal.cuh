@@ -305,6 +305,15 @@ cudaError_t launch_gibbs_prep(const float* cost, int K, float eps, float* G, flo
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
                               int32_t* assign, uint32_t* status, cudaStream_t s,
                               const int64_t* gather = nullptr);
+// the points list[0 .. *n_dev) (T = a host bound of *n_dev): assign[list[k]] (asot_map_tc.cu)
+cudaError_t launch_map_assign_list(const float* points, int64_t T, int dim, const float* anchors, int K,
+                                   int32_t* assign, uint32_t* status, cudaStream_t s, const int64_t* list,
+                                   const int64_t* n_dev);
+// a2 with the products on tcgen05 (BF16x3) and the exact kernel on the ambiguous points (R#37)
+bool map_tc_supported(int dim, int K);
+size_t map_tc_workspace_bytes(int64_t T, int K);
+cudaError_t launch_map_tc(const float* points, int64_t T, int dim, const float* anchors, int K, int32_t* assign,
+                          uint32_t* status, uint8_t* ws, int sms, cudaStream_t s);
 cudaError_t launch_histograms(const int32_t* assign, const float* weights, const int64_t* offsets,
                               int64_t n_dist, int K, float* H, uint32_t* status, cudaStream_t s,
                               float* const* peers = nullptr, int n_peers = 0, int64_t row_base = 0);

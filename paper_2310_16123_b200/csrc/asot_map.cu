@@ -100,7 +100,11 @@ template <int DP, int LPP>
 __global__ void __launch_bounds__(kMapThreads, 2)
 map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ gather, int64_t T,
                   int dim, const float* __restrict__ anchors, int K, int chunk,
-                  int32_t* __restrict__ assign, uint32_t* __restrict__ status) {
+                  int32_t* __restrict__ assign, uint32_t* __restrict__ status,
+                  const int64_t* __restrict__ T_dev, int scatter) {
+  // T_dev: the list length on the device (T is then its host-side bound); scatter: results go to
+  // assign[gather[k]] (the tensor-core mapping's ambiguous points) instead of assign[k]
+  if (T_dev != nullptr) T = *T_dev < T ? *T_dev : T;
   extern __shared__ float4 map_smem4[];
   constexpr int RS = DP + 4;                        // row stride (floats)
   float* Xs2 = reinterpret_cast<float*>(map_smem4); // 2 x [64][RS] points: current and next tile
@@ -303,7 +307,7 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
         }
         if (refine) b.idx = bi;
       }
-      if (valid && tx == 0) assign[p0 + pl] = b.idx;
+      if (valid && tx == 0) assign[scatter ? gather[p0 + pl] : p0 + pl] = b.idx;
     }
   }  // tiles
 }
@@ -311,7 +315,7 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
 template <int DP, int LPP>
 static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int64_t T, int dim,
                                  const float* anchors, int K, int32_t* assign, uint32_t* status,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const int64_t* T_dev = nullptr, int scatter = 0) {
   constexpr int kMapAnchorGroup = 4 * LPP;
   const int rs_bytes = (DP + 4) * 4;
   // anchor chunk: whole 64-anchor groups such that the CTA (with its one or two point tiles)
@@ -332,25 +336,37 @@ static cudaError_t launch_map_dp(const float* points, const int64_t* gather, int
   if (per_sm < 1) per_sm = 1;
   if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;   // persistent grid
   map_assign_kernel<DP, LPP><<<(unsigned)blocks, kMapThreads, smem, s>>>(points, gather, T, dim, anchors,
-                                                                   K, chunk, assign, status);
+                                                                        K, chunk, assign, status, T_dev, scatter);
   return cudaGetLastError();
+}
+
+static cudaError_t map_dispatch(const float* points, int64_t T, int dim, const float* anchors, int K,
+                                int32_t* assign, uint32_t* status, cudaStream_t s, const int64_t* gather,
+                                const int64_t* T_dev, int scatter) {
+  // K >= 128: 32 lanes share a thread's points (one broadcast wavefront per point load)
+  if (K >= 128 && dim > 8) {
+    if (dim <= 16) return launch_map_dp<16, 32>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+    if (dim <= 32) return launch_map_dp<32, 32>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+    if (dim <= 64) return launch_map_dp<64, 32>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+    return launch_map_dp<128, 32>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+  }
+  if (dim <= 8) return launch_map_dp<8, 16>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+  if (dim <= 16) return launch_map_dp<16, 16>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+  if (dim <= 32) return launch_map_dp<32, 16>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+  if (dim <= 64) return launch_map_dp<64, 16>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
+  return launch_map_dp<128, 16>(points, gather, T, dim, anchors, K, assign, status, s, T_dev, scatter);
 }
 
 cudaError_t launch_map_assign(const float* points, int64_t T, int dim, const float* anchors, int K,
                               int32_t* assign, uint32_t* status, cudaStream_t s,
                               const int64_t* gather) {
-  // K >= 128: 32 lanes share a thread's points (one broadcast wavefront per point load)
-  if (K >= 128 && dim > 8) {
-    if (dim <= 16) return launch_map_dp<16, 32>(points, gather, T, dim, anchors, K, assign, status, s);
-    if (dim <= 32) return launch_map_dp<32, 32>(points, gather, T, dim, anchors, K, assign, status, s);
-    if (dim <= 64) return launch_map_dp<64, 32>(points, gather, T, dim, anchors, K, assign, status, s);
-    return launch_map_dp<128, 32>(points, gather, T, dim, anchors, K, assign, status, s);
-  }
-  if (dim <= 8) return launch_map_dp<8, 16>(points, gather, T, dim, anchors, K, assign, status, s);
-  if (dim <= 16) return launch_map_dp<16, 16>(points, gather, T, dim, anchors, K, assign, status, s);
-  if (dim <= 32) return launch_map_dp<32, 16>(points, gather, T, dim, anchors, K, assign, status, s);
-  if (dim <= 64) return launch_map_dp<64, 16>(points, gather, T, dim, anchors, K, assign, status, s);
-  return launch_map_dp<128, 16>(points, gather, T, dim, anchors, K, assign, status, s);
+  return map_dispatch(points, T, dim, anchors, K, assign, status, s, gather, nullptr, 0);
+}
+
+cudaError_t launch_map_assign_list(const float* points, int64_t T, int dim, const float* anchors, int K,
+                                   int32_t* assign, uint32_t* status, cudaStream_t s, const int64_t* list,
+                                   const int64_t* n_dev) {
+  return map_dispatch(points, T, dim, anchors, K, assign, status, s, list, n_dev, 1);
 }
 
 // ------------------------------------------------------------------------------ a3: histograms

@@ -45,12 +45,29 @@ def oracle_full(cfg, n):
     return _oracle_cache[key]
 
 
+def map_via(asot, path, pts, offs, w, anc, offsets_host):
+    """The mapping through asot_map_to_anchors ("exact": the CUDA-core kernel on every point) or
+    through asot_distance_matrix with an empty tile range ("tc": with a workspace, the tensor-core
+    products and the exact kernel on the points they cannot decide, R#37)."""
+    if path == "exact":
+        return asot.map_to_anchors(pts, offs, w, anc, offsets_host=offsets_host)
+    N, K = offsets_host.shape[0] - 1, anc.shape[0]
+    assign = torch.empty(max(int(offsets_host[-1]), 1), dtype=torch.int32, device=pts.device)
+    H = torch.empty((N, K), dtype=torch.float32, device=pts.device)
+    st = asot.asot.new_status()
+    C = torch.zeros((K, K), dtype=torch.float32, device=pts.device)
+    asot.distance_matrix(pts, offs, w, anc, C, 0.05, 1, tile_range=(0, 0), assign_out=assign,
+                         hist_out=H, offsets_host=offsets_host, cost_max=0.0, status=st)
+    return assign, H, st
+
+
 # ------------------------------------------------------------------ mapping + histograms
+@pytest.mark.parametrize("path", ["exact", "tc"])
 @pytest.mark.parametrize("cfg,n", [("c1", 64), ("c2", 1000), ("c3", 200), ("c4", 8000), ("c5", 40)])
-def test_mapping_bit_exact(asot, cfg, n):
+def test_mapping_bit_exact(asot, cfg, n, path):
     inp = make_inputs(cfg, n_dist=n)
     pts, offs, w, anc, _ = dev_inputs(inp)
-    assign, H, st = asot.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+    assign, H, st = map_via(asot, path, pts, offs, w, anc, inp.offsets)
     torch.cuda.synchronize()
     asot.check_status(st)
     a_o = O.map_assign(inp.points, inp.anchors)
@@ -60,7 +77,8 @@ def test_mapping_bit_exact(asot, cfg, n):
     np.testing.assert_array_equal(H.cpu().numpy(), H_o)
 
 
-def test_mapping_adversarial_ties(asot):
+@pytest.mark.parametrize("path", ["exact", "tc"])
+def test_mapping_adversarial_ties(asot, path):
     rng = np.random.default_rng(5)
     d, K = 32, 64
     W = rng.integers(-3, 4, size=(K, d)).astype(np.float32)
@@ -79,15 +97,16 @@ def test_mapping_adversarial_ties(asot):
     off = np.array([0, X.shape[0]], np.int64)
     w = np.full(X.shape[0], np.float32(1.0 / X.shape[0]))
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    assign, H, st = asot.map_to_anchors(t(X), t(off), t(w), t(W), offsets_host=off)
+    assign, H, st = map_via(asot, path, t(X), t(off), t(w), t(W), off)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(assign.cpu().numpy(), O.map_assign(X, W))
     assert assign.cpu().numpy()[-2] == 3
 
 
+@pytest.mark.parametrize("path", ["exact", "tc"])
 @pytest.mark.parametrize("case", ["offset", "tiny", "huge", "mixed"])
 @pytest.mark.parametrize("d,K", [(16, 64), (64, 256), (128, 1024)])
-def test_mapping_extreme_magnitudes(asot, case, d, K):
+def test_mapping_extreme_magnitudes(asot, case, d, K, path):
     """The kernel decides in fp32 with the rigorous near-tie bound of R#8 and falls back to the
     fp64 op sequence: a large common offset (|x| >> the distances), coordinates near 1e-20
     (subnormal squares: the absolute slack), near 1e19 (fp32 overflow of the distances: every
@@ -111,7 +130,7 @@ def test_mapping_extreme_magnitudes(asot, case, d, K):
     off = np.array([0, X.shape[0]], np.int64)
     w = np.full(X.shape[0], np.float32(1.0 / X.shape[0]))
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    assign, H, st = asot.map_to_anchors(t(X), t(off), t(w), t(W), offsets_host=off)
+    assign, H, st = map_via(asot, path, t(X), t(off), t(w), t(W), off)
     torch.cuda.synchronize()
     a_o = O.map_assign(X, W)
     a_g = assign.cpu().numpy()

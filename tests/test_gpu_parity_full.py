@@ -32,9 +32,20 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def gpu_map(asot, inp):
-    assign, H, st = asot.map_to_anchors(dev(inp.points), dev(inp.offsets), dev(inp.weights),
-                                        dev(inp.anchors), offsets_host=inp.offsets)
+def gpu_map(asot, inp, path="exact"):
+    """asot_map_to_anchors (the CUDA-core kernel on every point), or the mapping inside
+    asot_distance_matrix (an empty tile range: tensor-core products + the exact kernel on the
+    points they cannot decide, R#37)."""
+    if path == "exact":
+        assign, H, st = asot.map_to_anchors(dev(inp.points), dev(inp.offsets), dev(inp.weights),
+                                            dev(inp.anchors), offsets_host=inp.offsets)
+    else:
+        assign = torch.empty(inp.n_points, dtype=torch.int32, device="cuda")
+        H = torch.empty((inp.n_dist, inp.n_anchors), dtype=torch.float32, device="cuda")
+        st = asot.asot.new_status()
+        asot.distance_matrix(dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors),
+                             dev(inp.cost), float(inp.eps), inp.iters, tile_range=(0, 0),
+                             assign_out=assign, hist_out=H, offsets_host=inp.offsets, status=st)
     torch.cuda.synchronize()
     asot.check_status(st)
     return assign.cpu().numpy(), H.cpu().numpy()
@@ -66,13 +77,24 @@ def c5_sample(asot):
 
 
 def test_mapping_bit_exact_c3_all_points(asot):
+    """All 349,010 c3 points, through both mapping paths (the default distance-matrix path is the
+    tensor-core one)."""
     inp = make_inputs("c3")
     assert inp.n_points == 349010
-    a_g, H_g = gpu_map(asot, inp)
     a_o = map_assign_parallel(inp.points, inp.anchors)
-    assert np.array_equal(a_g, a_o), f"{(a_g != a_o).sum()} of {a_o.size} assignments differ"
     H_o = O.histograms(a_o, inp.weights, inp.offsets, inp.n_anchors).astype(np.float32)
-    np.testing.assert_array_equal(H_g, H_o)
+    for path in ("exact", "tc"):
+        a_g, H_g = gpu_map(asot, inp, path)
+        assert np.array_equal(a_g, a_o), f"{path}: {(a_g != a_o).sum()} of {a_o.size} assignments differ"
+        np.testing.assert_array_equal(H_g, H_o)
+
+
+def test_mapping_bit_exact_c5_ten_percent_tc(asot):
+    """c5's seeded 10% of distributions through the tensor-core mapping path (d = 128, K = 1024)."""
+    s = c5_sample(asot)
+    a_g, H_g = gpu_map(asot, s["inp"], "tc")
+    assert np.array_equal(a_g[s["rows"]], s["a_o"]), f"{(a_g[s['rows']] != s['a_o']).sum()} differ"
+    np.testing.assert_array_equal(H_g[s["dists"]], s["H_o"].astype(np.float32))
 
 
 def test_mapping_bit_exact_c5_ten_percent(asot):
