@@ -737,6 +737,25 @@ def main():
                 "share_of_step": map_ms / max(tot_ms, 1e-9),
                 "note": "CUDA-core fp32 GEMM-like tiles (16 points x weights from L2/SMEM); "
                         "bound: FP32 FFMA peak 148 x 128 x 2 x 1.965 GHz"}
+        elif T_rank is not None and args.mapping == "onehot" and inp.dim in (32, 64, 128) and \
+                inp.n_anchors % 64 == 0 and world == 1:
+            # asot_distance_matrix maps on the tensor cores (R#37: asot_map_tc.cu's rule, d in
+            # {32, 64, 128}, K % 64 == 0) + the exact kernel on the listed ambiguous points
+            d_, K_ = inp.dim, inp.n_anchors
+            bytes_ = T_rank * (4 * d_ + 4) + K_ * d_ * 4
+            flops = 2 * K_ * d_ * T_rank                      # x . w per (point, anchor)
+            tpeak = peaks["bf16_tflops"] * TF32_OVER_BF16
+            mapping = {
+                "kernel": "map_tc_kernel (tcgen05 3xTF32 scores, R#37 bound) + map_assign_kernel on the "
+                          "ambiguous points", "ms_per_launch": map_avg_ms, "points_per_launch": T_rank,
+                "bound": "tensor", "hbm_gbs": bytes_ / (map_avg_ms / 1e3) / 1e9,
+                "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                "hbm_frac": bytes_ / (map_avg_ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                "tflops_algorithmic": flops / (map_avg_ms / 1e3) / 1e12,
+                "tf32_issued_frac": 3 * flops / (map_avg_ms / 1e3) / 1e12 / tpeak,
+                "share_of_step": map_ms / max(tot_ms, 1e-9),
+                "note": "ms covers the norms / images prep, the tensor-core pass and the exact pass on "
+                        "the listed points; the decision is the fp64 definition's (bit-exact tests)"}
         elif T_rank is not None and args.mapping == "onehot":
             d_, K_ = inp.dim, inp.n_anchors
             bytes_ = T_rank * (4 * d_ + 4) + K_ * d_ * 4     # points in, assignment out, anchors
