@@ -583,17 +583,22 @@ def main():
     mac_clk, per_product = {10: (4096, 3), 3: (2048, 3), 5: (2048, 3)}.get(kind, (2048, 1))
     sparse_info = None
     if kind == 11:
-        # the small-support kernel (R#36): thread per pair, an 8 x 8 register block of K (supports
-        # <= 8; 9-16: a local-memory form), fp32 FFMA2 -- bound by the FP32 pipe / issue rate.
-        # Issued work: 2 updates x 64 MACs per iteration + the cost on the real block; useful work:
+        # the small-support kernels (R#36): thread per pair, an S x S register block of K per
+        # support class (S = 4, 6, 8; 9-16 bins: a half-warp per pair), fp32 FFMA2 -- bound by the
+        # FP32 pipe / issue rate.  Issued work: 2 updates x S^2 MACs per iteration; useful work:
         # the real |S_a| x |S_b| blocks (sum over i < j of m_i m_j)
         S = supports
         useful_mn = float((S.sum() ** 2 - (S * S).sum()) / 2) if world == 1 else None
-        flops_issued = 4 * 64 * L
+        # issued: the register form each pair runs (support-ordered classes: the larger support of
+        # the pair picks 4 x 4, 6 x 6, 8 x 8, or the 16 x 16 half-warp form): sum over pairs of
+        # 4 S^2 L, via the sorted supports (pair (i', j'), i' < j': S = class of supp(j'))
+        ss = np.sort(S.cpu().numpy())
+        form = np.where(ss <= 4, 4, np.where(ss <= 6, 6, np.where(ss <= 8, 8, 16))).astype(np.float64)
+        flops_issued = float((np.arange(ss.size) * 4.0 * form * form * L).sum() / max(P, 1))
         peak = FP32_ALU_PEAK_TFLOPS
         bound, peak_note = "alu", "FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz"
         sparse_info = {"max_support": int(S.max()), "mean_support": float(S.mean()),
-                       "issued_flops_per_pair": flops_issued,
+                       "issued_flops_per_pair_mean": flops_issued,
                        "useful_flops_per_pair_mean": (4 * L + 2) * useful_mn / P if useful_mn else None,
                        "dense_equivalent_flops_per_pair": flops_per_pair}
         flops_per_pair = flops_issued

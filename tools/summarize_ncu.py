@@ -25,7 +25,8 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 
 
 def ours(name):
-    return 'asot' in name or 'sinkhorn' in name or 'map_assign' in name or 'histogram' in name
+    # libasot's kernels (namespaces asot, sps, maptc, mltc, dltc, tc*, ...) vs torch plumbing
+    return 'at::' not in name and 'cub::' not in name and 'cutlass' not in name
 
 
 def launches(csv_path, out_md):
