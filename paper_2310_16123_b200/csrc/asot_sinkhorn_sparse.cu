@@ -78,21 +78,21 @@ __global__ void support_kernel(const float* __restrict__ H, int64_t n_dist, int 
 }
 
 // x_e = m_e / d_e for N (even) anchors, bitwise div_clamped: the range test once for the N --
-// every d in [FLT_MIN, 2^126] exactly when no d is negative and sum_e d_e rcp(d_e) = N (+- N 2^-22;
+// every non-negative d lies in [FLT_MIN, 2^126] exactly when sum_e d_e rcp(d_e) = N (+- N 2^-22;
 // a d outside the range gives a product of 0, inf or NaN under rcp.approx.ftz) -- then
 // x = m rcp(d); otherwise the clamped per-element form (S:62 clamp + flag).
+// nonneg: every mass of the pair is >= 0 (checked once per pair), so no denominator can be
+// negative (K > 0, scalings >= 0) and the sign test is skipped; otherwise (negative or NaN
+// masses: a BAD_MASS input) the per-element form always.
 template <int N>
-__device__ __forceinline__ void divn(const float* m, const float* d, float* x, bool& clamped) {
+__device__ __forceinline__ void divn(const float* m, const float* d, float* x, bool& clamped, bool nonneg = false) {
   float r[N];
 #pragma unroll
   for (int e = 0; e < N; ++e) r[e] = rcp_ftz(d[e]);
   float2 t = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int e = 0; e < N; e += 2) t = ffma2(make_float2(d[e], d[e + 1]), make_float2(r[e], r[e + 1]), t);
-  uint32_t sg = 0u;
-#pragma unroll
-  for (int e = 0; e < N; ++e) sg |= __float_as_uint(d[e]);
-  if (fabsf((t.x + t.y) - (float)N) < 2e-6f && !(sg >> 31)) {
+  if (nonneg && fabsf((t.x + t.y) - (float)N) < 2e-6f) {
 #pragma unroll
     for (int e = 0; e < N; e += 2) {
       const float2 q = fmul2(make_float2(m[e], m[e + 1]), make_float2(r[e], r[e + 1]));
@@ -119,6 +119,7 @@ __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs
   float2 gp[Q][M];
   float2 up[Q];
   float v[M];
+  bool nonneg = true;
   {
     int ia[M], ib[M];
 #pragma unroll
@@ -127,6 +128,7 @@ __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs
       a[r] = r < m ? sp.val[(int64_t)i * kSparseCap + r] : 0.0f;
       ib[r] = r < n ? (int)sb[r] : 0;
       b[r] = r < n ? sp.val[(int64_t)j * kSparseCap + r] : 0.0f;
+      nonneg &= a[r] >= 0.0f && b[r] >= 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q)
@@ -152,7 +154,7 @@ __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs
       for (int q = 0; q < Q; ++q) t = ffma2(gp[q][c], up[q], t);
       den[c] = t.x + t.y;
     }
-    divn<M>(b, den, v, clamped);
+    divn<M>(b, den, v, clamped, nonneg);
   };
   v_update();
   for (int it = 1; it < iters; ++it) {
@@ -165,7 +167,7 @@ __device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs
       den[2 * q] = t.x;
       den[2 * q + 1] = t.y;
     }
-    divn<M>(a, den, un, clamped);
+    divn<M>(a, den, un, clamped, nonneg);
 #pragma unroll
     for (int q = 0; q < Q; ++q) up[q] = make_float2(un[2 * q], un[2 * q + 1]);
     v_update();
