@@ -105,87 +105,137 @@ __device__ __forceinline__ void divn(const float* m, const float* d, float* x, b
   }
 }
 
-// The fast form for |S_a|, |S_b| <= S (S in {4, 6, 8}; the warp's largest support picks S).
-// gp[q][c] = (K_{2q,c}, K_{2q+1,c}) of the block, up[q] = (u_{2q}, u_{2q+1}); padding: K = 1,
-// masses 0, so padded scalings are exactly 0.  u-update: rows in pairs, t = sum_c K_rc v_c (c
-// increasing); v-update: t = (even-r partial + odd-r partial) of sum_r K_rc u_r.
-template <int S>
-__device__ __forceinline__ float pair_fast(int i, int j, int K, const SparseBufs& sp, int iters, bool& clamped) {
-  constexpr int M = S, Q = S / 2;
-  const int m = sp.cnt[i], n = sp.cnt[j];
-  const uint16_t* sa = sp.idx + (int64_t)i * kSparseCap;
-  const uint16_t* sb = sp.idx + (int64_t)j * kSparseCap;
-  float a[M], b[M];
-  float2 gp[Q][M];
-  float2 up[Q];
-  float v[M];
+// Support class of a distribution (4: <= 4 bins, 6: 5-6, 8: 7-8, 16: 9-16).  The register forms
+// put the smaller class on the rows (R <= C), which makes the role deterministic: a pair of one
+// class keeps its u side on the rows.
+__device__ __forceinline__ int support_class(int cnt) { return cnt <= 4 ? 4 : cnt <= 6 ? 6 : cnt <= 8 ? 8 : 16; }
+
+// The fast form: an R x C register block of K with the row distribution's <= R bins and the column
+// distribution's <= C bins.  gp[q][c] = (K_{2q,c}, K_{2q+1,c}), rp[q] = the row scalings in pairs,
+// cs[c] the column scalings; padding: K = 1, masses 0, so padded scalings are exactly 0.
+//   row step: rows = m_row / (sum_c K_rc cs_c)   (c increasing; FFMA2 over row pairs)
+//   col step: cols = m_col / (even-r partial + odd-r partial of sum_r K_rc rp_r)
+// The recurrence (R#5) starts from v^0 = 1 on the v side, i.e. u^1 = a / R_u with the full row
+// sums of K (R#36), then alternates v, u, ..., v.  col_u (the u side is the column distribution,
+// R#10: u = the smaller original index) stores K^T's block (entry (r, c) = K[col anchor][row
+// anchor]), so u = cols and v = rows; both orientations run one alternating schedule of 2L steps
+// starting with a row step -- a u-on-rows pair skips step 0, a u-on-columns pair skips step
+// 2L - 1 -- so a warp diverges on two steps only.  d = sum_r sum_c rp_r KC(r, c) cs_c with KC
+// the same (K (.) C_s or its transpose) block.
+template <int R, int C>
+__device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K, const SparseBufs& sp, int iters,
+                                           bool& clamped) {
+  constexpr int Q = R / 2;
+  const int m = sp.cnt[rowd], n = sp.cnt[cold];
+  const uint16_t* sr = sp.idx + (int64_t)rowd * kSparseCap;
+  const uint16_t* sc = sp.idx + (int64_t)cold * kSparseCap;
+  float mr[R], mc[C];
+  float2 gp[Q][C];
+  float2 rp[Q];
+  float cs[C];
   bool nonneg = true;
   {
-    int ia[M], ib[M];
+    int ir[R], ic[C];
 #pragma unroll
-    for (int r = 0; r < M; ++r) {
-      ia[r] = r < m ? (int)sa[r] : 0;
-      a[r] = r < m ? sp.val[(int64_t)i * kSparseCap + r] : 0.0f;
-      ib[r] = r < n ? (int)sb[r] : 0;
-      b[r] = r < n ? sp.val[(int64_t)j * kSparseCap + r] : 0.0f;
-      nonneg &= a[r] >= 0.0f && b[r] >= 0.0f;
+    for (int r = 0; r < R; ++r) {
+      ir[r] = r < m ? (int)sr[r] : 0;
+      mr[r] = r < m ? sp.val[(int64_t)rowd * kSparseCap + r] : 0.0f;
+      nonneg &= mr[r] >= 0.0f;
     }
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        const bool cv = c < n;
-        gp[q][c].x = (2 * q < m && cv) ? __ldg(sp.G + (int64_t)ia[2 * q] * K + ib[c]) : 1.0f;
-        gp[q][c].y = (2 * q + 1 < m && cv) ? __ldg(sp.G + (int64_t)ia[2 * q + 1] * K + ib[c]) : 1.0f;
-      }
-    // half-iteration 1: v^0 = 1 on every anchor, so (K v^0)_r is the full row sum R_r
+    for (int c = 0; c < C; ++c) {
+      ic[c] = c < n ? (int)sc[c] : 0;
+      mc[c] = c < n ? sp.val[(int64_t)cold * kSparseCap + c] : 0.0f;
+      nonneg &= mc[c] >= 0.0f;
+      cs[c] = 0.0f;
+    }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      up[q].x = 2 * q < m ? div_clamped(a[2 * q], __ldg(sp.R + ia[2 * q]), clamped) : 0.0f;
-      up[q].y = 2 * q + 1 < m ? div_clamped(a[2 * q + 1], __ldg(sp.R + ia[2 * q + 1]), clamped) : 0.0f;
+      rp[q] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const bool cv = c < n;
+        const int64_t a0 = col_u ? (int64_t)ic[c] * K + ir[2 * q] : (int64_t)ir[2 * q] * K + ic[c];
+        const int64_t a1 = col_u ? (int64_t)ic[c] * K + ir[2 * q + 1] : (int64_t)ir[2 * q + 1] * K + ic[c];
+        gp[q][c].x = (2 * q < m && cv) ? __ldg(sp.G + a0) : 1.0f;
+        gp[q][c].y = (2 * q + 1 < m && cv) ? __ldg(sp.G + a1) : 1.0f;
+      }
+    }
+    // u^1 = a / R_u (v^0 = 1 on every anchor: (K v^0) is the full row sum)
+    if (!col_u) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        rp[q].x = 2 * q < m ? div_clamped(mr[2 * q], __ldg(sp.R + ir[2 * q]), clamped) : 0.0f;
+        rp[q].y = 2 * q + 1 < m ? div_clamped(mr[2 * q + 1], __ldg(sp.R + ir[2 * q + 1]), clamped) : 0.0f;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) cs[c] = c < n ? div_clamped(mc[c], __ldg(sp.R + ic[c]), clamped) : 0.0f;
     }
   }
-  auto v_update = [&]() {
-    float den[M];
+  auto row_step = [&]() {
+    float2 t[Q];
 #pragma unroll
-    for (int c = 0; c < M; ++c) {
+    for (int q = 0; q < Q; ++q) t[q] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) t[q] = ffma2(gp[q][c], make_float2(cs[c], cs[c]), t[q]);
+    float den[R], x[R];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      den[2 * q] = t[q].x;
+      den[2 * q + 1] = t[q].y;
+    }
+    divn<R>(mr, den, x, clamped, nonneg);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) rp[q] = make_float2(x[2 * q], x[2 * q + 1]);
+  };
+  auto col_step = [&]() {
+    float den[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
       float2 t = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int q = 0; q < Q; ++q) t = ffma2(gp[q][c], up[q], t);
+      for (int q = 0; q < Q; ++q) t = ffma2(gp[q][c], rp[q], t);
       den[c] = t.x + t.y;
     }
-    divn<M>(b, den, v, clamped, nonneg);
+    divn<C>(mc, den, cs, clamped, nonneg);
   };
-  v_update();
-  for (int it = 1; it < iters; ++it) {
-    float den[M], un[M];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      float2 t = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (int c = 0; c < M; ++c) t = ffma2(gp[q][c], make_float2(v[c], v[c]), t);
-      den[2 * q] = t.x;
-      den[2 * q + 1] = t.y;
-    }
-    divn<M>(a, den, un, clamped, nonneg);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) up[q] = make_float2(un[2 * q], un[2 * q + 1]);
-    v_update();
+  // steps s = 0 .. 2L - 1: even = row step, odd = col step; u on rows: v^1 at s = 1 ... v^L at
+  // s = 2L - 1 (step 0 skipped); u on columns: v^1 at s = 0 ... v^L at s = 2L - 2 (step 2L - 1
+  // skipped)
+  if (col_u) row_step();
+  for (int it = 0; it < iters; ++it) {
+    if (!(col_u && it == iters - 1)) col_step();   // s = 2 it + 1
+    if (it < iters - 1) row_step();                 // s = 2 it + 2
   }
-  // a6: d = sum_r u_r sum_c (K (.) C_s)_rc v_c over the block
+  // a6: d = sum_r rp_r sum_c KC(r, c) cs_c over the block
   float d = 0.0f;
 #pragma unroll
-  for (int r = 0; r < M; ++r) {
+  for (int r = 0; r < R; ++r) {
     if (r < m) {
-      const float* gc = sp.GC + (int64_t)sa[r] * K;
+      const int ir = (int)sr[r];
       float t = 0.0f;
 #pragma unroll
-      for (int c = 0; c < M; ++c)
-        if (c < n) t = fmaf(__ldg(gc + sb[c]), v[c], t);
-      d = fmaf((r & 1) ? up[r >> 1].y : up[r >> 1].x, t, d);
+      for (int c = 0; c < C; ++c)
+        if (c < n) {
+          const int icc = (int)sc[c];
+          t = fmaf(__ldg(sp.GC + (col_u ? (int64_t)icc * K + ir : (int64_t)ir * K + icc)), cs[c], t);
+        }
+      d = fmaf((r & 1) ? rp[r >> 1].y : rp[r >> 1].x, t, d);
     }
   }
   return d;
+}
+
+// (i, j): i the u side (R#10).  The row side is the smaller support class, the u side on equal
+// classes -- the role rule every traversal shares, so every path computes a pair bitwise alike.
+__device__ __forceinline__ void pair_roles(int i, int j, const SparseBufs& sp, int& rowd, int& cold, bool& col_u) {
+  const bool swap = support_class(sp.cnt[j]) < support_class(sp.cnt[i]);
+  rowd = swap ? j : i;
+  cold = swap ? i : j;
+  col_u = swap;
 }
 
 // Supports of 9-16 bins: the same recurrence with the block read from L1 / L2 every half-iteration.
@@ -335,9 +385,12 @@ sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int it
     const unsigned smax = __reduce_max_sync(0xffffffffu, slow ? 0u : (unsigned)(m > nn ? m : nn));
     float d = 0.0f;
     if (valid && !slow) {
-      if (smax <= 4) d = pair_fast<4>(i, j, K, sp, iters, clamped);
-      else if (smax <= 6) d = pair_fast<6>(i, j, K, sp, iters, clamped);
-      else d = pair_fast<8>(i, j, K, sp, iters, clamped);
+      int rd, cd;
+      bool cu;
+      pair_roles(i, j, sp, rd, cd, cu);
+      if (smax <= 4) d = pair_rect<4, 4>(rd, cd, cu, K, sp, iters, clamped);
+      else if (smax <= 6) d = pair_rect<6, 6>(rd, cd, cu, K, sp, iters, clamped);
+      else d = pair_rect<8, 8>(rd, cd, cu, K, sp, iters, clamped);
     } else if (valid) {
       d = pair_slow(i, j, K, sp, iters, &clamped);
     }
@@ -353,18 +406,19 @@ sinkhorn_sparse_kernel(PairSource ps, PairSink out, int K, SparseBufs sp, int it
 // one register form (S = 4, 6, 8; 0 = the 9-16 form) at the occupancy that form allows; a warp's
 // 32 consecutive k share (mostly) one column.  Each pair keeps its orientation (u side = the
 // smaller original index, R#10) and lands at (i, j) of the matrix; [k_lo, k_hi) bounds the part.
+// The columns of 9-16 bins (every row before them): a half-warp per pair.
 template <int S>
-__global__ void __launch_bounds__(kThreads, S == 4 ? 8 : S == 6 ? 5 : 4)
+__global__ void __launch_bounds__(kThreads, 2)
 sinkhorn_sparse_class_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp, int iters, int64_t k_lo,
                              int64_t k_hi) {
+  static_assert(S == 0, "the 9-16 bin form");
   if (*sp.flag != 0u) return;
-  constexpr int cls = S == 4 ? 0 : S == 6 ? 1 : S == 8 ? 2 : 3;
-  const int64_t c0 = cls == 0 ? 0 : sp.bounds[cls - 1], c1 = sp.bounds[cls];
+  const int64_t c0 = sp.bounds[2], c1 = sp.bounds[3];
   int64_t a = c0 * (c0 - 1) / 2, b = c1 * (c1 - 1) / 2;
   if (a < k_lo) a = k_lo;
   if (b > k_hi) b = k_hi;
   bool clamped = false;
-  if constexpr (S == 0) {
+  {
     // a half-warp per pair (warp-synchronous: both halves loop the same number of times)
     const int64_t hw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 4, nhw = ((int64_t)gridDim.x * kThreads) >> 4;
     for (int64_t k0 = a + (hw & ~(int64_t)1); k0 < b; k0 += nhw) {
@@ -390,19 +444,64 @@ sinkhorn_sparse_class_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp,
     if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
     return;
   }
-  for (int64_t k = a + (int64_t)blockIdx.x * kThreads + threadIdx.x; k < b; k += (int64_t)gridDim.x * kThreads) {
+}
+
+// Rows of support class R x columns of class C (R <= C) of the support-ordered pairs: the row
+// distributions perm[r0, r1), the columns perm[c0, c1) (classes are contiguous in perm).  R < C:
+// the full rectangle, enumerated column by column; R = C: the triangle i' < j' inside the class.
+// Pairs outside the part [k_lo, k_hi) of the column-major enumeration (k = j'(j'-1)/2 + i') are
+// skipped; the local range is cut to the part's columns first.
+template <int R, int C>
+__global__ void __launch_bounds__(kThreads, R * C <= 16 ? 8 : R * C <= 24 ? 7 : R * C <= 48 ? 5 : 4)
+sinkhorn_sparse_rect_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp, int iters, int64_t k_lo,
+                            int64_t k_hi) {
+  if (*sp.flag != 0u) return;
+  constexpr int rc = R == 4 ? 0 : R == 6 ? 1 : 2, cc = C == 4 ? 0 : C == 6 ? 1 : 2;
+  const int64_t r0 = rc == 0 ? 0 : sp.bounds[rc - 1], r1 = sp.bounds[rc];
+  const int64_t c0 = cc == 0 ? 0 : sp.bounds[cc - 1], c1 = sp.bounds[cc];
+  if (r1 <= r0 || c1 <= c0 || k_hi <= k_lo) return;
+  auto col_of = [](int64_t k) {   // the column j' of column-major pair index k
     int64_t jp = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)k)) * 0.5);
     while (jp * (jp - 1) / 2 > k) --jp;
     while ((jp + 1) * jp / 2 <= k) ++jp;
-    const int64_t ip = k - jp * (jp - 1) / 2;
-    int i = sp.perm[ip], j = sp.perm[jp];
-    if (i > j) {
-      const int t = i;
-      i = j;
-      j = t;
+    return jp;
+  };
+  const int64_t jlo = col_of(k_lo) > c0 ? col_of(k_lo) : c0;
+  const int64_t jhi = col_of(k_hi - 1) + 1 < c1 ? col_of(k_hi - 1) + 1 : c1;
+  if (jhi <= jlo) return;
+  const int64_t nr = r1 - r0;
+  const bool tri = R == C;
+  const int64_t q0 = tri ? (jlo - c0) * (jlo - c0 - 1) / 2 : (jlo - c0) * nr;
+  const int64_t q1 = tri ? (jhi - c0) * (jhi - c0 - 1) / 2 : (jhi - c0) * nr;
+  bool clamped = false;
+  for (int64_t q = q0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; q < q1; q += (int64_t)gridDim.x * kThreads) {
+    int64_t ip, jp;
+    if (tri) {
+      int64_t jj = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)q)) * 0.5);
+      while (jj * (jj - 1) / 2 > q) --jj;
+      while ((jj + 1) * jj / 2 <= q) ++jj;
+      jp = c0 + jj;
+      ip = c0 + (q - jj * (jj - 1) / 2);
+    } else {
+      jp = c0 + q / nr;
+      ip = r0 + q % nr;
     }
-    const float d = pair_fast<S == 0 ? 4 : S>(i, j, K, sp, iters, clamped);
-    write_result(out, 0, true, i, j, d);
+    const int64_t k = jp * (jp - 1) / 2 + ip;
+    if (k < k_lo || k >= k_hi) continue;
+    const int a = sp.perm[ip], b = sp.perm[jp];
+    int rowd, cold;
+    bool col_u;
+    if (tri) {   // one class: the u side (the smaller original index) on the rows
+      rowd = a < b ? a : b;
+      cold = a < b ? b : a;
+      col_u = false;
+    } else {     // the smaller class on the rows
+      rowd = a;
+      cold = b;
+      col_u = b < a;
+    }
+    const float d = pair_rect<R, C>(rowd, cold, col_u, K, sp, iters, clamped);
+    write_result(out, 0, true, rowd < cold ? rowd : cold, rowd < cold ? cold : rowd, d);
   }
   if (clamped) atomicOr(out.status, ASOT_FLAG_DENOM_CLAMPED);
 }
@@ -491,9 +590,12 @@ cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, in
     const int64_t P = ps.n_dist * (ps.n_dist - 1) / 2;
     const int64_t p0 = ps.tile_begin, p1 = ps.tile_begin + ps.n_slots / kTileSlots;
     const int64_t k_lo = T > 0 ? p0 * P / T : 0, k_hi = T > 0 ? p1 * P / T : 0;
-    sps::sinkhorn_sparse_class_kernel<4><<<sms * 8, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_class_kernel<6><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_class_kernel<8><<<sms * 4, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<4, 4><<<sms * 8, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<4, 6><<<sms * 7, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<6, 6><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<4, 8><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<6, 8><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<8, 8><<<sms * 4, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
     sps::sinkhorn_sparse_class_kernel<0><<<sms * 2, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
     return cudaGetLastError();
   }
