@@ -252,3 +252,34 @@ def test_partition_union_bitwise(asot, cfg, n):
     torch.cuda.synchronize()
     asot.check_status(st)
     assert torch.equal(R, D)
+
+
+def test_sparse_asymmetric_cost(asot):
+    """C_s need not be symmetric (an input; R#7): K v and K^T u differ.  Supports of 2, 5 and 7
+    bins (three support classes, so pairs run with the u side on the rows and on the columns of
+    the register forms, which then hold K^T's block): the whole matrix (support-ordered class
+    kernels) and an explicit list (the a4 / list traversal) against the oracle, within the fp32
+    bar, the list entries bitwise equal to the matrix entries."""
+    rng = np.random.default_rng(17)
+    K, n = 96, 40
+    C = rng.uniform(0.0, 1.0, size=(K, K)).astype(np.float32)
+    np.fill_diagonal(C, 0.0)
+    H = np.zeros((n, K), np.float32)
+    for i in range(n):
+        s = (2, 5, 7)[i % 3]
+        idx = rng.choice(K, size=s, replace=False)
+        H[i, idx] = rng.dirichlet(np.ones(s)).astype(np.float32)
+    eps, L = 0.1, 50
+    st = asot.asot.new_status()
+    D = asot.distance_matrix(None, None, None, None, dev(C), eps, L, precision=asot.TF32, hist=dev(H),
+                             cost_max=1.0, status=st)
+    pi, pj = np.triu_indices(n, k=1)
+    d = asot.pairwise_sinkhorn(dev(H), dev(C), eps, L, dev(pi.astype(np.int32)), dev(pj.astype(np.int32)),
+                               precision=asot.TF32, cost_max=1.0, status=st)
+    torch.cuda.synchronize()
+    asot.check_status(st)
+    do, _ = O.pair_costs(H, C, eps, L, pi.astype(np.int64), pj.astype(np.int64))
+    Dn = D.cpu().numpy()
+    r = rel_err(Dn[pi, pj], do, 1.0)
+    assert r.max() <= FP32_TOL, f"matrix: max rel {r.max():.3e}"
+    np.testing.assert_array_equal(d.cpu().numpy(), Dn[pi, pj])
