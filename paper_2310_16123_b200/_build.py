@@ -19,6 +19,11 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
 # ASOT_TC_DEBUG_MODE (epilogue or MMAs skipped, clock traces).  The product library never has them.
 if os.environ.get("ASOT_DEBUG_BUILD") == "1":
     FLAGS.append("-DASOT_DEBUG_KERNELS")
+# ASOT_CHECKED=1: device-side bounds checks (ASOT_DEV_CHECK: printf + trap) in the kernels' index
+# arithmetic -- this pool has compute-sanitizer closed, so the GPU suite also runs on a checked
+# build (tools/checked_tests.sh).  The product library never has them.
+if os.environ.get("ASOT_CHECKED") == "1":
+    FLAGS.append("-DASOT_CHECKED")
 
 
 def _compile(src: str) -> tuple[str, str]:

@@ -9,6 +9,22 @@
 
 #include "asot.h"
 
+// Device-side bounds checks of the ASOT_CHECKED build (see _build.py); nothing otherwise.
+#ifdef ASOT_CHECKED
+#include <cstdio>
+#define ASOT_DEV_CHECK(cond, what)                                                        \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("ASOT_CHECKED: %s failed at %s:%d\n", what, __FILE__, __LINE__);            \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define ASOT_DEV_CHECK(cond, what) \
+  do {                             \
+  } while (0)
+#endif
+
 namespace asot {
 
 constexpr int kTileSlots = ASOT_TILE_SLOTS;  // 128 pair slots per tile (8 rows x 16 cols)
@@ -96,7 +112,9 @@ __device__ __forceinline__ bool dense_skipped(const PairSink& out) {
 // entry with an index outside [0, N) stores NaN and raises ASOT_FLAG_BAD_INDEX.
 __device__ inline void write_result(const PairSink& out, int64_t s, bool valid, int i, int j, float d) {
   if (out.idx) s = out.idx[s];
+  ASOT_DEV_CHECK(s >= 0, "result slot >= 0");
   if (valid) {
+    ASOT_DEV_CHECK(i >= 0 && j >= 0 && i < out.n_dist && j < out.n_dist, "pair indices in [0, n_dist)");
     if (!isfinite(d)) atomicOr(out.status, ASOT_FLAG_NONFINITE_OUTPUT);
     if (out.vec) out.vec[s] = d;
     if (out.mat) {

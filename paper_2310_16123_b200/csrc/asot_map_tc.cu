@@ -255,9 +255,12 @@ map_tc_kernel(Args A) {
         const float xr = sqrtf(n2) * (1.0f + 1.5258789e-5f) + wmax;
         const float B = cB * xr * xr * (1.0f + 1.5258789e-5f);
         if (K == 1 || s2 > b + (2.0f * B + slack)) {
+          ASOT_DEV_CHECK(bi >= 0 && bi < K, "tensor-core winner in [0, K)");
           A.assign[t0 + p] = bi;
         } else {
-          A.amb[atomicAdd(A.amb_cnt, 1ull)] = t0 + p;
+          const unsigned long long slot = atomicAdd(A.amb_cnt, 1ull);
+          ASOT_DEV_CHECK(slot < (unsigned long long)A.T, "ambiguous list within T");
+          A.amb[slot] = t0 + p;
         }
       }
     }

@@ -65,6 +65,7 @@ __global__ void support_kernel(const float* __restrict__ H, int64_t n_dist, int 
       const uint32_t bal = __ballot_sync(0xffffffffu, nz);
       const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
       if (nz && pos < kSparseCap) {
+        ASOT_DEV_CHECK(r < K, "support bin < K");
         sp.idx[i * kSparseCap + pos] = (uint16_t)r;
         sp.val[i * kSparseCap + pos] = v;
       }
@@ -127,6 +128,7 @@ __device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K
                                            bool& clamped) {
   constexpr int Q = R / 2;
   const int m = sp.cnt[rowd], n = sp.cnt[cold];
+  ASOT_DEV_CHECK(m <= R && n <= C, "supports fit the register form");
   const uint16_t* sr = sp.idx + (int64_t)rowd * kSparseCap;
   const uint16_t* sc = sp.idx + (int64_t)cold * kSparseCap;
   float mr[R], mc[C];
@@ -488,7 +490,9 @@ sinkhorn_sparse_rect_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp, 
     }
     const int64_t k = jp * (jp - 1) / 2 + ip;
     if (k < k_lo || k >= k_hi) continue;
+    ASOT_DEV_CHECK(ip >= r0 && ip < r1 && jp >= c0 && jp < c1 && ip < jp, "pair inside its class block");
     const int a = sp.perm[ip], b = sp.perm[jp];
+    ASOT_DEV_CHECK(a >= 0 && a < n_dist && b >= 0 && b < n_dist, "perm entries in [0, n_dist)");
     int rowd, cold;
     bool col_u;
     if (tri) {   // one class: the u side (the smaller original index) on the rows
