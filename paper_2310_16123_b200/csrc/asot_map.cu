@@ -308,7 +308,8 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
         if (refine) b.idx = bi;
       }
       if (valid && tx == 0) {
-        ASOT_DEV_CHECK(b.idx >= 0 && b.idx < K, "assignment in [0, K)");
+        // (0x7fffffff: a point with a non-finite coordinate has no nearest anchor -- flagged)
+        ASOT_DEV_CHECK(b.idx == 0x7fffffff || (b.idx >= 0 && b.idx < K), "assignment in [0, K)");
         assign[scatter ? gather[p0 + pl] : p0 + pl] = b.idx;
       }
     }

@@ -255,7 +255,7 @@ map_tc_kernel(Args A) {
         const float xr = sqrtf(n2) * (1.0f + 1.5258789e-5f) + wmax;
         const float B = cB * xr * xr * (1.0f + 1.5258789e-5f);
         if (K == 1 || s2 > b + (2.0f * B + slack)) {
-          ASOT_DEV_CHECK(bi >= 0 && bi < K, "tensor-core winner in [0, K)");
+          ASOT_DEV_CHECK(bi == 0x7fffffff || (bi >= 0 && bi < K), "tensor-core winner in [0, K)");
           A.assign[t0 + p] = bi;
         } else {
           const unsigned long long slot = atomicAdd(A.amb_cnt, 1ull);
