@@ -283,16 +283,31 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
         int bi = 0x7fffffff;
         if (refine) {
           const float* xp = Xs + pl * RS;
-          for (int j = tx; j < K; j += LPP) {
-            const float* wj = anchors + (int64_t)j * dim;
-            double accd = 0.0;
-            for (int k = 0; k < dim; ++k) {
-              const double t = __dsub_rn((double)xp[k], (double)wj[k]);
-              accd = __dadd_rn(accd, __dmul_rn(t, t));
+          // four of the lane's anchors at a time: four independent fp64 chains, each in the
+          // pinned op order (sequential in k), compared in increasing j
+          for (int j0 = tx; j0 < K; j0 += 4 * LPP) {
+            const float* wj[4];
+            double accd[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = j0 + e * LPP;
+              wj[e] = anchors + (int64_t)(j < K ? j : j0) * dim;
+              accd[e] = 0.0;
             }
-            if (accd < bd) {
-              bd = accd;
-              bi = j;
+            for (int k = 0; k < dim; ++k) {
+              const double xk = (double)xp[k];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const double t = __dsub_rn(xk, (double)wj[e][k]);
+                accd[e] = __dadd_rn(accd[e], __dmul_rn(t, t));
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (j0 + e * LPP < K && accd[e] < bd) {
+                bd = accd[e];
+                bi = j0 + e * LPP;
+              }
             }
           }
         }
