@@ -589,12 +589,14 @@ def main():
         # the real |S_a| x |S_b| blocks (sum over i < j of m_i m_j)
         S = supports
         useful_mn = float((S.sum() ** 2 - (S * S).sum()) / 2) if world == 1 else None
-        # issued: the register form each pair runs (support-ordered classes: the larger support of
-        # the pair picks 4 x 4, 6 x 6, 8 x 8, or the 16 x 16 half-warp form): sum over pairs of
-        # 4 S^2 L, via the sorted supports (pair (i', j'), i' < j': S = class of supp(j'))
+        # issued: the register form each pair runs (support-ordered classes, pair (i', j'), i' < j':
+        # the R x C rectangle R = class of supp(i'), C = class of supp(j') for C in {4, 6, 8}, the
+        # 16 x 16 half-warp form when C = 16): sum over pairs of 4 R C L
         ss = np.sort(S.cpu().numpy())
         form = np.where(ss <= 4, 4, np.where(ss <= 6, 6, np.where(ss <= 8, 8, 16))).astype(np.float64)
-        flops_issued = float((np.arange(ss.size) * 4.0 * form * form * L).sum() / max(P, 1))
+        rows_before = np.concatenate([[0.0], np.cumsum(form)[:-1]])   # sum of R over i' < j'
+        per_col = np.where(form == 16, 256.0 * np.arange(ss.size), form * rows_before)
+        flops_issued = float((4.0 * L * per_col).sum() / max(P, 1))
         peak = FP32_ALU_PEAK_TFLOPS
         bound, peak_note = "alu", "FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz"
         sparse_info = {"max_support": int(S.max()), "mean_support": float(S.mean()),
