@@ -82,18 +82,20 @@ __global__ void support_kernel(const float* __restrict__ H, int64_t n_dist, int 
 // every non-negative d lies in [FLT_MIN, 2^126] exactly when sum_e d_e rcp(d_e) = N (+- N 2^-22;
 // a d outside the range gives a product of 0, inf or NaN under rcp.approx.ftz) -- then
 // x = m rcp(d); otherwise the clamped per-element form (S:62 clamp + flag).
-// nonneg: every mass of the pair is >= 0 (checked once per pair), so no denominator can be
-// negative (K > 0, scalings >= 0) and the sign test is skipped; otherwise (negative or NaN
-// masses: a BAD_MASS input) the per-element form always.
+// seed: +0 when every mass of the pair is >= 0 (checked once per pair), so no denominator can be
+// negative (K > 0, scalings >= 0) and the sign test is skipped; NaN otherwise (negative or NaN
+// masses: a BAD_MASS input), which fails the range test, so the per-element form always runs.
+// The seed starts the test's sum: one register held across the loop instead of a predicate
+// the compiler re-derives from the masses at every step (predicate registers are few).
 template <int N>
-__device__ __forceinline__ void divn(const float* m, const float* d, float* x, bool& clamped, bool nonneg = false) {
+__device__ __forceinline__ void divn(const float* m, const float* d, float* x, bool& clamped, float seed) {
   float r[N];
 #pragma unroll
   for (int e = 0; e < N; ++e) r[e] = rcp_ftz(d[e]);
-  float2 t = make_float2(0.0f, 0.0f);
+  float2 t = make_float2(seed, 0.0f);
 #pragma unroll
   for (int e = 0; e < N; e += 2) t = ffma2(make_float2(d[e], d[e + 1]), make_float2(r[e], r[e + 1]), t);
-  if (nonneg && fabsf((t.x + t.y) - (float)N) < 2e-6f) {
+  if (fabsf((t.x + t.y) - (float)N) < 2e-6f) {
 #pragma unroll
     for (int e = 0; e < N; e += 2) {
       const float2 q = fmul2(make_float2(m[e], m[e + 1]), make_float2(r[e], r[e + 1]));
@@ -103,6 +105,26 @@ __device__ __forceinline__ void divn(const float* m, const float* d, float* x, b
   } else {
 #pragma unroll
     for (int e = 0; e < N; ++e) x[e] = div_clamped(m[e], d[e], clamped);
+  }
+}
+
+// The lazy form of divn: x = m rcp(d) for the N, the range test's terms summed into chk across
+// the whole recurrence (no test, branch or reconvergence per step).  Every in-range d gives
+// d rcp(d) = 1 +- 2^-22; an out-of-range d gives 0 (d > 2^126: the reciprocal flushes), inf or
+// NaN (d < FLT_MIN, d = 0), so after S steps over n terms in all, chk = n +- 1e-3 exactly when
+// every step's divn test above would have passed -- else pair_rect reruns the pair with the
+// per-step tests, whose result the lazy pass then reproduces bitwise whenever it is kept.
+template <int N>
+__device__ __forceinline__ void divn_lazy(const float* m, const float* d, float* x, float2& chk) {
+  float r[N];
+#pragma unroll
+  for (int e = 0; e < N; ++e) r[e] = rcp_ftz(d[e]);
+#pragma unroll
+  for (int e = 0; e < N; e += 2) {
+    chk = ffma2(make_float2(d[e], d[e + 1]), make_float2(r[e], r[e + 1]), chk);
+    const float2 q = fmul2(make_float2(m[e], m[e + 1]), make_float2(r[e], r[e + 1]));
+    x[e] = q.x;
+    x[e + 1] = q.y;
   }
 }
 
@@ -123,9 +145,11 @@ __device__ __forceinline__ int support_class(int cnt) { return cnt <= 4 ? 4 : cn
 // starting with a row step -- a u-on-rows pair skips step 0, a u-on-columns pair skips step
 // 2L - 1 -- so a warp diverges on two steps only.  d = sum_r sum_c rp_r KC(r, c) cs_c with KC
 // the same (K (.) C_s or its transpose) block.
-template <int R, int C>
-__device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K, const SparseBufs& sp, int iters,
-                                           bool& clamped) {
+// kLazy: the divides as divn_lazy, ok = false when the summed range test fails (the caller then
+// reruns the pair with kLazy = false: per-step tests, the S:62 clamp + flag).
+template <int R, int C, bool kLazy>
+__device__ __forceinline__ float pair_rect_pass(int rowd, int cold, bool col_u, int K, const SparseBufs& sp,
+                                                int iters, bool& clamped, bool& ok) {
   constexpr int Q = R / 2;
   const int m = sp.cnt[rowd], n = sp.cnt[cold];
   ASOT_DEV_CHECK(m <= R && n <= C, "supports fit the register form");
@@ -175,6 +199,8 @@ __device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K
       for (int c = 0; c < C; ++c) cs[c] = c < n ? div_clamped(mc[c], __ldg(sp.R + ic[c]), clamped) : 0.0f;
     }
   }
+  const float seed = nonneg ? 0.0f : __int_as_float(0x7fc00000);
+  float2 chk = make_float2(seed, 0.0f);
   auto row_step = [&]() {
     float2 t[Q];
 #pragma unroll
@@ -189,7 +215,8 @@ __device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K
       den[2 * q] = t[q].x;
       den[2 * q + 1] = t[q].y;
     }
-    divn<R>(mr, den, x, clamped, nonneg);
+    if (kLazy) divn_lazy<R>(mr, den, x, chk);
+    else divn<R>(mr, den, x, clamped, seed);
 #pragma unroll
     for (int q = 0; q < Q; ++q) rp[q] = make_float2(x[2 * q], x[2 * q + 1]);
   };
@@ -202,15 +229,25 @@ __device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K
       for (int q = 0; q < Q; ++q) t = ffma2(gp[q][c], rp[q], t);
       den[c] = t.x + t.y;
     }
-    divn<C>(mc, den, cs, clamped, nonneg);
+    if (kLazy) divn_lazy<C>(mc, den, cs, chk);
+    else divn<C>(mc, den, cs, clamped, seed);
   };
   // steps s = 0 .. 2L - 1: even = row step, odd = col step; u on rows: v^1 at s = 1 ... v^L at
   // s = 2L - 1 (step 0 skipped); u on columns: v^1 at s = 0 ... v^L at s = 2L - 2 (step 2L - 1
   // skipped)
+  // (the two ends peeled, so the loop body carries no per-step conditions)
   if (col_u) row_step();
-  for (int it = 0; it < iters; ++it) {
-    if (!(col_u && it == iters - 1)) col_step();   // s = 2 it + 1
-    if (it < iters - 1) row_step();                 // s = 2 it + 2
+  for (int it = 0; it < iters - 1; ++it) {
+    col_step();   // s = 2 it + 1
+    row_step();   // s = 2 it + 2
+  }
+  if (!col_u && iters > 0) col_step();   // s = 2L - 1
+  if (kLazy) {
+    // terms summed: R per row step, C per column step
+    const int rows = (col_u ? 1 : 0) + (iters > 1 ? iters - 1 : 0);
+    const int cols = (iters > 1 ? iters - 1 : 0) + (!col_u && iters > 0 ? 1 : 0);
+    ok = fabsf((chk.x + chk.y) - (float)(rows * R + cols * C)) < 0.5f;
+    if (!ok) return 0.0f;
   }
   // a6: d = sum_r rp_r sum_c KC(r, c) cs_c over the block
   float d = 0.0f;
@@ -229,6 +266,15 @@ __device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K
     }
   }
   return d;
+}
+
+template <int R, int C>
+__device__ __forceinline__ float pair_rect(int rowd, int cold, bool col_u, int K, const SparseBufs& sp, int iters,
+                                           bool& clamped) {
+  bool ok = true;
+  const float d = pair_rect_pass<R, C, true>(rowd, cold, col_u, K, sp, iters, clamped, ok);
+  if (ok) return d;
+  return pair_rect_pass<R, C, false>(rowd, cold, col_u, K, sp, iters, clamped, ok);
 }
 
 // (i, j): i the u side (R#10).  The row side is the smaller support class, the u side on equal
@@ -454,7 +500,7 @@ sinkhorn_sparse_class_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp,
 // Pairs outside the part [k_lo, k_hi) of the column-major enumeration (k = j'(j'-1)/2 + i') are
 // skipped; the local range is cut to the part's columns first.
 template <int R, int C>
-__global__ void __launch_bounds__(kThreads, R * C <= 16 ? 8 : R * C <= 24 ? 7 : R * C <= 48 ? 5 : 4)
+__global__ void __launch_bounds__(kThreads, R * C <= 16 ? 8 : R * C <= 24 ? 7 : R * C < 48 ? 5 : 4)
 sinkhorn_sparse_rect_kernel(int64_t n_dist, PairSink out, int K, SparseBufs sp, int iters, int64_t k_lo,
                             int64_t k_hi) {
   if (*sp.flag != 0u) return;
@@ -579,6 +625,28 @@ cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const floa
   return cudaGetLastError();
 }
 
+namespace {
+// One non-blocking side stream and a fork / join event pair per (host thread, device), created on
+// first use and kept for the life of the thread.
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  constexpr int kMaxDev = 64;
+  thread_local SideStream per_dev[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& ss = per_dev[dev < kMaxDev ? dev : 0];
+  if (ss.side == nullptr) {
+    cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+  }
+  return ss;
+}
+}  // namespace
+
 cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, int K, const SparseBufs& sp, int iters,
                                    int upt, int64_t max_slots, int sms, cudaStream_t s, bool ordered) {
   if (max_slots <= 0) return cudaSuccess;
@@ -594,14 +662,26 @@ cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, in
     const int64_t P = ps.n_dist * (ps.n_dist - 1) / 2;
     const int64_t p0 = ps.tile_begin, p1 = ps.tile_begin + ps.n_slots / kTileSlots;
     const int64_t k_lo = T > 0 ? p0 * P / T : 0, k_hi = T > 0 ? p1 * P / T : 0;
-    sps::sinkhorn_sparse_rect_kernel<4, 4><<<sms * 8, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<4, 6><<<sms * 7, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    // The classes with the largest blocks (8 x 8, 9-16 bins) have the fewest pairs (c3: 21.7 k
+    // and 2.0 k of 2 M): alone they fill a few warps per SM and run one pair's latency chain
+    // (measured: 8% of the warp slots).  They run on a side stream forked from s and joined back
+    // before the call's next launch, beside the large classes (longest chain first on s, the
+    // short 4 x 4 pairs last to fill the tail).
+    SideStream& ss = side_stream();
+    cudaError_t e = cudaEventRecord(ss.fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.side, ss.fork, 0);
+    if (e != cudaSuccess) return e;
+    sps::sinkhorn_sparse_rect_kernel<8, 8><<<sms * 4, sps::kThreads, 0, ss.side>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_class_kernel<0><<<sms * 2, sps::kThreads, 0, ss.side>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<6, 8><<<sms * 4, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
     sps::sinkhorn_sparse_rect_kernel<6, 6><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
     sps::sinkhorn_sparse_rect_kernel<4, 8><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<6, 8><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<8, 8><<<sms * 4, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_class_kernel<0><<<sms * 2, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    return cudaGetLastError();
+    sps::sinkhorn_sparse_rect_kernel<4, 6><<<sms * 7, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<4, 4><<<sms * 8, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaEventRecord(ss.join, ss.side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ss.join, 0);
+    return e;
   }
   sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt, 0);
   return cudaGetLastError();

@@ -2,6 +2,9 @@
 
   python tools/summarize_ncu.py launches <launches.csv> <out.md>
   python tools/summarize_ncu.py full <prof.ncu-rep> <out.json> [summary-key, e.g. c3:tf32] [kernel-name substring]
+  python tools/summarize_ncu.py set <prof.ncu-rep> <out.json> <summary-key> <kernel-name substring>
+      (every captured launch whose name matches, one per kernel: times and DRAM bytes summed,
+      pipe / issue percentages weighted by time -- the small-support class kernels of one call)
 """
 import collections
 import csv
@@ -108,8 +111,52 @@ def full(rep, out_json, traffic_key=None, kernel=None):
         json.dump(t, open(spath, 'w'), indent=1)
 
 
+def kernel_set(rep, out_json, key, kernel):
+    raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, u = rows[0], rows[1]
+    ki = h.index('Kernel Name')
+    seen, cand = set(), []
+    for r in rows[2:]:
+        if kernel in r[ki] and r[ki] not in seen:
+            seen.add(r[ki])
+            cand.append(r)
+
+    def num(v, k):
+        i = h.index(k)
+        scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'hz': 1, 'Khz': 1e3, 'Mhz': 1e6,
+                 'Ghz': 1e9, 'ns': 1e-6, 'nsecond': 1e-6, 'us': 1e-3, 'usecond': 1e-3, 'ms': 1.0,
+                 'msecond': 1.0}.get(u[i], 1)
+        return float(v[i].replace(',', '')) * scale
+    per = []
+    for v in cand:
+        per.append({'kernel': v[ki][:80], 'gpu_time_ms': num(v, 'gpu__time_duration.sum'),
+                    'dram_bytes': num(v, 'dram__bytes_read.sum') + num(v, 'dram__bytes_write.sum'),
+                    'fma_pipe_active_pct': num(v, 'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active'),
+                    'xu_inst_pct': num(v, 'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active'),
+                    'issue_active_pct': num(v, 'sm__issue_active.avg.pct_of_peak_sustained_elapsed'),
+                    'warps_active_pct': num(v, 'sm__warps_active.avg.pct_of_peak_sustained_active'),
+                    'registers': num(v, 'launch__registers_per_thread'),
+                    'sm_clock_hz': num(v, 'sm__cycles_elapsed.avg.per_second')})
+    T = sum(p['gpu_time_ms'] for p in per)
+    w = lambda k: sum(p[k] * p['gpu_time_ms'] for p in per) / T
+    agg = {'source': os.path.relpath(out_json, ROOT), 'kernel': f"{len(per)} kernels matching '{kernel}'",
+           'gpu_time_ms': T, 'dram_bytes_per_launch': sum(p['dram_bytes'] for p in per),
+           'tensor_pipe_active_pct': 0.0, 'fma_pipe_active_pct': w('fma_pipe_active_pct'),
+           'xu_inst_pct': w('xu_inst_pct'), 'issue_active_pct': w('issue_active_pct'),
+           'sm_clock_hz': w('sm_clock_hz')}
+    json.dump({'aggregate': agg, 'per_kernel': per}, open(out_json, 'w'), indent=1)
+    print(json.dumps({'aggregate': agg, 'per_kernel': per}, indent=1))
+    spath = os.path.join(ROOT, 'profiles', 'ncu_summary.json')
+    t = json.load(open(spath)) if os.path.exists(spath) else {}
+    t[key] = agg
+    json.dump(t, open(spath, 'w'), indent=1)
+
+
 if __name__ == '__main__':
-    if sys.argv[1] == 'launches':
+    if sys.argv[1] == 'set':
+        kernel_set(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5])
+    elif sys.argv[1] == 'launches':
         launches(sys.argv[2], sys.argv[3])
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None,
