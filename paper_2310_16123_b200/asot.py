@@ -117,7 +117,7 @@ KERNEL_NAMES = {0: "sinkhorn_simt_kernel (fp32 CUDA cores)",
                 8: "sinkhorn_tc3_kernel (3xTF32 fp32-accurate, 1 SM, M=128, pair-list mode)",
                 9: "sinkhorn_warp_kernel (fp32 CUDA cores, lane per anchor, K < 32)",
                 10: "sinkhorn_tc6_kernel (BF16x3 fp32-accurate, resident, CTA pair, cta_group::2, M=256)",
-                11: "sinkhorn_sparse_class_kernel<4/6/8/16> (fp32 CUDA cores, thread per pair, support-ordered; histogram supports <= 16)"}
+                11: "sinkhorn_sparse_rect_kernel<R, C> per support-class pair + the 9-16-bin half-warp form (fp32 CUDA cores, thread per pair, support-ordered; histogram supports <= 16)"}
 
 
 def sinkhorn_path_kind(H: torch.Tensor, precision: int) -> int:
