@@ -284,16 +284,22 @@ map_assign_kernel(const float* __restrict__ points, const int64_t* __restrict__ 
         if (refine) {
           const float* xp = Xs + pl * RS;
           // four of the lane's anchors at a time: four independent fp64 chains, each in the
-          // pinned op order (sequential in k), compared in increasing j
+          // pinned op order (sequential in k), compared in increasing j.  The anchors come from
+          // the CTA's shared-memory copy when all of them are resident (the same fp32 values:
+          // an L2 round trip per coordinate had made the refine latency-bound -- it is most of
+          // the work on the tensor-core mapping's ambiguous list), else from global memory.
+          const float* wsrc = single ? Ws : anchors;
+          const int64_t wstride = single ? RS : dim;
           for (int j0 = tx; j0 < K; j0 += 4 * LPP) {
             const float* wj[4];
             double accd[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int j = j0 + e * LPP;
-              wj[e] = anchors + (int64_t)(j < K ? j : j0) * dim;
+              wj[e] = wsrc + (int64_t)(j < K ? j : j0) * wstride;
               accd[e] = 0.0;
             }
+#pragma unroll 4
             for (int k = 0; k < dim; ++k) {
               const double xk = (double)xp[k];
 #pragma unroll
