@@ -121,6 +121,25 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
                                       float* const* hist_peers, int32_t n_peers, int64_t row_base,
                                       uint32_t* status, void* stream);
 
+/* Workspace form of the two calls above (a2 + a3): with the caller's
+ * device workspace the score products x.w_j run on the tensor cores (3xTF32 tcgen05) and only the
+ * points whose two best scores lie within the rigorous error bound go through the exact kernel
+ * (DESIGN R#37), so assign_out and hist_out are bit-identical to asot_map_to_anchors.  The
+ * tensor-core pass needs dim in {32, 64, 128}, n_anchors a multiple of 64 and points 16-byte
+ * aligned; other shapes run the exact kernel on every point (the workspace is still required).
+ * hist_peers / n_peers / row_base as in asot_map_to_anchors_bcast (n_peers = 0: no peer stores).
+ * workspace: device, 256-byte aligned, >= asot_map_workspace_bytes(offsets_host[n_dist],
+ * n_anchors) bytes, owned by the caller, free for reuse once the stream has passed the call;
+ * too small / misaligned -> ASOT_ERR_WORKSPACE, nothing launched. */
+size_t asot_map_workspace_bytes(int64_t n_points, int32_t n_anchors);
+asot_status asot_map_to_anchors_ws(const float* points, const int64_t* offsets,
+                                   const int64_t* offsets_host, const float* weights,
+                                   int64_t n_dist, int32_t dim, const float* anchors,
+                                   int32_t n_anchors, int32_t* assign_out, float* hist_out,
+                                   float* const* hist_peers, int32_t n_peers, int64_t row_base,
+                                   uint32_t* status, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
 /* Steps a1 + a5 + a6 on an explicit pair list (SPEC batched_sinkhorn_fixed).
  * 32 <= K <= 128: the resident 1-SM tcgen05 kernels in pair-list mode (ASOT_PREC_TF32: TF32;
  * ASOT_PREC_FP32: 3xTF32), bitwise the values of the tile path; K < 32: the fp32 lane-per-anchor

@@ -66,6 +66,9 @@ _SIGS = {
                                  c_vp, c_vp, c_vp, c_vp, c_vp]),
     "asot_map_to_anchors_bcast": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp,
                                           c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "asot_map_workspace_bytes": (c_size, [c_i64, c_i32]),
+    "asot_map_to_anchors_ws": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp,
+                                       c_vp, c_i32, c_i64, c_vp, c_vp, c_size, c_vp]),
     "asot_profile_enable": (c_i32, [c_i32]),
     "asot_profile_read": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "asot_profile_clock": (c_i32, [c_i32, ctypes.POINTER(ctypes.c_double)]),

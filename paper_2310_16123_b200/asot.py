@@ -212,10 +212,25 @@ def _host_offsets(offsets, offsets_host):
     return np.ascontiguousarray(offsets.detach().cpu().numpy(), dtype=np.int64)
 
 
+def _map_ws_call(points, offsets, oh, weights, N, d, anchors, K, assign, H, peer_ptrs, row_base, st,
+                 workspace, stream):
+    """asot_map_to_anchors_ws: the mapping with the tensor-core score pass (same bits out)."""
+    lib = _lib_handle()
+    need = int(lib.asot_map_workspace_bytes(int(oh[-1]), int(K)))
+    buf = _ws(workspace, points.device).get(need)
+    _check(lib.asot_map_to_anchors_ws(
+        _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(anchors), int(K),
+        _ptr(assign), _ptr(H), _ptr(peer_ptrs) if peer_ptrs is not None else None,
+        int(peer_ptrs.numel()) if peer_ptrs is not None else 0, int(row_base), _ptr(st), _ptr(buf),
+        int(buf.numel()), _stream(stream)))
+
+
 def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
                    anchors: torch.Tensor, offsets_host: Optional[np.ndarray] = None,
-                   status: Optional[torch.Tensor] = None, stream=None):
-    """Steps a2 + a3: returns (assign [T] int32, H [N, K] f32, status)."""
+                   status: Optional[torch.Tensor] = None, stream=None, tensor_core: bool = False,
+                   workspace: Optional[Workspace] = None):
+    """Steps a2 + a3: returns (assign [T] int32, H [N, K] f32, status).  tensor_core=True:
+    asot_map_to_anchors_ws (score products on tcgen05, bit-identical results)."""
     _need_cuda(points, offsets, weights, anchors)
     _need_f32(points, weights, anchors)
     oh = _host_offsets(offsets, offsets_host)
@@ -225,6 +240,10 @@ def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.T
     assign = torch.empty(max(T, 1), dtype=torch.int32, device=points.device)
     H = torch.empty((N, K), dtype=torch.float32, device=points.device)
     st = new_status(points.device) if status is None else status
+    if tensor_core:
+        _map_ws_call(points, offsets, oh, weights, N, d, anchors, K, assign, H, None, 0, st, workspace,
+                     stream)
+        return assign[:T], H, st
     _check(_lib_handle().asot_map_to_anchors(
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(anchors), int(K),
         _ptr(assign), _ptr(H), _ptr(st), _stream(stream)))
@@ -234,7 +253,8 @@ def map_to_anchors(points: torch.Tensor, offsets: torch.Tensor, weights: torch.T
 def map_to_anchors_bcast(points: torch.Tensor, offsets: torch.Tensor, weights: torch.Tensor,
                          anchors: torch.Tensor, peer_ptrs: torch.Tensor, row_base: int,
                          offsets_host: Optional[np.ndarray] = None,
-                         status: Optional[torch.Tensor] = None, stream=None):
+                         status: Optional[torch.Tensor] = None, stream=None,
+                         tensor_core: bool = False, workspace: Optional[Workspace] = None):
     """map_to_anchors that also stores each H row into every matrix of `peer_ptrs` (int64 device
     tensor of device addresses of full [N_total, K] H buffers) at row row_base + i."""
     _need_cuda(points, offsets, weights, anchors, peer_ptrs)
@@ -246,6 +266,10 @@ def map_to_anchors_bcast(points: torch.Tensor, offsets: torch.Tensor, weights: t
     assign = torch.empty(max(T, 1), dtype=torch.int32, device=points.device)
     H = torch.empty((N, K), dtype=torch.float32, device=points.device)
     st = new_status(points.device) if status is None else status
+    if tensor_core:
+        _map_ws_call(points, offsets, oh, weights, N, d, anchors, K, assign, H, peer_ptrs, row_base, st,
+                     workspace, stream)
+        return assign[:T], H, st
     _check(_lib_handle().asot_map_to_anchors_bcast(
         _ptr(points), _ptr(offsets), _ptr(oh), _ptr(weights), N, int(d), _ptr(anchors), int(K),
         _ptr(assign), _ptr(H), _ptr(peer_ptrs), int(peer_ptrs.numel()), int(row_base), _ptr(st),

@@ -430,6 +430,27 @@ asot_status asot_map_to_anchors_bcast(const float* points, const int64_t* offset
                   hist_out, status, stream, hist_peers, n_peers, row_base, nullptr);
 }
 
+size_t asot_map_workspace_bytes(int64_t n_points, int32_t n_anchors) {
+  return align_up(asot::map_tc_workspace_bytes(n_points, n_anchors));
+}
+
+asot_status asot_map_to_anchors_ws(const float* points, const int64_t* offsets,
+                                   const int64_t* offsets_host, const float* weights,
+                                   int64_t n_dist, int32_t dim, const float* anchors,
+                                   int32_t n_anchors, int32_t* assign_out, float* hist_out,
+                                   float* const* hist_peers, int32_t n_peers, int64_t row_base,
+                                   uint32_t* status, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  ASOT_CHECK_ARG(n_peers >= 0 && (n_peers == 0 || hist_peers), "hist_peers required when n_peers > 0");
+  ASOT_CHECK_ARG(row_base >= 0, "row_base must be >= 0");
+  ASOT_CHECK_ARG(offsets_host && n_dist >= 1, "offsets_host required, n_dist must be >= 1");
+  if (!workspace || ((uintptr_t)workspace & 255u) != 0 ||
+      workspace_bytes < asot_map_workspace_bytes(offsets_host[n_dist], n_anchors))
+    return fail(ASOT_ERR_WORKSPACE, "workspace too small or not 256-byte aligned (asot_map_workspace_bytes)");
+  return map_impl(points, offsets, offsets_host, weights, n_dist, dim, anchors, n_anchors, assign_out,
+                  hist_out, status, stream, hist_peers, n_peers, row_base, (uint8_t*)workspace);
+}
+
 static asot_status map_impl(const float* points, const int64_t* offsets, const int64_t* offsets_host,
                             const float* weights, int64_t n_dist, int32_t dim, const float* anchors,
                             int32_t n_anchors, int32_t* assign_out, float* hist_out, uint32_t* status,

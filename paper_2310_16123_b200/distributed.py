@@ -183,13 +183,16 @@ def cuda_steps(points: torch.Tensor, offsets: torch.Tensor, offsets_host: np.nda
     from . import asot as A
 
     offs_h = np.asarray(offsets_host, dtype=np.int64)
+    # the mapping's own scratch (tensor-core score pass): the Sinkhorn workspace stays untouched
+    map_ws = A.Workspace(points.device)
 
     def map_range(lo: int, hi: int) -> torch.Tensor:
         s, e = int(offs_h[lo]), int(offs_h[hi])
         sub_off_h = offs_h[lo: hi + 1] - s
         sub_off = torch.from_numpy(sub_off_h).to(points.device, non_blocking=True)
         _, H, _ = A.map_to_anchors(points[s:e].contiguous(), sub_off, weights[s:e].contiguous(),
-                                   anchors, offsets_host=sub_off_h, status=status)
+                                   anchors, offsets_host=sub_off_h, status=status, tensor_core=True,
+                                   workspace=map_ws)
         return H
 
     def tiles(H: torch.Tensor, t0: int, t1: int) -> torch.Tensor:
@@ -210,7 +213,8 @@ def cuda_steps(points: torch.Tensor, offsets: torch.Tensor, offsets_host: np.nda
         sub_off_h = offs_h[lo: hi + 1] - s
         sub_off = torch.from_numpy(sub_off_h).to(points.device, non_blocking=True)
         A.map_to_anchors_bcast(points[s:e].contiguous(), sub_off, weights[s:e].contiguous(), anchors,
-                               peers, lo, offsets_host=sub_off_h, status=status)
+                               peers, lo, offsets_host=sub_off_h, status=status, tensor_core=True,
+                               workspace=map_ws)
 
     def tiles_into(H: torch.Tensor, t0: int, t1: int, d_addr: int) -> None:
         # part [t0, t1) of the enumeration the library picks (support order on the small-support

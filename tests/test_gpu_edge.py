@@ -213,3 +213,52 @@ def test_profile_clock_probe(asot):
     assert 300.0 < mhz < 2500.0, mhz
     with pytest.raises(Exception):
         asot.asot.profile_clock(0)
+
+
+def test_map_ws_entry_point(asot):
+    """asot_map_to_anchors_ws (include/asot.h): the same bits as asot_map_to_anchors, peer stores at
+    row_base, the status flags of the exact kernel, ASOT_ERR_WORKSPACE on a short or misaligned
+    workspace, an empty distribution and ragged point counts."""
+    import ctypes
+    import paper_2310_16123_b200.asot as A
+    from paper_2310_16123_b200 import _lib
+    inp = make_inputs("c3", n_dist=37)
+    pts, offs, w, anc = dev(inp.points), dev(inp.offsets), dev(inp.weights), dev(inp.anchors)
+    a0, H0, _ = A.map_to_anchors(pts, offs, w, anc, offsets_host=inp.offsets)
+    # peers: two full matrices of 50 rows, this call's rows land at row 9
+    full = [torch.full((50, inp.n_anchors), -1.0, device="cuda") for _ in range(2)]
+    peers = torch.tensor([f.data_ptr() for f in full], dtype=torch.int64, device="cuda")
+    a1, H1, st = A.map_to_anchors_bcast(pts, offs, w, anc, peers, 9, offsets_host=inp.offsets,
+                                        tensor_core=True)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert torch.equal(a0, a1) and torch.equal(H0, H1)
+    for f in full:
+        assert torch.equal(f[9:9 + 37], H0)
+        assert bool((f[:9] == -1).all()) and bool((f[46:] == -1).all())
+    # flags: NaN coordinate (no anchor decided on the tensor cores either) and an empty distribution
+    p2 = inp.points.copy(); p2[4, 1] = np.nan
+    offs2 = inp.offsets.copy(); offs2[3] = offs2[2]
+    st = A.new_status()
+    A.map_to_anchors(dev(p2), dev(offs2), w, anc, offsets_host=offs2, status=st, tensor_core=True)
+    torch.cuda.synchronize()
+    assert int(st.item()) & A.FLAG_NONFINITE_INPUT and int(st.item()) & A.FLAG_EMPTY_DIST
+    # workspace errors through the C-ABI itself
+    lib = _lib.load()
+    T, K, d = int(inp.offsets[-1]), inp.n_anchors, inp.points.shape[1]
+    need = int(lib.asot_map_workspace_bytes(T, K))
+    assert need > 0 and need % 256 == 0
+    ws = torch.empty(need + 256, dtype=torch.uint8, device="cuda")
+    asg = torch.empty(T, dtype=torch.int32, device="cuda")
+    H = torch.empty((37, K), dtype=torch.float32, device="cuda")
+    st = A.new_status()
+    oh = np.ascontiguousarray(inp.offsets, dtype=np.int64)
+    call = lambda wp, wb: lib.asot_map_to_anchors_ws(
+        pts.data_ptr(), offs.data_ptr(), oh.ctypes.data, w.data_ptr(), 37, d, anc.data_ptr(), K,
+        asg.data_ptr(), H.data_ptr(), None, 0, 0, st.data_ptr(), wp, wb, None)
+    assert call(ws.data_ptr(), need - 1) == 6   # ASOT_ERR_WORKSPACE
+    assert call(ws.data_ptr() + 16, need) == 6   # ASOT_ERR_WORKSPACE
+    assert call(None, need) == 6   # ASOT_ERR_WORKSPACE
+    assert call(ws.data_ptr(), need) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(asg, a0) and torch.equal(H, H0)

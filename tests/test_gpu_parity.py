@@ -51,6 +51,8 @@ def map_via(asot, path, pts, offs, w, anc, offsets_host):
     products and the exact kernel on the points they cannot decide, R#37)."""
     if path == "exact":
         return asot.map_to_anchors(pts, offs, w, anc, offsets_host=offsets_host)
+    if path == "ws":   # asot_map_to_anchors_ws: the standalone / multi-GPU mapping with a workspace
+        return asot.map_to_anchors(pts, offs, w, anc, offsets_host=offsets_host, tensor_core=True)
     N, K = offsets_host.shape[0] - 1, anc.shape[0]
     assign = torch.empty(max(int(offsets_host[-1]), 1), dtype=torch.int32, device=pts.device)
     H = torch.empty((N, K), dtype=torch.float32, device=pts.device)
@@ -62,7 +64,7 @@ def map_via(asot, path, pts, offs, w, anc, offsets_host):
 
 
 # ------------------------------------------------------------------ mapping + histograms
-@pytest.mark.parametrize("path", ["exact", "tc"])
+@pytest.mark.parametrize("path", ["exact", "tc", "ws"])
 @pytest.mark.parametrize("cfg,n", [("c1", 64), ("c2", 1000), ("c3", 200), ("c4", 8000), ("c5", 40)])
 def test_mapping_bit_exact(asot, cfg, n, path):
     inp = make_inputs(cfg, n_dist=n)
@@ -77,7 +79,7 @@ def test_mapping_bit_exact(asot, cfg, n, path):
     np.testing.assert_array_equal(H.cpu().numpy(), H_o)
 
 
-@pytest.mark.parametrize("path", ["exact", "tc"])
+@pytest.mark.parametrize("path", ["exact", "tc", "ws"])
 def test_mapping_adversarial_ties(asot, path):
     rng = np.random.default_rng(5)
     d, K = 32, 64
@@ -103,7 +105,7 @@ def test_mapping_adversarial_ties(asot, path):
     assert assign.cpu().numpy()[-2] == 3
 
 
-@pytest.mark.parametrize("path", ["exact", "tc"])
+@pytest.mark.parametrize("path", ["exact", "tc", "ws"])
 @pytest.mark.parametrize("case", ["offset", "tiny", "huge", "mixed"])
 @pytest.mark.parametrize("d,K", [(16, 64), (64, 256), (128, 1024)])
 def test_mapping_extreme_magnitudes(asot, case, d, K, path):
