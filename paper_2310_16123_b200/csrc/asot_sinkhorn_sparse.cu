@@ -626,11 +626,12 @@ cudaError_t launch_sparse_prep(const float* H, int64_t n_dist, int K, const floa
 }
 
 namespace {
-// One non-blocking side stream and a fork / join event pair per (host thread, device), created on
-// first use and kept for the life of the thread.
+// kSide non-blocking side streams with a fork event and a join event each per (host thread,
+// device), created on first use and kept for the life of the thread.
+constexpr int kSide = 5;
 struct SideStream {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t fork = nullptr, join[kSide] = {};
 };
 SideStream& side_stream() {
   constexpr int kMaxDev = 64;
@@ -638,10 +639,12 @@ SideStream& side_stream() {
   int dev = 0;
   cudaGetDevice(&dev);
   SideStream& ss = per_dev[dev < kMaxDev ? dev : 0];
-  if (ss.side == nullptr) {
-    cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking);
+  if (ss.fork == nullptr) {
     cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+    for (int i = 0; i < kSide; ++i) {
+      cudaStreamCreateWithFlags(&ss.side[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming);
+    }
   }
   return ss;
 }
@@ -662,25 +665,30 @@ cudaError_t launch_sinkhorn_sparse(const PairSource& ps, const PairSink& out, in
     const int64_t P = ps.n_dist * (ps.n_dist - 1) / 2;
     const int64_t p0 = ps.tile_begin, p1 = ps.tile_begin + ps.n_slots / kTileSlots;
     const int64_t k_lo = T > 0 ? p0 * P / T : 0, k_hi = T > 0 ? p1 * P / T : 0;
-    // The classes with the largest blocks (8 x 8, 9-16 bins) have the fewest pairs (c3: 21.7 k
-    // and 2.0 k of 2 M): alone they fill a few warps per SM and run one pair's latency chain
-    // (measured: 8% of the warp slots).  They run on a side stream forked from s and joined back
-    // before the call's next launch, beside the large classes (longest chain first on s, the
-    // short 4 x 4 pairs last to fill the tail).
+    // Every class kernel is one wave of resident CTAs striding over its pairs: a thread runs
+    // ceil or floor of (pairs / threads) latency chains, so the last round leaves part of the SM
+    // idle (measured: 20-25% of each kernel's resident warp slots), and the classes with the
+    // largest blocks (8 x 8, 9-16 bins; c3: 21.7 k and 2.0 k of 2 M pairs) fill a few warps per
+    // SM at most.  The class kernels therefore run on side streams forked from s and joined back
+    // before the call's next launch (longest chain first, the short 4 x 4 pairs on s, last): the
+    // CTAs of the next class take the slots a draining class frees.  Every pair is computed by
+    // the same code wherever it runs: the results do not depend on the overlap.
     SideStream& ss = side_stream();
     cudaError_t e = cudaEventRecord(ss.fork, s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.side, ss.fork, 0);
+    for (int i = 0; i < kSide && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(ss.side[i], ss.fork, 0);
     if (e != cudaSuccess) return e;
-    sps::sinkhorn_sparse_rect_kernel<8, 8><<<sms * 4, sps::kThreads, 0, ss.side>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_class_kernel<0><<<sms * 2, sps::kThreads, 0, ss.side>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<6, 8><<<sms * 4, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<6, 6><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<4, 8><<<sms * 5, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
-    sps::sinkhorn_sparse_rect_kernel<4, 6><<<sms * 7, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<8, 8><<<sms * 4, sps::kThreads, 0, ss.side[0]>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_class_kernel<0><<<sms * 2, sps::kThreads, 0, ss.side[0]>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<6, 8><<<sms * 4, sps::kThreads, 0, ss.side[1]>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<6, 6><<<sms * 5, sps::kThreads, 0, ss.side[2]>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<4, 8><<<sms * 5, sps::kThreads, 0, ss.side[3]>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
+    sps::sinkhorn_sparse_rect_kernel<4, 6><<<sms * 7, sps::kThreads, 0, ss.side[4]>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
     sps::sinkhorn_sparse_rect_kernel<4, 4><<<sms * 8, sps::kThreads, 0, s>>>(ps.n_dist, out, K, sp, iters, k_lo, k_hi);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaEventRecord(ss.join, ss.side);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ss.join, 0);
+    for (int i = 0; i < kSide && e == cudaSuccess; ++i) {
+      e = cudaEventRecord(ss.join[i], ss.side[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ss.join[i], 0);
+    }
     return e;
   }
   sps::sinkhorn_sparse_kernel<<<(unsigned)blocks, sps::kThreads, 0, s>>>(ps, out, K, sp, iters, upt, 0);
