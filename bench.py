@@ -1038,7 +1038,11 @@ def main():
             "roofline": roofline, "mapping": mapping, "kmeans": kmeans, "eot_baseline": eot_base,
             "exact_asot": exact, "pairs_api": pairs_api, "bounds": bounds,
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": gpu_launches, "clocks": clk,
+            "gpu_launches": gpu_launches,
+            "gpu_launches_note": "launch-helper calls of libasot inside the timed region (a lower bound on "
+                                 "kernels: each helper enqueues >= 1 of the library's kernels; the ncu "
+                                 "launch list under profiles/ has every kernel of a step)",
+            "clocks": clk,
             "wall_s_timed_region": wall,
             "env": asot_env(),
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
