@@ -413,10 +413,22 @@ histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ w
   if (lane == 0 && e <= s) atomicOr(status, ASOT_FLAG_EMPTY_DIST);
   double msum = 0.0;
   bool nonfinite = false, negative = false;
+  // Lane l owns the bins r = l (mod 32) and keeps the running sum of the bin it touched last in
+  // a register (cur, acc): the same additions in the same (point) order as h[at] += w, without a
+  // shared-memory round trip per point while consecutive points of the lane share a bin (small
+  // supports: almost always).
+  int cur = -1;
+  double acc = 0.0;
+  // the next 32 points' (assignment, weight) are loaded while the current 32 are summed (the
+  // weights come from HBM: one exposed load latency per distribution instead of one per batch)
+  int a_next = s + lane < e ? assign[s + lane] : 0;
+  float w_next = s + lane < e ? weights[s + lane] : 0.0f;
   for (int64_t p0 = s; p0 < e; p0 += 32) {
     const int64_t p = p0 + lane;
-    const int a = p < e ? assign[p] : 0;
-    const float w = p < e ? weights[p] : 0.0f;
+    const int a = a_next;
+    const float w = w_next;
+    a_next = p + 32 < e ? assign[p + 32] : 0;
+    w_next = p + 32 < e ? weights[p + 32] : 0.0f;
     if (p < e) {
       // a point with a non-finite coordinate has no nearest anchor (assignment out of range)
       nonfinite |= !isfinite(w) || a < 0 || a >= K;
@@ -424,12 +436,36 @@ histogram_kernel(const int32_t* __restrict__ assign, const float* __restrict__ w
       msum += (double)w;
     }
     const int cnt = (e - p0) < 32 ? (int)(e - p0) : 32;
-    for (int t = 0; t < cnt; ++t) {  // point order
-      const int at = __shfl_sync(0xffffffffu, a, t);
-      const float wt = __shfl_sync(0xffffffffu, w, t);
-      if (lane == (at & 31) && at >= 0 && at < K) h[at] = h[at] + (double)wt;
+    if (cnt == 32) {
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {  // point order (the shuffles of later points issue early)
+        const int at = __shfl_sync(0xffffffffu, a, t);
+        const float wt = __shfl_sync(0xffffffffu, w, t);
+        if (lane == (at & 31) && at >= 0 && at < K) {
+          if (at != cur) {   // another of this lane's bins: park the held sum, fetch the new one
+            if (cur >= 0) h[cur] = acc;
+            cur = at;
+            acc = h[at];
+          }
+          acc = acc + (double)wt;
+        }
+      }
+    } else {
+      for (int t = 0; t < cnt; ++t) {  // point order
+        const int at = __shfl_sync(0xffffffffu, a, t);
+        const float wt = __shfl_sync(0xffffffffu, w, t);
+        if (lane == (at & 31) && at >= 0 && at < K) {
+          if (at != cur) {   // another of this lane's bins: park the held sum, fetch the new one
+            if (cur >= 0) h[cur] = acc;
+            cur = at;
+            acc = h[at];
+          }
+          acc = acc + (double)wt;
+        }
+      }
     }
   }
+  if (cur >= 0) h[cur] = acc;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) msum += __shfl_xor_sync(0xffffffffu, msum, off);
   const bool any_nonfinite = __any_sync(0xffffffffu, nonfinite);
